@@ -1,0 +1,362 @@
+"""Benchmark: input triplets/s assembled to CSC on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl reference]
+
+A step is one full assembly S = sparse(i, j, s, m, n) of the workload
+(default: BASELINE configs[1], the 2D P1 FEM stiffness with N=1000 cells per
+side, L = 18e6 triplets).  Inputs (288 MB) and the workspace exceed the
+126 MB L2, so consecutive steps stream from HBM (no explicit flush).
+
+Prints ONE JSON line (rank 0):
+  value        whole-job triplets/s, device-resident inputs, CUDA events on
+               the launching stream, max over ranks
+  e2e          the same metric through the public host API
+               paper_1406_1066_b200.assemble(numpy arrays in pinned memory)
+               -> host CSC (H2D of the triplets and D2H of jc/ir/pr inside)
+  roofline     dominant kernel: its algorithmic bytes / its event-timed
+               duration vs MEASURED_PEAKS.json hbm_gbs
+  path_roofline  compulsory bytes of the whole assembly (16 L + 12 nnz +
+               4 (N+1)) / step time
+  cpu_baseline the reference's own compiled kernels (oracle/_ref, threaded
+               driver) on this host, same workload
+--impl reference runs only that CPU implementation and prints its line.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "input triplets/sec assembled to CSC"
+UNIT = "triplets/s"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (clocks + throttle reasons)."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                     "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                parts = [p.strip() for p in out.stdout.strip().split(",")]
+                if len(parts) == 6:
+                    self.samples.append(parts)
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for s in self.samples for k in range(4) if s[2 + k] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def _dist():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def cpu_reference_run(ii, jj, s, m, n, budget_s=12.0, max_reps=20, threads=None):
+    """Time the reference's CPU implementation: its own compiled kernels
+    (oracle/_ref) under the restated threaded driver (parallel.py:267-358)
+    with all host threads; falls back to the C restatement (1 core)."""
+    from oracle import oracle as O
+    from oracle import ref_driver
+
+    p = threads or len(os.sched_getaffinity(0))
+    if ref_driver.available():
+        kind = "reference"
+        run = (lambda: ref_driver.assemble_parallel(ii, jj, s, m, n, p)) if p > 1 else \
+            (lambda: ref_driver.assemble_serial(ii, jj, s, m, n))
+        cores = p
+    else:
+        kind = "port"
+        run = lambda: O.assemble_counting(ii, jj, s, m, n)  # noqa: E731
+        cores = 1
+    out = run()  # warm-up (untimed), also the parity reference
+    times = []
+    t_start = time.perf_counter()
+    while len(times) < max_reps and (time.perf_counter() - t_start) < budget_s:
+        t0 = time.perf_counter()
+        run()
+        times.append(time.perf_counter() - t0)
+    mean = sum(times) / len(times)
+    return dict(kind=kind, cores=cores, mean_s=mean, min_s=min(times), reps=len(times)), out
+
+
+def build_workload(cfg: int, device, rank: int, world: int):
+    from paper_1406_1066_b200 import workloads as W
+
+    if cfg == 5 or world > 1:
+        # sharded 2D FEM: rank r takes a contiguous cell chunk (weak scaling:
+        # each rank holds a cfg2-sized chunk of an N_mesh = 1000*sqrt(world) mesh)
+        import math
+
+        if cfg == 5:
+            Nm = 8000
+        else:
+            Nm = int(round(1000 * math.sqrt(world)))
+        cells = Nm * Nm
+        c0, c1 = cells * rank // world, cells * (rank + 1) // world
+        w = W.fem2d(Nm, device=device, cell_range=(c0, c1))
+        w.name = f"fem2d_N{Nm}_chunk{rank}of{world}"
+        return w
+    return W.config(cfg, device=device)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world, rank, local = _dist()
+    if args.warmup < 3:
+        args.warmup = 3
+
+    import numpy as np
+    import torch
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        w = build_workload(args.config, "cpu", 0, 1)
+        ii, jj, s = w.ii.numpy(), w.jj.numpy(), w.s.numpy()
+        from oracle import oracle as O
+        from oracle import ref_driver
+
+        p = len(os.sched_getaffinity(0))
+        if ref_driver.available():
+            info = {"kind": "reference", "cores": p}
+            run = lambda: ref_driver.assemble_parallel(ii, jj, s, w.m, w.n, p)  # noqa: E731
+        else:
+            info = {"kind": "port", "cores": 1}
+            run = lambda: O.assemble_counting(ii, jj, s, w.m, w.n)  # noqa: E731
+        for _ in range(args.warmup):
+            out = run()
+        times = []
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            run()
+            times.append(time.perf_counter() - t0)
+        mean = sum(times) / len(times)
+        val = w.L / mean
+        line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": mean * 1e3,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic",
+                "config": {"workload": w.name, "L": w.L, "m": w.m, "n": w.n, "nnz": out.nnz},
+                "cpu_baseline": {"value": val, "unit": UNIT, "cores": info["cores"], "kind": info["kind"],
+                                 "sample": f"full workload, {args.steps} timed runs"},
+                "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    import paper_1406_1066_b200 as sa
+    from paper_1406_1066_b200 import _capi
+
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    w = build_workload(args.config, dev, rank, world)
+    torch.cuda.synchronize()
+    L, M, N = w.L, w.m, w.n
+    asm = sa.default_assembler(local)
+    lib, ctx = asm.lib, asm.ctx
+    cap = L
+    jc = torch.empty(N + 1, dtype=torch.int32, device=dev)
+    ir = torch.empty(cap, dtype=torch.int32, device=dev)
+    pr = torch.empty(cap, dtype=torch.float64, device=dev)
+    asm._bind_stream()
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        rc = lib.sa_assemble_async(ctx, w.ii.data_ptr(), w.jj.data_ptr(), w.s.data_ptr(), 1, L, M, N,
+                                   jc.data_ptr(), ir.data_ptr(), pr.data_ptr(), cap)
+        if rc:
+            raise RuntimeError(asm._msg())
+
+    # correctness of the configuration (device result must be complete)
+    step()
+    import ctypes
+
+    nnz_c = ctypes.c_int64(0)
+    rc = lib.sa_finish(ctx, ctypes.byref(nnz_c), None, None)
+    if rc:
+        raise RuntimeError(f"assembly failed: {asm._msg()}")
+    nnz = nnz_c.value
+    launches_per_step = lib.sa_last_launch_count(ctx)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+
+    # per-kernel breakdown (events inside the library on the same stream)
+    lib.sa_enable_timing(ctx, 1)
+    kt = {}
+    nk = 0
+    reps = max(3, min(args.steps, 10))
+    for _ in range(reps):
+        step()
+        arr = (ctypes.c_float * 16)()
+        names = (ctypes.c_char_p * 16)()
+        nk = lib.sa_last_kernel_times(ctx, 16, arr, names)
+        for k in range(nk):
+            kt.setdefault(names[k].decode(), []).append(arr[k])
+    lib.sa_enable_timing(ctx, 0)
+    kern_ms = {k: sum(v) / len(v) for k, v in kt.items()}
+    dom = max(kern_ms, key=kern_ms.get)
+    # algorithmic bytes per launch of each kernel ("kernels")
+    alg = {
+        "k_init": 4 * (N + 1),
+        "k_hist": 8 * L,
+        "k_col_scan": 8 * N,
+        "k_scatter": 32 * L,
+        "k_bigcol": 0,
+        "k_tile_fold": 16 * L + 8 * N + 12 * nnz + 4 * (N + 1),
+    }
+    peak_gbs, peak_kind = _peaks()
+    dom_gbs = alg.get(dom, 0) / (kern_ms[dom] * 1e-3) / 1e9
+    compulsory = 16 * L + 12 * nnz + 4 * (N + 1)
+    path_gbs = compulsory / (ms * 1e-3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "dram_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(w.name, {}).get(dom)
+        except Exception:
+            traffic = None
+
+    # end-to-end through the public host API (pinned host inputs)
+    hi = torch.empty(L, dtype=torch.int32, pin_memory=True)
+    hj = torch.empty(L, dtype=torch.int32, pin_memory=True)
+    hs = torch.empty(L, dtype=torch.float64, pin_memory=True)
+    hi.copy_(w.ii)
+    hj.copy_(w.jj)
+    hs.copy_(w.s)
+    hin, hjn, hsn = hi.numpy(), hj.numpy(), hs.numpy()
+    out = sa.assemble(hin, hjn, hsn, m=M, n=N, device=local)  # warm-up
+    e2e_t = []
+    for _ in range(max(1, args.e2e_steps)):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        out = sa.assemble(hin, hjn, hsn, m=M, n=N, device=local)
+        e2e_t.append(time.perf_counter() - t0)
+    e2e_s = sum(e2e_t) / len(e2e_t)
+    if world > 1:
+        t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+
+    cpu = None
+    parity = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        info, ref = cpu_reference_run(hin, hjn, hsn, M, N)
+        parity = bool(out.same_as(ref))
+        cpu = {"value": L / info["mean_s"], "unit": UNIT, "cores": info["cores"], "kind": info["kind"],
+               "sample": f"full workload ({L} triplets), {info['reps']} timed runs after 1 warm-up, "
+                         f"mean {info['mean_s'] * 1e3:.1f} ms"}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    value = L * world / (ms * 1e-3)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": w.name, "L": L, "m": M, "n": N, "nnz": nnz,
+                   "l2": "inputs (16 B x L) and workspace exceed the 126 MB L2; no explicit flush",
+                   "parallelism": f"dp{world}" if world > 1 else "single"},
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": dom_gbs, "peak": peak_gbs,
+                     "peak_kind": peak_kind, "unit": "GB/s", "frac": dom_gbs / peak_gbs,
+                     "traffic": traffic, "alg_bytes_per_launch": alg.get(dom),
+                     "launch_ms": kern_ms[dom]},
+        "path_roofline": {"compulsory_bytes": compulsory, "achieved": path_gbs, "peak": peak_gbs,
+                          "unit": "GB/s", "frac": path_gbs / peak_gbs},
+        "kernel_ms": kern_ms,
+        "e2e": {"value": L * world / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 16 * L,
+                "d2h_bytes_per_step": 4 * (N + 1) + 12 * nnz, "ms_per_step": e2e_s * 1e3},
+        "gpu_launches": launches_per_step * args.steps,
+        "launches_per_step": launches_per_step,
+        "clocks": clk.summary(),
+        "cpu_baseline": cpu,
+        "parity_vs_cpu_reference": parity,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,422 @@
+// sa_capi.cu -- the C ABI (include/sparse_assembly.h): contexts, workspace,
+// launch sequencing and error mapping.  No torch types cross this boundary.
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "../../include/sparse_assembly.h"
+#include "sa_internal.cuh"
+
+using namespace sa;
+
+struct sa_ctx {
+    int device = 0;
+    int num_sms = 148;
+    cudaStream_t own_stream = nullptr;
+    cudaStream_t stream = nullptr;
+    std::string last_error;
+    int launches = 0;
+
+    // device workspace (grown on demand, reused across calls)
+    uint32_t *cur = nullptr;              size_t cur_cap = 0;     // N
+    int4 *rec = nullptr;                  size_t rec_cap = 0;     // L
+    int32_t *tile_first = nullptr;        size_t tf_cap = 0;      // ntiles+1
+    unsigned long long *tile_state = nullptr; size_t ts_cap = 0;  // ntiles
+    unsigned long long *scan_state = nullptr; size_t ss_cap = 0;  // scan CTAs
+    uint32_t *big_list = nullptr;         size_t bl_cap = 0;      // L/BIGCOL+1
+    uint32_t *bigu = nullptr;             size_t bu_cap = 0;      // N
+    ErrState *err = nullptr;              // device
+    ErrState *err_host = nullptr;         // pinned mirror
+
+    // buffers of the host-pointer entry point
+    int32_t *h_ii = nullptr;                   size_t hii_cap = 0;
+    int32_t *h_jj = nullptr;                   size_t hjj_cap = 0;
+    double *h_s = nullptr;                     size_t hs_cap = 0;
+    int32_t *o_jc = nullptr;                   size_t ojc_cap = 0;
+    int32_t *o_ir = nullptr;                   size_t oir_cap = 0;
+    double *o_pr = nullptr;                    size_t opr_cap = 0;
+    // optional per-kernel event timing
+    static constexpr int MAXEV = 16;
+    int timing = 0;
+    int nev = 0;
+    cudaEvent_t ev[MAXEV + 1] = {};
+    const char *ev_name[MAXEV] = {};
+
+    int64_t host_L = -1;
+    int64_t host_stride = 1;
+    int32_t host_N = 0;
+    int64_t host_nnz = -1;
+};
+
+namespace {
+
+int fail(sa_ctx *ctx, int code, const std::string &msg) {
+    if (ctx) ctx->last_error = msg;
+    return code;
+}
+
+int cuda_fail(sa_ctx *ctx, cudaError_t e, const char *where) {
+    std::string m = std::string(where) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")";
+    return fail(ctx, e == cudaErrorMemoryAllocation ? SA_ERR_NOMEM : SA_ERR_CUDA, m);
+}
+
+#define SA_CUDA(ctx, expr)                                    \
+    do {                                                      \
+        cudaError_t _e = (expr);                              \
+        if (_e != cudaSuccess) return cuda_fail(ctx, _e, #expr); \
+    } while (0)
+
+template <typename T>
+cudaError_t ensure(T *&ptr, size_t &cap, size_t need) {
+    if (need <= cap && ptr) return cudaSuccess;
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    cap = 0;
+    size_t n = std::max<size_t>(need, 1);
+    cudaError_t e = cudaMalloc(reinterpret_cast<void **>(&ptr), n * sizeof(T));
+    if (e == cudaSuccess) cap = n;
+    return e;
+}
+
+int bits_for(uint64_t v) {  // bits needed to represent v (0 -> 0)
+    int b = 0;
+    while (v) {
+        ++b;
+        v >>= 1;
+    }
+    return b;
+}
+
+// One launch that resets the per-call device state.
+__global__ void k_init(ErrState *err, uint32_t *cur, int64_t ncur, unsigned long long *ts,
+                       int64_t nts, unsigned long long *ss, int64_t nss) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t0 == 0) {
+        ErrState e;
+        memset(&e, 0, sizeof(e));
+        e.bad_i = ~0ull;
+        e.bad_j = ~0ull;
+        *err = e;
+    }
+    // cur: 16-byte stores where possible
+    const int64_t nq = ncur >> 2;
+    uint4 *cur4 = reinterpret_cast<uint4 *>(cur);
+    for (int64_t k = t0; k < nq; k += stride) cur4[k] = make_uint4(0, 0, 0, 0);
+    for (int64_t k = (nq << 2) + t0; k < ncur; k += stride) cur[k] = 0;
+    for (int64_t k = t0; k < nts; k += stride) ts[k] = 0ull;
+    for (int64_t k = t0; k < nss; k += stride) ss[k] = 0ull;
+}
+
+int launch_init(sa_ctx *ctx, Launch &lc, int64_t ncur, int64_t nts, int64_t nss) {
+    int64_t work = std::max<int64_t>({ncur / 4, nts, nss, 1});
+    int grid = (int)std::min<int64_t>((work + 255) / 256, (int64_t)ctx->num_sms * 4);
+    k_init<<<grid, 256, 0, lc.stream>>>(ctx->err, ctx->cur, ncur, ctx->tile_state, nts,
+                                        ctx->scan_state, nss);
+    lc.launches++;
+    SA_CUDA(ctx, cudaGetLastError());
+    return SA_OK;
+}
+
+int decode(sa_ctx *ctx, const ErrState &e, int64_t *nnz, int64_t *bad_pos, int *bad_which) {
+    if (bad_pos) *bad_pos = -1;
+    if (bad_which) *bad_which = -1;
+    if (e.bad_i != ~0ull || e.bad_j != ~0ull) {
+        const bool row = e.bad_i != ~0ull;
+        const int64_t pos = (int64_t)(row ? e.bad_i : e.bad_j);
+        if (bad_pos) *bad_pos = pos;
+        if (bad_which) *bad_which = row ? SA_WHICH_ROW : SA_WHICH_COL;
+        char buf[96];
+        snprintf(buf, sizeof buf, "bad %s index at position %lld", row ? "row" : "column",
+                 (long long)pos);
+        return fail(ctx, SA_ERR_BAD_INDEX, buf);
+    }
+    if (e.over_m || e.over_n) return fail(ctx, SA_ERR_DIM_TOO_SMALL, "indices exceed the explicit dimensions");
+    if (e.internal) return fail(ctx, SA_ERR_INTERNAL, "device consistency check failed");
+    if (e.cap_exceeded) {
+        if (nnz) *nnz = e.nnz;
+        return fail(ctx, SA_ERR_CAPACITY, "nnz exceeds the ir/pr capacity");
+    }
+    if (nnz) *nnz = e.nnz;
+    ctx->last_error.clear();
+    return SA_OK;
+}
+
+// Record a timing event before the next launch (name) or after the last (nullptr).
+int mark(sa_ctx *ctx, const char *name) {
+    if (!ctx->timing) return SA_OK;
+    if (ctx->nev > sa_ctx::MAXEV) return SA_OK;
+    cudaEvent_t &e = ctx->ev[ctx->nev];
+    if (!e) SA_CUDA(ctx, cudaEventCreate(&e));
+    SA_CUDA(ctx, cudaEventRecord(e, ctx->stream));
+    if (name && ctx->nev < sa_ctx::MAXEV) ctx->ev_name[ctx->nev] = name;
+    ctx->nev++;
+    return SA_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int sa_enable_timing(sa_ctx *ctx, int on) {
+    if (!ctx) return SA_ERR_INVALID_ARG;
+    ctx->timing = on ? 1 : 0;
+    ctx->nev = 0;
+    return SA_OK;
+}
+
+int sa_last_kernel_times(sa_ctx *ctx, int max, float *ms, const char **names) {
+    if (!ctx) return SA_ERR_INVALID_ARG;
+    if (ctx->nev < 2) return 0;
+    SA_CUDA(ctx, cudaEventSynchronize(ctx->ev[ctx->nev - 1]));
+    int n = std::min(ctx->nev - 1, max);
+    for (int k = 0; k < n; ++k) {
+        float t = 0.f;
+        SA_CUDA(ctx, cudaEventElapsedTime(&t, ctx->ev[k], ctx->ev[k + 1]));
+        if (ms) ms[k] = t;
+        if (names) names[k] = ctx->ev_name[k];
+    }
+    return n;
+}
+
+int sa_version(void) { return 1; }
+
+int sa_create(int device, sa_ctx **out) {
+    if (!out) return SA_ERR_INVALID_ARG;
+    *out = nullptr;
+    sa_ctx *ctx = new sa_ctx();
+    ctx->device = device;
+    cudaError_t e = cudaSetDevice(device);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void **>(&ctx->err), sizeof(ErrState));
+    if (e == cudaSuccess) e = cudaMallocHost(reinterpret_cast<void **>(&ctx->err_host), sizeof(ErrState));
+    if (e != cudaSuccess) {
+        int rc = cuda_fail(ctx, e, "sa_create");
+        sa_destroy(ctx);
+        return rc;
+    }
+    ctx->stream = ctx->own_stream;
+    *out = ctx;
+    return SA_OK;
+}
+
+void sa_destroy(sa_ctx *ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    cudaFree(ctx->cur);
+    cudaFree(ctx->rec);
+    cudaFree(ctx->tile_first);
+    cudaFree(ctx->tile_state);
+    cudaFree(ctx->scan_state);
+    cudaFree(ctx->big_list);
+    cudaFree(ctx->bigu);
+    cudaFree(ctx->err);
+    cudaFree(ctx->h_ii);
+    cudaFree(ctx->h_jj);
+    cudaFree(ctx->h_s);
+    cudaFree(ctx->o_jc);
+    cudaFree(ctx->o_ir);
+    cudaFree(ctx->o_pr);
+    if (ctx->err_host) cudaFreeHost(ctx->err_host);
+    for (int k = 0; k <= sa_ctx::MAXEV; ++k)
+        if (ctx->ev[k]) cudaEventDestroy(ctx->ev[k]);
+    if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+    delete ctx;
+}
+
+int sa_set_stream(sa_ctx *ctx, void *stream) {
+    if (!ctx) return SA_ERR_INVALID_ARG;
+    ctx->stream = stream ? reinterpret_cast<cudaStream_t>(stream) : ctx->own_stream;
+    return SA_OK;
+}
+
+const char *sa_last_error(const sa_ctx *ctx) { return ctx ? ctx->last_error.c_str() : "null context"; }
+
+int sa_last_launch_count(const sa_ctx *ctx) { return ctx ? ctx->launches : 0; }
+
+const int64_t *sa_device_nnz(sa_ctx *ctx) {
+    return ctx ? reinterpret_cast<const int64_t *>(&ctx->err->nnz) : nullptr;
+}
+
+int sa_convert_indices(sa_ctx *ctx, const void *d_raw, int dtype, int64_t L, int32_t *d_out,
+                       int64_t *first_bad, int32_t *max_out) {
+    if (!ctx) return SA_ERR_INVALID_ARG;
+    if (L < 0 || (L > 0 && (!d_raw || !d_out)) || dtype < 0 || dtype > 2)
+        return fail(ctx, SA_ERR_INVALID_ARG, "sa_convert_indices: bad arguments");
+    SA_CUDA(ctx, cudaSetDevice(ctx->device));
+    Launch lc{ctx->stream, ctx->num_sms, 0};
+    int rc = launch_init(ctx, lc, 0, 0, 0);
+    if (rc) return rc;
+    static const int kmap[3] = {0, 1, 2};
+    SA_CUDA(ctx, launch_convert(lc, d_raw, kmap[dtype], L, d_out, ctx->err));
+    SA_CUDA(ctx, cudaMemcpyAsync(ctx->err_host, ctx->err, sizeof(ErrState), cudaMemcpyDeviceToHost, ctx->stream));
+    SA_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    ctx->launches = lc.launches;
+    if (first_bad) *first_bad = ctx->err_host->bad_i == ~0ull ? -1 : (int64_t)ctx->err_host->bad_i;
+    if (max_out) *max_out = (int32_t)ctx->err_host->max_i;
+    return SA_OK;
+}
+
+int sa_infer_dims(sa_ctx *ctx, const int32_t *d_ii, const int32_t *d_jj, int64_t L, int32_t *M,
+                  int32_t *N, int64_t *bad_pos, int *bad_which) {
+    if (!ctx) return SA_ERR_INVALID_ARG;
+    if (L < 0 || (L > 0 && (!d_ii || !d_jj)))
+        return fail(ctx, SA_ERR_INVALID_ARG, "sa_infer_dims: bad arguments");
+    SA_CUDA(ctx, cudaSetDevice(ctx->device));
+    Launch lc{ctx->stream, ctx->num_sms, 0};
+    int rc = launch_init(ctx, lc, 0, 0, 0);
+    if (rc) return rc;
+    SA_CUDA(ctx, launch_hist(lc, d_ii, d_jj, L, 0, 0, nullptr, ctx->err, true));
+    SA_CUDA(ctx, cudaMemcpyAsync(ctx->err_host, ctx->err, sizeof(ErrState), cudaMemcpyDeviceToHost, ctx->stream));
+    SA_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    ctx->launches = lc.launches;
+    if (M) *M = (int32_t)ctx->err_host->max_i;
+    if (N) *N = (int32_t)ctx->err_host->max_j;
+    ErrState e = *ctx->err_host;
+    e.nnz = 0;
+    return decode(ctx, e, nullptr, bad_pos, bad_which);
+}
+
+int sa_assemble_async(sa_ctx *ctx, const int32_t *d_ii, const int32_t *d_jj, const double *d_s,
+                      int64_t s_stride, int64_t L, int32_t M, int32_t N, int32_t *d_jc,
+                      int32_t *d_ir, double *d_pr, int64_t cap) {
+    if (!ctx) return SA_ERR_INVALID_ARG;
+    if (L < 0 || M < 0 || N < 0 || cap < 0 || !d_jc || (s_stride != 0 && s_stride != 1))
+        return fail(ctx, SA_ERR_INVALID_ARG, "sa_assemble_async: bad arguments");
+    if (L > 0 && (!d_ii || !d_jj || !d_s))
+        return fail(ctx, SA_ERR_INVALID_ARG, "sa_assemble_async: null triplet pointer");
+    if (L > (int64_t)POSMASK)
+        return fail(ctx, SA_ERR_INVALID_ARG, "sa_assemble_async: more than 2^31-1 triplets");
+    SA_CUDA(ctx, cudaSetDevice(ctx->device));
+    Launch lc{ctx->stream, ctx->num_sms, 0};
+
+    if (L == 0 || N == 0) {
+        // nothing to assemble (L > 0 with N == 0 means every column index is
+        // out of range: k_hist still flags it)
+        int rc = launch_init(ctx, lc, 0, 0, 0);
+        if (rc) return rc;
+        // L > 0 with N == 0: validation only; every valid column index then
+        // exceeds N and k_hist flags DimensionTooSmall (no histogram writes)
+        if (L > 0) SA_CUDA(ctx, launch_hist(lc, d_ii, d_jj, L, M, N, ctx->cur, ctx->err, false));
+        SA_CUDA(ctx, cudaMemsetAsync(d_jc, 0, ((size_t)N + 1) * sizeof(int32_t), ctx->stream));
+        ctx->launches = lc.launches;
+        return SA_OK;
+    }
+
+    const int64_t ntiles = (L + TILE - 1) / TILE;
+    const int64_t nscan = (N + 4095) / 4096;
+    SA_CUDA(ctx, ensure(ctx->cur, ctx->cur_cap, (size_t)N + 4));
+    SA_CUDA(ctx, ensure(ctx->rec, ctx->rec_cap, (size_t)L));
+    SA_CUDA(ctx, ensure(ctx->tile_first, ctx->tf_cap, (size_t)ntiles + 1));
+    SA_CUDA(ctx, ensure(ctx->tile_state, ctx->ts_cap, (size_t)ntiles));
+    SA_CUDA(ctx, ensure(ctx->scan_state, ctx->ss_cap, (size_t)nscan));
+    SA_CUDA(ctx, ensure(ctx->big_list, ctx->bl_cap, (size_t)(L / BIGCOL + 1)));
+    SA_CUDA(ctx, ensure(ctx->bigu, ctx->bu_cap, (size_t)N));
+
+    ctx->nev = 0;
+    int rc = mark(ctx, "k_init");
+    if (rc) return rc;
+    rc = launch_init(ctx, lc, N, ntiles, nscan);
+    if (rc) return rc;
+    if ((rc = mark(ctx, "k_hist"))) return rc;
+    SA_CUDA(ctx, launch_hist(lc, d_ii, d_jj, L, M, N, ctx->cur, ctx->err, false));
+    if ((rc = mark(ctx, "k_col_scan"))) return rc;
+    SA_CUDA(ctx, launch_col_scan(lc, ctx->cur, N, L, ctx->tile_first, ntiles, ctx->big_list,
+                                 ctx->scan_state, ctx->err));
+    if ((rc = mark(ctx, "k_scatter"))) return rc;
+    SA_CUDA(ctx, launch_scatter(lc, d_ii, d_jj, d_s, s_stride, L, M, N, ctx->cur, ctx->rec));
+    if (L > BIGCOL) {
+        const int idx_bits = std::max(1, bits_for((uint64_t)(L - 1)));
+        const int row_bits = bits_for((uint64_t)(M > 0 ? M - 1 : 0));
+        const int passes = std::max(1, (idx_bits + row_bits + 7) / 8);
+        if ((rc = mark(ctx, "k_bigcol"))) return rc;
+        SA_CUDA(ctx, launch_bigcol(lc, ctx->cur, ctx->big_list, ctx->err, ctx->rec, d_s, s_stride,
+                                   ctx->bigu, idx_bits, passes));
+    }
+    if ((rc = mark(ctx, "k_tile_fold"))) return rc;
+    SA_CUDA(ctx, launch_tile_fold(lc, ctx->cur, ctx->tile_first, ntiles, ctx->rec, ctx->bigu,
+                                  ctx->tile_state, N, d_jc, d_ir, d_pr, cap, ctx->err));
+    if ((rc = mark(ctx, nullptr))) return rc;
+    ctx->launches = lc.launches;
+    return SA_OK;
+}
+
+int sa_finish(sa_ctx *ctx, int64_t *nnz, int64_t *bad_pos, int *bad_which) {
+    if (!ctx) return SA_ERR_INVALID_ARG;
+    SA_CUDA(ctx, cudaSetDevice(ctx->device));
+    SA_CUDA(ctx, cudaMemcpyAsync(ctx->err_host, ctx->err, sizeof(ErrState), cudaMemcpyDeviceToHost, ctx->stream));
+    SA_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    return decode(ctx, *ctx->err_host, nnz, bad_pos, bad_which);
+}
+
+int sa_host_upload(sa_ctx *ctx, const int32_t *h_ii, const int32_t *h_jj, const double *h_s,
+                   int64_t s_stride, int64_t L) {
+    if (!ctx) return SA_ERR_INVALID_ARG;
+    if (L < 0 || (L > 0 && (!h_ii || !h_jj || !h_s)) || (s_stride != 0 && s_stride != 1))
+        return fail(ctx, SA_ERR_INVALID_ARG, "sa_host_upload: bad arguments");
+    SA_CUDA(ctx, cudaSetDevice(ctx->device));
+    ctx->host_nnz = -1;
+    ctx->host_L = L;
+    ctx->host_stride = s_stride;
+    const size_t nl = (size_t)std::max<int64_t>(L, 1);
+    const size_t ns = s_stride ? nl : 1;
+    SA_CUDA(ctx, ensure(ctx->h_ii, ctx->hii_cap, nl));
+    SA_CUDA(ctx, ensure(ctx->h_jj, ctx->hjj_cap, nl));
+    SA_CUDA(ctx, ensure(ctx->h_s, ctx->hs_cap, ns));
+    if (L > 0) {
+        SA_CUDA(ctx, cudaMemcpyAsync(ctx->h_ii, h_ii, (size_t)L * 4, cudaMemcpyHostToDevice, ctx->stream));
+        SA_CUDA(ctx, cudaMemcpyAsync(ctx->h_jj, h_jj, (size_t)L * 4, cudaMemcpyHostToDevice, ctx->stream));
+        SA_CUDA(ctx, cudaMemcpyAsync(ctx->h_s, h_s, ns * 8, cudaMemcpyHostToDevice, ctx->stream));
+    }
+    return SA_OK;
+}
+
+int sa_host_dims(sa_ctx *ctx, int32_t *M, int32_t *N, int64_t *bad_pos, int *bad_which) {
+    if (!ctx) return SA_ERR_INVALID_ARG;
+    if (ctx->host_L < 0) return fail(ctx, SA_ERR_INVALID_ARG, "sa_host_dims: nothing uploaded");
+    return sa_infer_dims(ctx, ctx->h_ii, ctx->h_jj, ctx->host_L, M, N, bad_pos, bad_which);
+}
+
+int sa_host_assemble(sa_ctx *ctx, int32_t M, int32_t N, int64_t *nnz, int64_t *bad_pos,
+                     int *bad_which) {
+    if (!ctx) return SA_ERR_INVALID_ARG;
+    if (ctx->host_L < 0) return fail(ctx, SA_ERR_INVALID_ARG, "sa_host_assemble: nothing uploaded");
+    if (M < 0 || N < 0) return fail(ctx, SA_ERR_INVALID_ARG, "sa_host_assemble: negative dimensions");
+    ctx->host_nnz = -1;
+    SA_CUDA(ctx, cudaSetDevice(ctx->device));
+    const size_t nl = (size_t)std::max<int64_t>(ctx->host_L, 1);
+    SA_CUDA(ctx, ensure(ctx->o_jc, ctx->ojc_cap, (size_t)N + 1));
+    SA_CUDA(ctx, ensure(ctx->o_ir, ctx->oir_cap, nl));
+    SA_CUDA(ctx, ensure(ctx->o_pr, ctx->opr_cap, nl));
+    int rc = sa_assemble_async(ctx, ctx->h_ii, ctx->h_jj, ctx->h_s, ctx->host_stride, ctx->host_L,
+                               M, N, ctx->o_jc, ctx->o_ir, ctx->o_pr, (int64_t)nl);
+    if (rc) return rc;
+    int64_t z = 0;
+    rc = sa_finish(ctx, &z, bad_pos, bad_which);
+    if (rc) return rc;
+    if (nnz) *nnz = z;
+    ctx->host_nnz = z;
+    ctx->host_N = N;
+    return SA_OK;
+}
+
+int sa_host_fetch(sa_ctx *ctx, int32_t *h_jc, int32_t *h_ir, double *h_pr) {
+    if (!ctx) return SA_ERR_INVALID_ARG;
+    if (ctx->host_nnz < 0) return fail(ctx, SA_ERR_INVALID_ARG, "sa_host_fetch: no assembled result");
+    if (!h_jc || (ctx->host_nnz > 0 && (!h_ir || !h_pr)))
+        return fail(ctx, SA_ERR_INVALID_ARG, "sa_host_fetch: null output");
+    SA_CUDA(ctx, cudaSetDevice(ctx->device));
+    SA_CUDA(ctx, cudaMemcpyAsync(h_jc, ctx->o_jc, ((size_t)ctx->host_N + 1) * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    if (ctx->host_nnz > 0) {
+        SA_CUDA(ctx, cudaMemcpyAsync(h_ir, ctx->o_ir, (size_t)ctx->host_nnz * 4, cudaMemcpyDeviceToHost, ctx->stream));
+        SA_CUDA(ctx, cudaMemcpyAsync(h_pr, ctx->o_pr, (size_t)ctx->host_nnz * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    }
+    SA_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    return SA_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,225 @@
+// sa_internal.cuh -- shared device helpers and launch declarations for the
+// B200 sparse-assembly kernels (sm_100a).  Not part of the public ABI.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace sa {
+
+constexpr unsigned FULL = 0xffffffffu;
+
+// Column cursor word (cur[c]): low 31 bits a triplet offset, bit 31 set when
+// column c is "big" (more than BIGCOL triplets) and takes the big-column path.
+constexpr uint32_t BIGFLAG = 0x80000000u;
+constexpr uint32_t POSMASK = 0x7fffffffu;
+
+// Tile geometry of the column-tile fold (k_tile_fold).  A tile owns the
+// columns whose first triplet lies in [b*TILE, (b+1)*TILE); columns longer
+// than BIGCOL are folded by k_bigcol instead, so a tile holds at most
+// TILE + BIGCOL triplets in shared memory.
+constexpr int TILE = 512;
+constexpr int BIGCOL = 512;
+constexpr int TCAP = TILE + BIGCOL;
+constexpr int TILE_THREADS = 256;
+
+// Device-side outcome of one assembly (zeroed / reset before every call).
+struct ErrState {
+    unsigned long long bad_i;   // first row index < 1 (or invalid raw value)
+    unsigned long long bad_j;   // first column index < 1
+    unsigned int over_m;        // a valid row index exceeded M
+    unsigned int over_n;        // a valid column index exceeded N
+    unsigned int max_i;         // maxima, for dimension inference
+    unsigned int max_j;
+    unsigned int cap_exceeded;  // nnz > caller capacity
+    unsigned int internal;      // device consistency check failed
+    long long nnz;              // written by the last tile
+    unsigned int tile_ticket;   // dynamic tile counters (forward progress)
+    unsigned int scan_ticket;
+    unsigned int nbig;          // number of big columns
+    unsigned int pad;
+};
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+    unsigned m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+// x86 SSE `addsd acc, v` semantics, which the reference's compiled scatter
+// (_kernels.pyx:82-89, `pr[k] += sr[i]`) obeys.  B200 add.f64 agrees except
+// when both operands are NaN: it returns the second operand's payload while
+// x86 keeps the first (probe: tools/probe/nanprobe.cu).  A NaN accumulator
+// is already quiet (it came out of an add), so keeping it is exact.
+__device__ __forceinline__ double fold_add(double acc, double v) {
+    return (acc != acc) ? acc : __dadd_rn(acc, v);
+}
+
+// ---- decoupled look-back (single-pass chained scan) ----------------------
+// status word: bits 63:62 flag (0 empty, 1 aggregate, 2 inclusive prefix),
+// bits 61:0 value.
+constexpr unsigned long long LB_VALMASK = (1ull << 62) - 1;
+__device__ __forceinline__ unsigned long long lb_pack(unsigned flag, unsigned long long v) {
+    return (static_cast<unsigned long long>(flag) << 62) | v;
+}
+
+// Called by one full warp of tile `b`.  Publishes `agg`, returns the
+// exclusive prefix of all tiles < b, and publishes the inclusive prefix.
+__device__ __forceinline__ unsigned long long lookback_warp(
+    unsigned long long *st, long long b, unsigned long long agg) {
+    const int lane = threadIdx.x & 31;
+    volatile unsigned long long *vst = st;
+    if (b == 0) {
+        if (lane == 0) {
+            __threadfence();
+            vst[0] = lb_pack(2, agg);
+        }
+        return 0;
+    }
+    if (lane == 0) {
+        __threadfence();
+        vst[b] = lb_pack(1, agg);
+    }
+    unsigned long long excl = 0;
+    long long base = b - 1;
+    while (true) {
+        long long idx = base - lane;
+        unsigned long long w = (idx >= 0) ? vst[idx] : lb_pack(2, 0);
+        unsigned flag = static_cast<unsigned>(w >> 62);
+        if (__any_sync(FULL, flag == 0)) continue;  // predecessors not published yet
+        unsigned pm = __ballot_sync(FULL, flag == 2);
+        int stop = pm ? (__ffs(pm) - 1) : 31;
+        unsigned long long v = (lane <= stop) ? (w & LB_VALMASK) : 0ull;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+        excl += v;
+        if (pm) break;
+        base -= 32;
+    }
+    if (lane == 0) {
+        __threadfence();
+        vst[b] = lb_pack(2, excl + agg);
+    }
+    return excl;
+}
+
+// ---- block scans ----------------------------------------------------------
+// Exclusive sum over one value per thread; returns the exclusive prefix and
+// the block total.  s_warp needs NT/32 slots.  Ends with a barrier.
+template <int NT, typename T>
+__device__ __forceinline__ T block_excl_sum(T v, T *s_warp, T &total) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    T x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        T y = __shfl_up_sync(FULL, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) s_warp[w] = x;
+    __syncthreads();
+    if (w == 0) {
+        T t = (lane < NT / 32) ? s_warp[lane] : T(0);
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            T y = __shfl_up_sync(FULL, t, o);
+            if (lane >= o) t += y;
+        }
+        if (lane < NT / 32) s_warp[lane] = t;
+    }
+    __syncthreads();
+    T wpre = w ? s_warp[w - 1] : T(0);
+    total = s_warp[NT / 32 - 1];
+    __syncthreads();
+    return wpre + x - v;
+}
+
+// In-place exclusive sum over arr[0..n) in shared memory (n <= NT*IPT).
+// Returns the total.  Each thread owns IPT consecutive entries.
+template <int NT, int IPT, typename T>
+__device__ __forceinline__ T smem_excl_scan(T *arr, int n, T *s_warp) {
+    const int base = threadIdx.x * IPT;
+    T loc[IPT];
+    T sum = 0;
+#pragma unroll
+    for (int k = 0; k < IPT; ++k) {
+        loc[k] = (base + k < n) ? arr[base + k] : T(0);
+        sum += loc[k];
+    }
+    T total;
+    T pre = block_excl_sum<NT, T>(sum, s_warp, total);
+#pragma unroll
+    for (int k = 0; k < IPT; ++k) {
+        if (base + k < n) arr[base + k] = pre;
+        pre += loc[k];
+    }
+    __syncthreads();
+    return total;
+}
+
+// In-place inclusive max-scan over arr[0..n) (non-negative ints).
+template <int NT, int IPT>
+__device__ __forceinline__ void smem_incl_max(int *arr, int n, int *s_warp) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int base = threadIdx.x * IPT;
+    int loc[IPT];
+    int run = 0;
+#pragma unroll
+    for (int k = 0; k < IPT; ++k) {
+        int v = (base + k < n) ? arr[base + k] : 0;
+        run = max(run, v);
+        loc[k] = run;
+    }
+    int x = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(FULL, x, o);
+        if (lane >= o) x = max(x, y);
+    }
+    if (lane == 31) s_warp[w] = x;
+    __syncthreads();
+    if (w == 0) {
+        int t = (lane < NT / 32) ? s_warp[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int y = __shfl_up_sync(FULL, t, o);
+            if (lane >= o) t = max(t, y);
+        }
+        if (lane < NT / 32) s_warp[lane] = t;
+    }
+    __syncthreads();
+    int wpre = w ? s_warp[w - 1] : 0;
+    int tpre = __shfl_up_sync(FULL, x, 1);
+    if (lane == 0) tpre = 0;
+    int pre = max(wpre, tpre);
+#pragma unroll
+    for (int k = 0; k < IPT; ++k)
+        if (base + k < n) arr[base + k] = max(pre, loc[k]);
+    __syncthreads();
+}
+
+// ---- launchers (sa_kernels.cu) ---------------------------------------------
+struct Launch {
+    cudaStream_t stream;
+    int num_sms;
+    int launches;  // incremented per kernel launch
+};
+
+cudaError_t launch_convert(Launch &lc, const void *raw, int dtype, int64_t L, int32_t *out,
+                           ErrState *err);
+cudaError_t launch_hist(Launch &lc, const int32_t *ii, const int32_t *jj, int64_t L,
+                        int32_t M, int32_t N, uint32_t *cnt, ErrState *err, bool infer);
+cudaError_t launch_col_scan(Launch &lc, uint32_t *cur, int32_t N, int64_t L,
+                            int32_t *tile_first, int64_t ntiles, uint32_t *big_list,
+                            unsigned long long *scan_state, ErrState *err);
+cudaError_t launch_scatter(Launch &lc, const int32_t *ii, const int32_t *jj, const double *s,
+                           int64_t s_stride, int64_t L, int32_t M, int32_t N, uint32_t *cur,
+                           int4 *rec);
+cudaError_t launch_bigcol(Launch &lc, const uint32_t *cur, const uint32_t *big_list,
+                          const ErrState *err, int4 *rec, const double *s, int64_t s_stride,
+                          uint32_t *bigu, int idx_bits, int passes);
+cudaError_t launch_tile_fold(Launch &lc, const uint32_t *cur, const int32_t *tile_first,
+                             int64_t ntiles, const int4 *rec, const uint32_t *bigu,
+                             unsigned long long *tile_state, int32_t N, int32_t *jc,
+                             int32_t *ir, double *pr, int64_t cap, ErrState *err);
+
+}  // namespace sa

@@ -1,0 +1,804 @@
+// sa_kernels.cu -- hand-written sm_100a kernels for sparse(i,j,s,m,n).
+//
+// Pipeline (one stream, no host round trip):
+//   k_hist       column histogram of the triplets + index validation
+//                (types.py:121-165 semantics), warp-aggregated atomics
+//   k_col_scan   single-pass decoupled-look-back exclusive scan of the column
+//                counts -> column cursors; also the tile -> first-column map
+//                and the list of big columns
+//   k_scatter    counting-sort scatter by column: 16-byte records
+//                {row, input position, value} at cursor positions
+//   k_bigcol     columns longer than BIGCOL: in-place LSD radix sort by
+//                (row, input position), ordered fold
+//   k_tile_fold  per tile of columns, in shared memory: hash (column,row)
+//                groups, order each group by input position, fold from +0.0
+//                in input order (bit-exact with the reference scatter,
+//                _kernels.pyx:82-89), order groups by row, chained scan of
+//                the unique counts -> jc, ir, pr written once.
+//
+// Reference algorithm: serial.py:111-168 / _kernels.pyx:20-89 (row-first
+// counting sort).  This pipeline is column-first; it produces the same CSC
+// because both order entries by (column, row) and fold duplicates in
+// ascending input order.
+
+#include "sa_internal.cuh"
+
+namespace sa {
+
+// ---------------------------------------------------------------------------
+// index validation / conversion of raw (non-int32) index arrays
+// ---------------------------------------------------------------------------
+__global__ void k_convert(const void *__restrict__ raw, int dtype, int64_t L,
+                          int32_t *__restrict__ out, ErrState *err) {
+    unsigned mx = 0;
+    unsigned long long bad = ~0ull;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < L; t += stride) {
+        bool ok;
+        int32_t v = 0;
+        if (dtype == 1) {
+            long long x = static_cast<const long long *>(raw)[t];
+            ok = x >= 1 && x <= 2147483647LL;
+            v = (int32_t)x;
+        } else if (dtype == 2) {
+            double x = static_cast<const double *>(raw)[t];
+            ok = (x >= 1.0) && (x == ceil(x)) && (x <= 2147483647.0);
+            v = ok ? (int32_t)x : 0;
+        } else {
+            int32_t x = static_cast<const int32_t *>(raw)[t];
+            ok = x >= 1;
+            v = x;
+        }
+        if (!ok) bad = min(bad, (unsigned long long)t);
+        else {
+            out[t] = v;
+            mx = max(mx, (unsigned)v);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        mx = max(mx, __shfl_xor_sync(FULL, mx, o));
+        bad = min(bad, __shfl_xor_sync(FULL, bad, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (mx) atomicMax(&err->max_i, mx);
+        if (bad != ~0ull) atomicMin(&err->bad_i, bad);
+    }
+}
+
+cudaError_t launch_convert(Launch &lc, const void *raw, int dtype, int64_t L, int32_t *out,
+                           ErrState *err) {
+    if (L <= 0) return cudaSuccess;
+    int64_t want = (L + 255) / 256;
+    int grid = (int)std::min<int64_t>(want, (int64_t)lc.num_sms * 8);
+    k_convert<<<grid, 256, 0, lc.stream>>>(raw, dtype, L, out, err);
+    lc.launches++;
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// k_hist: column histogram + validation.  infer != 0: inference mode
+// (validation and maxima only).  Warp-aggregated: lanes holding the same
+// column issue one atomic (FEM element order makes neighbours share columns).
+// ---------------------------------------------------------------------------
+struct HistAcc {
+    unsigned long long bad_i = ~0ull, bad_j = ~0ull;
+    unsigned maxi = 0, maxj = 0;
+    unsigned over_m = 0, over_n = 0;
+};
+
+__device__ __forceinline__ void hist_one(int64_t t, int32_t i, int32_t j, bool live, int32_t M,
+                                         int32_t N, uint32_t *__restrict__ cnt, HistAcc &a) {
+    const bool bi = live && i < 1, bj = live && j < 1;
+    if (bi) a.bad_i = min(a.bad_i, (unsigned long long)t);
+    if (bj) a.bad_j = min(a.bad_j, (unsigned long long)t);
+    const bool valid = live && !bi && !bj;
+    if (valid) {
+        a.maxi = max(a.maxi, (unsigned)i);
+        a.maxj = max(a.maxj, (unsigned)j);
+    }
+    if (cnt == nullptr) return;  // inference mode (warp-uniform)
+    const bool ok = valid && i <= M && j <= N;
+    if (valid && !ok) {
+        if (i > M) a.over_m = 1;
+        if (j > N) a.over_n = 1;
+    }
+    const unsigned act = __ballot_sync(FULL, ok);
+    if (ok) {
+        const unsigned peers = __match_any_sync(act, j);
+        const int leader = __ffs(peers) - 1;
+        if ((threadIdx.x & 31) == leader) atomicAdd(&cnt[j - 1], (uint32_t)__popc(peers));
+    }
+}
+
+__global__ void __launch_bounds__(256) k_hist(const int32_t *__restrict__ ii,
+                                              const int32_t *__restrict__ jj, int64_t L,
+                                              int32_t M, int32_t N, uint32_t *__restrict__ cnt,
+                                              ErrState *err, int vec, int infer) {
+    HistAcc a;
+    if (infer) cnt = nullptr;
+    const int lane = threadIdx.x & 31;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t wbase0 = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31);
+    int64_t tail0 = 0;
+    if (vec) {
+        const int64_t nq = L >> 2;
+        const int4 *ii4 = reinterpret_cast<const int4 *>(ii);
+        const int4 *jj4 = reinterpret_cast<const int4 *>(jj);
+        for (int64_t qb = wbase0; qb < nq; qb += stride) {
+            const int64_t q = qb + lane;
+            const bool live = q < nq;
+            int4 vi = make_int4(1, 1, 1, 1), vj = make_int4(1, 1, 1, 1);
+            if (live) {
+                vi = __ldg(ii4 + q);
+                vj = __ldg(jj4 + q);
+            }
+            hist_one(4 * q + 0, vi.x, vj.x, live, M, N, cnt, a);
+            hist_one(4 * q + 1, vi.y, vj.y, live, M, N, cnt, a);
+            hist_one(4 * q + 2, vi.z, vj.z, live, M, N, cnt, a);
+            hist_one(4 * q + 3, vi.w, vj.w, live, M, N, cnt, a);
+        }
+        tail0 = nq << 2;
+    }
+    for (int64_t tb = tail0 + wbase0; tb < L; tb += stride) {
+        const int64_t t = tb + lane;
+        const bool live = t < L;
+        int32_t i = live ? ii[t] : 1, j = live ? jj[t] : 1;
+        hist_one(t, i, j, live, M, N, cnt, a);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        a.bad_i = min(a.bad_i, __shfl_xor_sync(FULL, a.bad_i, o));
+        a.bad_j = min(a.bad_j, __shfl_xor_sync(FULL, a.bad_j, o));
+        a.maxi = max(a.maxi, __shfl_xor_sync(FULL, a.maxi, o));
+        a.maxj = max(a.maxj, __shfl_xor_sync(FULL, a.maxj, o));
+        a.over_m |= __shfl_xor_sync(FULL, a.over_m, o);
+        a.over_n |= __shfl_xor_sync(FULL, a.over_n, o);
+    }
+    if (lane == 0) {
+        if (a.bad_i != ~0ull) atomicMin(&err->bad_i, a.bad_i);
+        if (a.bad_j != ~0ull) atomicMin(&err->bad_j, a.bad_j);
+        if (infer) {
+            if (a.maxi) atomicMax(&err->max_i, a.maxi);
+            if (a.maxj) atomicMax(&err->max_j, a.maxj);
+        }
+        if (a.over_m) err->over_m = 1;
+        if (a.over_n) err->over_n = 1;
+    }
+}
+
+static inline bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+cudaError_t launch_hist(Launch &lc, const int32_t *ii, const int32_t *jj, int64_t L, int32_t M,
+                        int32_t N, uint32_t *cnt, ErrState *err, bool infer) {
+    if (L <= 0) return cudaSuccess;
+    const int vec = aligned16(ii) && aligned16(jj);
+    int64_t want = ((vec ? (L >> 2) : L) + 255) / 256 + 1;
+    int grid = (int)std::min<int64_t>(want, (int64_t)lc.num_sms * 8);
+    k_hist<<<grid, 256, 0, lc.stream>>>(ii, jj, L, M, N, cnt, err, vec, infer ? 1 : 0);
+    lc.launches++;
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// k_col_scan: exclusive scan of cnt[0..N) in place (cur[c] = first triplet
+// slot of column c, | BIGFLAG for big columns), decoupled look-back across
+// CTAs (ticket-ordered for forward progress).  Also emits
+//   tile_first[b] = min{c : start(c) >= b*TILE}   for 0 <= b <= ntiles
+//   big_list[]    = columns with more than BIGCOL triplets.
+// ---------------------------------------------------------------------------
+constexpr int SCAN_NT = 256;
+constexpr int SCAN_IPT = 16;
+constexpr int SCAN_TILE = SCAN_NT * SCAN_IPT;
+
+__global__ void __launch_bounds__(SCAN_NT) k_col_scan(uint32_t *__restrict__ cur, int32_t N,
+                                                      int64_t L, int32_t *__restrict__ tile_first,
+                                                      int64_t ntiles, uint32_t *__restrict__ big_list,
+                                                      unsigned long long *scan_state,
+                                                      ErrState *err) {
+    __shared__ uint32_t s_v[SCAN_TILE];
+    __shared__ uint32_t s_warp[SCAN_NT / 32];
+    __shared__ long long s_b;
+    __shared__ unsigned long long s_excl;
+    if (threadIdx.x == 0) s_b = atomicAdd(&err->scan_ticket, 1u);
+    __syncthreads();
+    const long long b = s_b;
+    const int64_t c_base = b * SCAN_TILE;
+    for (int k = threadIdx.x; k < SCAN_TILE; k += SCAN_NT) {
+        int64_t c = c_base + k;
+        s_v[k] = (c < N) ? cur[c] : 0u;
+    }
+    __syncthreads();
+    uint32_t loc[SCAN_IPT];
+    uint32_t sum = 0;
+#pragma unroll
+    for (int k = 0; k < SCAN_IPT; ++k) {
+        loc[k] = s_v[threadIdx.x * SCAN_IPT + k];
+        sum += loc[k];
+    }
+    uint32_t total;
+    uint32_t pre = block_excl_sum<SCAN_NT, uint32_t>(sum, s_warp, total);
+    if (threadIdx.x < 32) {
+        unsigned long long e = lookback_warp(scan_state, b, total);
+        if (threadIdx.x == 0) s_excl = e;
+    }
+    __syncthreads();
+    uint64_t start = s_excl + pre;
+#pragma unroll
+    for (int k = 0; k < SCAN_IPT; ++k) {
+        const int64_t c = c_base + threadIdx.x * SCAN_IPT + k;
+        const uint32_t n = loc[k];
+        uint32_t word = (uint32_t)start;
+        if (c < N) {
+            if (n > (uint32_t)BIGCOL) {
+                word |= BIGFLAG;
+                unsigned slot = atomicAdd(&err->nbig, 1u);
+                big_list[slot] = (uint32_t)c;
+            }
+            // tiles b' with start < b'*TILE <= start + n begin at column c+1
+            if (n) {
+                int64_t first = (int64_t)(start / TILE) + 1;
+                int64_t last = (int64_t)((start + n) / TILE);
+                if (last > ntiles - 1) last = ntiles - 1;
+                for (int64_t bb = first; bb <= last; ++bb) tile_first[bb] = (int32_t)(c + 1);
+            }
+        }
+        if (c == N - 1) {
+            // tiles past the valid total (invalid triplets were dropped) are empty
+            for (int64_t bb = (int64_t)((start + n) / TILE) + 1; bb <= ntiles; ++bb) tile_first[bb] = N;
+        }
+        s_v[threadIdx.x * SCAN_IPT + k] = word;
+        start += n;
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < SCAN_TILE; k += SCAN_NT) {
+        int64_t c = c_base + k;
+        if (c < N) cur[c] = s_v[k];
+    }
+    if (b == 0 && threadIdx.x == 0) {
+        tile_first[0] = 0;
+        tile_first[ntiles] = N;
+    }
+}
+
+cudaError_t launch_col_scan(Launch &lc, uint32_t *cur, int32_t N, int64_t L, int32_t *tile_first,
+                            int64_t ntiles, uint32_t *big_list, unsigned long long *scan_state,
+                            ErrState *err) {
+    if (N <= 0) return cudaSuccess;
+    int grid = (int)((N + SCAN_TILE - 1) / SCAN_TILE);
+    k_col_scan<<<grid, SCAN_NT, 0, lc.stream>>>(cur, N, L, tile_first, ntiles, big_list,
+                                               scan_state, err);
+    lc.launches++;
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// k_scatter: counting-sort scatter by column.  Record = {row, input position,
+// value lo, value hi}.  Within a column the slot order is whatever the
+// atomics produce; the fold restores input order from the stored position.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void scatter_one(int64_t t, int32_t i, int32_t j, double v, bool live,
+                                            int32_t M, int32_t N, uint32_t *__restrict__ cur,
+                                            int4 *__restrict__ rec) {
+    const bool ok = live && i >= 1 && j >= 1 && i <= M && j <= N;
+    const unsigned act = __ballot_sync(FULL, ok);
+    if (!ok) return;
+    const unsigned peers = __match_any_sync(act, j);
+    const int lane = threadIdx.x & 31;
+    const int leader = __ffs(peers) - 1;
+    uint32_t base = 0;
+    if (lane == leader) base = atomicAdd(&cur[j - 1], (uint32_t)__popc(peers));
+    base = __shfl_sync(act, base, leader);
+    const uint32_t pos = (base & POSMASK) + __popc(peers & lanemask_lt());
+    rec[pos] = make_int4(i, (int)t, __double2loint(v), __double2hiint(v));
+}
+
+__global__ void __launch_bounds__(256) k_scatter(const int32_t *__restrict__ ii,
+                                                 const int32_t *__restrict__ jj,
+                                                 const double *__restrict__ s, int64_t s_stride,
+                                                 int64_t L, int32_t M, int32_t N,
+                                                 uint32_t *__restrict__ cur,
+                                                 int4 *__restrict__ rec, int vec) {
+    const int lane = threadIdx.x & 31;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t wbase0 = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31);
+    int64_t tail0 = 0;
+    if (vec) {
+        const int64_t nq = L >> 2;
+        const int4 *ii4 = reinterpret_cast<const int4 *>(ii);
+        const int4 *jj4 = reinterpret_cast<const int4 *>(jj);
+        const double2 *s2 = reinterpret_cast<const double2 *>(s);
+        const double s0 = s_stride ? 0.0 : __ldg(s);
+        for (int64_t qb = wbase0; qb < nq; qb += stride) {
+            const int64_t q = qb + lane;
+            const bool live = q < nq;
+            int4 vi = make_int4(1, 1, 1, 1), vj = make_int4(1, 1, 1, 1);
+            double2 va = make_double2(s0, s0), vb = make_double2(s0, s0);
+            if (live) {
+                vi = __ldg(ii4 + q);
+                vj = __ldg(jj4 + q);
+                if (s_stride) {
+                    va = __ldg(s2 + 2 * q);
+                    vb = __ldg(s2 + 2 * q + 1);
+                }
+            }
+            scatter_one(4 * q + 0, vi.x, vj.x, va.x, live, M, N, cur, rec);
+            scatter_one(4 * q + 1, vi.y, vj.y, va.y, live, M, N, cur, rec);
+            scatter_one(4 * q + 2, vi.z, vj.z, vb.x, live, M, N, cur, rec);
+            scatter_one(4 * q + 3, vi.w, vj.w, vb.y, live, M, N, cur, rec);
+        }
+        tail0 = nq << 2;
+    }
+    for (int64_t tb = tail0 + wbase0; tb < L; tb += stride) {
+        const int64_t t = tb + lane;
+        const bool live = t < L;
+        int32_t i = live ? ii[t] : 0, j = live ? jj[t] : 0;
+        double v = live ? s[t * s_stride] : 0.0;
+        scatter_one(t, i, j, v, live, M, N, cur, rec);
+    }
+}
+
+cudaError_t launch_scatter(Launch &lc, const int32_t *ii, const int32_t *jj, const double *s,
+                           int64_t s_stride, int64_t L, int32_t M, int32_t N, uint32_t *cur,
+                           int4 *rec) {
+    if (L <= 0) return cudaSuccess;
+    const int vec = aligned16(ii) && aligned16(jj) && (s_stride == 0 || aligned16(s));
+    int64_t want = ((vec ? (L >> 2) : L) + 255) / 256 + 1;
+    int grid = (int)std::min<int64_t>(want, (int64_t)lc.num_sms * 8);
+    k_scatter<<<grid, 256, 0, lc.stream>>>(ii, jj, s, s_stride, L, M, N, cur, rec, vec);
+    lc.launches++;
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// k_bigcol: one CTA per big column (grid-stride over the device-side list).
+// The column's 16-byte records are reused in place as two 8-byte key
+// buffers A|B: key = (row-1) << idx_bits | input position.  Stable LSD radix
+// passes (8-bit digits, warp match + per-warp digit counts) sort by (row,
+// position); values are gathered from the input by position; each run of
+// equal rows is folded from +0.0 in position order.  Results: row-1 in the
+// key buffer, value bits in the other buffer, at index = run number;
+// bigu[c] = runs | (BIGFLAG if keys ended in buffer B).
+// ---------------------------------------------------------------------------
+constexpr int BIG_NT = 256;
+
+__global__ void __launch_bounds__(BIG_NT) k_bigcol(const uint32_t *__restrict__ cur,
+                                                   const uint32_t *__restrict__ big_list,
+                                                   const ErrState *err, int4 *rec,
+                                                   const double *__restrict__ s, int64_t s_stride,
+                                                   uint32_t *__restrict__ bigu, int idx_bits,
+                                                   int passes) {
+    __shared__ uint32_t s_hist[256];
+    __shared__ uint32_t s_bin[256];
+    __shared__ uint16_t s_wcnt[BIG_NT / 32][257];
+    __shared__ uint32_t s_warp[BIG_NT / 32];
+    __shared__ unsigned long long s_prevrow;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const unsigned nbig = *((volatile const unsigned *)&err->nbig);
+    for (int k = tid; k < (BIG_NT / 32) * 257; k += BIG_NT) (&s_wcnt[0][0])[k] = 0;
+    __syncthreads();
+    const unsigned long long idx_mask = (1ull << idx_bits) - 1;
+    for (unsigned kb = blockIdx.x; kb < nbig; kb += gridDim.x) {
+        const uint32_t c = big_list[kb];
+        const uint32_t e = cur[c] & POSMASK;
+        const uint32_t st = c ? (cur[c - 1] & POSMASK) : 0u;
+        const int64_t n = (int64_t)e - st;
+        unsigned long long *A = reinterpret_cast<unsigned long long *>(rec + st);
+        unsigned long long *B = A + n;
+        // pack records -> keys in A (ascending chunks; reads stay ahead of writes)
+        for (int64_t base = 0; base < n; base += BIG_NT) {
+            const int64_t p = base + tid;
+            int4 r = make_int4(0, 0, 0, 0);
+            if (p < n) r = rec[st + p];
+            __syncthreads();
+            if (p < n)
+                A[p] = ((unsigned long long)(uint32_t)(r.x - 1) << idx_bits) | (uint32_t)r.y;
+            __syncthreads();
+        }
+        unsigned long long *src = A, *dst = B;
+        for (int ps = 0; ps < passes; ++ps) {
+            const int shift = 8 * ps;
+            for (int k = tid; k < 256; k += BIG_NT) s_hist[k] = 0;
+            __syncthreads();
+            for (int64_t p = tid; p < n; p += BIG_NT) atomicAdd(&s_hist[(src[p] >> shift) & 255], 1u);
+            __syncthreads();
+            {
+                uint32_t tot;
+                uint32_t v = s_hist[tid];
+                uint32_t pre = block_excl_sum<BIG_NT, uint32_t>(v, s_warp, tot);
+                s_bin[tid] = pre;
+            }
+            __syncthreads();
+            for (int64_t base = 0; base < n; base += BIG_NT) {
+                const int64_t p = base + tid;
+                const bool valid = p < n;
+                const unsigned long long key = valid ? src[p] : 0ull;
+                const int d = valid ? (int)((key >> shift) & 255) : 256;
+                const unsigned peers = __match_any_sync(FULL, d);
+                const int leader = __ffs(peers) - 1;
+                const int wrank = __popc(peers & lanemask_lt());
+                if (lane == leader) s_wcnt[warp][d] = (uint16_t)__popc(peers);
+                __syncthreads();
+                if (valid) {
+                    uint32_t pre = s_bin[d];
+                    for (int w2 = 0; w2 < warp; ++w2) pre += s_wcnt[w2][d];
+                    dst[pre + wrank] = key;
+                }
+                __syncthreads();
+                if (lane == leader) {
+                    if (valid) atomicAdd(&s_bin[d], (uint32_t)__popc(peers));
+                    s_wcnt[warp][d] = 0;
+                }
+                __syncthreads();
+            }
+            unsigned long long *tmp = src;
+            src = dst;
+            dst = tmp;
+        }
+        // gather values in sorted order into the other buffer
+        for (int64_t p = tid; p < n; p += BIG_NT) {
+            const unsigned long long idx = src[p] & idx_mask;
+            dst[p] = (unsigned long long)__double_as_longlong(s[idx * s_stride]);
+        }
+        if (tid == 0) s_prevrow = ~0ull;
+        __syncthreads();
+        // ordered fold of runs of equal rows
+        uint32_t carry = 0;
+        for (int64_t base = 0; base < n; base += BIG_NT) {
+            const int64_t p = base + tid;
+            const bool valid = p < n;
+            const unsigned long long row = valid ? (src[p] >> idx_bits) : 0ull;
+            const unsigned long long prev =
+                (tid == 0) ? s_prevrow : (valid ? (src[p - 1] >> idx_bits) : 0ull);
+            const bool head = valid && row != prev;
+            uint32_t tot;
+            uint32_t run = block_excl_sum<BIG_NT, uint32_t>(head ? 1u : 0u, s_warp, tot) + carry;
+            double acc = 0.0;
+            if (head) {
+                int64_t q = p;
+                bool more = true;
+                while (more) {
+                    unsigned long long kk[8], vv[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const bool in = q + u < n;
+                        kk[u] = in ? src[q + u] : ~0ull;
+                        vv[u] = in ? dst[q + u] : 0ull;
+                    }
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        if (more && (kk[u] >> idx_bits) == row)
+                            acc = fold_add(acc, __longlong_as_double((long long)vv[u]));
+                        else
+                            more = false;
+                    }
+                    q += 8;
+                }
+            }
+            if (p == base + BIG_NT - 1 && valid) s_prevrow = row;
+            if (!valid && tid == BIG_NT - 1) s_prevrow = row;
+            __syncthreads();
+            if (head) {
+                src[run] = row;  // row - 1 (key stores row-1)
+                dst[run] = (unsigned long long)__double_as_longlong(acc);
+            }
+            carry += tot;
+            __syncthreads();
+        }
+        if (tid == 0) bigu[c] = carry | ((src == B) ? BIGFLAG : 0u);
+        __syncthreads();
+    }
+}
+
+cudaError_t launch_bigcol(Launch &lc, const uint32_t *cur, const uint32_t *big_list,
+                          const ErrState *err, int4 *rec, const double *s, int64_t s_stride,
+                          uint32_t *bigu, int idx_bits, int passes) {
+    int grid = lc.num_sms;
+    k_bigcol<<<grid, BIG_NT, 0, lc.stream>>>(cur, big_list, err, rec, s, s_stride, bigu, idx_bits,
+                                            passes);
+    lc.launches++;
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// k_tile_fold: one CTA per column tile (ticket order), shared-memory only.
+// ---------------------------------------------------------------------------
+constexpr int HS = 2 * TCAP;  // hash slots (load factor <= 0.5)
+constexpr int CCAP = TILE;    // non-empty columns per tile (distinct starts in a TILE window)
+constexpr int NT = TILE_THREADS;
+constexpr int IPT = TCAP / NT;
+
+struct TileSmem {
+    int4 rec[TCAP];           // {row, input position, value lo, value hi}
+    int col[TCAP];            // head marks -> column-local index + 1
+    union {
+        struct {
+            unsigned long long key[HS];
+            int16_t gid[HS];
+        } h;
+        struct {
+            double sval[TCAP];     // group values in input order
+            int16_t members[TCAP]; // record ids grouped by (column,row)
+            int16_t colgrp[TCAP];  // group ids grouped by column
+        } o;
+    } u;
+    int g_cnt[TCAP];
+    int g_base[TCAP];
+    int16_t g_first[TCAP];
+    int16_t g_crank[TCAP];
+    int16_t r_gid[TCAP];
+    int16_t r_arr[TCAP];
+    int ci_col[CCAP];
+    int ci_start[CCAP];
+    int ci_q[CCAP];
+    int ci_cnt[CCAP];
+    int ci_u[CCAP];
+    int ci_base[CCAP + 1];
+    int warp_tmp[NT / 32];
+    int n_small, n_ci, n_groups, has_big, overflow;
+    long long tile;
+    long long P;
+};
+
+__device__ __forceinline__ unsigned hash_slot(unsigned long long key) {
+    return (unsigned)((key * 0x9E3779B97F4A7C15ull) >> 40) & (HS - 1);
+}
+
+__global__ void __launch_bounds__(NT, 2) k_tile_fold(const uint32_t *__restrict__ cur,
+                                                      const int32_t *__restrict__ tile_first,
+                                                      int64_t ntiles, const int4 *__restrict__ rec,
+                                                      const uint32_t *__restrict__ bigu,
+                                                      unsigned long long *tile_state, int32_t N,
+                                                      int32_t *__restrict__ jc,
+                                                      int32_t *__restrict__ ir,
+                                                      double *__restrict__ pr, int64_t cap,
+                                                      ErrState *err) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    TileSmem &S = *reinterpret_cast<TileSmem *>(smem_raw);
+    const int tid = threadIdx.x;
+
+    if (tid == 0) {
+        S.tile = atomicAdd(&err->tile_ticket, 1u);
+        S.n_groups = 0;
+        S.overflow = 0;
+    }
+    for (int k = tid; k < TCAP; k += NT) {
+        S.col[k] = 0;
+        S.g_cnt[k] = 0;
+    }
+    for (int k = tid; k < HS; k += NT) S.u.h.key[k] = 0ull;
+    __syncthreads();
+    const long long b = S.tile;
+    const int c0 = tile_first[b], c1 = tile_first[b + 1];
+
+    // ---- phase 1: columns of the tile -----------------------------------
+    int n_ci = 0, n_small = 0, has_big = 0;
+    for (int cb = c0; cb < c1; cb += NT) {
+        const int c = cb + tid;
+        const bool in = c < c1;
+        const uint32_t ew = in ? cur[c] : 0u;
+        const int e = (int)(ew & POSMASK);
+        const int big = (int)(ew >> 31);
+        const int st = in ? (c > 0 ? (int)(cur[c - 1] & POSMASK) : 0) : 0;
+        const int cnt = in ? e - st : 0;
+        const int ne = cnt > 0 ? 1 : 0;
+        const int sc = (ne && !big) ? cnt : 0;
+        int tot_ne, tot_sc;
+        const int ci = block_excl_sum<NT, int>(ne, S.warp_tmp, tot_ne) + n_ci;
+        const int q = block_excl_sum<NT, int>(sc, S.warp_tmp, tot_sc) + n_small;
+        const int anybig = __syncthreads_or(ne && big);
+        if (ne) {
+            if (ci < CCAP && q + sc <= TCAP) {
+                S.ci_col[ci] = c;
+                S.ci_start[ci] = st;
+                S.ci_q[ci] = big ? -1 : q;
+                S.ci_cnt[ci] = big ? 0 : cnt;
+                S.ci_u[ci] = big ? (int)(bigu[c] & POSMASK) : 0;
+                if (!big) S.col[q] = ci + 1;
+            } else {
+                S.overflow = 1;
+            }
+        }
+        n_ci += tot_ne;
+        n_small += tot_sc;
+        has_big |= anybig;
+    }
+    __syncthreads();
+    if (S.overflow) {
+        if (tid == 0) atomicExch(&err->internal, 1u);
+        n_ci = 0;
+        n_small = 0;
+    }
+
+    // ---- phase 2: stage the records ---------------------------------------
+    if (!has_big) {
+        const int r0 = n_ci ? S.ci_start[0] : 0;
+        for (int p = tid; p < n_small; p += NT) S.rec[p] = rec[r0 + p];
+    } else {
+        for (int ci = 0; ci < n_ci; ++ci) {
+            const int q = S.ci_q[ci];
+            if (q < 0) continue;
+            const int st = S.ci_start[ci], cnt = S.ci_cnt[ci];
+            for (int p = tid; p < cnt; p += NT) S.rec[q + p] = rec[st + p];
+        }
+    }
+    smem_incl_max<NT, IPT>(S.col, n_small, S.warp_tmp);  // ends with a barrier
+
+    // ---- phase 3: (column,row) groups via a shared-memory hash ------------
+    for (int p = tid; p < n_small; p += NT) {
+        const int row = S.rec[p].x;
+        const int ci = S.col[p] - 1;
+        const unsigned long long key = ((unsigned long long)(unsigned)ci << 32) | (unsigned)row;
+        unsigned h = hash_slot(key);
+        while (true) {
+            const unsigned long long old = atomicCAS(&S.u.h.key[h], 0ull, key);
+            if (old == 0ull) {
+                const int g = atomicAdd(&S.n_groups, 1);
+                S.u.h.gid[h] = (int16_t)g;
+                S.g_first[g] = (int16_t)p;
+                S.g_crank[g] = (int16_t)atomicAdd(&S.ci_u[ci], 1);
+                break;
+            }
+            if (old == key) break;
+            h = (h + 1) & (HS - 1);
+        }
+        S.r_gid[p] = (int16_t)h;
+    }
+    __syncthreads();
+    for (int p = tid; p < n_small; p += NT) {
+        const int g = S.u.h.gid[S.r_gid[p]];
+        S.r_gid[p] = (int16_t)g;
+        S.r_arr[p] = (int16_t)atomicAdd(&S.g_cnt[g], 1);
+    }
+    __syncthreads();
+    const int n_groups = S.n_groups;
+
+    // ---- phase 4: group offsets, column offsets, publish the aggregate ----
+    for (int g = tid; g < n_groups; g += NT) S.g_base[g] = S.g_cnt[g];
+    for (int k = tid; k < n_ci; k += NT) S.ci_base[k] = S.ci_u[k];
+    __syncthreads();
+    smem_excl_scan<NT, IPT, int>(S.g_base, n_groups, S.warp_tmp);
+    const int U = smem_excl_scan<NT, (CCAP + NT - 1) / NT, int>(S.ci_base, n_ci, S.warp_tmp);
+    if (tid == 0) {
+        S.ci_base[n_ci] = U;
+        volatile unsigned long long *vst = tile_state;
+        __threadfence();
+        if (b == 0) vst[0] = lb_pack(2, (unsigned long long)U);
+        else vst[b] = lb_pack(1, (unsigned long long)U);
+    }
+
+    // ---- phase 5: scatter members by group, groups by column --------------
+    for (int p = tid; p < n_small; p += NT) {
+        const int g = S.r_gid[p];
+        S.u.o.members[S.g_base[g] + S.r_arr[p]] = (int16_t)p;
+    }
+    for (int g = tid; g < n_groups; g += NT) {
+        const int ci = S.col[S.g_first[g]] - 1;
+        S.u.o.colgrp[S.ci_base[ci] + S.g_crank[g]] = (int16_t)g;
+    }
+    __syncthreads();
+
+    // ---- phase 6: order each group by input position ----------------------
+    for (int p = tid; p < n_small; p += NT) {
+        const int g = S.r_gid[p];
+        const int base = S.g_base[g], sz = S.g_cnt[g];
+        const int4 r = S.rec[p];
+        int rank = 0;
+        if (sz > 1) {
+            for (int k = 0; k < sz; ++k) rank += (S.rec[S.u.o.members[base + k]].y < r.y);
+        }
+        S.u.o.sval[base + rank] = __hiloint2double(r.w, r.z);
+    }
+
+    // ---- phase 7: tile prefix (look-back) ----------------------------------
+    if (tid < 32) {
+        unsigned long long excl = 0;
+        if (b > 0) {
+            const int lane = tid;
+            volatile unsigned long long *vst = tile_state;
+            long long base = b - 1;
+            while (true) {
+                const long long idx = base - lane;
+                const unsigned long long w = (idx >= 0) ? vst[idx] : lb_pack(2, 0);
+                const unsigned flag = (unsigned)(w >> 62);
+                if (__any_sync(FULL, flag == 0)) continue;
+                const unsigned pm = __ballot_sync(FULL, flag == 2);
+                const int stop = pm ? (__ffs(pm) - 1) : 31;
+                unsigned long long v = (lane <= stop) ? (w & LB_VALMASK) : 0ull;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+                excl += v;
+                if (pm) break;
+                base -= 32;
+            }
+            if (lane == 0) {
+                __threadfence();
+                vst[b] = lb_pack(2, excl + (unsigned long long)U);
+            }
+        }
+        if (tid == 0) S.P = (long long)excl;
+    }
+    __syncthreads();
+    const long long P = S.P;
+
+    // ---- phase 8: fold each group from +0.0 in input order, write ir/pr ---
+    bool over = false;
+    for (int g = tid; g < n_groups; g += NT) {
+        const int p0 = S.g_first[g];
+        const int row = S.rec[p0].x;
+        const int ci = S.col[p0] - 1;
+        const int cb = S.ci_base[ci], cu = S.ci_u[ci];
+        int rank = 0;
+        for (int k = 0; k < cu; ++k) rank += (S.rec[S.g_first[S.u.o.colgrp[cb + k]]].x < row);
+        const int base = S.g_base[g], sz = S.g_cnt[g];
+        double acc = 0.0;
+        for (int k = 0; k < sz; ++k) acc = fold_add(acc, S.u.o.sval[base + k]);
+        const long long o = P + cb + rank;
+        if (o < cap) {
+            ir[o] = row - 1;
+            pr[o] = acc;
+        } else {
+            over = true;
+        }
+    }
+    if (has_big) {
+        for (int ci = 0; ci < n_ci; ++ci) {
+            if (S.ci_q[ci] >= 0) continue;
+            const int c = S.ci_col[ci];
+            const uint32_t w = bigu[c];
+            const int ub = (int)(w & POSMASK);
+            const int st = S.ci_start[ci];
+            const int n = (int)((cur[c] & POSMASK) - (uint32_t)st);
+            const unsigned long long *R = reinterpret_cast<const unsigned long long *>(rec + st);
+            const unsigned long long *K = (w & BIGFLAG) ? R + n : R;
+            const unsigned long long *V = (w & BIGFLAG) ? R : R + n;
+            for (int k = tid; k < ub; k += NT) {
+                const long long o = P + S.ci_base[ci] + k;
+                if (o < cap) {
+                    ir[o] = (int32_t)K[k];
+                    pr[o] = __longlong_as_double((long long)V[k]);
+                } else {
+                    over = true;
+                }
+            }
+        }
+    }
+    if (over) atomicExch(&err->cap_exceeded, 1u);
+
+    // ---- phase 9: column pointers ------------------------------------------
+    int ne_run = 0;
+    for (int cb = c0; cb < c1; cb += NT) {
+        const int c = cb + tid;
+        const bool in = c < c1;
+        const int e = in ? (int)(cur[c] & POSMASK) : 0;
+        const int st = in ? (c > 0 ? (int)(cur[c - 1] & POSMASK) : 0) : 0;
+        const int ne = (in && e > st) ? 1 : 0;
+        int tot;
+        const int k = block_excl_sum<NT, int>(ne, S.warp_tmp, tot) + ne_run;
+        if (in) jc[c] = (int32_t)(P + S.ci_base[min(k, n_ci)]);
+        ne_run += tot;
+    }
+    if (b == ntiles - 1 && tid == 0) {
+        const long long nnz = P + U;
+        jc[N] = (int32_t)nnz;
+        err->nnz = nnz;
+        if (nnz > cap) atomicExch(&err->cap_exceeded, 1u);
+    }
+}
+
+cudaError_t launch_tile_fold(Launch &lc, const uint32_t *cur, const int32_t *tile_first,
+                             int64_t ntiles, const int4 *rec, const uint32_t *bigu,
+                             unsigned long long *tile_state, int32_t N, int32_t *jc, int32_t *ir,
+                             double *pr, int64_t cap, ErrState *err) {
+    if (ntiles <= 0) return cudaSuccess;
+    const size_t smem = sizeof(TileSmem);
+    cudaError_t e = cudaFuncSetAttribute(k_tile_fold, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+    k_tile_fold<<<(unsigned)ntiles, NT, smem, lc.stream>>>(cur, tile_first, ntiles, rec, bigu,
+                                                          tile_state, N, jc, ir, pr, cap, err);
+    lc.launches++;
+    return cudaGetLastError();
+}
+
+}  // namespace sa

@@ -1,0 +1,231 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's
+outputs (golden fixtures) and the CPU oracle.  Bar: jc/ir bit-exact and pr
+bit-exact (ordered-sum contract), NaN payloads included."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+import paper_1406_1066_b200 as sa  # noqa: E402
+from golden_io import error_cases, small_cases, sweep, workloads  # noqa: E402
+from instances import input_digest, output_digest, random_triplets  # noqa: E402
+from oracle import oracle as O  # noqa: E402
+
+CASES = small_cases()
+ERRS = error_cases()
+
+
+def _check(out, exp):
+    assert out.m == exp["m"] and out.n == exp["n"]
+    assert np.array_equal(out.jc, exp["jc"])
+    assert np.array_equal(out.ir, exp["ir"])
+    assert np.asarray(out.pr).tobytes() == exp["pr"].tobytes()
+
+
+def _same(a, b):
+    assert (a.m, a.n) == (b.m, b.n)
+    assert np.array_equal(np.asarray(a.jc), np.asarray(b.jc))
+    assert np.array_equal(np.asarray(a.ir), np.asarray(b.ir))
+    assert np.asarray(a.pr).tobytes() == np.asarray(b.pr).tobytes()
+
+
+def test_cuda_library_is_the_one_loaded():
+    from paper_1406_1066_b200 import _capi
+
+    lib = _capi.load(build_if_missing=False)
+    assert lib.sa_version() == 1
+    maps = open("/proc/self/maps").read()
+    assert _capi.library_path() in maps
+
+
+@pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
+def test_small_cases_host_api(case):
+    name, i, j, s, m, n, exp = case
+    ii = i.astype(np.int32) if i.dtype.kind == "i" else i
+    jj = j.astype(np.int32) if j.dtype.kind == "i" else j
+    _check(sa.assemble(ii, jj, s, m=m, n=n), exp)
+    # same through int64 / float64 index conversion on the device
+    _check(sa.assemble(i.astype(np.float64), j.astype(np.float64), s, m=m, n=n), exp)
+    _check(sa.assemble(i.astype(np.int64), j.astype(np.int64), s, m=m, n=n), exp)
+
+
+@pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
+def test_small_cases_device_api(case):
+    name, i, j, s, m, n, exp = case
+    dev = torch.device("cuda", 0)
+    ti = torch.from_numpy(i.astype(np.int32)).to(dev)
+    tj = torch.from_numpy(j.astype(np.int32)).to(dev)
+    ts = torch.from_numpy(s).to(dev)
+    out = sa.default_assembler(0).assemble_device(ti, tj, ts, m=m, n=n)
+    _check(out.to_host(), exp)
+
+
+@pytest.mark.parametrize("case", ERRS, ids=[e[0] for e in ERRS])
+def test_error_semantics(case):
+    name, i, j, s, m, n, exc, pos = case
+    expected = {"BadIndex": sa.BadIndex, "LengthMismatch": sa.LengthMismatch,
+                "DimensionTooSmall": sa.DimensionTooSmall}
+    if exc is None:
+        sa.assemble(i, j, s, m=m, n=n)
+        return
+    with pytest.raises(expected[exc]) as e:
+        sa.assemble(i, j, s, m=m, n=n)
+    if pos is not None:
+        assert e.value.position == pos
+    if exc == "BadIndex" and i.dtype.kind == "i" and j.dtype.kind == "i":
+        with pytest.raises(sa.BadIndex) as e2:  # the int32 fast path too
+            sa.assemble(i.astype(np.int32), j.astype(np.int32), s, m=m, n=n)
+        assert e2.value.position == pos
+
+
+@pytest.mark.parametrize("name", ["acceptance", "serial40"])
+def test_sweep_bit_exact_vs_reference(name):
+    """1000 acceptance-sweep instances (reference test_acceptance.py:50-71),
+    incl. empty, NaN, zeros, 1x1..7x7 matrices with ~50k-long duplicate runs."""
+    kw, rows = sweep(name)
+    bad = []
+    for r in rows:
+        ii, jj, sr = random_triplets(r["seed"], **kw)
+        out = sa.assemble(ii.astype(np.int32), jj.astype(np.int32), sr)
+        if (out.m, out.n, out.nnz) != (r["m"], r["n"], r["nnz"]) or \
+                output_digest(out.jc, out.ir, out.pr) != r["output"]:
+            bad.append(r["seed"])
+        if r["seed"] % 97 == 0:
+            assert sa.csc_validate(out) == []
+    assert bad == []
+
+
+def test_workload_digests_vs_reference():
+    from paper_1406_1066_b200 import workloads as W
+
+    for r in workloads():
+        w = getattr(W, r["kind"])(**r["kwargs"])
+        assert input_digest(w.ii.numpy(), w.jj.numpy(), w.s.numpy()) == r["input"]
+        dev = torch.device("cuda", 0)
+        out = sa.default_assembler(0).assemble_device(w.ii.to(dev), w.jj.to(dev), w.s.to(dev),
+                                                      m=w.m, n=w.n).to_host()
+        assert out.nnz == r["nnz"], r
+        assert output_digest(out.jc, out.ir, out.pr) == r["output"], r
+
+
+@pytest.mark.parametrize("k,scale", [(1, 1.0), (2, 1.0), (3, 1.0), (4, 0.1)])
+def test_baseline_configs_bit_exact_vs_c_oracle(k, scale):
+    """Full-size cfg1-cfg3 and 1/10-scale cfg4 against the C oracle."""
+    from paper_1406_1066_b200 import workloads as W
+
+    dev = torch.device("cuda", 0)
+    w = W.config(k, device=dev, scale=scale)
+    out = sa.default_assembler(0).assemble_device(w.ii, w.jj, w.s, m=w.m, n=w.n)
+    ref = O.assemble_counting(w.ii.cpu().numpy(), w.jj.cpu().numpy(), w.s.cpu().numpy(), w.m, w.n)
+    if w.expected_nnz is not None:
+        assert ref.nnz == w.expected_nnz
+    _same(out.to_host(), ref)
+
+
+def test_cfg5_properties_full_size():
+    """cfg5 (L = 1.152e9) is too big for the oracle in seconds: check
+    size-independent properties -- exact nnz, CSC invariants, zero column
+    sums (dyadic element matrices, exact in any order), and bit-exact spot
+    checks of sampled columns against the oracle on their triplets."""
+    from paper_1406_1066_b200 import workloads as W
+
+    dev = torch.device("cuda", 0)
+    N = 8000
+    w = W.fem2d(N, device=dev)
+    out = sa.default_assembler(0).assemble_device(w.ii, w.jj, w.s, m=w.m, n=w.n)
+    assert out.nnz == 7 * N * N + 6 * N + 1
+    jc = out.jc.to(torch.int64)
+    steps = jc[1:] - jc[:-1]
+    assert int(jc[0]) == 0 and int(jc[-1]) == out.nnz and bool((steps >= 1).all())
+    col = torch.repeat_interleave(torch.arange(w.n, device=dev), steps)
+    colsum = torch.zeros(w.n, dtype=torch.float64, device=dev).index_add_(0, col, out.pr)
+    assert bool((colsum == 0).all())
+    ir = out.ir.to(torch.int64)
+    same_col = col[1:] == col[:-1]
+    assert bool((ir[1:][same_col] > ir[:-1][same_col]).all())
+    cols = torch.tensor([1, 2, 8001, 32_000_000, w.n - 1, w.n], device=dev, dtype=torch.int32)
+    mask = torch.isin(w.jj, cols)
+    sub_i, sub_j, sub_s = w.ii[mask].cpu().numpy(), w.jj[mask].cpu().numpy(), w.s[mask].cpu().numpy()
+    ref = O.assemble_counting(sub_i, sub_j, sub_s, w.m, w.n)
+    for c in cols.tolist():
+        a0, a1 = int(out.jc[c - 1]), int(out.jc[c])
+        b0, b1 = int(ref.jc[c - 1]), int(ref.jc[c])
+        assert np.array_equal(out.ir[a0:a1].cpu().numpy(), ref.ir[b0:b1])
+        assert out.pr[a0:a1].cpu().numpy().tobytes() == ref.pr[b0:b1].tobytes()
+    del w, out
+
+
+def test_permuted_fem3d_values_follow_input_order():
+    """3D Kuhn values are not dyadic: a shuffled input changes some sums in
+    the last bit; the GPU must follow each input order exactly."""
+    from paper_1406_1066_b200 import workloads as W
+
+    w = W.fem3d(10)
+    perm = torch.from_numpy(np.random.default_rng(11).permutation(w.L))
+    ii, jj, s = w.ii[perm].numpy(), w.jj[perm].numpy(), w.s[perm].numpy()
+    out = sa.assemble(ii, jj, s, m=w.m, n=w.n)
+    _same(out, O.assemble_counting(ii, jj, s, w.m, w.n))
+    base = O.assemble_counting(w.ii.numpy(), w.jj.numpy(), w.s.numpy(), w.m, w.n)
+    assert (base.pr != out.pr).any()  # the test discriminates order
+
+
+def test_scalar_value_is_repeated_adds():
+    rng = np.random.default_rng(5)
+    ii = rng.integers(1, 6, size=5000).astype(np.int32)
+    jj = rng.integers(1, 4, size=5000).astype(np.int32)
+    out = sa.assemble(ii, jj, [0.1])
+    ref = O.assemble_counting(ii, jj, np.full(5000, 0.1), 5, 3)
+    _same(out, ref)
+
+
+def test_big_and_small_columns_mixed():
+    """A column longer than the tile cap next to ordinary columns, duplicates
+    inside the big column, and rows near the int32 limit."""
+    rng = np.random.default_rng(9)
+    L = 40_000
+    jj = rng.integers(1, 200, size=L).astype(np.int32)
+    jj[rng.random(L) < 0.4] = 77  # ~16k triplets in column 77
+    ii = rng.integers(1, 50, size=L).astype(np.int32)
+    ii[rng.random(L) < 0.1] = 2**31 - 1
+    s = rng.standard_normal(L)
+    s[rng.random(L) < 0.01] = np.nan
+    out = sa.assemble(ii, jj, s, m=2**31 - 1, n=200)
+    _same(out, O.assemble_counting(ii, jj, s, 2**31 - 1, 200))
+    assert sa.csc_validate(out) == []
+
+
+def test_many_empty_columns_and_sparse_tiles():
+    rng = np.random.default_rng(2)
+    L = 3000
+    ii = rng.integers(1, 10, size=L).astype(np.int32)
+    jj = rng.integers(1, 5_000_000, size=L).astype(np.int32)
+    s = rng.standard_normal(L)
+    out = sa.assemble(ii, jj, s, m=10, n=5_000_000)
+    _same(out, O.assemble_counting(ii, jj, s, 10, 5_000_000))
+
+
+def test_repeat_calls_reuse_workspace():
+    a = sa.default_assembler(0)
+    for seed in range(5):
+        ii, jj, sr = random_triplets(500 + seed, max_len=200_000, max_dim=5000)
+        ii, jj = ii.astype(np.int32), jj.astype(np.int32)
+        out = a.assemble(ii, jj, sr)
+        _same(out, O.assemble_counting(ii, jj, sr, int(ii.max(initial=0)), int(jj.max(initial=0))))
+    assert a.launch_count() >= 4
+
+
+def test_idempotent_reassembly():
+    ii, jj, sr = random_triplets(77, max_len=20_000, max_dim=300, allow_special=False)
+    first = sa.assemble(ii.astype(np.int32), jj.astype(np.int32), sr)
+    cols = np.repeat(np.arange(1, first.n + 1, dtype=np.int32), np.diff(first.jc))
+    again = sa.assemble(first.ir + 1, cols, first.pr, m=first.m, n=first.n)
+    _same(first, again)
+
+
+def test_prune_explicit_zeros_on_gpu_output():
+    out = sa.assemble(np.array([1, 1, 2], np.int32), np.array([1, 1, 1], np.int32), [2.0, -2.0, 5.0])
+    p = sa.prune_explicit_zeros(out)
+    assert p.nnz == 1 and p.jc.tolist() == [0, 1] and p.ir.tolist() == [1] and p.pr.tolist() == [5.0]

@@ -1,0 +1,137 @@
+"""CPU-only checks of the host side: argument normalisation, types, error
+classes, the C-ABI library (loads, exports every declared symbol), and the
+workload generators."""
+
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_1406_1066_b200 as sa
+from paper_1406_1066_b200 import _capi, workloads as W
+from paper_1406_1066_b200.types import normalize_raw
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _header_functions():
+    text = open(os.path.join(ROOT, "include", "sparse_assembly.h")).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(sa_[a-z_]+)\s*\(", text)))
+
+
+def test_library_builds_loads_and_exports_every_declared_symbol():
+    lib = _capi.load()  # builds with nvcc if missing; loads without a GPU
+    declared = _header_functions()
+    assert len(declared) >= 14
+    assert set(declared) == set(_capi.SIGNATURES)
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert lib.sa_version() == 1
+
+
+def test_library_is_sm100a():
+    import subprocess
+
+    out = subprocess.run(["cuobjdump", "--list-elf", _capi.library_path()],
+                         capture_output=True, text=True)
+    if out.returncode != 0:
+        pytest.skip("cuobjdump unavailable")
+    assert "sm_100a" in out.stdout
+
+
+def test_normalize_lengths_and_scalar_mode():
+    i, j, s, mode = normalize_raw([1, 2, 3], [1, 1, 1], [7.5])
+    assert mode == "scalar" and s.dtype == np.float64 and len(s) == 1
+    _, _, _, mode = normalize_raw([1], [1], [7.5])
+    assert mode == "vector"
+    with pytest.raises(sa.LengthMismatch):
+        normalize_raw([1, 2], [1], [1.0, 1.0])
+    with pytest.raises(sa.LengthMismatch):
+        normalize_raw([1, 2], [1, 1], [1.0, 2.0, 3.0])
+    i, j, s, mode = normalize_raw(3, 4, 5)  # scalars become length-1 arrays
+    assert len(i) == len(j) == len(s) == 1
+
+
+def test_request_from_raw():
+    req = sa.AssemblyRequest.from_raw([1, 2], [1, 1], [3.0])
+    assert req.value_mode == "scalar" and req.dims is None
+    req = sa.AssemblyRequest.from_raw([1, 2], [1, 1], [3.0, 4.0], m=5, n=2, nzmax=9)
+    assert req.value_mode == "vector" and req.dims == sa.Dimensions(5, 2)
+    assert req.capacity_hint == 9
+    with pytest.raises(sa.LengthMismatch):
+        sa.AssemblyRequest.from_raw([1], [1], [1.0], m=3)
+    with pytest.raises(ValueError):
+        sa.Dimensions(-1, 2)
+
+
+def test_errors_mirror_reference_fields():
+    e = sa.BadIndex(3, 0.5)
+    assert isinstance(e, ValueError) and e.position == 3 and e.value == 0.5
+    assert issubclass(sa.LengthMismatch, ValueError)
+    assert issubclass(sa.DimensionTooSmall, ValueError)
+
+
+def _mat(jc, ir, pr, m, n):
+    return sa.CscMatrix(np.asarray(jc, np.int32), np.asarray(ir, np.int32),
+                        np.asarray(pr, np.float64), m, n)
+
+
+def test_csc_validate():
+    assert sa.csc_validate(_mat([0, 3, 5, 7, 10], [0, 1, 3, 1, 2, 2, 3, 0, 2, 3],
+                                [10, 3, 3, 9, 7, 8, 8, -2, 7, 5], 4, 4)) == []
+    assert sa.csc_validate(_mat([0, 0, 0], [], [], 3, 2)) == []
+    assert any("non-decreasing jc" in v for v in sa.csc_validate(_mat([0, 2, 1], [0, 1], [1, 1], 2, 2)))
+    assert any("jc[0]" in v for v in sa.csc_validate(_mat([1, 2], [0, 1], [1, 1], 2, 1)))
+    assert any("jc[n]" in v for v in sa.csc_validate(_mat([0, 1], [0, 1], [1, 1], 2, 1)))
+    assert any("strictly increasing" in v for v in sa.csc_validate(_mat([0, 2], [1, 1], [1, 1], 2, 1)))
+    assert any("strictly increasing" in v for v in sa.csc_validate(_mat([0, 2], [1, 0], [1, 1], 2, 1)))
+    assert sa.csc_validate(_mat([0, 1, 2], [1, 1], [1, 1], 2, 2)) == []
+    assert any("outside" in v for v in sa.csc_validate(_mat([0, 1], [5], [1], 3, 1)))
+    assert any("jc length" in v for v in sa.csc_validate(_mat([0, 1], [0], [1], 2, 2)))
+
+
+def test_prune_explicit_zeros():
+    m = _mat([0, 2], [0, 1], [1.0, 2.0], 2, 1)
+    p = sa.prune_explicit_zeros(m)
+    assert p.same_as(m) and p.pr is not m.pr
+    p = sa.prune_explicit_zeros(_mat([0, 2, 3], [0, 1, 1], [0.0, 5.0, -0.0], 2, 2))
+    assert p.jc.tolist() == [0, 1, 1] and p.ir.tolist() == [1] and p.pr.tolist() == [5.0]
+    p = sa.prune_explicit_zeros(_mat([0, 1, 2], [0, 0], [np.nan, 0.0], 1, 2))
+    assert p.nnz == 1 and np.isnan(p.pr[0]) and p.jc.tolist() == [0, 1, 1]
+
+
+def test_same_as_is_bitwise():
+    a = _mat([0, 1], [0], [np.nan], 1, 1)
+    b = _mat([0, 1], [0], [np.nan], 1, 1)
+    assert a.same_as(b)
+    c = _mat([0, 1], [0], [-0.0], 1, 1)
+    d = _mat([0, 1], [0], [0.0], 1, 1)
+    assert not c.same_as(d)
+
+
+def test_workload_shapes():
+    w = W.fem2d(5)
+    assert w.L == 18 * 25 and w.m == w.n == 36 and w.expected_nnz == 7 * 25 + 31
+    assert int(w.ii.min()) == 1 and int(w.ii.max()) == 36
+    w = W.fem3d(2)
+    assert w.L == 96 * 8 and w.m == 27
+    # a chunk of cells is the matching slice of the whole
+    full = W.fem2d(6)
+    part = W.fem2d(6, cell_range=(10, 20))
+    assert np.array_equal(part.ii.numpy(), full.ii.numpy()[10 * 18:20 * 18])
+    assert np.array_equal(part.s.numpy(), full.s.numpy()[10 * 18:20 * 18])
+    w = W.random_coo(L=1000, seed=3)
+    assert w.L == 1000 and int(w.ii.max()) <= 1000 and float(w.s.abs().max()) <= 1.0
+    w = W.heavy_dup(m=1000, positions=2000, seed=1)
+    assert 5000 < w.L < 15000
+
+
+def test_product_package_never_imports_the_oracle():
+    pkg = os.path.join(ROOT, "paper_1406_1066_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h")):
+                text = open(os.path.join(dirpath, f)).read()
+                assert "oracle" not in re.sub(r"#.*|//.*", "", text).replace("oracle/", ""), f
