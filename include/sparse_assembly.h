@@ -68,7 +68,8 @@ int sa_version(void);
 int sa_create(int device, sa_ctx **out);
 /* Destroy a context and free its device / pinned workspace. */
 void sa_destroy(sa_ctx *ctx);
-/* Run subsequent work on `stream` (a cudaStream_t; NULL = the context's own). */
+/* Run subsequent work on `stream` (a cudaStream_t; 0/NULL = the legacy
+ * default stream).  A new context starts on its own non-blocking stream. */
 int sa_set_stream(sa_ctx *ctx, void *stream);
 /* Message describing the last failure on this context ("" if none). */
 const char *sa_last_error(const sa_ctx *ctx);

@@ -230,7 +230,7 @@ void sa_destroy(sa_ctx *ctx) {
 
 int sa_set_stream(sa_ctx *ctx, void *stream) {
     if (!ctx) return SA_ERR_INVALID_ARG;
-    ctx->stream = stream ? reinterpret_cast<cudaStream_t>(stream) : ctx->own_stream;
+    ctx->stream = reinterpret_cast<cudaStream_t>(stream);  // 0 = the legacy default stream
     return SA_OK;
 }
 

@@ -667,31 +667,11 @@ __global__ void __launch_bounds__(NT, 2) k_tile_fold(const uint32_t *__restrict_
         else vst[b] = lb_pack(1, (unsigned long long)U);
     }
 
-    // ---- phase 5: scatter members by group, groups by column --------------
-    for (int p = tid; p < n_small; p += NT) {
-        const int g = S.r_gid[p];
-        S.u.o.members[S.g_base[g] + S.r_arr[p]] = (int16_t)p;
-    }
-    for (int g = tid; g < n_groups; g += NT) {
-        const int ci = S.col[S.g_first[g]] - 1;
-        S.u.o.colgrp[S.ci_base[ci] + S.g_crank[g]] = (int16_t)g;
-    }
-    __syncthreads();
-
-    // ---- phase 6: order each group by input position ----------------------
-    for (int p = tid; p < n_small; p += NT) {
-        const int g = S.r_gid[p];
-        const int base = S.g_base[g], sz = S.g_cnt[g];
-        const int4 r = S.rec[p];
-        int rank = 0;
-        if (sz > 1) {
-            for (int k = 0; k < sz; ++k) rank += (S.rec[S.u.o.members[base + k]].y < r.y);
-        }
-        S.u.o.sval[base + rank] = __hiloint2double(r.w, r.z);
-    }
-
-    // ---- phase 7: tile prefix (look-back) ----------------------------------
-    if (tid < 32) {
+    // ---- phases 5-7: warp 0 resolves the tile prefix (decoupled look-back)
+    // while warps 1.. scatter members by group / groups by column (phase 5)
+    // and order each group by input position (phase 6).
+    const int warp = tid >> 5;
+    if (warp == 0) {
         unsigned long long excl = 0;
         if (b > 0) {
             const int lane = tid;
@@ -717,6 +697,28 @@ __global__ void __launch_bounds__(NT, 2) k_tile_fold(const uint32_t *__restrict_
             }
         }
         if (tid == 0) S.P = (long long)excl;
+    } else {
+        const int wt = tid - 32;
+        constexpr int WN = NT - 32;
+        for (int p = wt; p < n_small; p += WN) {
+            const int g = S.r_gid[p];
+            S.u.o.members[S.g_base[g] + S.r_arr[p]] = (int16_t)p;
+        }
+        for (int g = wt; g < n_groups; g += WN) {
+            const int ci = S.col[S.g_first[g]] - 1;
+            S.u.o.colgrp[S.ci_base[ci] + S.g_crank[g]] = (int16_t)g;
+        }
+        asm volatile("bar.sync 1, %0;" ::"r"(WN) : "memory");
+        for (int p = wt; p < n_small; p += WN) {
+            const int g = S.r_gid[p];
+            const int base = S.g_base[g], sz = S.g_cnt[g];
+            const int4 r = S.rec[p];
+            int rank = 0;
+            if (sz > 1) {
+                for (int k = 0; k < sz; ++k) rank += (S.rec[S.u.o.members[base + k]].y < r.y);
+            }
+            S.u.o.sval[base + rank] = __hiloint2double(r.w, r.z);
+        }
     }
     __syncthreads();
     const long long P = S.P;
