@@ -500,307 +500,4 @@ cudaError_t launch_bigcol(Launch &lc, const uint32_t *cur, const uint32_t *big_l
     return cudaGetLastError();
 }
 
-// ---------------------------------------------------------------------------
-// k_tile_fold: one CTA per column tile (ticket order), shared-memory only.
-// ---------------------------------------------------------------------------
-constexpr int HS = 2 * TCAP;  // hash slots (load factor <= 0.5)
-constexpr int CCAP = TILE;    // non-empty columns per tile (distinct starts in a TILE window)
-constexpr int NT = TILE_THREADS;
-constexpr int IPT = TCAP / NT;
-
-struct TileSmem {
-    int4 rec[TCAP];           // {row, input position, value lo, value hi}
-    int col[TCAP];            // head marks -> column-local index + 1
-    union {
-        struct {
-            unsigned long long key[HS];
-            int16_t gid[HS];
-        } h;
-        struct {
-            double sval[TCAP];     // group values in input order
-            int16_t members[TCAP]; // record ids grouped by (column,row)
-            int16_t colgrp[TCAP];  // group ids grouped by column
-        } o;
-    } u;
-    int g_cnt[TCAP];
-    int g_base[TCAP];
-    int16_t g_first[TCAP];
-    int16_t g_crank[TCAP];
-    int16_t r_gid[TCAP];
-    int16_t r_arr[TCAP];
-    int ci_col[CCAP];
-    int ci_start[CCAP];
-    int ci_q[CCAP];
-    int ci_cnt[CCAP];
-    int ci_u[CCAP];
-    int ci_base[CCAP + 1];
-    int warp_tmp[NT / 32];
-    int n_small, n_ci, n_groups, has_big, overflow;
-    long long tile;
-    long long P;
-};
-
-__device__ __forceinline__ unsigned hash_slot(unsigned long long key) {
-    return (unsigned)((key * 0x9E3779B97F4A7C15ull) >> 40) & (HS - 1);
-}
-
-__global__ void __launch_bounds__(NT, 2) k_tile_fold(const uint32_t *__restrict__ cur,
-                                                      const int32_t *__restrict__ tile_first,
-                                                      int64_t ntiles, const int4 *__restrict__ rec,
-                                                      const uint32_t *__restrict__ bigu,
-                                                      unsigned long long *tile_state, int32_t N,
-                                                      int32_t *__restrict__ jc,
-                                                      int32_t *__restrict__ ir,
-                                                      double *__restrict__ pr, int64_t cap,
-                                                      ErrState *err) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    TileSmem &S = *reinterpret_cast<TileSmem *>(smem_raw);
-    const int tid = threadIdx.x;
-
-    if (tid == 0) {
-        S.tile = atomicAdd(&err->tile_ticket, 1u);
-        S.n_groups = 0;
-        S.overflow = 0;
-    }
-    for (int k = tid; k < TCAP; k += NT) {
-        S.col[k] = 0;
-        S.g_cnt[k] = 0;
-    }
-    for (int k = tid; k < HS; k += NT) S.u.h.key[k] = 0ull;
-    __syncthreads();
-    const long long b = S.tile;
-    const int c0 = tile_first[b], c1 = tile_first[b + 1];
-
-    // ---- phase 1: columns of the tile -----------------------------------
-    int n_ci = 0, n_small = 0, has_big = 0;
-    for (int cb = c0; cb < c1; cb += NT) {
-        const int c = cb + tid;
-        const bool in = c < c1;
-        const uint32_t ew = in ? cur[c] : 0u;
-        const int e = (int)(ew & POSMASK);
-        const int big = (int)(ew >> 31);
-        const int st = in ? (c > 0 ? (int)(cur[c - 1] & POSMASK) : 0) : 0;
-        const int cnt = in ? e - st : 0;
-        const int ne = cnt > 0 ? 1 : 0;
-        const int sc = (ne && !big) ? cnt : 0;
-        int tot_ne, tot_sc;
-        const int ci = block_excl_sum<NT, int>(ne, S.warp_tmp, tot_ne) + n_ci;
-        const int q = block_excl_sum<NT, int>(sc, S.warp_tmp, tot_sc) + n_small;
-        const int anybig = __syncthreads_or(ne && big);
-        if (ne) {
-            if (ci < CCAP && q + sc <= TCAP) {
-                S.ci_col[ci] = c;
-                S.ci_start[ci] = st;
-                S.ci_q[ci] = big ? -1 : q;
-                S.ci_cnt[ci] = big ? 0 : cnt;
-                S.ci_u[ci] = big ? (int)(bigu[c] & POSMASK) : 0;
-                if (!big) S.col[q] = ci + 1;
-            } else {
-                S.overflow = 1;
-            }
-        }
-        n_ci += tot_ne;
-        n_small += tot_sc;
-        has_big |= anybig;
-    }
-    __syncthreads();
-    if (S.overflow) {
-        if (tid == 0) atomicExch(&err->internal, 1u);
-        n_ci = 0;
-        n_small = 0;
-    }
-
-    // ---- phase 2: stage the records ---------------------------------------
-    if (!has_big) {
-        const int r0 = n_ci ? S.ci_start[0] : 0;
-        for (int p = tid; p < n_small; p += NT) S.rec[p] = rec[r0 + p];
-    } else {
-        for (int ci = 0; ci < n_ci; ++ci) {
-            const int q = S.ci_q[ci];
-            if (q < 0) continue;
-            const int st = S.ci_start[ci], cnt = S.ci_cnt[ci];
-            for (int p = tid; p < cnt; p += NT) S.rec[q + p] = rec[st + p];
-        }
-    }
-    smem_incl_max<NT, IPT>(S.col, n_small, S.warp_tmp);  // ends with a barrier
-
-    // ---- phase 3: (column,row) groups via a shared-memory hash ------------
-    for (int p = tid; p < n_small; p += NT) {
-        const int row = S.rec[p].x;
-        const int ci = S.col[p] - 1;
-        const unsigned long long key = ((unsigned long long)(unsigned)ci << 32) | (unsigned)row;
-        unsigned h = hash_slot(key);
-        while (true) {
-            const unsigned long long old = atomicCAS(&S.u.h.key[h], 0ull, key);
-            if (old == 0ull) {
-                const int g = atomicAdd(&S.n_groups, 1);
-                S.u.h.gid[h] = (int16_t)g;
-                S.g_first[g] = (int16_t)p;
-                S.g_crank[g] = (int16_t)atomicAdd(&S.ci_u[ci], 1);
-                break;
-            }
-            if (old == key) break;
-            h = (h + 1) & (HS - 1);
-        }
-        S.r_gid[p] = (int16_t)h;
-    }
-    __syncthreads();
-    for (int p = tid; p < n_small; p += NT) {
-        const int g = S.u.h.gid[S.r_gid[p]];
-        S.r_gid[p] = (int16_t)g;
-        S.r_arr[p] = (int16_t)atomicAdd(&S.g_cnt[g], 1);
-    }
-    __syncthreads();
-    const int n_groups = S.n_groups;
-
-    // ---- phase 4: group offsets, column offsets, publish the aggregate ----
-    for (int g = tid; g < n_groups; g += NT) S.g_base[g] = S.g_cnt[g];
-    for (int k = tid; k < n_ci; k += NT) S.ci_base[k] = S.ci_u[k];
-    __syncthreads();
-    smem_excl_scan<NT, IPT, int>(S.g_base, n_groups, S.warp_tmp);
-    const int U = smem_excl_scan<NT, (CCAP + NT - 1) / NT, int>(S.ci_base, n_ci, S.warp_tmp);
-    if (tid == 0) {
-        S.ci_base[n_ci] = U;
-        volatile unsigned long long *vst = tile_state;
-        __threadfence();
-        if (b == 0) vst[0] = lb_pack(2, (unsigned long long)U);
-        else vst[b] = lb_pack(1, (unsigned long long)U);
-    }
-
-    // ---- phases 5-7: warp 0 resolves the tile prefix (decoupled look-back)
-    // while warps 1.. scatter members by group / groups by column (phase 5)
-    // and order each group by input position (phase 6).
-    const int warp = tid >> 5;
-    if (warp == 0) {
-        unsigned long long excl = 0;
-        if (b > 0) {
-            const int lane = tid;
-            volatile unsigned long long *vst = tile_state;
-            long long base = b - 1;
-            while (true) {
-                const long long idx = base - lane;
-                const unsigned long long w = (idx >= 0) ? vst[idx] : lb_pack(2, 0);
-                const unsigned flag = (unsigned)(w >> 62);
-                if (__any_sync(FULL, flag == 0)) continue;
-                const unsigned pm = __ballot_sync(FULL, flag == 2);
-                const int stop = pm ? (__ffs(pm) - 1) : 31;
-                unsigned long long v = (lane <= stop) ? (w & LB_VALMASK) : 0ull;
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
-                excl += v;
-                if (pm) break;
-                base -= 32;
-            }
-            if (lane == 0) {
-                __threadfence();
-                vst[b] = lb_pack(2, excl + (unsigned long long)U);
-            }
-        }
-        if (tid == 0) S.P = (long long)excl;
-    } else {
-        const int wt = tid - 32;
-        constexpr int WN = NT - 32;
-        for (int p = wt; p < n_small; p += WN) {
-            const int g = S.r_gid[p];
-            S.u.o.members[S.g_base[g] + S.r_arr[p]] = (int16_t)p;
-        }
-        for (int g = wt; g < n_groups; g += WN) {
-            const int ci = S.col[S.g_first[g]] - 1;
-            S.u.o.colgrp[S.ci_base[ci] + S.g_crank[g]] = (int16_t)g;
-        }
-        asm volatile("bar.sync 1, %0;" ::"r"(WN) : "memory");
-        for (int p = wt; p < n_small; p += WN) {
-            const int g = S.r_gid[p];
-            const int base = S.g_base[g], sz = S.g_cnt[g];
-            const int4 r = S.rec[p];
-            int rank = 0;
-            if (sz > 1) {
-                for (int k = 0; k < sz; ++k) rank += (S.rec[S.u.o.members[base + k]].y < r.y);
-            }
-            S.u.o.sval[base + rank] = __hiloint2double(r.w, r.z);
-        }
-    }
-    __syncthreads();
-    const long long P = S.P;
-
-    // ---- phase 8: fold each group from +0.0 in input order, write ir/pr ---
-    bool over = false;
-    for (int g = tid; g < n_groups; g += NT) {
-        const int p0 = S.g_first[g];
-        const int row = S.rec[p0].x;
-        const int ci = S.col[p0] - 1;
-        const int cb = S.ci_base[ci], cu = S.ci_u[ci];
-        int rank = 0;
-        for (int k = 0; k < cu; ++k) rank += (S.rec[S.g_first[S.u.o.colgrp[cb + k]]].x < row);
-        const int base = S.g_base[g], sz = S.g_cnt[g];
-        double acc = 0.0;
-        for (int k = 0; k < sz; ++k) acc = fold_add(acc, S.u.o.sval[base + k]);
-        const long long o = P + cb + rank;
-        if (o < cap) {
-            ir[o] = row - 1;
-            pr[o] = acc;
-        } else {
-            over = true;
-        }
-    }
-    if (has_big) {
-        for (int ci = 0; ci < n_ci; ++ci) {
-            if (S.ci_q[ci] >= 0) continue;
-            const int c = S.ci_col[ci];
-            const uint32_t w = bigu[c];
-            const int ub = (int)(w & POSMASK);
-            const int st = S.ci_start[ci];
-            const int n = (int)((cur[c] & POSMASK) - (uint32_t)st);
-            const unsigned long long *R = reinterpret_cast<const unsigned long long *>(rec + st);
-            const unsigned long long *K = (w & BIGFLAG) ? R + n : R;
-            const unsigned long long *V = (w & BIGFLAG) ? R : R + n;
-            for (int k = tid; k < ub; k += NT) {
-                const long long o = P + S.ci_base[ci] + k;
-                if (o < cap) {
-                    ir[o] = (int32_t)K[k];
-                    pr[o] = __longlong_as_double((long long)V[k]);
-                } else {
-                    over = true;
-                }
-            }
-        }
-    }
-    if (over) atomicExch(&err->cap_exceeded, 1u);
-
-    // ---- phase 9: column pointers ------------------------------------------
-    int ne_run = 0;
-    for (int cb = c0; cb < c1; cb += NT) {
-        const int c = cb + tid;
-        const bool in = c < c1;
-        const int e = in ? (int)(cur[c] & POSMASK) : 0;
-        const int st = in ? (c > 0 ? (int)(cur[c - 1] & POSMASK) : 0) : 0;
-        const int ne = (in && e > st) ? 1 : 0;
-        int tot;
-        const int k = block_excl_sum<NT, int>(ne, S.warp_tmp, tot) + ne_run;
-        if (in) jc[c] = (int32_t)(P + S.ci_base[min(k, n_ci)]);
-        ne_run += tot;
-    }
-    if (b == ntiles - 1 && tid == 0) {
-        const long long nnz = P + U;
-        jc[N] = (int32_t)nnz;
-        err->nnz = nnz;
-        if (nnz > cap) atomicExch(&err->cap_exceeded, 1u);
-    }
-}
-
-cudaError_t launch_tile_fold(Launch &lc, const uint32_t *cur, const int32_t *tile_first,
-                             int64_t ntiles, const int4 *rec, const uint32_t *bigu,
-                             unsigned long long *tile_state, int32_t N, int32_t *jc, int32_t *ir,
-                             double *pr, int64_t cap, ErrState *err) {
-    if (ntiles <= 0) return cudaSuccess;
-    const size_t smem = sizeof(TileSmem);
-    cudaError_t e = cudaFuncSetAttribute(k_tile_fold, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
-    if (e != cudaSuccess) return e;
-    k_tile_fold<<<(unsigned)ntiles, NT, smem, lc.stream>>>(cur, tile_first, ntiles, rec, bigu,
-                                                          tile_state, N, jc, ir, pr, cap, err);
-    lc.launches++;
-    return cudaGetLastError();
-}
-
 }  // namespace sa

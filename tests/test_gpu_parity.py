@@ -209,12 +209,13 @@ def test_many_empty_columns_and_sparse_tiles():
 
 def test_repeat_calls_reuse_workspace():
     a = sa.default_assembler(0)
-    for seed in range(5):
+    for seed in range(8):
         ii, jj, sr = random_triplets(500 + seed, max_len=200_000, max_dim=5000)
         ii, jj = ii.astype(np.int32), jj.astype(np.int32)
         out = a.assemble(ii, jj, sr)
         _same(out, O.assemble_counting(ii, jj, sr, int(ii.max(initial=0)), int(jj.max(initial=0))))
-    assert a.launch_count() >= 4
+        if len(ii) > 1000:
+            assert a.launch_count() >= 5  # init, hist, scan, scatter, (bigcol), fold
 
 
 def test_idempotent_reassembly():
