@@ -1,23 +1,29 @@
 // sa_tile.cu -- k_tile_fold: the ordered segmented fold (sm_100a).
 //
-// Input: 16-byte records {row, input position, value} already grouped by
-// column (k_scatter), column cursors cur[] (end of column c, k_col_scan +
-// k_scatter), tile_first[] (first column of each TILE-wide window of record
-// positions).  Output: jc, ir, pr.
+// Input: 16-byte records {row, input position, value} grouped by column
+// (k_scatter), column cursors cur[] (cur[c] = end of column c), tile_first[]
+// (first column whose records start in each TILE-wide window).  Output: jc,
+// ir, pr.
 //
-// Persistent CTAs take tiles in ticket order.  Per tile, entirely in shared
-// memory:
-//   1. column pass: the tile's columns, their record ranges, big columns
-//   2. records arrive by TMA bulk copy (cp.async.bulk, issued one tile ahead)
-//   3. (column,row) groups through a shared-memory hash table
-//   4. each group ordered by input position; fold from +0.0 in that order
-//      (the reference's scatter contract, _kernels.pyx:82-89), x86 NaN rule
-//   5. groups ordered by row inside each column -> staged (row, value) in
-//      final CSC order, tile unique count U published (decoupled look-back)
-//   6. one tile LATER (so the look-back has resolved meanwhile): block-wide
-//      look-back for the tile prefix P, coalesced writes of ir/pr/jc.
-// Tiles holding a column longer than BIGCOL use the synchronous path (the
-// column itself was folded by k_bigcol).
+// Persistent CTAs take tiles in ticket order.  Per tile:
+//   block  column pass: the tile's non-empty columns and record ranges
+//   TMA    records arrive by cp.async.bulk, issued one tile ahead
+//   warps  each warp owns the columns starting in its TILE/8 window and, with
+//          warp-synchronous code only (no block barriers):
+//            (a) column id of each record
+//            (b) (column,row) groups: warp-private shared-memory hash,
+//                group ids by ballot
+//            (c) group sizes / arrival ranks, (d) warp scans of group and
+//                column offsets, (e) member lists, (f) members ordered by
+//                input position
+//   block  tile unique count U -> decoupled look-back aggregate; the
+//          PREVIOUS tile (whose look-back had a whole tile of time to
+//          resolve) is finished: block-wide look-back, coalesced ir/pr/jc
+//   warps  (g) fold each group from +0.0 in input order (the reference's
+//          scatter contract, _kernels.pyx:82-89; x86 NaN rule), order groups
+//          by row inside each column, stage (row, value) in CSC order.
+// Tiles with a column longer than BIGCOL (folded by k_bigcol) take a
+// synchronous path that writes straight to global memory.
 
 #include "sa_internal.cuh"
 
@@ -25,52 +31,51 @@ namespace sa {
 
 namespace {
 
-constexpr int HS = 2 * TCAP;   // hash slots (load factor <= 0.5)
-constexpr int CCAP = TILE;     // non-empty columns per tile (distinct starts in a TILE window)
 constexpr int NT = TILE_THREADS;
-constexpr int IPT = TCAP / NT;
-
-struct OutStage {
-    int row[TCAP];           // ir values (row - 1), tile-local CSC order
-    double val[TCAP];        // pr values
-    int ci_base[CCAP + 1];   // tile-local output offset of each non-empty column
-    int c0, c1, n_ci, U;
-    long long tile;
-};
+constexpr int NW = NT / 32;
+constexpr int WIN = TILE / NW;  // record-position window per warp
+constexpr int HSZ = 2 * TCAP;   // hash slots: 2 per record position
+constexpr int CCAP = TILE;      // non-empty columns per tile (distinct starts in a TILE window)
 
 struct TileSmem {
     int4 rec[2][TCAP];                 // double-buffered records (TMA destination)
     unsigned long long mbar[2];
-    int col[TCAP];                     // head marks -> column-local index + 1
-    union {
+    int col[TCAP];                     // column heads -> column-local index + 1
+    // One 16-byte cell per record position k: first the two hash slots 2k,
+    // 2k+1 of the owning warp's private table, then (hash dead) per-index
+    // fields.  Warps only touch cells of their own record range.
+    union HCell {
+        unsigned long long key[2];
         struct {
-            unsigned long long key[HS];
-            int16_t gid[HS];
-        } h;
-        struct {
-            double sval[TCAP];         // group values in input order
-            int16_t members[TCAP];     // record ids grouped by (column,row)
-            int16_t colgrp[TCAP];      // group ids grouped by column
+            double sval;               // group values ordered by input position
+            int g_base;                // group offset (index qa + gid)
+            int16_t mem;               // member lists (record ids), per group
+            int16_t cgrp;              // group ids listed per column
         } o;
-    } u;
-    int g_cnt[TCAP];
-    int g_base[TCAP];
+    } hc[TCAP];
+    int16_t hgid[HSZ];
+    int g_cnt[TCAP];                   // per group (indexed qa + gid)
+    int cg_base[CCAP];                 // warp-relative offset of a column in cgrp
     int16_t g_first[TCAP];
     int16_t g_crank[TCAP];
-    int16_t r_gid[TCAP];
+    int16_t r_gid[TCAP];               // per record
     int16_t r_arr[TCAP];
     int ci_col[CCAP];
     int ci_start[CCAP];
     int ci_q[CCAP];
-    int ci_cnt[CCAP];
-    int ci_u[CCAP];
-    OutStage out[2];
-    int warp_tmp[NT / 32];
-    long long red_ll[NT / 32];
-    int n_groups, overflow;
+    int ci_cnt[CCAP];                  // 0 for big columns
+    int ci_u[CCAP];                    // groups per column (or k_bigcol's count)
+    int ci_base[2][CCAP + 1];          // tile-local output offsets (current / pending)
+    int st_row[TCAP];                  // staged outputs of the pending tile
+    double st_val[TCAP];
+    int w_u[NW], w_base[NW];
+    int warp_tmp[NW];
+    long long red_ll[NW];
+    int pre_n[2];
     long long next_tile;
-    int pre_r0[2], pre_n[2];           // prefetched record range per buffer
-    long long P;
+    // pending tile metadata
+    long long p_tile;
+    int p_c0, p_c1, p_nci, p_U;
 };
 
 __device__ __forceinline__ unsigned smem_u32(const void *p) {
@@ -106,17 +111,47 @@ __device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned pari
     }
 }
 
-__device__ __forceinline__ unsigned hash_slot(unsigned long long key) {
-    return (unsigned)((key * 0x9E3779B97F4A7C15ull) >> 40) & (HS - 1);
-}
-
 __device__ __forceinline__ int col_start(const uint32_t *cur, int c) {
     return c > 0 ? (int)(cur[c - 1] & POSMASK) : 0;
 }
 
-// Block-wide decoupled look-back: exclusive prefix of tile b (all tiles < b),
-// then publish b's inclusive prefix.  NT predecessors are inspected per L2
-// round trip.  Must be called by all threads.
+// warp-level inclusive sum / max
+__device__ __forceinline__ int warp_incl_sum(int x) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(FULL, x, o);
+        if (lane >= o) x += y;
+    }
+    return x;
+}
+
+__device__ __forceinline__ int warp_incl_max(int x) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(FULL, x, o);
+        if (lane >= o) x = max(x, y);
+    }
+    return x;
+}
+
+// In-place warp exclusive scan over a[lo, hi) (lanes stride 32); returns total.
+__device__ __forceinline__ int warp_excl_scan(int *a, int lo, int hi) {
+    const int lane = threadIdx.x & 31;
+    int carry = 0;
+    for (int p0 = lo; p0 < hi; p0 += 32) {
+        const int p = p0 + lane;
+        const int v = (p < hi) ? a[p] : 0;
+        const int inc = warp_incl_sum(v);
+        if (p < hi) a[p] = carry + inc - v;
+        carry += __shfl_sync(FULL, inc, 31);
+    }
+    return carry;
+}
+
+// Block-wide decoupled look-back: exclusive prefix of tile b, then publish
+// b's inclusive prefix.  NT predecessors per L2 round trip.  All threads.
 __device__ long long lookback_block(unsigned long long *st, long long b, unsigned long long agg,
                                    TileSmem &S) {
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
@@ -128,7 +163,6 @@ __device__ long long lookback_block(unsigned long long *st, long long b, unsigne
         const unsigned long long word = (idx >= 0) ? vst[idx] : lb_pack(2, 0);
         const unsigned flag = (unsigned)(word >> 62);
         if (__syncthreads_or(flag == 0)) continue;
-        // nearest inclusive prefix = smallest tid with flag 2
         int stop = (flag == 2) ? tid : NT;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) stop = min(stop, __shfl_xor_sync(FULL, stop, o));
@@ -136,7 +170,7 @@ __device__ long long lookback_block(unsigned long long *st, long long b, unsigne
         __syncthreads();
         stop = NT;
 #pragma unroll
-        for (int k = 0; k < NT / 32; ++k) stop = min(stop, S.warp_tmp[k]);
+        for (int k = 0; k < NW; ++k) stop = min(stop, S.warp_tmp[k]);
         long long v = (tid <= stop) ? (long long)(word & LB_VALMASK) : 0;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
@@ -144,7 +178,7 @@ __device__ long long lookback_block(unsigned long long *st, long long b, unsigne
         __syncthreads();
         long long sum = 0;
 #pragma unroll
-        for (int k = 0; k < NT / 32; ++k) sum += S.red_ll[k];
+        for (int k = 0; k < NW; ++k) sum += S.red_ll[k];
         excl += sum;
         __syncthreads();
         if (stop < NT) break;
@@ -157,16 +191,14 @@ __device__ long long lookback_block(unsigned long long *st, long long b, unsigne
     return excl;
 }
 
-// Issue the record prefetch of tile t into buffer `buf` (thread 0 only).
+// Record prefetch of tile t into buffer buf (thread 0).
 __device__ void prefetch_tile(TileSmem &S, int buf, long long t, long long ntiles,
-                              const int32_t *tile_first, const uint32_t *cur, const int4 *rec,
-                              unsigned *phase) {
+                              const int32_t *tile_first, const uint32_t *cur, const int4 *rec) {
     S.pre_n[buf] = -1;
     if (t >= ntiles) return;
     const int c0 = tile_first[t], c1 = tile_first[t + 1];
     const int r0 = col_start(cur, c0), r1 = col_start(cur, c1);
     const int n = r1 - r0;
-    S.pre_r0[buf] = r0;
     if (n > 0 && n <= TCAP) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         tma_load(S.rec[buf], rec + r0, (unsigned)n * 16u, &S.mbar[buf]);
@@ -174,40 +206,48 @@ __device__ void prefetch_tile(TileSmem &S, int buf, long long t, long long ntile
     } else {
         S.pre_n[buf] = (n == 0) ? 0 : -1;
     }
-    (void)phase;
 }
 
-// Write the staged outputs of a finished tile (after its look-back).
-__device__ void finish_tile(TileSmem &S, const OutStage &O, unsigned long long *tile_state,
-                            long long ntiles, const uint32_t *cur, int32_t N, int32_t *jc,
-                            int32_t *ir, double *pr, int64_t cap, ErrState *err) {
+// jc entries of columns [c0, c1): jc[c] = P + base[# non-empty columns before c]
+__device__ void write_jc(TileSmem &S, const uint32_t *cur, int c0, int c1, int n_ci,
+                         const int *base, long long P, int32_t *jc) {
     const int tid = threadIdx.x;
-    const long long P = lookback_block(tile_state, O.tile, (unsigned long long)O.U, S);
-    bool over = false;
-    for (int k = tid; k < O.U; k += NT) {
-        const long long o = P + k;
-        if (o < cap) {
-            ir[o] = O.row[k];
-            pr[o] = O.val[k];
-        } else {
-            over = true;
-        }
-    }
-    if (over) atomicExch(&err->cap_exceeded, 1u);
     int ne_run = 0;
-    for (int cb = O.c0; cb < O.c1; cb += NT) {
+    for (int cb = c0; cb < c1; cb += NT) {
         const int c = cb + tid;
-        const bool in = c < O.c1;
+        const bool in = c < c1;
         const int e = in ? (int)(cur[c] & POSMASK) : 0;
         const int st = in ? col_start(cur, c) : 0;
         const int ne = (in && e > st) ? 1 : 0;
         int tot;
         const int k = block_excl_sum<NT, int>(ne, S.warp_tmp, tot) + ne_run;
-        if (in) jc[c] = (int32_t)(P + O.ci_base[min(k, O.n_ci)]);
+        if (in) jc[c] = (int32_t)(P + base[min(k, n_ci)]);
         ne_run += tot;
     }
-    if (O.tile == ntiles - 1 && tid == 0) {
-        const long long nnz = P + O.U;
+}
+
+// Finish the pending tile: look-back, staged ir/pr, jc, nnz.
+__device__ void finish_pending(TileSmem &S, unsigned long long *tile_state, long long ntiles,
+                               const uint32_t *cur, int32_t N, int32_t *jc, int32_t *ir,
+                               double *pr, int64_t cap, ErrState *err, int pb) {
+    const int tid = threadIdx.x;
+    const long long t = S.p_tile;
+    const int U = S.p_U;
+    const long long P = lookback_block(tile_state, t, (unsigned long long)U, S);
+    bool over = false;
+    for (int k = tid; k < U; k += NT) {
+        const long long o = P + k;
+        if (o < cap) {
+            ir[o] = S.st_row[k];
+            pr[o] = S.st_val[k];
+        } else {
+            over = true;
+        }
+    }
+    if (over) atomicExch(&err->cap_exceeded, 1u);
+    write_jc(S, cur, S.p_c0, S.p_c1, S.p_nci, S.ci_base[pb], P, jc);
+    if (t == ntiles - 1 && tid == 0) {
+        const long long nnz = P + U;
         jc[N] = (int32_t)nnz;
         err->nnz = nnz;
         if (nnz > cap) atomicExch(&err->cap_exceeded, 1u);
@@ -227,8 +267,9 @@ __global__ void __launch_bounds__(NT, 2) k_tile_fold(const uint32_t *__restrict_
                                                       ErrState *err) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     TileSmem &S = *reinterpret_cast<TileSmem *>(smem_raw);
-    const int tid = threadIdx.x;
-    unsigned phase[2] = {0u, 0u};
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const unsigned lt = lanemask_lt();
+    unsigned phase0 = 0u, phase1 = 0u;
 
     if (tid == 0) {
         mbar_init(&S.mbar[0]);
@@ -236,33 +277,27 @@ __global__ void __launch_bounds__(NT, 2) k_tile_fold(const uint32_t *__restrict_
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         const long long t0 = atomicAdd(&err->tile_ticket, 1u);
         S.next_tile = t0;
-        prefetch_tile(S, 0, t0, ntiles, tile_first, cur, rec, phase);
+        prefetch_tile(S, 0, t0, ntiles, tile_first, cur, rec);
     }
     __syncthreads();
     long long b = S.next_tile;
-    int buf = 0, ob = 0;
-    long long pending = -1;
+    int buf = 0, cbuf = 0;
+    bool pending = false;
 
     while (b < ntiles) {
-        // ---- claim the next tile and start its record prefetch ------------
+        // ---- claim the next tile, prefetch its records ----------------------
         if (tid == 0) {
             const long long t1 = atomicAdd(&err->tile_ticket, 1u);
             S.next_tile = t1;
-            prefetch_tile(S, buf ^ 1, t1, ntiles, tile_first, cur, rec, phase);
-            S.n_groups = 0;
-            S.overflow = 0;
+            prefetch_tile(S, buf ^ 1, t1, ntiles, tile_first, cur, rec);
         }
-        for (int k = tid; k < TCAP; k += NT) {
-            S.col[k] = 0;
-            S.g_cnt[k] = 0;
-        }
-        for (int k = tid; k < HS; k += NT) S.u.h.key[k] = 0ull;
+        for (int k = tid; k < TCAP; k += NT) S.col[k] = 0;
         const int c0 = tile_first[b], c1 = tile_first[b + 1];
         __syncthreads();
 
-        // ---- phase 1: columns of the tile ---------------------------------
-        int n_ci = 0, n_small = 0, has_big = 0;
-        const int r0 = col_start(cur, c0);
+        // ---- column pass (block) ---------------------------------------------
+        // packed scan: bits 0-11 non-empty count, 12-23 small records, 24+ big
+        int n_ci = 0, n_small = 0, has_big = 0, overflow = 0;
         for (int cb = c0; cb < c1; cb += NT) {
             const int c = cb + tid;
             const bool in = c < c1;
@@ -273,167 +308,247 @@ __global__ void __launch_bounds__(NT, 2) k_tile_fold(const uint32_t *__restrict_
             const int cnt = in ? e - st : 0;
             const int ne = cnt > 0 ? 1 : 0;
             const int sc = (ne && !big) ? cnt : 0;
-            int tot_ne, tot_sc;
-            const int ci = block_excl_sum<NT, int>(ne, S.warp_tmp, tot_ne) + n_ci;
-            const int q = block_excl_sum<NT, int>(sc, S.warp_tmp, tot_sc) + n_small;
-            const int anybig = __syncthreads_or(ne && big);
+            const int scc = min(sc, 4095);
+            const int packed = ne | (scc << 12) | ((ne && big) ? (1 << 24) : 0);
+            int tot;
+            const int pre = block_excl_sum<NT, int>(packed, S.warp_tmp, tot);
+            const int ci = n_ci + (pre & 4095);
+            const int q = n_small + ((pre >> 12) & 4095);
             if (ne) {
                 if (ci < CCAP && q + sc <= TCAP) {
                     S.ci_col[ci] = c;
                     S.ci_start[ci] = st;
-                    S.ci_q[ci] = big ? -1 : q;
+                    S.ci_q[ci] = q;
                     S.ci_cnt[ci] = big ? 0 : cnt;
                     S.ci_u[ci] = big ? (int)(bigu[c] & POSMASK) : 0;
                     if (!big) S.col[q] = ci + 1;
                 } else {
-                    S.overflow = 1;
+                    overflow = 1;
                 }
             }
-            n_ci += tot_ne;
-            n_small += tot_sc;
-            has_big |= anybig;
+            n_ci += tot & 4095;
+            n_small += (tot >> 12) & 4095;
+            has_big |= (tot >> 24) != 0;
+            overflow |= (n_ci > CCAP) || (n_small > TCAP);
         }
-        __syncthreads();
-        if (S.overflow) {
+        overflow = __syncthreads_or(overflow);
+        if (overflow) {  // cannot happen for consistent cursors; fail loudly
             if (tid == 0) atomicExch(&err->internal, 1u);
             n_ci = 0;
             n_small = 0;
-            has_big = 1;  // no staging: take the synchronous path with nothing to write
+            has_big = 1;
         }
 
-        // ---- phase 2: records in shared memory --------------------------------
+        // ---- records in shared memory ----------------------------------------
         int4 *R = S.rec[buf];
         const int pn = S.pre_n[buf];
-        if (pn > 0) {  // a TMA load was issued for this buffer: wait for it
-            mbar_wait(&S.mbar[buf], phase[buf]);
-            phase[buf] ^= 1u;
+        if (pn > 0) {
+            if (buf == 0) {
+                mbar_wait(&S.mbar[0], phase0);
+                phase0 ^= 1u;
+            } else {
+                mbar_wait(&S.mbar[1], phase1);
+                phase1 ^= 1u;
+            }
         }
         if (has_big) {
-            __syncthreads();  // everyone past the wait before overwriting
+            __syncthreads();
             for (int ci = 0; ci < n_ci; ++ci) {
-                const int q = S.ci_q[ci];
-                if (q < 0) continue;
-                const int st = S.ci_start[ci], cnt = S.ci_cnt[ci];
+                const int cnt = S.ci_cnt[ci];
+                if (cnt == 0) continue;
+                const int q = S.ci_q[ci], st = S.ci_start[ci];
                 for (int p = tid; p < cnt; p += NT) R[q + p] = rec[st + p];
             }
+            __syncthreads();
         } else if (pn < 0 && n_small > 0) {
+            const int r0 = S.ci_start[0];
             for (int p = tid; p < n_small; p += NT) R[p] = rec[r0 + p];
+            __syncthreads();
         }
-        smem_incl_max<NT, IPT>(S.col, n_small, S.warp_tmp);  // ends with a barrier
 
-        // ---- phase 3: (column,row) groups via a shared-memory hash -------------
-        for (int p = tid; p < n_small; p += NT) {
-            const int row = R[p].x;
-            const int ci = S.col[p] - 1;
-            const unsigned long long key = ((unsigned long long)(unsigned)ci << 32) | (unsigned)row;
-            unsigned h = hash_slot(key);
-            while (true) {
-                const unsigned long long old = atomicCAS(&S.u.h.key[h], 0ull, key);
-                if (old == 0ull) {
-                    const int g = atomicAdd(&S.n_groups, 1);
-                    S.u.h.gid[h] = (int16_t)g;
-                    S.g_first[g] = (int16_t)p;
-                    S.g_crank[g] = (int16_t)atomicAdd(&S.ci_u[ci], 1);
-                    break;
-                }
-                if (old == key) break;
-                h = (h + 1) & (HS - 1);
+        // ---- warp window: columns whose first record lies in [w*WIN, (w+1)*WIN)
+        int cw_lo, cw_hi;
+        {
+            // lower_bound over ci_q (non-decreasing) for the two window edges
+            int lo = 0, hi = n_ci;
+            const int key_lo = warp * WIN;
+            while (lo < hi) {
+                int mid = (lo + hi) >> 1;
+                if (S.ci_q[mid] < key_lo) lo = mid + 1; else hi = mid;
             }
-            S.r_gid[p] = (int16_t)h;
+            cw_lo = lo;
+            hi = n_ci;
+            const int key_hi = (warp == NW - 1) ? 0x7fffffff : (warp + 1) * WIN;
+            while (lo < hi) {
+                int mid = (lo + hi) >> 1;
+                if (S.ci_q[mid] < key_hi) lo = mid + 1; else hi = mid;
+            }
+            cw_hi = lo;
         }
-        __syncthreads();
-        for (int p = tid; p < n_small; p += NT) {
-            const int g = S.u.h.gid[S.r_gid[p]];
+        const int qa = (cw_lo < n_ci) ? S.ci_q[cw_lo] : n_small;
+        const int qb = (cw_hi < n_ci) ? S.ci_q[cw_hi] : n_small;
+
+        // (a) column id of each record: warp max-scan of the head marks
+        {
+            int carry = 0;
+            for (int p0 = qa; p0 < qb; p0 += 32) {
+                const int p = p0 + lane;
+                const int v = (p < qb) ? S.col[p] : 0;
+                const int m = max(warp_incl_max(v), carry);
+                if (p < qb) S.col[p] = m;
+                carry = __shfl_sync(FULL, m, 31);
+            }
+        }
+        // clear this warp's hash region and group counters
+        const int hb = 2 * qa, hn = 2 * (qb - qa);  // hash slots of this warp
+        for (int k = qa + lane; k < qb; k += 32) {
+            S.hc[k].key[0] = 0ull;
+            S.hc[k].key[1] = 0ull;
+        }
+        for (int k = qa + lane; k < qb; k += 32) S.g_cnt[k] = 0;
+        __syncwarp();
+
+        // (b) (column,row) groups: hash insert, group ids by ballot
+        int ng = 0;
+        for (int p0 = qa; p0 < qb; p0 += 32) {
+            const int p = p0 + lane;
+            const bool act = p < qb;
+            bool leader = false;
+            int h = 0, ci = 0;
+            if (act) {
+                const int row = R[p].x;
+                ci = S.col[p] - 1;
+                const unsigned long long key = ((unsigned long long)(unsigned)ci << 32) | (unsigned)row;
+                const unsigned hk = (unsigned)((key * 0x9E3779B97F4A7C15ull) >> 32);
+                h = hb + (int)(((unsigned long long)hk * (unsigned)hn) >> 32);
+                while (true) {
+                    const unsigned long long old = atomicCAS(&S.hc[h >> 1].key[h & 1], 0ull, key);
+                    if (old == 0ull) { leader = true; break; }
+                    if (old == key) break;
+                    h = (h + 1 == hb + hn) ? hb : h + 1;
+                }
+            }
+            const unsigned lm = __ballot_sync(FULL, leader);
+            if (leader) {
+                const int g = ng + __popc(lm & lt);
+                S.hgid[h] = (int16_t)g;
+                S.g_first[qa + g] = (int16_t)p;
+                S.g_crank[qa + g] = (int16_t)atomicAdd(&S.ci_u[ci], 1);
+            }
+            if (act) S.r_gid[p] = (int16_t)h;
+            ng += __popc(lm);
+        }
+        __syncwarp();
+        // (c) group of each record, arrival rank inside its group
+        for (int p = qa + lane; p < qb; p += 32) {
+            const int g = S.hgid[S.r_gid[p]];
             S.r_gid[p] = (int16_t)g;
-            S.r_arr[p] = (int16_t)atomicAdd(&S.g_cnt[g], 1);
+            S.r_arr[p] = (int16_t)atomicAdd(&S.g_cnt[qa + g], 1);
         }
-        __syncthreads();
-        const int n_groups = S.n_groups;
-
-        // ---- phase 4: group offsets, column offsets, publish the aggregate -----
-        OutStage &O = S.out[ob];
-        for (int g = tid; g < n_groups; g += NT) S.g_base[g] = S.g_cnt[g];
-        for (int k = tid; k < n_ci; k += NT) O.ci_base[k] = S.ci_u[k];
-        __syncthreads();
-        smem_excl_scan<NT, IPT, int>(S.g_base, n_groups, S.warp_tmp);
-        const int U = smem_excl_scan<NT, (CCAP + NT - 1) / NT, int>(O.ci_base, n_ci, S.warp_tmp);
-        if (tid == 0) {
-            O.ci_base[n_ci] = U;
-            O.c0 = c0;
-            O.c1 = c1;
-            O.n_ci = n_ci;
-            O.U = U;
-            O.tile = b;
-            volatile unsigned long long *vst = tile_state;
-            __threadfence();
-            if (b == 0) vst[0] = lb_pack(2, (unsigned long long)U);
-            else vst[b] = lb_pack(1, (unsigned long long)U);
+        __syncwarp();
+        // (d) group offsets (relative to qa), column offsets (relative to the
+        //     warp; with and without big columns)
+        for (int k = qa + lane; k < qa + ng; k += 32) S.hc[k].o.g_base = S.g_cnt[k];
+        int *cib = S.ci_base[cbuf];
+        for (int k = cw_lo + lane; k < cw_hi; k += 32) {
+            cib[k] = S.ci_u[k];
+            S.cg_base[k] = (S.ci_cnt[k] > 0) ? S.ci_u[k] : 0;
         }
-
-        // ---- phase 5: members by group, groups by column -----------------------
-        for (int p = tid; p < n_small; p += NT) {
+        __syncwarp();
+        {
+            int carry = 0;
+            for (int p0 = qa; p0 < qa + ng; p0 += 32) {
+                const int p = p0 + lane;
+                const int v = (p < qa + ng) ? S.hc[p].o.g_base : 0;
+                const int inc = warp_incl_sum(v);
+                if (p < qa + ng) S.hc[p].o.g_base = carry + inc - v;
+                carry += __shfl_sync(FULL, inc, 31);
+            }
+        }
+        const int Uw = warp_excl_scan(cib, cw_lo, cw_hi);
+        warp_excl_scan(S.cg_base, cw_lo, cw_hi);
+        __syncwarp();
+        // (e) member lists by group, group lists by column
+        for (int p = qa + lane; p < qb; p += 32) {
             const int g = S.r_gid[p];
-            S.u.o.members[S.g_base[g] + S.r_arr[p]] = (int16_t)p;
+            S.hc[qa + S.hc[qa + g].o.g_base + S.r_arr[p]].o.mem = (int16_t)p;
         }
-        for (int g = tid; g < n_groups; g += NT) {
-            const int ci = S.col[S.g_first[g]] - 1;
-            S.u.o.colgrp[O.ci_base[ci] + S.g_crank[g]] = (int16_t)g;
+        for (int g = lane; g < ng; g += 32) {
+            const int ci = S.col[S.g_first[qa + g]] - 1;
+            S.hc[qa + S.cg_base[ci] + S.g_crank[qa + g]].o.cgrp = (int16_t)g;
         }
-        __syncthreads();
-        // ---- phase 6: order each group by input position -----------------------
-        for (int p = tid; p < n_small; p += NT) {
+        __syncwarp();
+        // (f) order each group by input position
+        for (int p = qa + lane; p < qb; p += 32) {
             const int g = S.r_gid[p];
-            const int base = S.g_base[g], sz = S.g_cnt[g];
+            const int base = qa + S.hc[qa + g].o.g_base, sz = S.g_cnt[qa + g];
             const int4 r = R[p];
             int rank = 0;
-            if (sz > 1) {
-                for (int k = 0; k < sz; ++k) rank += (R[S.u.o.members[base + k]].y < r.y);
-            }
-            S.u.o.sval[base + rank] = __hiloint2double(r.w, r.z);
+            for (int k = 0; k < sz; ++k) rank += (R[S.hc[base + k].o.mem].y < r.y);
+            S.hc[base + rank].o.sval = __hiloint2double(r.w, r.z);
         }
-        __syncthreads();
-        // ---- phase 7: fold each group, order groups by row, stage outputs -----
-        for (int g = tid; g < n_groups; g += NT) {
-            const int p0 = S.g_first[g];
-            const int row = R[p0].x;
-            const int ci = S.col[p0] - 1;
-            const int cb = O.ci_base[ci], cu = S.ci_u[ci];
-            int rank = 0;
-            for (int k = 0; k < cu; ++k) rank += (R[S.g_first[S.u.o.colgrp[cb + k]]].x < row);
-            const int base = S.g_base[g], sz = S.g_cnt[g];
-            double acc = 0.0;
-            for (int k = 0; k < sz; ++k) acc = fold_add(acc, S.u.o.sval[base + k]);
-            if (!has_big) {
-                O.row[cb + rank] = row - 1;
-                O.val[cb + rank] = acc;
-            } else {
-                S.u.o.sval[base] = acc;  // keep for the synchronous write below
-                S.g_cnt[g] = cb + rank;  // tile-local output index
-            }
-        }
+        if (lane == 0) S.w_u[warp] = Uw;
         __syncthreads();
 
-        if (!has_big) {
-            // ---- deferred output of the previous tile ------------------------
-            if (pending >= 0) finish_tile(S, S.out[ob ^ 1], tile_state, ntiles, cur, N, jc, ir, pr, cap, err);
-            pending = b;
-            ob ^= 1;
-        } else {
-            // ---- synchronous path (tile with a big column) --------------------
-            const long long P = lookback_block(tile_state, b, (unsigned long long)U, S);
-            bool over = false;
-            for (int g = tid; g < n_groups; g += NT) {
-                const int p0 = S.g_first[g];
-                const long long o = P + S.g_cnt[g];
-                if (o < cap) {
-                    ir[o] = R[p0].x - 1;
-                    pr[o] = S.u.o.sval[S.g_base[g]];
+        // ---- tile count, aggregate, warp output bases --------------------------
+        if (tid < 32) {
+            const int v = (tid < NW) ? S.w_u[tid] : 0;
+            const int inc = warp_incl_sum(v);
+            if (tid < NW) S.w_base[tid] = inc - v;
+            if (tid == NW - 1) {
+                const int U = inc;
+                cib[n_ci] = U;
+                volatile unsigned long long *vst = tile_state;
+                __threadfence();
+                if (b == 0) vst[0] = lb_pack(2, (unsigned long long)U);
+                else vst[b] = lb_pack(1, (unsigned long long)U);
+                S.warp_tmp[0] = U;
+            }
+        }
+        __syncthreads();
+        const int U = S.warp_tmp[0];
+        const int wbase = S.w_base[warp];
+        for (int k = cw_lo + lane; k < cw_hi; k += 32) cib[k] += wbase;
+        __syncthreads();
+
+        // ---- finish the previous tile (its look-back had a tile of time) -------
+        if (pending) finish_pending(S, tile_state, ntiles, cur, N, jc, ir, pr, cap, err, cbuf ^ 1);
+
+        long long P = 0;
+        if (has_big) P = lookback_block(tile_state, b, (unsigned long long)U, S);
+        __syncthreads();
+
+        // (g) fold each group in input order, order groups by row, stage/write
+        bool over = false;
+        for (int g = lane; g < ng; g += 32) {
+            const int p0 = S.g_first[qa + g];
+            const int row = R[p0].x;
+            const int ci = S.col[p0] - 1;
+            const int cl = S.cg_base[ci];        // warp-relative column offset in cgrp
+            const int cu = S.ci_u[ci];
+            int rank = 0;
+            for (int k = 0; k < cu; ++k) rank += (R[S.g_first[qa + S.hc[qa + cl + k].o.cgrp]].x < row);
+            const int base = qa + S.hc[qa + g].o.g_base, sz = S.g_cnt[qa + g];
+            double acc = 0.0;
+            for (int k = 0; k < sz; ++k) acc = fold_add(acc, S.hc[base + k].o.sval);
+            const int o = cib[ci] + rank;        // tile-local output index
+            if (!has_big) {
+                S.st_row[o] = row - 1;
+                S.st_val[o] = acc;
+            } else {
+                const long long go = P + o;
+                if (go < cap) {
+                    ir[go] = row - 1;
+                    pr[go] = acc;
                 } else {
                     over = true;
                 }
             }
+        }
+        if (has_big) {
+            __syncthreads();
             for (int ci = 0; ci < n_ci; ++ci) {
-                if (S.ci_q[ci] >= 0) continue;
+                if (S.ci_cnt[ci] != 0) continue;  // small column: done above
                 const int c = S.ci_col[ci];
                 const uint32_t w = bigu[c];
                 const int ub = (int)(w & POSMASK);
@@ -443,41 +558,40 @@ __global__ void __launch_bounds__(NT, 2) k_tile_fold(const uint32_t *__restrict_
                 const unsigned long long *K = (w & BIGFLAG) ? RR + n : RR;
                 const unsigned long long *V = (w & BIGFLAG) ? RR : RR + n;
                 for (int k = tid; k < ub; k += NT) {
-                    const long long o = P + O.ci_base[ci] + k;
-                    if (o < cap) {
-                        ir[o] = (int32_t)K[k];
-                        pr[o] = __longlong_as_double((long long)V[k]);
+                    const long long go = P + cib[ci] + k;
+                    if (go < cap) {
+                        ir[go] = (int32_t)K[k];
+                        pr[go] = __longlong_as_double((long long)V[k]);
                     } else {
                         over = true;
                     }
                 }
             }
             if (over) atomicExch(&err->cap_exceeded, 1u);
-            int ne_run = 0;
-            for (int cb = c0; cb < c1; cb += NT) {
-                const int c = cb + tid;
-                const bool in = c < c1;
-                const int e = in ? (int)(cur[c] & POSMASK) : 0;
-                const int st = in ? col_start(cur, c) : 0;
-                const int ne = (in && e > st) ? 1 : 0;
-                int tot;
-                const int k = block_excl_sum<NT, int>(ne, S.warp_tmp, tot) + ne_run;
-                if (in) jc[c] = (int32_t)(P + O.ci_base[min(k, n_ci)]);
-                ne_run += tot;
-            }
+            write_jc(S, cur, c0, c1, n_ci, cib, P, jc);
             if (b == ntiles - 1 && tid == 0) {
                 const long long nnz = P + U;
                 jc[N] = (int32_t)nnz;
                 err->nnz = nnz;
                 if (nnz > cap) atomicExch(&err->cap_exceeded, 1u);
             }
+            pending = false;
+        } else {
+            if (tid == 0) {
+                S.p_tile = b;
+                S.p_c0 = c0;
+                S.p_c1 = c1;
+                S.p_nci = n_ci;
+                S.p_U = U;
+            }
+            pending = true;
+            cbuf ^= 1;
         }
         __syncthreads();
         b = S.next_tile;
         buf ^= 1;
     }
-    if (pending >= 0) finish_tile(S, S.out[ob ^ 1], tile_state, ntiles, cur, N, jc, ir, pr, cap, err);
-    // drain a prefetch that was issued past the end (none: t >= ntiles issues nothing)
+    if (pending) finish_pending(S, tile_state, ntiles, cur, N, jc, ir, pr, cap, err, cbuf ^ 1);
 }
 
 cudaError_t launch_tile_fold(Launch &lc, const uint32_t *cur, const int32_t *tile_first,
@@ -499,6 +613,5 @@ cudaError_t launch_tile_fold(Launch &lc, const uint32_t *cur, const int32_t *til
     lc.launches++;
     return cudaGetLastError();
 }
-
 
 }  // namespace sa
