@@ -20,13 +20,15 @@ struct sa_ctx {
     int launches = 0;
 
     // device workspace (grown on demand, reused across calls)
-    uint32_t *cur = nullptr;              size_t cur_cap = 0;     // N
-    int4 *rec = nullptr;                  size_t rec_cap = 0;     // L
-    int32_t *tile_first = nullptr;        size_t tf_cap = 0;      // ntiles+1
+    uint32_t *cur = nullptr;              size_t cur_cap = 0;     // N (counts, then cursors)
+    uint32_t *sstart = nullptr;           size_t st_cap = 0;      // N+1 small-space starts
+    int4 *rec = nullptr;                  size_t rec_cap = 0;     // L + placeholders
+    int32_t *win_first = nullptr;         size_t wf_cap = 0;      // nwin+1
+    uint8_t *tile_big = nullptr;          size_t tb_cap = 0;      // ntiles
     unsigned long long *tile_state = nullptr; size_t ts_cap = 0;  // ntiles
     unsigned long long *scan_state = nullptr; size_t ss_cap = 0;  // scan CTAs
-    uint32_t *big_list = nullptr;         size_t bl_cap = 0;      // L/BIGCOL+1
-    uint32_t *bigu = nullptr;             size_t bu_cap = 0;      // N
+    BigCol *big_list = nullptr;           size_t bl_cap = 0;      // L/(BIGCOL+1)+1
+    uint32_t *bigk = nullptr;             size_t bk_cap = 0;      // N
     ErrState *err = nullptr;              // device
     ErrState *err_host = nullptr;         // pinned mirror
 
@@ -91,7 +93,7 @@ int bits_for(uint64_t v) {  // bits needed to represent v (0 -> 0)
 
 // One launch that resets the per-call device state.
 __global__ void k_init(ErrState *err, uint32_t *cur, int64_t ncur, unsigned long long *ts,
-                       int64_t nts, unsigned long long *ss, int64_t nss) {
+                       int64_t nts, unsigned long long *ss, int64_t nss, uint8_t *tb) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t0 == 0) {
@@ -106,7 +108,10 @@ __global__ void k_init(ErrState *err, uint32_t *cur, int64_t ncur, unsigned long
     uint4 *cur4 = reinterpret_cast<uint4 *>(cur);
     for (int64_t k = t0; k < nq; k += stride) cur4[k] = make_uint4(0, 0, 0, 0);
     for (int64_t k = (nq << 2) + t0; k < ncur; k += stride) cur[k] = 0;
-    for (int64_t k = t0; k < nts; k += stride) ts[k] = 0ull;
+    for (int64_t k = t0; k < nts; k += stride) {
+        ts[k] = 0ull;
+        tb[k] = 0;
+    }
     for (int64_t k = t0; k < nss; k += stride) ss[k] = 0ull;
 }
 
@@ -114,7 +119,7 @@ int launch_init(sa_ctx *ctx, Launch &lc, int64_t ncur, int64_t nts, int64_t nss)
     int64_t work = std::max<int64_t>({ncur / 4, nts, nss, 1});
     int grid = (int)std::min<int64_t>((work + 255) / 256, (int64_t)ctx->num_sms * 4);
     k_init<<<grid, 256, 0, lc.stream>>>(ctx->err, ctx->cur, ncur, ctx->tile_state, nts,
-                                        ctx->scan_state, nss);
+                                        ctx->scan_state, nss, ctx->tile_big);
     lc.launches++;
     SA_CUDA(ctx, cudaGetLastError());
     return SA_OK;
@@ -208,12 +213,14 @@ void sa_destroy(sa_ctx *ctx) {
     cudaSetDevice(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     cudaFree(ctx->cur);
+    cudaFree(ctx->sstart);
     cudaFree(ctx->rec);
-    cudaFree(ctx->tile_first);
+    cudaFree(ctx->win_first);
+    cudaFree(ctx->tile_big);
     cudaFree(ctx->tile_state);
     cudaFree(ctx->scan_state);
     cudaFree(ctx->big_list);
-    cudaFree(ctx->bigu);
+    cudaFree(ctx->bigk);
     cudaFree(ctx->err);
     cudaFree(ctx->h_ii);
     cudaFree(ctx->h_jj);
@@ -307,15 +314,19 @@ int sa_assemble_async(sa_ctx *ctx, const int32_t *d_ii, const int32_t *d_jj, con
         return SA_OK;
     }
 
-    const int64_t ntiles = (L + TILE - 1) / TILE;
+    const int64_t nbig_max = L / (BIGCOL + 1) + 1;
+    const int64_t ntiles = (L + nbig_max + TILE - 1) / TILE;
+    const int64_t nwin = ntiles * TILE_WARPS;
     const int64_t nscan = (N + 4095) / 4096;
     SA_CUDA(ctx, ensure(ctx->cur, ctx->cur_cap, (size_t)N + 4));
-    SA_CUDA(ctx, ensure(ctx->rec, ctx->rec_cap, (size_t)L));
-    SA_CUDA(ctx, ensure(ctx->tile_first, ctx->tf_cap, (size_t)ntiles + 1));
+    SA_CUDA(ctx, ensure(ctx->sstart, ctx->st_cap, (size_t)N + 1));
+    SA_CUDA(ctx, ensure(ctx->rec, ctx->rec_cap, (size_t)(L + nbig_max)));
+    SA_CUDA(ctx, ensure(ctx->win_first, ctx->wf_cap, (size_t)nwin + 1));
+    SA_CUDA(ctx, ensure(ctx->tile_big, ctx->tb_cap, (size_t)ntiles));
     SA_CUDA(ctx, ensure(ctx->tile_state, ctx->ts_cap, (size_t)ntiles));
     SA_CUDA(ctx, ensure(ctx->scan_state, ctx->ss_cap, (size_t)nscan));
-    SA_CUDA(ctx, ensure(ctx->big_list, ctx->bl_cap, (size_t)(L / BIGCOL + 1)));
-    SA_CUDA(ctx, ensure(ctx->bigu, ctx->bu_cap, (size_t)N));
+    SA_CUDA(ctx, ensure(ctx->big_list, ctx->bl_cap, (size_t)nbig_max));
+    SA_CUDA(ctx, ensure(ctx->bigk, ctx->bk_cap, (size_t)N));
 
     ctx->nev = 0;
     int rc = mark(ctx, "k_init");
@@ -325,21 +336,23 @@ int sa_assemble_async(sa_ctx *ctx, const int32_t *d_ii, const int32_t *d_jj, con
     if ((rc = mark(ctx, "k_hist"))) return rc;
     SA_CUDA(ctx, launch_hist(lc, d_ii, d_jj, L, M, N, ctx->cur, ctx->err, false));
     if ((rc = mark(ctx, "k_col_scan"))) return rc;
-    SA_CUDA(ctx, launch_col_scan(lc, ctx->cur, N, L, ctx->tile_first, ntiles, ctx->big_list,
-                                 ctx->scan_state, ctx->err));
+    SA_CUDA(ctx, launch_col_scan(lc, ctx->cur, ctx->sstart, ctx->cur, N, nwin, ctx->win_first,
+                                 ctx->tile_big, ntiles, ctx->big_list, ctx->bigk, ctx->scan_state,
+                                 ctx->err));
     if ((rc = mark(ctx, "k_scatter"))) return rc;
-    SA_CUDA(ctx, launch_scatter(lc, d_ii, d_jj, d_s, s_stride, L, M, N, ctx->cur, ctx->rec));
+    SA_CUDA(ctx, launch_scatter(lc, d_ii, d_jj, d_s, s_stride, L, M, N, ctx->cur, ctx->rec, ctx->err));
     if (L > BIGCOL) {
         const int idx_bits = std::max(1, bits_for((uint64_t)(L - 1)));
         const int row_bits = bits_for((uint64_t)(M > 0 ? M - 1 : 0));
         const int passes = std::max(1, (idx_bits + row_bits + 7) / 8);
         if ((rc = mark(ctx, "k_bigcol"))) return rc;
-        SA_CUDA(ctx, launch_bigcol(lc, ctx->cur, ctx->big_list, ctx->err, ctx->rec, d_s, s_stride,
-                                   ctx->bigu, idx_bits, passes));
+        SA_CUDA(ctx, launch_bigcol(lc, ctx->big_list, ctx->err, ctx->rec, d_s, s_stride, idx_bits,
+                                   passes));
     }
     if ((rc = mark(ctx, "k_tile_fold"))) return rc;
-    SA_CUDA(ctx, launch_tile_fold(lc, ctx->cur, ctx->tile_first, ntiles, ctx->rec, ctx->bigu,
-                                  ctx->tile_state, N, d_jc, d_ir, d_pr, cap, ctx->err));
+    SA_CUDA(ctx, launch_tile_fold(lc, ctx->sstart, ctx->win_first, ctx->tile_big, ntiles, ctx->rec,
+                                  ctx->big_list, ctx->bigk, ctx->tile_state, N, d_jc, d_ir, d_pr,
+                                  cap, ctx->err));
     if ((rc = mark(ctx, nullptr))) return rc;
     ctx->launches = lc.launches;
     return SA_OK;

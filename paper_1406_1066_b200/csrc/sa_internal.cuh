@@ -9,19 +9,31 @@ namespace sa {
 
 constexpr unsigned FULL = 0xffffffffu;
 
-// Column cursor word (cur[c]): low 31 bits a triplet offset, bit 31 set when
-// column c is "big" (more than BIGCOL triplets) and takes the big-column path.
+// Record space.  Columns with at most BIGCOL triplets ("small") are laid out
+// in column order in [0, Lsmall); longer ("big") columns get their own space
+// [Lsmall, L) and are folded by k_bigcol.  Column words carry BIGFLAG for big
+// columns; the low 31 bits are an offset.
 constexpr uint32_t BIGFLAG = 0x80000000u;
 constexpr uint32_t POSMASK = 0x7fffffffu;
 
-// Tile geometry of the column-tile fold (k_tile_fold).  A tile owns the
-// columns whose first triplet lies in [b*TILE, (b+1)*TILE); columns longer
-// than BIGCOL are folded by k_bigcol instead, so a tile holds at most
-// TILE + BIGCOL triplets in shared memory.
+// Fold geometry (k_tile_fold).  Tile b owns the columns whose small-space
+// start lies in [b*TILE, (b+1)*TILE); inside the CTA, warp w owns the
+// columns starting in its WIN-wide sub-window.  A tile holds at most
+// TILE + BIGCOL - 1 small records.
 constexpr int TILE = 512;
+constexpr int TILE_THREADS = 256;
+constexpr int TILE_WARPS = TILE_THREADS / 32;
+constexpr int WIN = TILE / TILE_WARPS;
 constexpr int BIGCOL = 512;
 constexpr int TCAP = TILE + BIGCOL;
-constexpr int TILE_THREADS = 256;
+
+// One big column (k_col_scan appends, k_bigcol folds, k_tile_fold copies out).
+struct BigCol {
+    uint32_t col;     // column index
+    uint32_t start;   // absolute record offset (Lsmall + big-space offset)
+    uint32_t n;       // triplets
+    uint32_t u;       // unique rows (after k_bigcol) | BIGFLAG if keys ended in buffer B
+};
 
 // Device-side outcome of one assembly (zeroed / reset before every call).
 struct ErrState {
@@ -37,7 +49,7 @@ struct ErrState {
     unsigned int tile_ticket;   // dynamic tile counters (forward progress)
     unsigned int scan_ticket;
     unsigned int nbig;          // number of big columns
-    unsigned int pad;
+    unsigned int lsmall;        // triplets in small columns (small record space)
 };
 
 __device__ __forceinline__ unsigned lanemask_lt() {
@@ -208,17 +220,18 @@ cudaError_t launch_convert(Launch &lc, const void *raw, int dtype, int64_t L, in
                            ErrState *err);
 cudaError_t launch_hist(Launch &lc, const int32_t *ii, const int32_t *jj, int64_t L,
                         int32_t M, int32_t N, uint32_t *cnt, ErrState *err, bool infer);
-cudaError_t launch_col_scan(Launch &lc, uint32_t *cur, int32_t N, int64_t L,
-                            int32_t *tile_first, int64_t ntiles, uint32_t *big_list,
+cudaError_t launch_col_scan(Launch &lc, const uint32_t *cnt, uint32_t *sstart, uint32_t *cur,
+                            int32_t N, int64_t nwin, int32_t *win_first, uint8_t *tile_big,
+                            int64_t ntiles, BigCol *big_list, uint32_t *bigk,
                             unsigned long long *scan_state, ErrState *err);
 cudaError_t launch_scatter(Launch &lc, const int32_t *ii, const int32_t *jj, const double *s,
                            int64_t s_stride, int64_t L, int32_t M, int32_t N, uint32_t *cur,
-                           int4 *rec);
-cudaError_t launch_bigcol(Launch &lc, const uint32_t *cur, const uint32_t *big_list,
-                          const ErrState *err, int4 *rec, const double *s, int64_t s_stride,
-                          uint32_t *bigu, int idx_bits, int passes);
-cudaError_t launch_tile_fold(Launch &lc, const uint32_t *cur, const int32_t *tile_first,
-                             int64_t ntiles, const int4 *rec, const uint32_t *bigu,
+                           int4 *rec, const ErrState *err);
+cudaError_t launch_bigcol(Launch &lc, BigCol *big_list, const ErrState *err, int4 *rec,
+                          const double *s, int64_t s_stride, int idx_bits, int passes);
+cudaError_t launch_tile_fold(Launch &lc, const uint32_t *sstart, const int32_t *win_first,
+                             const uint8_t *tile_big, int64_t ntiles, const int4 *rec,
+                             const BigCol *big_list, const uint32_t *bigk,
                              unsigned long long *tile_state, int32_t N, int32_t *jc,
                              int32_t *ir, double *pr, int64_t cap, ErrState *err);
 

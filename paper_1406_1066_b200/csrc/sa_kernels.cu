@@ -181,23 +181,34 @@ cudaError_t launch_hist(Launch &lc, const int32_t *ii, const int32_t *jj, int64_
 }
 
 // ---------------------------------------------------------------------------
-// k_col_scan: exclusive scan of cnt[0..N) in place (cur[c] = first triplet
-// slot of column c, | BIGFLAG for big columns), decoupled look-back across
-// CTAs (ticket-ordered for forward progress).  Also emits
-//   tile_first[b] = min{c : start(c) >= b*TILE}   for 0 <= b <= ntiles
-//   big_list[]    = columns with more than BIGCOL triplets.
+// k_col_scan: one pass over the column counts (decoupled look-back across
+// CTAs, ticket-ordered for forward progress).  Two exclusive prefixes at once,
+// packed (big << 31 | small): small columns (<= BIGCOL triplets) get offsets
+// in the small record space, big columns in the big space.  Emits
+//   sstart[c]     small-space start of column c (| BIGFLAG if big; a big
+//                 column sits at the start of the next small column)
+//   cur[c]        scatter cursor (small start, or big-space start | BIGFLAG)
+//   win_first[w]  min{c : sstart(c) >= w*WIN}, 0 <= w <= nwin (fold windows)
+//   tile_big[b]   tile b owns a big column
+//   big_list[]    big columns {col, big-space start, n}; bigk[c] = list index
+//   err->lsmall   size of the small space
 // ---------------------------------------------------------------------------
 constexpr int SCAN_NT = 256;
 constexpr int SCAN_IPT = 16;
 constexpr int SCAN_TILE = SCAN_NT * SCAN_IPT;
+constexpr unsigned long long SMALL_MASK = (1ull << 31) - 1;
 
-__global__ void __launch_bounds__(SCAN_NT) k_col_scan(uint32_t *__restrict__ cur, int32_t N,
-                                                      int64_t L, int32_t *__restrict__ tile_first,
-                                                      int64_t ntiles, uint32_t *__restrict__ big_list,
+__global__ void __launch_bounds__(SCAN_NT) k_col_scan(const uint32_t *__restrict__ cnt,
+                                                      uint32_t *__restrict__ sstart,
+                                                      uint32_t *__restrict__ cur, int32_t N,
+                                                      int64_t nwin, int32_t *__restrict__ win_first,
+                                                      uint8_t *__restrict__ tile_big, int64_t ntiles,
+                                                      BigCol *__restrict__ big_list,
+                                                      uint32_t *__restrict__ bigk,
                                                       unsigned long long *scan_state,
                                                       ErrState *err) {
     __shared__ uint32_t s_v[SCAN_TILE];
-    __shared__ uint32_t s_warp[SCAN_NT / 32];
+    __shared__ unsigned long long s_warp[SCAN_NT / 32];
     __shared__ long long s_b;
     __shared__ unsigned long long s_excl;
     if (threadIdx.x == 0) s_b = atomicAdd(&err->scan_ticket, 1u);
@@ -205,69 +216,84 @@ __global__ void __launch_bounds__(SCAN_NT) k_col_scan(uint32_t *__restrict__ cur
     const long long b = s_b;
     const int64_t c_base = b * SCAN_TILE;
     for (int k = threadIdx.x; k < SCAN_TILE; k += SCAN_NT) {
-        int64_t c = c_base + k;
-        s_v[k] = (c < N) ? cur[c] : 0u;
+        const int64_t c = c_base + k;
+        s_v[k] = (c < N) ? cnt[c] : 0u;
     }
     __syncthreads();
     uint32_t loc[SCAN_IPT];
-    uint32_t sum = 0;
+    unsigned long long sum = 0;
 #pragma unroll
     for (int k = 0; k < SCAN_IPT; ++k) {
         loc[k] = s_v[threadIdx.x * SCAN_IPT + k];
-        sum += loc[k];
+        // a big column adds its triplets to the big space and one placeholder
+        // slot to the small space (so every column has a distinct fold position)
+        sum += (loc[k] > (uint32_t)BIGCOL) ? (((unsigned long long)loc[k] << 31) | 1ull) : loc[k];
     }
-    uint32_t total;
-    uint32_t pre = block_excl_sum<SCAN_NT, uint32_t>(sum, s_warp, total);
+    unsigned long long total;
+    unsigned long long pre = block_excl_sum<SCAN_NT, unsigned long long>(sum, s_warp, total);
     if (threadIdx.x < 32) {
-        unsigned long long e = lookback_warp(scan_state, b, total);
+        const unsigned long long e = lookback_warp(scan_state, b, total);
         if (threadIdx.x == 0) s_excl = e;
     }
     __syncthreads();
-    uint64_t start = s_excl + pre;
+    const unsigned long long run0 = s_excl + pre;
+    uint64_t small = run0 & SMALL_MASK;
+    uint64_t bigp = run0 >> 31;
 #pragma unroll
     for (int k = 0; k < SCAN_IPT; ++k) {
         const int64_t c = c_base + threadIdx.x * SCAN_IPT + k;
         const uint32_t n = loc[k];
-        uint32_t word = (uint32_t)start;
+        const bool big = n > (uint32_t)BIGCOL;
         if (c < N) {
-            if (n > (uint32_t)BIGCOL) {
-                word |= BIGFLAG;
-                unsigned slot = atomicAdd(&err->nbig, 1u);
-                big_list[slot] = (uint32_t)c;
+            sstart[c] = (uint32_t)small | (big ? BIGFLAG : 0u);
+            if (big) {
+                cur[c] = (uint32_t)bigp | BIGFLAG;
+                const unsigned slot = atomicAdd(&err->nbig, 1u);
+                big_list[slot] = BigCol{(uint32_t)c, (uint32_t)bigp, n, 0u};
+                bigk[c] = slot;
+                int64_t tb = (int64_t)(small / TILE);
+                if (tb > ntiles - 1) tb = ntiles - 1;
+                tile_big[tb] = 1;
+            } else {
+                cur[c] = (uint32_t)small;
             }
-            // tiles b' with start < b'*TILE <= start + n begin at column c+1
-            if (n) {
-                int64_t first = (int64_t)(start / TILE) + 1;
-                int64_t last = (int64_t)((start + n) / TILE);
-                if (last > ntiles - 1) last = ntiles - 1;
-                for (int64_t bb = first; bb <= last; ++bb) tile_first[bb] = (int32_t)(c + 1);
+            // fold windows w with small < w*WIN <= small + extent start at column c+1
+            const uint32_t ext = big ? 1u : n;
+            if (ext) {
+                int64_t first = (int64_t)(small / WIN) + 1;
+                int64_t last = (int64_t)((small + ext) / WIN);
+                if (last > nwin - 1) last = nwin - 1;
+                for (int64_t w = first; w <= last; ++w) win_first[w] = (int32_t)(c + 1);
+            }
+            if (c == N - 1) {
+                const uint64_t tot_small = small + (big ? 1 : n);
+                err->lsmall = (unsigned)tot_small;
+                sstart[N] = (uint32_t)tot_small;
+                // windows past the small space (and past dropped invalid triplets) are empty
+                for (int64_t w = (int64_t)(tot_small / WIN) + 1; w <= nwin; ++w) win_first[w] = N;
             }
         }
-        if (c == N - 1) {
-            // tiles past the valid total (invalid triplets were dropped) are empty
-            for (int64_t bb = (int64_t)((start + n) / TILE) + 1; bb <= ntiles; ++bb) tile_first[bb] = N;
+        if (big) {
+            bigp += n;
+            small += 1;
+        } else {
+            small += n;
         }
-        s_v[threadIdx.x * SCAN_IPT + k] = word;
-        start += n;
-    }
-    __syncthreads();
-    for (int k = threadIdx.x; k < SCAN_TILE; k += SCAN_NT) {
-        int64_t c = c_base + k;
-        if (c < N) cur[c] = s_v[k];
     }
     if (b == 0 && threadIdx.x == 0) {
-        tile_first[0] = 0;
-        tile_first[ntiles] = N;
+        win_first[0] = 0;
+        win_first[nwin] = N;
     }
 }
 
-cudaError_t launch_col_scan(Launch &lc, uint32_t *cur, int32_t N, int64_t L, int32_t *tile_first,
-                            int64_t ntiles, uint32_t *big_list, unsigned long long *scan_state,
-                            ErrState *err) {
+cudaError_t launch_col_scan(Launch &lc, const uint32_t *cnt, uint32_t *sstart, uint32_t *cur,
+                            int32_t N, int64_t nwin, int32_t *win_first, uint8_t *tile_big,
+                            int64_t ntiles, BigCol *big_list, uint32_t *bigk,
+                            unsigned long long *scan_state, ErrState *err) {
     if (N <= 0) return cudaSuccess;
     int grid = (int)((N + SCAN_TILE - 1) / SCAN_TILE);
-    k_col_scan<<<grid, SCAN_NT, 0, lc.stream>>>(cur, N, L, tile_first, ntiles, big_list,
-                                               scan_state, err);
+    k_col_scan<<<grid, SCAN_NT, 0, lc.stream>>>(cnt, sstart, cur, N, nwin, win_first, tile_big,
+                                               ntiles, big_list, bigk, scan_state, err);
     lc.launches++;
     return cudaGetLastError();
 }
@@ -279,7 +305,7 @@ cudaError_t launch_col_scan(Launch &lc, uint32_t *cur, int32_t N, int64_t L, int
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void scatter_one(int64_t t, int32_t i, int32_t j, double v, bool live,
                                             int32_t M, int32_t N, uint32_t *__restrict__ cur,
-                                            int4 *__restrict__ rec) {
+                                            int4 *__restrict__ rec, uint32_t lsmall) {
     const bool ok = live && i >= 1 && j >= 1 && i <= M && j <= N;
     const unsigned act = __ballot_sync(FULL, ok);
     if (!ok) return;
@@ -289,7 +315,8 @@ __device__ __forceinline__ void scatter_one(int64_t t, int32_t i, int32_t j, dou
     uint32_t base = 0;
     if (lane == leader) base = atomicAdd(&cur[j - 1], (uint32_t)__popc(peers));
     base = __shfl_sync(act, base, leader);
-    const uint32_t pos = (base & POSMASK) + __popc(peers & lanemask_lt());
+    const uint32_t pos = (base & POSMASK) + ((base & BIGFLAG) ? lsmall : 0u) +
+                         __popc(peers & lanemask_lt());
     rec[pos] = make_int4(i, (int)t, __double2loint(v), __double2hiint(v));
 }
 
@@ -298,8 +325,10 @@ __global__ void __launch_bounds__(256) k_scatter(const int32_t *__restrict__ ii,
                                                  const double *__restrict__ s, int64_t s_stride,
                                                  int64_t L, int32_t M, int32_t N,
                                                  uint32_t *__restrict__ cur,
-                                                 int4 *__restrict__ rec, int vec) {
+                                                 int4 *__restrict__ rec, int vec,
+                                                 const ErrState *err) {
     const int lane = threadIdx.x & 31;
+    const uint32_t lsmall = err->lsmall;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     const int64_t wbase0 = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31);
     int64_t tail0 = 0;
@@ -322,10 +351,10 @@ __global__ void __launch_bounds__(256) k_scatter(const int32_t *__restrict__ ii,
                     vb = __ldg(s2 + 2 * q + 1);
                 }
             }
-            scatter_one(4 * q + 0, vi.x, vj.x, va.x, live, M, N, cur, rec);
-            scatter_one(4 * q + 1, vi.y, vj.y, va.y, live, M, N, cur, rec);
-            scatter_one(4 * q + 2, vi.z, vj.z, vb.x, live, M, N, cur, rec);
-            scatter_one(4 * q + 3, vi.w, vj.w, vb.y, live, M, N, cur, rec);
+            scatter_one(4 * q + 0, vi.x, vj.x, va.x, live, M, N, cur, rec, lsmall);
+            scatter_one(4 * q + 1, vi.y, vj.y, va.y, live, M, N, cur, rec, lsmall);
+            scatter_one(4 * q + 2, vi.z, vj.z, vb.x, live, M, N, cur, rec, lsmall);
+            scatter_one(4 * q + 3, vi.w, vj.w, vb.y, live, M, N, cur, rec, lsmall);
         }
         tail0 = nq << 2;
     }
@@ -334,18 +363,18 @@ __global__ void __launch_bounds__(256) k_scatter(const int32_t *__restrict__ ii,
         const bool live = t < L;
         int32_t i = live ? ii[t] : 0, j = live ? jj[t] : 0;
         double v = live ? s[t * s_stride] : 0.0;
-        scatter_one(t, i, j, v, live, M, N, cur, rec);
+        scatter_one(t, i, j, v, live, M, N, cur, rec, lsmall);
     }
 }
 
 cudaError_t launch_scatter(Launch &lc, const int32_t *ii, const int32_t *jj, const double *s,
                            int64_t s_stride, int64_t L, int32_t M, int32_t N, uint32_t *cur,
-                           int4 *rec) {
+                           int4 *rec, const ErrState *err) {
     if (L <= 0) return cudaSuccess;
     const int vec = aligned16(ii) && aligned16(jj) && (s_stride == 0 || aligned16(s));
     int64_t want = ((vec ? (L >> 2) : L) + 255) / 256 + 1;
     int grid = (int)std::min<int64_t>(want, (int64_t)lc.num_sms * 8);
-    k_scatter<<<grid, 256, 0, lc.stream>>>(ii, jj, s, s_stride, L, M, N, cur, rec, vec);
+    k_scatter<<<grid, 256, 0, lc.stream>>>(ii, jj, s, s_stride, L, M, N, cur, rec, vec, err);
     lc.launches++;
     return cudaGetLastError();
 }
@@ -362,12 +391,10 @@ cudaError_t launch_scatter(Launch &lc, const int32_t *ii, const int32_t *jj, con
 // ---------------------------------------------------------------------------
 constexpr int BIG_NT = 256;
 
-__global__ void __launch_bounds__(BIG_NT) k_bigcol(const uint32_t *__restrict__ cur,
-                                                   const uint32_t *__restrict__ big_list,
+__global__ void __launch_bounds__(BIG_NT) k_bigcol(BigCol *__restrict__ big_list,
                                                    const ErrState *err, int4 *rec,
                                                    const double *__restrict__ s, int64_t s_stride,
-                                                   uint32_t *__restrict__ bigu, int idx_bits,
-                                                   int passes) {
+                                                   int idx_bits, int passes) {
     __shared__ uint32_t s_hist[256];
     __shared__ uint32_t s_bin[256];
     __shared__ uint16_t s_wcnt[BIG_NT / 32][257];
@@ -375,14 +402,13 @@ __global__ void __launch_bounds__(BIG_NT) k_bigcol(const uint32_t *__restrict__ 
     __shared__ unsigned long long s_prevrow;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const unsigned nbig = *((volatile const unsigned *)&err->nbig);
+    const unsigned lsmall = *((volatile const unsigned *)&err->lsmall);
     for (int k = tid; k < (BIG_NT / 32) * 257; k += BIG_NT) (&s_wcnt[0][0])[k] = 0;
     __syncthreads();
     const unsigned long long idx_mask = (1ull << idx_bits) - 1;
     for (unsigned kb = blockIdx.x; kb < nbig; kb += gridDim.x) {
-        const uint32_t c = big_list[kb];
-        const uint32_t e = cur[c] & POSMASK;
-        const uint32_t st = c ? (cur[c - 1] & POSMASK) : 0u;
-        const int64_t n = (int64_t)e - st;
+        const uint32_t st = big_list[kb].start + lsmall;
+        const int64_t n = big_list[kb].n;
         unsigned long long *A = reinterpret_cast<unsigned long long *>(rec + st);
         unsigned long long *B = A + n;
         // pack records -> keys in A (ascending chunks; reads stay ahead of writes)
@@ -485,17 +511,18 @@ __global__ void __launch_bounds__(BIG_NT) k_bigcol(const uint32_t *__restrict__ 
             carry += tot;
             __syncthreads();
         }
-        if (tid == 0) bigu[c] = carry | ((src == B) ? BIGFLAG : 0u);
+        if (tid == 0) {
+            big_list[kb].start = st;  // absolute from here on
+            big_list[kb].u = carry | ((src == B) ? BIGFLAG : 0u);
+        }
         __syncthreads();
     }
 }
 
-cudaError_t launch_bigcol(Launch &lc, const uint32_t *cur, const uint32_t *big_list,
-                          const ErrState *err, int4 *rec, const double *s, int64_t s_stride,
-                          uint32_t *bigu, int idx_bits, int passes) {
+cudaError_t launch_bigcol(Launch &lc, BigCol *big_list, const ErrState *err, int4 *rec,
+                          const double *s, int64_t s_stride, int idx_bits, int passes) {
     int grid = lc.num_sms;
-    k_bigcol<<<grid, BIG_NT, 0, lc.stream>>>(cur, big_list, err, rec, s, s_stride, bigu, idx_bits,
-                                            passes);
+    k_bigcol<<<grid, BIG_NT, 0, lc.stream>>>(big_list, err, rec, s, s_stride, idx_bits, passes);
     lc.launches++;
     return cudaGetLastError();
 }

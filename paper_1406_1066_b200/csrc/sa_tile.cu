@@ -1,29 +1,31 @@
 // sa_tile.cu -- k_tile_fold: the ordered segmented fold (sm_100a).
 //
 // Input: 16-byte records {row, input position, value} grouped by column
-// (k_scatter), column cursors cur[] (cur[c] = end of column c), tile_first[]
-// (first column whose records start in each TILE-wide window).  Output: jc,
-// ir, pr.
+// (k_scatter) in the small record space; sstart[c] = small-space start of
+// column c (| BIGFLAG for a big column, which occupies one placeholder
+// slot); win_first[w] = first column starting in fold window w.
+// Output: jc, ir, pr.
 //
-// Persistent CTAs take tiles in ticket order.  Per tile:
-//   block  column pass: the tile's non-empty columns and record ranges
-//   TMA    records arrive by cp.async.bulk, issued one tile ahead
-//   warps  each warp owns the columns starting in its TILE/8 window and, with
-//          warp-synchronous code only (no block barriers):
-//            (a) column id of each record
-//            (b) (column,row) groups: warp-private shared-memory hash,
-//                group ids by ballot
-//            (c) group sizes / arrival ranks, (d) warp scans of group and
-//                column offsets, (e) member lists, (f) members ordered by
-//                input position
-//   block  tile unique count U -> decoupled look-back aggregate; the
-//          PREVIOUS tile (whose look-back had a whole tile of time to
-//          resolve) is finished: block-wide look-back, coalesced ir/pr/jc
-//   warps  (g) fold each group from +0.0 in input order (the reference's
-//          scatter contract, _kernels.pyx:82-89; x86 NaN rule), order groups
-//          by row inside each column, stage (row, value) in CSC order.
-// Tiles with a column longer than BIGCOL (folded by k_bigcol) take a
-// synchronous path that writes straight to global memory.
+// Persistent CTAs take tiles (TILE_WARPS consecutive windows) in ticket
+// order; the tile's records arrive by one TMA bulk copy issued a tile ahead.
+// Each warp then folds the columns starting in its window on its own
+// (warp-synchronous, no block barriers):
+//   (1) its non-empty columns (lanes over columns), record column ids
+//   (2) (column,row) groups via a warp-private shared-memory hash; group ids
+//       assigned by ballot
+//   (3) group sizes and arrival ranks; warp scans of group offsets
+//   (4) group-major member list (input position, value)
+//   (5) each member ranked by input position inside its group
+//   (6) per column: output offsets (groups, or k_bigcol's count)
+// then the block adds the warp counts into the tile count U (decoupled
+// look-back aggregate), finishes the PREVIOUS tile (block-wide look-back --
+// which had a whole tile of time to resolve -- and coalesced ir/pr/jc
+// writes), and each warp
+//   (7) folds every group from +0.0 in input order (the reference's scatter
+//       contract, _kernels.pyx:82-89; x86 NaN rule) and places it by row
+//       inside its column, staging (row-1, value) in CSC order.
+// Tiles holding a big column (folded by k_bigcol) write straight to global
+// memory after an inline look-back.
 
 #include "sa_internal.cuh"
 
@@ -32,50 +34,47 @@ namespace sa {
 namespace {
 
 constexpr int NT = TILE_THREADS;
-constexpr int NW = NT / 32;
-constexpr int WIN = TILE / NW;  // record-position window per warp
-constexpr int HSZ = 2 * TCAP;   // hash slots: 2 per record position
-constexpr int CCAP = TILE;      // non-empty columns per tile (distinct starts in a TILE window)
+constexpr int NW = TILE_WARPS;
+constexpr int WSTRIDE = WIN + 1;  // per-warp column slots + sentinel
 
 struct TileSmem {
     int4 rec[2][TCAP];                 // double-buffered records (TMA destination)
     unsigned long long mbar[2];
-    int col[TCAP];                     // column heads -> column-local index + 1
-    // One 16-byte cell per record position k: first the two hash slots 2k,
-    // 2k+1 of the owning warp's private table, then (hash dead) per-index
-    // fields.  Warps only touch cells of their own record range.
+    int col[TCAP];                     // column heads -> column slot + 1
+    // One 16-byte cell per record position k of the owning warp's range:
+    // first hash slots 2k, 2k+1; after the hash is dead, per-index fields.
     union HCell {
         unsigned long long key[2];
         struct {
-            double sval;               // group values ordered by input position
+            double sval;               // group-major values ordered by input position
+            int midx;                  // group-major member input positions
             int g_base;                // group offset (index qa + gid)
-            int16_t mem;               // member lists (record ids), per group
-            int16_t cgrp;              // group ids listed per column
         } o;
     } hc[TCAP];
-    int16_t hgid[HSZ];
-    int g_cnt[TCAP];                   // per group (indexed qa + gid)
-    int cg_base[CCAP];                 // warp-relative offset of a column in cgrp
+    double mval[TCAP];                 // group-major member values (arrival order)
+    int crow[TCAP];                    // rows of a column's groups (column-major)
+    int16_t hgid[2 * TCAP];
+    int g_cnt[TCAP];                   // per group (index qa + gid)
     int16_t g_first[TCAP];
     int16_t g_crank[TCAP];
     int16_t r_gid[TCAP];               // per record
     int16_t r_arr[TCAP];
-    int ci_col[CCAP];
-    int ci_start[CCAP];
-    int ci_q[CCAP];
-    int ci_cnt[CCAP];                  // 0 for big columns
-    int ci_u[CCAP];                    // groups per column (or k_bigcol's count)
-    int ci_base[2][CCAP + 1];          // tile-local output offsets (current / pending)
+    int ci_c[TILE];                    // per column slot (warp w: slots [w*WIN, w*WIN+WIN))
+    int ci_q[TILE];
+    int ci_n[TILE];                    // small record count (0 for a big placeholder)
+    int ci_u[TILE];                    // groups, or k_bigcol's unique count
+    int cg_base[TILE];                 // warp-relative offset of the column in crow
+    int cib[2][NW * WSTRIDE];          // warp-relative output offsets (+ sentinel), 2 tiles
+    int w_base[2][NW];                 // warp output base inside the tile, 2 tiles
+    int w_u[NW];
     int st_row[TCAP];                  // staged outputs of the pending tile
     double st_val[TCAP];
-    int w_u[NW], w_base[NW];
     int warp_tmp[NW];
     long long red_ll[NW];
     int pre_n[2];
     long long next_tile;
-    // pending tile metadata
     long long p_tile;
-    int p_c0, p_c1, p_nci, p_U;
+    int p_U;
 };
 
 __device__ __forceinline__ unsigned smem_u32(const void *p) {
@@ -111,11 +110,6 @@ __device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned pari
     }
 }
 
-__device__ __forceinline__ int col_start(const uint32_t *cur, int c) {
-    return c > 0 ? (int)(cur[c - 1] & POSMASK) : 0;
-}
-
-// warp-level inclusive sum / max
 __device__ __forceinline__ int warp_incl_sum(int x) {
     const int lane = threadIdx.x & 31;
 #pragma unroll
@@ -134,20 +128,6 @@ __device__ __forceinline__ int warp_incl_max(int x) {
         if (lane >= o) x = max(x, y);
     }
     return x;
-}
-
-// In-place warp exclusive scan over a[lo, hi) (lanes stride 32); returns total.
-__device__ __forceinline__ int warp_excl_scan(int *a, int lo, int hi) {
-    const int lane = threadIdx.x & 31;
-    int carry = 0;
-    for (int p0 = lo; p0 < hi; p0 += 32) {
-        const int p = p0 + lane;
-        const int v = (p < hi) ? a[p] : 0;
-        const int inc = warp_incl_sum(v);
-        if (p < hi) a[p] = carry + inc - v;
-        carry += __shfl_sync(FULL, inc, 31);
-    }
-    return carry;
 }
 
 // Block-wide decoupled look-back: exclusive prefix of tile b, then publish
@@ -191,13 +171,18 @@ __device__ long long lookback_block(unsigned long long *st, long long b, unsigne
     return excl;
 }
 
+__device__ __forceinline__ int tile_r0(const uint32_t *sstart, const int32_t *win_first,
+                                       long long t) {
+    return (int)(sstart[win_first[t * NW]] & POSMASK);
+}
+
 // Record prefetch of tile t into buffer buf (thread 0).
 __device__ void prefetch_tile(TileSmem &S, int buf, long long t, long long ntiles,
-                              const int32_t *tile_first, const uint32_t *cur, const int4 *rec) {
+                              const int32_t *win_first, const uint32_t *sstart, const int4 *rec) {
     S.pre_n[buf] = -1;
     if (t >= ntiles) return;
-    const int c0 = tile_first[t], c1 = tile_first[t + 1];
-    const int r0 = col_start(cur, c0), r1 = col_start(cur, c1);
+    const int r0 = tile_r0(sstart, win_first, t);
+    const int r1 = (int)(sstart[win_first[(t + 1) * NW]] & POSMASK);
     const int n = r1 - r0;
     if (n > 0 && n <= TCAP) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -208,58 +193,31 @@ __device__ void prefetch_tile(TileSmem &S, int buf, long long t, long long ntile
     }
 }
 
-// jc entries of columns [c0, c1): jc[c] = P + base[# non-empty columns before c]
-__device__ void write_jc(TileSmem &S, const uint32_t *cur, int c0, int c1, int n_ci,
-                         const int *base, long long P, int32_t *jc) {
-    const int tid = threadIdx.x;
-    int ne_run = 0;
-    for (int cb = c0; cb < c1; cb += NT) {
-        const int c = cb + tid;
-        const bool in = c < c1;
-        const int e = in ? (int)(cur[c] & POSMASK) : 0;
-        const int st = in ? col_start(cur, c) : 0;
-        const int ne = (in && e > st) ? 1 : 0;
-        int tot;
-        const int k = block_excl_sum<NT, int>(ne, S.warp_tmp, tot) + ne_run;
-        if (in) jc[c] = (int32_t)(P + base[min(k, n_ci)]);
-        ne_run += tot;
-    }
-}
-
-// Finish the pending tile: look-back, staged ir/pr, jc, nnz.
-__device__ void finish_pending(TileSmem &S, unsigned long long *tile_state, long long ntiles,
-                               const uint32_t *cur, int32_t N, int32_t *jc, int32_t *ir,
-                               double *pr, int64_t cap, ErrState *err, int pb) {
-    const int tid = threadIdx.x;
-    const long long t = S.p_tile;
-    const int U = S.p_U;
-    const long long P = lookback_block(tile_state, t, (unsigned long long)U, S);
-    bool over = false;
-    for (int k = tid; k < U; k += NT) {
-        const long long o = P + k;
-        if (o < cap) {
-            ir[o] = S.st_row[k];
-            pr[o] = S.st_val[k];
-        } else {
-            over = true;
-        }
-    }
-    if (over) atomicExch(&err->cap_exceeded, 1u);
-    write_jc(S, cur, S.p_c0, S.p_c1, S.p_nci, S.ci_base[pb], P, jc);
-    if (t == ntiles - 1 && tid == 0) {
-        const long long nnz = P + U;
-        jc[N] = (int32_t)nnz;
-        err->nnz = nnz;
-        if (nnz > cap) atomicExch(&err->cap_exceeded, 1u);
+// jc of one warp's columns: jc[c] = P + wbase + cib[first non-empty column >= c]
+__device__ void warp_write_jc(const uint32_t *sstart, int c_lo, int c_hi, const int *cibw,
+                              long long Pw, int32_t *jc) {
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = lanemask_lt();
+    int k0 = 0;
+    for (int cb = c_lo; cb < c_hi; cb += 32) {
+        const int c = cb + lane;
+        const bool in = c < c_hi;
+        int ne = 0;
+        if (in) ne = (sstart[c + 1] & POSMASK) > (sstart[c] & POSMASK);
+        const unsigned m = __ballot_sync(FULL, ne);
+        if (in) jc[c] = (int32_t)(Pw + cibw[k0 + __popc(m & lt)]);
+        k0 += __popc(m);
     }
 }
 
 }  // namespace
 
-__global__ void __launch_bounds__(NT, 2) k_tile_fold(const uint32_t *__restrict__ cur,
-                                                      const int32_t *__restrict__ tile_first,
+__global__ void __launch_bounds__(NT, 2) k_tile_fold(const uint32_t *__restrict__ sstart,
+                                                      const int32_t *__restrict__ win_first,
+                                                      const uint8_t *__restrict__ tile_big,
                                                       int64_t ntiles, const int4 *__restrict__ rec,
-                                                      const uint32_t *__restrict__ bigu,
+                                                      const BigCol *__restrict__ big_list,
+                                                      const uint32_t *__restrict__ bigk,
                                                       unsigned long long *tile_state, int32_t N,
                                                       int32_t *__restrict__ jc,
                                                       int32_t *__restrict__ ir,
@@ -277,69 +235,65 @@ __global__ void __launch_bounds__(NT, 2) k_tile_fold(const uint32_t *__restrict_
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         const long long t0 = atomicAdd(&err->tile_ticket, 1u);
         S.next_tile = t0;
-        prefetch_tile(S, 0, t0, ntiles, tile_first, cur, rec);
+        prefetch_tile(S, 0, t0, ntiles, win_first, sstart, rec);
     }
     __syncthreads();
     long long b = S.next_tile;
-    int buf = 0, cbuf = 0;
+    int buf = 0, cb2 = 0;
     bool pending = false;
 
     while (b < ntiles) {
-        // ---- claim the next tile, prefetch its records ----------------------
         if (tid == 0) {
             const long long t1 = atomicAdd(&err->tile_ticket, 1u);
             S.next_tile = t1;
-            prefetch_tile(S, buf ^ 1, t1, ntiles, tile_first, cur, rec);
+            prefetch_tile(S, buf ^ 1, t1, ntiles, win_first, sstart, rec);
         }
-        for (int k = tid; k < TCAP; k += NT) S.col[k] = 0;
-        const int c0 = tile_first[b], c1 = tile_first[b + 1];
-        __syncthreads();
+        const bool has_big = tile_big[b] != 0;
+        const int r0 = tile_r0(sstart, win_first, b);
+        const int gw = (int)(b * NW) + warp;
+        const int c_lo = win_first[gw], c_hi = win_first[gw + 1];
+        const int slot0 = warp * WIN;
+        int *cibw = &S.cib[cb2][warp * WSTRIDE];
 
-        // ---- column pass (block) ---------------------------------------------
-        // packed scan: bits 0-11 non-empty count, 12-23 small records, 24+ big
-        int n_ci = 0, n_small = 0, has_big = 0, overflow = 0;
-        for (int cb = c0; cb < c1; cb += NT) {
-            const int c = cb + tid;
-            const bool in = c < c1;
-            const uint32_t ew = in ? cur[c] : 0u;
-            const int e = (int)(ew & POSMASK);
-            const int big = (int)(ew >> 31);
-            const int st = in ? col_start(cur, c) : 0;
-            const int cnt = in ? e - st : 0;
-            const int ne = cnt > 0 ? 1 : 0;
-            const int sc = (ne && !big) ? cnt : 0;
-            const int scc = min(sc, 4095);
-            const int packed = ne | (scc << 12) | ((ne && big) ? (1 << 24) : 0);
-            int tot;
-            const int pre = block_excl_sum<NT, int>(packed, S.warp_tmp, tot);
-            const int ci = n_ci + (pre & 4095);
-            const int q = n_small + ((pre >> 12) & 4095);
+        // ---- (1) the warp's non-empty columns ----------------------------------
+        int ncw = 0;
+        for (int cb = c_lo; cb < c_hi; cb += 32) {
+            const int c = cb + lane;
+            const bool in = c < c_hi;
+            uint32_t w0 = 0, w1 = 0;
+            if (in) {
+                w0 = sstart[c];
+                w1 = sstart[c + 1];
+            }
+            const int s0 = (int)(w0 & POSMASK), s1 = (int)(w1 & POSMASK);
+            const bool big = (w0 & BIGFLAG) != 0;
+            const bool ne = in && s1 > s0;
+            const unsigned m = __ballot_sync(FULL, ne);
             if (ne) {
-                if (ci < CCAP && q + sc <= TCAP) {
-                    S.ci_col[ci] = c;
-                    S.ci_start[ci] = st;
-                    S.ci_q[ci] = q;
-                    S.ci_cnt[ci] = big ? 0 : cnt;
-                    S.ci_u[ci] = big ? (int)(bigu[c] & POSMASK) : 0;
-                    if (!big) S.col[q] = ci + 1;
+                const int k = ncw + __popc(m & lt);
+                if (k < WIN) {
+                    const int sl = slot0 + k;
+                    S.ci_c[sl] = c;
+                    S.ci_q[sl] = s0 - r0;
+                    S.ci_n[sl] = big ? 0 : s1 - s0;
+                    S.ci_u[sl] = big ? (int)(big_list[bigk[c]].u & POSMASK) : 0;
                 } else {
-                    overflow = 1;
+                    atomicExch(&err->internal, 1u);
                 }
             }
-            n_ci += tot & 4095;
-            n_small += (tot >> 12) & 4095;
-            has_big |= (tot >> 24) != 0;
-            overflow |= (n_ci > CCAP) || (n_small > TCAP);
+            ncw += __popc(m);
         }
-        overflow = __syncthreads_or(overflow);
-        if (overflow) {  // cannot happen for consistent cursors; fail loudly
-            if (tid == 0) atomicExch(&err->internal, 1u);
-            n_ci = 0;
-            n_small = 0;
-            has_big = 1;
-        }
+        ncw = min(ncw, WIN);
+        const int qa = ncw ? S.ci_q[slot0] : 0;
+        int qb = qa;
+        if (ncw) qb = (int)(sstart[c_hi] & POSMASK) - r0;
+        __syncwarp();
+        // head marks (cleared over the warp's range first)
+        for (int p = qa + lane; p < qb; p += 32) S.col[p] = 0;
+        __syncwarp();
+        for (int k = lane; k < ncw; k += 32) S.col[S.ci_q[slot0 + k]] = slot0 + k + 1;
 
-        // ---- records in shared memory ----------------------------------------
+        // ---- records: TMA (or synchronous) -------------------------------------
         int4 *R = S.rec[buf];
         const int pn = S.pre_n[buf];
         if (pn > 0) {
@@ -350,45 +304,13 @@ __global__ void __launch_bounds__(NT, 2) k_tile_fold(const uint32_t *__restrict_
                 mbar_wait(&S.mbar[1], phase1);
                 phase1 ^= 1u;
             }
+        } else if (pn < 0) {
+            // tile too large for one copy (cannot happen: small columns only)
+            if (tid == 0) atomicExch(&err->internal, 1u);
         }
-        if (has_big) {
-            __syncthreads();
-            for (int ci = 0; ci < n_ci; ++ci) {
-                const int cnt = S.ci_cnt[ci];
-                if (cnt == 0) continue;
-                const int q = S.ci_q[ci], st = S.ci_start[ci];
-                for (int p = tid; p < cnt; p += NT) R[q + p] = rec[st + p];
-            }
-            __syncthreads();
-        } else if (pn < 0 && n_small > 0) {
-            const int r0 = S.ci_start[0];
-            for (int p = tid; p < n_small; p += NT) R[p] = rec[r0 + p];
-            __syncthreads();
-        }
+        __syncwarp();
 
-        // ---- warp window: columns whose first record lies in [w*WIN, (w+1)*WIN)
-        int cw_lo, cw_hi;
-        {
-            // lower_bound over ci_q (non-decreasing) for the two window edges
-            int lo = 0, hi = n_ci;
-            const int key_lo = warp * WIN;
-            while (lo < hi) {
-                int mid = (lo + hi) >> 1;
-                if (S.ci_q[mid] < key_lo) lo = mid + 1; else hi = mid;
-            }
-            cw_lo = lo;
-            hi = n_ci;
-            const int key_hi = (warp == NW - 1) ? 0x7fffffff : (warp + 1) * WIN;
-            while (lo < hi) {
-                int mid = (lo + hi) >> 1;
-                if (S.ci_q[mid] < key_hi) lo = mid + 1; else hi = mid;
-            }
-            cw_hi = lo;
-        }
-        const int qa = (cw_lo < n_ci) ? S.ci_q[cw_lo] : n_small;
-        const int qb = (cw_hi < n_ci) ? S.ci_q[cw_hi] : n_small;
-
-        // (a) column id of each record: warp max-scan of the head marks
+        // column slot of each record: max-scan of the head marks
         {
             int carry = 0;
             for (int p0 = qa; p0 < qb; p0 += 32) {
@@ -399,26 +321,29 @@ __global__ void __launch_bounds__(NT, 2) k_tile_fold(const uint32_t *__restrict_
                 carry = __shfl_sync(FULL, m, 31);
             }
         }
-        // clear this warp's hash region and group counters
-        const int hb = 2 * qa, hn = 2 * (qb - qa);  // hash slots of this warp
         for (int k = qa + lane; k < qb; k += 32) {
             S.hc[k].key[0] = 0ull;
             S.hc[k].key[1] = 0ull;
+            S.g_cnt[k] = 0;
         }
-        for (int k = qa + lane; k < qb; k += 32) S.g_cnt[k] = 0;
         __syncwarp();
 
-        // (b) (column,row) groups: hash insert, group ids by ballot
+        // ---- (2) (column,row) groups --------------------------------------------
+        const int hb = 2 * qa, hn = 2 * (qb - qa);
         int ng = 0;
         for (int p0 = qa; p0 < qb; p0 += 32) {
             const int p = p0 + lane;
-            const bool act = p < qb;
+            bool act = p < qb;
+            int sl = 0;
+            if (act) {
+                sl = S.col[p] - 1;
+                act = S.ci_n[sl] > 0;  // skip big-column placeholders
+            }
             bool leader = false;
-            int h = 0, ci = 0;
+            int h = 0;
             if (act) {
                 const int row = R[p].x;
-                ci = S.col[p] - 1;
-                const unsigned long long key = ((unsigned long long)(unsigned)ci << 32) | (unsigned)row;
+                const unsigned long long key = ((unsigned long long)(unsigned)sl << 32) | (unsigned)row;
                 const unsigned hk = (unsigned)((key * 0x9E3779B97F4A7C15ull) >> 32);
                 h = hb + (int)(((unsigned long long)hk * (unsigned)hn) >> 32);
                 while (true) {
@@ -433,105 +358,143 @@ __global__ void __launch_bounds__(NT, 2) k_tile_fold(const uint32_t *__restrict_
                 const int g = ng + __popc(lm & lt);
                 S.hgid[h] = (int16_t)g;
                 S.g_first[qa + g] = (int16_t)p;
-                S.g_crank[qa + g] = (int16_t)atomicAdd(&S.ci_u[ci], 1);
+                S.g_crank[qa + g] = (int16_t)atomicAdd(&S.ci_u[sl], 1);
             }
-            if (act) S.r_gid[p] = (int16_t)h;
+            if (p < qb) S.r_gid[p] = act ? (int16_t)h : (int16_t)-1;
             ng += __popc(lm);
         }
         __syncwarp();
-        // (c) group of each record, arrival rank inside its group
+        // ---- (3) group of each record, arrival rank ------------------------------
         for (int p = qa + lane; p < qb; p += 32) {
-            const int g = S.hgid[S.r_gid[p]];
-            S.r_gid[p] = (int16_t)g;
-            S.r_arr[p] = (int16_t)atomicAdd(&S.g_cnt[qa + g], 1);
+            const int h = S.r_gid[p];
+            if (h >= 0) {
+                const int g = S.hgid[h];
+                S.r_gid[p] = (int16_t)g;
+                S.r_arr[p] = (int16_t)atomicAdd(&S.g_cnt[qa + g], 1);
+            }
         }
         __syncwarp();
-        // (d) group offsets (relative to qa), column offsets (relative to the
-        //     warp; with and without big columns)
-        for (int k = qa + lane; k < qa + ng; k += 32) S.hc[k].o.g_base = S.g_cnt[k];
-        int *cib = S.ci_base[cbuf];
-        for (int k = cw_lo + lane; k < cw_hi; k += 32) {
-            cib[k] = S.ci_u[k];
-            S.cg_base[k] = (S.ci_cnt[k] > 0) ? S.ci_u[k] : 0;
-        }
-        __syncwarp();
+        // group offsets (relative to qa); hash cells are dead from here on
         {
             int carry = 0;
             for (int p0 = qa; p0 < qa + ng; p0 += 32) {
                 const int p = p0 + lane;
-                const int v = (p < qa + ng) ? S.hc[p].o.g_base : 0;
+                const int v = (p < qa + ng) ? S.g_cnt[p] : 0;
                 const int inc = warp_incl_sum(v);
                 if (p < qa + ng) S.hc[p].o.g_base = carry + inc - v;
                 carry += __shfl_sync(FULL, inc, 31);
             }
         }
-        const int Uw = warp_excl_scan(cib, cw_lo, cw_hi);
-        warp_excl_scan(S.cg_base, cw_lo, cw_hi);
         __syncwarp();
-        // (e) member lists by group, group lists by column
+        // ---- (4) group-major member list; (6) column offsets -------------------
         for (int p = qa + lane; p < qb; p += 32) {
+            if (S.r_gid[p] < 0 || S.ci_n[S.col[p] - 1] == 0) continue;
             const int g = S.r_gid[p];
-            S.hc[qa + S.hc[qa + g].o.g_base + S.r_arr[p]].o.mem = (int16_t)p;
-        }
-        for (int g = lane; g < ng; g += 32) {
-            const int ci = S.col[S.g_first[qa + g]] - 1;
-            S.hc[qa + S.cg_base[ci] + S.g_crank[qa + g]].o.cgrp = (int16_t)g;
-        }
-        __syncwarp();
-        // (f) order each group by input position
-        for (int p = qa + lane; p < qb; p += 32) {
-            const int g = S.r_gid[p];
-            const int base = qa + S.hc[qa + g].o.g_base, sz = S.g_cnt[qa + g];
+            const int j = qa + S.hc[qa + g].o.g_base + S.r_arr[p];
             const int4 r = R[p];
+            S.hc[j].o.midx = r.y;
+            S.mval[j] = __hiloint2double(r.w, r.z);
+        }
+        int Uw = 0;
+        {
+            int carry = 0, gcarry = 0;
+            for (int k0 = 0; k0 < ncw; k0 += 32) {
+                const int k = k0 + lane;
+                const int u = (k < ncw) ? S.ci_u[slot0 + k] : 0;
+                const int gu = (k < ncw && S.ci_n[slot0 + k] > 0) ? u : 0;
+                const int inc = warp_incl_sum(u);
+                const int ginc = warp_incl_sum(gu);
+                if (k < ncw) {
+                    cibw[k] = carry + inc - u;
+                    S.cg_base[slot0 + k] = gcarry + ginc - gu;
+                }
+                carry += __shfl_sync(FULL, inc, 31);
+                gcarry += __shfl_sync(FULL, ginc, 31);
+            }
+            Uw = carry;
+            if (lane == 0) cibw[ncw] = Uw;
+        }
+        __syncwarp();
+        // group rows listed per column (for the row order inside a column)
+        for (int g = lane; g < ng; g += 32) {
+            const int p = S.g_first[qa + g];
+            const int sl = S.col[p] - 1;
+            S.crow[qa + S.cg_base[sl] + S.g_crank[qa + g]] = R[p].x;
+        }
+        // ---- (5) members ranked by input position inside their group ----------
+        for (int p = qa + lane; p < qb; p += 32) {
+            if (S.r_gid[p] < 0 || S.ci_n[S.col[p] - 1] == 0) continue;
+            const int g = S.r_gid[p];
+            const int base = qa + S.hc[qa + g].o.g_base;
+            const int sz = S.g_cnt[qa + g];
+            const int j = base + S.r_arr[p];
+            const int my = S.hc[j].o.midx;
             int rank = 0;
-            for (int k = 0; k < sz; ++k) rank += (R[S.hc[base + k].o.mem].y < r.y);
-            S.hc[base + rank].o.sval = __hiloint2double(r.w, r.z);
+            for (int k = base; k < base + sz; ++k) rank += (S.hc[k].o.midx < my);
+            S.hc[base + rank].o.sval = S.mval[j];
         }
         if (lane == 0) S.w_u[warp] = Uw;
         __syncthreads();
 
-        // ---- tile count, aggregate, warp output bases --------------------------
+        // ---- tile count, aggregate ---------------------------------------------
         if (tid < 32) {
             const int v = (tid < NW) ? S.w_u[tid] : 0;
             const int inc = warp_incl_sum(v);
-            if (tid < NW) S.w_base[tid] = inc - v;
+            if (tid < NW) S.w_base[cb2][tid] = inc - v;
             if (tid == NW - 1) {
-                const int U = inc;
-                cib[n_ci] = U;
                 volatile unsigned long long *vst = tile_state;
                 __threadfence();
-                if (b == 0) vst[0] = lb_pack(2, (unsigned long long)U);
-                else vst[b] = lb_pack(1, (unsigned long long)U);
-                S.warp_tmp[0] = U;
+                if (b == 0) vst[0] = lb_pack(2, (unsigned long long)inc);
+                else vst[b] = lb_pack(1, (unsigned long long)inc);
+                S.warp_tmp[0] = inc;
             }
         }
         __syncthreads();
         const int U = S.warp_tmp[0];
-        const int wbase = S.w_base[warp];
-        for (int k = cw_lo + lane; k < cw_hi; k += 32) cib[k] += wbase;
+        const int wbase = S.w_base[cb2][warp];
         __syncthreads();
 
-        // ---- finish the previous tile (its look-back had a tile of time) -------
-        if (pending) finish_pending(S, tile_state, ntiles, cur, N, jc, ir, pr, cap, err, cbuf ^ 1);
-
+        // ---- finish the previous tile -------------------------------------------
+        if (pending) {
+            const long long pt = S.p_tile;
+            const int pU = S.p_U;
+            const long long P = lookback_block(tile_state, pt, (unsigned long long)pU, S);
+            for (int k = tid; k < pU; k += NT) {
+                const long long o = P + k;
+                if (o < cap) {
+                    ir[o] = S.st_row[k];
+                    pr[o] = S.st_val[k];
+                }
+            }
+            if (tid == 0 && P + pU > cap) atomicExch(&err->cap_exceeded, 1u);
+            const int pgw = (int)(pt * NW) + warp;
+            warp_write_jc(sstart, win_first[pgw], win_first[pgw + 1],
+                          &S.cib[cb2 ^ 1][warp * WSTRIDE], P + S.w_base[cb2 ^ 1][warp], jc);
+            if (pt == ntiles - 1 && tid == 0) {
+                jc[N] = (int32_t)(P + pU);
+                err->nnz = P + pU;
+            }
+            pending = false;
+        }
         long long P = 0;
         if (has_big) P = lookback_block(tile_state, b, (unsigned long long)U, S);
         __syncthreads();
 
-        // (g) fold each group in input order, order groups by row, stage/write
+        // ---- (7) fold each group in input order, place it by row ----------------
         bool over = false;
         for (int g = lane; g < ng; g += 32) {
             const int p0 = S.g_first[qa + g];
             const int row = R[p0].x;
-            const int ci = S.col[p0] - 1;
-            const int cl = S.cg_base[ci];        // warp-relative column offset in cgrp
-            const int cu = S.ci_u[ci];
+            const int sl = S.col[p0] - 1;
+            const int cl = qa + S.cg_base[sl];
+            const int cu = S.ci_u[sl];
             int rank = 0;
-            for (int k = 0; k < cu; ++k) rank += (R[S.g_first[qa + S.hc[qa + cl + k].o.cgrp]].x < row);
-            const int base = qa + S.hc[qa + g].o.g_base, sz = S.g_cnt[qa + g];
+            for (int k = cl; k < cl + cu; ++k) rank += (S.crow[k] < row);
+            const int base = qa + S.hc[qa + g].o.g_base;
+            const int sz = S.g_cnt[qa + g];
             double acc = 0.0;
-            for (int k = 0; k < sz; ++k) acc = fold_add(acc, S.hc[base + k].o.sval);
-            const int o = cib[ci] + rank;        // tile-local output index
+            for (int k = base; k < base + sz; ++k) acc = fold_add(acc, S.hc[k].o.sval);
+            const int o = wbase + cibw[sl - slot0] + rank;  // tile-local output index
             if (!has_big) {
                 S.st_row[o] = row - 1;
                 S.st_val[o] = acc;
@@ -546,56 +509,69 @@ __global__ void __launch_bounds__(NT, 2) k_tile_fold(const uint32_t *__restrict_
             }
         }
         if (has_big) {
-            __syncthreads();
-            for (int ci = 0; ci < n_ci; ++ci) {
-                if (S.ci_cnt[ci] != 0) continue;  // small column: done above
-                const int c = S.ci_col[ci];
-                const uint32_t w = bigu[c];
-                const int ub = (int)(w & POSMASK);
-                const int st = S.ci_start[ci];
-                const int n = (int)((cur[c] & POSMASK) - (uint32_t)st);
-                const unsigned long long *RR = reinterpret_cast<const unsigned long long *>(rec + st);
-                const unsigned long long *K = (w & BIGFLAG) ? RR + n : RR;
-                const unsigned long long *V = (w & BIGFLAG) ? RR : RR + n;
-                for (int k = tid; k < ub; k += NT) {
-                    const long long go = P + cib[ci] + k;
-                    if (go < cap) {
-                        ir[go] = (int32_t)K[k];
-                        pr[go] = __longlong_as_double((long long)V[k]);
+            // big columns of this warp: copy k_bigcol's results
+            for (int k = 0; k < ncw; ++k) {
+                const int sl = slot0 + k;
+                if (S.ci_n[sl] != 0) continue;
+                const BigCol bc = big_list[bigk[S.ci_c[sl]]];
+                const int ub = (int)(bc.u & POSMASK);
+                const unsigned long long *RR = reinterpret_cast<const unsigned long long *>(rec + bc.start);
+                const unsigned long long *K = (bc.u & BIGFLAG) ? RR + bc.n : RR;
+                const unsigned long long *V = (bc.u & BIGFLAG) ? RR : RR + bc.n;
+                const long long ob = P + wbase + cibw[k];
+                for (int e = lane; e < ub; e += 32) {
+                    if (ob + e < cap) {
+                        ir[ob + e] = (int32_t)K[e];
+                        pr[ob + e] = __longlong_as_double((long long)V[e]);
                     } else {
                         over = true;
                     }
                 }
             }
             if (over) atomicExch(&err->cap_exceeded, 1u);
-            write_jc(S, cur, c0, c1, n_ci, cib, P, jc);
+            warp_write_jc(sstart, c_lo, c_hi, cibw, P + wbase, jc);
             if (b == ntiles - 1 && tid == 0) {
-                const long long nnz = P + U;
-                jc[N] = (int32_t)nnz;
-                err->nnz = nnz;
-                if (nnz > cap) atomicExch(&err->cap_exceeded, 1u);
+                jc[N] = (int32_t)(P + U);
+                err->nnz = P + U;
+                if (P + U > cap) atomicExch(&err->cap_exceeded, 1u);
             }
-            pending = false;
         } else {
             if (tid == 0) {
                 S.p_tile = b;
-                S.p_c0 = c0;
-                S.p_c1 = c1;
-                S.p_nci = n_ci;
                 S.p_U = U;
             }
             pending = true;
-            cbuf ^= 1;
+            cb2 ^= 1;
         }
         __syncthreads();
         b = S.next_tile;
         buf ^= 1;
     }
-    if (pending) finish_pending(S, tile_state, ntiles, cur, N, jc, ir, pr, cap, err, cbuf ^ 1);
+    if (pending) {
+        const long long pt = S.p_tile;
+        const int pU = S.p_U;
+        const long long P = lookback_block(tile_state, pt, (unsigned long long)pU, S);
+        for (int k = tid; k < pU; k += NT) {
+            const long long o = P + k;
+            if (o < cap) {
+                ir[o] = S.st_row[k];
+                pr[o] = S.st_val[k];
+            }
+        }
+        if (tid == 0 && P + pU > cap) atomicExch(&err->cap_exceeded, 1u);
+        const int pgw = (int)(pt * NW) + warp;
+        warp_write_jc(sstart, win_first[pgw], win_first[pgw + 1], &S.cib[cb2 ^ 1][warp * WSTRIDE],
+                      P + S.w_base[cb2 ^ 1][warp], jc);
+        if (pt == ntiles - 1 && tid == 0) {
+            jc[N] = (int32_t)(P + pU);
+            err->nnz = P + pU;
+        }
+    }
 }
 
-cudaError_t launch_tile_fold(Launch &lc, const uint32_t *cur, const int32_t *tile_first,
-                             int64_t ntiles, const int4 *rec, const uint32_t *bigu,
+cudaError_t launch_tile_fold(Launch &lc, const uint32_t *sstart, const int32_t *win_first,
+                             const uint8_t *tile_big, int64_t ntiles, const int4 *rec,
+                             const BigCol *big_list, const uint32_t *bigk,
                              unsigned long long *tile_state, int32_t N, int32_t *jc, int32_t *ir,
                              double *pr, int64_t cap, ErrState *err) {
     if (ntiles <= 0) return cudaSuccess;
@@ -608,8 +584,9 @@ cudaError_t launch_tile_fold(Launch &lc, const uint32_t *cur, const int32_t *til
     if (e != cudaSuccess) return e;
     if (per_sm < 1) per_sm = 1;
     int64_t grid = std::min<int64_t>(ntiles, (int64_t)lc.num_sms * per_sm);
-    k_tile_fold<<<(unsigned)grid, NT, smem, lc.stream>>>(cur, tile_first, ntiles, rec, bigu,
-                                                        tile_state, N, jc, ir, pr, cap, err);
+    k_tile_fold<<<(unsigned)grid, NT, smem, lc.stream>>>(sstart, win_first, tile_big, ntiles, rec,
+                                                        big_list, bigk, tile_state, N, jc, ir, pr,
+                                                        cap, err);
     lc.launches++;
     return cudaGetLastError();
 }
