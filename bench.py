@@ -292,7 +292,9 @@ def main():
     tpath = os.path.join(ROOT, "profiles", "dram_traffic.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get(w.name, {}).get(dom)
+            rec = json.load(open(tpath)).get(w.name, {}).get(dom)
+            if rec:
+                traffic = rec["dram_read_bytes"] + rec["dram_write_bytes"]
         except Exception:
             traffic = None
 
