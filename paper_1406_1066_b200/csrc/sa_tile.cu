@@ -7,23 +7,22 @@
 // Output: jc, ir, pr.
 //
 // Persistent CTAs take tiles (TILE_WARPS consecutive windows) in ticket
-// order; the tile's records arrive by one TMA bulk copy issued a tile ahead.
-// Each warp then folds the columns starting in its window on its own
-// (warp-synchronous, no block barriers):
-//   (1) its non-empty columns (lanes over columns), record column ids
-//   (2) (column,row) groups via a warp-private shared-memory hash; group ids
-//       assigned by ballot
-//   (3) group sizes and arrival ranks; warp scans of group offsets
-//   (4) group-major member list (input position, value)
-//   (5) each member ranked by input position inside its group
-//   (6) per column: output offsets (groups, or k_bigcol's count)
-// then the block adds the warp counts into the tile count U (decoupled
-// look-back aggregate), finishes the PREVIOUS tile (block-wide look-back --
-// which had a whole tile of time to resolve -- and coalesced ir/pr/jc
-// writes), and each warp
-//   (7) folds every group from +0.0 in input order (the reference's scatter
-//       contract, _kernels.pyx:82-89; x86 NaN rule) and places it by row
-//       inside its column, staging (row-1, value) in CSC order.
+// order; a tile's records arrive by one TMA bulk copy issued a tile ahead.
+// Each warp folds the columns starting in its window, warp-synchronously:
+//   A  one pass over its records: column slot (max-scan of head marks),
+//      (slot,row) -> group via a warp-private shared-memory hash (group ids
+//      by ballot), arrival rank inside the group by match.any in position
+//      order (deterministic, no atomics)
+//   B  warp scans: group offsets, column offsets
+//   C  group-major member list (input position, value)
+//   D  members ranked by input position inside their group
+// the block then adds the warp counts into the tile count U (decoupled
+// look-back aggregate) and finishes the PREVIOUS tile (warp-0 look-back,
+// which had a whole tile of time to resolve; coalesced ir/pr; jc per warp);
+// then each warp
+//   E  folds every group from +0.0 in input order (the reference's scatter
+//      contract, _kernels.pyx:82-89; x86 NaN rule) and places it by row
+//      inside its column, staging (row-1, value) in CSC order.
 // Tiles holding a big column (folded by k_bigcol) write straight to global
 // memory after an inline look-back.
 
@@ -40,26 +39,27 @@ constexpr int WSTRIDE = WIN + 1;  // per-warp column slots + sentinel
 struct TileSmem {
     int4 rec[2][TCAP];                 // double-buffered records (TMA destination)
     unsigned long long mbar[2];
-    int col[TCAP];                     // column heads -> column slot + 1
     // One 16-byte cell per record position k of the owning warp's range:
-    // first hash slots 2k, 2k+1; after the hash is dead, per-index fields.
+    // first hash slots 2k, 2k+1; after the hash is dead, group-major fields.
     union HCell {
         unsigned long long key[2];
         struct {
-            double sval;               // group-major values ordered by input position
-            int midx;                  // group-major member input positions
-            int g_base;                // group offset (index qa + gid)
+            double sval;               // values ordered by input position
+            int midx;                  // member input positions (arrival order)
+            int pad;
         } o;
     } hc[TCAP];
-    double mval[TCAP];                 // group-major member values (arrival order)
+    double mval[TCAP];                 // member values (arrival order)
+    int ga[TCAP];                      // per record: gid << 16 | arrival rank
     int crow[TCAP];                    // rows of a column's groups (column-major)
+    int g_row[TCAP];                   // per group (index qa + gid)
     int16_t hgid[2 * TCAP];
-    int g_cnt[TCAP];                   // per group (index qa + gid)
-    int16_t g_first[TCAP];
+    int16_t col[TCAP];                 // column heads -> column slot + 1
+    int16_t g_cnt[TCAP];
+    int16_t g_base[TCAP];
+    int16_t g_slot[TCAP];
     int16_t g_crank[TCAP];
-    int16_t r_gid[TCAP];               // per record
-    int16_t r_arr[TCAP];
-    int ci_c[TILE];                    // per column slot (warp w: slots [w*WIN, w*WIN+WIN))
+    int ci_c[TILE];                    // per column slot (warp w: [w*WIN, w*WIN+WIN))
     int ci_q[TILE];
     int ci_n[TILE];                    // small record count (0 for a big placeholder)
     int ci_u[TILE];                    // groups, or k_bigcol's unique count
@@ -69,9 +69,10 @@ struct TileSmem {
     int w_u[NW];
     int st_row[TCAP];                  // staged outputs of the pending tile
     double st_val[TCAP];
-    int warp_tmp[NW];
-    long long red_ll[NW];
     int pre_n[2];
+    int U_cur;
+    long long P_bc;
+    long long P_big;
     long long next_tile;
     long long p_tile;
     int p_U;
@@ -130,45 +131,32 @@ __device__ __forceinline__ int warp_incl_max(int x) {
     return x;
 }
 
-// Block-wide decoupled look-back: exclusive prefix of tile b, then publish
-// b's inclusive prefix.  NT predecessors per L2 round trip.  All threads.
-__device__ long long lookback_block(unsigned long long *st, long long b, unsigned long long agg,
-                                   TileSmem &S) {
-    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+// Warp-level decoupled look-back (32 predecessors per L2 round trip):
+// exclusive prefix of tile b; publishes b's inclusive prefix.
+__device__ long long lookback_warp32(unsigned long long *st, long long b, unsigned long long agg) {
+    const int lane = threadIdx.x & 31;
     volatile unsigned long long *vst = st;
-    long long excl = 0;
+    unsigned long long excl = 0;
     long long base = b - 1;
     while (base >= 0) {
-        const long long idx = base - tid;
-        const unsigned long long word = (idx >= 0) ? vst[idx] : lb_pack(2, 0);
-        const unsigned flag = (unsigned)(word >> 62);
-        if (__syncthreads_or(flag == 0)) continue;
-        int stop = (flag == 2) ? tid : NT;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) stop = min(stop, __shfl_xor_sync(FULL, stop, o));
-        if (lane == 0) S.warp_tmp[w] = stop;
-        __syncthreads();
-        stop = NT;
-#pragma unroll
-        for (int k = 0; k < NW; ++k) stop = min(stop, S.warp_tmp[k]);
-        long long v = (tid <= stop) ? (long long)(word & LB_VALMASK) : 0;
+        const long long idx = base - lane;
+        const unsigned long long w = (idx >= 0) ? vst[idx] : lb_pack(2, 0);
+        const unsigned flag = (unsigned)(w >> 62);
+        if (__any_sync(FULL, flag == 0)) continue;
+        const unsigned pm = __ballot_sync(FULL, flag == 2);
+        const int stop = pm ? (__ffs(pm) - 1) : 31;
+        unsigned long long v = (lane <= stop) ? (w & LB_VALMASK) : 0ull;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
-        if (lane == 0) S.red_ll[w] = v;
-        __syncthreads();
-        long long sum = 0;
-#pragma unroll
-        for (int k = 0; k < NW; ++k) sum += S.red_ll[k];
-        excl += sum;
-        __syncthreads();
-        if (stop < NT) break;
-        base -= NT;
+        excl += v;
+        if (pm) break;
+        base -= 32;
     }
-    if (tid == 0) {
+    if (lane == 0) {
         __threadfence();
-        vst[b] = lb_pack(2, (unsigned long long)excl + agg);
+        vst[b] = lb_pack(2, excl + agg);
     }
-    return excl;
+    return (long long)excl;
 }
 
 __device__ __forceinline__ int tile_r0(const uint32_t *sstart, const int32_t *win_first,
@@ -193,7 +181,7 @@ __device__ void prefetch_tile(TileSmem &S, int buf, long long t, long long ntile
     }
 }
 
-// jc of one warp's columns: jc[c] = P + wbase + cib[first non-empty column >= c]
+// jc of one warp's columns: jc[c] = P + cib[first non-empty column >= c]
 __device__ void warp_write_jc(const uint32_t *sstart, int c_lo, int c_hi, const int *cibw,
                               long long Pw, int32_t *jc) {
     const int lane = threadIdx.x & 31;
@@ -208,6 +196,37 @@ __device__ void warp_write_jc(const uint32_t *sstart, int c_lo, int c_hi, const 
         if (in) jc[c] = (int32_t)(Pw + cibw[k0 + __popc(m & lt)]);
         k0 += __popc(m);
     }
+}
+
+// Finish a staged tile: look-back (warp 0), coalesced ir/pr, jc per warp.
+__device__ void finish_staged(TileSmem &S, unsigned long long *tile_state, long long ntiles,
+                              const uint32_t *sstart, const int32_t *win_first, int32_t N,
+                              int32_t *jc, int32_t *ir, double *pr, int64_t cap, ErrState *err,
+                              int pb) {
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const long long pt = S.p_tile;
+    const int pU = S.p_U;
+    if (warp == 0) {
+        const long long P = lookback_warp32(tile_state, pt, (unsigned long long)pU);
+        if (tid == 0) S.P_bc = P;
+    }
+    __syncthreads();
+    const long long P = S.P_bc;
+    for (int k = tid; k < pU; k += NT) {
+        const long long o = P + k;
+        if (o < cap) {
+            ir[o] = S.st_row[k];
+            pr[o] = S.st_val[k];
+        }
+    }
+    const int pgw = (int)(pt * NW) + warp;
+    warp_write_jc(sstart, win_first[pgw], win_first[pgw + 1], &S.cib[pb][warp * WSTRIDE],
+                  P + S.w_base[pb][warp], jc);
+    if (pt == ntiles - 1 && tid == 0) {
+        jc[N] = (int32_t)(P + pU);
+        err->nnz = P + pU;
+    }
+    if (tid == 0 && P + pU > cap) atomicExch(&err->cap_exceeded, 1u);
 }
 
 }  // namespace
@@ -255,7 +274,7 @@ __global__ void __launch_bounds__(NT, 2) k_tile_fold(const uint32_t *__restrict_
         const int slot0 = warp * WIN;
         int *cibw = &S.cib[cb2][warp * WSTRIDE];
 
-        // ---- (1) the warp's non-empty columns ----------------------------------
+        // ---- the warp's non-empty columns (lanes over columns) ------------------
         int ncw = 0;
         for (int cb = c_lo; cb < c_hi; cb += 32) {
             const int c = cb + lane;
@@ -266,13 +285,13 @@ __global__ void __launch_bounds__(NT, 2) k_tile_fold(const uint32_t *__restrict_
                 w1 = sstart[c + 1];
             }
             const int s0 = (int)(w0 & POSMASK), s1 = (int)(w1 & POSMASK);
-            const bool big = (w0 & BIGFLAG) != 0;
             const bool ne = in && s1 > s0;
             const unsigned m = __ballot_sync(FULL, ne);
             if (ne) {
                 const int k = ncw + __popc(m & lt);
                 if (k < WIN) {
                     const int sl = slot0 + k;
+                    const bool big = (w0 & BIGFLAG) != 0;
                     S.ci_c[sl] = c;
                     S.ci_q[sl] = s0 - r0;
                     S.ci_n[sl] = big ? 0 : s1 - s0;
@@ -284,16 +303,20 @@ __global__ void __launch_bounds__(NT, 2) k_tile_fold(const uint32_t *__restrict_
             ncw += __popc(m);
         }
         ncw = min(ncw, WIN);
-        const int qa = ncw ? S.ci_q[slot0] : 0;
-        int qb = qa;
-        if (ncw) qb = (int)(sstart[c_hi] & POSMASK) - r0;
+        int qa = 0, qb = 0;
+        if (ncw) {
+            qa = (int)(sstart[c_lo] & POSMASK) - r0;
+            qb = (int)(sstart[c_hi] & POSMASK) - r0;
+        }
+        for (int p = qa + lane; p < qb; p += 32) {
+            S.col[p] = 0;
+            S.hc[p].key[0] = 0ull;
+            S.hc[p].key[1] = 0ull;
+        }
         __syncwarp();
-        // head marks (cleared over the warp's range first)
-        for (int p = qa + lane; p < qb; p += 32) S.col[p] = 0;
-        __syncwarp();
-        for (int k = lane; k < ncw; k += 32) S.col[S.ci_q[slot0 + k]] = slot0 + k + 1;
+        for (int k = lane; k < ncw; k += 32) S.col[S.ci_q[slot0 + k]] = (int16_t)(slot0 + k + 1);
 
-        // ---- records: TMA (or synchronous) -------------------------------------
+        // ---- records arrive (TMA) ------------------------------------------------
         int4 *R = S.rec[buf];
         const int pn = S.pre_n[buf];
         if (pn > 0) {
@@ -304,45 +327,25 @@ __global__ void __launch_bounds__(NT, 2) k_tile_fold(const uint32_t *__restrict_
                 mbar_wait(&S.mbar[1], phase1);
                 phase1 ^= 1u;
             }
-        } else if (pn < 0) {
-            // tile too large for one copy (cannot happen: small columns only)
-            if (tid == 0) atomicExch(&err->internal, 1u);
+        } else if (pn < 0 && tid == 0) {
+            atomicExch(&err->internal, 1u);  // cannot happen: tiles hold small columns only
         }
         __syncwarp();
 
-        // column slot of each record: max-scan of the head marks
-        {
-            int carry = 0;
-            for (int p0 = qa; p0 < qb; p0 += 32) {
-                const int p = p0 + lane;
-                const int v = (p < qb) ? S.col[p] : 0;
-                const int m = max(warp_incl_max(v), carry);
-                if (p < qb) S.col[p] = m;
-                carry = __shfl_sync(FULL, m, 31);
-            }
-        }
-        for (int k = qa + lane; k < qb; k += 32) {
-            S.hc[k].key[0] = 0ull;
-            S.hc[k].key[1] = 0ull;
-            S.g_cnt[k] = 0;
-        }
-        __syncwarp();
-
-        // ---- (2) (column,row) groups --------------------------------------------
+        // ---- A: slot, group, arrival rank (one pass, position order) -------------
         const int hb = 2 * qa, hn = 2 * (qb - qa);
-        int ng = 0;
+        int ng = 0, carry = 0;
         for (int p0 = qa; p0 < qb; p0 += 32) {
             const int p = p0 + lane;
-            bool act = p < qb;
-            int sl = 0;
-            if (act) {
-                sl = S.col[p] - 1;
-                act = S.ci_n[sl] > 0;  // skip big-column placeholders
-            }
+            const bool inr = p < qb;
+            const int hm = inr ? (int)S.col[p] : 0;
+            const int sl = max(warp_incl_max(hm), carry) - 1;
+            carry = __shfl_sync(FULL, sl + 1, 31);
+            const bool act = inr && S.ci_n[sl] > 0;  // skip big placeholders
+            int row = 0, h = -1;
             bool leader = false;
-            int h = 0;
             if (act) {
-                const int row = R[p].x;
+                row = R[p].x;
                 const unsigned long long key = ((unsigned long long)(unsigned)sl << 32) | (unsigned)row;
                 const unsigned hk = (unsigned)((key * 0x9E3779B97F4A7C15ull) >> 32);
                 h = hb + (int)(((unsigned long long)hk * (unsigned)hn) >> 32);
@@ -357,47 +360,41 @@ __global__ void __launch_bounds__(NT, 2) k_tile_fold(const uint32_t *__restrict_
             if (leader) {
                 const int g = ng + __popc(lm & lt);
                 S.hgid[h] = (int16_t)g;
-                S.g_first[qa + g] = (int16_t)p;
+                S.g_row[qa + g] = row;
+                S.g_slot[qa + g] = (int16_t)sl;
+                S.g_cnt[qa + g] = 0;
                 S.g_crank[qa + g] = (int16_t)atomicAdd(&S.ci_u[sl], 1);
             }
-            if (p < qb) S.r_gid[p] = act ? (int16_t)h : (int16_t)-1;
             ng += __popc(lm);
-        }
-        __syncwarp();
-        // ---- (3) group of each record, arrival rank ------------------------------
-        for (int p = qa + lane; p < qb; p += 32) {
-            const int h = S.r_gid[p];
-            if (h >= 0) {
-                const int g = S.hgid[h];
-                S.r_gid[p] = (int16_t)g;
-                S.r_arr[p] = (int16_t)atomicAdd(&S.g_cnt[qa + g], 1);
+            __syncwarp();
+            const int g = act ? (int)S.hgid[h] : -1 - lane;  // unique dummy keys for idle lanes
+            const unsigned peers = __match_any_sync(FULL, g);
+            const int before = act ? (int)S.g_cnt[qa + g] : 0;
+            __syncwarp();
+            if (act) {
+                const int arr = before + __popc(peers & lt);
+                S.ga[p] = (g << 16) | arr;
+                if ((peers & lt) == 0) S.g_cnt[qa + g] = (int16_t)(before + __popc(peers));
+            } else if (inr) {
+                S.ga[p] = -1;
             }
+            __syncwarp();
         }
-        __syncwarp();
-        // group offsets (relative to qa); hash cells are dead from here on
+
+        // ---- B: group offsets, column offsets -------------------------------------
         {
-            int carry = 0;
-            for (int p0 = qa; p0 < qa + ng; p0 += 32) {
-                const int p = p0 + lane;
-                const int v = (p < qa + ng) ? S.g_cnt[p] : 0;
+            int gc = 0;
+            for (int g0 = 0; g0 < ng; g0 += 32) {
+                const int g = g0 + lane;
+                const int v = (g < ng) ? (int)S.g_cnt[qa + g] : 0;
                 const int inc = warp_incl_sum(v);
-                if (p < qa + ng) S.hc[p].o.g_base = carry + inc - v;
-                carry += __shfl_sync(FULL, inc, 31);
+                if (g < ng) S.g_base[qa + g] = (int16_t)(gc + inc - v);
+                gc += __shfl_sync(FULL, inc, 31);
             }
-        }
-        __syncwarp();
-        // ---- (4) group-major member list; (6) column offsets -------------------
-        for (int p = qa + lane; p < qb; p += 32) {
-            if (S.r_gid[p] < 0 || S.ci_n[S.col[p] - 1] == 0) continue;
-            const int g = S.r_gid[p];
-            const int j = qa + S.hc[qa + g].o.g_base + S.r_arr[p];
-            const int4 r = R[p];
-            S.hc[j].o.midx = r.y;
-            S.mval[j] = __hiloint2double(r.w, r.z);
         }
         int Uw = 0;
         {
-            int carry = 0, gcarry = 0;
+            int cc = 0, gcc = 0;
             for (int k0 = 0; k0 < ncw; k0 += 32) {
                 const int k = k0 + lane;
                 const int u = (k < ncw) ? S.ci_u[slot0 + k] : 0;
@@ -405,32 +402,42 @@ __global__ void __launch_bounds__(NT, 2) k_tile_fold(const uint32_t *__restrict_
                 const int inc = warp_incl_sum(u);
                 const int ginc = warp_incl_sum(gu);
                 if (k < ncw) {
-                    cibw[k] = carry + inc - u;
-                    S.cg_base[slot0 + k] = gcarry + ginc - gu;
+                    cibw[k] = cc + inc - u;
+                    S.cg_base[slot0 + k] = gcc + ginc - gu;
                 }
-                carry += __shfl_sync(FULL, inc, 31);
-                gcarry += __shfl_sync(FULL, ginc, 31);
+                cc += __shfl_sync(FULL, inc, 31);
+                gcc += __shfl_sync(FULL, ginc, 31);
             }
-            Uw = carry;
+            Uw = cc;
             if (lane == 0) cibw[ncw] = Uw;
         }
         __syncwarp();
-        // group rows listed per column (for the row order inside a column)
-        for (int g = lane; g < ng; g += 32) {
-            const int p = S.g_first[qa + g];
-            const int sl = S.col[p] - 1;
-            S.crow[qa + S.cg_base[sl] + S.g_crank[qa + g]] = R[p].x;
-        }
-        // ---- (5) members ranked by input position inside their group ----------
+        // ---- C: group-major members; group rows per column ---------------------
         for (int p = qa + lane; p < qb; p += 32) {
-            if (S.r_gid[p] < 0 || S.ci_n[S.col[p] - 1] == 0) continue;
-            const int g = S.r_gid[p];
-            const int base = qa + S.hc[qa + g].o.g_base;
+            const int ga = S.ga[p];
+            if (ga < 0) continue;
+            const int g = ga >> 16;
+            const int j = qa + S.g_base[qa + g] + (ga & 0xffff);
+            const int4 r = R[p];
+            S.hc[j].o.midx = r.y;
+            S.mval[j] = __hiloint2double(r.w, r.z);
+        }
+        for (int g = lane; g < ng; g += 32)
+            S.crow[qa + S.cg_base[S.g_slot[qa + g]] + S.g_crank[qa + g]] = S.g_row[qa + g];
+        __syncwarp();
+        // ---- D: members ranked by input position inside their group -------------
+        for (int p = qa + lane; p < qb; p += 32) {
+            const int ga = S.ga[p];
+            if (ga < 0) continue;
+            const int g = ga >> 16;
+            const int base = qa + S.g_base[qa + g];
             const int sz = S.g_cnt[qa + g];
-            const int j = base + S.r_arr[p];
-            const int my = S.hc[j].o.midx;
+            const int j = base + (ga & 0xffff);
             int rank = 0;
-            for (int k = base; k < base + sz; ++k) rank += (S.hc[k].o.midx < my);
+            if (sz > 1) {
+                const int my = S.hc[j].o.midx;
+                for (int k = base; k < base + sz; ++k) rank += (S.hc[k].o.midx < my);
+            }
             S.hc[base + rank].o.sval = S.mval[j];
         }
         if (lane == 0) S.w_u[warp] = Uw;
@@ -446,51 +453,38 @@ __global__ void __launch_bounds__(NT, 2) k_tile_fold(const uint32_t *__restrict_
                 __threadfence();
                 if (b == 0) vst[0] = lb_pack(2, (unsigned long long)inc);
                 else vst[b] = lb_pack(1, (unsigned long long)inc);
-                S.warp_tmp[0] = inc;
+                S.U_cur = inc;
             }
         }
         __syncthreads();
-        const int U = S.warp_tmp[0];
+        const int U = S.U_cur;
         const int wbase = S.w_base[cb2][warp];
-        __syncthreads();
 
         // ---- finish the previous tile -------------------------------------------
         if (pending) {
-            const long long pt = S.p_tile;
-            const int pU = S.p_U;
-            const long long P = lookback_block(tile_state, pt, (unsigned long long)pU, S);
-            for (int k = tid; k < pU; k += NT) {
-                const long long o = P + k;
-                if (o < cap) {
-                    ir[o] = S.st_row[k];
-                    pr[o] = S.st_val[k];
-                }
-            }
-            if (tid == 0 && P + pU > cap) atomicExch(&err->cap_exceeded, 1u);
-            const int pgw = (int)(pt * NW) + warp;
-            warp_write_jc(sstart, win_first[pgw], win_first[pgw + 1],
-                          &S.cib[cb2 ^ 1][warp * WSTRIDE], P + S.w_base[cb2 ^ 1][warp], jc);
-            if (pt == ntiles - 1 && tid == 0) {
-                jc[N] = (int32_t)(P + pU);
-                err->nnz = P + pU;
-            }
+            finish_staged(S, tile_state, ntiles, sstart, win_first, N, jc, ir, pr, cap, err, cb2 ^ 1);
             pending = false;
         }
         long long P = 0;
-        if (has_big) P = lookback_block(tile_state, b, (unsigned long long)U, S);
+        if (has_big) {
+            if (warp == 0) {
+                const long long Pb = lookback_warp32(tile_state, b, (unsigned long long)U);
+                if (tid == 0) S.P_big = Pb;
+            }
+        }
         __syncthreads();
+        if (has_big) P = S.P_big;
 
-        // ---- (7) fold each group in input order, place it by row ----------------
+        // ---- E: fold each group in input order, place it by row ------------------
         bool over = false;
         for (int g = lane; g < ng; g += 32) {
-            const int p0 = S.g_first[qa + g];
-            const int row = R[p0].x;
-            const int sl = S.col[p0] - 1;
+            const int row = S.g_row[qa + g];
+            const int sl = S.g_slot[qa + g];
             const int cl = qa + S.cg_base[sl];
             const int cu = S.ci_u[sl];
             int rank = 0;
             for (int k = cl; k < cl + cu; ++k) rank += (S.crow[k] < row);
-            const int base = qa + S.hc[qa + g].o.g_base;
+            const int base = qa + S.g_base[qa + g];
             const int sz = S.g_cnt[qa + g];
             double acc = 0.0;
             for (int k = base; k < base + sz; ++k) acc = fold_add(acc, S.hc[k].o.sval);
@@ -509,8 +503,7 @@ __global__ void __launch_bounds__(NT, 2) k_tile_fold(const uint32_t *__restrict_
             }
         }
         if (has_big) {
-            // big columns of this warp: copy k_bigcol's results
-            for (int k = 0; k < ncw; ++k) {
+            for (int k = 0; k < ncw; ++k) {  // big columns of this warp: k_bigcol's results
                 const int sl = slot0 + k;
                 if (S.ci_n[sl] != 0) continue;
                 const BigCol bc = big_list[bigk[S.ci_c[sl]]];
@@ -547,26 +540,7 @@ __global__ void __launch_bounds__(NT, 2) k_tile_fold(const uint32_t *__restrict_
         b = S.next_tile;
         buf ^= 1;
     }
-    if (pending) {
-        const long long pt = S.p_tile;
-        const int pU = S.p_U;
-        const long long P = lookback_block(tile_state, pt, (unsigned long long)pU, S);
-        for (int k = tid; k < pU; k += NT) {
-            const long long o = P + k;
-            if (o < cap) {
-                ir[o] = S.st_row[k];
-                pr[o] = S.st_val[k];
-            }
-        }
-        if (tid == 0 && P + pU > cap) atomicExch(&err->cap_exceeded, 1u);
-        const int pgw = (int)(pt * NW) + warp;
-        warp_write_jc(sstart, win_first[pgw], win_first[pgw + 1], &S.cib[cb2 ^ 1][warp * WSTRIDE],
-                      P + S.w_base[cb2 ^ 1][warp], jc);
-        if (pt == ntiles - 1 && tid == 0) {
-            jc[N] = (int32_t)(P + pU);
-            err->nnz = P + pU;
-        }
-    }
+    if (pending) finish_staged(S, tile_state, ntiles, sstart, win_first, N, jc, ir, pr, cap, err, cb2 ^ 1);
 }
 
 cudaError_t launch_tile_fold(Launch &lc, const uint32_t *sstart, const int32_t *win_first,
