@@ -17,13 +17,12 @@ constexpr uint32_t BIGFLAG = 0x80000000u;
 constexpr uint32_t POSMASK = 0x7fffffffu;
 
 // Fold geometry (k_tile_fold).  Tile b owns the columns whose small-space
-// start lies in [b*TILE, (b+1)*TILE); inside the CTA, warp w owns the
+// start lies in [b*TILE, (b+1)*TILE); inside the CTA, thread t owns the
 // columns starting in its WIN-wide sub-window.  A tile holds at most
 // TILE + BIGCOL - 1 small records.
-constexpr int TILE = 512;
-constexpr int TILE_THREADS = 256;
-constexpr int TILE_WARPS = TILE_THREADS / 32;
-constexpr int WIN = TILE / TILE_WARPS;
+constexpr int TILE = 2048;
+constexpr int TILE_THREADS = 128;
+constexpr int WIN = TILE / TILE_THREADS;  // 16 record positions per thread
 constexpr int BIGCOL = 512;
 constexpr int TCAP = TILE + BIGCOL;
 
