@@ -33,15 +33,27 @@ namespace {
 constexpr int NT = TILE_THREADS;
 constexpr int SHORT_COL = 24;
 
+constexpr int NWARP = NT / 32;
+constexpr int LCAP = TILE / (SHORT_COL + 1) + 2;  // long columns per tile
+constexpr int MAXU = 96;                          // distinct rows of a long column (warp table)
+
+struct WarpScratch {
+    uint8_t gid[BIGCOL];               // group (table entry) of each record
+    int16_t arr[BIGCOL];               // arrival rank inside the group
+    int16_t mem[BIGCOL];               // group-major member list (record slots)
+    int gcnt[MAXU];
+    int gbase[MAXU];
+};
+
 struct TileSmem {
     int4 rec[TCAP];                    // the tile's records (TMA destination)
-    int st_row[TCAP];                  // staged outputs in CSC order
-    double st_val[TCAP];
+    WarpScratch ws[NWARP];
+    int lcol[LCAP];                    // long columns: record offset | (count << 16)
     unsigned long long mbar;
-    int warp_u[NT / 32];
+    int nlong;
+    int warp_u[NWARP];
     long long tile;
     long long P;
-    int U;
 };
 
 __device__ __forceinline__ unsigned smem_u32(const void *p) {
@@ -73,9 +85,12 @@ __device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned pari
     }
 }
 
-// (row, position) order of two records
+// (row, position) order of two records (both non-negative int32)
+__device__ __forceinline__ unsigned long long rec_key(const int4 &a) {
+    return ((unsigned long long)(unsigned)a.x << 32) | (unsigned)a.y;
+}
 __device__ __forceinline__ bool rec_less(const int4 &a, const int4 &b) {
-    return (a.x < b.x) || (a.x == b.x && a.y < b.y);
+    return rec_key(a) < rec_key(b);
 }
 
 __device__ __forceinline__ double rec_val(const int4 &r) { return __hiloint2double(r.w, r.z); }
@@ -146,6 +161,133 @@ __device__ int fold_column(int4 *R, int c) {
     return u;
 }
 
+__device__ __forceinline__ int warp_incl_sum(int x) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(FULL, x, o);
+        if (lane >= o) x += y;
+    }
+    return x;
+}
+
+__device__ __forceinline__ int tab_get(const int (&tab)[3], int k) {
+    return (k == 0) ? tab[0] : ((k == 1) ? tab[1] : tab[2]);
+}
+
+// Warp-cooperative fold of one column with c > SHORT_COL records (all 32
+// lanes call it; returns u, warp-uniform).  Lanes hold a table of the
+// column's distinct rows (entry t in lane t%32); each batch of 32 records
+// looks its rows up by shuffles, appends new rows, and takes arrival ranks
+// in position order (match.any; deterministic).  Then per group (lane per
+// group): members ordered by input position, folded from +0.0, placed by row.
+// More than MAXU distinct rows: lane 0 folds the column alone.
+__device__ int fold_column_warp(int4 *R, int c, WarpScratch &W) {
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = lanemask_lt();
+    int tab[3] = {0, 0, 0};
+    int u = 0;
+    bool overflow = false;
+    for (int t = lane; t < MAXU; t += 32) W.gcnt[t] = 0;
+    __syncwarp();
+    for (int b0 = 0; b0 < c && !overflow; b0 += 32) {
+        const int i = b0 + lane;
+        const bool act = i < c;
+        const int r = act ? R[i].x : -1;
+        int gid = -1;
+        for (int t = 0; t < u; ++t) {
+            const int rt = __shfl_sync(FULL, tab_get(tab, t >> 5), t & 31);
+            if (r == rt) gid = t;
+        }
+        unsigned miss = __ballot_sync(FULL, act && gid < 0);
+        while (miss) {
+            if (u >= MAXU) {
+                overflow = true;
+                break;
+            }
+            const int rl = __shfl_sync(FULL, r, __ffs(miss) - 1);
+            if (act && gid < 0 && r == rl) gid = u;
+            if (lane == (u & 31)) {
+                const int k = u >> 5;
+                if (k == 0) tab[0] = rl;
+                else if (k == 1) tab[1] = rl;
+                else tab[2] = rl;
+            }
+            ++u;
+            miss = __ballot_sync(FULL, act && gid < 0);
+        }
+        if (overflow) break;
+        const unsigned peers = __match_any_sync(FULL, act ? gid : -1 - lane);
+        const int leader = __ffs(peers) - 1;
+        int base = 0;
+        if (act && lane == leader) base = atomicAdd(&W.gcnt[gid], __popc(peers));
+        base = __shfl_sync(FULL, base, leader);
+        if (act) {
+            W.gid[i] = (uint8_t)gid;
+            W.arr[i] = (int16_t)(base + __popc(peers & lt));
+        }
+    }
+    if (overflow) {
+        int uu = 0;
+        if (lane == 0) uu = fold_column(R, c);
+        __syncwarp();
+        return __shfl_sync(FULL, uu, 0);
+    }
+    __syncwarp();
+    {
+        int carry = 0;
+        for (int t0 = 0; t0 < u; t0 += 32) {
+            const int t = t0 + lane;
+            const int v = (t < u) ? W.gcnt[t] : 0;
+            const int inc = warp_incl_sum(v);
+            if (t < u) W.gbase[t] = carry + inc - v;
+            carry += __shfl_sync(FULL, inc, 31);
+        }
+    }
+    __syncwarp();
+    for (int i = lane; i < c; i += 32) W.mem[W.gbase[W.gid[i]] + W.arr[i]] = (int16_t)i;
+    __syncwarp();
+    double acc[3] = {0.0, 0.0, 0.0};
+    int rank[3] = {0, 0, 0};
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const int t = lane + 32 * k;
+        if (t < u) {
+            const int base = W.gbase[t], g = W.gcnt[t];
+            for (int a = base + 1; a < base + g; ++a) {
+                const int sl = W.mem[a];
+                const int key = R[sl].y;
+                int bb = a;
+                while (bb > base) {
+                    const int prev = W.mem[bb - 1];
+                    if (R[prev].y < key) break;
+                    W.mem[bb] = (int16_t)prev;
+                    --bb;
+                }
+                W.mem[bb] = (int16_t)sl;
+            }
+            double s = 0.0;
+            for (int a = base; a < base + g; ++a) s = fold_add(s, rec_val(R[W.mem[a]]));
+            acc[k] = s;
+        }
+    }
+    for (int t2 = 0; t2 < u; ++t2) {
+        const int rt = __shfl_sync(FULL, tab_get(tab, t2 >> 5), t2 & 31);
+#pragma unroll
+        for (int k = 0; k < 3; ++k) rank[k] += (rt < tab[k]);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const int t = lane + 32 * k;
+        if (t < u) R[rank[k]] = make_int4(tab[k] - 1, 0, __double2loint(acc[k]), __double2hiint(acc[k]));
+    }
+    __syncwarp();
+    if (lane == 0) R[0].y = u;
+    __syncwarp();
+    return u;
+}
+
 // Warp-level decoupled look-back (32 predecessors per L2 round trip).
 __device__ long long lookback_warp32(unsigned long long *st, long long b, unsigned long long agg) {
     const int lane = threadIdx.x & 31;
@@ -203,6 +345,7 @@ __global__ void __launch_bounds__(NT) k_tile_fold(const uint32_t *__restrict__ s
 
     if (tid == 0) {
         S.tile = atomicAdd(&err->tile_ticket, 1u);
+        S.nlong = 0;
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&S.mbar)) : "memory");
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -215,34 +358,52 @@ __global__ void __launch_bounds__(NT) k_tile_fold(const uint32_t *__restrict__ s
         if (n > 0 && n <= TCAP) tma_load(S.rec, rec + r0, (unsigned)n * 16u, &S.mbar);
         else if (n > TCAP) atomicExch(&err->internal, 1u);
     }
-    const bool has_big = tile_big[b] != 0;
     const int c_lo = win_first[b * NT + tid], c_hi = win_first[b * NT + tid + 1];
     if (n > 0 && n <= TCAP) mbar_wait(&S.mbar, 0u);
+    const bool staged = n <= TCAP;
 
-    // ---- fold this thread's columns -------------------------------------------
+    // ---- pass 1: each thread folds its short columns; long ones are listed -------
+    if (staged) {
+        for (int c = c_lo; c < c_hi; ++c) {
+            const uint32_t w0 = sstart[c];
+            if (w0 & BIGFLAG) continue;
+            const int s0 = (int)(w0 & POSMASK), s1 = (int)(sstart[c + 1] & POSMASK);
+            const int cnt = s1 - s0;
+            if (cnt <= 0) continue;
+            if (cnt <= SHORT_COL) {
+                fold_column(&S.rec[s0 - r0], cnt);
+            } else {
+                const int e = atomicAdd(&S.nlong, 1);
+                if (e < LCAP) S.lcol[e] = (s0 - r0) | (cnt << 16);
+                else atomicExch(&err->internal, 1u);
+            }
+        }
+    }
+    __syncthreads();
+    // ---- pass 2: warps fold the long columns --------------------------------------
+    {
+        const int nl = min(S.nlong, LCAP);
+        for (int e = warp; e < nl; e += NWARP) {
+            const int v = S.lcol[e];
+            fold_column_warp(&S.rec[v & 0xffff], v >> 16, S.ws[warp]);
+        }
+    }
+    __syncthreads();
+
+    // ---- tile count, thread output bases, look-back --------------------------------
     int ut = 0;
     for (int c = c_lo; c < c_hi; ++c) {
         const uint32_t w0 = sstart[c];
         const int s0 = (int)(w0 & POSMASK), s1 = (int)(sstart[c + 1] & POSMASK);
-        if (w0 & BIGFLAG) {
-            ut += (int)(big_list[bigk[c]].u & POSMASK);
-        } else if (s1 > s0 && n <= TCAP) {
-            ut += fold_column(&S.rec[s0 - r0], s1 - s0);
-        }
+        if (w0 & BIGFLAG) ut += (int)(big_list[bigk[c]].u & POSMASK);
+        else if (s1 > s0 && staged) ut += S.rec[s0 - r0].y;
     }
-
-    // ---- tile count, thread output bases, look-back -------------------------------
-    int inc = ut;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(FULL, inc, o);
-        if (lane >= o) inc += y;
-    }
+    const int inc = warp_incl_sum(ut);
     if (lane == 31) S.warp_u[warp] = inc;
     __syncthreads();
     int wpre = 0, U = 0;
 #pragma unroll
-    for (int k = 0; k < NT / 32; ++k) {
+    for (int k = 0; k < NWARP; ++k) {
         const int v = S.warp_u[k];
         if (k < warp) wpre += v;
         U += v;
@@ -252,85 +413,47 @@ __global__ void __launch_bounds__(NT) k_tile_fold(const uint32_t *__restrict__ s
         const long long P = lookback_warp32(tile_state, b, (unsigned long long)U);
         if (lane == 0) S.P = P;
     }
-    // ---- stage (or, with a big column, write) the outputs in CSC order ---------
-    if (!has_big) {
-        int o = tbase;
-        for (int c = c_lo; c < c_hi; ++c) {
-            const int s0 = (int)(sstart[c] & POSMASK), s1 = (int)(sstart[c + 1] & POSMASK);
-            if (s1 <= s0) continue;
+    __syncthreads();
+    const long long P = S.P;
+
+    // ---- outputs (each thread: its columns, contiguous) and column pointers --------
+    bool over = false;
+    long long o = P + tbase;
+    for (int c = c_lo; c < c_hi; ++c) {
+        jc[c] = (int32_t)o;
+        const uint32_t w0 = sstart[c];
+        const int s0 = (int)(w0 & POSMASK), s1 = (int)(sstart[c + 1] & POSMASK);
+        if (w0 & BIGFLAG) {
+            const BigCol bc = big_list[bigk[c]];
+            const int ub = (int)(bc.u & POSMASK);
+            const unsigned long long *RR = reinterpret_cast<const unsigned long long *>(rec + bc.start);
+            const unsigned long long *K = (bc.u & BIGFLAG) ? RR + bc.n : RR;
+            const unsigned long long *V = (bc.u & BIGFLAG) ? RR : RR + bc.n;
+            for (int e = 0; e < ub; ++e) {
+                if (o + e < cap) {
+                    ir[o + e] = (int32_t)K[e];
+                    pr[o + e] = __longlong_as_double((long long)V[e]);
+                } else {
+                    over = true;
+                }
+            }
+            o += ub;
+        } else if (s1 > s0 && staged) {
             const int4 *R = &S.rec[s0 - r0];
             const int u = R[0].y;
             for (int k = 0; k < u; ++k) {
                 const int4 r = R[k];
-                S.st_row[o + k] = r.x;
-                S.st_val[o + k] = rec_val(r);
+                if (o + k < cap) {
+                    ir[o + k] = r.x;
+                    pr[o + k] = rec_val(r);
+                } else {
+                    over = true;
+                }
             }
             o += u;
         }
     }
-    __syncthreads();
-    const long long P = S.P;
-    bool over = false;
-    if (!has_big) {
-        for (int k = tid; k < U; k += NT) {
-            const long long go = P + k;
-            if (go < cap) {
-                ir[go] = S.st_row[k];
-                pr[go] = S.st_val[k];
-            } else {
-                over = true;
-            }
-        }
-    } else {
-        int o = tbase;
-        for (int c = c_lo; c < c_hi; ++c) {
-            const uint32_t w0 = sstart[c];
-            const int s0 = (int)(w0 & POSMASK), s1 = (int)(sstart[c + 1] & POSMASK);
-            if (w0 & BIGFLAG) {
-                const BigCol bc = big_list[bigk[c]];
-                const int ub = (int)(bc.u & POSMASK);
-                const unsigned long long *RR = reinterpret_cast<const unsigned long long *>(rec + bc.start);
-                const unsigned long long *K = (bc.u & BIGFLAG) ? RR + bc.n : RR;
-                const unsigned long long *V = (bc.u & BIGFLAG) ? RR : RR + bc.n;
-                for (int e = 0; e < ub; ++e) {
-                    const long long go = P + o + e;
-                    if (go < cap) {
-                        ir[go] = (int32_t)K[e];
-                        pr[go] = __longlong_as_double((long long)V[e]);
-                    } else {
-                        over = true;
-                    }
-                }
-                o += ub;
-            } else if (s1 > s0) {
-                const int4 *R = &S.rec[s0 - r0];
-                const int u = R[0].y;
-                for (int k = 0; k < u; ++k) {
-                    const int4 r = R[k];
-                    const long long go = P + o + k;
-                    if (go < cap) {
-                        ir[go] = r.x;
-                        pr[go] = rec_val(r);
-                    } else {
-                        over = true;
-                    }
-                }
-                o += u;
-            }
-        }
-    }
     if (over) atomicExch(&err->cap_exceeded, 1u);
-    // ---- column pointers of this thread's columns -------------------------------------
-    {
-        long long o = P + tbase;
-        for (int c = c_lo; c < c_hi; ++c) {
-            jc[c] = (int32_t)o;
-            const uint32_t w0 = sstart[c];
-            const int s0 = (int)(w0 & POSMASK), s1 = (int)(sstart[c + 1] & POSMASK);
-            if (w0 & BIGFLAG) o += (int)(big_list[bigk[c]].u & POSMASK);
-            else if (s1 > s0) o += S.rec[s0 - r0].y;
-        }
-    }
     if (b == ntiles - 1 && tid == 0) {
         jc[N] = (int32_t)(P + U);
         err->nnz = P + U;
