@@ -247,6 +247,44 @@ __device__ int fold_column_warp(int4 *R, int c, WarpScratch &W) {
     __syncwarp();
     for (int i = lane; i < c; i += 32) W.mem[W.gbase[W.gid[i]] + W.arr[i]] = (int16_t)i;
     __syncwarp();
+    // rank of every record inside its group by input position:
+    // small groups -- each record compares against its group's members
+    for (int i = lane; i < c; i += 32) {
+        const int t = W.gid[i];
+        const int g = W.gcnt[t];
+        if (g > 8) continue;
+        int rank = 0;
+        if (g > 1) {
+            const int base = W.gbase[t], my = R[i].y;
+            for (int k = 0; k < g; ++k) rank += (R[W.mem[base + k]].y < my);
+        }
+        W.arr[i] = (int16_t)rank;
+    }
+    // large groups -- the whole warp, member positions exchanged by shuffles
+    for (int t = 0; t < u; ++t) {
+        const int g = W.gcnt[t];
+        if (g <= 8) continue;
+        const int base = W.gbase[t];
+        if (g <= 32) {
+            const int sl = (lane < g) ? (int)W.mem[base + lane] : 0;
+            const int my = (lane < g) ? R[sl].y : 0x7fffffff;
+            int rank = 0;
+            for (int m = 0; m < g; ++m) rank += (__shfl_sync(FULL, my, m) < my);
+            if (lane < g) W.arr[sl] = (int16_t)rank;
+        } else {
+            for (int k = lane; k < g; k += 32) {
+                const int sl = W.mem[base + k];
+                const int my = R[sl].y;
+                int rank = 0;
+                for (int m = 0; m < g; ++m) rank += (R[W.mem[base + m]].y < my);
+                W.arr[sl] = (int16_t)rank;
+            }
+        }
+    }
+    __syncwarp();
+    // group-major list in input-position order
+    for (int i = lane; i < c; i += 32) W.mem[W.gbase[W.gid[i]] + W.arr[i]] = (int16_t)i;
+    __syncwarp();
     double acc[3] = {0.0, 0.0, 0.0};
     int rank[3] = {0, 0, 0};
 #pragma unroll
@@ -254,21 +292,9 @@ __device__ int fold_column_warp(int4 *R, int c, WarpScratch &W) {
         const int t = lane + 32 * k;
         if (t < u) {
             const int base = W.gbase[t], g = W.gcnt[t];
-            for (int a = base + 1; a < base + g; ++a) {
-                const int sl = W.mem[a];
-                const int key = R[sl].y;
-                int bb = a;
-                while (bb > base) {
-                    const int prev = W.mem[bb - 1];
-                    if (R[prev].y < key) break;
-                    W.mem[bb] = (int16_t)prev;
-                    --bb;
-                }
-                W.mem[bb] = (int16_t)sl;
-            }
-            double s = 0.0;
-            for (int a = base; a < base + g; ++a) s = fold_add(s, rec_val(R[W.mem[a]]));
-            acc[k] = s;
+            double sacc = 0.0;
+            for (int a = base; a < base + g; ++a) sacc = fold_add(sacc, rec_val(R[W.mem[a]]));
+            acc[k] = sacc;
         }
     }
     for (int t2 = 0; t2 < u; ++t2) {
