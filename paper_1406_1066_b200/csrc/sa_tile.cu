@@ -47,8 +47,6 @@ struct WarpScratch {
 
 struct TileSmem {
     int4 rec[TCAP];                    // the tile's records (TMA destination)
-    int srow[TCAP];                    // short columns: rows in sorted order
-    double sval[TCAP];                 // short columns: values in sorted order
     WarpScratch ws[NWARP];
     int lcol[LCAP];                    // long columns: record offset | (count << 16)
     unsigned long long mbar;
@@ -159,56 +157,6 @@ __device__ int fold_column(int4 *R, int c) {
         ++u;
         k += g;
     }
-    R[0].y = u;
-    return u;
-}
-
-// Short column (c <= S records): rank sort with the (row, position) keys in
-// registers -- all S*(S-1)/2 comparisons are independent (ILP, no dependent
-// shared-memory chain) -- then (row, value) scattered into sorted order and
-// folded in one pass.  Outputs compacted in place at R[0..u), R[0].y = u.
-template <int S>
-__device__ int fold_short_rank(int4 *R, int c, int *srow, double *sval) {
-    unsigned long long key[S];
-    int rank[S];
-#pragma unroll
-    for (int s = 0; s < S; ++s) {
-        key[s] = (s < c) ? rec_key(R[s]) : (~0ull - (unsigned long long)(S - s));
-        rank[s] = 0;
-    }
-#pragma unroll
-    for (int i = 0; i < S; ++i) {
-#pragma unroll
-        for (int j = i + 1; j < S; ++j) {
-            const int lt = key[i] < key[j];
-            rank[j] += lt;
-            rank[i] += 1 - lt;
-        }
-    }
-#pragma unroll
-    for (int s = 0; s < S; ++s) {
-        if (s < c) {
-            srow[rank[s]] = R[s].x;
-            sval[rank[s]] = rec_val(R[s]);
-        }
-    }
-    int u = 0;
-    int prev = srow[0];
-    double acc = fold_add(0.0, sval[0]);
-    for (int k = 1; k < c; ++k) {
-        const int row = srow[k];
-        const double v = sval[k];
-        if (row != prev) {
-            R[u] = make_int4(prev - 1, 0, __double2loint(acc), __double2hiint(acc));
-            ++u;
-            prev = row;
-            acc = fold_add(0.0, v);
-        } else {
-            acc = fold_add(acc, v);
-        }
-    }
-    R[u] = make_int4(prev - 1, 0, __double2loint(acc), __double2hiint(acc));
-    ++u;
     R[0].y = u;
     return u;
 }
@@ -442,37 +390,18 @@ __global__ void __launch_bounds__(NT) k_tile_fold(const uint32_t *__restrict__ s
 
     // ---- pass 1: each thread folds its short columns; long ones are listed -------
     if (staged) {
-        const int ncols = c_hi - c_lo;
-        int maxcols = ncols;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) maxcols = max(maxcols, __shfl_xor_sync(FULL, maxcols, o));
-        for (int k = 0; k < maxcols; ++k) {
-            const int c = c_lo + k;
-            int cnt = 0, off = 0;
-            if (k < ncols) {
-                const uint32_t w0 = sstart[c];
-                const int s0 = (int)(w0 & POSMASK), s1 = (int)(sstart[c + 1] & POSMASK);
-                if (!(w0 & BIGFLAG) && s1 > s0) {
-                    cnt = s1 - s0;
-                    off = s0 - r0;
-                }
-            }
-            if (cnt > SHORT_COL) {
-                const int e = atomicAdd(&S.nlong, 1);
-                if (e < LCAP) S.lcol[e] = off | (cnt << 16);
-                else atomicExch(&err->internal, 1u);
-                cnt = 0;
-            }
-            int wmax = cnt;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) wmax = max(wmax, __shfl_xor_sync(FULL, wmax, o));
-            if (wmax == 0) continue;
-            if (wmax <= 8) {
-                if (cnt) fold_short_rank<8>(&S.rec[off], cnt, &S.srow[off], &S.sval[off]);
-            } else if (wmax <= 16) {
-                if (cnt) fold_short_rank<16>(&S.rec[off], cnt, &S.srow[off], &S.sval[off]);
+        for (int c = c_lo; c < c_hi; ++c) {
+            const uint32_t w0 = sstart[c];
+            if (w0 & BIGFLAG) continue;
+            const int s0 = (int)(w0 & POSMASK), s1 = (int)(sstart[c + 1] & POSMASK);
+            const int cnt = s1 - s0;
+            if (cnt <= 0) continue;
+            if (cnt <= SHORT_COL) {
+                fold_column(&S.rec[s0 - r0], cnt);
             } else {
-                if (cnt) fold_short_rank<24>(&S.rec[off], cnt, &S.srow[off], &S.sval[off]);
+                const int e = atomicAdd(&S.nlong, 1);
+                if (e < LCAP) S.lcol[e] = (s0 - r0) | (cnt << 16);
+                else atomicExch(&err->internal, 1u);
             }
         }
     }
