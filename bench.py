@@ -278,7 +278,7 @@ def main():
     # algorithmic bytes per launch of each kernel ("kernels")
     alg = {
         "k_init": 4 * (N + 1),
-        "k_hist": 8 * L,
+        "k_colcount": 4 * L,
         "k_col_scan": 8 * N,
         "k_scatter": 32 * L,
         "k_bigcol": 0,

@@ -333,8 +333,8 @@ int sa_assemble_async(sa_ctx *ctx, const int32_t *d_ii, const int32_t *d_jj, con
     if (rc) return rc;
     rc = launch_init(ctx, lc, N, ntiles, nscan);
     if (rc) return rc;
-    if ((rc = mark(ctx, "k_hist"))) return rc;
-    SA_CUDA(ctx, launch_hist(lc, d_ii, d_jj, L, M, N, ctx->cur, ctx->err, false));
+    if ((rc = mark(ctx, "k_colcount"))) return rc;
+    SA_CUDA(ctx, launch_colcount(lc, d_jj, L, N, ctx->cur, ctx->err));
     if ((rc = mark(ctx, "k_col_scan"))) return rc;
     SA_CUDA(ctx, launch_col_scan(lc, ctx->cur, ctx->sstart, ctx->cur, N, nwin, ctx->win_first,
                                  ctx->tile_big, ntiles, ctx->big_list, ctx->bigk, ctx->scan_state,

@@ -223,9 +223,11 @@ cudaError_t launch_col_scan(Launch &lc, const uint32_t *cnt, uint32_t *sstart, u
                             int32_t N, int64_t nwin, int32_t *win_first, uint8_t *tile_big,
                             int64_t ntiles, BigCol *big_list, uint32_t *bigk,
                             unsigned long long *scan_state, ErrState *err);
+cudaError_t launch_colcount(Launch &lc, const int32_t *jj, int64_t L, int32_t N, uint32_t *cnt,
+                            ErrState *err);
 cudaError_t launch_scatter(Launch &lc, const int32_t *ii, const int32_t *jj, const double *s,
                            int64_t s_stride, int64_t L, int32_t M, int32_t N, uint32_t *cur,
-                           int4 *rec, const ErrState *err);
+                           int4 *rec, ErrState *err);
 cudaError_t launch_bigcol(Launch &lc, BigCol *big_list, const ErrState *err, int4 *rec,
                           const double *s, int64_t s_stride, int idx_bits, int passes);
 cudaError_t launch_tile_fold(Launch &lc, const uint32_t *sstart, const int32_t *win_first,

@@ -299,26 +299,105 @@ cudaError_t launch_col_scan(Launch &lc, const uint32_t *cnt, uint32_t *sstart, u
 }
 
 // ---------------------------------------------------------------------------
-// k_scatter: counting-sort scatter by column.  Record = {row, input position,
-// value lo, value hi}.  Within a column the slot order is whatever the
-// atomics produce; the fold restores input order from the stored position.
+// k_colcount: column histogram of the assembly path.  Reads only jj (row
+// indices are validated by k_scatter, which reads them anyway).  Each thread
+// walks a run of RUN consecutive triplets with a 4-entry column cache in
+// registers (element-ordered FEM input revisits a handful of columns), and
+// flushes evicted counts with fire-and-forget reductions.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void scatter_one(int64_t t, int32_t i, int32_t j, double v, bool live,
-                                            int32_t M, int32_t N, uint32_t *__restrict__ cur,
-                                            int4 *__restrict__ rec, uint32_t lsmall) {
-    const bool ok = live && i >= 1 && j >= 1 && i <= M && j <= N;
-    const unsigned act = __ballot_sync(FULL, ok);
-    if (!ok) return;
-    const unsigned peers = __match_any_sync(act, j);
-    const int lane = threadIdx.x & 31;
-    const int leader = __ffs(peers) - 1;
-    uint32_t base = 0;
-    if (lane == leader) base = atomicAdd(&cur[j - 1], (uint32_t)__popc(peers));
-    base = __shfl_sync(act, base, leader);
-    const uint32_t pos = (base & POSMASK) + ((base & BIGFLAG) ? lsmall : 0u) +
-                         __popc(peers & lanemask_lt());
-    rec[pos] = make_int4(i, (int)t, __double2loint(v), __double2hiint(v));
+constexpr int RUN = 16;
+
+__global__ void __launch_bounds__(256) k_colcount(const int32_t *__restrict__ jj, int64_t L,
+                                                  int32_t N, uint32_t *__restrict__ cnt,
+                                                  ErrState *err, int vec) {
+    const int64_t nrun = (L + RUN - 1) / RUN;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    unsigned long long bad = ~0ull;
+    unsigned over = 0;
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < nrun; r += stride) {
+        const int64_t t0 = r * RUN;
+        int j[RUN];
+        if (vec && t0 + RUN <= L) {
+            const int4 *p = reinterpret_cast<const int4 *>(jj + t0);
+#pragma unroll
+            for (int q = 0; q < RUN / 4; ++q) {
+                const int4 v = __ldg(p + q);
+                j[4 * q] = v.x;
+                j[4 * q + 1] = v.y;
+                j[4 * q + 2] = v.z;
+                j[4 * q + 3] = v.w;
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < RUN; ++k) j[k] = (t0 + k < L) ? jj[t0 + k] : 0x7fffffff;
+        }
+        int key[4] = {0, 0, 0, 0};
+        unsigned cn[4] = {0u, 0u, 0u, 0u};
+        int victim = 0;
+#pragma unroll
+        for (int k = 0; k < RUN; ++k) {
+            const int c = j[k];
+            const bool live = t0 + k < L;
+            if (live && c < 1) bad = min(bad, (unsigned long long)(t0 + k));
+            if (live && c > N) over = 1;
+            if (!(live && c >= 1 && c <= N)) continue;
+            bool hit = false;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                if (key[e] == c) {
+                    cn[e] += 1u;
+                    hit = true;
+                }
+            }
+            if (!hit) {
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    if (e == victim) {
+                        if (cn[e]) atomicAdd(&cnt[key[e] - 1], cn[e]);
+                        key[e] = c;
+                        cn[e] = 1u;
+                    }
+                }
+                victim = (victim + 1) & 3;
+            }
+        }
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+            if (cn[e]) atomicAdd(&cnt[key[e] - 1], cn[e]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        bad = min(bad, __shfl_xor_sync(FULL, bad, o));
+        over |= __shfl_xor_sync(FULL, over, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (bad != ~0ull) atomicMin(&err->bad_j, bad);
+        if (over) err->over_n = 1;
+    }
 }
+
+cudaError_t launch_colcount(Launch &lc, const int32_t *jj, int64_t L, int32_t N, uint32_t *cnt,
+                            ErrState *err) {
+    if (L <= 0) return cudaSuccess;
+    const int vec = aligned16(jj);
+    const int64_t nrun = (L + RUN - 1) / RUN;
+    int grid = (int)std::min<int64_t>((nrun + 255) / 256, (int64_t)lc.num_sms * 8);
+    k_colcount<<<grid, 256, 0, lc.stream>>>(jj, L, N, cnt, err, vec);
+    lc.launches++;
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// k_scatter: counting-sort scatter by column.  Record = {row, input position,
+// value lo, value hi}.  Each thread takes a run of SRUN consecutive
+// triplets: duplicates of a column inside the run share one reservation
+// (atomicAdd of the run's count on the column cursor), and the run's
+// reservations are independent, so their round trips overlap.  Row indices
+// are validated here (first bad position, rows above M).  Within a column
+// the slot order is whatever the reservations produce; the fold restores
+// input order from the stored position.
+// ---------------------------------------------------------------------------
+constexpr int SRUN = 8;
 
 __global__ void __launch_bounds__(256) k_scatter(const int32_t *__restrict__ ii,
                                                  const int32_t *__restrict__ jj,
@@ -326,54 +405,116 @@ __global__ void __launch_bounds__(256) k_scatter(const int32_t *__restrict__ ii,
                                                  int64_t L, int32_t M, int32_t N,
                                                  uint32_t *__restrict__ cur,
                                                  int4 *__restrict__ rec, int vec,
-                                                 const ErrState *err) {
-    const int lane = threadIdx.x & 31;
+                                                 ErrState *err) {
     const uint32_t lsmall = err->lsmall;
+    const int64_t nrun = (L + SRUN - 1) / SRUN;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    const int64_t wbase0 = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31);
-    int64_t tail0 = 0;
-    if (vec) {
-        const int64_t nq = L >> 2;
-        const int4 *ii4 = reinterpret_cast<const int4 *>(ii);
-        const int4 *jj4 = reinterpret_cast<const int4 *>(jj);
-        const double2 *s2 = reinterpret_cast<const double2 *>(s);
-        const double s0 = s_stride ? 0.0 : __ldg(s);
-        for (int64_t qb = wbase0; qb < nq; qb += stride) {
-            const int64_t q = qb + lane;
-            const bool live = q < nq;
-            int4 vi = make_int4(1, 1, 1, 1), vj = make_int4(1, 1, 1, 1);
-            double2 va = make_double2(s0, s0), vb = make_double2(s0, s0);
-            if (live) {
-                vi = __ldg(ii4 + q);
-                vj = __ldg(jj4 + q);
-                if (s_stride) {
-                    va = __ldg(s2 + 2 * q);
-                    vb = __ldg(s2 + 2 * q + 1);
+    const double s0v = s_stride ? 0.0 : __ldg(s);
+    unsigned long long bad = ~0ull;
+    unsigned over = 0;
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < nrun; r += stride) {
+        const int64_t t0 = r * SRUN;
+        int iv[SRUN], jv[SRUN];
+        double vv[SRUN];
+        if (vec && t0 + SRUN <= L) {
+            const int4 *pi = reinterpret_cast<const int4 *>(ii + t0);
+            const int4 *pj = reinterpret_cast<const int4 *>(jj + t0);
+#pragma unroll
+            for (int q = 0; q < SRUN / 4; ++q) {
+                const int4 a = __ldg(pi + q), b = __ldg(pj + q);
+                iv[4 * q] = a.x; iv[4 * q + 1] = a.y; iv[4 * q + 2] = a.z; iv[4 * q + 3] = a.w;
+                jv[4 * q] = b.x; jv[4 * q + 1] = b.y; jv[4 * q + 2] = b.z; jv[4 * q + 3] = b.w;
+            }
+            if (s_stride) {
+                const double2 *ps = reinterpret_cast<const double2 *>(s + t0);
+#pragma unroll
+                for (int q = 0; q < SRUN / 2; ++q) {
+                    const double2 d = __ldg(ps + q);
+                    vv[2 * q] = d.x;
+                    vv[2 * q + 1] = d.y;
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < SRUN; ++k) vv[k] = s0v;
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < SRUN; ++k) {
+                const bool live = t0 + k < L;
+                iv[k] = live ? ii[t0 + k] : 1;
+                jv[k] = live ? jj[t0 + k] : 0;
+                vv[k] = live ? s[(t0 + k) * s_stride] : 0.0;
+            }
+        }
+        // columns scattered: valid column index (k_colcount validated/counted
+        // exactly these); rows are data here, validated for the error report
+        bool ok[SRUN];
+#pragma unroll
+        for (int k = 0; k < SRUN; ++k) {
+            const bool live = t0 + k < L;
+            ok[k] = live && jv[k] >= 1 && jv[k] <= N;
+            if (live && iv[k] < 1) bad = min(bad, (unsigned long long)(t0 + k));
+            if (live && iv[k] > M) over = 1;
+        }
+        // first occurrence of each column in the run, rank, and run counts
+        int first[SRUN], rank[SRUN];
+        unsigned cnt[SRUN];
+#pragma unroll
+        for (int k = 0; k < SRUN; ++k) {
+            first[k] = k;
+            rank[k] = 0;
+            cnt[k] = 0u;
+        }
+#pragma unroll
+        for (int k = 0; k < SRUN; ++k) {
+#pragma unroll
+            for (int q = 0; q < k; ++q) {
+                if (ok[k] && ok[q] && jv[q] == jv[k]) {
+                    rank[k] += 1;
+                    first[k] = min(first[k], q);
                 }
             }
-            scatter_one(4 * q + 0, vi.x, vj.x, va.x, live, M, N, cur, rec, lsmall);
-            scatter_one(4 * q + 1, vi.y, vj.y, va.y, live, M, N, cur, rec, lsmall);
-            scatter_one(4 * q + 2, vi.z, vj.z, vb.x, live, M, N, cur, rec, lsmall);
-            scatter_one(4 * q + 3, vi.w, vj.w, vb.y, live, M, N, cur, rec, lsmall);
         }
-        tail0 = nq << 2;
+#pragma unroll
+        for (int k = 0; k < SRUN; ++k)
+#pragma unroll
+            for (int q = 0; q < SRUN; ++q)
+                if (ok[k] && first[k] == q) cnt[q] += 1u;
+        uint32_t base[SRUN];
+#pragma unroll
+        for (int k = 0; k < SRUN; ++k) {
+            base[k] = 0u;
+            if (ok[k] && first[k] == k) base[k] = atomicAdd(&cur[jv[k] - 1], cnt[k]);
+        }
+#pragma unroll
+        for (int k = 0; k < SRUN; ++k) {
+            if (!ok[k]) continue;
+            uint32_t bw = 0u;
+#pragma unroll
+            for (int q = 0; q < SRUN; ++q)
+                if (first[k] == q) bw = base[q];
+            const uint32_t pos = (bw & POSMASK) + ((bw & BIGFLAG) ? lsmall : 0u) + (uint32_t)rank[k];
+            rec[pos] = make_int4(iv[k], (int)(t0 + k), __double2loint(vv[k]), __double2hiint(vv[k]));
+        }
     }
-    for (int64_t tb = tail0 + wbase0; tb < L; tb += stride) {
-        const int64_t t = tb + lane;
-        const bool live = t < L;
-        int32_t i = live ? ii[t] : 0, j = live ? jj[t] : 0;
-        double v = live ? s[t * s_stride] : 0.0;
-        scatter_one(t, i, j, v, live, M, N, cur, rec, lsmall);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        bad = min(bad, __shfl_xor_sync(FULL, bad, o));
+        over |= __shfl_xor_sync(FULL, over, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (bad != ~0ull) atomicMin(&err->bad_i, bad);
+        if (over) err->over_m = 1;
     }
 }
 
 cudaError_t launch_scatter(Launch &lc, const int32_t *ii, const int32_t *jj, const double *s,
                            int64_t s_stride, int64_t L, int32_t M, int32_t N, uint32_t *cur,
-                           int4 *rec, const ErrState *err) {
+                           int4 *rec, ErrState *err) {
     if (L <= 0) return cudaSuccess;
     const int vec = aligned16(ii) && aligned16(jj) && (s_stride == 0 || aligned16(s));
-    int64_t want = ((vec ? (L >> 2) : L) + 255) / 256 + 1;
-    int grid = (int)std::min<int64_t>(want, (int64_t)lc.num_sms * 8);
+    const int64_t nrun = (L + SRUN - 1) / SRUN;
+    int grid = (int)std::min<int64_t>((nrun + 255) / 256, (int64_t)lc.num_sms * 8);
     k_scatter<<<grid, 256, 0, lc.stream>>>(ii, jj, s, s_stride, L, M, N, cur, rec, vec, err);
     lc.launches++;
     return cudaGetLastError();
