@@ -299,78 +299,105 @@ cudaError_t launch_col_scan(Launch &lc, const uint32_t *cnt, uint32_t *sstart, u
 }
 
 // ---------------------------------------------------------------------------
-// k_colcount: column histogram of the assembly path.  Reads only jj (row
-// indices are validated by k_scatter, which reads them anyway).  Each thread
-// walks a run of RUN consecutive triplets with a 4-entry column cache in
-// registers (element-ordered FEM input revisits a handful of columns), and
-// flushes evicted counts with fire-and-forget reductions.
+// CTA-scope column aggregation shared by k_colcount and k_scatter.  A CTA
+// takes CHUNK consecutive triplets (CPT per thread, loaded with 16-byte
+// vector loads) and counts their columns in a shared-memory hash (open
+// addressing, HT slots, list of used slots so only those are visited again).
+// Element-ordered FEM input touches ~CHUNK/9 distinct columns per chunk, so
+// global atomics drop by an order of magnitude and stay independent.
 // ---------------------------------------------------------------------------
-constexpr int RUN = 16;
+constexpr int AGG_NT = 256;
+constexpr int CPT = 8;
+constexpr int CHUNK = AGG_NT * CPT;
+constexpr int HT = 2 * CHUNK;
 
-__global__ void __launch_bounds__(256) k_colcount(const int32_t *__restrict__ jj, int64_t L,
-                                                  int32_t N, uint32_t *__restrict__ cnt,
-                                                  ErrState *err, int vec) {
-    const int64_t nrun = (L + RUN - 1) / RUN;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+struct AggSmem {
+    int key[HT];        // column + 1 (0 = empty)
+    int ctr[HT];        // per column: triplets in the chunk, then the reserved cursor word
+    int used[CHUNK];    // used slots
+    int nused;
+};
+
+__device__ __forceinline__ int agg_insert(AggSmem &A, int col) {
+    const int key = col + 1;
+    unsigned h = ((unsigned)key * 0x9E3779B1u) >> (32 - 12);  // HT = 4096
+    while (true) {
+        const int old = atomicCAS(&A.key[h], 0, key);
+        if (old == 0) {
+            A.used[atomicAdd(&A.nused, 1)] = (int)h;
+            return (int)h;
+        }
+        if (old == key) return (int)h;
+        h = (h + 1) & (HT - 1);
+    }
+}
+
+// load CPT consecutive int32 (vector path when aligned and complete)
+__device__ __forceinline__ void load_run(const int32_t *__restrict__ p, int64_t t0, int64_t L,
+                                         int vec, int (&v)[CPT], int fill) {
+    if (vec && t0 + CPT <= L) {
+        const int4 *q = reinterpret_cast<const int4 *>(p + t0);
+#pragma unroll
+        for (int k = 0; k < CPT / 4; ++k) {
+            const int4 x = __ldg(q + k);
+            v[4 * k] = x.x;
+            v[4 * k + 1] = x.y;
+            v[4 * k + 2] = x.z;
+            v[4 * k + 3] = x.w;
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < CPT; ++k) v[k] = (t0 + k < L) ? p[t0 + k] : fill;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// k_colcount: column histogram of the assembly path (reads jj only; rows
+// are validated by k_scatter, which reads them anyway).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(AGG_NT) k_colcount(const int32_t *__restrict__ jj, int64_t L,
+                                                     int32_t N, uint32_t *__restrict__ cnt,
+                                                     ErrState *err, int vec) {
+    __shared__ AggSmem A;
+    const int tid = threadIdx.x;
+    for (int k = tid; k < HT; k += AGG_NT) A.key[k] = 0;
+    if (tid == 0) A.nused = 0;
+    __syncthreads();
     unsigned long long bad = ~0ull;
     unsigned over = 0;
-    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < nrun; r += stride) {
-        const int64_t t0 = r * RUN;
-        int j[RUN];
-        if (vec && t0 + RUN <= L) {
-            const int4 *p = reinterpret_cast<const int4 *>(jj + t0);
+    const int64_t nchunk = (L + CHUNK - 1) / CHUNK;
+    for (int64_t ch = blockIdx.x; ch < nchunk; ch += gridDim.x) {
+        const int64_t t0 = ch * CHUNK + (int64_t)tid * CPT;
+        int j[CPT];
+        load_run(jj, t0, L, vec, j, 0x7fffffff);
 #pragma unroll
-            for (int q = 0; q < RUN / 4; ++q) {
-                const int4 v = __ldg(p + q);
-                j[4 * q] = v.x;
-                j[4 * q + 1] = v.y;
-                j[4 * q + 2] = v.z;
-                j[4 * q + 3] = v.w;
-            }
-        } else {
-#pragma unroll
-            for (int k = 0; k < RUN; ++k) j[k] = (t0 + k < L) ? jj[t0 + k] : 0x7fffffff;
-        }
-        int key[4] = {0, 0, 0, 0};
-        unsigned cn[4] = {0u, 0u, 0u, 0u};
-        int victim = 0;
-#pragma unroll
-        for (int k = 0; k < RUN; ++k) {
-            const int c = j[k];
+        for (int k = 0; k < CPT; ++k) {
             const bool live = t0 + k < L;
-            if (live && c < 1) bad = min(bad, (unsigned long long)(t0 + k));
-            if (live && c > N) over = 1;
-            if (!(live && c >= 1 && c <= N)) continue;
-            bool hit = false;
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                if (key[e] == c) {
-                    cn[e] += 1u;
-                    hit = true;
-                }
-            }
-            if (!hit) {
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    if (e == victim) {
-                        if (cn[e]) atomicAdd(&cnt[key[e] - 1], cn[e]);
-                        key[e] = c;
-                        cn[e] = 1u;
-                    }
-                }
-                victim = (victim + 1) & 3;
+            if (live && j[k] < 1) bad = min(bad, (unsigned long long)(t0 + k));
+            if (live && j[k] > N) over = 1;
+            if (live && j[k] >= 1 && j[k] <= N) {
+                const int h = agg_insert(A, j[k] - 1);
+                atomicAdd(&A.ctr[h], 1);
             }
         }
-#pragma unroll
-        for (int e = 0; e < 4; ++e)
-            if (cn[e]) atomicAdd(&cnt[key[e] - 1], cn[e]);
+        __syncthreads();
+        const int nu = A.nused;
+        for (int e = tid; e < nu; e += AGG_NT) {
+            const int h = A.used[e];
+            atomicAdd(&cnt[A.key[h] - 1], (uint32_t)A.ctr[h]);
+            A.key[h] = 0;
+            A.ctr[h] = 0;
+        }
+        __syncthreads();
+        if (tid == 0) A.nused = 0;
+        __syncthreads();
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         bad = min(bad, __shfl_xor_sync(FULL, bad, o));
         over |= __shfl_xor_sync(FULL, over, o);
     }
-    if ((threadIdx.x & 31) == 0) {
+    if ((tid & 31) == 0) {
         if (bad != ~0ull) atomicMin(&err->bad_j, bad);
         if (over) err->over_n = 1;
     }
@@ -380,129 +407,107 @@ cudaError_t launch_colcount(Launch &lc, const int32_t *jj, int64_t L, int32_t N,
                             ErrState *err) {
     if (L <= 0) return cudaSuccess;
     const int vec = aligned16(jj);
-    const int64_t nrun = (L + RUN - 1) / RUN;
-    int grid = (int)std::min<int64_t>((nrun + 255) / 256, (int64_t)lc.num_sms * 8);
-    k_colcount<<<grid, 256, 0, lc.stream>>>(jj, L, N, cnt, err, vec);
+    const int64_t nchunk = (L + CHUNK - 1) / CHUNK;
+    int grid = (int)std::min<int64_t>(nchunk, (int64_t)lc.num_sms * 4);
+    k_colcount<<<grid, AGG_NT, 0, lc.stream>>>(jj, L, N, cnt, err, vec);
     lc.launches++;
     return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------------------
 // k_scatter: counting-sort scatter by column.  Record = {row, input position,
-// value lo, value hi}.  Each thread takes a run of SRUN consecutive
-// triplets: duplicates of a column inside the run share one reservation
-// (atomicAdd of the run's count on the column cursor), and the run's
-// reservations are independent, so their round trips overlap.  Row indices
-// are validated here (first bad position, rows above M).  Within a column
-// the slot order is whatever the reservations produce; the fold restores
-// input order from the stored position.
+// value lo, value hi}.  Per chunk: (1) each column's triplets get chunk-local
+// slots from a shared-memory counter, (2) one global atomicAdd per distinct
+// column reserves the chunk's slots on the column cursor, (3) records are
+// written.  Row indices are validated here (first bad position, rows above
+// M).  The slot order inside a column is arbitrary; the fold restores input
+// order from the stored position.
 // ---------------------------------------------------------------------------
-constexpr int SRUN = 8;
-
-__global__ void __launch_bounds__(256) k_scatter(const int32_t *__restrict__ ii,
-                                                 const int32_t *__restrict__ jj,
-                                                 const double *__restrict__ s, int64_t s_stride,
-                                                 int64_t L, int32_t M, int32_t N,
-                                                 uint32_t *__restrict__ cur,
-                                                 int4 *__restrict__ rec, int vec,
-                                                 ErrState *err) {
+__global__ void __launch_bounds__(AGG_NT) k_scatter(const int32_t *__restrict__ ii,
+                                                    const int32_t *__restrict__ jj,
+                                                    const double *__restrict__ s, int64_t s_stride,
+                                                    int64_t L, int32_t M, int32_t N,
+                                                    uint32_t *__restrict__ cur,
+                                                    int4 *__restrict__ rec, int vec,
+                                                    ErrState *err) {
+    __shared__ AggSmem A;
+    const int tid = threadIdx.x;
+    for (int k = tid; k < HT; k += AGG_NT) {
+        A.key[k] = 0;
+        A.ctr[k] = 0;
+    }
+    if (tid == 0) A.nused = 0;
+    __syncthreads();
     const uint32_t lsmall = err->lsmall;
-    const int64_t nrun = (L + SRUN - 1) / SRUN;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     const double s0v = s_stride ? 0.0 : __ldg(s);
     unsigned long long bad = ~0ull;
     unsigned over = 0;
-    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < nrun; r += stride) {
-        const int64_t t0 = r * SRUN;
-        int iv[SRUN], jv[SRUN];
-        double vv[SRUN];
-        if (vec && t0 + SRUN <= L) {
-            const int4 *pi = reinterpret_cast<const int4 *>(ii + t0);
-            const int4 *pj = reinterpret_cast<const int4 *>(jj + t0);
-#pragma unroll
-            for (int q = 0; q < SRUN / 4; ++q) {
-                const int4 a = __ldg(pi + q), b = __ldg(pj + q);
-                iv[4 * q] = a.x; iv[4 * q + 1] = a.y; iv[4 * q + 2] = a.z; iv[4 * q + 3] = a.w;
-                jv[4 * q] = b.x; jv[4 * q + 1] = b.y; jv[4 * q + 2] = b.z; jv[4 * q + 3] = b.w;
-            }
-            if (s_stride) {
+    const int64_t nchunk = (L + CHUNK - 1) / CHUNK;
+    for (int64_t ch = blockIdx.x; ch < nchunk; ch += gridDim.x) {
+        const int64_t t0 = ch * CHUNK + (int64_t)tid * CPT;
+        int iv[CPT], jv[CPT];
+        double vv[CPT];
+        load_run(ii, t0, L, vec, iv, 1);
+        load_run(jj, t0, L, vec, jv, 0);
+        if (s_stride) {
+            if (vec && t0 + CPT <= L) {
                 const double2 *ps = reinterpret_cast<const double2 *>(s + t0);
 #pragma unroll
-                for (int q = 0; q < SRUN / 2; ++q) {
+                for (int q = 0; q < CPT / 2; ++q) {
                     const double2 d = __ldg(ps + q);
                     vv[2 * q] = d.x;
                     vv[2 * q + 1] = d.y;
                 }
             } else {
 #pragma unroll
-                for (int k = 0; k < SRUN; ++k) vv[k] = s0v;
+                for (int k = 0; k < CPT; ++k) vv[k] = (t0 + k < L) ? s[t0 + k] : 0.0;
             }
         } else {
 #pragma unroll
-            for (int k = 0; k < SRUN; ++k) {
-                const bool live = t0 + k < L;
-                iv[k] = live ? ii[t0 + k] : 1;
-                jv[k] = live ? jj[t0 + k] : 0;
-                vv[k] = live ? s[(t0 + k) * s_stride] : 0.0;
-            }
+            for (int k = 0; k < CPT; ++k) vv[k] = s0v;
         }
-        // columns scattered: valid column index (k_colcount validated/counted
-        // exactly these); rows are data here, validated for the error report
-        bool ok[SRUN];
+        int hk[CPT], rk[CPT];
 #pragma unroll
-        for (int k = 0; k < SRUN; ++k) {
+        for (int k = 0; k < CPT; ++k) {
             const bool live = t0 + k < L;
-            ok[k] = live && jv[k] >= 1 && jv[k] <= N;
             if (live && iv[k] < 1) bad = min(bad, (unsigned long long)(t0 + k));
             if (live && iv[k] > M) over = 1;
-        }
-        // first occurrence of each column in the run, rank, and run counts
-        int first[SRUN], rank[SRUN];
-        unsigned cnt[SRUN];
-#pragma unroll
-        for (int k = 0; k < SRUN; ++k) {
-            first[k] = k;
-            rank[k] = 0;
-            cnt[k] = 0u;
-        }
-#pragma unroll
-        for (int k = 0; k < SRUN; ++k) {
-#pragma unroll
-            for (int q = 0; q < k; ++q) {
-                if (ok[k] && ok[q] && jv[q] == jv[k]) {
-                    rank[k] += 1;
-                    first[k] = min(first[k], q);
-                }
+            hk[k] = -1;
+            rk[k] = 0;
+            if (live && jv[k] >= 1 && jv[k] <= N) {
+                hk[k] = agg_insert(A, jv[k] - 1);
+                rk[k] = atomicAdd(&A.ctr[hk[k]], 1);
             }
         }
-#pragma unroll
-        for (int k = 0; k < SRUN; ++k)
-#pragma unroll
-            for (int q = 0; q < SRUN; ++q)
-                if (ok[k] && first[k] == q) cnt[q] += 1u;
-        uint32_t base[SRUN];
-#pragma unroll
-        for (int k = 0; k < SRUN; ++k) {
-            base[k] = 0u;
-            if (ok[k] && first[k] == k) base[k] = atomicAdd(&cur[jv[k] - 1], cnt[k]);
+        __syncthreads();
+        const int nu = A.nused;
+        for (int e = tid; e < nu; e += AGG_NT) {
+            const int h = A.used[e];
+            A.ctr[h] = (int)atomicAdd(&cur[A.key[h] - 1], (uint32_t)A.ctr[h]);
         }
+        __syncthreads();
 #pragma unroll
-        for (int k = 0; k < SRUN; ++k) {
-            if (!ok[k]) continue;
-            uint32_t bw = 0u;
-#pragma unroll
-            for (int q = 0; q < SRUN; ++q)
-                if (first[k] == q) bw = base[q];
-            const uint32_t pos = (bw & POSMASK) + ((bw & BIGFLAG) ? lsmall : 0u) + (uint32_t)rank[k];
+        for (int k = 0; k < CPT; ++k) {
+            if (hk[k] < 0) continue;
+            const uint32_t bw = (uint32_t)A.ctr[hk[k]];
+            const uint32_t pos = (bw & POSMASK) + ((bw & BIGFLAG) ? lsmall : 0u) + (uint32_t)rk[k];
             rec[pos] = make_int4(iv[k], (int)(t0 + k), __double2loint(vv[k]), __double2hiint(vv[k]));
         }
+        __syncthreads();
+        for (int e = tid; e < nu; e += AGG_NT) {
+            const int h = A.used[e];
+            A.key[h] = 0;
+            A.ctr[h] = 0;
+        }
+        if (tid == 0) A.nused = 0;
+        __syncthreads();
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         bad = min(bad, __shfl_xor_sync(FULL, bad, o));
         over |= __shfl_xor_sync(FULL, over, o);
     }
-    if ((threadIdx.x & 31) == 0) {
+    if ((tid & 31) == 0) {
         if (bad != ~0ull) atomicMin(&err->bad_i, bad);
         if (over) err->over_m = 1;
     }
@@ -513,9 +518,9 @@ cudaError_t launch_scatter(Launch &lc, const int32_t *ii, const int32_t *jj, con
                            int4 *rec, ErrState *err) {
     if (L <= 0) return cudaSuccess;
     const int vec = aligned16(ii) && aligned16(jj) && (s_stride == 0 || aligned16(s));
-    const int64_t nrun = (L + SRUN - 1) / SRUN;
-    int grid = (int)std::min<int64_t>((nrun + 255) / 256, (int64_t)lc.num_sms * 8);
-    k_scatter<<<grid, 256, 0, lc.stream>>>(ii, jj, s, s_stride, L, M, N, cur, rec, vec, err);
+    const int64_t nchunk = (L + CHUNK - 1) / CHUNK;
+    int grid = (int)std::min<int64_t>(nchunk, (int64_t)lc.num_sms * 4);
+    k_scatter<<<grid, AGG_NT, 0, lc.stream>>>(ii, jj, s, s_stride, L, M, N, cur, rec, vec, err);
     lc.launches++;
     return cudaGetLastError();
 }
