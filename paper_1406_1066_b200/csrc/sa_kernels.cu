@@ -360,7 +360,10 @@ __global__ void __launch_bounds__(AGG_NT) k_colcount(const int32_t *__restrict__
                                                      ErrState *err, int vec) {
     __shared__ AggSmem A;
     const int tid = threadIdx.x;
-    for (int k = tid; k < HT; k += AGG_NT) A.key[k] = 0;
+    for (int k = tid; k < HT; k += AGG_NT) {
+        A.key[k] = 0;
+        A.ctr[k] = 0;
+    }
     if (tid == 0) A.nused = 0;
     __syncthreads();
     unsigned long long bad = ~0ull;
