@@ -369,10 +369,16 @@ __global__ void __launch_bounds__(AGG_NT) k_colcount(const int32_t *__restrict__
     unsigned long long bad = ~0ull;
     unsigned over = 0;
     const int64_t nchunk = (L + CHUNK - 1) / CHUNK;
+    int jn[CPT];
+    if ((int64_t)blockIdx.x < nchunk)
+        load_run(jj, (int64_t)blockIdx.x * CHUNK + (int64_t)tid * CPT, L, vec, jn, 0x7fffffff);
     for (int64_t ch = blockIdx.x; ch < nchunk; ch += gridDim.x) {
         const int64_t t0 = ch * CHUNK + (int64_t)tid * CPT;
         int j[CPT];
-        load_run(jj, t0, L, vec, j, 0x7fffffff);
+#pragma unroll
+        for (int k = 0; k < CPT; ++k) j[k] = jn[k];
+        if (ch + gridDim.x < nchunk)  // prefetch the next chunk while this one is counted
+            load_run(jj, (ch + gridDim.x) * CHUNK + (int64_t)tid * CPT, L, vec, jn, 0x7fffffff);
 #pragma unroll
         for (int k = 0; k < CPT; ++k) {
             const bool live = t0 + k < L;
@@ -446,29 +452,42 @@ __global__ void __launch_bounds__(AGG_NT) k_scatter(const int32_t *__restrict__ 
     unsigned long long bad = ~0ull;
     unsigned over = 0;
     const int64_t nchunk = (L + CHUNK - 1) / CHUNK;
-    for (int64_t ch = blockIdx.x; ch < nchunk; ch += gridDim.x) {
-        const int64_t t0 = ch * CHUNK + (int64_t)tid * CPT;
-        int iv[CPT], jv[CPT];
-        double vv[CPT];
-        load_run(ii, t0, L, vec, iv, 1);
-        load_run(jj, t0, L, vec, jv, 0);
+    int ivn[CPT], jvn[CPT];
+    double vvn[CPT];
+    auto load_all = [&](int64_t c0) {
+        const int64_t t0 = c0 * CHUNK + (int64_t)tid * CPT;
+        load_run(ii, t0, L, vec, ivn, 1);
+        load_run(jj, t0, L, vec, jvn, 0);
         if (s_stride) {
             if (vec && t0 + CPT <= L) {
                 const double2 *ps = reinterpret_cast<const double2 *>(s + t0);
 #pragma unroll
                 for (int q = 0; q < CPT / 2; ++q) {
                     const double2 d = __ldg(ps + q);
-                    vv[2 * q] = d.x;
-                    vv[2 * q + 1] = d.y;
+                    vvn[2 * q] = d.x;
+                    vvn[2 * q + 1] = d.y;
                 }
             } else {
 #pragma unroll
-                for (int k = 0; k < CPT; ++k) vv[k] = (t0 + k < L) ? s[t0 + k] : 0.0;
+                for (int k = 0; k < CPT; ++k) vvn[k] = (t0 + k < L) ? s[t0 + k] : 0.0;
             }
         } else {
 #pragma unroll
-            for (int k = 0; k < CPT; ++k) vv[k] = s0v;
+            for (int k = 0; k < CPT; ++k) vvn[k] = s0v;
         }
+    };
+    if ((int64_t)blockIdx.x < nchunk) load_all(blockIdx.x);
+    for (int64_t ch = blockIdx.x; ch < nchunk; ch += gridDim.x) {
+        const int64_t t0 = ch * CHUNK + (int64_t)tid * CPT;
+        int iv[CPT], jv[CPT];
+        double vv[CPT];
+#pragma unroll
+        for (int k = 0; k < CPT; ++k) {
+            iv[k] = ivn[k];
+            jv[k] = jvn[k];
+            vv[k] = vvn[k];
+        }
+        if (ch + gridDim.x < nchunk) load_all(ch + gridDim.x);  // next chunk in flight
         int hk[CPT], rk[CPT];
 #pragma unroll
         for (int k = 0; k < CPT; ++k) {
