@@ -16,7 +16,7 @@ CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "lib")
 LIBNAME = "libsa_b200.so"
 SOURCES = ["sa_kernels.cu", "sa_tile.cu", "sa_capi.cu"]
-HEADERS = ["sa_internal.cuh", os.path.join("..", "..", "include", "sparse_assembly.h")]
+HEADERS = ["sa_internal.cuh", "sa_network.cuh", os.path.join("..", "..", "include", "sparse_assembly.h")]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

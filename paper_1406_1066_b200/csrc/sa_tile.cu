@@ -25,6 +25,7 @@
 // big column (folded by k_bigcol) copy its results from the big space.
 
 #include "sa_internal.cuh"
+#include "sa_network.cuh"
 
 namespace sa {
 
@@ -157,6 +158,74 @@ __device__ int fold_column(int4 *R, int c) {
         ++u;
         k += g;
     }
+    R[0].y = u;
+    return u;
+}
+
+// Short column (c <= W records): static Batcher sorting network on the
+// (row, position) keys held in registers -- compare-exchanges within a layer
+// are independent, so the sort runs at instruction throughput instead of
+// shared-memory latency -- then one pass folds each run of equal rows.
+// Outputs compacted in place at R[0..u), R[0].y = u.
+template <int W>
+__device__ int fold_short_net(int4 *R, int c) {
+    unsigned long long k[W];
+    int sl[W];
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+        if (w < c) {
+            const int2 kk = *reinterpret_cast<const int2 *>(&R[w]);
+            k[w] = ((unsigned long long)(unsigned)kk.x << 32) | (unsigned)kk.y;
+        } else {
+            k[w] = ~0ull;
+        }
+        sl[w] = w;
+    }
+#define SA_CE(i, j)                                            \
+    {                                                          \
+        const bool sw = k[j] < k[i];                           \
+        const unsigned long long lo_ = sw ? k[j] : k[i];       \
+        const unsigned long long hi_ = sw ? k[i] : k[j];       \
+        const int sa_ = sw ? sl[j] : sl[i];                    \
+        const int sb_ = sw ? sl[i] : sl[j];                    \
+        k[i] = lo_;                                            \
+        k[j] = hi_;                                            \
+        sl[i] = sa_;                                           \
+        sl[j] = sb_;                                           \
+    }
+    if constexpr (W == 8) {
+        SA_NET8(SA_CE)
+    } else if constexpr (W == 16) {
+        SA_NET16(SA_CE)
+    } else {
+        SA_NET24(SA_CE)
+    }
+#undef SA_CE
+    int row[W];
+    double v[W];
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+        row[w] = (int)(k[w] >> 32);
+        v[w] = (w < c) ? *reinterpret_cast<const double *>(&R[sl[w]].z) : 0.0;
+    }
+    int u = 0;
+    int prev = row[0];
+    double acc = fold_add(0.0, v[0]);
+#pragma unroll
+    for (int w = 1; w < W; ++w) {
+        if (w < c) {
+            if (row[w] != prev) {
+                R[u] = make_int4(prev - 1, 0, __double2loint(acc), __double2hiint(acc));
+                ++u;
+                prev = row[w];
+                acc = fold_add(0.0, v[w]);
+            } else {
+                acc = fold_add(acc, v[w]);
+            }
+        }
+    }
+    R[u] = make_int4(prev - 1, 0, __double2loint(acc), __double2hiint(acc));
+    ++u;
     R[0].y = u;
     return u;
 }
@@ -390,18 +459,37 @@ __global__ void __launch_bounds__(NT) k_tile_fold(const uint32_t *__restrict__ s
 
     // ---- pass 1: each thread folds its short columns; long ones are listed -------
     if (staged) {
-        for (int c = c_lo; c < c_hi; ++c) {
-            const uint32_t w0 = sstart[c];
-            if (w0 & BIGFLAG) continue;
-            const int s0 = (int)(w0 & POSMASK), s1 = (int)(sstart[c + 1] & POSMASK);
-            const int cnt = s1 - s0;
-            if (cnt <= 0) continue;
-            if (cnt <= SHORT_COL) {
-                fold_column(&S.rec[s0 - r0], cnt);
-            } else {
+        const int ncols = c_hi - c_lo;
+        int maxcols = ncols;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) maxcols = max(maxcols, __shfl_xor_sync(FULL, maxcols, o));
+        for (int k = 0; k < maxcols; ++k) {
+            const int c = c_lo + k;
+            int cnt = 0, off = 0;
+            if (k < ncols) {
+                const uint32_t w0 = sstart[c];
+                const int s0 = (int)(w0 & POSMASK), s1 = (int)(sstart[c + 1] & POSMASK);
+                if (!(w0 & BIGFLAG) && s1 > s0) {
+                    cnt = s1 - s0;
+                    off = s0 - r0;
+                }
+            }
+            if (cnt > SHORT_COL) {
                 const int e = atomicAdd(&S.nlong, 1);
-                if (e < LCAP) S.lcol[e] = (s0 - r0) | (cnt << 16);
+                if (e < LCAP) S.lcol[e] = off | (cnt << 16);
                 else atomicExch(&err->internal, 1u);
+                cnt = 0;
+            }
+            int wmax = cnt;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) wmax = max(wmax, __shfl_xor_sync(FULL, wmax, o));
+            if (wmax == 0) continue;
+            if (wmax <= 8) {
+                if (cnt) fold_short_net<8>(&S.rec[off], cnt);
+            } else if (wmax <= 16) {
+                if (cnt) fold_short_net<16>(&S.rec[off], cnt);
+            } else {
+                if (cnt) fold_short_net<24>(&S.rec[off], cnt);
             }
         }
     }
