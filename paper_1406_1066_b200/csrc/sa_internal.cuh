@@ -23,7 +23,7 @@ constexpr uint32_t POSMASK = 0x7fffffffu;
 constexpr int TILE = 2048;
 constexpr int TILE_THREADS = 128;
 constexpr int WIN = TILE / TILE_THREADS;  // 16 record positions per thread
-constexpr int BIGCOL = 512;
+constexpr int BIGCOL = 384;
 constexpr int TCAP = TILE + BIGCOL;
 
 // One big column (k_col_scan appends, k_bigcol folds, k_tile_fold copies out).

@@ -48,6 +48,7 @@ struct WarpScratch {
 
 struct TileSmem {
     int4 rec[TCAP];                    // the tile's records (TMA destination)
+    uint8_t perm[TCAP];                // per column: sorted order, then output slots
     WarpScratch ws[NWARP];
     int lcol[LCAP];                    // long columns: record offset | (count << 16)
     unsigned long long mbar;
@@ -165,10 +166,10 @@ __device__ int fold_column(int4 *R, int c) {
 // Short column (c <= W records): static Batcher sorting network on the
 // (row, position) keys held in registers -- compare-exchanges within a layer
 // are independent, so the sort runs at instruction throughput instead of
-// shared-memory latency -- then one pass folds each run of equal rows.
-// Outputs compacted in place at R[0..u), R[0].y = u.
+// shared-memory latency.  Writes the sorted order to perm and returns the
+// number of distinct rows u (the values are folded later, fold_from_perm).
 template <int W>
-__device__ int fold_short_net(int4 *R, int c) {
+__device__ int fold_short_net(const int4 *R, int c, uint8_t *perm) {
     unsigned long long k[W];
     int sl[W];
 #pragma unroll
@@ -201,33 +202,41 @@ __device__ int fold_short_net(int4 *R, int c) {
         SA_NET24(SA_CE)
     }
 #undef SA_CE
-    int row[W];
-    double v[W];
+    int u = 1;
 #pragma unroll
     for (int w = 0; w < W; ++w) {
-        row[w] = (int)(k[w] >> 32);
-        v[w] = (w < c) ? *reinterpret_cast<const double *>(&R[sl[w]].z) : 0.0;
+        if (w < c) perm[w] = (uint8_t)sl[w];
+        if (w > 0 && w < c && (k[w] >> 32) != (k[w - 1] >> 32)) ++u;
     }
+    return u;
+}
+
+// Fold a short column from its sorted order: each run of equal rows from
+// +0.0 in input-position order.  A run's output (row-1, value) is stored in
+// the slot of the run's first record (already read, never read again),
+// with un (the column's output count) in its .y, and perm[j] becomes the
+// slot of output j.
+__device__ void fold_from_perm(int4 *R, uint8_t *perm, int c, int un) {
+    int head = perm[0];
+    int4 x = R[head];
+    int prev = x.x;
+    double acc = fold_add(0.0, rec_val(x));
     int u = 0;
-    int prev = row[0];
-    double acc = fold_add(0.0, v[0]);
-#pragma unroll
-    for (int w = 1; w < W; ++w) {
-        if (w < c) {
-            if (row[w] != prev) {
-                R[u] = make_int4(prev - 1, 0, __double2loint(acc), __double2hiint(acc));
-                ++u;
-                prev = row[w];
-                acc = fold_add(0.0, v[w]);
-            } else {
-                acc = fold_add(acc, v[w]);
-            }
+    for (int w = 1; w < c; ++w) {
+        const int sl = perm[w];
+        const int4 y = R[sl];
+        if (y.x != prev) {
+            R[head] = make_int4(prev - 1, un, __double2loint(acc), __double2hiint(acc));
+            perm[u++] = (uint8_t)head;
+            head = sl;
+            prev = y.x;
+            acc = fold_add(0.0, rec_val(y));
+        } else {
+            acc = fold_add(acc, rec_val(y));
         }
     }
-    R[u] = make_int4(prev - 1, 0, __double2loint(acc), __double2hiint(acc));
-    ++u;
-    R[0].y = u;
-    return u;
+    R[head] = make_int4(prev - 1, un, __double2loint(acc), __double2hiint(acc));
+    perm[u] = (uint8_t)head;
 }
 
 __device__ __forceinline__ int warp_incl_sum(int x) {
@@ -375,36 +384,37 @@ __device__ int fold_column_warp(int4 *R, int c, WarpScratch &W) {
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
         const int t = lane + 32 * k;
-        if (t < u) R[rank[k]] = make_int4(tab[k] - 1, 0, __double2loint(acc[k]), __double2hiint(acc[k]));
+        if (t < u) R[rank[k]] = make_int4(tab[k] - 1, u, __double2loint(acc[k]), __double2hiint(acc[k]));
     }
-    __syncwarp();
-    if (lane == 0) R[0].y = u;
     __syncwarp();
     return u;
 }
 
-// Warp-level decoupled look-back (32 predecessors per L2 round trip).
+// Publish tile b's aggregate (the inclusive prefix right away for tile 0).
+__device__ __forceinline__ void lookback_publish(unsigned long long *st, long long b,
+                                                 unsigned long long agg) {
+    volatile unsigned long long *vst = st;
+    __threadfence();
+    vst[b] = lb_pack(b == 0 ? 2 : 1, agg);
+}
+
+// Warp-level decoupled look-back (32 predecessors per L2 round trip, with
+// back-off); the aggregate was published before.  Returns the exclusive
+// prefix and publishes the inclusive one.
 __device__ long long lookback_warp32(unsigned long long *st, long long b, unsigned long long agg) {
     const int lane = threadIdx.x & 31;
     volatile unsigned long long *vst = st;
-    if (b == 0) {
-        if (lane == 0) {
-            __threadfence();
-            vst[0] = lb_pack(2, agg);
-        }
-        return 0;
-    }
-    if (lane == 0) {
-        __threadfence();
-        vst[b] = lb_pack(1, agg);
-    }
+    if (b == 0) return 0;
     unsigned long long excl = 0;
     long long base = b - 1;
     while (base >= 0) {
         const long long idx = base - lane;
         const unsigned long long w = (idx >= 0) ? vst[idx] : lb_pack(2, 0);
         const unsigned flag = (unsigned)(w >> 62);
-        if (__any_sync(FULL, flag == 0)) continue;
+        if (__any_sync(FULL, flag == 0)) {
+            __nanosleep(64);
+            continue;
+        }
         const unsigned pm = __ballot_sync(FULL, flag == 2);
         const int stop = pm ? (__ffs(pm) - 1) : 31;
         unsigned long long v = (lane <= stop) ? (w & LB_VALMASK) : 0ull;
@@ -484,13 +494,15 @@ __global__ void __launch_bounds__(NT) k_tile_fold(const uint32_t *__restrict__ s
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) wmax = max(wmax, __shfl_xor_sync(FULL, wmax, o));
             if (wmax == 0) continue;
+            int u = 0;
             if (wmax <= 8) {
-                if (cnt) fold_short_net<8>(&S.rec[off], cnt);
+                if (cnt) u = fold_short_net<8>(&S.rec[off], cnt, &S.perm[off]);
             } else if (wmax <= 16) {
-                if (cnt) fold_short_net<16>(&S.rec[off], cnt);
+                if (cnt) u = fold_short_net<16>(&S.rec[off], cnt, &S.perm[off]);
             } else {
-                if (cnt) fold_short_net<24>(&S.rec[off], cnt);
+                if (cnt) u = fold_short_net<24>(&S.rec[off], cnt, &S.perm[off]);
             }
+            if (cnt) S.rec[off].y = u;  // input positions are no longer needed
         }
     }
     __syncthreads();
@@ -499,12 +511,14 @@ __global__ void __launch_bounds__(NT) k_tile_fold(const uint32_t *__restrict__ s
         const int nl = min(S.nlong, LCAP);
         for (int e = warp; e < nl; e += NWARP) {
             const int v = S.lcol[e];
-            fold_column_warp(&S.rec[v & 0xffff], v >> 16, S.ws[warp]);
+            const int off = v & 0xffff;
+            const int u = fold_column_warp(&S.rec[off], v >> 16, S.ws[warp]);
+            for (int j = lane; j < u; j += 32) S.perm[off + j] = (uint8_t)j;
         }
     }
     __syncthreads();
 
-    // ---- tile count, thread output bases, look-back --------------------------------
+    // ---- tile count and thread output bases; publish the aggregate early -------
     int ut = 0;
     for (int c = c_lo; c < c_hi; ++c) {
         const uint32_t w0 = sstart[c];
@@ -523,6 +537,19 @@ __global__ void __launch_bounds__(NT) k_tile_fold(const uint32_t *__restrict__ s
         U += v;
     }
     const int tbase = wpre + inc - ut;  // this thread's first output, tile-local
+    if (tid == 0) lookback_publish(tile_state, b, (unsigned long long)U);
+
+    // ---- pass 3: fold the short columns' values (predecessors publish meanwhile)
+    if (staged) {
+        for (int c = c_lo; c < c_hi; ++c) {
+            const uint32_t w0 = sstart[c];
+            if (w0 & BIGFLAG) continue;
+            const int s0 = (int)(w0 & POSMASK), s1 = (int)(sstart[c + 1] & POSMASK);
+            const int cnt = s1 - s0;
+            if (cnt > 0 && cnt <= SHORT_COL)
+                fold_from_perm(&S.rec[s0 - r0], &S.perm[s0 - r0], cnt, S.rec[s0 - r0].y);
+        }
+    }
     if (warp == 0) {
         const long long P = lookback_warp32(tile_state, b, (unsigned long long)U);
         if (lane == 0) S.P = P;
@@ -554,9 +581,10 @@ __global__ void __launch_bounds__(NT) k_tile_fold(const uint32_t *__restrict__ s
             o += ub;
         } else if (s1 > s0 && staged) {
             const int4 *R = &S.rec[s0 - r0];
-            const int u = R[0].y;
+            const uint8_t *pm = &S.perm[s0 - r0];
+            const int u = R[pm[0]].y;  // every output record carries u
             for (int k = 0; k < u; ++k) {
-                const int4 r = R[k];
+                const int4 r = R[pm[k]];
                 if (o + k < cap) {
                     ir[o + k] = r.x;
                     pr[o + k] = rec_val(r);
