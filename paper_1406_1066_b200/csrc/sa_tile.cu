@@ -512,8 +512,7 @@ __global__ void __launch_bounds__(NT) k_tile_fold(const uint32_t *__restrict__ s
         for (int e = warp; e < nl; e += NWARP) {
             const int v = S.lcol[e];
             const int off = v & 0xffff;
-            const int u = fold_column_warp(&S.rec[off], v >> 16, S.ws[warp]);
-            for (int j = lane; j < u; j += 32) S.perm[off + j] = (uint8_t)j;
+            fold_column_warp(&S.rec[off], v >> 16, S.ws[warp]);  // outputs at R[0..u)
         }
     }
     __syncthreads();
@@ -582,9 +581,10 @@ __global__ void __launch_bounds__(NT) k_tile_fold(const uint32_t *__restrict__ s
         } else if (s1 > s0 && staged) {
             const int4 *R = &S.rec[s0 - r0];
             const uint8_t *pm = &S.perm[s0 - r0];
-            const int u = R[pm[0]].y;  // every output record carries u
+            const bool shrt = s1 - s0 <= SHORT_COL;  // short: outputs at slots pm[k]
+            const int u = R[shrt ? pm[0] : 0].y;     // every output record carries u
             for (int k = 0; k < u; ++k) {
-                const int4 r = R[pm[k]];
+                const int4 r = R[shrt ? pm[k] : k];
                 if (o + k < cap) {
                     ir[o + k] = r.x;
                     pr[o + k] = rec_val(r);
