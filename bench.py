@@ -223,22 +223,40 @@ def main():
     asm._bind_stream()
     stream = torch.cuda.current_stream(dev)
 
-    def step():
-        rc = lib.sa_assemble_async(ctx, w.ii.data_ptr(), w.jj.data_ptr(), w.s.data_ptr(), 1, L, M, N,
-                                   jc.data_ptr(), ir.data_ptr(), pr.data_ptr(), cap)
-        if rc:
-            raise RuntimeError(asm._msg())
+    if world > 1:
+        # column-block sharding: histogram + all_reduce, stable partition,
+        # NCCL all_to_all of the triplets, local CUDA assembly, nnz all_gather
+        from paper_1406_1066_b200.distributed import assemble_sharded, gpu_local_assembler
+
+        local = gpu_local_assembler(local)
+        shard_info = {}
+
+        def step():
+            res = assemble_sharded(w.ii, w.jj, w.s, M, N, local)
+            shard_info["nnz"] = res.nnz_total
+            shard_info["sent_remote"] = res.sent_remote
+            shard_info["recv"] = res.recv_triplets
+    else:
+        def step():
+            rc = lib.sa_assemble_async(ctx, w.ii.data_ptr(), w.jj.data_ptr(), w.s.data_ptr(), 1, L,
+                                       M, N, jc.data_ptr(), ir.data_ptr(), pr.data_ptr(), cap)
+            if rc:
+                raise RuntimeError(asm._msg())
 
     # correctness of the configuration (device result must be complete)
     step()
     import ctypes
 
-    nnz_c = ctypes.c_int64(0)
-    rc = lib.sa_finish(ctx, ctypes.byref(nnz_c), None, None)
-    if rc:
-        raise RuntimeError(f"assembly failed: {asm._msg()}")
-    nnz = nnz_c.value
-    launches_per_step = lib.sa_last_launch_count(ctx)
+    if world > 1:
+        nnz = shard_info["nnz"]
+        launches_per_step = lib.sa_last_launch_count(ctx)
+    else:
+        nnz_c = ctypes.c_int64(0)
+        rc = lib.sa_finish(ctx, ctypes.byref(nnz_c), None, None)
+        if rc:
+            raise RuntimeError(f"assembly failed: {asm._msg()}")
+        nnz = nnz_c.value
+        launches_per_step = lib.sa_last_launch_count(ctx)
 
     for _ in range(args.warmup):
         step()
@@ -306,13 +324,34 @@ def main():
     hj.copy_(w.jj)
     hs.copy_(w.s)
     hin, hjn, hsn = hi.numpy(), hj.numpy(), hs.numpy()
-    out = sa.assemble(hin, hjn, hsn, m=M, n=N, device=local)  # warm-up
+    d2h = 4 * (N + 1) + 12 * nnz
+    if world > 1:
+        # host chunk -> device, sharded assembly, the rank's column block -> host
+        def e2e_call():
+            di = hi.to(dev, non_blocking=True)
+            dj = hj.to(dev, non_blocking=True)
+            ds = hs.to(dev, non_blocking=True)
+            res = assemble_sharded(di, dj, ds, M, N, local)
+            return res.jc.cpu(), res.ir.cpu(), res.pr.cpu()
+
+        jc_h, ir_h, pr_h = e2e_call()
+        d2h = 8 * len(jc_h) + 12 * len(ir_h)
+        out = None
+    else:
+        def e2e_call():
+            return sa.assemble(hin, hjn, hsn, m=M, n=N, device=local)
+
+        out = e2e_call()  # warm-up
     e2e_t = []
     for _ in range(max(1, args.e2e_steps)):
         torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
         t0 = time.perf_counter()
-        out = sa.assemble(hin, hjn, hsn, m=M, n=N, device=local)
+        r = e2e_call()
         e2e_t.append(time.perf_counter() - t0)
+        if world == 1:
+            out = r
     e2e_s = sum(e2e_t) / len(e2e_t)
     if world > 1:
         t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
@@ -348,13 +387,18 @@ def main():
                           "unit": "GB/s", "frac": path_gbs / peak_gbs},
         "kernel_ms": kern_ms,
         "e2e": {"value": L * world / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 16 * L,
-                "d2h_bytes_per_step": 4 * (N + 1) + 12 * nnz, "ms_per_step": e2e_s * 1e3},
+                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3},
         "gpu_launches": launches_per_step * args.steps,
         "launches_per_step": launches_per_step,
         "clocks": clk.summary(),
         "cpu_baseline": cpu,
         "parity_vs_cpu_reference": parity,
     }
+    if world > 1:
+        line["exchange"] = {"sent_remote_triplets_rank0": shard_info.get("sent_remote"),
+                            "received_triplets_rank0": shard_info.get("recv"),
+                            "collectives": "all_reduce(block histogram), all_to_all(triplets), "
+                                           "all_gather(nnz) over NCCL"}
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -1,0 +1,111 @@
+"""Host logic of the multi-GPU column-block assembly (paper_1406_1066_b200/
+distributed.py) with world_size 2 on CPU (gloo): the concatenation of the
+ranks' column blocks must equal the single-process oracle bit for bit.  The
+local assembler here is the CPU oracle (test infrastructure); on GPUs it is
+the CUDA pipeline (distributed.gpu_local_assembler)."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _oracle_local(ii, jj, s, m, n_local):
+    from oracle import oracle as O
+
+    out = O.assemble_counting(ii.numpy(), jj.numpy(), s.numpy(), m, n_local)
+    return torch.from_numpy(out.jc), torch.from_numpy(out.ir), torch.from_numpy(out.pr)
+
+
+def _case(kind):
+    from paper_1406_1066_b200 import workloads as W
+    from instances import random_triplets
+
+    if kind == "fem2d":
+        w = W.fem2d(24)
+        return w.ii.numpy(), w.jj.numpy(), w.s.numpy(), w.m, w.n
+    if kind == "fem3d":
+        w = W.fem3d(5)
+        return w.ii.numpy(), w.jj.numpy(), w.s.numpy(), w.m, w.n
+    if kind == "heavy":
+        w = W.heavy_dup(m=500, positions=3000, seed=2)
+        return w.ii.numpy(), w.jj.numpy(), w.s.numpy(), w.m, w.n
+    ii, jj, s = random_triplets(1_000_777, max_len=20_000, max_dim=300)
+    ii, jj = ii.astype(np.int32), jj.astype(np.int32)
+    return ii, jj, s, int(ii.max(initial=0)), int(jj.max(initial=0))
+
+
+def _worker(rank, world, port, kind, result_q):
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path[:0] = [root, os.path.join(root, "tests")]
+    from paper_1406_1066_b200.distributed import assemble_sharded
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    try:
+        ii, jj, s, m, n = _case(kind)
+        L = len(ii)
+        lo, hi = L * rank // world, L * (rank + 1) // world
+        res = assemble_sharded(torch.from_numpy(ii[lo:hi].copy()), torch.from_numpy(jj[lo:hi].copy()),
+                               torch.from_numpy(s[lo:hi].copy()), m, n, _oracle_local, nblocks=64)
+        result_q.put((rank, res.col_lo, res.col_hi, res.jc.numpy(), res.ir.numpy(), res.pr.numpy(),
+                      res.nnz_offset, res.nnz_total, res.sent_remote))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("kind", ["fem2d", "fem3d", "heavy", "random"])
+def test_two_rank_column_blocks_match_single_process(kind):
+    from oracle import oracle as O
+
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, kind, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = sorted([q.get(timeout=180) for _ in range(world)])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    ii, jj, s, m, n = _case(kind)
+    ref = O.assemble_counting(ii, jj, s, m, n)
+    # stitch the column blocks back together
+    jc = [0]
+    ir, pr = [], []
+    assert got[0][1] == 0 and got[-1][2] == n
+    for rank, lo, hi, bjc, bir, bpr, off, tot, _ in got:
+        assert bjc[0] == off and tot == ref.nnz
+        jc.extend(bjc[1:].tolist())
+        ir.append(bir)
+        pr.append(bpr)
+    assert np.array_equal(np.array(jc), ref.jc)
+    assert np.array_equal(np.concatenate(ir), ref.ir)
+    assert np.concatenate(pr).tobytes() == ref.pr.tobytes()
+    if kind in ("fem2d", "fem3d"):
+        # element order keeps most triplets local
+        sent = sum(g[-1] for g in got)
+        assert sent < 0.25 * len(ii)
+
+
+def test_block_boundaries_balance():
+    from paper_1406_1066_b200.distributed import block_boundaries
+
+    hist = torch.tensor([10, 0, 30, 10, 50, 0, 0, 100], dtype=torch.int64)
+    b = block_boundaries(hist, 4, 8, 80)
+    assert b[0] == 0 and b[-1] == 80 and all(x <= y for x, y in zip(b, b[1:]))
+    b1 = block_boundaries(torch.zeros(8, dtype=torch.int64), 2, 8, 80)
+    assert b1 == [0, 40, 80]
