@@ -138,6 +138,14 @@ int sa_host_assemble(sa_ctx *ctx, int32_t M, int32_t N, int64_t *nnz, int64_t *b
                      int *bad_which);
 int sa_host_fetch(sa_ctx *ctx, int32_t *h_jc, int32_t *h_ir, double *h_pr);
 
+/*
+ * Page-locked host buffers from a process-wide cache (size classes of powers
+ * of two), for host outputs that the device->host copies fill at full link
+ * bandwidth.  sa_host_buffer returns NULL on failure.
+ */
+void *sa_host_buffer(uint64_t bytes);
+void sa_host_buffer_release(void *ptr);
+
 /* Number of kernel launches enqueued by the last sa_assemble_async. */
 int sa_last_launch_count(const sa_ctx *ctx);
 

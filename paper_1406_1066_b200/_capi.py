@@ -54,6 +54,8 @@ SIGNATURES = {
     "sa_host_fetch": (_int, [_vp, _vp, _vp, _vp]),
     "sa_last_launch_count": (_int, [_vp]),
     "sa_enable_timing": (_int, [_vp, _int]),
+    "sa_host_buffer": (_vp, [ctypes.c_uint64]),
+    "sa_host_buffer_release": (None, [_vp]),
     "sa_last_kernel_times": (_int, [_vp, _int, ctypes.POINTER(ctypes.c_float),
                                     ctypes.POINTER(ctypes.c_char_p)]),
 }

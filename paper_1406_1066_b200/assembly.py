@@ -250,13 +250,29 @@ class Assembler:
         self._raise(rc)
 
 
-def _pinned_empty(n, dtype):
-    """numpy array backed by pinned host memory (freed back to torch's cache
-    when the array dies)."""
-    import torch
+class _PinnedBlock:
+    """Owner of one page-locked block from the library's host-buffer cache;
+    numpy arrays (and every view of them) keep it alive through .base."""
 
-    tdt = {np.int32: torch.int32, np.float64: torch.float64}[dtype]
-    return torch.empty(max(int(n), 0), dtype=tdt, pin_memory=True).numpy()
+    def __init__(self, lib, n, dtype):
+        self._lib = lib
+        nbytes = max(int(n), 1) * np.dtype(dtype).itemsize
+        self._ptr = lib.sa_host_buffer(nbytes)
+        if not self._ptr:
+            raise MemoryError(f"page-locked host allocation of {nbytes} bytes failed")
+        self.__array_interface__ = {"data": (self._ptr, False), "shape": (int(n),),
+                                    "typestr": np.dtype(dtype).str, "version": 3}
+
+    def __del__(self):
+        if getattr(self, "_ptr", None):
+            self._lib.sa_host_buffer_release(self._ptr)
+            self._ptr = None
+
+
+def _pinned_empty(n, dtype):
+    """numpy array in page-locked memory (returned to the cache when the
+    array and all its views are gone)."""
+    return np.asarray(_PinnedBlock(_capi.load(), n, dtype))
 
 
 def _bad_value(arr, k):

@@ -4,7 +4,11 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
+#include <unordered_map>
+#include <vector>
 
 #include "../../include/sparse_assembly.h"
 #include "sa_internal.cuh"
@@ -163,7 +167,67 @@ int mark(sa_ctx *ctx, const char *name) {
 
 }  // namespace
 
+// ---- process-wide cache of page-locked host buffers ------------------------
+namespace {
+struct PinnedCache {
+    std::mutex mu;
+    std::map<uint64_t, std::vector<void *>> free_by_class;  // class bytes -> blocks
+    std::unordered_map<void *, uint64_t> live;               // block -> class bytes
+    uint64_t cached = 0;
+    static constexpr uint64_t kMaxCached = 8ull << 30;
+};
+PinnedCache &pinned_cache() {
+    static PinnedCache *c = new PinnedCache();  // leaked on purpose (process lifetime)
+    return *c;
+}
+uint64_t size_class(uint64_t b) {
+    uint64_t c = 1ull << 16;
+    while (c < b) c <<= 1;
+    return c;
+}
+}  // namespace
+
 extern "C" {
+
+void *sa_host_buffer(uint64_t bytes) {
+    PinnedCache &pc = pinned_cache();
+    const uint64_t cls = size_class(std::max<uint64_t>(bytes, 1));
+    {
+        std::lock_guard<std::mutex> g(pc.mu);
+        auto it = pc.free_by_class.find(cls);
+        if (it != pc.free_by_class.end() && !it->second.empty()) {
+            void *p = it->second.back();
+            it->second.pop_back();
+            pc.cached -= cls;
+            pc.live[p] = cls;
+            return p;
+        }
+    }
+    void *p = nullptr;
+    if (cudaHostAlloc(&p, cls, cudaHostAllocPortable) != cudaSuccess) return nullptr;
+    std::lock_guard<std::mutex> g(pc.mu);
+    pc.live[p] = cls;
+    return p;
+}
+
+void sa_host_buffer_release(void *ptr) {
+    if (!ptr) return;
+    PinnedCache &pc = pinned_cache();
+    uint64_t cls = 0;
+    {
+        std::lock_guard<std::mutex> g(pc.mu);
+        auto it = pc.live.find(ptr);
+        if (it == pc.live.end()) return;
+        cls = it->second;
+        pc.live.erase(it);
+        if (pc.cached + cls <= PinnedCache::kMaxCached) {
+            pc.free_by_class[cls].push_back(ptr);
+            pc.cached += cls;
+            return;
+        }
+    }
+    cudaFreeHost(ptr);
+}
 
 int sa_enable_timing(sa_ctx *ctx, int on) {
     if (!ctx) return SA_ERR_INVALID_ARG;
