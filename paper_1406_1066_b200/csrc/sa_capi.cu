@@ -381,7 +381,7 @@ int sa_assemble_async(sa_ctx *ctx, const int32_t *d_ii, const int32_t *d_jj, con
     const int64_t nbig_max = L / (BIGCOL + 1) + 1;
     const int64_t ntiles = (L + nbig_max + TILE - 1) / TILE;
     const int64_t nwin = ntiles * TILE_THREADS;
-    const int64_t nscan = (N + 4095) / 4096;
+    const int64_t nscan = (N + 8191) / 8192;
     SA_CUDA(ctx, ensure(ctx->cur, ctx->cur_cap, (size_t)N + 4));
     SA_CUDA(ctx, ensure(ctx->sstart, ctx->st_cap, (size_t)N + 1));
     SA_CUDA(ctx, ensure(ctx->rec, ctx->rec_cap, (size_t)(L + nbig_max)));

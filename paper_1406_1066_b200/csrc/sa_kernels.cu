@@ -193,7 +193,7 @@ cudaError_t launch_hist(Launch &lc, const int32_t *ii, const int32_t *jj, int64_
 //   big_list[]    big columns {col, big-space start, n}; bigk[c] = list index
 //   err->lsmall   size of the small space
 // ---------------------------------------------------------------------------
-constexpr int SCAN_NT = 256;
+constexpr int SCAN_NT = 512;
 constexpr int SCAN_IPT = 16;
 constexpr int SCAN_TILE = SCAN_NT * SCAN_IPT;
 constexpr unsigned long long SMALL_MASK = (1ull << 31) - 1;
