@@ -441,8 +441,7 @@ __global__ void __launch_bounds__(AGG_NT) k_scatter(const int32_t *__restrict__ 
                                                     ErrState *err) {
     extern __shared__ __align__(16) unsigned char scat_smem[];
     AggSmem &A = *reinterpret_cast<AggSmem *>(scat_smem);
-    constexpr size_t kStageOff = (sizeof(AggSmem) + 15) & ~size_t(15);
-    int4 *stage = reinterpret_cast<int4 *>(scat_smem + kStageOff);  // CHUNK records
+    int4 *stage = reinterpret_cast<int4 *>(scat_smem + sizeof(AggSmem));  // CHUNK records
     uint32_t *stage_pos = reinterpret_cast<uint32_t *>(stage + CHUNK);     // their slots
     __shared__ int s_warp[AGG_NT / 32];
     const int tid = threadIdx.x;
@@ -571,7 +570,7 @@ cudaError_t launch_scatter(Launch &lc, const int32_t *ii, const int32_t *jj, con
     const int vec = aligned16(ii) && aligned16(jj) && (s_stride == 0 || aligned16(s));
     const int64_t nchunk = (L + CHUNK - 1) / CHUNK;
     int grid = (int)std::min<int64_t>(nchunk, (int64_t)lc.num_sms * 2);
-    const size_t smem = ((sizeof(AggSmem) + 15) & ~size_t(15)) + (size_t)CHUNK * (sizeof(int4) + sizeof(uint32_t));
+    const size_t smem = sizeof(AggSmem) + (size_t)CHUNK * (sizeof(int4) + sizeof(uint32_t));
     cudaError_t e = cudaFuncSetAttribute(k_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return e;
