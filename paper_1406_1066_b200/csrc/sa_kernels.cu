@@ -439,11 +439,7 @@ __global__ void __launch_bounds__(AGG_NT) k_scatter(const int32_t *__restrict__ 
                                                     uint32_t *__restrict__ cur,
                                                     int4 *__restrict__ rec, int vec,
                                                     ErrState *err) {
-    extern __shared__ __align__(16) unsigned char scat_smem[];
-    AggSmem &A = *reinterpret_cast<AggSmem *>(scat_smem);
-    int4 *stage = reinterpret_cast<int4 *>(scat_smem + sizeof(AggSmem));  // CHUNK records
-    uint32_t *stage_pos = reinterpret_cast<uint32_t *>(stage + CHUNK);     // their slots
-    __shared__ int s_warp[AGG_NT / 32];
+    __shared__ AggSmem A;
     const int tid = threadIdx.x;
     for (int k = tid; k < HT; k += AGG_NT) {
         A.key[k] = 0;
@@ -506,43 +502,19 @@ __global__ void __launch_bounds__(AGG_NT) k_scatter(const int32_t *__restrict__ 
             }
         }
         __syncthreads();
-        // reserve each column's slots (one global atomic per distinct column),
-        // and give each column a contiguous range of the staging buffer
         const int nu = A.nused;
-        constexpr int EPT = CHUNK / AGG_NT;  // used slots per thread (nu <= CHUNK)
-        int cnt_l[EPT];
-        int run = 0;
-#pragma unroll
-        for (int q = 0; q < EPT; ++q) {
-            const int e = tid * EPT + q;
-            cnt_l[q] = 0;
-            if (e < nu) {
-                const int h = A.used[e];
-                cnt_l[q] = A.ctr[h];
-                A.ctr[h] = (int)atomicAdd(&cur[A.key[h] - 1], (uint32_t)cnt_l[q]);
-            }
-            run += cnt_l[q];
-        }
-        int tot;
-        int pre = block_excl_sum<AGG_NT, int>(run, s_warp, tot);  // ends with a barrier
-#pragma unroll
-        for (int q = 0; q < EPT; ++q) {
-            const int e = tid * EPT + q;
-            if (e < nu) A.key[A.used[e]] = pre;  // keys are dead now: local run base
-            pre += cnt_l[q];
+        for (int e = tid; e < nu; e += AGG_NT) {
+            const int h = A.used[e];
+            A.ctr[h] = (int)atomicAdd(&cur[A.key[h] - 1], (uint32_t)A.ctr[h]);
         }
         __syncthreads();
 #pragma unroll
         for (int k = 0; k < CPT; ++k) {
             if (hk[k] < 0) continue;
             const uint32_t bw = (uint32_t)A.ctr[hk[k]];
-            const int q = A.key[hk[k]] + rk[k];
-            stage[q] = make_int4(iv[k], (int)(t0 + k), __double2loint(vv[k]), __double2hiint(vv[k]));
-            stage_pos[q] = (bw & POSMASK) + ((bw & BIGFLAG) ? lsmall : 0u) + (uint32_t)rk[k];
+            const uint32_t pos = (bw & POSMASK) + ((bw & BIGFLAG) ? lsmall : 0u) + (uint32_t)rk[k];
+            rec[pos] = make_int4(iv[k], (int)(t0 + k), __double2loint(vv[k]), __double2hiint(vv[k]));
         }
-        __syncthreads();
-        // consecutive lanes write consecutive slots of each column's run
-        for (int q = tid; q < tot; q += AGG_NT) rec[stage_pos[q]] = stage[q];
         __syncthreads();
         for (int e = tid; e < nu; e += AGG_NT) {
             const int h = A.used[e];
@@ -569,12 +541,8 @@ cudaError_t launch_scatter(Launch &lc, const int32_t *ii, const int32_t *jj, con
     if (L <= 0) return cudaSuccess;
     const int vec = aligned16(ii) && aligned16(jj) && (s_stride == 0 || aligned16(s));
     const int64_t nchunk = (L + CHUNK - 1) / CHUNK;
-    int grid = (int)std::min<int64_t>(nchunk, (int64_t)lc.num_sms * 2);
-    const size_t smem = sizeof(AggSmem) + (size_t)CHUNK * (sizeof(int4) + sizeof(uint32_t));
-    cudaError_t e = cudaFuncSetAttribute(k_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
-    if (e != cudaSuccess) return e;
-    k_scatter<<<grid, AGG_NT, smem, lc.stream>>>(ii, jj, s, s_stride, L, M, N, cur, rec, vec, err);
+    int grid = (int)std::min<int64_t>(nchunk, (int64_t)lc.num_sms * 4);
+    k_scatter<<<grid, AGG_NT, 0, lc.stream>>>(ii, jj, s, s_stride, L, M, N, cur, rec, vec, err);
     lc.launches++;
     return cudaGetLastError();
 }
