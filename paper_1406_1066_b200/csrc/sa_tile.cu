@@ -196,8 +196,12 @@ __device__ int fold_short_net(const int4 *R, int c, uint8_t *perm) {
     }
     if constexpr (W == 8) {
         SA_NET8(SA_CE)
+    } else if constexpr (W == 12) {
+        SA_NET12(SA_CE)
     } else if constexpr (W == 16) {
         SA_NET16(SA_CE)
+    } else if constexpr (W == 18) {
+        SA_NET18(SA_CE)
     } else {
         SA_NET24(SA_CE)
     }
@@ -497,8 +501,12 @@ __global__ void __launch_bounds__(NT) k_tile_fold(const uint32_t *__restrict__ s
             int u = 0;
             if (wmax <= 8) {
                 if (cnt) u = fold_short_net<8>(&S.rec[off], cnt, &S.perm[off]);
+            } else if (wmax <= 12) {
+                if (cnt) u = fold_short_net<12>(&S.rec[off], cnt, &S.perm[off]);
             } else if (wmax <= 16) {
                 if (cnt) u = fold_short_net<16>(&S.rec[off], cnt, &S.perm[off]);
+            } else if (wmax <= 18) {
+                if (cnt) u = fold_short_net<18>(&S.rec[off], cnt, &S.perm[off]);
             } else {
                 if (cnt) u = fold_short_net<24>(&S.rec[off], cnt, &S.perm[off]);
             }
