@@ -165,34 +165,23 @@ __device__ int fold_column(int4 *R, int c) {
 
 // Short column (c <= W records): static Batcher sorting network on the
 // (row, position) keys held in registers -- compare-exchanges within a layer
-// are independent, so the sort runs at instruction throughput instead of
-// shared-memory latency.  Writes the sorted order to perm and returns the
-// number of distinct rows u (the values are folded later, fold_from_perm).
-template <int W>
-__device__ int fold_short_net(const int4 *R, int c, uint8_t *perm) {
-    unsigned long long k[W];
-    int sl[W];
-#pragma unroll
-    for (int w = 0; w < W; ++w) {
-        if (w < c) {
-            const int2 kk = *reinterpret_cast<const int2 *>(&R[w]);
-            k[w] = ((unsigned long long)(unsigned)kk.x << 32) | (unsigned)kk.y;
-        } else {
-            k[w] = ~0ull;
-        }
-        sl[w] = w;
-    }
-#define SA_CE(i, j)                                            \
-    {                                                          \
-        const bool sw = k[j] < k[i];                           \
-        const unsigned long long lo_ = sw ? k[j] : k[i];       \
-        const unsigned long long hi_ = sw ? k[i] : k[j];       \
-        const int sa_ = sw ? sl[j] : sl[i];                    \
-        const int sb_ = sw ? sl[i] : sl[j];                    \
-        k[i] = lo_;                                            \
-        k[j] = hi_;                                            \
-        sl[i] = sa_;                                           \
-        sl[j] = sb_;                                           \
+// are independent, so the sort runs at instruction throughput.  The key is
+// packed with the record slot so a compare-exchange is a min/max pair:
+//   32-bit  (row - rmin) | (pos - pmin) | slot   when the spans fit 27 bits
+//   64-bit  row | (pos - pmin) | slot            when the position span fits 27
+//   64-bit  row | pos, slot carried separately   otherwise
+// Writes the sorted order (record slots) to perm and returns the number of
+// distinct rows u; the values are folded later (fold_from_perm).
+__device__ __forceinline__ int span_bits(unsigned x) { return x ? 32 - __clz(x) : 0; }
+
+template <int W, typename K>
+__device__ __forceinline__ void run_network(K (&k)[W]) {
+#define SA_CE(i, j)                         \
+    {                                       \
+        const K lo_ = k[i] < k[j] ? k[i] : k[j]; \
+        const K hi_ = k[i] < k[j] ? k[j] : k[i]; \
+        k[i] = lo_;                         \
+        k[j] = hi_;                         \
     }
     if constexpr (W == 8) {
         SA_NET8(SA_CE)
@@ -206,11 +195,95 @@ __device__ int fold_short_net(const int4 *R, int c, uint8_t *perm) {
         SA_NET24(SA_CE)
     }
 #undef SA_CE
-    int u = 1;
+}
+
+template <int W>
+__device__ int fold_short_net(const int4 *R, int c, uint8_t *perm) {
+    int rowv[W], posv[W];
+    unsigned rmin = 0xffffffffu, rmax = 0u, pmin = 0xffffffffu, pmax = 0u;
 #pragma unroll
     for (int w = 0; w < W; ++w) {
-        if (w < c) perm[w] = (uint8_t)sl[w];
-        if (w > 0 && w < c && (k[w] >> 32) != (k[w - 1] >> 32)) ++u;
+        if (w < c) {
+            const int2 kk = *reinterpret_cast<const int2 *>(&R[w]);
+            rowv[w] = kk.x;
+            posv[w] = kk.y;
+            rmin = min(rmin, (unsigned)kk.x);
+            rmax = max(rmax, (unsigned)kk.x);
+            pmin = min(pmin, (unsigned)kk.y);
+            pmax = max(pmax, (unsigned)kk.y);
+        } else {
+            rowv[w] = 0;
+            posv[w] = 0;
+        }
+    }
+    const int rb = span_bits(rmax - rmin), pb = span_bits(pmax - pmin);
+    int u = 1;
+    if (rb + pb <= 27) {
+        const int sh = pb + 5;
+        unsigned k[W];
+#pragma unroll
+        for (int w = 0; w < W; ++w)
+            k[w] = (w < c) ? (unsigned)(((unsigned long long)((unsigned)rowv[w] - rmin) << sh) |
+                                        (((unsigned)posv[w] - pmin) << 5) | w)
+                           : 0xffffffffu;
+        run_network<W, unsigned>(k);
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+            if (w < c) perm[w] = (uint8_t)(k[w] & 31u);
+            if (w > 0 && w < c && ((unsigned long long)k[w] >> sh) != ((unsigned long long)k[w - 1] >> sh)) ++u;
+        }
+    } else if (pb <= 27) {
+        unsigned long long k[W];
+#pragma unroll
+        for (int w = 0; w < W; ++w)
+            k[w] = (w < c) ? (((unsigned long long)(unsigned)rowv[w] << 32) |
+                              ((((unsigned)posv[w] - pmin) << 5) | w))
+                           : ~0ull;
+        run_network<W, unsigned long long>(k);
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+            if (w < c) perm[w] = (uint8_t)(k[w] & 31u);
+            if (w > 0 && w < c && (k[w] >> 32) != (k[w - 1] >> 32)) ++u;
+        }
+    } else {
+        // full (row, position) keys with the slot carried alongside
+        unsigned long long k[W];
+        int sl[W];
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+            k[w] = (w < c) ? (((unsigned long long)(unsigned)rowv[w] << 32) | (unsigned)posv[w])
+                           : ~0ull - (unsigned long long)(W - w);
+            sl[w] = w;
+        }
+#define SA_CE(i, j)                                            \
+    {                                                          \
+        const bool sw = k[j] < k[i];                           \
+        const unsigned long long lo_ = sw ? k[j] : k[i];       \
+        const unsigned long long hi_ = sw ? k[i] : k[j];       \
+        const int sa_ = sw ? sl[j] : sl[i];                    \
+        const int sb_ = sw ? sl[i] : sl[j];                    \
+        k[i] = lo_;                                            \
+        k[j] = hi_;                                            \
+        sl[i] = sa_;                                           \
+        sl[j] = sb_;                                           \
+    }
+        if constexpr (W == 8) {
+            SA_NET8(SA_CE)
+        } else if constexpr (W == 12) {
+            SA_NET12(SA_CE)
+        } else if constexpr (W == 16) {
+            SA_NET16(SA_CE)
+        } else if constexpr (W == 18) {
+            SA_NET18(SA_CE)
+        } else {
+            SA_NET24(SA_CE)
+        }
+#undef SA_CE
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+            if (w < c) perm[w] = (uint8_t)sl[w];
+            if (w > 0 && w < c && (k[w] >> 32) != (k[w - 1] >> 32)) ++u;
+        }
     }
     return u;
 }
