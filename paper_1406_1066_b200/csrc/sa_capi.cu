@@ -27,7 +27,7 @@ struct sa_ctx {
     uint32_t *cur = nullptr;              size_t cur_cap = 0;     // N (counts, then cursors)
     uint32_t *sstart = nullptr;           size_t st_cap = 0;      // N+1 small-space starts
     int4 *rec = nullptr;                  size_t rec_cap = 0;     // L + placeholders
-    int32_t *win_first = nullptr;         size_t wf_cap = 0;      // nwin+1
+    int2 *tile_info = nullptr;            size_t ti_cap = 0;      // ntiles+1
     uint8_t *tile_big = nullptr;          size_t tb_cap = 0;      // ntiles
     unsigned long long *tile_state = nullptr; size_t ts_cap = 0;  // ntiles
     unsigned long long *scan_state = nullptr; size_t ss_cap = 0;  // scan CTAs
@@ -113,10 +113,10 @@ __global__ void k_init(ErrState *err, uint32_t *cur, int64_t ncur, unsigned long
     for (int64_t k = t0; k < nq; k += stride) cur4[k] = make_uint4(0, 0, 0, 0);
     for (int64_t k = (nq << 2) + t0; k < ncur; k += stride) cur[k] = 0;
     for (int64_t k = t0; k < nts; k += stride) {
-        ts[k] = 0ull;
+        ts[k * LB_STRIDE] = 0ull;
         tb[k] = 0;
     }
-    for (int64_t k = t0; k < nss; k += stride) ss[k] = 0ull;
+    for (int64_t k = t0; k < nss; k += stride) ss[k * LB_STRIDE] = 0ull;
 }
 
 int launch_init(sa_ctx *ctx, Launch &lc, int64_t ncur, int64_t nts, int64_t nss) {
@@ -279,7 +279,7 @@ void sa_destroy(sa_ctx *ctx) {
     cudaFree(ctx->cur);
     cudaFree(ctx->sstart);
     cudaFree(ctx->rec);
-    cudaFree(ctx->win_first);
+    cudaFree(ctx->tile_info);
     cudaFree(ctx->tile_big);
     cudaFree(ctx->tile_state);
     cudaFree(ctx->scan_state);
@@ -380,15 +380,14 @@ int sa_assemble_async(sa_ctx *ctx, const int32_t *d_ii, const int32_t *d_jj, con
 
     const int64_t nbig_max = L / (BIGCOL + 1) + 1;
     const int64_t ntiles = (L + nbig_max + TILE - 1) / TILE;
-    const int64_t nwin = ntiles * TILE_THREADS;
-    const int64_t nscan = (N + 8191) / 8192;
+    const int64_t nscan = (N + SCAN_TILE - 1) / SCAN_TILE;
     SA_CUDA(ctx, ensure(ctx->cur, ctx->cur_cap, (size_t)N + 4));
     SA_CUDA(ctx, ensure(ctx->sstart, ctx->st_cap, (size_t)N + 1));
     SA_CUDA(ctx, ensure(ctx->rec, ctx->rec_cap, (size_t)(L + nbig_max)));
-    SA_CUDA(ctx, ensure(ctx->win_first, ctx->wf_cap, (size_t)nwin + 1));
+    SA_CUDA(ctx, ensure(ctx->tile_info, ctx->ti_cap, (size_t)ntiles + 1));
     SA_CUDA(ctx, ensure(ctx->tile_big, ctx->tb_cap, (size_t)ntiles));
-    SA_CUDA(ctx, ensure(ctx->tile_state, ctx->ts_cap, (size_t)ntiles));
-    SA_CUDA(ctx, ensure(ctx->scan_state, ctx->ss_cap, (size_t)nscan));
+    SA_CUDA(ctx, ensure(ctx->tile_state, ctx->ts_cap, (size_t)ntiles * LB_STRIDE));
+    SA_CUDA(ctx, ensure(ctx->scan_state, ctx->ss_cap, (size_t)nscan * LB_STRIDE));
     SA_CUDA(ctx, ensure(ctx->big_list, ctx->bl_cap, (size_t)nbig_max));
     SA_CUDA(ctx, ensure(ctx->bigk, ctx->bk_cap, (size_t)N));
 
@@ -400,7 +399,7 @@ int sa_assemble_async(sa_ctx *ctx, const int32_t *d_ii, const int32_t *d_jj, con
     if ((rc = mark(ctx, "k_colcount"))) return rc;
     SA_CUDA(ctx, launch_colcount(lc, d_jj, L, N, ctx->cur, ctx->err));
     if ((rc = mark(ctx, "k_col_scan"))) return rc;
-    SA_CUDA(ctx, launch_col_scan(lc, ctx->cur, ctx->sstart, ctx->cur, N, nwin, ctx->win_first,
+    SA_CUDA(ctx, launch_col_scan(lc, ctx->cur, ctx->sstart, ctx->cur, N, ctx->tile_info,
                                  ctx->tile_big, ntiles, ctx->big_list, ctx->bigk, ctx->scan_state,
                                  ctx->err));
     if ((rc = mark(ctx, "k_scatter"))) return rc;
@@ -414,7 +413,7 @@ int sa_assemble_async(sa_ctx *ctx, const int32_t *d_ii, const int32_t *d_jj, con
                                    passes));
     }
     if ((rc = mark(ctx, "k_tile_fold"))) return rc;
-    SA_CUDA(ctx, launch_tile_fold(lc, ctx->sstart, ctx->win_first, ctx->tile_big, ntiles, ctx->rec,
+    SA_CUDA(ctx, launch_tile_fold(lc, ctx->sstart, ctx->tile_info, ctx->tile_big, ntiles, ctx->rec,
                                   ctx->big_list, ctx->bigk, ctx->tile_state, N, d_jc, d_ir, d_pr,
                                   cap, ctx->err));
     if ((rc = mark(ctx, nullptr))) return rc;

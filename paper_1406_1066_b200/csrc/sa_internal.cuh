@@ -15,6 +15,10 @@ constexpr unsigned FULL = 0xffffffffu;
 // columns; the low 31 bits are an offset.
 constexpr uint32_t BIGFLAG = 0x80000000u;
 constexpr uint32_t POSMASK = 0x7fffffffu;
+// k_col_scan: threads per CTA and consecutive columns per thread
+constexpr int SCAN_NT = 256;
+constexpr int SCAN_IPT = 8;  // multiple of 4 (16-byte vectors)
+constexpr int SCAN_TILE = SCAN_NT * SCAN_IPT;
 
 // Fold geometry (k_tile_fold).  Tile b owns the columns whose small-space
 // start lies in [b*TILE, (b+1)*TILE); inside the CTA, thread t owns the
@@ -70,6 +74,13 @@ __device__ __forceinline__ double fold_add(double acc, double v) {
 // status word: bits 63:62 flag (0 empty, 1 aggregate, 2 inclusive prefix),
 // bits 61:0 value.
 constexpr unsigned long long LB_VALMASK = (1ull << 62) - 1;
+// A status word carries its own payload (flag and value in one 64-bit
+// store), and consumers read nothing else the producer wrote, so publishing
+// needs no memory fence: a fence would only add ~0.5 us per chain hop.
+// One status word per 128-byte line: the words of neighbouring tiles land in
+// different L2 slices, so the polling of hundreds of CTAs does not queue on
+// one slice.
+constexpr int LB_STRIDE = 16;
 __device__ __forceinline__ unsigned long long lb_pack(unsigned flag, unsigned long long v) {
     return (static_cast<unsigned long long>(flag) << 62) | v;
 }
@@ -82,20 +93,18 @@ __device__ __forceinline__ unsigned long long lookback_warp(
     volatile unsigned long long *vst = st;
     if (b == 0) {
         if (lane == 0) {
-            __threadfence();
-            vst[0] = lb_pack(2, agg);
+            vst[(0) * LB_STRIDE] = lb_pack(2, agg);
         }
         return 0;
     }
     if (lane == 0) {
-        __threadfence();
-        vst[b] = lb_pack(1, agg);
+        vst[(b) * LB_STRIDE] = lb_pack(1, agg);
     }
     unsigned long long excl = 0;
     long long base = b - 1;
     while (true) {
         long long idx = base - lane;
-        unsigned long long w = (idx >= 0) ? vst[idx] : lb_pack(2, 0);
+        unsigned long long w = (idx >= 0) ? vst[(idx) * LB_STRIDE] : lb_pack(2, 0);
         unsigned flag = static_cast<unsigned>(w >> 62);
         if (__any_sync(FULL, flag == 0)) continue;  // predecessors not published yet
         unsigned pm = __ballot_sync(FULL, flag == 2);
@@ -108,8 +117,56 @@ __device__ __forceinline__ unsigned long long lookback_warp(
         base -= 32;
     }
     if (lane == 0) {
-        __threadfence();
-        vst[b] = lb_pack(2, excl + agg);
+        vst[(b) * LB_STRIDE] = lb_pack(2, excl + agg);
+    }
+    return excl;
+}
+
+// Block-wide look-back: each round reads NT predecessor words at once (one
+// per thread), so a CTA reaches the nearest inclusive prefix in one or two
+// L2 round trips even when hundreds of predecessors are in flight.  All
+// threads call it; returns the exclusive prefix of tile b.  s_red needs NT/32
+// slots.  Ends with a barrier.
+template <int NT>
+__device__ __forceinline__ unsigned long long lookback_block(unsigned long long *st, long long b,
+                                                             unsigned long long agg,
+                                                             unsigned long long *s_red,
+                                                             int *s_stop) {
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    volatile unsigned long long *vst = st;
+    if (tid == 0) {
+        vst[(b) * LB_STRIDE] = lb_pack(b == 0 ? 2 : 1, agg);
+    }
+    if (b == 0) return 0;
+    unsigned long long excl = 0;
+    long long base = b - 1;
+    while (true) {
+        const long long idx = base - tid;
+        unsigned long long wd;
+        do {
+            wd = (idx >= 0) ? vst[(idx) * LB_STRIDE] : lb_pack(2, 0);
+        } while ((wd >> 62) == 0);  // predecessor not published yet
+        if (tid == 0) *s_stop = NT;
+        __syncthreads();
+        const unsigned inc = __ballot_sync(FULL, (wd >> 62) == 2);
+        if (lane == 0 && inc) atomicMin(s_stop, w * 32 + __ffs(inc) - 1);
+        __syncthreads();
+        const int stop = *s_stop;
+        unsigned long long v = (tid <= stop) ? (wd & LB_VALMASK) : 0ull;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+        if (lane == 0) s_red[w] = v;
+        __syncthreads();
+        unsigned long long t = 0;
+#pragma unroll
+        for (int k = 0; k < NT / 32; ++k) t += s_red[k];
+        excl += t;
+        __syncthreads();  // s_red / s_stop reused next round
+        if (stop < NT) break;
+        base -= NT;
+    }
+    if (tid == 0) {
+        vst[(b) * LB_STRIDE] = lb_pack(2, excl + agg);
     }
     return excl;
 }
@@ -220,7 +277,7 @@ cudaError_t launch_convert(Launch &lc, const void *raw, int dtype, int64_t L, in
 cudaError_t launch_hist(Launch &lc, const int32_t *ii, const int32_t *jj, int64_t L,
                         int32_t M, int32_t N, uint32_t *cnt, ErrState *err, bool infer);
 cudaError_t launch_col_scan(Launch &lc, const uint32_t *cnt, uint32_t *sstart, uint32_t *cur,
-                            int32_t N, int64_t nwin, int32_t *win_first, uint8_t *tile_big,
+                            int32_t N, int2 *tile_info, uint8_t *tile_big,
                             int64_t ntiles, BigCol *big_list, uint32_t *bigk,
                             unsigned long long *scan_state, ErrState *err);
 cudaError_t launch_colcount(Launch &lc, const int32_t *jj, int64_t L, int32_t N, uint32_t *cnt,
@@ -230,7 +287,7 @@ cudaError_t launch_scatter(Launch &lc, const int32_t *ii, const int32_t *jj, con
                            int4 *rec, ErrState *err);
 cudaError_t launch_bigcol(Launch &lc, BigCol *big_list, const ErrState *err, int4 *rec,
                           const double *s, int64_t s_stride, int idx_bits, int passes);
-cudaError_t launch_tile_fold(Launch &lc, const uint32_t *sstart, const int32_t *win_first,
+cudaError_t launch_tile_fold(Launch &lc, const uint32_t *sstart, const int2 *tile_info,
                              const uint8_t *tile_big, int64_t ntiles, const int4 *rec,
                              const BigCol *big_list, const uint32_t *bigk,
                              unsigned long long *tile_state, int32_t N, int32_t *jc,

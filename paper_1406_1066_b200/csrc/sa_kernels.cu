@@ -188,89 +188,113 @@ cudaError_t launch_hist(Launch &lc, const int32_t *ii, const int32_t *jj, int64_
 //   sstart[c]     small-space start of column c (| BIGFLAG if big; a big
 //                 column sits at the start of the next small column)
 //   cur[c]        scatter cursor (small start, or big-space start | BIGFLAG)
-//   win_first[w]  min{c : sstart(c) >= w*WIN}, 0 <= w <= nwin (fold windows)
+//   tile_info[t]  {min{c : sstart(c) >= t*TILE}, its sstart}, 0 <= t <= ntiles
+//                 (the fold tile t owns the columns starting in its range)
 //   tile_big[b]   tile b owns a big column
 //   big_list[]    big columns {col, big-space start, n}; bigk[c] = list index
 //   err->lsmall   size of the small space
 // ---------------------------------------------------------------------------
-constexpr int SCAN_NT = 512;
-constexpr int SCAN_IPT = 16;
-constexpr int SCAN_TILE = SCAN_NT * SCAN_IPT;
 constexpr unsigned long long SMALL_MASK = (1ull << 31) - 1;
+#ifdef SA_TRACE
+__device__ unsigned long long g_trace[1 << 16][4];
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ unsigned smid_() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+    return r;
+}
+#define TRACE(b, k) if (threadIdx.x == 0 && (b) < (1 << 16)) g_trace[b][k] = gtime() | ((unsigned long long)smid_() << 54)
+#else
+#define TRACE(b, k)
+#endif
 
-__global__ void __launch_bounds__(SCAN_NT) k_col_scan(const uint32_t *__restrict__ cnt,
+// One column's contribution to the packed (big << 31 | small) prefix.
+__device__ __forceinline__ unsigned long long scan_word(uint32_t n) {
+    return (n > (uint32_t)BIGCOL) ? (((unsigned long long)n << 31) | 1ull) : n;
+}
+
+// Each thread owns SCAN_IPT = 8 consecutive columns: 16-byte loads of the
+// counts, 16-byte stores of sstart / cur, so the kernel streams at HBM speed;
+// small CTAs keep many of them resident per SM for memory parallelism.
+__global__ void __launch_bounds__(SCAN_NT) k_col_scan(const uint32_t *cnt,
                                                       uint32_t *__restrict__ sstart,
-                                                      uint32_t *__restrict__ cur, int32_t N,
-                                                      int64_t nwin, int32_t *__restrict__ win_first,
+                                                      uint32_t *cur, int32_t N,
+                                                      int2 *__restrict__ tile_info,
                                                       uint8_t *__restrict__ tile_big, int64_t ntiles,
                                                       BigCol *__restrict__ big_list,
                                                       uint32_t *__restrict__ bigk,
                                                       unsigned long long *scan_state,
                                                       ErrState *err) {
-    __shared__ uint32_t s_v[SCAN_TILE];
     __shared__ unsigned long long s_warp[SCAN_NT / 32];
     __shared__ long long s_b;
     __shared__ unsigned long long s_excl;
+    __shared__ long long s_tail;
+    __shared__ int s_tot;
     if (threadIdx.x == 0) s_b = atomicAdd(&err->scan_ticket, 1u);
     __syncthreads();
     const long long b = s_b;
-    const int64_t c_base = b * SCAN_TILE;
-    for (int k = threadIdx.x; k < SCAN_TILE; k += SCAN_NT) {
-        const int64_t c = c_base + k;
-        s_v[k] = (c < N) ? cnt[c] : 0u;
-    }
-    __syncthreads();
+    TRACE(b, 0);
+    const int64_t c0 = b * SCAN_TILE + (int64_t)threadIdx.x * SCAN_IPT;
     uint32_t loc[SCAN_IPT];
+    if (c0 + SCAN_IPT <= N) {
+#pragma unroll
+        for (int v = 0; v < SCAN_IPT / 4; ++v) {
+            const uint4 q = *reinterpret_cast<const uint4 *>(cnt + c0 + 4 * v);
+            loc[4 * v] = q.x; loc[4 * v + 1] = q.y; loc[4 * v + 2] = q.z; loc[4 * v + 3] = q.w;
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < SCAN_IPT; ++k) loc[k] = (c0 + k < N) ? cnt[c0 + k] : 0u;
+    }
     unsigned long long sum = 0;
 #pragma unroll
-    for (int k = 0; k < SCAN_IPT; ++k) {
-        loc[k] = s_v[threadIdx.x * SCAN_IPT + k];
-        // a big column adds its triplets to the big space and one placeholder
-        // slot to the small space (so every column has a distinct fold position)
-        sum += (loc[k] > (uint32_t)BIGCOL) ? (((unsigned long long)loc[k] << 31) | 1ull) : loc[k];
-    }
+    for (int k = 0; k < SCAN_IPT; ++k) sum += scan_word(loc[k]);
     unsigned long long total;
-    unsigned long long pre = block_excl_sum<SCAN_NT, unsigned long long>(sum, s_warp, total);
+    const unsigned long long pre = block_excl_sum<SCAN_NT, unsigned long long>(sum, s_warp, total);
+    TRACE(b, 1);
     if (threadIdx.x < 32) {
         const unsigned long long e = lookback_warp(scan_state, b, total);
         if (threadIdx.x == 0) s_excl = e;
     }
     __syncthreads();
+    TRACE(b, 2);
     const unsigned long long run0 = s_excl + pre;
     uint64_t small = run0 & SMALL_MASK;
     uint64_t bigp = run0 >> 31;
+    uint32_t o_s[SCAN_IPT], o_c[SCAN_IPT];
 #pragma unroll
     for (int k = 0; k < SCAN_IPT; ++k) {
-        const int64_t c = c_base + threadIdx.x * SCAN_IPT + k;
+        const int64_t c = c0 + k;
         const uint32_t n = loc[k];
         const bool big = n > (uint32_t)BIGCOL;
+        o_s[k] = (uint32_t)small | (big ? BIGFLAG : 0u);
+        o_c[k] = big ? ((uint32_t)bigp | BIGFLAG) : (uint32_t)small;
         if (c < N) {
-            sstart[c] = (uint32_t)small | (big ? BIGFLAG : 0u);
             if (big) {
-                cur[c] = (uint32_t)bigp | BIGFLAG;
                 const unsigned slot = atomicAdd(&err->nbig, 1u);
                 big_list[slot] = BigCol{(uint32_t)c, (uint32_t)bigp, n, 0u};
                 bigk[c] = slot;
                 int64_t tb = (int64_t)(small / TILE);
                 if (tb > ntiles - 1) tb = ntiles - 1;
                 tile_big[tb] = 1;
-            } else {
-                cur[c] = (uint32_t)small;
             }
-            // fold windows w with small < w*WIN <= small + extent start at column c+1
+            // fold tiles t with small < t*TILE <= small + extent start at column c+1
             const uint32_t ext = big ? 1u : n;
             if (ext) {
-                int64_t first = (int64_t)(small / WIN) + 1;
-                int64_t last = (int64_t)((small + ext) / WIN);
-                if (last > nwin - 1) last = nwin - 1;
-                for (int64_t w = first; w <= last; ++w) win_first[w] = (int32_t)(c + 1);
+                int64_t t = (int64_t)(small / TILE) + 1;
+                const int64_t last = min((int64_t)((small + ext) / TILE), ntiles - 1);
+                for (; t <= last; ++t) tile_info[t] = make_int2((int)(c + 1), (int)(small + ext));
             }
             if (c == N - 1) {
-                const uint64_t tot_small = small + (big ? 1 : n);
+                const uint64_t tot_small = small + ext;
                 err->lsmall = (unsigned)tot_small;
                 sstart[N] = (uint32_t)tot_small;
-                // windows past the small space (and past dropped invalid triplets) are empty
-                for (int64_t w = (int64_t)(tot_small / WIN) + 1; w <= nwin; ++w) win_first[w] = N;
+                s_tail = (long long)(tot_small / TILE) + 1;
+                s_tot = (int)tot_small;
             }
         }
         if (big) {
@@ -280,19 +304,40 @@ __global__ void __launch_bounds__(SCAN_NT) k_col_scan(const uint32_t *__restrict
             small += n;
         }
     }
-    if (b == 0 && threadIdx.x == 0) {
-        win_first[0] = 0;
-        win_first[nwin] = N;
+    if (c0 + SCAN_IPT <= N) {
+#pragma unroll
+        for (int v = 0; v < SCAN_IPT / 4; ++v) {
+            *reinterpret_cast<uint4 *>(sstart + c0 + 4 * v) =
+                make_uint4(o_s[4 * v], o_s[4 * v + 1], o_s[4 * v + 2], o_s[4 * v + 3]);
+            *reinterpret_cast<uint4 *>(cur + c0 + 4 * v) =
+                make_uint4(o_c[4 * v], o_c[4 * v + 1], o_c[4 * v + 2], o_c[4 * v + 3]);
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < SCAN_IPT; ++k)
+            if (c0 + k < N) {
+                sstart[c0 + k] = o_s[k];
+                cur[c0 + k] = o_c[k];
+            }
+    }
+    if (b == 0 && threadIdx.x == 0) tile_info[0] = make_int2(0, 0);
+    TRACE(b, 3);
+    // tiles past the small space (and past dropped invalid triplets) are
+    // empty; the CTA holding column N-1 fills them together
+    if (b == (long long)(N - 1) / SCAN_TILE) {
+        __syncthreads();
+        for (int64_t t = s_tail + threadIdx.x; t <= ntiles; t += SCAN_NT)
+            tile_info[t] = make_int2(N, s_tot);
     }
 }
 
 cudaError_t launch_col_scan(Launch &lc, const uint32_t *cnt, uint32_t *sstart, uint32_t *cur,
-                            int32_t N, int64_t nwin, int32_t *win_first, uint8_t *tile_big,
+                            int32_t N, int2 *tile_info, uint8_t *tile_big,
                             int64_t ntiles, BigCol *big_list, uint32_t *bigk,
                             unsigned long long *scan_state, ErrState *err) {
     if (N <= 0) return cudaSuccess;
     int grid = (int)((N + SCAN_TILE - 1) / SCAN_TILE);
-    k_col_scan<<<grid, SCAN_NT, 0, lc.stream>>>(cnt, sstart, cur, N, nwin, win_first, tile_big,
+    k_col_scan<<<grid, SCAN_NT, 0, lc.stream>>>(cnt, sstart, cur, N, tile_info, tile_big,
                                                ntiles, big_list, bigk, scan_state, err);
     lc.launches++;
     return cudaGetLastError();
@@ -696,3 +741,9 @@ cudaError_t launch_bigcol(Launch &lc, BigCol *big_list, const ErrState *err, int
 }
 
 }  // namespace sa
+
+#ifdef SA_TRACE
+extern "C" int sa_debug_trace(void *host, int n) {
+    return (int)cudaMemcpyFromSymbol(host, sa::g_trace, (size_t)n * 32);
+}
+#endif

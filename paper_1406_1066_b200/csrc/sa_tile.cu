@@ -3,8 +3,9 @@
 // Input: 16-byte records {row, input position, value} grouped by column
 // (k_scatter) in the small record space; sstart[c] = small-space start of
 // column c (| BIGFLAG for a big column, which occupies one placeholder
-// slot); win_first[w] = first column starting in thread window w
-// (WIN = 16 record positions).  Output: jc, ir, pr.
+// slot); tile_info[t] = {first column of tile t, its start}.  Thread tid
+// owns the columns starting in its window of WIN = 16 record positions.
+// Output: jc, ir, pr.
 //
 // One CTA per tile (TILE = 2048 record positions, ticket order for
 // forward progress); the tile's records arrive by one TMA bulk copy
@@ -36,6 +37,7 @@ constexpr int SHORT_COL = 24;
 
 constexpr int NWARP = NT / 32;
 constexpr int LCAP = TILE / (SHORT_COL + 1) + 2;  // long columns per tile
+constexpr int SCAP = 256;                         // staged column starts per tile
 constexpr int MAXU = 96;                          // distinct rows of a long column (warp table)
 
 struct WarpScratch {
@@ -51,6 +53,8 @@ struct TileSmem {
     uint8_t perm[TCAP];                // per column: sorted order, then output slots
     WarpScratch ws[NWARP];
     int lcol[LCAP];                    // long columns: record offset | (count << 16)
+    uint32_t scol[SCAP];               // sstart of the tile's columns (when they fit)
+    int wl[NT + 1];                    // first column of each thread window (tile-relative)
     unsigned long long mbar;
     int nlong;
     int warp_u[NWARP];
@@ -471,8 +475,7 @@ __device__ int fold_column_warp(int4 *R, int c, WarpScratch &W) {
 __device__ __forceinline__ void lookback_publish(unsigned long long *st, long long b,
                                                  unsigned long long agg) {
     volatile unsigned long long *vst = st;
-    __threadfence();
-    vst[b] = lb_pack(b == 0 ? 2 : 1, agg);
+    vst[(b) * LB_STRIDE] = lb_pack(b == 0 ? 2 : 1, agg);
 }
 
 // Warp-level decoupled look-back (32 predecessors per L2 round trip, with
@@ -486,7 +489,7 @@ __device__ long long lookback_warp32(unsigned long long *st, long long b, unsign
     long long base = b - 1;
     while (base >= 0) {
         const long long idx = base - lane;
-        const unsigned long long w = (idx >= 0) ? vst[idx] : lb_pack(2, 0);
+        const unsigned long long w = (idx >= 0) ? vst[(idx) * LB_STRIDE] : lb_pack(2, 0);
         const unsigned flag = (unsigned)(w >> 62);
         if (__any_sync(FULL, flag == 0)) {
             __nanosleep(64);
@@ -502,8 +505,7 @@ __device__ long long lookback_warp32(unsigned long long *st, long long b, unsign
         base -= 32;
     }
     if (lane == 0) {
-        __threadfence();
-        vst[b] = lb_pack(2, excl + agg);
+        vst[(b) * LB_STRIDE] = lb_pack(2, excl + agg);
     }
     return (long long)excl;
 }
@@ -511,7 +513,7 @@ __device__ long long lookback_warp32(unsigned long long *st, long long b, unsign
 }  // namespace
 
 __global__ void __launch_bounds__(NT) k_tile_fold(const uint32_t *__restrict__ sstart,
-                                                  const int32_t *__restrict__ win_first,
+                                                  const int2 *__restrict__ tile_info,
                                                   const uint8_t *__restrict__ tile_big,
                                                   int64_t ntiles, const int4 *__restrict__ rec,
                                                   const BigCol *__restrict__ big_list,
@@ -533,29 +535,49 @@ __global__ void __launch_bounds__(NT) k_tile_fold(const uint32_t *__restrict__ s
     }
     __syncthreads();
     const long long b = S.tile;
-    const int r0 = (int)(sstart[win_first[b * NT]] & POSMASK);
-    const int r1 = (int)(sstart[win_first[(b + 1) * NT]] & POSMASK);
+    const int2 ti0 = tile_info[b], ti1 = tile_info[b + 1];
+    const int c_a = ti0.x, r0 = ti0.y, r1 = ti1.y;
     const int n = r1 - r0;
     if (tid == 0) {
         if (n > 0 && n <= TCAP) tma_load(S.rec, rec + r0, (unsigned)n * 16u, &S.mbar);
         else if (n > TCAP) atomicExch(&err->internal, 1u);
     }
-    const int c_lo = win_first[b * NT + tid], c_hi = win_first[b * NT + tid + 1];
+    // the tile's column starts: staged in shared memory unless the tile holds
+    // very many (empty) columns; cs[k] = sstart[c_a + k], 0 <= k <= ncols
+    const int ncols = ti1.x - c_a;
+    const bool cs_staged = ncols < SCAP;
+    if (cs_staged)
+        for (int k = tid; k <= ncols; k += NT) S.scol[k] = sstart[c_a + k];
+    __syncthreads();
+    const uint32_t *cs = cs_staged ? S.scol : sstart + c_a;
+    {  // thread window tid = record positions [b*TILE + tid*WIN, +WIN): its first column
+        const uint32_t key = (uint32_t)(b * TILE + tid * WIN);
+        int lo = 0, hi = ncols;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if ((cs[mid] & POSMASK) < key) lo = mid + 1;
+            else hi = mid;
+        }
+        S.wl[tid] = lo;
+        if (tid == 0) S.wl[NT] = ncols;
+    }
+    __syncthreads();
+    const int k_lo = S.wl[tid], k_hi = S.wl[tid + 1];  // tile-relative columns
     if (n > 0 && n <= TCAP) mbar_wait(&S.mbar, 0u);
     const bool staged = n <= TCAP;
 
     // ---- pass 1: each thread folds its short columns; long ones are listed -------
     if (staged) {
-        const int ncols = c_hi - c_lo;
-        int maxcols = ncols;
+        const int nmine = k_hi - k_lo;
+        int maxcols = nmine;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) maxcols = max(maxcols, __shfl_xor_sync(FULL, maxcols, o));
         for (int k = 0; k < maxcols; ++k) {
-            const int c = c_lo + k;
+            const int c = k_lo + k;
             int cnt = 0, off = 0;
-            if (k < ncols) {
-                const uint32_t w0 = sstart[c];
-                const int s0 = (int)(w0 & POSMASK), s1 = (int)(sstart[c + 1] & POSMASK);
+            if (k < nmine) {
+                const uint32_t w0 = cs[c];
+                const int s0 = (int)(w0 & POSMASK), s1 = (int)(cs[c + 1] & POSMASK);
                 if (!(w0 & BIGFLAG) && s1 > s0) {
                     cnt = s1 - s0;
                     off = s0 - r0;
@@ -600,10 +622,10 @@ __global__ void __launch_bounds__(NT) k_tile_fold(const uint32_t *__restrict__ s
 
     // ---- tile count and thread output bases; publish the aggregate early -------
     int ut = 0;
-    for (int c = c_lo; c < c_hi; ++c) {
-        const uint32_t w0 = sstart[c];
-        const int s0 = (int)(w0 & POSMASK), s1 = (int)(sstart[c + 1] & POSMASK);
-        if (w0 & BIGFLAG) ut += (int)(big_list[bigk[c]].u & POSMASK);
+    for (int c = k_lo; c < k_hi; ++c) {
+        const uint32_t w0 = cs[c];
+        const int s0 = (int)(w0 & POSMASK), s1 = (int)(cs[c + 1] & POSMASK);
+        if (w0 & BIGFLAG) ut += (int)(big_list[bigk[c_a + c]].u & POSMASK);
         else if (s1 > s0 && staged) ut += S.rec[s0 - r0].y;
     }
     const int inc = warp_incl_sum(ut);
@@ -621,10 +643,10 @@ __global__ void __launch_bounds__(NT) k_tile_fold(const uint32_t *__restrict__ s
 
     // ---- pass 3: fold the short columns' values (predecessors publish meanwhile)
     if (staged) {
-        for (int c = c_lo; c < c_hi; ++c) {
-            const uint32_t w0 = sstart[c];
+        for (int c = k_lo; c < k_hi; ++c) {
+            const uint32_t w0 = cs[c];
             if (w0 & BIGFLAG) continue;
-            const int s0 = (int)(w0 & POSMASK), s1 = (int)(sstart[c + 1] & POSMASK);
+            const int s0 = (int)(w0 & POSMASK), s1 = (int)(cs[c + 1] & POSMASK);
             const int cnt = s1 - s0;
             if (cnt > 0 && cnt <= SHORT_COL)
                 fold_from_perm(&S.rec[s0 - r0], &S.perm[s0 - r0], cnt, S.rec[s0 - r0].y);
@@ -640,12 +662,12 @@ __global__ void __launch_bounds__(NT) k_tile_fold(const uint32_t *__restrict__ s
     // ---- outputs (each thread: its columns, contiguous) and column pointers --------
     bool over = false;
     long long o = P + tbase;
-    for (int c = c_lo; c < c_hi; ++c) {
-        jc[c] = (int32_t)o;
-        const uint32_t w0 = sstart[c];
-        const int s0 = (int)(w0 & POSMASK), s1 = (int)(sstart[c + 1] & POSMASK);
+    for (int c = k_lo; c < k_hi; ++c) {
+        jc[c_a + c] = (int32_t)o;
+        const uint32_t w0 = cs[c];
+        const int s0 = (int)(w0 & POSMASK), s1 = (int)(cs[c + 1] & POSMASK);
         if (w0 & BIGFLAG) {
-            const BigCol bc = big_list[bigk[c]];
+            const BigCol bc = big_list[bigk[c_a + c]];
             const int ub = (int)(bc.u & POSMASK);
             const unsigned long long *RR = reinterpret_cast<const unsigned long long *>(rec + bc.start);
             const unsigned long long *K = (bc.u & BIGFLAG) ? RR + bc.n : RR;
@@ -684,7 +706,7 @@ __global__ void __launch_bounds__(NT) k_tile_fold(const uint32_t *__restrict__ s
     }
 }
 
-cudaError_t launch_tile_fold(Launch &lc, const uint32_t *sstart, const int32_t *win_first,
+cudaError_t launch_tile_fold(Launch &lc, const uint32_t *sstart, const int2 *tile_info,
                              const uint8_t *tile_big, int64_t ntiles, const int4 *rec,
                              const BigCol *big_list, const uint32_t *bigk,
                              unsigned long long *tile_state, int32_t N, int32_t *jc, int32_t *ir,
@@ -694,7 +716,7 @@ cudaError_t launch_tile_fold(Launch &lc, const uint32_t *sstart, const int32_t *
     cudaError_t e = cudaFuncSetAttribute(k_tile_fold, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return e;
-    k_tile_fold<<<(unsigned)ntiles, NT, smem, lc.stream>>>(sstart, win_first, tile_big, ntiles, rec,
+    k_tile_fold<<<(unsigned)ntiles, NT, smem, lc.stream>>>(sstart, tile_info, tile_big, ntiles, rec,
                                                           big_list, bigk, tile_state, N, jc, ir, pr,
                                                           cap, err);
     lc.launches++;
