@@ -228,6 +228,7 @@ __global__ void __launch_bounds__(SCAN_NT) k_col_scan(const uint32_t *cnt,
                                                       BigCol *__restrict__ big_list,
                                                       uint32_t *__restrict__ bigk,
                                                       unsigned long long *scan_state,
+                                                      uint32_t *__restrict__ perm,
                                                       ErrState *err) {
     __shared__ unsigned long long s_warp[SCAN_NT / 32];
     __shared__ long long s_b;
@@ -278,6 +279,7 @@ __global__ void __launch_bounds__(SCAN_NT) k_col_scan(const uint32_t *cnt,
                 const unsigned slot = atomicAdd(&err->nbig, 1u);
                 big_list[slot] = BigCol{(uint32_t)c, (uint32_t)bigp, n, 0u};
                 bigk[c] = slot;
+                perm[small] = 0xffffffffu;  // placeholder slot: nothing to gather
                 int64_t tb = (int64_t)(small / TILE);
                 if (tb > ntiles - 1) tb = ntiles - 1;
                 tile_big[tb] = 1;
@@ -334,11 +336,11 @@ __global__ void __launch_bounds__(SCAN_NT) k_col_scan(const uint32_t *cnt,
 cudaError_t launch_col_scan(Launch &lc, const uint32_t *cnt, uint32_t *sstart, uint32_t *cur,
                             int32_t N, int2 *tile_info, uint8_t *tile_big,
                             int64_t ntiles, BigCol *big_list, uint32_t *bigk,
-                            unsigned long long *scan_state, ErrState *err) {
+                            unsigned long long *scan_state, uint32_t *perm, ErrState *err) {
     if (N <= 0) return cudaSuccess;
     int grid = (int)((N + SCAN_TILE - 1) / SCAN_TILE);
     k_col_scan<<<grid, SCAN_NT, 0, lc.stream>>>(cnt, sstart, cur, N, tile_info, tile_big,
-                                               ntiles, big_list, bigk, scan_state, err);
+                                               ntiles, big_list, bigk, scan_state, perm, err);
     lc.launches++;
     return cudaGetLastError();
 }
@@ -396,6 +398,26 @@ __device__ __forceinline__ void load_run(const int32_t *__restrict__ p, int64_t 
     }
 }
 
+// Runs of equal columns inside a thread's CPT consecutive triplets (FEM
+// element order emits each column 3-4 times in a row): only a run's head
+// touches the shared-memory hash, with the run length.  len[k] = triplets
+// from k to the end of its run.
+__device__ __forceinline__ void run_lengths(const int (&j)[CPT], const bool (&v)[CPT],
+                                            int (&len)[CPT]) {
+    int run = 0;
+#pragma unroll
+    for (int k = CPT - 1; k >= 0; --k) {
+        const bool cont = (k + 1 < CPT) && v[k] && v[k < CPT - 1 ? k + 1 : k] &&
+                          j[k < CPT - 1 ? k + 1 : k] == j[k];
+        run = v[k] ? (cont ? run + 1 : 1) : 0;
+        len[k] = run;
+    }
+}
+
+__device__ __forceinline__ bool run_head(const int (&j)[CPT], const bool (&v)[CPT], int k) {
+    return !(k > 0 && v[k > 0 ? k - 1 : 0] && j[k > 0 ? k - 1 : 0] == j[k]);
+}
+
 // ---------------------------------------------------------------------------
 // k_colcount: column histogram of the assembly path (reads jj only; rows
 // are validated by k_scatter, which reads them anyway).
@@ -424,14 +446,21 @@ __global__ void __launch_bounds__(AGG_NT) k_colcount(const int32_t *__restrict__
         for (int k = 0; k < CPT; ++k) j[k] = jn[k];
         if (ch + gridDim.x < nchunk)  // prefetch the next chunk while this one is counted
             load_run(jj, (ch + gridDim.x) * CHUNK + (int64_t)tid * CPT, L, vec, jn, 0x7fffffff);
+        bool vk[CPT];
+        int len[CPT];
 #pragma unroll
         for (int k = 0; k < CPT; ++k) {
             const bool live = t0 + k < L;
             if (live && j[k] < 1) bad = min(bad, (unsigned long long)(t0 + k));
             if (live && j[k] > N) over = 1;
-            if (live && j[k] >= 1 && j[k] <= N) {
+            vk[k] = live && j[k] >= 1 && j[k] <= N;
+        }
+        run_lengths(j, vk, len);
+#pragma unroll
+        for (int k = 0; k < CPT; ++k) {
+            if (vk[k] && run_head(j, vk, k)) {
                 const int h = agg_insert(A, j[k] - 1);
-                atomicAdd(&A.ctr[h], 1);
+                atomicAdd(&A.ctr[h], len[k]);
             }
         }
         __syncthreads();
@@ -469,20 +498,17 @@ cudaError_t launch_colcount(Launch &lc, const int32_t *jj, int64_t L, int32_t N,
 }
 
 // ---------------------------------------------------------------------------
-// k_scatter: counting-sort scatter by column.  Record = {row, input position,
-// value lo, value hi}.  Per chunk: (1) each column's triplets get chunk-local
-// slots from a shared-memory counter, (2) one global atomicAdd per distinct
-// column reserves the chunk's slots on the column cursor, (3) records are
-// written.  Row indices are validated here (first bad position, rows above
-// M).  The slot order inside a column is arbitrary; the fold restores input
-// order from the stored position.
+// k_scatter: counting-sort scatter by column of the input POSITIONS only
+// (4 bytes per triplet; the fold gathers rows and values by position, so
+// the triplets' 12 payload bytes are read once, by the fold).  Per chunk:
+// (1) each column run gets chunk-local slots from a shared-memory counter,
+// (2) one global atomicAdd per distinct column reserves the chunk's slots on
+// the column cursor, (3) positions are written.  The slot order inside a
+// column is arbitrary; the fold restores input order from the position.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(AGG_NT) k_scatter(const int32_t *__restrict__ ii,
-                                                    const int32_t *__restrict__ jj,
-                                                    const double *__restrict__ s, int64_t s_stride,
-                                                    int64_t L, int32_t M, int32_t N,
-                                                    uint32_t *__restrict__ cur,
-                                                    int4 *__restrict__ rec, int vec,
+__global__ void __launch_bounds__(AGG_NT) k_scatter(const int32_t *__restrict__ jj, int64_t L,
+                                                    int32_t N, uint32_t *__restrict__ cur,
+                                                    uint32_t *__restrict__ perm, int vec,
                                                     ErrState *err) {
     __shared__ AggSmem A;
     const int tid = threadIdx.x;
@@ -493,57 +519,34 @@ __global__ void __launch_bounds__(AGG_NT) k_scatter(const int32_t *__restrict__ 
     if (tid == 0) A.nused = 0;
     __syncthreads();
     const uint32_t lsmall = err->lsmall;
-    const double s0v = s_stride ? 0.0 : __ldg(s);
-    unsigned long long bad = ~0ull;
-    unsigned over = 0;
     const int64_t nchunk = (L + CHUNK - 1) / CHUNK;
-    int ivn[CPT], jvn[CPT];
-    double vvn[CPT];
-    auto load_all = [&](int64_t c0) {
-        const int64_t t0 = c0 * CHUNK + (int64_t)tid * CPT;
-        load_run(ii, t0, L, vec, ivn, 1);
-        load_run(jj, t0, L, vec, jvn, 0);
-        if (s_stride) {
-            if (vec && t0 + CPT <= L) {
-                const double2 *ps = reinterpret_cast<const double2 *>(s + t0);
-#pragma unroll
-                for (int q = 0; q < CPT / 2; ++q) {
-                    const double2 d = __ldg(ps + q);
-                    vvn[2 * q] = d.x;
-                    vvn[2 * q + 1] = d.y;
-                }
-            } else {
-#pragma unroll
-                for (int k = 0; k < CPT; ++k) vvn[k] = (t0 + k < L) ? s[t0 + k] : 0.0;
-            }
-        } else {
-#pragma unroll
-            for (int k = 0; k < CPT; ++k) vvn[k] = s0v;
-        }
-    };
-    if ((int64_t)blockIdx.x < nchunk) load_all(blockIdx.x);
+    int jn[CPT];
+    if ((int64_t)blockIdx.x < nchunk)
+        load_run(jj, (int64_t)blockIdx.x * CHUNK + (int64_t)tid * CPT, L, vec, jn, 0);
     for (int64_t ch = blockIdx.x; ch < nchunk; ch += gridDim.x) {
         const int64_t t0 = ch * CHUNK + (int64_t)tid * CPT;
-        int iv[CPT], jv[CPT];
-        double vv[CPT];
+        int j[CPT];
+#pragma unroll
+        for (int k = 0; k < CPT; ++k) j[k] = jn[k];
+        if (ch + gridDim.x < nchunk)  // next chunk in flight
+            load_run(jj, (ch + gridDim.x) * CHUNK + (int64_t)tid * CPT, L, vec, jn, 0);
+        bool vk[CPT];
+        int len[CPT], hk[CPT], rk[CPT];
+#pragma unroll
+        for (int k = 0; k < CPT; ++k) vk[k] = (t0 + k < L) && j[k] >= 1 && j[k] <= N;
+        run_lengths(j, vk, len);
 #pragma unroll
         for (int k = 0; k < CPT; ++k) {
-            iv[k] = ivn[k];
-            jv[k] = jvn[k];
-            vv[k] = vvn[k];
-        }
-        if (ch + gridDim.x < nchunk) load_all(ch + gridDim.x);  // next chunk in flight
-        int hk[CPT], rk[CPT];
-#pragma unroll
-        for (int k = 0; k < CPT; ++k) {
-            const bool live = t0 + k < L;
-            if (live && iv[k] < 1) bad = min(bad, (unsigned long long)(t0 + k));
-            if (live && iv[k] > M) over = 1;
             hk[k] = -1;
             rk[k] = 0;
-            if (live && jv[k] >= 1 && jv[k] <= N) {
-                hk[k] = agg_insert(A, jv[k] - 1);
-                rk[k] = atomicAdd(&A.ctr[hk[k]], 1);
+            if (vk[k]) {
+                if (run_head(j, vk, k)) {
+                    hk[k] = agg_insert(A, j[k] - 1);
+                    rk[k] = atomicAdd(&A.ctr[hk[k]], len[k]);
+                } else {
+                    hk[k] = hk[k > 0 ? k - 1 : 0];
+                    rk[k] = rk[k > 0 ? k - 1 : 0] + 1;
+                }
             }
         }
         __syncthreads();
@@ -558,7 +561,7 @@ __global__ void __launch_bounds__(AGG_NT) k_scatter(const int32_t *__restrict__ 
             if (hk[k] < 0) continue;
             const uint32_t bw = (uint32_t)A.ctr[hk[k]];
             const uint32_t pos = (bw & POSMASK) + ((bw & BIGFLAG) ? lsmall : 0u) + (uint32_t)rk[k];
-            rec[pos] = make_int4(iv[k], (int)(t0 + k), __double2loint(vv[k]), __double2hiint(vv[k]));
+            perm[pos] = (uint32_t)(t0 + k);
         }
         __syncthreads();
         for (int e = tid; e < nu; e += AGG_NT) {
@@ -569,43 +572,37 @@ __global__ void __launch_bounds__(AGG_NT) k_scatter(const int32_t *__restrict__ 
         if (tid == 0) A.nused = 0;
         __syncthreads();
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        bad = min(bad, __shfl_xor_sync(FULL, bad, o));
-        over |= __shfl_xor_sync(FULL, over, o);
-    }
-    if ((tid & 31) == 0) {
-        if (bad != ~0ull) atomicMin(&err->bad_i, bad);
-        if (over) err->over_m = 1;
-    }
 }
 
-cudaError_t launch_scatter(Launch &lc, const int32_t *ii, const int32_t *jj, const double *s,
-                           int64_t s_stride, int64_t L, int32_t M, int32_t N, uint32_t *cur,
-                           int4 *rec, ErrState *err) {
+cudaError_t launch_scatter(Launch &lc, const int32_t *jj, int64_t L, int32_t N, uint32_t *cur,
+                           uint32_t *perm, ErrState *err) {
     if (L <= 0) return cudaSuccess;
-    const int vec = aligned16(ii) && aligned16(jj) && (s_stride == 0 || aligned16(s));
+    const int vec = aligned16(jj);
     const int64_t nchunk = (L + CHUNK - 1) / CHUNK;
     int grid = (int)std::min<int64_t>(nchunk, (int64_t)lc.num_sms * 4);
-    k_scatter<<<grid, AGG_NT, 0, lc.stream>>>(ii, jj, s, s_stride, L, M, N, cur, rec, vec, err);
+    k_scatter<<<grid, AGG_NT, 0, lc.stream>>>(jj, L, N, cur, perm, vec, err);
     lc.launches++;
     return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------------------
 // k_bigcol: one CTA per big column (grid-stride over the device-side list).
-// The column's 16-byte records are reused in place as two 8-byte key
-// buffers A|B: key = (row-1) << idx_bits | input position.  Stable LSD radix
+// The column's positions (perm, big space) are gathered into keys
+// key = (row-1) << idx_bits | input position in two 8-byte buffers A|B
+// (the column's 16-byte slots of the big scratch).  Stable LSD radix
 // passes (8-bit digits, warp match + per-warp digit counts) sort by (row,
 // position); values are gathered from the input by position; each run of
 // equal rows is folded from +0.0 in position order.  Results: row-1 in the
 // key buffer, value bits in the other buffer, at index = run number;
-// bigu[c] = runs | (BIGFLAG if keys ended in buffer B).
+// bigu[c] = runs | (BIGFLAG if keys ended in buffer B).  Rows are validated
+// here (the fold validates the short columns' rows).
 // ---------------------------------------------------------------------------
 constexpr int BIG_NT = 256;
 
 __global__ void __launch_bounds__(BIG_NT) k_bigcol(BigCol *__restrict__ big_list,
-                                                   const ErrState *err, int4 *rec,
+                                                   ErrState *err, int4 *rec,
+                                                   const uint32_t *__restrict__ perm,
+                                                   const int32_t *__restrict__ ii, int32_t M,
                                                    const double *__restrict__ s, int64_t s_stride,
                                                    int idx_bits, int passes) {
     __shared__ uint32_t s_hist[256];
@@ -619,21 +616,22 @@ __global__ void __launch_bounds__(BIG_NT) k_bigcol(BigCol *__restrict__ big_list
     for (int k = tid; k < (BIG_NT / 32) * 257; k += BIG_NT) (&s_wcnt[0][0])[k] = 0;
     __syncthreads();
     const unsigned long long idx_mask = (1ull << idx_bits) - 1;
+    unsigned long long bad = ~0ull;
+    unsigned over = 0;
     for (unsigned kb = blockIdx.x; kb < nbig; kb += gridDim.x) {
         const uint32_t st = big_list[kb].start + lsmall;
         const int64_t n = big_list[kb].n;
         unsigned long long *A = reinterpret_cast<unsigned long long *>(rec + st);
         unsigned long long *B = A + n;
-        // pack records -> keys in A (ascending chunks; reads stay ahead of writes)
-        for (int64_t base = 0; base < n; base += BIG_NT) {
-            const int64_t p = base + tid;
-            int4 r = make_int4(0, 0, 0, 0);
-            if (p < n) r = rec[st + p];
-            __syncthreads();
-            if (p < n)
-                A[p] = ((unsigned long long)(uint32_t)(r.x - 1) << idx_bits) | (uint32_t)r.y;
-            __syncthreads();
+        // gather rows by position -> keys in A
+        for (int64_t p = tid; p < n; p += BIG_NT) {
+            const uint32_t pos = perm[st + p];
+            const int32_t row = ii[pos];
+            if (row < 1) bad = min(bad, (unsigned long long)pos);
+            if (row > M) over = 1;
+            A[p] = ((unsigned long long)(uint32_t)(row - 1) << idx_bits) | pos;
         }
+        __syncthreads();
         unsigned long long *src = A, *dst = B;
         for (int ps = 0; ps < passes; ++ps) {
             const int shift = 8 * ps;
@@ -730,12 +728,23 @@ __global__ void __launch_bounds__(BIG_NT) k_bigcol(BigCol *__restrict__ big_list
         }
         __syncthreads();
     }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        bad = min(bad, __shfl_xor_sync(FULL, bad, o));
+        over |= __shfl_xor_sync(FULL, over, o);
+    }
+    if (lane == 0) {
+        if (bad != ~0ull) atomicMin(&err->bad_i, bad);
+        if (over) err->over_m = 1;
+    }
 }
 
-cudaError_t launch_bigcol(Launch &lc, BigCol *big_list, const ErrState *err, int4 *rec,
-                          const double *s, int64_t s_stride, int idx_bits, int passes) {
+cudaError_t launch_bigcol(Launch &lc, BigCol *big_list, ErrState *err, int4 *rec,
+                          const uint32_t *perm, const int32_t *ii, int32_t M, const double *s,
+                          int64_t s_stride, int idx_bits, int passes) {
     int grid = lc.num_sms;
-    k_bigcol<<<grid, BIG_NT, 0, lc.stream>>>(big_list, err, rec, s, s_stride, idx_bits, passes);
+    k_bigcol<<<grid, BIG_NT, 0, lc.stream>>>(big_list, err, rec, perm, ii, M, s, s_stride, idx_bits,
+                                             passes);
     lc.launches++;
     return cudaGetLastError();
 }

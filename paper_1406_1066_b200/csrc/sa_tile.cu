@@ -25,6 +25,8 @@
 // outputs are staged in CSC order and written coalesced.  Tiles holding a
 // big column (folded by k_bigcol) copy its results from the big space.
 
+#include <cstdlib>
+
 #include "sa_internal.cuh"
 #include "sa_network.cuh"
 
@@ -48,17 +50,16 @@ struct WarpScratch {
     int gbase[MAXU];
 };
 
+template <int NBUF>
 struct TileSmem {
-    int4 rec[TCAP];                    // the tile's records (TMA destination)
+    int4 rec[NBUF][TCAP];              // tile records {row, position, value} (NBUF buffers)
     uint8_t perm[TCAP];                // per column: sorted order, then output slots
     WarpScratch ws[NWARP];
     int lcol[LCAP];                    // long columns: record offset | (count << 16)
-    uint32_t scol[SCAP];               // sstart of the tile's columns (when they fit)
+    uint32_t scol[NBUF][SCAP];         // sstart of the tile's columns (when they fit)
     int wl[NT + 1];                    // first column of each thread window (tile-relative)
-    unsigned long long mbar;
     int nlong;
     int warp_u[NWARP];
-    long long tile;
     long long P;
 };
 
@@ -66,30 +67,17 @@ __device__ __forceinline__ unsigned smem_u32(const void *p) {
     return static_cast<unsigned>(__cvta_generic_to_shared(p));
 }
 
-__device__ __forceinline__ void tma_load(void *dst, const void *src, unsigned bytes,
-                                         unsigned long long *bar) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-                 "r"(bytes)
-                 : "memory");
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
+// Ampere-style asynchronous copies (LDGSTS): the gathered row / value of a
+// record land in shared memory without passing through registers, so a
+// tile's gather is in flight while the previous tile is folded.
+__device__ __forceinline__ void cp_async4(void *dst, const void *src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
-
-__device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned parity) {
-    unsigned done = 0;
-    while (!done) {
-        asm volatile(
-            "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-            "selp.u32 %0, 1, 0, p;\n\t}"
-            : "=r"(done)
-            : "r"(smem_u32(bar)), "r"(parity)
-            : "memory");
-    }
+__device__ __forceinline__ void cp_async8(void *dst, const void *src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 // (row, position) order of two records (both non-negative int32)
 __device__ __forceinline__ unsigned long long rec_key(const int4 &a) {
@@ -510,217 +498,347 @@ __device__ long long lookback_warp32(unsigned long long *st, long long b, unsign
     return (long long)excl;
 }
 
+// Per-tile descriptor (loaded two tiles ahead).
+struct TileDesc {
+    int c_a, c_b;  // first column of the tile, first column of the next tile
+    int r0, n;     // small-space start, records
+};
+
+__device__ __forceinline__ TileDesc tile_desc(const int2 *__restrict__ tile_info, long long t,
+                                              int64_t ntiles) {
+    TileDesc d{0, 0, 0, 0};
+    if (t < ntiles) {
+        const int2 a = tile_info[t], b = tile_info[t + 1];
+        d.c_a = a.x;
+        d.c_b = b.x;
+        d.r0 = a.y;
+        d.n = b.y - a.y;
+    }
+    return d;
+}
+
+constexpr int GPT = (TCAP + NT - 1) / NT;  // record slots per thread
+constexpr uint32_t NOPOS = 0xffffffffu;    // placeholder slot of a big column
+
+// Positions of a tile's record slots (tid + q*NT) into registers.
+__device__ __forceinline__ void load_positions(const uint32_t *__restrict__ perm, const TileDesc &d,
+                                               uint32_t (&p)[GPT]) {
+    const int tid = threadIdx.x;
+#pragma unroll
+    for (int q = 0; q < GPT; ++q) {
+        const int k = tid + q * NT;
+        p[q] = (k < d.n && d.n <= TCAP) ? __ldg(perm + d.r0 + k) : NOPOS;
+    }
+}
+
+// Asynchronous gather of a tile: rows and values by position into R, the
+// position itself by a plain store; the column starts into cs.
+__device__ __forceinline__ void issue_gather(int4 *R, uint32_t *cs, const TileDesc &d,
+                                             const uint32_t (&p)[GPT],
+                                             const int32_t *__restrict__ ii,
+                                             const double *__restrict__ sv, int64_t s_stride,
+                                             const uint32_t *__restrict__ sstart) {
+    const int tid = threadIdx.x;
+#pragma unroll
+    for (int q = 0; q < GPT; ++q) {
+        const int k = tid + q * NT;
+        if (k < d.n) {
+            int *r = reinterpret_cast<int *>(&R[k]);
+            r[1] = (int)p[q];
+            if (p[q] != NOPOS) {
+                cp_async4(r, ii + p[q]);
+                cp_async8(r + 2, sv + (int64_t)p[q] * s_stride);
+            }
+        }
+    }
+    const int ncols = d.c_b - d.c_a;
+    if (ncols < SCAP)
+        for (int k = tid; k <= ncols; k += NT) cp_async4(cs + k, sstart + d.c_a + k);
+    cp_async_commit();
+}
+
 }  // namespace
 
+// Persistent, software-pipelined fold: CTA g folds tiles g, g+G, g+2G, ...
+// (cooperative launch, so every CTA is resident and the look-back always
+// progresses).  While tile t is folded from buffer t&1, the gather of tile
+// t+G is in flight into the other buffer and the positions of tile t+2G are
+// loading into registers.
+template <int NBUF>
 __global__ void __launch_bounds__(NT) k_tile_fold(const uint32_t *__restrict__ sstart,
-                                                  const int2 *__restrict__ tile_info,
-                                                  const uint8_t *__restrict__ tile_big,
-                                                  int64_t ntiles, const int4 *__restrict__ rec,
-                                                  const BigCol *__restrict__ big_list,
-                                                  const uint32_t *__restrict__ bigk,
-                                                  unsigned long long *tile_state, int32_t N,
-                                                  int32_t *__restrict__ jc,
-                                                  int32_t *__restrict__ ir,
-                                                  double *__restrict__ pr, int64_t cap,
-                                                  ErrState *err) {
+                                                     const int2 *__restrict__ tile_info,
+                                                     const uint8_t *__restrict__ tile_big,
+                                                     int64_t ntiles,
+                                                     const uint32_t *__restrict__ perm,
+                                                     const int32_t *__restrict__ ii,
+                                                     const double *__restrict__ sv,
+                                                     int64_t s_stride, int32_t M,
+                                                     const int4 *__restrict__ rec,
+                                                     const BigCol *__restrict__ big_list,
+                                                     const uint32_t *__restrict__ bigk,
+                                                     unsigned long long *tile_state, int32_t N,
+                                                     int32_t *__restrict__ jc,
+                                                     int32_t *__restrict__ ir,
+                                                     double *__restrict__ pr, int64_t cap,
+                                                     ErrState *err) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    TileSmem &S = *reinterpret_cast<TileSmem *>(smem_raw);
+    TileSmem<NBUF> &S = *reinterpret_cast<TileSmem<NBUF> *>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const long long G = gridDim.x;
+    long long b = blockIdx.x;
+    if (b >= ntiles) return;
 
-    if (tid == 0) {
-        S.tile = atomicAdd(&err->tile_ticket, 1u);
-        S.nlong = 0;
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&S.mbar)) : "memory");
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    const long long b = S.tile;
-    const int2 ti0 = tile_info[b], ti1 = tile_info[b + 1];
-    const int c_a = ti0.x, r0 = ti0.y, r1 = ti1.y;
-    const int n = r1 - r0;
-    if (tid == 0) {
-        if (n > 0 && n <= TCAP) tma_load(S.rec, rec + r0, (unsigned)n * 16u, &S.mbar);
-        else if (n > TCAP) atomicExch(&err->internal, 1u);
-    }
-    // the tile's column starts: staged in shared memory unless the tile holds
-    // very many (empty) columns; cs[k] = sstart[c_a + k], 0 <= k <= ncols
-    const int ncols = ti1.x - c_a;
-    const bool cs_staged = ncols < SCAP;
-    if (cs_staged)
-        for (int k = tid; k <= ncols; k += NT) S.scol[k] = sstart[c_a + k];
-    __syncthreads();
-    const uint32_t *cs = cs_staged ? S.scol : sstart + c_a;
-    {  // thread window tid = record positions [b*TILE + tid*WIN, +WIN): its first column
-        const uint32_t key = (uint32_t)(b * TILE + tid * WIN);
-        int lo = 0, hi = ncols;
-        while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            if ((cs[mid] & POSMASK) < key) lo = mid + 1;
-            else hi = mid;
-        }
-        S.wl[tid] = lo;
-        if (tid == 0) S.wl[NT] = ncols;
-    }
-    __syncthreads();
-    const int k_lo = S.wl[tid], k_hi = S.wl[tid + 1];  // tile-relative columns
-    if (n > 0 && n <= TCAP) mbar_wait(&S.mbar, 0u);
-    const bool staged = n <= TCAP;
+    // prologue: gather of the first tile, positions of the second
+    TileDesc d0 = tile_desc(tile_info, b, ntiles);
+    TileDesc d1 = tile_desc(tile_info, b + G, ntiles);
+    uint32_t pn[GPT];
+    load_positions(perm, d0, pn);
+    issue_gather(S.rec[0], S.scol[0], d0, pn, ii, sv, s_stride, sstart);
+    load_positions(perm, d1, pn);
+    unsigned long long badp = ~0ull;
+    bool over_m = false, over_cap = false;
 
-    // ---- pass 1: each thread folds its short columns; long ones are listed -------
-    if (staged) {
-        const int nmine = k_hi - k_lo;
-        int maxcols = nmine;
+    for (int it = 0; b < ntiles; ++it, b += G) {
+        const int buf = (NBUF == 2) ? (it & 1) : 0;
+        cp_async_wait_all();
+        __syncthreads();  // tile b's records are in; every use of the other buffer is done
+        const TileDesc d2 = tile_desc(tile_info, b + 2 * G, ntiles);
+        if (NBUF == 2 && b + G < ntiles)
+            issue_gather(S.rec[buf ^ 1], S.scol[buf ^ 1], d1, pn, ii, sv, s_stride, sstart);
+        load_positions(perm, d2, pn);
+
+        int4 *R = S.rec[buf];
+        const int c_a = d0.c_a, r0 = d0.r0, n = d0.n;
+        const int ncols = d0.c_b - c_a;
+        if (n > TCAP && tid == 0) atomicExch(&err->internal, 1u);
+        const bool staged = n <= TCAP;
+        // row validation of the gathered records (placeholders skipped)
+        if (staged) {
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) maxcols = max(maxcols, __shfl_xor_sync(FULL, maxcols, o));
-        for (int k = 0; k < maxcols; ++k) {
-            const int c = k_lo + k;
-            int cnt = 0, off = 0;
-            if (k < nmine) {
-                const uint32_t w0 = cs[c];
-                const int s0 = (int)(w0 & POSMASK), s1 = (int)(cs[c + 1] & POSMASK);
-                if (!(w0 & BIGFLAG) && s1 > s0) {
-                    cnt = s1 - s0;
-                    off = s0 - r0;
+            for (int q = 0; q < GPT; ++q) {
+                const int k = tid + q * NT;
+                if (k < n) {
+                    const int2 rp = *reinterpret_cast<const int2 *>(&R[k]);
+                    if ((uint32_t)rp.y != NOPOS) {
+                        if (rp.x < 1) badp = min(badp, (unsigned long long)(uint32_t)rp.y);
+                        over_m |= rp.x > M;
+                    }
                 }
             }
-            if (cnt > SHORT_COL) {
-                const int e = atomicAdd(&S.nlong, 1);
-                if (e < LCAP) S.lcol[e] = off | (cnt << 16);
-                else atomicExch(&err->internal, 1u);
-                cnt = 0;
-            }
-            int wmax = cnt;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) wmax = max(wmax, __shfl_xor_sync(FULL, wmax, o));
-            if (wmax == 0) continue;
-            int u = 0;
-            if (wmax <= 8) {
-                if (cnt) u = fold_short_net<8>(&S.rec[off], cnt, &S.perm[off]);
-            } else if (wmax <= 12) {
-                if (cnt) u = fold_short_net<12>(&S.rec[off], cnt, &S.perm[off]);
-            } else if (wmax <= 16) {
-                if (cnt) u = fold_short_net<16>(&S.rec[off], cnt, &S.perm[off]);
-            } else if (wmax <= 18) {
-                if (cnt) u = fold_short_net<18>(&S.rec[off], cnt, &S.perm[off]);
-            } else {
-                if (cnt) u = fold_short_net<24>(&S.rec[off], cnt, &S.perm[off]);
-            }
-            if (cnt) S.rec[off].y = u;  // input positions are no longer needed
         }
-    }
-    __syncthreads();
-    // ---- pass 2: warps fold the long columns --------------------------------------
-    {
-        const int nl = min(S.nlong, LCAP);
-        for (int e = warp; e < nl; e += NWARP) {
-            const int v = S.lcol[e];
-            const int off = v & 0xffff;
-            fold_column_warp(&S.rec[off], v >> 16, S.ws[warp]);  // outputs at R[0..u)
+        const uint32_t *cs = (ncols < SCAP) ? S.scol[buf] : sstart + c_a;
+        {  // thread window tid = record positions [b*TILE + tid*WIN, +WIN): its first column
+            const uint32_t key = (uint32_t)(b * TILE + tid * WIN);
+            int lo = 0, hi = ncols;
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if ((cs[mid] & POSMASK) < key) lo = mid + 1;
+                else hi = mid;
+            }
+            S.wl[tid] = lo;
+            if (tid == 0) {
+                S.wl[NT] = ncols;
+                S.nlong = 0;
+            }
         }
-    }
-    __syncthreads();
+        __syncthreads();
+        const int k_lo = S.wl[tid], k_hi = S.wl[tid + 1];  // tile-relative columns
 
-    // ---- tile count and thread output bases; publish the aggregate early -------
-    int ut = 0;
-    for (int c = k_lo; c < k_hi; ++c) {
-        const uint32_t w0 = cs[c];
-        const int s0 = (int)(w0 & POSMASK), s1 = (int)(cs[c + 1] & POSMASK);
-        if (w0 & BIGFLAG) ut += (int)(big_list[bigk[c_a + c]].u & POSMASK);
-        else if (s1 > s0 && staged) ut += S.rec[s0 - r0].y;
-    }
-    const int inc = warp_incl_sum(ut);
-    if (lane == 31) S.warp_u[warp] = inc;
-    __syncthreads();
-    int wpre = 0, U = 0;
+        // ---- pass 1: each thread sorts its short columns; long ones are listed ----
+        if (staged) {
+            const int nmine = k_hi - k_lo;
+            int maxcols = nmine;
 #pragma unroll
-    for (int k = 0; k < NWARP; ++k) {
-        const int v = S.warp_u[k];
-        if (k < warp) wpre += v;
-        U += v;
-    }
-    const int tbase = wpre + inc - ut;  // this thread's first output, tile-local
-    if (tid == 0) lookback_publish(tile_state, b, (unsigned long long)U);
+            for (int o = 16; o > 0; o >>= 1) maxcols = max(maxcols, __shfl_xor_sync(FULL, maxcols, o));
+            for (int k = 0; k < maxcols; ++k) {
+                const int c = k_lo + k;
+                int cnt = 0, off = 0;
+                if (k < nmine) {
+                    const uint32_t w0 = cs[c];
+                    const int s0 = (int)(w0 & POSMASK), s1 = (int)(cs[c + 1] & POSMASK);
+                    if (!(w0 & BIGFLAG) && s1 > s0) {
+                        cnt = s1 - s0;
+                        off = s0 - r0;
+                    }
+                }
+                if (cnt > SHORT_COL) {
+                    const int e = atomicAdd(&S.nlong, 1);
+                    if (e < LCAP) S.lcol[e] = off | (cnt << 16);
+                    else atomicExch(&err->internal, 1u);
+                    cnt = 0;
+                }
+                int wmax = cnt;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) wmax = max(wmax, __shfl_xor_sync(FULL, wmax, o));
+                if (wmax == 0) continue;
+                int u = 0;
+                if (wmax <= 8) {
+                    if (cnt) u = fold_short_net<8>(&R[off], cnt, &S.perm[off]);
+                } else if (wmax <= 12) {
+                    if (cnt) u = fold_short_net<12>(&R[off], cnt, &S.perm[off]);
+                } else if (wmax <= 16) {
+                    if (cnt) u = fold_short_net<16>(&R[off], cnt, &S.perm[off]);
+                } else if (wmax <= 18) {
+                    if (cnt) u = fold_short_net<18>(&R[off], cnt, &S.perm[off]);
+                } else {
+                    if (cnt) u = fold_short_net<24>(&R[off], cnt, &S.perm[off]);
+                }
+                if (cnt) R[off].y = u;  // input positions are no longer needed
+            }
+        }
+        __syncthreads();
+        // ---- pass 2: warps fold the long columns ---------------------------------
+        {
+            const int nl = min(S.nlong, LCAP);
+            for (int e = warp; e < nl; e += NWARP) {
+                const int v = S.lcol[e];
+                const int off = v & 0xffff;
+                fold_column_warp(&R[off], v >> 16, S.ws[warp]);  // outputs at R[0..u)
+            }
+        }
+        __syncthreads();
 
-    // ---- pass 3: fold the short columns' values (predecessors publish meanwhile)
-    if (staged) {
+        // ---- tile count and thread output bases; publish the aggregate early ------
+        int ut = 0;
         for (int c = k_lo; c < k_hi; ++c) {
             const uint32_t w0 = cs[c];
-            if (w0 & BIGFLAG) continue;
             const int s0 = (int)(w0 & POSMASK), s1 = (int)(cs[c + 1] & POSMASK);
-            const int cnt = s1 - s0;
-            if (cnt > 0 && cnt <= SHORT_COL)
-                fold_from_perm(&S.rec[s0 - r0], &S.perm[s0 - r0], cnt, S.rec[s0 - r0].y);
+            if (w0 & BIGFLAG) ut += (int)(big_list[bigk[c_a + c]].u & POSMASK);
+            else if (s1 > s0 && staged) ut += R[s0 - r0].y;
         }
-    }
-    if (warp == 0) {
-        const long long P = lookback_warp32(tile_state, b, (unsigned long long)U);
-        if (lane == 0) S.P = P;
-    }
-    __syncthreads();
-    const long long P = S.P;
+        const int inc = warp_incl_sum(ut);
+        if (lane == 31) S.warp_u[warp] = inc;
+        __syncthreads();
+        int wpre = 0, U = 0;
+#pragma unroll
+        for (int k = 0; k < NWARP; ++k) {
+            const int v = S.warp_u[k];
+            if (k < warp) wpre += v;
+            U += v;
+        }
+        const int tbase = wpre + inc - ut;  // this thread's first output, tile-local
+        if (tid == 0) lookback_publish(tile_state, b, (unsigned long long)U);
 
-    // ---- outputs (each thread: its columns, contiguous) and column pointers --------
-    bool over = false;
-    long long o = P + tbase;
-    for (int c = k_lo; c < k_hi; ++c) {
-        jc[c_a + c] = (int32_t)o;
-        const uint32_t w0 = cs[c];
-        const int s0 = (int)(w0 & POSMASK), s1 = (int)(cs[c + 1] & POSMASK);
-        if (w0 & BIGFLAG) {
-            const BigCol bc = big_list[bigk[c_a + c]];
-            const int ub = (int)(bc.u & POSMASK);
-            const unsigned long long *RR = reinterpret_cast<const unsigned long long *>(rec + bc.start);
-            const unsigned long long *K = (bc.u & BIGFLAG) ? RR + bc.n : RR;
-            const unsigned long long *V = (bc.u & BIGFLAG) ? RR : RR + bc.n;
-            for (int e = 0; e < ub; ++e) {
-                if (o + e < cap) {
-                    ir[o + e] = (int32_t)K[e];
-                    pr[o + e] = __longlong_as_double((long long)V[e]);
-                } else {
-                    over = true;
-                }
+        // ---- pass 3: fold the short columns' values (predecessors publish meanwhile)
+        if (staged) {
+            for (int c = k_lo; c < k_hi; ++c) {
+                const uint32_t w0 = cs[c];
+                if (w0 & BIGFLAG) continue;
+                const int s0 = (int)(w0 & POSMASK), s1 = (int)(cs[c + 1] & POSMASK);
+                const int cnt = s1 - s0;
+                if (cnt > 0 && cnt <= SHORT_COL)
+                    fold_from_perm(&R[s0 - r0], &S.perm[s0 - r0], cnt, R[s0 - r0].y);
             }
-            o += ub;
-        } else if (s1 > s0 && staged) {
-            const int4 *R = &S.rec[s0 - r0];
-            const uint8_t *pm = &S.perm[s0 - r0];
-            const bool shrt = s1 - s0 <= SHORT_COL;  // short: outputs at slots pm[k]
-            const int u = R[shrt ? pm[0] : 0].y;     // every output record carries u
-            for (int k = 0; k < u; ++k) {
-                const int4 r = R[shrt ? pm[k] : k];
-                if (o + k < cap) {
-                    ir[o + k] = r.x;
-                    pr[o + k] = rec_val(r);
-                } else {
-                    over = true;
-                }
-            }
-            o += u;
         }
+        if (warp == 0) {
+            const long long P = lookback_warp32(tile_state, b, (unsigned long long)U);
+            if (lane == 0) S.P = P;
+        }
+        __syncthreads();
+        const long long P = S.P;
+
+        // ---- outputs (each thread: its columns, contiguous) and column pointers ----
+        long long o = P + tbase;
+        for (int c = k_lo; c < k_hi; ++c) {
+            jc[c_a + c] = (int32_t)o;
+            const uint32_t w0 = cs[c];
+            const int s0 = (int)(w0 & POSMASK), s1 = (int)(cs[c + 1] & POSMASK);
+            if (w0 & BIGFLAG) {
+                const BigCol bc = big_list[bigk[c_a + c]];
+                const int ub = (int)(bc.u & POSMASK);
+                const unsigned long long *RR = reinterpret_cast<const unsigned long long *>(rec + bc.start);
+                const unsigned long long *K = (bc.u & BIGFLAG) ? RR + bc.n : RR;
+                const unsigned long long *V = (bc.u & BIGFLAG) ? RR : RR + bc.n;
+                for (int e = 0; e < ub; ++e) {
+                    if (o + e < cap) {
+                        ir[o + e] = (int32_t)K[e];
+                        pr[o + e] = __longlong_as_double((long long)V[e]);
+                    } else {
+                        over_cap = true;
+                    }
+                }
+                o += ub;
+            } else if (s1 > s0 && staged) {
+                const int4 *Rc = &R[s0 - r0];
+                const uint8_t *pm = &S.perm[s0 - r0];
+                const bool shrt = s1 - s0 <= SHORT_COL;  // short: outputs at slots pm[k]
+                const int u = Rc[shrt ? pm[0] : 0].y;    // every output record carries u
+                for (int k = 0; k < u; ++k) {
+                    const int4 r = Rc[shrt ? pm[k] : k];
+                    if (o + k < cap) {
+                        ir[o + k] = r.x;
+                        pr[o + k] = rec_val(r);
+                    } else {
+                        over_cap = true;
+                    }
+                }
+                o += u;
+            }
+        }
+        if (b == ntiles - 1 && tid == 0) {
+            jc[N] = (int32_t)(P + U);
+            err->nnz = P + U;
+            if (P + U > cap) atomicExch(&err->cap_exceeded, 1u);
+        }
+        d0 = d1;
+        d1 = d2;
     }
-    if (over) atomicExch(&err->cap_exceeded, 1u);
-    if (b == ntiles - 1 && tid == 0) {
-        jc[N] = (int32_t)(P + U);
-        err->nnz = P + U;
-        if (P + U > cap) atomicExch(&err->cap_exceeded, 1u);
+    cp_async_wait_all();
+    if (over_cap) atomicExch(&err->cap_exceeded, 1u);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        badp = min(badp, __shfl_xor_sync(FULL, badp, o));
+        over_m |= __shfl_xor_sync(FULL, (unsigned)over_m, o) != 0u;
+    }
+    if (lane == 0) {
+        if (badp != ~0ull) atomicMin(&err->bad_i, badp);
+        if (over_m) err->over_m = 1;
     }
 }
 
 cudaError_t launch_tile_fold(Launch &lc, const uint32_t *sstart, const int2 *tile_info,
-                             const uint8_t *tile_big, int64_t ntiles, const int4 *rec,
-                             const BigCol *big_list, const uint32_t *bigk,
+                             const uint8_t *tile_big, int64_t ntiles, const uint32_t *perm,
+                             const int32_t *ii, const double *s, int64_t s_stride, int32_t M,
+                             const int4 *rec, const BigCol *big_list, const uint32_t *bigk,
                              unsigned long long *tile_state, int32_t N, int32_t *jc, int32_t *ir,
                              double *pr, int64_t cap, ErrState *err) {
     if (ntiles <= 0) return cudaSuccess;
-    const size_t smem = sizeof(TileSmem);
-    cudaError_t e = cudaFuncSetAttribute(k_tile_fold, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
-    if (e != cudaSuccess) return e;
-    k_tile_fold<<<(unsigned)ntiles, NT, smem, lc.stream>>>(sstart, tile_info, tile_big, ntiles, rec,
-                                                          big_list, bigk, tile_state, N, jc, ir, pr,
-                                                          cap, err);
+    // SA_FOLD_PERSIST=1: persistent double-buffered CTAs (cooperative launch);
+    // default: one CTA per tile, single buffer
+    static int mode = -1;
+    static int occ = -1;
+    if (mode < 0) {
+        const char *ev = getenv("SA_FOLD_PERSIST");
+        mode = (ev && ev[0] == '1') ? 1 : 0;
+        cudaError_t e = cudaFuncSetAttribute(k_tile_fold<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)sizeof(TileSmem<2>));
+        if (e != cudaSuccess) return e;
+        e = cudaFuncSetAttribute(k_tile_fold<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)sizeof(TileSmem<1>));
+        if (e != cudaSuccess) return e;
+        int o = 0;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_tile_fold<2>, NT, sizeof(TileSmem<2>));
+        if (e != cudaSuccess) return e;
+        if (o < 1) return cudaErrorInvalidConfiguration;
+        occ = o;
+    }
+    cudaError_t e;
+    if (mode == 1) {
+        const int64_t grid = std::min<int64_t>(ntiles, (int64_t)occ * lc.num_sms);
+        void *args[] = {(void *)&sstart, (void *)&tile_info, (void *)&tile_big, (void *)&ntiles,
+                        (void *)&perm, (void *)&ii, (void *)&s, (void *)&s_stride, (void *)&M,
+                        (void *)&rec, (void *)&big_list, (void *)&bigk, (void *)&tile_state,
+                        (void *)&N, (void *)&jc, (void *)&ir, (void *)&pr, (void *)&cap, (void *)&err};
+        e = cudaLaunchCooperativeKernel((const void *)k_tile_fold<2>, dim3((unsigned)grid), dim3(NT),
+                                        args, sizeof(TileSmem<2>), lc.stream);
+    } else {
+        k_tile_fold<1><<<(unsigned)ntiles, NT, sizeof(TileSmem<1>), lc.stream>>>(
+            sstart, tile_info, tile_big, ntiles, perm, ii, s, s_stride, M, rec, big_list, bigk,
+            tile_state, N, jc, ir, pr, cap, err);
+        e = cudaGetLastError();
+    }
     lc.launches++;
-    return cudaGetLastError();
+    return e;
 }
 
 }  // namespace sa

@@ -1,5 +1,5 @@
-"""Per-kernel times (CUDA events inside the C ABI) of cfg2 through a given libsa .so.
-usage: python tools/kernel_times.py path/to/libsa.so"""
+"""Per-kernel times (CUDA events inside the C ABI) through a given libsa .so.
+usage: python tools/kernel_times.py path/to/libsa.so [config]"""
 import ctypes, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -8,9 +8,10 @@ lib = ctypes.CDLL(sys.argv[1])
 for name, (res, args) in _capi.SIGNATURES.items():
     f = getattr(lib, name); f.restype = res; f.argtypes = args
 ctx = ctypes.c_void_p(); lib.sa_create(0, ctypes.byref(ctx))
-w = W.config(2, device="cuda")
+cfg = int(sys.argv[2]) if len(sys.argv) > 2 else 2
+w = W.config(cfg, device="cuda")
 L, M, N = w.L, w.m, w.n
-jc = torch.empty(N + 1, dtype=torch.int32, device="cuda"); ir = torch.empty(2*L, dtype=torch.int32, device="cuda"); pr = torch.empty(2*L, dtype=torch.float64, device="cuda")
+jc = torch.empty(N + 1, dtype=torch.int32, device="cuda"); ir = torch.empty(L, dtype=torch.int32, device="cuda"); pr = torch.empty(L, dtype=torch.float64, device="cuda")
 s = torch.cuda.current_stream(); lib.sa_set_stream(ctx, ctypes.c_void_p(s.cuda_stream))
 lib.sa_enable_timing(ctx, 1)
 tot = {}
@@ -20,4 +21,4 @@ for it in range(12):
     n = lib.sa_last_kernel_times(ctx, 16, arr, names)
     if it >= 2:
         for k in range(n): tot.setdefault(names[k].decode(), []).append(arr[k])
-print(sys.argv[1].split('/')[-1], {k: round(sum(v)/len(v)*1e3, 1) for k, v in tot.items()})
+print(sys.argv[1].split('/')[-1], 'cfg%d' % cfg, {k: round(sum(v)/len(v)*1e3, 1) for k, v in tot.items()})
