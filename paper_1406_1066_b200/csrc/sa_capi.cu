@@ -26,7 +26,7 @@ struct sa_ctx {
     // device workspace (grown on demand, reused across calls)
     uint32_t *cur = nullptr;              size_t cur_cap = 0;     // N (counts, then cursors)
     uint32_t *sstart = nullptr;           size_t st_cap = 0;      // N+1 small-space starts
-    uint32_t *perm = nullptr;             size_t perm_cap = 0;    // L + placeholders: positions by column
+    uint2 *perm = nullptr;                size_t perm_cap = 0;    // L + placeholders: {position, row} by column
     int4 *rec = nullptr;                  size_t rec_cap = 0;     // big-column scratch (16 B per slot)
     int2 *tile_info = nullptr;            size_t ti_cap = 0;      // ntiles+1
     uint8_t *tile_big = nullptr;          size_t tb_cap = 0;      // ntiles
@@ -50,11 +50,6 @@ struct sa_ctx {
     int nev = 0;
     cudaEvent_t ev[MAXEV + 1] = {};
     const char *ev_name[MAXEV] = {};
-
-    // the last device assembly (for the row re-validation of the error path)
-    const int32_t *last_ii = nullptr;
-    const int32_t *last_jj = nullptr;
-    int64_t last_L = 0;
 
     int64_t host_L = -1;
     int64_t host_stride = 1;
@@ -372,7 +367,6 @@ int sa_assemble_async(sa_ctx *ctx, const int32_t *d_ii, const int32_t *d_jj, con
     SA_CUDA(ctx, cudaSetDevice(ctx->device));
     Launch lc{ctx->stream, ctx->num_sms, 0};
 
-    ctx->last_L = 0;
     if (L == 0 || N == 0) {
         // nothing to assemble (L > 0 with N == 0 means every column index is
         // out of range: k_hist still flags it)
@@ -412,26 +406,23 @@ int sa_assemble_async(sa_ctx *ctx, const int32_t *d_ii, const int32_t *d_jj, con
                                  ctx->tile_big, ntiles, ctx->big_list, ctx->bigk, ctx->scan_state,
                                  ctx->perm, ctx->err));
     if ((rc = mark(ctx, "k_scatter"))) return rc;
-    SA_CUDA(ctx, launch_scatter(lc, d_jj, L, N, ctx->cur, ctx->perm, ctx->err));
+    SA_CUDA(ctx, launch_scatter(lc, d_ii, d_jj, L, M, N, ctx->cur, ctx->perm, ctx->err));
     if (L > BIGCOL) {
         const int idx_bits = std::max(1, bits_for((uint64_t)(L - 1)));
         const int row_bits = bits_for((uint64_t)(M > 0 ? M - 1 : 0));
         const int passes = std::max(1, (idx_bits + row_bits + 7) / 8);
         if ((rc = mark(ctx, "k_bigcol"))) return rc;
-        SA_CUDA(ctx, launch_bigcol(lc, ctx->big_list, ctx->err, ctx->rec, ctx->perm, d_ii, M, d_s,
-                                   s_stride, idx_bits,
+        SA_CUDA(ctx, launch_bigcol(lc, ctx->big_list, ctx->err, ctx->rec, ctx->perm, d_s, s_stride,
+                                   idx_bits,
                                    passes));
     }
     if ((rc = mark(ctx, "k_tile_fold"))) return rc;
     SA_CUDA(ctx, launch_tile_fold(lc, ctx->sstart, ctx->tile_info, ctx->tile_big, ntiles, ctx->perm,
-                                  d_ii, d_s, s_stride, M, ctx->rec,
+                                  d_s, s_stride, ctx->rec,
                                   ctx->big_list, ctx->bigk, ctx->tile_state, N, d_jc, d_ir, d_pr,
                                   cap, ctx->err));
     if ((rc = mark(ctx, nullptr))) return rc;
     ctx->launches = lc.launches;
-    ctx->last_ii = d_ii;
-    ctx->last_jj = d_jj;
-    ctx->last_L = L;
     return SA_OK;
 }
 
@@ -440,16 +431,6 @@ int sa_finish(sa_ctx *ctx, int64_t *nnz, int64_t *bad_pos, int *bad_which) {
     SA_CUDA(ctx, cudaSetDevice(ctx->device));
     SA_CUDA(ctx, cudaMemcpyAsync(ctx->err_host, ctx->err, sizeof(ErrState), cudaMemcpyDeviceToHost, ctx->stream));
     SA_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-    const ErrState &e = *ctx->err_host;
-    if (e.bad_i == ~0ull && (e.bad_j != ~0ull || e.over_n) && ctx->last_L > 0) {
-        // error path: triplets with invalid columns never reached the fold,
-        // so their rows were not validated; rows take precedence
-        // (types.py:161-162) -- validate every row now
-        Launch lc{ctx->stream, ctx->num_sms, 0};
-        SA_CUDA(ctx, launch_hist(lc, ctx->last_ii, ctx->last_jj, ctx->last_L, 0, 0, nullptr, ctx->err, true));
-        SA_CUDA(ctx, cudaMemcpyAsync(ctx->err_host, ctx->err, sizeof(ErrState), cudaMemcpyDeviceToHost, ctx->stream));
-        SA_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-    }
     return decode(ctx, *ctx->err_host, nnz, bad_pos, bad_which);
 }
 

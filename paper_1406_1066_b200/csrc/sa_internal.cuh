@@ -279,18 +279,17 @@ cudaError_t launch_hist(Launch &lc, const int32_t *ii, const int32_t *jj, int64_
 cudaError_t launch_col_scan(Launch &lc, const uint32_t *cnt, uint32_t *sstart, uint32_t *cur,
                             int32_t N, int2 *tile_info, uint8_t *tile_big,
                             int64_t ntiles, BigCol *big_list, uint32_t *bigk,
-                            unsigned long long *scan_state, uint32_t *perm, ErrState *err);
+                            unsigned long long *scan_state, uint2 *perm, ErrState *err);
 cudaError_t launch_colcount(Launch &lc, const int32_t *jj, int64_t L, int32_t N, uint32_t *cnt,
                             ErrState *err);
-cudaError_t launch_scatter(Launch &lc, const int32_t *jj, int64_t L, int32_t N, uint32_t *cur,
-                           uint32_t *perm, ErrState *err);
-cudaError_t launch_bigcol(Launch &lc, BigCol *big_list, ErrState *err, int4 *rec,
-                          const uint32_t *perm, const int32_t *ii, int32_t M, const double *s,
-                          int64_t s_stride, int idx_bits, int passes);
+cudaError_t launch_scatter(Launch &lc, const int32_t *ii, const int32_t *jj, int64_t L, int32_t M,
+                           int32_t N, uint32_t *cur, uint2 *perm, ErrState *err);
+cudaError_t launch_bigcol(Launch &lc, BigCol *big_list, const ErrState *err, int4 *rec,
+                          const uint2 *perm, const double *s, int64_t s_stride, int idx_bits,
+                          int passes);
 cudaError_t launch_tile_fold(Launch &lc, const uint32_t *sstart, const int2 *tile_info,
-                             const uint8_t *tile_big, int64_t ntiles, const uint32_t *perm,
-                             const int32_t *ii, const double *s, int64_t s_stride, int32_t M,
-                             const int4 *rec,
+                             const uint8_t *tile_big, int64_t ntiles, const uint2 *perm,
+                             const double *s, int64_t s_stride, const int4 *rec,
                              const BigCol *big_list, const uint32_t *bigk,
                              unsigned long long *tile_state, int32_t N, int32_t *jc,
                              int32_t *ir, double *pr, int64_t cap, ErrState *err);

@@ -21,6 +21,8 @@
 // because both order entries by (column, row) and fold duplicates in
 // ascending input order.
 
+#include <cstdlib>
+
 #include "sa_internal.cuh"
 
 namespace sa {
@@ -228,7 +230,7 @@ __global__ void __launch_bounds__(SCAN_NT) k_col_scan(const uint32_t *cnt,
                                                       BigCol *__restrict__ big_list,
                                                       uint32_t *__restrict__ bigk,
                                                       unsigned long long *scan_state,
-                                                      uint32_t *__restrict__ perm,
+                                                      uint2 *__restrict__ perm,
                                                       ErrState *err) {
     __shared__ unsigned long long s_warp[SCAN_NT / 32];
     __shared__ long long s_b;
@@ -279,7 +281,7 @@ __global__ void __launch_bounds__(SCAN_NT) k_col_scan(const uint32_t *cnt,
                 const unsigned slot = atomicAdd(&err->nbig, 1u);
                 big_list[slot] = BigCol{(uint32_t)c, (uint32_t)bigp, n, 0u};
                 bigk[c] = slot;
-                perm[small] = 0xffffffffu;  // placeholder slot: nothing to gather
+                perm[small] = make_uint2(0xffffffffu, 0u);  // placeholder slot: nothing to gather
                 int64_t tb = (int64_t)(small / TILE);
                 if (tb > ntiles - 1) tb = ntiles - 1;
                 tile_big[tb] = 1;
@@ -336,7 +338,7 @@ __global__ void __launch_bounds__(SCAN_NT) k_col_scan(const uint32_t *cnt,
 cudaError_t launch_col_scan(Launch &lc, const uint32_t *cnt, uint32_t *sstart, uint32_t *cur,
                             int32_t N, int2 *tile_info, uint8_t *tile_big,
                             int64_t ntiles, BigCol *big_list, uint32_t *bigk,
-                            unsigned long long *scan_state, uint32_t *perm, ErrState *err) {
+                            unsigned long long *scan_state, uint2 *perm, ErrState *err) {
     if (N <= 0) return cudaSuccess;
     int grid = (int)((N + SCAN_TILE - 1) / SCAN_TILE);
     k_col_scan<<<grid, SCAN_NT, 0, lc.stream>>>(cnt, sstart, cur, N, tile_info, tile_big,
@@ -486,29 +488,95 @@ __global__ void __launch_bounds__(AGG_NT) k_colcount(const int32_t *__restrict__
     }
 }
 
+// Direct variant: each column run (per thread, CPT consecutive triplets)
+// issues one global reduction, with no shared-memory aggregation.
+__global__ void __launch_bounds__(AGG_NT) k_colcount_direct(const int32_t *__restrict__ jj,
+                                                            int64_t L, int32_t N,
+                                                            uint32_t *__restrict__ cnt,
+                                                            ErrState *err, int vec) {
+    unsigned long long bad = ~0ull;
+    unsigned over = 0;
+    const int64_t nrun = (L + CPT - 1) / CPT;
+    for (int64_t r = (int64_t)blockIdx.x * AGG_NT + threadIdx.x; r < nrun;
+         r += (int64_t)gridDim.x * AGG_NT) {
+        const int64_t t0 = r * CPT;
+        int j[CPT];
+        load_run(jj, t0, L, vec, j, 0x7fffffff);
+        bool vk[CPT];
+        int len[CPT];
+#pragma unroll
+        for (int k = 0; k < CPT; ++k) {
+            const bool live = t0 + k < L;
+            if (live && j[k] < 1) bad = min(bad, (unsigned long long)(t0 + k));
+            if (live && j[k] > N) over = 1;
+            vk[k] = live && j[k] >= 1 && j[k] <= N;
+        }
+        run_lengths(j, vk, len);
+#pragma unroll
+        for (int k = 0; k < CPT; ++k)
+            if (vk[k] && run_head(j, vk, k)) atomicAdd(&cnt[j[k] - 1], (uint32_t)len[k]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        bad = min(bad, __shfl_xor_sync(FULL, bad, o));
+        over |= __shfl_xor_sync(FULL, over, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (bad != ~0ull) atomicMin(&err->bad_j, bad);
+        if (over) err->over_n = 1;
+    }
+}
+
+// Experiment switches (measured on cfg2/cfg3/cfg4): the
+// column histogram defaults to direct reductions, the scatter to CTA-scope
+// aggregation.  SA_COLCOUNT_AGG=1 / SA_SCATTER_DIRECT=1 flip them.
+static bool env_flag(const char *name) {
+    const char *e = getenv(name);
+    return e && e[0] == '1';
+}
+static bool colcount_agg() {
+    static int m = -1;
+    if (m < 0) m = env_flag("SA_COLCOUNT_AGG") ? 1 : 0;
+    return m == 1;
+}
+static bool scatter_agg() {
+    static int m = -1;
+    if (m < 0) m = env_flag("SA_SCATTER_DIRECT") ? 0 : 1;
+    return m == 1;
+}
+
 cudaError_t launch_colcount(Launch &lc, const int32_t *jj, int64_t L, int32_t N, uint32_t *cnt,
                             ErrState *err) {
     if (L <= 0) return cudaSuccess;
     const int vec = aligned16(jj);
     const int64_t nchunk = (L + CHUNK - 1) / CHUNK;
     int grid = (int)std::min<int64_t>(nchunk, (int64_t)lc.num_sms * 4);
-    k_colcount<<<grid, AGG_NT, 0, lc.stream>>>(jj, L, N, cnt, err, vec);
+    if (colcount_agg()) {
+        k_colcount<<<grid, AGG_NT, 0, lc.stream>>>(jj, L, N, cnt, err, vec);
+    } else {
+        const int64_t want = ((L + CPT - 1) / CPT + AGG_NT - 1) / AGG_NT;
+        const int g = (int)std::min<int64_t>(want, (int64_t)lc.num_sms * 8);
+        k_colcount_direct<<<g, AGG_NT, 0, lc.stream>>>(jj, L, N, cnt, err, vec);
+    }
     lc.launches++;
     return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------------------
-// k_scatter: counting-sort scatter by column of the input POSITIONS only
-// (4 bytes per triplet; the fold gathers rows and values by position, so
-// the triplets' 12 payload bytes are read once, by the fold).  Per chunk:
-// (1) each column run gets chunk-local slots from a shared-memory counter,
-// (2) one global atomicAdd per distinct column reserves the chunk's slots on
-// the column cursor, (3) positions are written.  The slot order inside a
-// column is arbitrary; the fold restores input order from the position.
+// k_scatter: counting-sort scatter by column of 8-byte entries {input
+// position, row} (the fold gathers the values by position, so the 8-byte
+// values are read once, by the fold).  Per chunk: (1) each column run gets
+// chunk-local slots from a shared-memory counter, (2) one global atomicAdd
+// per distinct column reserves the chunk's slots on the column cursor, (3)
+// entries are written.  Row indices are validated here for every triplet
+// (first bad position, rows above M).  The slot order inside a column is
+// arbitrary; the fold restores input order from the position.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(AGG_NT) k_scatter(const int32_t *__restrict__ jj, int64_t L,
-                                                    int32_t N, uint32_t *__restrict__ cur,
-                                                    uint32_t *__restrict__ perm, int vec,
+__global__ void __launch_bounds__(AGG_NT) k_scatter(const int32_t *__restrict__ ii,
+                                                    const int32_t *__restrict__ jj, int64_t L,
+                                                    int32_t M, int32_t N,
+                                                    uint32_t *__restrict__ cur,
+                                                    uint2 *__restrict__ perm, int vec,
                                                     ErrState *err) {
     __shared__ AggSmem A;
     const int tid = threadIdx.x;
@@ -519,21 +587,37 @@ __global__ void __launch_bounds__(AGG_NT) k_scatter(const int32_t *__restrict__ 
     if (tid == 0) A.nused = 0;
     __syncthreads();
     const uint32_t lsmall = err->lsmall;
+    unsigned long long bad = ~0ull;
+    unsigned over = 0;
     const int64_t nchunk = (L + CHUNK - 1) / CHUNK;
-    int jn[CPT];
-    if ((int64_t)blockIdx.x < nchunk)
-        load_run(jj, (int64_t)blockIdx.x * CHUNK + (int64_t)tid * CPT, L, vec, jn, 0);
+    int in_[CPT], jn[CPT];
+    if ((int64_t)blockIdx.x < nchunk) {
+        const int64_t t0 = (int64_t)blockIdx.x * CHUNK + (int64_t)tid * CPT;
+        load_run(ii, t0, L, vec, in_, 1);
+        load_run(jj, t0, L, vec, jn, 0);
+    }
     for (int64_t ch = blockIdx.x; ch < nchunk; ch += gridDim.x) {
         const int64_t t0 = ch * CHUNK + (int64_t)tid * CPT;
-        int j[CPT];
+        int i[CPT], j[CPT];
 #pragma unroll
-        for (int k = 0; k < CPT; ++k) j[k] = jn[k];
-        if (ch + gridDim.x < nchunk)  // next chunk in flight
-            load_run(jj, (ch + gridDim.x) * CHUNK + (int64_t)tid * CPT, L, vec, jn, 0);
+        for (int k = 0; k < CPT; ++k) {
+            i[k] = in_[k];
+            j[k] = jn[k];
+        }
+        if (ch + gridDim.x < nchunk) {  // next chunk in flight
+            const int64_t t1 = (ch + gridDim.x) * CHUNK + (int64_t)tid * CPT;
+            load_run(ii, t1, L, vec, in_, 1);
+            load_run(jj, t1, L, vec, jn, 0);
+        }
         bool vk[CPT];
         int len[CPT], hk[CPT], rk[CPT];
 #pragma unroll
-        for (int k = 0; k < CPT; ++k) vk[k] = (t0 + k < L) && j[k] >= 1 && j[k] <= N;
+        for (int k = 0; k < CPT; ++k) {
+            const bool live = t0 + k < L;
+            if (live && i[k] < 1) bad = min(bad, (unsigned long long)(t0 + k));
+            if (live && i[k] > M) over = 1;
+            vk[k] = live && j[k] >= 1 && j[k] <= N;
+        }
         run_lengths(j, vk, len);
 #pragma unroll
         for (int k = 0; k < CPT; ++k) {
@@ -561,7 +645,7 @@ __global__ void __launch_bounds__(AGG_NT) k_scatter(const int32_t *__restrict__ 
             if (hk[k] < 0) continue;
             const uint32_t bw = (uint32_t)A.ctr[hk[k]];
             const uint32_t pos = (bw & POSMASK) + ((bw & BIGFLAG) ? lsmall : 0u) + (uint32_t)rk[k];
-            perm[pos] = (uint32_t)(t0 + k);
+            perm[pos] = make_uint2((uint32_t)(t0 + k), (uint32_t)i[k]);
         }
         __syncthreads();
         for (int e = tid; e < nu; e += AGG_NT) {
@@ -572,37 +656,104 @@ __global__ void __launch_bounds__(AGG_NT) k_scatter(const int32_t *__restrict__ 
         if (tid == 0) A.nused = 0;
         __syncthreads();
     }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        bad = min(bad, __shfl_xor_sync(FULL, bad, o));
+        over |= __shfl_xor_sync(FULL, over, o);
+    }
+    if ((tid & 31) == 0) {
+        if (bad != ~0ull) atomicMin(&err->bad_i, bad);
+        if (over) err->over_m = 1;
+    }
 }
 
-cudaError_t launch_scatter(Launch &lc, const int32_t *jj, int64_t L, int32_t N, uint32_t *cur,
-                           uint32_t *perm, ErrState *err) {
+// Direct variant: one global cursor reservation (atomicAdd with return) per
+// column run; all of a thread's reservations are in flight together.
+__global__ void __launch_bounds__(AGG_NT) k_scatter_direct(const int32_t *__restrict__ ii,
+                                                           const int32_t *__restrict__ jj,
+                                                           int64_t L, int32_t M, int32_t N,
+                                                           uint32_t *__restrict__ cur,
+                                                           uint2 *__restrict__ perm, int vec,
+                                                           ErrState *err) {
+    const uint32_t lsmall = err->lsmall;
+    unsigned long long bad = ~0ull;
+    unsigned over = 0;
+    const int64_t nrun = (L + CPT - 1) / CPT;
+    for (int64_t r = (int64_t)blockIdx.x * AGG_NT + threadIdx.x; r < nrun;
+         r += (int64_t)gridDim.x * AGG_NT) {
+        const int64_t t0 = r * CPT;
+        int i[CPT], j[CPT];
+        load_run(ii, t0, L, vec, i, 1);
+        load_run(jj, t0, L, vec, j, 0);
+        bool vk[CPT];
+        int len[CPT];
+#pragma unroll
+        for (int k = 0; k < CPT; ++k) {
+            const bool live = t0 + k < L;
+            if (live && i[k] < 1) bad = min(bad, (unsigned long long)(t0 + k));
+            if (live && i[k] > M) over = 1;
+            vk[k] = live && j[k] >= 1 && j[k] <= N;
+        }
+        run_lengths(j, vk, len);
+        uint32_t w[CPT];
+#pragma unroll
+        for (int k = 0; k < CPT; ++k) {
+            w[k] = 0;
+            if (vk[k] && run_head(j, vk, k)) w[k] = atomicAdd(&cur[j[k] - 1], (uint32_t)len[k]);
+        }
+        uint32_t slot = 0;
+#pragma unroll
+        for (int k = 0; k < CPT; ++k) {
+            if (!vk[k]) continue;
+            if (run_head(j, vk, k)) slot = (w[k] & POSMASK) + ((w[k] & BIGFLAG) ? lsmall : 0u);
+            else slot += 1;
+            perm[slot] = make_uint2((uint32_t)(t0 + k), (uint32_t)i[k]);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        bad = min(bad, __shfl_xor_sync(FULL, bad, o));
+        over |= __shfl_xor_sync(FULL, over, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (bad != ~0ull) atomicMin(&err->bad_i, bad);
+        if (over) err->over_m = 1;
+    }
+}
+
+cudaError_t launch_scatter(Launch &lc, const int32_t *ii, const int32_t *jj, int64_t L, int32_t M,
+                           int32_t N, uint32_t *cur, uint2 *perm, ErrState *err) {
     if (L <= 0) return cudaSuccess;
-    const int vec = aligned16(jj);
+    const int vec = aligned16(ii) && aligned16(jj);
     const int64_t nchunk = (L + CHUNK - 1) / CHUNK;
     int grid = (int)std::min<int64_t>(nchunk, (int64_t)lc.num_sms * 4);
-    k_scatter<<<grid, AGG_NT, 0, lc.stream>>>(jj, L, N, cur, perm, vec, err);
+    if (scatter_agg()) {
+        k_scatter<<<grid, AGG_NT, 0, lc.stream>>>(ii, jj, L, M, N, cur, perm, vec, err);
+    } else {
+        const int64_t want = ((L + CPT - 1) / CPT + AGG_NT - 1) / AGG_NT;
+        const int g = (int)std::min<int64_t>(want, (int64_t)lc.num_sms * 8);
+        k_scatter_direct<<<g, AGG_NT, 0, lc.stream>>>(ii, jj, L, M, N, cur, perm, vec, err);
+    }
     lc.launches++;
     return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------------------
 // k_bigcol: one CTA per big column (grid-stride over the device-side list).
-// The column's positions (perm, big space) are gathered into keys
+// The column's entries {position, row} (big space) become keys
 // key = (row-1) << idx_bits | input position in two 8-byte buffers A|B
 // (the column's 16-byte slots of the big scratch).  Stable LSD radix
 // passes (8-bit digits, warp match + per-warp digit counts) sort by (row,
 // position); values are gathered from the input by position; each run of
 // equal rows is folded from +0.0 in position order.  Results: row-1 in the
 // key buffer, value bits in the other buffer, at index = run number;
-// bigu[c] = runs | (BIGFLAG if keys ended in buffer B).  Rows are validated
-// here (the fold validates the short columns' rows).
+// bigu[c] = runs | (BIGFLAG if keys ended in buffer B).
 // ---------------------------------------------------------------------------
 constexpr int BIG_NT = 256;
 
 __global__ void __launch_bounds__(BIG_NT) k_bigcol(BigCol *__restrict__ big_list,
-                                                   ErrState *err, int4 *rec,
-                                                   const uint32_t *__restrict__ perm,
-                                                   const int32_t *__restrict__ ii, int32_t M,
+                                                   const ErrState *err, int4 *rec,
+                                                   const uint2 *__restrict__ perm,
                                                    const double *__restrict__ s, int64_t s_stride,
                                                    int idx_bits, int passes) {
     __shared__ uint32_t s_hist[256];
@@ -616,20 +767,15 @@ __global__ void __launch_bounds__(BIG_NT) k_bigcol(BigCol *__restrict__ big_list
     for (int k = tid; k < (BIG_NT / 32) * 257; k += BIG_NT) (&s_wcnt[0][0])[k] = 0;
     __syncthreads();
     const unsigned long long idx_mask = (1ull << idx_bits) - 1;
-    unsigned long long bad = ~0ull;
-    unsigned over = 0;
     for (unsigned kb = blockIdx.x; kb < nbig; kb += gridDim.x) {
         const uint32_t st = big_list[kb].start + lsmall;
         const int64_t n = big_list[kb].n;
         unsigned long long *A = reinterpret_cast<unsigned long long *>(rec + st);
         unsigned long long *B = A + n;
-        // gather rows by position -> keys in A
+        // entries {position, row} -> keys in A
         for (int64_t p = tid; p < n; p += BIG_NT) {
-            const uint32_t pos = perm[st + p];
-            const int32_t row = ii[pos];
-            if (row < 1) bad = min(bad, (unsigned long long)pos);
-            if (row > M) over = 1;
-            A[p] = ((unsigned long long)(uint32_t)(row - 1) << idx_bits) | pos;
+            const uint2 e = perm[st + p];
+            A[p] = ((unsigned long long)(e.y - 1u) << idx_bits) | e.x;
         }
         __syncthreads();
         unsigned long long *src = A, *dst = B;
@@ -728,23 +874,13 @@ __global__ void __launch_bounds__(BIG_NT) k_bigcol(BigCol *__restrict__ big_list
         }
         __syncthreads();
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        bad = min(bad, __shfl_xor_sync(FULL, bad, o));
-        over |= __shfl_xor_sync(FULL, over, o);
-    }
-    if (lane == 0) {
-        if (bad != ~0ull) atomicMin(&err->bad_i, bad);
-        if (over) err->over_m = 1;
-    }
 }
 
-cudaError_t launch_bigcol(Launch &lc, BigCol *big_list, ErrState *err, int4 *rec,
-                          const uint32_t *perm, const int32_t *ii, int32_t M, const double *s,
-                          int64_t s_stride, int idx_bits, int passes) {
+cudaError_t launch_bigcol(Launch &lc, BigCol *big_list, const ErrState *err, int4 *rec,
+                          const uint2 *perm, const double *s, int64_t s_stride, int idx_bits,
+                          int passes) {
     int grid = lc.num_sms;
-    k_bigcol<<<grid, BIG_NT, 0, lc.stream>>>(big_list, err, rec, perm, ii, M, s, s_stride, idx_bits,
-                                             passes);
+    k_bigcol<<<grid, BIG_NT, 0, lc.stream>>>(big_list, err, rec, perm, s, s_stride, idx_bits, passes);
     lc.launches++;
     return cudaGetLastError();
 }

@@ -42,12 +42,16 @@ constexpr int LCAP = TILE / (SHORT_COL + 1) + 2;  // long columns per tile
 constexpr int SCAP = 256;                         // staged column starts per tile
 constexpr int MAXU = 96;                          // distinct rows of a long column (warp table)
 
-struct WarpScratch {
+struct WarpScratchGroups {
     uint8_t gid[BIGCOL];               // group (table entry) of each record
     int16_t arr[BIGCOL];               // arrival rank inside the group
     int16_t mem[BIGCOL];               // group-major member list (record slots)
     int gcnt[MAXU];
     int gbase[MAXU];
+};
+union WarpScratch {
+    WarpScratchGroups g;               // fold_column_warp (fallback)
+    unsigned long long skey[256];      // fold_column_bitonic: sorted keys
 };
 
 template <int NBUF>
@@ -57,7 +61,6 @@ struct TileSmem {
     WarpScratch ws[NWARP];
     int lcol[LCAP];                    // long columns: record offset | (count << 16)
     uint32_t scol[NBUF][SCAP];         // sstart of the tile's columns (when they fit)
-    int wl[NT + 1];                    // first column of each thread window (tile-relative)
     int nlong;
     int warp_u[NWARP];
     long long P;
@@ -329,7 +332,7 @@ __device__ __forceinline__ int tab_get(const int (&tab)[3], int k) {
 // in position order (match.any; deterministic).  Then per group (lane per
 // group): members ordered by input position, folded from +0.0, placed by row.
 // More than MAXU distinct rows: lane 0 folds the column alone.
-__device__ int fold_column_warp(int4 *R, int c, WarpScratch &W) {
+__device__ int fold_column_warp(int4 *R, int c, WarpScratchGroups &W) {
     const int lane = threadIdx.x & 31;
     const unsigned lt = lanemask_lt();
     int tab[3] = {0, 0, 0};
@@ -459,6 +462,136 @@ __device__ int fold_column_warp(int4 *R, int c, WarpScratch &W) {
     return u;
 }
 
+// Warp-wide bitonic sort of 32*E 64-bit keys, blocked layout (lane holds
+// elements lane*E .. lane*E+E-1): partner distances >= E are shuffles,
+// shorter ones are register compare-exchanges.
+template <int E>
+__device__ __forceinline__ void warp_bitonic(unsigned long long (&k)[E]) {
+    const int lane = threadIdx.x & 31;
+    constexpr int P = 32 * E;
+#pragma unroll
+    for (int size = 2; size <= P; size <<= 1) {
+#pragma unroll
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            if (stride >= E) {
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    const int i = lane * E + e;
+                    const unsigned long long o = __shfl_xor_sync(FULL, k[e], stride / E);
+                    const bool up = (i & size) == 0;
+                    const bool lower = (i & stride) == 0;
+                    const bool take = (lower == up) ? (o < k[e]) : (k[e] < o);
+                    k[e] = take ? o : k[e];
+                }
+            } else {
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    const int q = e ^ stride;
+                    if (q > e) {
+                        const bool up = ((lane * E + e) & size) == 0;
+                        const unsigned long long a = k[e], b = k[q];
+                        const bool sw = up ? (b < a) : (a < b);
+                        k[e] = sw ? b : a;
+                        k[q] = sw ? a : b;
+                    }
+                }
+            }
+        }
+    }
+}
+
+// Warp-cooperative fold of one column of c (<= 32*E) records: one bitonic
+// sort of the packed key (row - rmin) << (PB+SB) | (pos - pmin) << SB | slot
+// puts the records in (row, input position) order; the lane holding a run
+// head folds the run of equal rows from +0.0 in that order (the reference's
+// order, _kernels.pyx:82-89).  Outputs (row-1, u, value) at R[0..u).
+// Returns u, or -1 (nothing written) when the spans do not fit 64 bits.
+template <int E>
+__device__ int fold_column_bitonic(int4 *R, int c, unsigned long long *skey) {
+    constexpr int SB = (E == 1) ? 5 : (E == 2) ? 6 : (E == 4) ? 7 : (E == 8) ? 8 : 9;
+    const int lane = threadIdx.x & 31;
+    int2 rp[E];
+    unsigned rmin = 0xffffffffu, rmax = 0u, pmin = 0xffffffffu, pmax = 0u;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        const int i = lane * E + e;
+        rp[e] = (i < c) ? *reinterpret_cast<const int2 *>(&R[i]) : make_int2(0, 0);
+        if (i < c) {
+            rmin = min(rmin, (unsigned)rp[e].x);
+            rmax = max(rmax, (unsigned)rp[e].x);
+            pmin = min(pmin, (unsigned)rp[e].y);
+            pmax = max(pmax, (unsigned)rp[e].y);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        rmin = min(rmin, __shfl_xor_sync(FULL, rmin, o));
+        rmax = max(rmax, __shfl_xor_sync(FULL, rmax, o));
+        pmin = min(pmin, __shfl_xor_sync(FULL, pmin, o));
+        pmax = max(pmax, __shfl_xor_sync(FULL, pmax, o));
+    }
+    const int pb = span_bits(pmax - pmin), rb = span_bits(rmax - rmin);
+    if (rb + pb + SB > 63) return -1;
+    const int rs = pb + SB;
+    unsigned long long k[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        const int i = lane * E + e;
+        k[e] = (i < c) ? ((((unsigned long long)((unsigned)rp[e].x - rmin)) << rs) |
+                          ((unsigned long long)((unsigned)rp[e].y - pmin) << SB) | (unsigned)i)
+                       : ~0ull;
+    }
+    warp_bitonic<E>(k);
+#pragma unroll
+    for (int e = 0; e < E; ++e)
+        if (lane * E + e < c) skey[lane * E + e] = k[e];
+    // run heads and their output ranks
+    const unsigned long long prev_last = __shfl_up_sync(FULL, k[E - 1], 1);
+    unsigned hmask = 0;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        const int i = lane * E + e;
+        const unsigned long long pk = (e > 0) ? k[e > 0 ? e - 1 : 0] : prev_last;
+        if (i < c && (i == 0 || (k[e] >> rs) != (pk >> rs))) hmask |= 1u << e;
+    }
+    const int hc = __popc(hmask);
+    int incl = hc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(FULL, incl, o);
+        if (lane >= o) incl += y;
+    }
+    const int u = __shfl_sync(FULL, incl, 31);
+    int oidx = incl - hc;
+    __syncwarp();
+    constexpr unsigned SMASK = (1u << SB) - 1;
+    double acc[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        acc[e] = 0.0;
+        if (!(hmask & (1u << e))) continue;
+        const int i = lane * E + e;
+        const unsigned long long rk = k[e] >> rs;
+        double sacc = fold_add(0.0, rec_val(R[(unsigned)k[e] & SMASK]));
+        for (int j = i + 1; j < c; ++j) {
+            const unsigned long long y = skey[j];
+            if ((y >> rs) != rk) break;
+            sacc = fold_add(sacc, rec_val(R[(unsigned)y & SMASK]));
+        }
+        acc[e] = sacc;
+    }
+    __syncwarp();
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        if (!(hmask & (1u << e))) continue;
+        const int orow = (int)(rmin + (unsigned)(k[e] >> rs));
+        R[oidx] = make_int4(orow - 1, u, __double2loint(acc[e]), __double2hiint(acc[e]));
+        ++oidx;
+    }
+    __syncwarp();
+    return u;
+}
+
 // Publish tile b's aggregate (the inclusive prefix right away for tile 0).
 __device__ __forceinline__ void lookback_publish(unsigned long long *st, long long b,
                                                  unsigned long long agg) {
@@ -520,22 +653,21 @@ __device__ __forceinline__ TileDesc tile_desc(const int2 *__restrict__ tile_info
 constexpr int GPT = (TCAP + NT - 1) / NT;  // record slots per thread
 constexpr uint32_t NOPOS = 0xffffffffu;    // placeholder slot of a big column
 
-// Positions of a tile's record slots (tid + q*NT) into registers.
-__device__ __forceinline__ void load_positions(const uint32_t *__restrict__ perm, const TileDesc &d,
-                                               uint32_t (&p)[GPT]) {
+// Entries {position, row} of a tile's record slots (tid + q*NT) into registers.
+__device__ __forceinline__ void load_entries(const uint2 *__restrict__ perm, const TileDesc &d,
+                                             uint2 (&p)[GPT]) {
     const int tid = threadIdx.x;
 #pragma unroll
     for (int q = 0; q < GPT; ++q) {
         const int k = tid + q * NT;
-        p[q] = (k < d.n && d.n <= TCAP) ? __ldg(perm + d.r0 + k) : NOPOS;
+        p[q] = (k < d.n && d.n <= TCAP) ? __ldg(perm + d.r0 + k) : make_uint2(NOPOS, 0u);
     }
 }
 
-// Asynchronous gather of a tile: rows and values by position into R, the
-// position itself by a plain store; the column starts into cs.
+// Gather of a tile: {row, position} by a plain store, the value by position
+// asynchronously (cp.async) into R; the column starts into cs.
 __device__ __forceinline__ void issue_gather(int4 *R, uint32_t *cs, const TileDesc &d,
-                                             const uint32_t (&p)[GPT],
-                                             const int32_t *__restrict__ ii,
+                                             const uint2 (&p)[GPT],
                                              const double *__restrict__ sv, int64_t s_stride,
                                              const uint32_t *__restrict__ sstart) {
     const int tid = threadIdx.x;
@@ -544,11 +676,8 @@ __device__ __forceinline__ void issue_gather(int4 *R, uint32_t *cs, const TileDe
         const int k = tid + q * NT;
         if (k < d.n) {
             int *r = reinterpret_cast<int *>(&R[k]);
-            r[1] = (int)p[q];
-            if (p[q] != NOPOS) {
-                cp_async4(r, ii + p[q]);
-                cp_async8(r + 2, sv + (int64_t)p[q] * s_stride);
-            }
+            *reinterpret_cast<int2 *>(r) = make_int2((int)p[q].y, (int)p[q].x);
+            if (p[q].x != NOPOS) cp_async8(r + 2, sv + (int64_t)p[q].x * s_stride);
         }
     }
     const int ncols = d.c_b - d.c_a;
@@ -565,14 +694,13 @@ __device__ __forceinline__ void issue_gather(int4 *R, uint32_t *cs, const TileDe
 // t+G is in flight into the other buffer and the positions of tile t+2G are
 // loading into registers.
 template <int NBUF>
-__global__ void __launch_bounds__(NT) k_tile_fold(const uint32_t *__restrict__ sstart,
+__global__ void __launch_bounds__(NT, 4) k_tile_fold(const uint32_t *__restrict__ sstart,
                                                      const int2 *__restrict__ tile_info,
                                                      const uint8_t *__restrict__ tile_big,
                                                      int64_t ntiles,
-                                                     const uint32_t *__restrict__ perm,
-                                                     const int32_t *__restrict__ ii,
+                                                     const uint2 *__restrict__ perm,
                                                      const double *__restrict__ sv,
-                                                     int64_t s_stride, int32_t M,
+                                                     int64_t s_stride,
                                                      const int4 *__restrict__ rec,
                                                      const BigCol *__restrict__ big_list,
                                                      const uint32_t *__restrict__ bigk,
@@ -591,12 +719,11 @@ __global__ void __launch_bounds__(NT) k_tile_fold(const uint32_t *__restrict__ s
     // prologue: gather of the first tile, positions of the second
     TileDesc d0 = tile_desc(tile_info, b, ntiles);
     TileDesc d1 = tile_desc(tile_info, b + G, ntiles);
-    uint32_t pn[GPT];
-    load_positions(perm, d0, pn);
-    issue_gather(S.rec[0], S.scol[0], d0, pn, ii, sv, s_stride, sstart);
-    load_positions(perm, d1, pn);
-    unsigned long long badp = ~0ull;
-    bool over_m = false, over_cap = false;
+    uint2 pn[GPT];
+    load_entries(perm, d0, pn);
+    issue_gather(S.rec[0], S.scol[0], d0, pn, sv, s_stride, sstart);
+    load_entries(perm, d1, pn);
+    bool over_cap = false;
 
     for (int it = 0; b < ntiles; ++it, b += G) {
         const int buf = (NBUF == 2) ? (it & 1) : 0;
@@ -604,45 +731,20 @@ __global__ void __launch_bounds__(NT) k_tile_fold(const uint32_t *__restrict__ s
         __syncthreads();  // tile b's records are in; every use of the other buffer is done
         const TileDesc d2 = tile_desc(tile_info, b + 2 * G, ntiles);
         if (NBUF == 2 && b + G < ntiles)
-            issue_gather(S.rec[buf ^ 1], S.scol[buf ^ 1], d1, pn, ii, sv, s_stride, sstart);
-        load_positions(perm, d2, pn);
+            issue_gather(S.rec[buf ^ 1], S.scol[buf ^ 1], d1, pn, sv, s_stride, sstart);
+        load_entries(perm, d2, pn);
 
         int4 *R = S.rec[buf];
         const int c_a = d0.c_a, r0 = d0.r0, n = d0.n;
         const int ncols = d0.c_b - c_a;
         if (n > TCAP && tid == 0) atomicExch(&err->internal, 1u);
         const bool staged = n <= TCAP;
-        // row validation of the gathered records (placeholders skipped)
-        if (staged) {
-#pragma unroll
-            for (int q = 0; q < GPT; ++q) {
-                const int k = tid + q * NT;
-                if (k < n) {
-                    const int2 rp = *reinterpret_cast<const int2 *>(&R[k]);
-                    if ((uint32_t)rp.y != NOPOS) {
-                        if (rp.x < 1) badp = min(badp, (unsigned long long)(uint32_t)rp.y);
-                        over_m |= rp.x > M;
-                    }
-                }
-            }
-        }
         const uint32_t *cs = (ncols < SCAP) ? S.scol[buf] : sstart + c_a;
-        {  // thread window tid = record positions [b*TILE + tid*WIN, +WIN): its first column
-            const uint32_t key = (uint32_t)(b * TILE + tid * WIN);
-            int lo = 0, hi = ncols;
-            while (lo < hi) {
-                const int mid = (lo + hi) >> 1;
-                if ((cs[mid] & POSMASK) < key) lo = mid + 1;
-                else hi = mid;
-            }
-            S.wl[tid] = lo;
-            if (tid == 0) {
-                S.wl[NT] = ncols;
-                S.nlong = 0;
-            }
-        }
+        if (tid == 0) S.nlong = 0;
         __syncthreads();
-        const int k_lo = S.wl[tid], k_hi = S.wl[tid + 1];  // tile-relative columns
+        // thread tid owns the contiguous columns [k_lo, k_hi) of the tile
+        const int k_lo = (int)(((long long)tid * ncols) / NT);
+        const int k_hi = (int)(((long long)(tid + 1) * ncols) / NT);
 
         // ---- pass 1: each thread sorts its short columns; long ones are listed ----
         if (staged) {
@@ -693,7 +795,12 @@ __global__ void __launch_bounds__(NT) k_tile_fold(const uint32_t *__restrict__ s
             for (int e = warp; e < nl; e += NWARP) {
                 const int v = S.lcol[e];
                 const int off = v & 0xffff;
-                fold_column_warp(&R[off], v >> 16, S.ws[warp]);  // outputs at R[0..u)
+                const int c = v >> 16;
+                int u = -1;  // outputs at R[0..u)
+                if (c <= 64) u = fold_column_bitonic<2>(&R[off], c, S.ws[warp].skey);
+                else if (c <= 128) u = fold_column_bitonic<4>(&R[off], c, S.ws[warp].skey);
+                else if (c <= 256) u = fold_column_bitonic<8>(&R[off], c, S.ws[warp].skey);
+                if (u < 0) fold_column_warp(&R[off], c, S.ws[warp].g);
             }
         }
         __syncthreads();
@@ -785,21 +892,12 @@ __global__ void __launch_bounds__(NT) k_tile_fold(const uint32_t *__restrict__ s
     }
     cp_async_wait_all();
     if (over_cap) atomicExch(&err->cap_exceeded, 1u);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        badp = min(badp, __shfl_xor_sync(FULL, badp, o));
-        over_m |= __shfl_xor_sync(FULL, (unsigned)over_m, o) != 0u;
-    }
-    if (lane == 0) {
-        if (badp != ~0ull) atomicMin(&err->bad_i, badp);
-        if (over_m) err->over_m = 1;
-    }
 }
 
 cudaError_t launch_tile_fold(Launch &lc, const uint32_t *sstart, const int2 *tile_info,
-                             const uint8_t *tile_big, int64_t ntiles, const uint32_t *perm,
-                             const int32_t *ii, const double *s, int64_t s_stride, int32_t M,
-                             const int4 *rec, const BigCol *big_list, const uint32_t *bigk,
+                             const uint8_t *tile_big, int64_t ntiles, const uint2 *perm,
+                             const double *s, int64_t s_stride, const int4 *rec,
+                             const BigCol *big_list, const uint32_t *bigk,
                              unsigned long long *tile_state, int32_t N, int32_t *jc, int32_t *ir,
                              double *pr, int64_t cap, ErrState *err) {
     if (ntiles <= 0) return cudaSuccess;
@@ -826,14 +924,14 @@ cudaError_t launch_tile_fold(Launch &lc, const uint32_t *sstart, const int2 *til
     if (mode == 1) {
         const int64_t grid = std::min<int64_t>(ntiles, (int64_t)occ * lc.num_sms);
         void *args[] = {(void *)&sstart, (void *)&tile_info, (void *)&tile_big, (void *)&ntiles,
-                        (void *)&perm, (void *)&ii, (void *)&s, (void *)&s_stride, (void *)&M,
+                        (void *)&perm, (void *)&s, (void *)&s_stride,
                         (void *)&rec, (void *)&big_list, (void *)&bigk, (void *)&tile_state,
                         (void *)&N, (void *)&jc, (void *)&ir, (void *)&pr, (void *)&cap, (void *)&err};
         e = cudaLaunchCooperativeKernel((const void *)k_tile_fold<2>, dim3((unsigned)grid), dim3(NT),
                                         args, sizeof(TileSmem<2>), lc.stream);
     } else {
         k_tile_fold<1><<<(unsigned)ntiles, NT, sizeof(TileSmem<1>), lc.stream>>>(
-            sstart, tile_info, tile_big, ntiles, perm, ii, s, s_stride, M, rec, big_list, bigk,
+            sstart, tile_info, tile_big, ntiles, perm, s, s_stride, rec, big_list, bigk,
             tile_state, N, jc, ir, pr, cap, err);
         e = cudaGetLastError();
     }
