@@ -298,7 +298,7 @@ def main():
         "k_init": 4 * (N + 1),
         "k_colcount": 4 * L,
         "k_col_scan": 8 * N,
-        "k_scatter": 32 * L,
+        "k_scatter": 16 * L,
         "k_bigcol": 0,
         "k_tile_fold": 16 * L + 8 * N + 12 * nnz + 4 * (N + 1),
     }
