@@ -26,7 +26,7 @@ struct sa_ctx {
     // device workspace (grown on demand, reused across calls)
     uint32_t *cur = nullptr;              size_t cur_cap = 0;     // N (counts, then cursors)
     uint32_t *sstart = nullptr;           size_t st_cap = 0;      // N+1 small-space starts
-    uint2 *perm = nullptr;                size_t perm_cap = 0;    // L + placeholders: {position, row} by column
+    uint2 *perm = nullptr;                size_t perm_cap = 0;    // L + placeholders (+2): {row, position} by column
     int4 *rec = nullptr;                  size_t rec_cap = 0;     // big-column scratch (16 B per slot)
     int2 *tile_info = nullptr;            size_t ti_cap = 0;      // ntiles+1
     uint8_t *tile_big = nullptr;          size_t tb_cap = 0;      // ntiles
@@ -385,7 +385,7 @@ int sa_assemble_async(sa_ctx *ctx, const int32_t *d_ii, const int32_t *d_jj, con
     const int64_t nscan = (N + SCAN_TILE - 1) / SCAN_TILE;
     SA_CUDA(ctx, ensure(ctx->cur, ctx->cur_cap, (size_t)N + 4));
     SA_CUDA(ctx, ensure(ctx->sstart, ctx->st_cap, (size_t)N + 1));
-    SA_CUDA(ctx, ensure(ctx->perm, ctx->perm_cap, (size_t)(L + nbig_max)));
+    SA_CUDA(ctx, ensure(ctx->perm, ctx->perm_cap, (size_t)(L + nbig_max + 2)));  // TMA over-read
     SA_CUDA(ctx, ensure(ctx->rec, ctx->rec_cap, (size_t)(L + nbig_max)));
     SA_CUDA(ctx, ensure(ctx->tile_info, ctx->ti_cap, (size_t)ntiles + 1));
     SA_CUDA(ctx, ensure(ctx->tile_big, ctx->tb_cap, (size_t)ntiles));
@@ -417,8 +417,8 @@ int sa_assemble_async(sa_ctx *ctx, const int32_t *d_ii, const int32_t *d_jj, con
                                    passes));
     }
     if ((rc = mark(ctx, "k_tile_fold"))) return rc;
-    SA_CUDA(ctx, launch_tile_fold(lc, ctx->sstart, ctx->tile_info, ctx->tile_big, ntiles, ctx->perm,
-                                  d_s, s_stride, ctx->rec,
+    SA_CUDA(ctx, launch_tile_fold(lc, ctx->sstart, ctx->tile_info, ctx->tile_big, ntiles,
+                                  reinterpret_cast<const int2 *>(ctx->perm), d_s, s_stride, ctx->rec,
                                   ctx->big_list, ctx->bigk, ctx->tile_state, N, d_jc, d_ir, d_pr,
                                   cap, ctx->err));
     if ((rc = mark(ctx, nullptr))) return rc;

@@ -288,10 +288,10 @@ cudaError_t launch_bigcol(Launch &lc, BigCol *big_list, const ErrState *err, int
                           const uint2 *perm, const double *s, int64_t s_stride, int idx_bits,
                           int passes);
 cudaError_t launch_tile_fold(Launch &lc, const uint32_t *sstart, const int2 *tile_info,
-                             const uint8_t *tile_big, int64_t ntiles, const uint2 *perm,
+                             const uint8_t *tile_big, int64_t ntiles, const int2 *entries,
                              const double *s, int64_t s_stride, const int4 *rec,
                              const BigCol *big_list, const uint32_t *bigk,
-                             unsigned long long *tile_state, int32_t N, int32_t *jc,
-                             int32_t *ir, double *pr, int64_t cap, ErrState *err);
+                             unsigned long long *tile_state, int32_t N, int32_t *jc, int32_t *ir,
+                             double *pr, int64_t cap, ErrState *err);
 
 }  // namespace sa

@@ -281,7 +281,7 @@ __global__ void __launch_bounds__(SCAN_NT) k_col_scan(const uint32_t *cnt,
                 const unsigned slot = atomicAdd(&err->nbig, 1u);
                 big_list[slot] = BigCol{(uint32_t)c, (uint32_t)bigp, n, 0u};
                 bigk[c] = slot;
-                perm[small] = make_uint2(0xffffffffu, 0u);  // placeholder slot: nothing to gather
+                perm[small] = make_uint2(0u, 0xffffffffu);  // placeholder slot: nothing to gather
                 int64_t tb = (int64_t)(small / TILE);
                 if (tb > ntiles - 1) tb = ntiles - 1;
                 tile_big[tb] = 1;
@@ -563,8 +563,8 @@ cudaError_t launch_colcount(Launch &lc, const int32_t *jj, int64_t L, int32_t N,
 }
 
 // ---------------------------------------------------------------------------
-// k_scatter: counting-sort scatter by column of 8-byte entries {input
-// position, row} (the fold gathers the values by position, so the 8-byte
+// k_scatter: counting-sort scatter by column of 8-byte entries {row,
+// input position} (the fold gathers the values by position, so the 8-byte
 // values are read once, by the fold).  Per chunk: (1) each column run gets
 // chunk-local slots from a shared-memory counter, (2) one global atomicAdd
 // per distinct column reserves the chunk's slots on the column cursor, (3)
@@ -645,7 +645,7 @@ __global__ void __launch_bounds__(AGG_NT) k_scatter(const int32_t *__restrict__ 
             if (hk[k] < 0) continue;
             const uint32_t bw = (uint32_t)A.ctr[hk[k]];
             const uint32_t pos = (bw & POSMASK) + ((bw & BIGFLAG) ? lsmall : 0u) + (uint32_t)rk[k];
-            perm[pos] = make_uint2((uint32_t)(t0 + k), (uint32_t)i[k]);
+            perm[pos] = make_uint2((uint32_t)i[k], (uint32_t)(t0 + k));
         }
         __syncthreads();
         for (int e = tid; e < nu; e += AGG_NT) {
@@ -707,7 +707,7 @@ __global__ void __launch_bounds__(AGG_NT) k_scatter_direct(const int32_t *__rest
             if (!vk[k]) continue;
             if (run_head(j, vk, k)) slot = (w[k] & POSMASK) + ((w[k] & BIGFLAG) ? lsmall : 0u);
             else slot += 1;
-            perm[slot] = make_uint2((uint32_t)(t0 + k), (uint32_t)i[k]);
+            perm[slot] = make_uint2((uint32_t)i[k], (uint32_t)(t0 + k));
         }
     }
 #pragma unroll
@@ -740,7 +740,7 @@ cudaError_t launch_scatter(Launch &lc, const int32_t *ii, const int32_t *jj, int
 
 // ---------------------------------------------------------------------------
 // k_bigcol: one CTA per big column (grid-stride over the device-side list).
-// The column's entries {position, row} (big space) become keys
+// The column's entries {row, position} (big space) become keys
 // key = (row-1) << idx_bits | input position in two 8-byte buffers A|B
 // (the column's 16-byte slots of the big scratch).  Stable LSD radix
 // passes (8-bit digits, warp match + per-warp digit counts) sort by (row,
@@ -772,10 +772,10 @@ __global__ void __launch_bounds__(BIG_NT) k_bigcol(BigCol *__restrict__ big_list
         const int64_t n = big_list[kb].n;
         unsigned long long *A = reinterpret_cast<unsigned long long *>(rec + st);
         unsigned long long *B = A + n;
-        // entries {position, row} -> keys in A
+        // entries {row, position} -> keys in A
         for (int64_t p = tid; p < n; p += BIG_NT) {
             const uint2 e = perm[st + p];
-            A[p] = ((unsigned long long)(e.y - 1u) << idx_bits) | e.x;
+            A[p] = ((unsigned long long)(e.x - 1u) << idx_bits) | e.y;
         }
         __syncthreads();
         unsigned long long *src = A, *dst = B;
