@@ -24,10 +24,10 @@ constexpr int SCAN_TILE = SCAN_NT * SCAN_IPT;
 // start lies in [b*TILE, (b+1)*TILE); inside the CTA, thread t owns the
 // columns starting in its WIN-wide sub-window.  A tile holds at most
 // TILE + BIGCOL - 1 small records.
-constexpr int TILE = 2048;
+constexpr int TILE = 1792;
 constexpr int TILE_THREADS = 128;
 constexpr int WIN = TILE / TILE_THREADS;  // 16 record positions per thread
-constexpr int BIGCOL = 384;
+constexpr int BIGCOL = 256;
 constexpr int TCAP = TILE + BIGCOL;
 
 // One big column (k_col_scan appends, k_bigcol folds, k_tile_fold copies out).

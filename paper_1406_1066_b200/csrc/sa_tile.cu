@@ -43,8 +43,10 @@ struct TileSmem {
     int2 kbuf[TCAP + 2];               // TMA destination (16-byte aligned start)
     double val[TCAP];                  // gathered values
     uint8_t perm[TCAP];                // per short column: sorted order, then output slots
-    uint16_t omap[TCAP];               // tile-local output index -> slot
-    unsigned long long skey[NWARP][LONGCAP];  // long columns: sorted keys
+    union {
+        unsigned long long skey[NWARP][LONGCAP];  // pass 2: long columns' sorted keys
+        uint16_t omap[TCAP];                       // pass 3+: tile-local output index -> slot
+    };
     int lcol[LCAP];                    // long columns: offset | (count << 16)
     uint32_t scol[SCAP];               // sstart of the tile's columns (when they fit)
     unsigned long long mbar;
@@ -468,7 +470,7 @@ __device__ long long lookback_warp32(unsigned long long *st, long long b, unsign
 
 }  // namespace
 
-__global__ void __launch_bounds__(NT, 4) k_tile_fold(const uint32_t *__restrict__ sstart,
+__global__ void __launch_bounds__(NT, 5) k_tile_fold(const uint32_t *__restrict__ sstart,
                                                      const int2 *__restrict__ tile_info,
                                                      const uint8_t *__restrict__ tile_big,
                                                      int64_t ntiles,
