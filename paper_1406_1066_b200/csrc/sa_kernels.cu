@@ -527,22 +527,108 @@ __global__ void __launch_bounds__(AGG_NT) k_colcount_direct(const int32_t *__res
     }
 }
 
-// Experiment switches (measured on cfg2/cfg3/cfg4): the
-// column histogram defaults to direct reductions, the scatter to CTA-scope
-// aggregation.  SA_COLCOUNT_AGG=1 / SA_SCATTER_DIRECT=1 flip them.
-static bool env_flag(const char *name) {
+// ---------------------------------------------------------------------------
+// Window aggregation (k_colcount_win, k_scatter_win).  A CTA takes CHUNK
+// consecutive triplets; element-ordered input keeps a chunk's columns near
+// the chunk's first column, so the column runs (per thread) count into a
+// directly indexed shared-memory window of WB bins around it (one shared
+// atomic per run, no hashing).  The first touch of a bin lists it; after
+// the chunk, every listed bin issues one global atomic.  Columns outside
+// the window go to global memory directly.
+// ---------------------------------------------------------------------------
+constexpr int WB = 8192;
+
+struct WinSmem {
+    uint32_t bin[WB];      // per window column: triplets of the chunk, then the cursor word
+    int used[CHUNK];       // listed bins
+    int nused;
+};
+
+__device__ __forceinline__ int window_base(const int32_t *__restrict__ jj, int64_t t) {
+    return __ldg(jj + t) - 1 - WB / 2;
+}
+
+__global__ void __launch_bounds__(AGG_NT) k_colcount_win(const int32_t *__restrict__ jj, int64_t L,
+                                                         int32_t N, uint32_t *__restrict__ cnt,
+                                                         ErrState *err, int vec) {
+    __shared__ WinSmem W;
+    const int tid = threadIdx.x;
+    for (int k = tid; k < WB; k += AGG_NT) W.bin[k] = 0;
+    if (tid == 0) W.nused = 0;
+    __syncthreads();
+    unsigned long long bad = ~0ull;
+    unsigned over = 0;
+    const int64_t nchunk = (L + CHUNK - 1) / CHUNK;
+    int jn[CPT];
+    if ((int64_t)blockIdx.x < nchunk)
+        load_run(jj, (int64_t)blockIdx.x * CHUNK + (int64_t)tid * CPT, L, vec, jn, 0x7fffffff);
+    for (int64_t ch = blockIdx.x; ch < nchunk; ch += gridDim.x) {
+        const int64_t t0 = ch * CHUNK + (int64_t)tid * CPT;
+        const int cb = window_base(jj, ch * CHUNK);
+        int j[CPT];
+#pragma unroll
+        for (int k = 0; k < CPT; ++k) j[k] = jn[k];
+        if (ch + gridDim.x < nchunk)  // prefetch the next chunk while this one is counted
+            load_run(jj, (ch + gridDim.x) * CHUNK + (int64_t)tid * CPT, L, vec, jn, 0x7fffffff);
+        bool vk[CPT];
+        int len[CPT];
+#pragma unroll
+        for (int k = 0; k < CPT; ++k) {
+            const bool live = t0 + k < L;
+            if (live && j[k] < 1) bad = min(bad, (unsigned long long)(t0 + k));
+            if (live && j[k] > N) over = 1;
+            vk[k] = live && j[k] >= 1 && j[k] <= N;
+        }
+        run_lengths(j, vk, len);
+#pragma unroll
+        for (int k = 0; k < CPT; ++k) {
+            if (vk[k] && run_head(j, vk, k)) {
+                const unsigned b = (unsigned)(j[k] - 1 - cb);
+                if (b < (unsigned)WB) {
+                    if (atomicAdd(&W.bin[b], (uint32_t)len[k]) == 0u) W.used[atomicAdd(&W.nused, 1)] = (int)b;
+                } else {
+                    atomicAdd(&cnt[j[k] - 1], (uint32_t)len[k]);
+                }
+            }
+        }
+        __syncthreads();
+        const int nu = W.nused;
+        for (int e = tid; e < nu; e += AGG_NT) {
+            const int b = W.used[e];
+            atomicAdd(&cnt[cb + b], W.bin[b]);
+            W.bin[b] = 0;
+        }
+        __syncthreads();
+        if (tid == 0) W.nused = 0;
+        __syncthreads();
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        bad = min(bad, __shfl_xor_sync(FULL, bad, o));
+        over |= __shfl_xor_sync(FULL, over, o);
+    }
+    if ((tid & 31) == 0) {
+        if (bad != ~0ull) atomicMin(&err->bad_j, bad);
+        if (over) err->over_n = 1;
+    }
+}
+
+// Aggregation variants (measured on cfg2/cfg3/cfg4), chosen
+// by SA_COLCOUNT_MODE / SA_SCATTER_MODE = 0 direct, 1 hash, 2 window.
+static int env_mode(const char *name, int dflt) {
     const char *e = getenv(name);
-    return e && e[0] == '1';
+    return (e && e[0] >= '0' && e[0] <= '2') ? e[0] - '0' : dflt;
 }
-static bool colcount_agg() {
+// 0 direct, 1 shared-memory hash, 2 shared-memory window
+static int colcount_mode() {
     static int m = -1;
-    if (m < 0) m = env_flag("SA_COLCOUNT_AGG") ? 1 : 0;
-    return m == 1;
+    if (m < 0) m = env_mode("SA_COLCOUNT_MODE", 2);
+    return m;
 }
-static bool scatter_agg() {
+static int scatter_mode() {
     static int m = -1;
-    if (m < 0) m = env_flag("SA_SCATTER_DIRECT") ? 0 : 1;
-    return m == 1;
+    if (m < 0) m = env_mode("SA_SCATTER_MODE", 1);
+    return m;
 }
 
 cudaError_t launch_colcount(Launch &lc, const int32_t *jj, int64_t L, int32_t N, uint32_t *cnt,
@@ -551,8 +637,10 @@ cudaError_t launch_colcount(Launch &lc, const int32_t *jj, int64_t L, int32_t N,
     const int vec = aligned16(jj);
     const int64_t nchunk = (L + CHUNK - 1) / CHUNK;
     int grid = (int)std::min<int64_t>(nchunk, (int64_t)lc.num_sms * 4);
-    if (colcount_agg()) {
+    if (colcount_mode() == 1) {
         k_colcount<<<grid, AGG_NT, 0, lc.stream>>>(jj, L, N, cnt, err, vec);
+    } else if (colcount_mode() == 2) {
+        k_colcount_win<<<grid, AGG_NT, 0, lc.stream>>>(jj, L, N, cnt, err, vec);
     } else {
         const int64_t want = ((L + CPT - 1) / CPT + AGG_NT - 1) / AGG_NT;
         const int g = (int)std::min<int64_t>(want, (int64_t)lc.num_sms * 8);
@@ -721,14 +809,113 @@ __global__ void __launch_bounds__(AGG_NT) k_scatter_direct(const int32_t *__rest
     }
 }
 
+__global__ void __launch_bounds__(AGG_NT) k_scatter_win(const int32_t *__restrict__ ii,
+                                                        const int32_t *__restrict__ jj, int64_t L,
+                                                        int32_t M, int32_t N,
+                                                        uint32_t *__restrict__ cur,
+                                                        uint2 *__restrict__ perm, int vec,
+                                                        ErrState *err) {
+    __shared__ WinSmem W;
+    const int tid = threadIdx.x;
+    for (int k = tid; k < WB; k += AGG_NT) W.bin[k] = 0;
+    if (tid == 0) W.nused = 0;
+    __syncthreads();
+    const uint32_t lsmall = err->lsmall;
+    unsigned long long bad = ~0ull;
+    unsigned over = 0;
+    const int64_t nchunk = (L + CHUNK - 1) / CHUNK;
+    int in_[CPT], jn[CPT];
+    if ((int64_t)blockIdx.x < nchunk) {
+        const int64_t t0 = (int64_t)blockIdx.x * CHUNK + (int64_t)tid * CPT;
+        load_run(ii, t0, L, vec, in_, 1);
+        load_run(jj, t0, L, vec, jn, 0);
+    }
+    for (int64_t ch = blockIdx.x; ch < nchunk; ch += gridDim.x) {
+        const int64_t t0 = ch * CHUNK + (int64_t)tid * CPT;
+        const int cb = window_base(jj, ch * CHUNK);
+        int i[CPT], j[CPT];
+#pragma unroll
+        for (int k = 0; k < CPT; ++k) {
+            i[k] = in_[k];
+            j[k] = jn[k];
+        }
+        if (ch + gridDim.x < nchunk) {  // next chunk in flight
+            const int64_t t1 = (ch + gridDim.x) * CHUNK + (int64_t)tid * CPT;
+            load_run(ii, t1, L, vec, in_, 1);
+            load_run(jj, t1, L, vec, jn, 0);
+        }
+        bool vk[CPT];
+        int len[CPT];
+        uint32_t rk[CPT];
+#pragma unroll
+        for (int k = 0; k < CPT; ++k) {
+            const bool live = t0 + k < L;
+            if (live && i[k] < 1) bad = min(bad, (unsigned long long)(t0 + k));
+            if (live && i[k] > M) over = 1;
+            vk[k] = live && j[k] >= 1 && j[k] <= N;
+        }
+        run_lengths(j, vk, len);
+        // heads: rank inside the window bin, or (outside the window) the
+        // global cursor word itself
+#pragma unroll
+        for (int k = 0; k < CPT; ++k) {
+            rk[k] = 0;
+            if (vk[k] && run_head(j, vk, k)) {
+                const unsigned b = (unsigned)(j[k] - 1 - cb);
+                if (b < (unsigned)WB) {
+                    rk[k] = atomicAdd(&W.bin[b], (uint32_t)len[k]);
+                    if (rk[k] == 0u) W.used[atomicAdd(&W.nused, 1)] = (int)b;
+                } else {
+                    rk[k] = atomicAdd(&cur[j[k] - 1], (uint32_t)len[k]);
+                }
+            }
+        }
+        __syncthreads();
+        const int nu = W.nused;
+        for (int e = tid; e < nu; e += AGG_NT) {
+            const int b = W.used[e];
+            W.bin[b] = atomicAdd(&cur[cb + b], W.bin[b]);
+        }
+        __syncthreads();
+        uint32_t slot = 0;
+#pragma unroll
+        for (int k = 0; k < CPT; ++k) {
+            if (!vk[k]) continue;
+            if (run_head(j, vk, k)) {
+                const unsigned b = (unsigned)(j[k] - 1 - cb);
+                const uint32_t w = (b < (unsigned)WB) ? W.bin[b] + rk[k] : rk[k];
+                slot = (w & POSMASK) + ((w & BIGFLAG) ? lsmall : 0u);
+            } else {
+                slot += 1;
+            }
+            perm[slot] = make_uint2((uint32_t)i[k], (uint32_t)(t0 + k));
+        }
+        __syncthreads();
+        for (int e = tid; e < nu; e += AGG_NT) W.bin[W.used[e]] = 0;
+        if (tid == 0) W.nused = 0;
+        __syncthreads();
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        bad = min(bad, __shfl_xor_sync(FULL, bad, o));
+        over |= __shfl_xor_sync(FULL, over, o);
+    }
+    if ((tid & 31) == 0) {
+        if (bad != ~0ull) atomicMin(&err->bad_i, bad);
+        if (over) err->over_m = 1;
+    }
+}
+
 cudaError_t launch_scatter(Launch &lc, const int32_t *ii, const int32_t *jj, int64_t L, int32_t M,
                            int32_t N, uint32_t *cur, uint2 *perm, ErrState *err) {
     if (L <= 0) return cudaSuccess;
     const int vec = aligned16(ii) && aligned16(jj);
     const int64_t nchunk = (L + CHUNK - 1) / CHUNK;
     int grid = (int)std::min<int64_t>(nchunk, (int64_t)lc.num_sms * 4);
-    if (scatter_agg()) {
+    if (scatter_mode() == 1) {
         k_scatter<<<grid, AGG_NT, 0, lc.stream>>>(ii, jj, L, M, N, cur, perm, vec, err);
+    } else if (scatter_mode() == 2) {
+        k_scatter_win<<<grid, AGG_NT, 0, lc.stream>>>(ii, jj, L, M, N, cur, perm, vec, err);
     } else {
         const int64_t want = ((L + CPT - 1) / CPT + AGG_NT - 1) / AGG_NT;
         const int g = (int)std::min<int64_t>(want, (int64_t)lc.num_sms * 8);
