@@ -445,12 +445,14 @@ __device__ long long lookback_warp32(unsigned long long *st, long long b, unsign
     if (b == 0) return 0;
     unsigned long long excl = 0;
     long long base = b - 1;
+    unsigned ns = 32;  // exponential back-off: a waiting warp leaves the issue slots to others
     while (base >= 0) {
         const long long idx = base - lane;
         const unsigned long long w = (idx >= 0) ? vst[(idx) * LB_STRIDE] : lb_pack(2, 0);
         const unsigned flag = (unsigned)(w >> 62);
         if (__any_sync(FULL, flag == 0)) {
-            __nanosleep(64);
+            __nanosleep(ns);
+            ns = min(ns * 2, 1024u);
             continue;
         }
         const unsigned pm = __ballot_sync(FULL, flag == 2);
