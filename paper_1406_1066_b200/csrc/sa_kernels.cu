@@ -367,18 +367,34 @@ struct AggSmem {
     int nused;
 };
 
+// Append `item` to a shared list when `take`; the lanes of the calling
+// (possibly partial) warp share one atomic on the list counter.
+__device__ __forceinline__ void list_push(int *list, int *count, bool take, int item) {
+    const unsigned act = __activemask();
+    const unsigned m = __ballot_sync(act, take);
+    if (m == 0u) return;
+    const int leader = __ffs(m) - 1;
+    int base = 0;
+    if ((int)(threadIdx.x & 31) == leader) base = atomicAdd(count, __popc(m));
+    base = __shfl_sync(act, base, leader);
+    if (take) list[base + __popc(m & lanemask_lt())] = item;
+}
+
 __device__ __forceinline__ int agg_insert(AggSmem &A, int col) {
     const int key = col + 1;
     unsigned h = ((unsigned)key * 0x9E3779B1u) >> (32 - 12);  // HT = 4096
+    bool fresh = false;
     while (true) {
         const int old = atomicCAS(&A.key[h], 0, key);
         if (old == 0) {
-            A.used[atomicAdd(&A.nused, 1)] = (int)h;
-            return (int)h;
+            fresh = true;
+            break;
         }
-        if (old == key) return (int)h;
+        if (old == key) break;
         h = (h + 1) & (HT - 1);
     }
+    list_push(A.used, &A.nused, fresh, (int)h);
+    return (int)h;
 }
 
 // load CPT consecutive int32 (vector path when aligned and complete)
