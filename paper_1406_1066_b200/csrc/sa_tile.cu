@@ -29,6 +29,19 @@
 
 namespace sa {
 
+#ifdef SA_TRACE
+// per-tile timeline (tools/fold_trace.py): 8 stamps per tile, globaltimer ns
+__device__ unsigned long long g_ftrace[1 << 15][8];
+#define FTRACE(b, k)                                                                   \
+    if (threadIdx.x == 0 && (b) < (1 << 15)) {                                         \
+        unsigned long long t_;                                                         \
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                        \
+        g_ftrace[b][k] = t_;                                                           \
+    }
+#else
+#define FTRACE(b, k)
+#endif
+
 namespace {
 
 constexpr int NT = TILE_THREADS;
@@ -491,6 +504,7 @@ __global__ void __launch_bounds__(NT, 5) k_tile_fold(const uint32_t *__restrict_
     TileSmem &S = *reinterpret_cast<TileSmem *>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const long long b = blockIdx.x;
+    FTRACE(b, 0);
     const int2 ti0 = tile_info[b], ti1 = tile_info[b + 1];
     const int c_a = ti0.x, r0 = ti0.y;
     int n = ti1.y - r0;
@@ -516,6 +530,7 @@ __global__ void __launch_bounds__(NT, 5) k_tile_fold(const uint32_t *__restrict_
     int2 *K = S.kbuf + shift;
     double *V = S.val;
     if (n > 0) mbar_wait(&S.mbar, 0u);
+    FTRACE(b, 1);
     for (int k = tid; k < n; k += NT) {
         const uint32_t pos = (uint32_t)K[k].y;
         if (pos != NOPOS) cp_async8(&V[k], sv + (int64_t)pos * s_stride);
@@ -568,8 +583,10 @@ __global__ void __launch_bounds__(NT, 5) k_tile_fold(const uint32_t *__restrict_
             if (cnt) K[off].y = u;  // input positions of a sorted column are no longer needed
         }
     }
+    FTRACE(b, 2);
     cp_async_wait_all();
     __syncthreads();  // values in; long-column list complete
+    FTRACE(b, 3);
     // ---- pass 2: warps sort and fold the long columns -------------------------
     {
         const int nl = min(S.nlong, LCAP);
@@ -609,6 +626,7 @@ __global__ void __launch_bounds__(NT, 5) k_tile_fold(const uint32_t *__restrict_
     }
     const int tbase = wpre + inc - ut;  // this thread's first output, tile-local
     if (tid == 0) lookback_publish(tile_state, b, (unsigned long long)U);
+    FTRACE(b, 4);
 
     // ---- pass 3: fold the short columns' values; output map -------------------
     {
@@ -631,12 +649,14 @@ __global__ void __launch_bounds__(NT, 5) k_tile_fold(const uint32_t *__restrict_
             o += u;
         }
     }
+    FTRACE(b, 5);
     if (warp == 0) {
         const long long P = lookback_warp32(tile_state, b, (unsigned long long)U);
         if (lane == 0) S.P = P;
     }
     __syncthreads();
     const long long P = S.P;
+    FTRACE(b, 6);
 
     // ---- column pointers and, in tiles with a big column, all outputs per thread
     bool over = false;
@@ -693,6 +713,7 @@ __global__ void __launch_bounds__(NT, 5) k_tile_fold(const uint32_t *__restrict_
         }
     }
     if (over) atomicExch(&err->cap_exceeded, 1u);
+    FTRACE(b, 7);
     if (b == ntiles - 1 && tid == 0) {
         jc[N] = (int32_t)(P + U);
         err->nnz = P + U;
@@ -723,3 +744,9 @@ cudaError_t launch_tile_fold(Launch &lc, const uint32_t *sstart, const int2 *til
 }
 
 }  // namespace sa
+
+#ifdef SA_TRACE
+extern "C" int sa_debug_ftrace(void *host, int n) {
+    return (int)cudaMemcpyFromSymbol(host, sa::g_ftrace, (size_t)n * 64);
+}
+#endif
