@@ -60,10 +60,11 @@ struct TileSmem {
         unsigned long long skey[NWARP][LONGCAP];  // pass 2: long columns' sorted keys
         uint16_t omap[TCAP];                       // pass 3+: tile-local output index -> slot
     };
-    int lcol[LCAP];                    // long columns: offset | (count << 16)
+    int lcol[4][LCAP];                 // long columns by class (<=64, <=128, <=256, fallback):
+                                       // offset | (count << 16)
+    int ncls[4];
     uint32_t scol[SCAP];               // sstart of the tile's columns (when they fit)
     unsigned long long mbar;
-    int nlong;
     int warp_u[NWARP];
     long long P;
 };
@@ -311,13 +312,13 @@ __device__ __forceinline__ int warp_incl_sum(int x) {
     return x;
 }
 
-// Warp-wide bitonic sort of 32*E 64-bit keys, blocked layout (lane holds
-// elements lane*E .. lane*E+E-1): partner distances >= E are shuffles,
-// shorter ones are register compare-exchanges.
-template <int E>
-__device__ __forceinline__ void warp_bitonic(unsigned long long (&k)[E]) {
-    const int lane = threadIdx.x & 31;
-    constexpr int P = 32 * E;
+// Bitonic sort of G*E 64-bit keys held by a group of G lanes (E per lane,
+// blocked layout); 32/G groups of one warp sort independent sequences at
+// once, so the shuffle latency of one is hidden behind the others.
+template <int G, int E>
+__device__ __forceinline__ void group_bitonic(unsigned long long (&k)[E]) {
+    const int li = threadIdx.x & (G - 1);
+    constexpr int P = G * E;
 #pragma unroll
     for (int size = 2; size <= P; size <<= 1) {
 #pragma unroll
@@ -325,7 +326,7 @@ __device__ __forceinline__ void warp_bitonic(unsigned long long (&k)[E]) {
             if (stride >= E) {
 #pragma unroll
                 for (int e = 0; e < E; ++e) {
-                    const int i = lane * E + e;
+                    const int i = li * E + e;
                     const unsigned long long o = __shfl_xor_sync(FULL, k[e], stride / E);
                     const bool up = (i & size) == 0;
                     const bool lower = (i & stride) == 0;
@@ -337,7 +338,7 @@ __device__ __forceinline__ void warp_bitonic(unsigned long long (&k)[E]) {
                 for (int e = 0; e < E; ++e) {
                     const int q = e ^ stride;
                     if (q > e) {
-                        const bool up = ((lane * E + e) & size) == 0;
+                        const bool up = ((li * E + e) & size) == 0;
                         const unsigned long long a = k[e], b = k[q];
                         const bool sw = up ? (b < a) : (a < b);
                         k[e] = sw ? b : a;
@@ -349,22 +350,32 @@ __device__ __forceinline__ void warp_bitonic(unsigned long long (&k)[E]) {
     }
 }
 
-// Warp-cooperative fold of one column of c (<= 32*E) records: one bitonic
-// sort of the packed key (row - rmin) << (PB+SB) | (pos - pmin) << SB | slot
-// puts the records in (row, input position) order; the lane holding a run
-// head folds the run of equal rows from +0.0 in that order (the reference's
-// order, _kernels.pyx:82-89).  Outputs (row-1, u) in K[0..u), values in V[0..u).
-// Returns u, or -1 (nothing written) when the spans do not fit 64 bits.
-template <int E>
-__device__ int fold_column_bitonic(int2 *K, double *V, int c, unsigned long long *skey) {
-    constexpr int SB = (E == 1) ? 5 : (E == 2) ? 6 : (E == 4) ? 7 : (E == 8) ? 8 : 9;
-    const int lane = threadIdx.x & 31;
+// Up to 32/G long columns (list entries: offset | count << 16, count <=
+// G*E) folded at once by one warp, G lanes per column: one group bitonic
+// sort of the packed key (row - rmin) << (PB+SB) | (pos - pmin) << SB | slot,
+// then the lane holding a run head folds the run of equal rows from +0.0 in
+// input-position order (the reference's order, _kernels.pyx:82-89).
+// Outputs (row-1, u) in K[off..off+u), values in V[off..off+u).  A column
+// whose spans do not fit 64 bits is appended to `fb` instead.
+template <int G, int E>
+__device__ void fold_columns_group(int2 *K, double *V, const int *list, int count,
+                                   unsigned long long *skey, int *fb, int *nfb) {
+    constexpr int P = G * E;
+    constexpr int SB = (P <= 32) ? 5 : (P <= 64) ? 6 : (P <= 128) ? 7 : 8;
+    constexpr unsigned SMASK = (1u << SB) - 1;
+    const int lane = threadIdx.x & 31, g = lane / G, li = lane & (G - 1);
+    const bool has = g < count;
+    const int ent = has ? list[g] : 0;
+    const int off = ent & 0xffff, c = has ? (ent >> 16) : 0;
+    int2 *Kc = K + off;
+    double *Vc = V + off;
+    unsigned long long *sk = skey + g * P;
     int2 rp[E];
     unsigned rmin = 0xffffffffu, rmax = 0u, pmin = 0xffffffffu, pmax = 0u;
 #pragma unroll
     for (int e = 0; e < E; ++e) {
-        const int i = lane * E + e;
-        rp[e] = (i < c) ? K[i] : make_int2(0, 0);
+        const int i = li * E + e;
+        rp[e] = (i < c) ? Kc[i] : make_int2(0, 0);
         if (i < c) {
             rmin = min(rmin, (unsigned)rp[e].x);
             rmax = max(rmax, (unsigned)rp[e].x);
@@ -373,59 +384,63 @@ __device__ int fold_column_bitonic(int2 *K, double *V, int c, unsigned long long
         }
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
+    for (int o = G / 2; o > 0; o >>= 1) {
         rmin = min(rmin, __shfl_xor_sync(FULL, rmin, o));
         rmax = max(rmax, __shfl_xor_sync(FULL, rmax, o));
         pmin = min(pmin, __shfl_xor_sync(FULL, pmin, o));
         pmax = max(pmax, __shfl_xor_sync(FULL, pmax, o));
     }
     const int pb = span_bits(pmax - pmin), rb = span_bits(rmax - rmin);
-    if (rb + pb + SB > 63) return -1;
+    const bool fits = rb + pb + SB <= 63;
+    if (has && !fits && li == 0) {
+        const int e = atomicAdd(nfb, 1);
+        if (e < LCAP) fb[e] = ent;
+    }
+    const bool act = has && fits;
     const int rs = pb + SB;
     unsigned long long k[E];
 #pragma unroll
     for (int e = 0; e < E; ++e) {
-        const int i = lane * E + e;
-        k[e] = (i < c) ? ((((unsigned long long)((unsigned)rp[e].x - rmin)) << rs) |
-                          ((unsigned long long)((unsigned)rp[e].y - pmin) << SB) | (unsigned)i)
-                       : ~0ull;
+        const int i = li * E + e;
+        k[e] = (act && i < c) ? ((((unsigned long long)((unsigned)rp[e].x - rmin)) << rs) |
+                                 ((unsigned long long)((unsigned)rp[e].y - pmin) << SB) | (unsigned)i)
+                              : ~0ull;
     }
-    warp_bitonic<E>(k);
+    group_bitonic<G, E>(k);
 #pragma unroll
     for (int e = 0; e < E; ++e)
-        if (lane * E + e < c) skey[lane * E + e] = k[e];
-    // run heads and their output ranks
-    const unsigned long long prev_last = __shfl_up_sync(FULL, k[E - 1], 1);
+        if (act && li * E + e < c) sk[li * E + e] = k[e];
+    // run heads and their output ranks inside the group
+    const unsigned long long prev_last = __shfl_up_sync(FULL, k[E - 1], 1, G);
     unsigned hmask = 0;
 #pragma unroll
     for (int e = 0; e < E; ++e) {
-        const int i = lane * E + e;
+        const int i = li * E + e;
         const unsigned long long pk = (e > 0) ? k[e > 0 ? e - 1 : 0] : prev_last;
-        if (i < c && (i == 0 || (k[e] >> rs) != (pk >> rs))) hmask |= 1u << e;
+        if (act && i < c && (i == 0 || (k[e] >> rs) != (pk >> rs))) hmask |= 1u << e;
     }
     const int hc = __popc(hmask);
     int incl = hc;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(FULL, incl, o);
-        if (lane >= o) incl += y;
+    for (int o = 1; o < G; o <<= 1) {
+        const int y = __shfl_up_sync(FULL, incl, o, G);
+        if (li >= o) incl += y;
     }
-    const int u = __shfl_sync(FULL, incl, 31);
+    const int u = __shfl_sync(FULL, incl, G - 1, G);
     int oidx = incl - hc;
     __syncwarp();
-    constexpr unsigned SMASK = (1u << SB) - 1;
     double acc[E];
 #pragma unroll
     for (int e = 0; e < E; ++e) {
         acc[e] = 0.0;
         if (!(hmask & (1u << e))) continue;
-        const int i = lane * E + e;
+        const int i = li * E + e;
         const unsigned long long rk = k[e] >> rs;
-        double sacc = fold_add(0.0, V[(unsigned)k[e] & SMASK]);
+        double sacc = fold_add(0.0, Vc[(unsigned)k[e] & SMASK]);
         for (int j = i + 1; j < c; ++j) {
-            const unsigned long long y = skey[j];
+            const unsigned long long y = sk[j];
             if ((y >> rs) != rk) break;
-            sacc = fold_add(sacc, V[(unsigned)y & SMASK]);
+            sacc = fold_add(sacc, Vc[(unsigned)y & SMASK]);
         }
         acc[e] = sacc;
     }
@@ -434,12 +449,11 @@ __device__ int fold_column_bitonic(int2 *K, double *V, int c, unsigned long long
     for (int e = 0; e < E; ++e) {
         if (!(hmask & (1u << e))) continue;
         const int orow = (int)(rmin + (unsigned)(k[e] >> rs));
-        K[oidx] = make_int2(orow - 1, u);
-        V[oidx] = acc[e];
+        Kc[oidx] = make_int2(orow - 1, u);
+        Vc[oidx] = acc[e];
         ++oidx;
     }
     __syncwarp();
-    return u;
 }
 
 // Publish tile b's aggregate (the inclusive prefix right away for tile 0).
@@ -516,7 +530,7 @@ __global__ void __launch_bounds__(NT, 5) k_tile_fold(const uint32_t *__restrict_
     const bool has_big = tile_big[b] != 0;  // outputs written per thread (no output map)
     const int shift = r0 & 1;  // TMA source must be 16-byte aligned
     if (tid == 0) {
-        S.nlong = 0;
+        S.ncls[0] = S.ncls[1] = S.ncls[2] = S.ncls[3] = 0;
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&S.mbar)) : "memory");
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         if (n > 0)
@@ -559,8 +573,9 @@ __global__ void __launch_bounds__(NT, 5) k_tile_fold(const uint32_t *__restrict_
                 }
             }
             if (cnt > SHORT_COL) {
-                const int e = atomicAdd(&S.nlong, 1);
-                if (e < LCAP) S.lcol[e] = off | (cnt << 16);
+                const int cls = (cnt <= 64) ? 0 : (cnt <= 128) ? 1 : (cnt <= LONGCAP) ? 2 : 3;
+                const int e = atomicAdd(&S.ncls[cls], 1);
+                if (e < LCAP) S.lcol[cls][e] = off | (cnt << 16);
                 else atomicExch(&err->internal, 1u);
                 cnt = 0;
             }
@@ -587,21 +602,28 @@ __global__ void __launch_bounds__(NT, 5) k_tile_fold(const uint32_t *__restrict_
     cp_async_wait_all();
     __syncthreads();  // values in; long-column list complete
     FTRACE(b, 3);
-    // ---- pass 2: warps sort and fold the long columns -------------------------
+    // ---- pass 2: warps sort and fold the long columns, 4 / 2 / 1 per warp ------
     {
-        const int nl = min(S.nlong, LCAP);
-        for (int e = warp; e < nl; e += NWARP) {
-            const int v = S.lcol[e];
-            const int off = v & 0xffff;
-            const int c = v >> 16;
-            int u = -1;  // outputs at [off, off+u)
-            if (c <= 64) u = fold_column_bitonic<2>(&K[off], &V[off], c, S.skey[warp]);
-            else if (c <= 128) u = fold_column_bitonic<4>(&K[off], &V[off], c, S.skey[warp]);
-            else if (c <= LONGCAP) u = fold_column_bitonic<8>(&K[off], &V[off], c, S.skey[warp]);
-            if (u < 0) {
-                if (lane == 0) fold_column_serial(&K[off], &V[off], c);
-                __syncwarp();
-            }
+        const int n0 = min(S.ncls[0], LCAP), n1 = min(S.ncls[1], LCAP), n2 = min(S.ncls[2], LCAP);
+        const int b0 = (n0 + 3) / 4, b1 = (n1 + 1) / 2;
+        for (int t = warp; t < b0 + b1 + n2; t += NWARP) {
+            if (t < b0)
+                fold_columns_group<8, 8>(K, V, &S.lcol[0][4 * t], min(4, n0 - 4 * t), S.skey[warp],
+                                         S.lcol[3], &S.ncls[3]);
+            else if (t < b0 + b1)
+                fold_columns_group<16, 8>(K, V, &S.lcol[1][2 * (t - b0)], min(2, n1 - 2 * (t - b0)),
+                                          S.skey[warp], S.lcol[3], &S.ncls[3]);
+            else
+                fold_columns_group<32, 8>(K, V, &S.lcol[2][t - b0 - b1], 1, S.skey[warp], S.lcol[3],
+                                          &S.ncls[3]);
+        }
+    }
+    __syncthreads();
+    {  // columns whose spans do not fit the packed key (and counts above LONGCAP)
+        const int nf = min(S.ncls[3], LCAP);
+        for (int e = tid; e < nf; e += NT) {
+            const int v = S.lcol[3][e];
+            fold_column_serial(&K[v & 0xffff], &V[v & 0xffff], v >> 16);
         }
     }
     __syncthreads();
