@@ -18,6 +18,7 @@
  *                                     parallel.find_max_parallel  parallel.py:87-122
  *                                     _kernels.validate_chunk     _kernels.pyx:92-110
  *   sa_infer_dims                  <- AssemblyRequest.effective_dims (inferred) types.py:102-118
+ *   sa_prune_zeros                 <- types.prune_explicit_zeros types.py:204-213
  *
  * Conventions
  *   - Every call returns an sa_status (0 = SA_OK).  sa_last_error() gives a
@@ -145,6 +146,16 @@ int sa_host_fetch(sa_ctx *ctx, int32_t *h_jc, int32_t *h_ir, double *h_pr);
  */
 void *sa_host_buffer(uint64_t bytes);
 void sa_host_buffer_release(void *ptr);
+
+/*
+ * Matlab-style post-pass on a device CSC (types.py:204-213): drop entries
+ * stored as exactly 0.0 (either sign; NaN is kept), keep the order, recompact
+ * jc.  d_jc_out[N+1], d_ir_out / d_pr_out (capacity nnz) must not alias the
+ * inputs.  Synchronous; *nnz_out receives the pruned count.
+ */
+int sa_prune_zeros(sa_ctx *ctx, const int32_t *d_jc, const int32_t *d_ir, const double *d_pr,
+                   int32_t N, int64_t nnz, int32_t *d_jc_out, int32_t *d_ir_out,
+                   double *d_pr_out, int64_t *nnz_out);
 
 /* Number of kernel launches enqueued by the last sa_assemble_async. */
 int sa_last_launch_count(const sa_ctx *ctx);

@@ -190,3 +190,15 @@ def validate_c(raw, L=None):
     mx = ctypes.c_int32(0)
     bad = lib.sao_validate(arr.ctypes.data, kind, len(arr), out.ctypes.data, ctypes.byref(mx))
     return int(bad), out[: len(arr)], int(mx.value)
+
+
+def prune_zeros(jc, ir, pr, m, n) -> "Csc":
+    """Reference types.py:204-213 (prune_explicit_zeros): drop entries stored
+    as exactly 0.0 (either sign; NaN != 0.0 is kept), keep the order,
+    recompact jc.  Checker for the device post-pass (sa_prune_zeros)."""
+    jc = np.asarray(jc, dtype=np.int64)
+    pr = np.asarray(pr, dtype=np.float64)
+    keep = pr != 0.0
+    before = np.zeros(len(pr) + 1, dtype=np.int64)
+    np.cumsum(keep, out=before[1:])
+    return Csc(before[jc].astype(np.int32), np.asarray(ir, dtype=np.int32)[keep], pr[keep], m, n)

@@ -11,8 +11,22 @@ host side.  There is no CPU fallback: without the CUDA library every entry
 point raises.
 """
 
-from .assembly import Assembler, DeviceCsc, assemble, default_assembler, validate_and_convert
-from .errors import BadIndex, DeviceError, DimensionTooSmall, LengthMismatch, ResultMismatch
+from .assembly import (
+    Assembler,
+    DeviceCsc,
+    assemble,
+    default_assembler,
+    prune_explicit_zeros,
+    validate_and_convert,
+)
+from .errors import (
+    BadIndex,
+    DeviceError,
+    DimensionTooSmall,
+    LengthMismatch,
+    ParseError,
+    ResultMismatch,
+)
 from .types import (
     AssemblyRequest,
     CscMatrix,
@@ -20,7 +34,6 @@ from .types import (
     TripletList,
     csc_validate,
     normalize_raw,
-    prune_explicit_zeros,
 )
 
 __version__ = "0.1.0"
@@ -35,6 +48,7 @@ __all__ = [
     "DimensionTooSmall",
     "Dimensions",
     "LengthMismatch",
+    "ParseError",
     "ResultMismatch",
     "TripletList",
     "assemble",

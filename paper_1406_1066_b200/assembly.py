@@ -240,6 +240,42 @@ class Assembler:
         k = nnz.value
         return DeviceCsc(jc, ir[:k], pr[:k], dims.m, dims.n)
 
+    # -- Matlab-style post-pass (types.py:204-213) on the device ---------------
+    def prune_zeros_device(self, m: DeviceCsc) -> DeviceCsc:
+        """Drop entries stored as exactly 0.0 (either sign; NaN kept) from a
+        device CSC; returns a new DeviceCsc (sa_prune_zeros)."""
+        import torch
+
+        nnz = m.nnz
+        dev = m.jc.device
+        jc = torch.empty(m.n + 1, dtype=torch.int32, device=dev)
+        ir = torch.empty(max(nnz, 1), dtype=torch.int32, device=dev)
+        pr = torch.empty(max(nnz, 1), dtype=torch.float64, device=dev)
+        self._bind_stream()
+        out = ctypes.c_int64(0)
+        src_ir = m.ir.contiguous()
+        src_pr = m.pr.contiguous()
+        rc = self.lib.sa_prune_zeros(self.ctx, _ptr(m.jc.contiguous()), _ptr(src_ir), _ptr(src_pr),
+                                     m.n, nnz, _ptr(jc), _ptr(ir), _ptr(pr), ctypes.byref(out))
+        if rc:
+            self._raise(rc)
+        k = out.value
+        return DeviceCsc(jc, ir[:k], pr[:k], m.m, m.n)
+
+    def prune_zeros(self, m):
+        """prune_explicit_zeros for a host CscMatrix (uploaded, pruned on the
+        device, fetched) or a DeviceCsc (stays on the device)."""
+        if isinstance(m, DeviceCsc):
+            return self.prune_zeros_device(m)
+        import torch
+
+        dev = torch.device("cuda", self.device)
+        d = DeviceCsc(torch.from_numpy(np.ascontiguousarray(m.jc, dtype=np.int32)).to(dev),
+                      torch.from_numpy(np.ascontiguousarray(m.ir, dtype=np.int32)).to(dev),
+                      torch.from_numpy(np.ascontiguousarray(m.pr, dtype=np.float64)).to(dev),
+                      int(m.m), int(m.n))
+        return self.prune_zeros_device(d).to_host()
+
     def _raise_dev(self, rc, pos, which, raw_i, raw_j, ii, jj):
         if rc == _capi.SA_ERR_BAD_INDEX:
             arr = raw_i if which == _capi.SA_WHICH_ROW else raw_j
@@ -309,6 +345,14 @@ def assemble(i, j, s, m=None, n=None, nzmax=None, threads=None, *, device: int =
     ignored; ``nzmax`` is a hint only.
     """
     return default_assembler(device).assemble(i, j, s, m=m, n=n, nzmax=nzmax)
+
+
+def prune_explicit_zeros(m, *, device: int = 0):
+    """Matlab-style post-pass of the reference (types.py:204-213): drop the
+    entries stored as exactly 0.0 (+0.0 and -0.0; NaN is kept) and recompact
+    jc.  Runs on the GPU (sa_prune_zeros) for a host CscMatrix or a
+    DeviceCsc; returns the same kind."""
+    return default_assembler(device).prune_zeros(m)
 
 
 def validate_and_convert(raw_i, raw_j, raw_s, *, device: int = 0):

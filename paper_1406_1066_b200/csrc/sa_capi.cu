@@ -34,6 +34,8 @@ struct sa_ctx {
     unsigned long long *scan_state = nullptr; size_t ss_cap = 0;  // scan CTAs
     BigCol *big_list = nullptr;           size_t bl_cap = 0;      // L/(BIGCOL+1)+1
     uint32_t *bigk = nullptr;             size_t bk_cap = 0;      // N
+    unsigned long long *pr_state = nullptr; size_t prs_cap = 0;  // prune look-back words
+    long long *pr_nnz = nullptr;          // prune: device nnz of the result
     ErrState *err = nullptr;              // device
     ErrState *err_host = nullptr;         // pinned mirror
 
@@ -251,7 +253,7 @@ int sa_last_kernel_times(sa_ctx *ctx, int max, float *ms, const char **names) {
     return n;
 }
 
-int sa_version(void) { return 1; }
+int sa_version(void) { return 2; }
 
 int sa_create(int device, sa_ctx **out) {
     if (!out) return SA_ERR_INVALID_ARG;
@@ -288,6 +290,8 @@ void sa_destroy(sa_ctx *ctx) {
     cudaFree(ctx->big_list);
     cudaFree(ctx->bigk);
     cudaFree(ctx->err);
+    cudaFree(ctx->pr_state);
+    cudaFree(ctx->pr_nnz);
     cudaFree(ctx->h_ii);
     cudaFree(ctx->h_jj);
     cudaFree(ctx->h_s);
@@ -497,6 +501,26 @@ int sa_host_fetch(sa_ctx *ctx, int32_t *h_jc, int32_t *h_ir, double *h_pr) {
         SA_CUDA(ctx, cudaMemcpyAsync(h_pr, ctx->o_pr, (size_t)ctx->host_nnz * 8, cudaMemcpyDeviceToHost, ctx->stream));
     }
     SA_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    return SA_OK;
+}
+
+int sa_prune_zeros(sa_ctx *ctx, const int32_t *d_jc, const int32_t *d_ir, const double *d_pr,
+                   int32_t N, int64_t nnz, int32_t *d_jc_out, int32_t *d_ir_out,
+                   double *d_pr_out, int64_t *nnz_out) {
+    if (!ctx) return SA_ERR_INVALID_ARG;
+    if (N < 0 || nnz < 0 || !d_jc || !d_jc_out || (nnz > 0 && (!d_ir || !d_pr || !d_ir_out || !d_pr_out)))
+        return fail(ctx, SA_ERR_INVALID_ARG, "sa_prune_zeros: bad arguments");
+    SA_CUDA(ctx, cudaSetDevice(ctx->device));
+    Launch lc{ctx->stream, ctx->num_sms, 0};
+    SA_CUDA(ctx, ensure(ctx->pr_state, ctx->prs_cap, (size_t)std::max<int64_t>(prune_tiles(nnz), 1) * LB_STRIDE));
+    if (!ctx->pr_nnz) SA_CUDA(ctx, cudaMalloc(reinterpret_cast<void **>(&ctx->pr_nnz), sizeof(long long)));
+    SA_CUDA(ctx, launch_prune(lc, d_jc, d_ir, d_pr, N, nnz, d_jc_out, d_ir_out, d_pr_out,
+                              ctx->pr_state, ctx->pr_nnz));
+    long long h = 0;
+    SA_CUDA(ctx, cudaMemcpyAsync(&h, ctx->pr_nnz, sizeof(long long), cudaMemcpyDeviceToHost, ctx->stream));
+    SA_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    ctx->launches = lc.launches;
+    if (nnz_out) *nnz_out = h;
     return SA_OK;
 }
 

@@ -294,4 +294,9 @@ cudaError_t launch_tile_fold(Launch &lc, const uint32_t *sstart, const int2 *til
                              unsigned long long *tile_state, int32_t N, int32_t *jc, int32_t *ir,
                              double *pr, int64_t cap, ErrState *err);
 
+cudaError_t launch_prune(Launch &lc, const int32_t *jc, const int32_t *ir, const double *pr,
+                         int32_t N, int64_t nnz, int32_t *jc_out, int32_t *ir_out,
+                         double *pr_out, unsigned long long *state, long long *nnz_out);
+int64_t prune_tiles(int64_t nnz);
+
 }  // namespace sa

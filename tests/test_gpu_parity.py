@@ -36,7 +36,7 @@ def test_cuda_library_is_the_one_loaded():
     from paper_1406_1066_b200 import _capi
 
     lib = _capi.load(build_if_missing=False)
-    assert lib.sa_version() == 1
+    assert lib.sa_version() == 2
     maps = open("/proc/self/maps").read()
     assert _capi.library_path() in maps
 
@@ -230,3 +230,98 @@ def test_prune_explicit_zeros_on_gpu_output():
     out = sa.assemble(np.array([1, 1, 2], np.int32), np.array([1, 1, 1], np.int32), [2.0, -2.0, 5.0])
     p = sa.prune_explicit_zeros(out)
     assert p.nnz == 1 and p.jc.tolist() == [0, 1] and p.ir.tolist() == [1] and p.pr.tolist() == [5.0]
+
+
+def _prune_case(jc, ir, pr, m, n):
+    from oracle import oracle as O
+
+    mat = sa.CscMatrix(np.asarray(jc, np.int32), np.asarray(ir, np.int32), np.asarray(pr, np.float64), m, n)
+    got = sa.prune_explicit_zeros(mat)
+    ref = O.prune_zeros(jc, ir, pr, m, n)
+    _same(got, ref)
+    return got
+
+
+def test_prune_explicit_zeros_reference_cases():
+    p = _prune_case([0, 2], [0, 1], [1.0, 2.0], 2, 1)
+    assert p.pr.tolist() == [1.0, 2.0]
+    p = _prune_case([0, 2, 3], [0, 1, 1], [0.0, 5.0, -0.0], 2, 2)
+    assert p.jc.tolist() == [0, 1, 1] and p.ir.tolist() == [1] and p.pr.tolist() == [5.0]
+    p = _prune_case([0, 1, 2], [0, 0], [np.nan, 0.0], 1, 2)
+    assert p.nnz == 1 and np.isnan(p.pr[0]) and p.jc.tolist() == [0, 1, 1]
+    p = _prune_case([0, 0, 0, 0], [], [], 4, 3)
+    assert p.nnz == 0 and p.jc.tolist() == [0, 0, 0, 0]
+    p = _prune_case([0, 3], [0, 1, 2], [0.0, -0.0, 0.0], 3, 1)
+    assert p.nnz == 0 and p.jc.tolist() == [0, 0]
+
+
+def test_prune_explicit_zeros_multi_tile():
+    """Many tiles, empty and all-zero columns, zeros at tile boundaries,
+    NaN payloads, a device-resident input."""
+    import torch
+
+    rng = np.random.default_rng(7)
+    n = 20_000
+    counts = rng.integers(0, 9, size=n)
+    counts[rng.integers(0, n, 300)] = 0
+    jc = np.zeros(n + 1, np.int64)
+    np.cumsum(counts, out=jc[1:])
+    nnz = int(jc[-1])
+    ir = np.concatenate([np.sort(rng.choice(1000, size=c, replace=False)) for c in counts]).astype(np.int32)
+    pr = rng.standard_normal(nnz)
+    pr[rng.random(nnz) < 0.3] = 0.0
+    pr[rng.random(nnz) < 0.05] = -0.0
+    pr[2047:2050] = 0.0
+    pr[rng.random(nnz) < 0.01] = np.nan
+    _prune_case(jc, ir, pr, 1000, n)
+    dev = torch.device("cuda", 0)
+    d = sa.DeviceCsc(torch.from_numpy(jc.astype(np.int32)).to(dev), torch.from_numpy(ir).to(dev),
+                     torch.from_numpy(pr).to(dev), 1000, n)
+    got = sa.prune_explicit_zeros(d)
+    assert isinstance(got, sa.DeviceCsc)
+    from oracle import oracle as O
+
+    _same(got.to_host(), O.prune_zeros(jc, ir, pr, 1000, n))
+
+
+def test_harness_impl_with_reference_shaped_request():
+    """make_impl("b200") runs both request types (the reference's validated
+    AssemblyRequest shape and this package's), with phase times."""
+    from types import SimpleNamespace
+
+    from paper_1406_1066_b200.harness import make_impl
+
+    ii, jj, sr = random_triplets(5, max_len=30_000, max_dim=400, allow_special=False)
+    ii, jj = ii.astype(np.int32), jj.astype(np.int32)
+    ref = O.assemble_counting(ii, jj, sr, int(ii.max()), int(jj.max()))
+    impl = make_impl("b200")
+    assert impl.threads == 1 and impl.name.startswith("b200")
+    req_ref = SimpleNamespace(triplets=SimpleNamespace(ii=ii, jj=jj, sr=sr), dims=None,
+                              capacity_hint=None)
+    pt = {}
+    _same(impl.run(req_ref, pt), ref)
+    assert set(pt) == {"upload", "assemble", "fetch"} and all(v >= 0 for v in pt.values())
+    req = sa.AssemblyRequest.from_raw(ii, jj, sr, m=ref.m, n=ref.n)
+    _same(impl.run(req), ref)
+
+
+def test_matrixmarket_round_trip_bit_faithful(tmp_path):
+    """write -> read keeps every value bit-exact; the read triplets assemble
+    to the oracle's matrix; indices beyond the declared size are rejected."""
+    from paper_1406_1066_b200.mmio import read_triplets_matrixmarket, write_triplets_matrixmarket
+
+    ii, jj, sr = random_triplets(11, max_len=3_000, max_dim=50, allow_special=False)
+    t = sa.TripletList(ii.astype(np.int32), jj.astype(np.int32), sr)
+    p = tmp_path / "r.mtx"
+    write_triplets_matrixmarket(t, sa.Dimensions(60, 70), p)
+    t2, d2 = read_triplets_matrixmarket(p)
+    assert (d2.m, d2.n) == (60, 70)
+    assert np.array_equal(t2.ii, t.ii) and np.array_equal(t2.jj, t.jj)
+    assert t2.sr.tobytes() == t.sr.tobytes()
+    _same(sa.assemble(t2.ii, t2.jj, t2.sr, m=60, n=70), O.assemble_counting(t.ii, t.jj, t.sr, 60, 70))
+    p.write_text("%%MatrixMarket matrix coordinate real general\n2 2 1\n3 1 1.0\n")
+    with pytest.raises(sa.ParseError):
+        read_triplets_matrixmarket(p)
+    p.write_text("%%MatrixMarket matrix coordinate real general\n2 2 1\n1.5 1 1.0\n")
+    with pytest.raises(sa.BadIndex):
+        read_triplets_matrixmarket(p)

@@ -28,7 +28,7 @@ def test_library_builds_loads_and_exports_every_declared_symbol():
     assert set(declared) == set(_capi.SIGNATURES)
     for name in declared:
         assert hasattr(lib, name), name
-    assert lib.sa_version() == 1
+    assert lib.sa_version() == 2
 
 
 def test_library_is_sm100a():
@@ -92,14 +92,18 @@ def test_csc_validate():
     assert any("jc length" in v for v in sa.csc_validate(_mat([0, 1], [0], [1], 2, 2)))
 
 
-def test_prune_explicit_zeros():
-    m = _mat([0, 2], [0, 1], [1.0, 2.0], 2, 1)
-    p = sa.prune_explicit_zeros(m)
-    assert p.same_as(m) and p.pr is not m.pr
-    p = sa.prune_explicit_zeros(_mat([0, 2, 3], [0, 1, 1], [0.0, 5.0, -0.0], 2, 2))
+def test_prune_oracle_restates_reference_cases():
+    """oracle.prune_zeros pins the reference's prune semantics (types.py:204-213)."""
+    from oracle import oracle as O
+
+    p = O.prune_zeros([0, 2], [0, 1], [1.0, 2.0], 2, 1)
+    assert p.jc.tolist() == [0, 2] and p.ir.tolist() == [0, 1] and p.pr.tolist() == [1.0, 2.0]
+    p = O.prune_zeros([0, 2, 3], [0, 1, 1], [0.0, 5.0, -0.0], 2, 2)
     assert p.jc.tolist() == [0, 1, 1] and p.ir.tolist() == [1] and p.pr.tolist() == [5.0]
-    p = sa.prune_explicit_zeros(_mat([0, 1, 2], [0, 0], [np.nan, 0.0], 1, 2))
+    p = O.prune_zeros([0, 1, 2], [0, 0], [np.nan, 0.0], 1, 2)
     assert p.nnz == 1 and np.isnan(p.pr[0]) and p.jc.tolist() == [0, 1, 1]
+    p = O.prune_zeros([0, 0, 0], [], [], 3, 2)
+    assert p.jc.tolist() == [0, 0, 0] and p.nnz == 0
 
 
 def test_same_as_is_bitwise():
@@ -135,3 +139,52 @@ def test_product_package_never_imports_the_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".h")):
                 text = open(os.path.join(dirpath, f)).read()
                 assert "oracle" not in re.sub(r"#.*|//.*", "", text).replace("oracle/", ""), f
+
+
+def test_harness_impl_shape():
+    """The harness hook has the reference's Impl shape (bench.py:101-107)."""
+    from paper_1406_1066_b200.harness import Impl, make_impl
+
+    impl = make_impl("b200", threads=8)
+    assert isinstance(impl, Impl) and impl.threads == 1 and callable(impl.run)
+    with pytest.raises(ValueError):
+        make_impl("serial")
+
+
+def test_matrixmarket_parse_errors(tmp_path):
+    """Header / size-line / entry errors are raised before any device work
+    (reference mmio.py:43-114 contract)."""
+    from paper_1406_1066_b200.mmio import read_triplets_matrixmarket
+
+    def bad(text, line):
+        p = tmp_path / "x.mtx"
+        p.write_text(text)
+        with pytest.raises(sa.ParseError) as e:
+            read_triplets_matrixmarket(p)
+        assert e.value.line == line
+
+    bad("", 1)
+    bad("%%MatrixMarket matrix array real general\n1 1\n", 1)
+    bad("%%MatrixMarket matrix coordinate complex general\n1 1 0\n", 1)
+    bad("%%MatrixMarket matrix coordinate real general\n% c\n2 x 1\n", 3)
+    bad("%%MatrixMarket matrix coordinate real general\n2 -2 1\n", 2)
+    bad("%%MatrixMarket matrix coordinate real general\n2 2 1\n1 1\n", 3)
+    bad("%%MatrixMarket matrix coordinate real general\n2 2 1\n1 1 q\n", 3)
+    bad("%%MatrixMarket matrix coordinate real general\n2 2 2\n1 1 1.0\n", 3)
+    bad("%%MatrixMarket matrix coordinate real general\n% only comments\n", 2)
+
+
+def test_matrixmarket_empty_and_writers(tmp_path):
+    from paper_1406_1066_b200.mmio import (read_triplets_matrixmarket, write_csc_matrixmarket,
+                                           write_triplets_matrixmarket)
+
+    p = tmp_path / "e.mtx"
+    p.write_text("%%MatrixMarket matrix coordinate integer general\n3 4 0\n")
+    t, d = read_triplets_matrixmarket(p)
+    assert len(t) == 0 and (d.m, d.n) == (3, 4)
+    write_triplets_matrixmarket(sa.TripletList(np.array([2, 1], np.int32), np.array([1, 3], np.int32),
+                                               np.array([0.1, -2.5])), sa.Dimensions(2, 3), p)
+    assert p.read_text().splitlines() == ["%%MatrixMarket matrix coordinate real general", "2 3 2",
+                                          "2 1 0.10000000000000001", "1 3 -2.5"]
+    write_csc_matrixmarket(_mat([0, 1, 1, 3], [1, 0, 1], [1.0, 2.0, 3.0], 2, 3), p)
+    assert p.read_text().splitlines()[1:] == ["2 3 3", "2 1 1", "1 3 2", "2 3 3"]
