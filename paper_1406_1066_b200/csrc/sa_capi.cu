@@ -103,6 +103,8 @@ __global__ void k_init(ErrState *err, uint32_t *cur, int64_t ncur, unsigned long
                        int64_t nts, unsigned long long *ss, int64_t nss, uint8_t *tb) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    pdl_wait();  // the previous call's fold may still read the look-back words
+    pdl_trigger();
     if (t0 == 0) {
         ErrState e;
         memset(&e, 0, sizeof(e));
@@ -125,10 +127,9 @@ __global__ void k_init(ErrState *err, uint32_t *cur, int64_t ncur, unsigned long
 int launch_init(sa_ctx *ctx, Launch &lc, int64_t ncur, int64_t nts, int64_t nss) {
     int64_t work = std::max<int64_t>({ncur / 4, nts, nss, 1});
     int grid = (int)std::min<int64_t>((work + 255) / 256, (int64_t)ctx->num_sms * 4);
-    k_init<<<grid, 256, 0, lc.stream>>>(ctx->err, ctx->cur, ncur, ctx->tile_state, nts,
-                                        ctx->scan_state, nss, ctx->tile_big);
+    SA_CUDA(ctx, launch_pdl(k_init, dim3(grid), dim3(256), 0, lc.stream, ctx->err, ctx->cur, ncur,
+                            ctx->tile_state, nts, ctx->scan_state, nss, ctx->tile_big));
     lc.launches++;
-    SA_CUDA(ctx, cudaGetLastError());
     return SA_OK;
 }
 

@@ -265,6 +265,33 @@ __device__ __forceinline__ void smem_incl_max(int *arr, int n, int *s_warp) {
     __syncthreads();
 }
 
+// ---- programmatic dependent launch -------------------------------------------
+// Every kernel of the assembly chain is launched with programmatic stream
+// serialisation: it may start (smem set-up) while its predecessor drains,
+// and waits at pdl_wait() before touching global memory the predecessor
+// writes or reads.  pdl_trigger() lets the successor launch once every CTA
+// of this grid has started.  Both are no-ops for a plain launch.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+bool pdl_enabled();  // SA_PDL=0 disables (A/B measurement)
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t stream, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 // ---- launchers (sa_kernels.cu) ---------------------------------------------
 struct Launch {
     cudaStream_t stream;

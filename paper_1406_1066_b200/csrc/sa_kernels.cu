@@ -237,6 +237,8 @@ __global__ void __launch_bounds__(SCAN_NT) k_col_scan(const uint32_t *cnt,
     __shared__ unsigned long long s_excl;
     __shared__ long long s_tail;
     __shared__ int s_tot;
+    pdl_wait();
+    pdl_trigger();
     if (threadIdx.x == 0) s_b = atomicAdd(&err->scan_ticket, 1u);
     __syncthreads();
     const long long b = s_b;
@@ -341,8 +343,9 @@ cudaError_t launch_col_scan(Launch &lc, const uint32_t *cnt, uint32_t *sstart, u
                             unsigned long long *scan_state, uint2 *perm, ErrState *err) {
     if (N <= 0) return cudaSuccess;
     int grid = (int)((N + SCAN_TILE - 1) / SCAN_TILE);
-    k_col_scan<<<grid, SCAN_NT, 0, lc.stream>>>(cnt, sstart, cur, N, tile_info, tile_big,
-                                               ntiles, big_list, bigk, scan_state, perm, err);
+    cudaError_t e = launch_pdl(k_col_scan, dim3(grid), dim3(SCAN_NT), 0, lc.stream, cnt, sstart, cur, N,
+                               tile_info, tile_big, ntiles, big_list, bigk, scan_state, perm, err);
+    if (e != cudaSuccess) return e;
     lc.launches++;
     return cudaGetLastError();
 }
@@ -572,6 +575,8 @@ __global__ void __launch_bounds__(AGG_NT) k_colcount_win(const int32_t *__restri
     for (int k = tid; k < WB; k += AGG_NT) W.bin[k] = 0;
     if (tid == 0) W.nused = 0;
     __syncthreads();
+    pdl_wait();
+    pdl_trigger();
     unsigned long long bad = ~0ull;
     unsigned over = 0;
     const int64_t nchunk = (L + CHUNK - 1) / CHUNK;
@@ -631,6 +636,15 @@ __global__ void __launch_bounds__(AGG_NT) k_colcount_win(const int32_t *__restri
 
 // Aggregation variants (measured on cfg2/cfg3/cfg4), chosen
 // by SA_COLCOUNT_MODE / SA_SCATTER_MODE = 0 direct, 1 hash, 2 window.
+bool pdl_enabled() {
+    static int m = -1;
+    if (m < 0) {
+        const char *e = getenv("SA_PDL");
+        m = (e && e[0] == '0') ? 0 : 1;
+    }
+    return m == 1;
+}
+
 static int env_mode(const char *name, int dflt) {
     const char *e = getenv(name);
     return (e && e[0] >= '0' && e[0] <= '2') ? e[0] - '0' : dflt;
@@ -656,7 +670,9 @@ cudaError_t launch_colcount(Launch &lc, const int32_t *jj, int64_t L, int32_t N,
     if (colcount_mode() == 1) {
         k_colcount<<<grid, AGG_NT, 0, lc.stream>>>(jj, L, N, cnt, err, vec);
     } else if (colcount_mode() == 2) {
-        k_colcount_win<<<grid, AGG_NT, 0, lc.stream>>>(jj, L, N, cnt, err, vec);
+        cudaError_t e = launch_pdl(k_colcount_win, dim3(grid), dim3(AGG_NT), 0, lc.stream, jj, L, N, cnt,
+                                   err, vec);
+        if (e != cudaSuccess) return e;
     } else {
         const int64_t want = ((L + CPT - 1) / CPT + AGG_NT - 1) / AGG_NT;
         const int g = (int)std::min<int64_t>(want, (int64_t)lc.num_sms * 8);
@@ -690,6 +706,8 @@ __global__ void __launch_bounds__(AGG_NT) k_scatter(const int32_t *__restrict__ 
     }
     if (tid == 0) A.nused = 0;
     __syncthreads();
+    pdl_wait();
+    pdl_trigger();
     const uint32_t lsmall = err->lsmall;
     unsigned long long bad = ~0ull;
     unsigned over = 0;
@@ -929,7 +947,9 @@ cudaError_t launch_scatter(Launch &lc, const int32_t *ii, const int32_t *jj, int
     const int64_t nchunk = (L + CHUNK - 1) / CHUNK;
     int grid = (int)std::min<int64_t>(nchunk, (int64_t)lc.num_sms * 4);
     if (scatter_mode() == 1) {
-        k_scatter<<<grid, AGG_NT, 0, lc.stream>>>(ii, jj, L, M, N, cur, perm, vec, err);
+        cudaError_t e = launch_pdl(k_scatter, dim3(grid), dim3(AGG_NT), 0, lc.stream, ii, jj, L, M, N, cur,
+                                   perm, vec, err);
+        if (e != cudaSuccess) return e;
     } else if (scatter_mode() == 2) {
         k_scatter_win<<<grid, AGG_NT, 0, lc.stream>>>(ii, jj, L, M, N, cur, perm, vec, err);
     } else {
@@ -965,7 +985,10 @@ __global__ void __launch_bounds__(BIG_NT) k_bigcol(BigCol *__restrict__ big_list
     __shared__ uint32_t s_warp[BIG_NT / 32];
     __shared__ unsigned long long s_prevrow;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    pdl_wait();
+    pdl_trigger();
     const unsigned nbig = *((volatile const unsigned *)&err->nbig);
+    if (blockIdx.x >= nbig) return;
     const unsigned lsmall = *((volatile const unsigned *)&err->lsmall);
     for (int k = tid; k < (BIG_NT / 32) * 257; k += BIG_NT) (&s_wcnt[0][0])[k] = 0;
     __syncthreads();
@@ -1083,7 +1106,9 @@ cudaError_t launch_bigcol(Launch &lc, BigCol *big_list, const ErrState *err, int
                           const uint2 *perm, const double *s, int64_t s_stride, int idx_bits,
                           int passes) {
     int grid = lc.num_sms;
-    k_bigcol<<<grid, BIG_NT, 0, lc.stream>>>(big_list, err, rec, perm, s, s_stride, idx_bits, passes);
+    cudaError_t e = launch_pdl(k_bigcol, dim3(grid), dim3(BIG_NT), 0, lc.stream, big_list, err, rec, perm, s,
+                               s_stride, idx_bits, passes);
+    if (e != cudaSuccess) return e;
     lc.launches++;
     return cudaGetLastError();
 }

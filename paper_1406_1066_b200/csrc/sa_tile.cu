@@ -518,6 +518,8 @@ __global__ void __launch_bounds__(NT, 5) k_tile_fold(const uint32_t *__restrict_
     TileSmem &S = *reinterpret_cast<TileSmem *>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const long long b = blockIdx.x;
+    pdl_wait();
+    pdl_trigger();
     FTRACE(b, 0);
     const int2 ti0 = tile_info[b], ti1 = tile_info[b + 1];
     const int c_a = ti0.x, r0 = ti0.y;
@@ -757,12 +759,11 @@ cudaError_t launch_tile_fold(Launch &lc, const uint32_t *sstart, const int2 *til
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    k_tile_fold<<<(unsigned)ntiles, NT, sizeof(TileSmem), lc.stream>>>(
-        sstart, tile_info, tile_big, ntiles, entries, s, s_stride, rec, big_list, bigk, tile_state, N,
-        jc, ir,
-        pr, cap, err);
+    cudaError_t e = launch_pdl(k_tile_fold, dim3((unsigned)ntiles), dim3(NT), sizeof(TileSmem), lc.stream,
+                               sstart, tile_info, tile_big, ntiles, entries, s, s_stride, rec, big_list,
+                               bigk, tile_state, N, jc, ir, pr, cap, err);
     lc.launches++;
-    return cudaGetLastError();
+    return e;
 }
 
 }  // namespace sa
