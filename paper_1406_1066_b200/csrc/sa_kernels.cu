@@ -843,7 +843,7 @@ __global__ void __launch_bounds__(AGG_NT) k_scatter_direct(const int32_t *__rest
     }
 }
 
-__global__ void __launch_bounds__(AGG_NT) k_scatter_win(const int32_t *__restrict__ ii,
+__global__ void __launch_bounds__(AGG_NT, 4) k_scatter_win(const int32_t *__restrict__ ii,
                                                         const int32_t *__restrict__ jj, int64_t L,
                                                         int32_t M, int32_t N,
                                                         uint32_t *__restrict__ cur,

@@ -31,3 +31,9 @@ for k in range(1, 8):
     print(f"{names[k-1]:9s} mean {d.mean():6.2f} us  p50 {np.median(d):6.2f}  p90 {np.percentile(d, 90):6.2f}  max {d.max():7.2f}")
 tot = t[:, 7] - t[:, 0]
 print(f"{'total':9s} mean {tot.mean():6.2f} us  p50 {np.median(tot):6.2f}  p90 {np.percentile(tot, 90):6.2f}")
+# ordering diagnostics: how far behind is the predecessor when a tile publishes?
+st = t[:, 0]
+pub = t[:, 4]
+lag = pub[:-1] - pub[1:]          # predecessor publish - own publish (>0: predecessor later)
+print("start order violations (tile starts before its predecessor): %.1f%%" % (100.0 * (st[1:] < st[:-1]).mean()))
+print("predecessor publishes after me: %.1f%%, mean lag when late %.2f us" % (100.0 * (lag > 0).mean(), lag[lag > 0].mean() if (lag > 0).any() else 0.0))
