@@ -19,6 +19,9 @@
  *                                     _kernels.validate_chunk     _kernels.pyx:92-110
  *   sa_infer_dims                  <- AssemblyRequest.effective_dims (inferred) types.py:102-118
  *   sa_prune_zeros                 <- types.prune_explicit_zeros types.py:204-213
+ *   sa_partition                   <- (new: multi-GPU column-block sharding, SURVEY 8(e);
+ *                                     the reference's threaded driver partitions by
+ *                                     element range, parallel.py:28-35, 267-358)
  *
  * Conventions
  *   - Every call returns an sa_status (0 = SA_OK).  sa_last_error() gives a
@@ -156,6 +159,22 @@ void sa_host_buffer_release(void *ptr);
 int sa_prune_zeros(sa_ctx *ctx, const int32_t *d_jc, const int32_t *d_ir, const double *d_pr,
                    int32_t N, int64_t nnz, int32_t *d_jc_out, int32_t *d_ir_out,
                    double *d_pr_out, int64_t *nnz_out);
+
+/*
+ * Multi-GPU column-block sharding (one process per GPU).  sa_partition
+ * groups a rank's triplets by destination rank -- the owner of the column,
+ * h_bounds[r] <= j-1 < h_bounds[r+1] for r < world (<= 8) -- into the arrays
+ * d_ii_out, d_jj_out (j - h_bounds[dest], 1-based inside the block), d_s_out
+ * (capacity L each): destinations in rank order, input order inside each
+ * (stable), ready for the all-to-all and for sa_assemble_async on the
+ * receiver.  The chunk is validated on the way: SA_ERR_BAD_INDEX with
+ * *bad_pos (chunk-local) / *bad_which, SA_ERR_DIM_TOO_SMALL for indices
+ * above the global M / N.  Synchronous; h_counts[r] = triplets for rank r.
+ */
+int sa_partition(sa_ctx *ctx, const int32_t *d_ii, const int32_t *d_jj, const double *d_s,
+                 int64_t s_stride, int64_t L, int32_t M, int32_t N, int32_t world,
+                 const int32_t *h_bounds, int32_t *d_ii_out, int32_t *d_jj_out, double *d_s_out,
+                 int64_t *h_counts, int64_t *bad_pos, int *bad_which);
 
 /* Number of kernel launches enqueued by the last sa_assemble_async. */
 int sa_last_launch_count(const sa_ctx *ctx);

@@ -36,6 +36,10 @@ struct sa_ctx {
     uint32_t *bigk = nullptr;             size_t bk_cap = 0;      // N
     unsigned long long *pr_state = nullptr; size_t prs_cap = 0;  // prune look-back words
     long long *pr_nnz = nullptr;          // prune: device nnz of the result
+    int32_t *pt_cnt = nullptr;            size_t ptc_cap = 0;    // partition: tile x rank counts
+    int64_t *pt_off = nullptr;            size_t pto_cap = 0;    // partition: tile x rank offsets
+    int64_t *pt_counts = nullptr;         // partition: per-rank counts and bases (16)
+    unsigned char *pt_chk = nullptr;      size_t ptk_cap = 0;    // partition: per-tile index checks
     ErrState *err = nullptr;              // device
     ErrState *err_host = nullptr;         // pinned mirror
 
@@ -292,6 +296,10 @@ void sa_destroy(sa_ctx *ctx) {
     cudaFree(ctx->bigk);
     cudaFree(ctx->err);
     cudaFree(ctx->pr_state);
+    cudaFree(ctx->pt_cnt);
+    cudaFree(ctx->pt_off);
+    cudaFree(ctx->pt_counts);
+    cudaFree(ctx->pt_chk);
     cudaFree(ctx->pr_nnz);
     cudaFree(ctx->h_ii);
     cudaFree(ctx->h_jj);
@@ -523,6 +531,40 @@ int sa_prune_zeros(sa_ctx *ctx, const int32_t *d_jc, const int32_t *d_ir, const 
     ctx->launches = lc.launches;
     if (nnz_out) *nnz_out = h;
     return SA_OK;
+}
+
+int sa_partition(sa_ctx *ctx, const int32_t *d_ii, const int32_t *d_jj, const double *d_s,
+                 int64_t s_stride, int64_t L, int32_t M, int32_t N, int32_t world,
+                 const int32_t *h_bounds, int32_t *d_ii_out, int32_t *d_jj_out, double *d_s_out,
+                 int64_t *h_counts, int64_t *bad_pos, int *bad_which) {
+    if (!ctx) return SA_ERR_INVALID_ARG;
+    if (L < 0 || M < 0 || N < 0 || world < 1 || world > 8 || !h_bounds || !h_counts ||
+        (s_stride != 0 && s_stride != 1) ||
+        (L > 0 && (!d_ii || !d_jj || !d_s || !d_ii_out || !d_jj_out || !d_s_out)))
+        return fail(ctx, SA_ERR_INVALID_ARG, "sa_partition: bad arguments");
+    SA_CUDA(ctx, cudaSetDevice(ctx->device));
+    Launch lc{ctx->stream, ctx->num_sms, 0};
+    const size_t nt = (size_t)std::max<int64_t>(partition_tiles(L), 1) * (size_t)world;
+    SA_CUDA(ctx, ensure(ctx->pt_cnt, ctx->ptc_cap, nt));
+    SA_CUDA(ctx, ensure(ctx->pt_off, ctx->pto_cap, nt));
+    SA_CUDA(ctx, ensure(ctx->pt_chk, ctx->ptk_cap, std::max<size_t>(partition_check_bytes(L), 16)));
+    if (!ctx->pt_counts) SA_CUDA(ctx, cudaMalloc(reinterpret_cast<void **>(&ctx->pt_counts), 16 * sizeof(int64_t)));
+    int rc = launch_init(ctx, lc, 0, 0, 0);  // error state
+    if (rc) return rc;
+    SA_CUDA(ctx, launch_partition(lc, d_ii, d_jj, d_s, s_stride, L, world, h_bounds, ctx->pt_cnt,
+                                  ctx->pt_off, ctx->pt_counts, d_ii_out, d_jj_out, d_s_out, ctx->pt_chk,
+                                  ctx->err));
+    int64_t h[16];
+    SA_CUDA(ctx, cudaMemcpyAsync(h, ctx->pt_counts, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+    SA_CUDA(ctx, cudaMemcpyAsync(ctx->err_host, ctx->err, sizeof(ErrState), cudaMemcpyDeviceToHost, ctx->stream));
+    SA_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    for (int r = 0; r < world; ++r) h_counts[r] = h[r];
+    ctx->launches = lc.launches;
+    ErrState e = *ctx->err_host;
+    if (e.bad_i == ~0ull && e.bad_j == ~0ull && ((int64_t)e.max_i > M || (int64_t)e.max_j > N))
+        e.over_m = 1;  // a valid index beyond the global dimensions
+    e.nnz = 0;
+    return decode(ctx, e, nullptr, bad_pos, bad_which);
 }
 
 }  // extern "C"

@@ -3,12 +3,15 @@
 Each rank holds a contiguous chunk of the global triplet stream (chunks in
 rank order = input order).  Per call:
 
-1. every rank histograms its triplets into ``nblocks`` equal column blocks;
-   one ``all_reduce`` gives the global block histogram;
+1. every rank histograms (a strided sample of) its triplets into
+   ``nblocks`` equal column blocks; one ``all_reduce`` gives the global block
+   histogram;
 2. contiguous column ranges are assigned to ranks so that each receives about
    L / world triplets (block granularity);
-3. each rank partitions its chunk by destination rank, *stably*, and one
-   ``all_to_all`` moves the triplets (row, column, value) to their owners;
+3. each rank partitions its chunk by destination rank, *stably* (the CUDA
+   kernels of sa_partition: per-tile counts, a scan, a block-scanned scatter
+   of (row, local column, value), validating the chunk on the way), and
+   ``all_to_all`` moves them to their owners;
    a rank concatenates what it receives in source-rank order, which is the
    global input order restricted to its columns -- so duplicates are still
    folded in input order and the result is bit-identical to one GPU;
@@ -63,45 +66,98 @@ def block_boundaries(block_hist: torch.Tensor, world: int, nblocks: int, n: int)
     return bounds
 
 
+def partition_torch(ii, jj, s, bounds, world):
+    """Host restatement of sa_partition (CPU tensors: the gloo tests).
+    Returns ((i, j - bounds[dest], s) grouped by destination rank, stably;
+    per-rank counts).  Columns outside [1, bounds[-1]] go nowhere."""
+    jj64 = jj.to(torch.int64)
+    bt = torch.tensor(bounds[1:-1], dtype=torch.int64, device=jj.device)
+    valid = (jj64 >= 1) & (jj64 <= bounds[-1])
+    dest = torch.searchsorted(bt, jj64 - 1, right=True)
+    dest = torch.where(valid, dest, torch.full_like(dest, world))
+    key = dest.to(torch.uint8) if world < 255 else dest
+    order = torch.sort(key, stable=True).indices
+    counts = torch.bincount(dest, minlength=world + 1)[:world]
+    keep = order[: int(counts.sum())]
+    base = torch.tensor(bounds, dtype=torch.int64, device=jj.device)[dest[keep]]
+    sv = s.expand(len(jj)) if s.numel() == 1 and len(jj) != 1 else s
+    out = (ii[keep].contiguous(), (jj64[keep] - base).to(torch.int32), sv[keep].contiguous())
+    return out, [int(c) for c in counts.tolist()]
+
+
+def _partition_cuda(ii, jj, s, m, n, bounds, world):
+    """sa_partition: the CUDA partition (validates the chunk on the way)."""
+    import ctypes
+
+    from .assembly import _ptr, default_assembler
+
+    dev = ii.device
+    asm = default_assembler(dev.index if dev.index is not None else 0)
+    asm._bind_stream()
+    L = len(ii)
+    outs = (torch.empty(max(L, 1), dtype=torch.int32, device=dev),
+            torch.empty(max(L, 1), dtype=torch.int32, device=dev),
+            torch.empty(max(L, 1), dtype=torch.float64, device=dev))
+    hb = (ctypes.c_int32 * (world + 1))(*bounds)
+    hc = (ctypes.c_int64 * world)()
+    bp, bw = ctypes.c_int64(-1), ctypes.c_int(-1)
+    sv = s.contiguous()
+    ii, jj = ii.contiguous(), jj.contiguous()
+    rc = asm.lib.sa_partition(asm.ctx, _ptr(ii), _ptr(jj), _ptr(sv),
+                              0 if (sv.numel() == 1 and L != 1) else 1, L, m, n, world, hb,
+                              _ptr(outs[0]), _ptr(outs[1]), _ptr(outs[2]), hc, ctypes.byref(bp),
+                              ctypes.byref(bw))
+    if rc:
+        asm._raise_dev(rc, bp.value, bw.value, None, None, ii, jj)
+    counts = [int(hc[r]) for r in range(world)]
+    k = sum(counts)
+    return tuple(x[:k] for x in outs), counts
+
+
 def assemble_sharded(ii: torch.Tensor, jj: torch.Tensor, s: torch.Tensor, m: int, n: int,
                      local_assemble, group=None, nblocks: int = 4096) -> ShardResult:
     """Assemble the global matrix whose triplets are split across the ranks
     of `group` (contiguous chunks in rank order).  `local_assemble(ii, jj, s,
-    m, n_local)` -> (jc int, ir int32, pr float64) tensors on ii's device."""
+    m, n_local)` -> (jc int, ir int32, pr float64) tensors on ii's device.
+
+    CUDA tensors: the partition is the CUDA kernel set of sa_partition (which
+    also validates the chunk: BadIndex with the chunk-local position,
+    DimensionTooSmall); CPU tensors (gloo tests): its torch restatement."""
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     dev = ii.device
+    if world == 1:  # one rank owns every column: no partition, no exchange
+        jc, ir, pr = local_assemble(ii, jj, s, m, n)
+        k = int(jc[-1]) if len(jc) else 0
+        return ShardResult(0, n, jc.to(torch.int64), ir, pr, 0, k, m, n, int(ii.shape[0]), 0)
     nblocks = max(1, min(nblocks, n))
     bsize = (n + nblocks - 1) // nblocks
-    jj64 = jj.to(torch.int64)
-    blk = torch.clamp((jj64 - 1) // bsize, 0, nblocks - 1)
-    hist = torch.bincount(blk, minlength=nblocks).to(torch.int64)
+    # the boundaries only balance the ranks' work: a strided sample of the
+    # columns (<= 2^20 per rank) is enough and keeps this off the critical path
+    step = max(1, len(jj) >> 20)
+    blk = torch.clamp((jj[::step].to(torch.int64) - 1) // bsize, 0, nblocks - 1)
+    hist = torch.bincount(blk, minlength=nblocks).to(torch.int64) * step
     dist.all_reduce(hist, group=group)
     bounds = block_boundaries(hist, world, nblocks, n)
-    bt = torch.tensor(bounds[1:-1], dtype=torch.int64, device=dev)
-    dest = torch.searchsorted(bt, jj64 - 1, right=True)  # owner rank of each triplet
-    # stable partition by destination (input order kept inside each destination)
-    order = torch.sort(dest, stable=True).indices
-    send_counts = torch.bincount(dest, minlength=world).to(torch.int64)
+    if ii.is_cuda:
+        parts, sc = _partition_cuda(ii, jj, s, m, n, bounds, world)
+    else:
+        parts, sc = partition_torch(ii, jj, s, bounds, world)
+    send_counts = torch.tensor(sc, dtype=torch.int64, device=dev)
     recv_counts = torch.empty_like(send_counts)
     dist.all_to_all_single(recv_counts, send_counts, group=group)
-    sc = send_counts.cpu().tolist()
-    rc = recv_counts.cpu().tolist()
+    rc_ = recv_counts.cpu().tolist()
     sent_remote = sum(c for r, c in enumerate(sc) if r != rank)
 
     def exchange(x):
-        out = torch.empty(sum(rc), dtype=x.dtype, device=dev)
-        dist.all_to_all_single(out, x[order].contiguous(), output_split_sizes=rc,
-                               input_split_sizes=sc, group=group)
+        out = torch.empty(sum(rc_), dtype=x.dtype, device=dev)
+        dist.all_to_all_single(out, x, output_split_sizes=rc_, input_split_sizes=sc, group=group)
         return out
 
-    r_ii = exchange(ii)
-    r_jj = exchange(jj)
-    r_s = exchange(s)
+    r_ii, r_jj, r_s = (exchange(x) for x in parts)
     col_lo, col_hi = bounds[rank], bounds[rank + 1]
     n_local = col_hi - col_lo
-    r_jj_local = (r_jj.to(torch.int64) - col_lo).to(torch.int32)
-    jc, ir, pr = local_assemble(r_ii, r_jj_local, r_s, m, n_local)
+    jc, ir, pr = local_assemble(r_ii, r_jj, r_s, m, n_local)
     nnz_local = torch.tensor([int(jc[-1]) if len(jc) else 0], dtype=torch.int64, device=dev)
     all_nnz = [torch.empty_like(nnz_local) for _ in range(world)]
     dist.all_gather(all_nnz, nnz_local, group=group)

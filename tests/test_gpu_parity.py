@@ -325,3 +325,82 @@ def test_matrixmarket_round_trip_bit_faithful(tmp_path):
     p.write_text("%%MatrixMarket matrix coordinate real general\n2 2 1\n1.5 1 1.0\n")
     with pytest.raises(sa.BadIndex):
         read_triplets_matrixmarket(p)
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+def test_partition_kernel_matches_torch_restatement(world):
+    """sa_partition (CUDA) == partition_torch: destinations in rank order,
+    stable inside each, out-of-block columns dropped, local columns; and the
+    chunk validation (first bad position, dimensions)."""
+    import ctypes
+
+    from paper_1406_1066_b200.assembly import _ptr
+    from paper_1406_1066_b200.distributed import partition_torch
+
+    rng = np.random.default_rng(world)
+    L, n = 70_001, 5_000
+    ii = rng.integers(1, 900, size=L).astype(np.int32)
+    jj = rng.integers(1, n + 1, size=L).astype(np.int32)
+    s = rng.standard_normal(L)
+    cuts = sorted(rng.choice(np.arange(1, n), size=world - 1, replace=False).tolist())
+    bounds = [0] + cuts + [n]
+    dev = torch.device("cuda", 0)
+    a = sa.default_assembler(0)
+    a._bind_stream()
+
+    def run(ii, jj, m, nn):
+        ti, tj, ts = (torch.from_numpy(x).to(dev) for x in (ii, jj, s))
+        outs = [torch.empty(L, dtype=dt, device=dev) for dt in (torch.int32, torch.int32, torch.float64)]
+        hb = (ctypes.c_int32 * (world + 1))(*bounds)
+        hc = (ctypes.c_int64 * world)()
+        bp, bw = ctypes.c_int64(-1), ctypes.c_int(-1)
+        rc = a.lib.sa_partition(a.ctx, _ptr(ti), _ptr(tj), _ptr(ts), 1, L, m, nn, world, hb,
+                                *(_ptr(x) for x in outs), hc, ctypes.byref(bp), ctypes.byref(bw))
+        return rc, outs, [hc[r] for r in range(world)], bp.value, bw.value
+
+    rc, outs, counts, _, _ = run(ii, jj, 900, n)
+    assert rc == 0
+    ref, rcounts = partition_torch(torch.from_numpy(ii), torch.from_numpy(jj), torch.from_numpy(s),
+                                   bounds, world)
+    k = sum(rcounts)
+    assert counts == rcounts and k == L
+    assert torch.equal(outs[0][:k].cpu(), ref[0]) and torch.equal(outs[1][:k].cpu(), ref[1])
+    assert outs[2][:k].cpu().numpy().tobytes() == ref[2].numpy().tobytes()
+    bad = jj.copy()
+    bad[[10, 20_000]] = 0
+    rc, _, _, bp, bw = run(ii, bad, 900, n)
+    assert rc != 0 and bp == 10 and bw == 1  # SA_WHICH_COL
+    rc, _, _, _, _ = run(ii, jj, 500, n)  # rows above M
+    assert rc != 0
+
+
+def test_sharded_path_one_rank_nccl():
+    """assemble_sharded through the CUDA partition / NCCL exchange / CUDA
+    local assembly (world 1 on the one GPU) == the oracle."""
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_1406_1066_b200 import workloads as W
+    from paper_1406_1066_b200.distributed import assemble_sharded, gpu_local_assembler
+
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        w = W.fem3d(7)
+        dev = torch.device("cuda", 0)
+        res = assemble_sharded(w.ii.to(dev), w.jj.to(dev), w.s.to(dev), w.m, w.n, gpu_local_assembler(0))
+        ref = O.assemble_counting(w.ii.numpy(), w.jj.numpy(), w.s.numpy(), w.m, w.n)
+        assert res.col_lo == 0 and res.col_hi == w.n and res.nnz_total == ref.nnz
+        assert np.array_equal(res.jc.cpu().numpy(), ref.jc)
+        assert np.array_equal(res.ir.cpu().numpy(), ref.ir)
+        assert res.pr.cpu().numpy().tobytes() == ref.pr.tobytes()
+        with pytest.raises(sa.BadIndex):
+            bad = w.jj.clone()
+            bad[5] = 0
+            assemble_sharded(w.ii.to(dev), bad.to(dev), w.s.to(dev), w.m, w.n, gpu_local_assembler(0))
+    finally:
+        dist.destroy_process_group()
