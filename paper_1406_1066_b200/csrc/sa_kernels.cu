@@ -435,6 +435,22 @@ __device__ __forceinline__ void run_lengths(const int (&j)[CPT], const bool (&v)
     }
 }
 
+// The same runs as bit masks over the CPT slots: bit k of `heads` starts a
+// run of valid triplets, and a head's run length is the distance to the next
+// set bit of `stops` (a new run or an invalid slot, or the end).
+struct Runs {
+    unsigned heads, stops;
+};
+__device__ __forceinline__ Runs run_masks(const int (&j)[CPT], unsigned vmask) {
+    unsigned eq = 0;
+#pragma unroll
+    for (int k = 1; k < CPT; ++k)
+        if (j[k] == j[k - 1]) eq |= 1u << k;
+    eq &= vmask & (vmask << 1);
+    return Runs{vmask & ~eq, ~eq | (1u << CPT)};
+}
+__device__ __forceinline__ int run_len(const Runs &r, int k) { return __ffs(r.stops >> (k + 1)); }
+
 __device__ __forceinline__ bool run_head(const int (&j)[CPT], const bool (&v)[CPT], int k) {
     return !(k > 0 && v[k > 0 ? k - 1 : 0] && j[k > 0 ? k - 1 : 0] == j[k]);
 }
@@ -591,24 +607,36 @@ __global__ void __launch_bounds__(AGG_NT) k_colcount_win(const int32_t *__restri
         for (int k = 0; k < CPT; ++k) j[k] = jn[k];
         if (ch + gridDim.x < nchunk)  // prefetch the next chunk while this one is counted
             load_run(jj, (ch + gridDim.x) * CHUNK + (int64_t)tid * CPT, L, vec, jn, 0x7fffffff);
-        bool vk[CPT];
-        int len[CPT];
+        // validity: one min/max over the run; per-slot checks only when needed
+        unsigned vmask = (1u << CPT) - 1;
+        {
+            int lo = j[0], hi = j[0];
 #pragma unroll
-        for (int k = 0; k < CPT; ++k) {
-            const bool live = t0 + k < L;
-            if (live && j[k] < 1) bad = min(bad, (unsigned long long)(t0 + k));
-            if (live && j[k] > N) over = 1;
-            vk[k] = live && j[k] >= 1 && j[k] <= N;
+            for (int k = 1; k < CPT; ++k) {
+                lo = min(lo, j[k]);
+                hi = max(hi, j[k]);
+            }
+            if (lo < 1 || hi > N || t0 + CPT > L) {
+                vmask = 0;
+#pragma unroll
+                for (int k = 0; k < CPT; ++k) {
+                    const bool live = t0 + k < L;
+                    if (live && j[k] < 1) bad = min(bad, (unsigned long long)(t0 + k));
+                    if (live && j[k] > N) over = 1;
+                    if (live && j[k] >= 1 && j[k] <= N) vmask |= 1u << k;
+                }
+            }
         }
-        run_lengths(j, vk, len);
+        const Runs R = run_masks(j, vmask);
 #pragma unroll
         for (int k = 0; k < CPT; ++k) {
-            if (vk[k] && run_head(j, vk, k)) {
+            if (R.heads & (1u << k)) {
+                const int len = run_len(R, k);
                 const unsigned b = (unsigned)(j[k] - 1 - cb);
                 if (b < (unsigned)WB) {
-                    if (atomicAdd(&W.bin[b], (uint32_t)len[k]) == 0u) W.used[atomicAdd(&W.nused, 1)] = (int)b;
+                    if (atomicAdd(&W.bin[b], (uint32_t)len) == 0u) W.used[atomicAdd(&W.nused, 1)] = (int)b;
                 } else {
-                    atomicAdd(&cnt[j[k] - 1], (uint32_t)len[k]);
+                    atomicAdd(&cnt[j[k] - 1], (uint32_t)len);
                 }
             }
         }
@@ -731,28 +759,40 @@ __global__ void __launch_bounds__(AGG_NT) k_scatter(const int32_t *__restrict__ 
             load_run(ii, t1, L, vec, in_, 1);
             load_run(jj, t1, L, vec, jn, 0);
         }
-        bool vk[CPT];
-        int len[CPT], hk[CPT], rk[CPT];
+        // validity: min/max over the run; per-slot checks only when needed
+        unsigned vmask = (1u << CPT) - 1;
+        {
+            int jlo = j[0], jhi = j[0], ilo = i[0], ihi = i[0];
 #pragma unroll
-        for (int k = 0; k < CPT; ++k) {
-            const bool live = t0 + k < L;
-            if (live && i[k] < 1) bad = min(bad, (unsigned long long)(t0 + k));
-            if (live && i[k] > M) over = 1;
-            vk[k] = live && j[k] >= 1 && j[k] <= N;
+            for (int k = 1; k < CPT; ++k) {
+                jlo = min(jlo, j[k]);
+                jhi = max(jhi, j[k]);
+                ilo = min(ilo, i[k]);
+                ihi = max(ihi, i[k]);
+            }
+            if (jlo < 1 || jhi > N || ilo < 1 || ihi > M || t0 + CPT > L) {
+                vmask = 0;
+#pragma unroll
+                for (int k = 0; k < CPT; ++k) {
+                    const bool live = t0 + k < L;
+                    if (live && i[k] < 1) bad = min(bad, (unsigned long long)(t0 + k));
+                    if (live && i[k] > M) over = 1;
+                    if (live && j[k] >= 1 && j[k] <= N) vmask |= 1u << k;
+                }
+            }
         }
-        run_lengths(j, vk, len);
+        const Runs R = run_masks(j, vmask);
+        int hk[CPT], rk[CPT];
 #pragma unroll
         for (int k = 0; k < CPT; ++k) {
             hk[k] = -1;
             rk[k] = 0;
-            if (vk[k]) {
-                if (run_head(j, vk, k)) {
-                    hk[k] = agg_insert(A, j[k] - 1);
-                    rk[k] = atomicAdd(&A.ctr[hk[k]], len[k]);
-                } else {
-                    hk[k] = hk[k > 0 ? k - 1 : 0];
-                    rk[k] = rk[k > 0 ? k - 1 : 0] + 1;
-                }
+            if (R.heads & (1u << k)) {
+                hk[k] = agg_insert(A, j[k] - 1);
+                rk[k] = atomicAdd(&A.ctr[hk[k]], run_len(R, k));
+            } else if (vmask & (1u << k)) {  // continues the run of slot k-1
+                hk[k] = hk[k > 0 ? k - 1 : 0];
+                rk[k] = rk[k > 0 ? k - 1 : 0] + 1;
             }
         }
         __syncthreads();
