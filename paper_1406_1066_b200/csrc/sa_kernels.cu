@@ -918,29 +918,41 @@ __global__ void __launch_bounds__(AGG_NT, 4) k_scatter_win(const int32_t *__rest
             load_run(ii, t1, L, vec, in_, 1);
             load_run(jj, t1, L, vec, jn, 0);
         }
-        bool vk[CPT];
-        int len[CPT];
-        uint32_t rk[CPT];
+        unsigned vmask = (1u << CPT) - 1;
+        {
+            int jlo = j[0], jhi = j[0], ilo = i[0], ihi = i[0];
 #pragma unroll
-        for (int k = 0; k < CPT; ++k) {
-            const bool live = t0 + k < L;
-            if (live && i[k] < 1) bad = min(bad, (unsigned long long)(t0 + k));
-            if (live && i[k] > M) over = 1;
-            vk[k] = live && j[k] >= 1 && j[k] <= N;
+            for (int k = 1; k < CPT; ++k) {
+                jlo = min(jlo, j[k]);
+                jhi = max(jhi, j[k]);
+                ilo = min(ilo, i[k]);
+                ihi = max(ihi, i[k]);
+            }
+            if (jlo < 1 || jhi > N || ilo < 1 || ihi > M || t0 + CPT > L) {
+                vmask = 0;
+#pragma unroll
+                for (int k = 0; k < CPT; ++k) {
+                    const bool live = t0 + k < L;
+                    if (live && i[k] < 1) bad = min(bad, (unsigned long long)(t0 + k));
+                    if (live && i[k] > M) over = 1;
+                    if (live && j[k] >= 1 && j[k] <= N) vmask |= 1u << k;
+                }
+            }
         }
-        run_lengths(j, vk, len);
+        const Runs R = run_masks(j, vmask);
+        uint32_t rk[CPT];
         // heads: rank inside the window bin, or (outside the window) the
         // global cursor word itself
 #pragma unroll
         for (int k = 0; k < CPT; ++k) {
             rk[k] = 0;
-            if (vk[k] && run_head(j, vk, k)) {
+            if (R.heads & (1u << k)) {
                 const unsigned b = (unsigned)(j[k] - 1 - cb);
                 if (b < (unsigned)WB) {
-                    rk[k] = atomicAdd(&W.bin[b], (uint32_t)len[k]);
+                    rk[k] = atomicAdd(&W.bin[b], (uint32_t)run_len(R, k));
                     if (rk[k] == 0u) W.used[atomicAdd(&W.nused, 1)] = (int)b;
                 } else {
-                    rk[k] = atomicAdd(&cur[j[k] - 1], (uint32_t)len[k]);
+                    rk[k] = atomicAdd(&cur[j[k] - 1], (uint32_t)run_len(R, k));
                 }
             }
         }
@@ -954,8 +966,8 @@ __global__ void __launch_bounds__(AGG_NT, 4) k_scatter_win(const int32_t *__rest
         uint32_t slot = 0;
 #pragma unroll
         for (int k = 0; k < CPT; ++k) {
-            if (!vk[k]) continue;
-            if (run_head(j, vk, k)) {
+            if (!(vmask & (1u << k))) continue;
+            if (R.heads & (1u << k)) {
                 const unsigned b = (unsigned)(j[k] - 1 - cb);
                 const uint32_t w = (b < (unsigned)WB) ? W.bin[b] + rk[k] : rk[k];
                 slot = (w & POSMASK) + ((w & BIGFLAG) ? lsmall : 0u);
