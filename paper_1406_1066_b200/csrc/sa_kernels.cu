@@ -1024,86 +1024,140 @@ cudaError_t launch_scatter(Launch &lc, const int32_t *ii, const int32_t *jj, int
 // key buffer, value bits in the other buffer, at index = run number;
 // bigu[c] = runs | (BIGFLAG if keys ended in buffer B).
 // ---------------------------------------------------------------------------
-constexpr int BIG_NT = 256;
+constexpr int BIG_NT = 1024;
+constexpr int BIG_NW = BIG_NT / 32;
+
+// One stable LSD radix pass (8-bit digit at `shift`) of n keys src -> dst by
+// one CTA: every warp owns a contiguous segment; per-warp digit counts, one
+// block scan over (digit, warp), then each warp places its segment in order
+// (match.any ranks + a warp-private running counter per digit) -- no block
+// barrier inside the loops.
+__device__ __forceinline__ void big_radix_pass(const unsigned long long *src,
+                                               unsigned long long *dst, int64_t n, int shift,
+                                               uint32_t (*s_cnt)[256], uint32_t *s_warp) {
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const unsigned lt = lanemask_lt();
+    for (int k = tid; k < BIG_NW * 256; k += BIG_NT) (&s_cnt[0][0])[k] = 0;
+    __syncthreads();
+    const int64_t lo = (int64_t)w * n / BIG_NW, hi = (int64_t)(w + 1) * n / BIG_NW;
+    for (int64_t p = lo + lane; p < hi; p += 32) atomicAdd(&s_cnt[w][(src[p] >> shift) & 255], 1u);
+    __syncthreads();
+    {  // digit-major exclusive scan: thread t owns entries 8t .. 8t+7 of (digit, warp)
+        uint32_t v[8], sum = 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int q = 8 * tid + k;
+            v[k] = s_cnt[q % BIG_NW][q / BIG_NW];
+            sum += v[k];
+        }
+        uint32_t tot;
+        uint32_t pre = block_excl_sum<BIG_NT, uint32_t>(sum, s_warp, tot);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int q = 8 * tid + k;
+            s_cnt[q % BIG_NW][q / BIG_NW] = pre;
+            pre += v[k];
+        }
+    }
+    __syncthreads();
+    for (int64_t b0 = lo; b0 < hi; b0 += 32) {
+        const int64_t p = b0 + lane;
+        const bool valid = p < hi;
+        const unsigned long long key = valid ? src[p] : 0ull;
+        const int d = valid ? (int)((key >> shift) & 255) : 256;
+        const unsigned peers = __match_any_sync(FULL, d);
+        const uint32_t base = valid ? s_cnt[w][d] : 0u;
+        if (valid) dst[base + __popc(peers & lt)] = key;
+        __syncwarp();
+        if (valid && (peers & lt) == 0u) s_cnt[w][d] = base + __popc(peers);
+        __syncwarp();
+    }
+    __syncthreads();
+}
 
 __global__ void __launch_bounds__(BIG_NT) k_bigcol(BigCol *__restrict__ big_list,
                                                    const ErrState *err, int4 *rec,
                                                    const uint2 *__restrict__ perm,
                                                    const double *__restrict__ s, int64_t s_stride,
                                                    int idx_bits, int passes) {
-    __shared__ uint32_t s_hist[256];
-    __shared__ uint32_t s_bin[256];
-    __shared__ uint16_t s_wcnt[BIG_NT / 32][257];
-    __shared__ uint32_t s_warp[BIG_NT / 32];
+    __shared__ uint32_t s_cnt[BIG_NW][256];
+    __shared__ uint32_t s_warp[BIG_NW];
     __shared__ unsigned long long s_prevrow;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int tid = threadIdx.x;
     pdl_wait();
     pdl_trigger();
     const unsigned nbig = *((volatile const unsigned *)&err->nbig);
     if (blockIdx.x >= nbig) return;
     const unsigned lsmall = *((volatile const unsigned *)&err->lsmall);
-    for (int k = tid; k < (BIG_NT / 32) * 257; k += BIG_NT) (&s_wcnt[0][0])[k] = 0;
-    __syncthreads();
     const unsigned long long idx_mask = (1ull << idx_bits) - 1;
     for (unsigned kb = blockIdx.x; kb < nbig; kb += gridDim.x) {
         const uint32_t st = big_list[kb].start + lsmall;
         const int64_t n = big_list[kb].n;
         unsigned long long *A = reinterpret_cast<unsigned long long *>(rec + st);
         unsigned long long *B = A + n;
-        // entries {row, position} -> keys in A
-        for (int64_t p = tid; p < n; p += BIG_NT) {
-            const uint2 e = perm[st + p];
-            A[p] = ((unsigned long long)(e.x - 1u) << idx_bits) | e.y;
+        // entries {row, position} -> keys in A (8 loads per thread in flight)
+        for (int64_t p0 = 0; p0 < n; p0 += 8 * BIG_NT) {
+            uint2 e[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int64_t p = p0 + u * BIG_NT + tid;
+                e[u] = (p < n) ? perm[st + p] : make_uint2(0u, 0u);
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int64_t p = p0 + u * BIG_NT + tid;
+                if (p < n) A[p] = ((unsigned long long)(e[u].x - 1u) << idx_bits) | e[u].y;
+            }
         }
         __syncthreads();
         unsigned long long *src = A, *dst = B;
         for (int ps = 0; ps < passes; ++ps) {
-            const int shift = 8 * ps;
-            for (int k = tid; k < 256; k += BIG_NT) s_hist[k] = 0;
-            __syncthreads();
-            for (int64_t p = tid; p < n; p += BIG_NT) atomicAdd(&s_hist[(src[p] >> shift) & 255], 1u);
-            __syncthreads();
-            {
-                uint32_t tot;
-                uint32_t v = s_hist[tid];
-                uint32_t pre = block_excl_sum<BIG_NT, uint32_t>(v, s_warp, tot);
-                s_bin[tid] = pre;
-            }
-            __syncthreads();
-            for (int64_t base = 0; base < n; base += BIG_NT) {
-                const int64_t p = base + tid;
-                const bool valid = p < n;
-                const unsigned long long key = valid ? src[p] : 0ull;
-                const int d = valid ? (int)((key >> shift) & 255) : 256;
-                const unsigned peers = __match_any_sync(FULL, d);
-                const int leader = __ffs(peers) - 1;
-                const int wrank = __popc(peers & lanemask_lt());
-                if (lane == leader) s_wcnt[warp][d] = (uint16_t)__popc(peers);
-                __syncthreads();
-                if (valid) {
-                    uint32_t pre = s_bin[d];
-                    for (int w2 = 0; w2 < warp; ++w2) pre += s_wcnt[w2][d];
-                    dst[pre + wrank] = key;
-                }
-                __syncthreads();
-                if (lane == leader) {
-                    if (valid) atomicAdd(&s_bin[d], (uint32_t)__popc(peers));
-                    s_wcnt[warp][d] = 0;
-                }
-                __syncthreads();
-            }
+            big_radix_pass(src, dst, n, 8 * ps, s_cnt, s_warp);
             unsigned long long *tmp = src;
             src = dst;
             dst = tmp;
         }
-        // gather values in sorted order into the other buffer
-        for (int64_t p = tid; p < n; p += BIG_NT) {
-            const unsigned long long idx = src[p] & idx_mask;
-            dst[p] = (unsigned long long)__double_as_longlong(s[idx * s_stride]);
+        // gather values in sorted order into the other buffer (8 in flight)
+        for (int64_t p0 = 0; p0 < n; p0 += 8 * BIG_NT) {
+            double v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int64_t p = p0 + u * BIG_NT + tid;
+                v[u] = (p < n) ? s[(src[p] & idx_mask) * s_stride] : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int64_t p = p0 + u * BIG_NT + tid;
+                if (p < n) dst[p] = (unsigned long long)__double_as_longlong(v[u]);
+            }
         }
+        __syncthreads();
+        // ordered fold of runs of equal rows, all runs at once: thread t folds
+        // the runs whose head lies in its segment (a run may extend past it);
+        // the result lands at the run's head (row in src, value in dst)
+        {
+            const int64_t lo = (int64_t)tid * n / BIG_NT, hi = (int64_t)(tid + 1) * n / BIG_NT;
+            int64_t p = lo;
+            while (p < hi) {
+                const unsigned long long row = src[p] >> idx_bits;
+                if (p > 0 && (src[p - 1] >> idx_bits) == row) {  // not a head: skip to the next one
+                    ++p;
+                    continue;
+                }
+                double acc = fold_add(0.0, __longlong_as_double((long long)dst[p]));
+                int64_t q = p + 1;
+                while (q < n && (src[q] >> idx_bits) == row) {
+                    acc = fold_add(acc, __longlong_as_double((long long)dst[q]));
+                    ++q;
+                }
+                dst[p] = (unsigned long long)__double_as_longlong(acc);
+                p = q;
+            }
+        }
+        __syncthreads();
         if (tid == 0) s_prevrow = ~0ull;
         __syncthreads();
-        // ordered fold of runs of equal rows
+        // compact the heads to [0, runs) in order
         uint32_t carry = 0;
         for (int64_t base = 0; base < n; base += BIG_NT) {
             const int64_t p = base + tid;
@@ -1112,36 +1166,15 @@ __global__ void __launch_bounds__(BIG_NT) k_bigcol(BigCol *__restrict__ big_list
             const unsigned long long prev =
                 (tid == 0) ? s_prevrow : (valid ? (src[p - 1] >> idx_bits) : 0ull);
             const bool head = valid && row != prev;
+            const unsigned long long val = head ? dst[p] : 0ull;
             uint32_t tot;
-            uint32_t run = block_excl_sum<BIG_NT, uint32_t>(head ? 1u : 0u, s_warp, tot) + carry;
-            double acc = 0.0;
-            if (head) {
-                int64_t q = p;
-                bool more = true;
-                while (more) {
-                    unsigned long long kk[8], vv[8];
-#pragma unroll
-                    for (int u = 0; u < 8; ++u) {
-                        const bool in = q + u < n;
-                        kk[u] = in ? src[q + u] : ~0ull;
-                        vv[u] = in ? dst[q + u] : 0ull;
-                    }
-#pragma unroll
-                    for (int u = 0; u < 8; ++u) {
-                        if (more && (kk[u] >> idx_bits) == row)
-                            acc = fold_add(acc, __longlong_as_double((long long)vv[u]));
-                        else
-                            more = false;
-                    }
-                    q += 8;
-                }
-            }
+            const uint32_t run = block_excl_sum<BIG_NT, uint32_t>(head ? 1u : 0u, s_warp, tot) + carry;
             if (p == base + BIG_NT - 1 && valid) s_prevrow = row;
             if (!valid && tid == BIG_NT - 1) s_prevrow = row;
-            __syncthreads();
+            __syncthreads();  // the chunk is read before any of it is overwritten
             if (head) {
                 src[run] = row;  // row - 1 (key stores row-1)
-                dst[run] = (unsigned long long)__double_as_longlong(acc);
+                dst[run] = val;
             }
             carry += tot;
             __syncthreads();

@@ -684,6 +684,12 @@ __global__ void __launch_bounds__(NT, 5) k_tile_fold(const uint32_t *__restrict_
 
     // ---- column pointers and, in tiles with a big column, all outputs per thread
     bool over = false;
+    // big columns are copied by the whole CTA below: (tile-local output base,
+    // big-list index) pairs in the (now free) long-column lists
+    int *bcopy = &S.lcol[0][0];
+    constexpr int BCAP = (int)(sizeof(S.lcol) / (2 * sizeof(int)));
+    if (tid == 0) S.ncls[0] = 0;
+    __syncthreads();
     {
         long long o = P + tbase;
         for (int c = k_lo; c < k_hi; ++c) {
@@ -691,17 +697,24 @@ __global__ void __launch_bounds__(NT, 5) k_tile_fold(const uint32_t *__restrict_
             const uint32_t w0 = cs[c];
             const int s0 = (int)(w0 & POSMASK), s1 = (int)(cs[c + 1] & POSMASK);
             if (w0 & BIGFLAG) {
-                const BigCol bc = big_list[bigk[c_a + c]];
+                const uint32_t kb = bigk[c_a + c];
+                const BigCol bc = big_list[kb];
                 const int ub = (int)(bc.u & POSMASK);
-                const unsigned long long *RR = reinterpret_cast<const unsigned long long *>(rec + bc.start);
-                const unsigned long long *BK = (bc.u & BIGFLAG) ? RR + bc.n : RR;
-                const unsigned long long *BV = (bc.u & BIGFLAG) ? RR : RR + bc.n;
-                for (int e = 0; e < ub; ++e) {
-                    if (o + e < cap) {
-                        ir[o + e] = (int32_t)BK[e];
-                        pr[o + e] = __longlong_as_double((long long)BV[e]);
-                    } else {
-                        over = true;
+                const int e = atomicAdd(&S.ncls[0], 1);
+                if (e < BCAP) {
+                    bcopy[2 * e] = (int)(o - P);
+                    bcopy[2 * e + 1] = (int)kb;
+                } else {  // (more big columns in one tile than list slots) copy alone
+                    const unsigned long long *RR = reinterpret_cast<const unsigned long long *>(rec + bc.start);
+                    const unsigned long long *BK = (bc.u & BIGFLAG) ? RR + bc.n : RR;
+                    const unsigned long long *BV = (bc.u & BIGFLAG) ? RR : RR + bc.n;
+                    for (int q = 0; q < ub; ++q) {
+                        if (o + q < cap) {
+                            ir[o + q] = (int32_t)BK[q];
+                            pr[o + q] = __longlong_as_double((long long)BV[q]);
+                        } else {
+                            over = true;
+                        }
                     }
                 }
                 o += ub;
@@ -721,6 +734,38 @@ __global__ void __launch_bounds__(NT, 5) k_tile_fold(const uint32_t *__restrict_
                     }
                 }
                 o += u;
+            }
+        }
+    }
+    __syncthreads();
+    {  // the tile's big columns, each copied by all threads
+        const int nb = min(S.ncls[0], BCAP);
+        for (int e = 0; e < nb; ++e) {
+            const long long o = P + bcopy[2 * e];
+            const BigCol bc = big_list[bcopy[2 * e + 1]];
+            const int ub = (int)(bc.u & POSMASK);
+            const unsigned long long *RR = reinterpret_cast<const unsigned long long *>(rec + bc.start);
+            const unsigned long long *BK = (bc.u & BIGFLAG) ? RR + bc.n : RR;
+            const unsigned long long *BV = (bc.u & BIGFLAG) ? RR : RR + bc.n;
+            for (int q0 = 0; q0 < ub; q0 += 8 * NT) {  // 8 loads per thread in flight
+                unsigned long long kk[8], vv[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int q = q0 + u * NT + tid;
+                    kk[u] = (q < ub) ? BK[q] : 0ull;
+                    vv[u] = (q < ub) ? BV[q] : 0ull;
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int q = q0 + u * NT + tid;
+                    if (q >= ub) continue;
+                    if (o + q < cap) {
+                        ir[o + q] = (int32_t)kk[u];
+                        pr[o + q] = __longlong_as_double((long long)vv[u]);
+                    } else {
+                        over = true;
+                    }
+                }
             }
         }
     }
