@@ -112,6 +112,22 @@ int sa_assemble_async(sa_ctx *ctx, const int32_t *d_ii, const int32_t *d_jj,
                       int32_t *d_jc, int32_t *d_ir, double *d_pr, int64_t cap);
 
 /*
+ * The same pipeline over up to 3 input segments read in place and
+ * concatenated in order (input positions, which order the duplicate fold,
+ * run through the segments one after the other) -- the sharded path: a
+ * rank's own chunk, in place, between the triplets received from lower and
+ * from higher ranks.  Columns are j - col_lo; columns outside [1, N] are
+ * another rank's and are skipped (the chunks were validated by
+ * sa_partition).  Per segment: d_ii[g], d_jj[g] (int32), d_s[g] (float64,
+ * s_stride[g] 0 or 1), len[g].
+ */
+int sa_assemble_segments_async(sa_ctx *ctx, int nseg, const int32_t *const *d_ii,
+                               const int32_t *const *d_jj, const double *const *d_s,
+                               const int64_t *s_stride, const int64_t *len, int32_t col_lo,
+                               int32_t M, int32_t N, int32_t *d_jc, int32_t *d_ir, double *d_pr,
+                               int64_t cap);
+
+/*
  * Synchronise the stream and report the outcome of the last
  * sa_assemble_async: *nnz, and for SA_ERR_BAD_INDEX *bad_pos / *bad_which.
  */
@@ -164,15 +180,17 @@ int sa_prune_zeros(sa_ctx *ctx, const int32_t *d_jc, const int32_t *d_ir, const 
  * Multi-GPU column-block sharding (one process per GPU).  sa_partition
  * groups a rank's triplets by destination rank -- the owner of the column,
  * h_bounds[r] <= j-1 < h_bounds[r+1] for r < world (<= 8) -- into the arrays
- * d_ii_out, d_jj_out (j - h_bounds[dest], 1-based inside the block), d_s_out
- * (capacity L each): destinations in rank order, input order inside each
- * (stable), ready for the all-to-all and for sa_assemble_async on the
- * receiver.  The chunk is validated on the way: SA_ERR_BAD_INDEX with
- * *bad_pos (chunk-local) / *bad_which, SA_ERR_DIM_TOO_SMALL for indices
- * above the global M / N.  Synchronous; h_counts[r] = triplets for rank r.
+ * d_ii_out, d_jj_out (global columns), d_s_out (capacity L each):
+ * destinations in rank order, input order inside each (stable).  The
+ * triplets of rank `self` (>= 0) are counted but not written: they stay in
+ * place and the rank's assembly reads them there
+ * (sa_assemble_segments_async); self = -1 writes every destination.  The
+ * chunk is validated on the way: SA_ERR_BAD_INDEX with *bad_pos
+ * (chunk-local) / *bad_which, SA_ERR_DIM_TOO_SMALL for indices above the
+ * global M / N.  Synchronous; h_counts[r] = triplets for rank r.
  */
 int sa_partition(sa_ctx *ctx, const int32_t *d_ii, const int32_t *d_jj, const double *d_s,
-                 int64_t s_stride, int64_t L, int32_t M, int32_t N, int32_t world,
+                 int64_t s_stride, int64_t L, int32_t M, int32_t N, int32_t world, int32_t self,
                  const int32_t *h_bounds, int32_t *d_ii_out, int32_t *d_jj_out, double *d_s_out,
                  int64_t *h_counts, int64_t *bad_pos, int *bad_which);
 

@@ -53,8 +53,11 @@ SIGNATURES = {
     "sa_host_assemble": (_int, [_vp, _i32, _i32, _pi64, _pi64, _pint]),
     "sa_host_fetch": (_int, [_vp, _vp, _vp, _vp]),
     "sa_prune_zeros": (_int, [_vp, _vp, _vp, _vp, _i32, _i64, _vp, _vp, _vp, _pi64]),
-    "sa_partition": (_int, [_vp, _vp, _vp, _vp, _i64, _i64, _i32, _i32, _i32, ctypes.POINTER(_i32),
+    "sa_partition": (_int, [_vp, _vp, _vp, _vp, _i64, _i64, _i32, _i32, _i32, _i32, ctypes.POINTER(_i32),
                             _vp, _vp, _vp, _pi64, _pi64, _pint]),
+    "sa_assemble_segments_async": (_int, [_vp, _int, ctypes.POINTER(_vp), ctypes.POINTER(_vp),
+                                          ctypes.POINTER(_vp), _pi64, _pi64, _i32, _i32, _i32, _vp,
+                                          _vp, _vp, _i64]),
     "sa_last_launch_count": (_int, [_vp]),
     "sa_enable_timing": (_int, [_vp, _int]),
     "sa_host_buffer": (_vp, [ctypes.c_uint64]),

@@ -2,6 +2,7 @@
 // launch sequencing and error mapping.  No torch types cross this boundary.
 
 #include <algorithm>
+#include <cstdint>
 #include <cstdio>
 #include <cstring>
 #include <map>
@@ -367,16 +368,11 @@ int sa_infer_dims(sa_ctx *ctx, const int32_t *d_ii, const int32_t *d_jj, int64_t
     return decode(ctx, e, nullptr, bad_pos, bad_which);
 }
 
-int sa_assemble_async(sa_ctx *ctx, const int32_t *d_ii, const int32_t *d_jj, const double *d_s,
-                      int64_t s_stride, int64_t L, int32_t M, int32_t N, int32_t *d_jc,
+namespace {
+
+// The assembly pipeline over a segment table (Ltot triplets in total).
+int assemble_segments(sa_ctx *ctx, const Segs &S, int64_t L, int32_t M, int32_t N, int32_t *d_jc,
                       int32_t *d_ir, double *d_pr, int64_t cap) {
-    if (!ctx) return SA_ERR_INVALID_ARG;
-    if (L < 0 || M < 0 || N < 0 || cap < 0 || !d_jc || (s_stride != 0 && s_stride != 1))
-        return fail(ctx, SA_ERR_INVALID_ARG, "sa_assemble_async: bad arguments");
-    if (L > 0 && (!d_ii || !d_jj || !d_s))
-        return fail(ctx, SA_ERR_INVALID_ARG, "sa_assemble_async: null triplet pointer");
-    if (L > (int64_t)POSMASK)
-        return fail(ctx, SA_ERR_INVALID_ARG, "sa_assemble_async: more than 2^31-1 triplets");
     SA_CUDA(ctx, cudaSetDevice(ctx->device));
     Launch lc{ctx->stream, ctx->num_sms, 0};
 
@@ -387,7 +383,9 @@ int sa_assemble_async(sa_ctx *ctx, const int32_t *d_ii, const int32_t *d_jj, con
         if (rc) return rc;
         // L > 0 with N == 0: validation only; every valid column index then
         // exceeds N and k_hist flags DimensionTooSmall (no histogram writes)
-        if (L > 0) SA_CUDA(ctx, launch_hist(lc, d_ii, d_jj, L, M, N, ctx->cur, ctx->err, false));
+        if (L > 0 && !S.skip_foreign)
+            for (int g = 0; g < S.nseg; ++g)
+                SA_CUDA(ctx, launch_hist(lc, S.ii[g], S.jj[g], S.len[g], M, N, ctx->cur, ctx->err, false));
         SA_CUDA(ctx, cudaMemsetAsync(d_jc, 0, ((size_t)N + 1) * sizeof(int32_t), ctx->stream));
         ctx->launches = lc.launches;
         return SA_OK;
@@ -413,30 +411,96 @@ int sa_assemble_async(sa_ctx *ctx, const int32_t *d_ii, const int32_t *d_jj, con
     rc = launch_init(ctx, lc, N, ntiles, nscan);
     if (rc) return rc;
     if ((rc = mark(ctx, "k_colcount"))) return rc;
-    SA_CUDA(ctx, launch_colcount(lc, d_jj, L, N, ctx->cur, ctx->err));
+    SA_CUDA(ctx, launch_colcount(lc, S, N, ctx->cur, ctx->err));
     if ((rc = mark(ctx, "k_col_scan"))) return rc;
     SA_CUDA(ctx, launch_col_scan(lc, ctx->cur, ctx->sstart, ctx->cur, N, ctx->tile_info,
                                  ctx->tile_big, ntiles, ctx->big_list, ctx->bigk, ctx->scan_state,
                                  ctx->perm, ctx->err));
     if ((rc = mark(ctx, "k_scatter"))) return rc;
-    SA_CUDA(ctx, launch_scatter(lc, d_ii, d_jj, L, M, N, ctx->cur, ctx->perm, ctx->err));
+    SA_CUDA(ctx, launch_scatter(lc, S, M, N, ctx->cur, ctx->perm, ctx->err));
     if (L > BIGCOL) {
         const int idx_bits = std::max(1, bits_for((uint64_t)(L - 1)));
         const int row_bits = bits_for((uint64_t)(M > 0 ? M - 1 : 0));
         const int passes = std::max(1, (idx_bits + row_bits + 7) / 8);
         if ((rc = mark(ctx, "k_bigcol"))) return rc;
-        SA_CUDA(ctx, launch_bigcol(lc, ctx->big_list, ctx->err, ctx->rec, ctx->perm, d_s, s_stride,
-                                   idx_bits,
+        SA_CUDA(ctx, launch_bigcol(lc, ctx->big_list, ctx->err, ctx->rec, ctx->perm, S, idx_bits,
                                    passes));
     }
     if ((rc = mark(ctx, "k_tile_fold"))) return rc;
     SA_CUDA(ctx, launch_tile_fold(lc, ctx->sstart, ctx->tile_info, ctx->tile_big, ntiles,
-                                  reinterpret_cast<const int2 *>(ctx->perm), d_s, s_stride, ctx->rec,
+                                  reinterpret_cast<const int2 *>(ctx->perm), S, ctx->rec,
                                   ctx->big_list, ctx->bigk, ctx->tile_state, N, d_jc, d_ir, d_pr,
                                   cap, ctx->err));
     if ((rc = mark(ctx, nullptr))) return rc;
     ctx->launches = lc.launches;
     return SA_OK;
+}
+
+bool aligned16p(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+// Segment table; false if a segment is malformed.
+bool make_segs(int nseg, const int32_t *const *ii, const int32_t *const *jj,
+               const double *const *s, const int64_t *s_stride, const int64_t *len, int32_t col_lo,
+               int skip_foreign, Segs &S, int64_t &total) {
+    constexpr int64_t CH = 2048;  // = CHUNK of sa_kernels.cu
+    S = Segs{};
+    S.nseg = nseg;
+    S.col_lo = col_lo;
+    S.skip_foreign = skip_foreign;
+    total = 0;
+    int64_t ch = 0;
+    for (int g = 0; g < nseg; ++g) {
+        if (len[g] < 0 || (s_stride[g] != 0 && s_stride[g] != 1)) return false;
+        if (len[g] > 0 && (!ii[g] || !jj[g] || !s[g])) return false;
+        S.ii[g] = ii[g];
+        S.jj[g] = jj[g];
+        S.s[g] = s[g];
+        S.stride[g] = s_stride[g];
+        S.len[g] = len[g];
+        S.pos0[g] = total;
+        S.ch0[g] = ch;
+        S.vec[g] = aligned16p(ii[g]) && aligned16p(jj[g]);
+        total += len[g];
+        ch += (len[g] + CH - 1) / CH;
+    }
+    S.ch0[nseg] = ch;
+    return true;
+}
+
+}  // namespace
+
+int sa_assemble_async(sa_ctx *ctx, const int32_t *d_ii, const int32_t *d_jj, const double *d_s,
+                      int64_t s_stride, int64_t L, int32_t M, int32_t N, int32_t *d_jc,
+                      int32_t *d_ir, double *d_pr, int64_t cap) {
+    if (!ctx) return SA_ERR_INVALID_ARG;
+    if (L < 0 || M < 0 || N < 0 || cap < 0 || !d_jc || (s_stride != 0 && s_stride != 1))
+        return fail(ctx, SA_ERR_INVALID_ARG, "sa_assemble_async: bad arguments");
+    if (L > 0 && (!d_ii || !d_jj || !d_s))
+        return fail(ctx, SA_ERR_INVALID_ARG, "sa_assemble_async: null triplet pointer");
+    if (L > (int64_t)POSMASK)
+        return fail(ctx, SA_ERR_INVALID_ARG, "sa_assemble_async: more than 2^31-1 triplets");
+    Segs S;
+    int64_t total = 0;
+    make_segs(1, &d_ii, &d_jj, &d_s, &s_stride, &L, 0, 0, S, total);
+    return assemble_segments(ctx, S, L, M, N, d_jc, d_ir, d_pr, cap);
+}
+
+int sa_assemble_segments_async(sa_ctx *ctx, int nseg, const int32_t *const *d_ii,
+                               const int32_t *const *d_jj, const double *const *d_s,
+                               const int64_t *s_stride, const int64_t *len, int32_t col_lo,
+                               int32_t M, int32_t N, int32_t *d_jc, int32_t *d_ir, double *d_pr,
+                               int64_t cap) {
+    if (!ctx) return SA_ERR_INVALID_ARG;
+    if (nseg < 1 || nseg > MAXSEG || !d_ii || !d_jj || !d_s || !s_stride || !len || M < 0 ||
+        N < 0 || col_lo < 0 || cap < 0 || !d_jc)
+        return fail(ctx, SA_ERR_INVALID_ARG, "sa_assemble_segments_async: bad arguments");
+    Segs S;
+    int64_t total = 0;
+    if (!make_segs(nseg, d_ii, d_jj, d_s, s_stride, len, col_lo, 1, S, total))
+        return fail(ctx, SA_ERR_INVALID_ARG, "sa_assemble_segments_async: bad segment");
+    if (total > (int64_t)POSMASK)
+        return fail(ctx, SA_ERR_INVALID_ARG, "sa_assemble_segments_async: more than 2^31-1 triplets");
+    return assemble_segments(ctx, S, total, M, N, d_jc, d_ir, d_pr, cap);
 }
 
 int sa_finish(sa_ctx *ctx, int64_t *nnz, int64_t *bad_pos, int *bad_which) {
@@ -534,11 +598,12 @@ int sa_prune_zeros(sa_ctx *ctx, const int32_t *d_jc, const int32_t *d_ir, const 
 }
 
 int sa_partition(sa_ctx *ctx, const int32_t *d_ii, const int32_t *d_jj, const double *d_s,
-                 int64_t s_stride, int64_t L, int32_t M, int32_t N, int32_t world,
+                 int64_t s_stride, int64_t L, int32_t M, int32_t N, int32_t world, int32_t self,
                  const int32_t *h_bounds, int32_t *d_ii_out, int32_t *d_jj_out, double *d_s_out,
                  int64_t *h_counts, int64_t *bad_pos, int *bad_which) {
     if (!ctx) return SA_ERR_INVALID_ARG;
-    if (L < 0 || M < 0 || N < 0 || world < 1 || world > 8 || !h_bounds || !h_counts ||
+    if (L < 0 || M < 0 || N < 0 || world < 1 || world > 8 || self < -1 || self >= world ||
+        !h_bounds || !h_counts ||
         (s_stride != 0 && s_stride != 1) ||
         (L > 0 && (!d_ii || !d_jj || !d_s || !d_ii_out || !d_jj_out || !d_s_out)))
         return fail(ctx, SA_ERR_INVALID_ARG, "sa_partition: bad arguments");
@@ -551,7 +616,7 @@ int sa_partition(sa_ctx *ctx, const int32_t *d_ii, const int32_t *d_jj, const do
     if (!ctx->pt_counts) SA_CUDA(ctx, cudaMalloc(reinterpret_cast<void **>(&ctx->pt_counts), 16 * sizeof(int64_t)));
     int rc = launch_init(ctx, lc, 0, 0, 0);  // error state
     if (rc) return rc;
-    SA_CUDA(ctx, launch_partition(lc, d_ii, d_jj, d_s, s_stride, L, world, h_bounds, ctx->pt_cnt,
+    SA_CUDA(ctx, launch_partition(lc, d_ii, d_jj, d_s, s_stride, L, world, self, h_bounds, ctx->pt_cnt,
                                   ctx->pt_off, ctx->pt_counts, d_ii_out, d_jj_out, d_s_out, ctx->pt_chk,
                                   ctx->err));
     int64_t h[16];

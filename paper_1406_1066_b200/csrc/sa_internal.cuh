@@ -38,6 +38,33 @@ struct BigCol {
     uint32_t u;       // unique rows (after k_bigcol) | BIGFLAG if keys ended in buffer B
 };
 
+// The triplet input: up to MAXSEG segments read in place, concatenated in
+// order (sa_assemble_segments_async; one segment for sa_assemble_async).
+// A triplet's input position = pos0 of its segment + its index there.
+constexpr int MAXSEG = 3;
+struct Segs {
+    const int32_t *ii[MAXSEG];
+    const int32_t *jj[MAXSEG];
+    const double *s[MAXSEG];
+    int64_t stride[MAXSEG];   // value stride (0: one value broadcast)
+    int64_t len[MAXSEG];
+    int64_t pos0[MAXSEG];     // global position of the first triplet
+    int64_t ch0[MAXSEG + 1];  // first CHUNK of each segment; ch0[nseg] = chunks in total
+    int vec[MAXSEG];          // ii and jj 16-byte aligned
+    int nseg;
+    int col_lo;               // columns are j - col_lo
+    int skip_foreign;         // columns outside [1, N] are another rank's: skipped, not errors
+};
+
+// Address of the value of input position p.
+__device__ __forceinline__ const double *seg_value(const Segs &S, int64_t p) {
+    const double *v = S.s[0] + (p - S.pos0[0]) * S.stride[0];
+#pragma unroll
+    for (int q = 1; q < MAXSEG; ++q)
+        if (q < S.nseg && p >= S.pos0[q]) v = S.s[q] + (p - S.pos0[q]) * S.stride[q];
+    return v;
+}
+
 // Device-side outcome of one assembly (zeroed / reset before every call).
 struct ErrState {
     unsigned long long bad_i;   // first row index < 1 (or invalid raw value)
@@ -307,16 +334,14 @@ cudaError_t launch_col_scan(Launch &lc, const uint32_t *cnt, uint32_t *sstart, u
                             int32_t N, int2 *tile_info, uint8_t *tile_big,
                             int64_t ntiles, BigCol *big_list, uint32_t *bigk,
                             unsigned long long *scan_state, uint2 *perm, ErrState *err);
-cudaError_t launch_colcount(Launch &lc, const int32_t *jj, int64_t L, int32_t N, uint32_t *cnt,
-                            ErrState *err);
-cudaError_t launch_scatter(Launch &lc, const int32_t *ii, const int32_t *jj, int64_t L, int32_t M,
-                           int32_t N, uint32_t *cur, uint2 *perm, ErrState *err);
+cudaError_t launch_colcount(Launch &lc, const Segs &S, int32_t N, uint32_t *cnt, ErrState *err);
+cudaError_t launch_scatter(Launch &lc, const Segs &S, int32_t M, int32_t N, uint32_t *cur,
+                           uint2 *perm, ErrState *err);
 cudaError_t launch_bigcol(Launch &lc, BigCol *big_list, const ErrState *err, int4 *rec,
-                          const uint2 *perm, const double *s, int64_t s_stride, int idx_bits,
-                          int passes);
+                          const uint2 *perm, const Segs &S, int idx_bits, int passes);
 cudaError_t launch_tile_fold(Launch &lc, const uint32_t *sstart, const int2 *tile_info,
                              const uint8_t *tile_big, int64_t ntiles, const int2 *entries,
-                             const double *s, int64_t s_stride, const int4 *rec,
+                             const Segs &S, const int4 *rec,
                              const BigCol *big_list, const uint32_t *bigk,
                              unsigned long long *tile_state, int32_t N, int32_t *jc, int32_t *ir,
                              double *pr, int64_t cap, ErrState *err);
@@ -326,7 +351,7 @@ cudaError_t launch_prune(Launch &lc, const int32_t *jc, const int32_t *ir, const
                          double *pr_out, unsigned long long *state, long long *nnz_out);
 int64_t prune_tiles(int64_t nnz);
 cudaError_t launch_partition(Launch &lc, const int32_t *ii, const int32_t *jj, const double *s,
-                             int64_t s_stride, int64_t L, int world, const int32_t *bounds,
+                             int64_t s_stride, int64_t L, int world, int self, const int32_t *bounds,
                              int32_t *tile_cnt, int64_t *tile_off, int64_t *counts,
                              int32_t *out_i, int32_t *out_j, double *out_s, void *checks,
                              ErrState *err);

@@ -351,17 +351,40 @@ cudaError_t launch_col_scan(Launch &lc, const uint32_t *cnt, uint32_t *sstart, u
 }
 
 // ---------------------------------------------------------------------------
-// CTA-scope column aggregation shared by k_colcount and k_scatter.  A CTA
-// takes CHUNK consecutive triplets (CPT per thread, loaded with 16-byte
-// vector loads) and counts their columns in a shared-memory hash (open
-// addressing, HT slots, list of used slots so only those are visited again).
-// Element-ordered FEM input touches ~CHUNK/9 distinct columns per chunk, so
-// global atomics drop by an order of magnitude and stay independent.
+// The triplet input of an assembly: up to MAXSEG segments read in place, in
+// order (one segment on one GPU; a rank's own chunk between the triplets
+// received from lower and from higher ranks in the sharded path).  A CTA
+// takes CHUNK consecutive triplets of one segment (CPT per thread, 16-byte
+// vector loads, the next chunk in flight in registers).  The input position
+// of a triplet -- its order for the duplicate fold -- is the segment's pos0
+// plus its index.  Columns are j - col_lo; with skip_foreign, columns
+// outside [1, N] belong to another rank and are skipped, not errors.
 // ---------------------------------------------------------------------------
 constexpr int AGG_NT = 256;
 constexpr int CPT = 8;
 constexpr int CHUNK = AGG_NT * CPT;
 constexpr int HT = 2 * CHUNK;
+
+struct SegChunk {  // one chunk of one segment
+    const int32_t *ii, *jj;
+    int64_t t0;    // segment-local index of the chunk's first triplet
+    int64_t len;   // segment length
+    int64_t pos0;  // global position of the segment's first triplet
+    int vec;
+};
+
+__device__ __forceinline__ SegChunk seg_chunk(const Segs &S, int64_t ch) {
+    int g = 0;
+#pragma unroll
+    for (int q = 1; q < MAXSEG; ++q)
+        if (q < S.nseg && ch >= S.ch0[q]) g = q;
+    SegChunk c{S.ii[0], S.jj[0], 0, S.len[0], S.pos0[0], S.vec[0]};
+#pragma unroll
+    for (int q = 1; q < MAXSEG; ++q)
+        if (q == g) c = SegChunk{S.ii[q], S.jj[q], 0, S.len[q], S.pos0[q], S.vec[q]};
+    c.t0 = (ch - (g == 0 ? 0 : (g == 1 ? S.ch0[1] : S.ch0[2]))) * CHUNK;
+    return c;
+}
 
 struct AggSmem {
     int key[HT];        // column + 1 (0 = empty)
@@ -421,23 +444,10 @@ __device__ __forceinline__ void load_run(const int32_t *__restrict__ p, int64_t 
 
 // Runs of equal columns inside a thread's CPT consecutive triplets (FEM
 // element order emits each column 3-4 times in a row): only a run's head
-// touches the shared-memory hash, with the run length.  len[k] = triplets
-// from k to the end of its run.
-__device__ __forceinline__ void run_lengths(const int (&j)[CPT], const bool (&v)[CPT],
-                                            int (&len)[CPT]) {
-    int run = 0;
-#pragma unroll
-    for (int k = CPT - 1; k >= 0; --k) {
-        const bool cont = (k + 1 < CPT) && v[k] && v[k < CPT - 1 ? k + 1 : k] &&
-                          j[k < CPT - 1 ? k + 1 : k] == j[k];
-        run = v[k] ? (cont ? run + 1 : 1) : 0;
-        len[k] = run;
-    }
-}
-
-// The same runs as bit masks over the CPT slots: bit k of `heads` starts a
-// run of valid triplets, and a head's run length is the distance to the next
-// set bit of `stops` (a new run or an invalid slot, or the end).
+// touches the shared-memory aggregation, with the run length.  Bit k of
+// `heads` starts a run of valid triplets; a head's run length is the
+// distance to the next set bit of `stops` (a new run, an invalid slot, or
+// the end).
 struct Runs {
     unsigned heads, stops;
 };
@@ -451,141 +461,51 @@ __device__ __forceinline__ Runs run_masks(const int (&j)[CPT], unsigned vmask) {
 }
 __device__ __forceinline__ int run_len(const Runs &r, int k) { return __ffs(r.stops >> (k + 1)); }
 
-__device__ __forceinline__ bool run_head(const int (&j)[CPT], const bool (&v)[CPT], int k) {
-    return !(k > 0 && v[k > 0 ? k - 1 : 0] && j[k > 0 ? k - 1 : 0] == j[k]);
-}
-
-// ---------------------------------------------------------------------------
-// k_colcount: column histogram of the assembly path (reads jj only; rows
-// are validated by k_scatter, which reads them anyway).
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(AGG_NT) k_colcount(const int32_t *__restrict__ jj, int64_t L,
-                                                     int32_t N, uint32_t *__restrict__ cnt,
-                                                     ErrState *err, int vec) {
-    __shared__ AggSmem A;
-    const int tid = threadIdx.x;
-    for (int k = tid; k < HT; k += AGG_NT) {
-        A.key[k] = 0;
-        A.ctr[k] = 0;
+// Column validity of a thread's run (relabelled columns): one min/max test,
+// per-slot checks only when something is off.  Out-of-range columns are
+// errors (first bad position, over_n) unless skip_foreign.
+__device__ __forceinline__ unsigned column_mask(const int (&j)[CPT], int64_t t0, int64_t len,
+                                               int64_t pos0, int32_t N, bool skip_foreign,
+                                               unsigned long long &bad, unsigned &over) {
+    int lo = j[0], hi = j[0];
+#pragma unroll
+    for (int k = 1; k < CPT; ++k) {
+        lo = min(lo, j[k]);
+        hi = max(hi, j[k]);
     }
-    if (tid == 0) A.nused = 0;
-    __syncthreads();
-    unsigned long long bad = ~0ull;
-    unsigned over = 0;
-    const int64_t nchunk = (L + CHUNK - 1) / CHUNK;
-    int jn[CPT];
-    if ((int64_t)blockIdx.x < nchunk)
-        load_run(jj, (int64_t)blockIdx.x * CHUNK + (int64_t)tid * CPT, L, vec, jn, 0x7fffffff);
-    for (int64_t ch = blockIdx.x; ch < nchunk; ch += gridDim.x) {
-        const int64_t t0 = ch * CHUNK + (int64_t)tid * CPT;
-        int j[CPT];
+    if (lo >= 1 && hi <= N && t0 + CPT <= len) return (1u << CPT) - 1;
+    unsigned vmask = 0;
 #pragma unroll
-        for (int k = 0; k < CPT; ++k) j[k] = jn[k];
-        if (ch + gridDim.x < nchunk)  // prefetch the next chunk while this one is counted
-            load_run(jj, (ch + gridDim.x) * CHUNK + (int64_t)tid * CPT, L, vec, jn, 0x7fffffff);
-        bool vk[CPT];
-        int len[CPT];
-#pragma unroll
-        for (int k = 0; k < CPT; ++k) {
-            const bool live = t0 + k < L;
-            if (live && j[k] < 1) bad = min(bad, (unsigned long long)(t0 + k));
+    for (int k = 0; k < CPT; ++k) {
+        const bool live = t0 + k < len;
+        if (!skip_foreign) {
+            if (live && j[k] < 1) bad = min(bad, (unsigned long long)(pos0 + t0 + k));
             if (live && j[k] > N) over = 1;
-            vk[k] = live && j[k] >= 1 && j[k] <= N;
         }
-        run_lengths(j, vk, len);
-#pragma unroll
-        for (int k = 0; k < CPT; ++k) {
-            if (vk[k] && run_head(j, vk, k)) {
-                const int h = agg_insert(A, j[k] - 1);
-                atomicAdd(&A.ctr[h], len[k]);
-            }
-        }
-        __syncthreads();
-        const int nu = A.nused;
-        for (int e = tid; e < nu; e += AGG_NT) {
-            const int h = A.used[e];
-            atomicAdd(&cnt[A.key[h] - 1], (uint32_t)A.ctr[h]);
-            A.key[h] = 0;
-            A.ctr[h] = 0;
-        }
-        __syncthreads();
-        if (tid == 0) A.nused = 0;
-        __syncthreads();
+        if (live && j[k] >= 1 && j[k] <= N) vmask |= 1u << k;
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        bad = min(bad, __shfl_xor_sync(FULL, bad, o));
-        over |= __shfl_xor_sync(FULL, over, o);
-    }
-    if ((tid & 31) == 0) {
-        if (bad != ~0ull) atomicMin(&err->bad_j, bad);
-        if (over) err->over_n = 1;
-    }
-}
-
-// Direct variant: each column run (per thread, CPT consecutive triplets)
-// issues one global reduction, with no shared-memory aggregation.
-__global__ void __launch_bounds__(AGG_NT) k_colcount_direct(const int32_t *__restrict__ jj,
-                                                            int64_t L, int32_t N,
-                                                            uint32_t *__restrict__ cnt,
-                                                            ErrState *err, int vec) {
-    unsigned long long bad = ~0ull;
-    unsigned over = 0;
-    const int64_t nrun = (L + CPT - 1) / CPT;
-    for (int64_t r = (int64_t)blockIdx.x * AGG_NT + threadIdx.x; r < nrun;
-         r += (int64_t)gridDim.x * AGG_NT) {
-        const int64_t t0 = r * CPT;
-        int j[CPT];
-        load_run(jj, t0, L, vec, j, 0x7fffffff);
-        bool vk[CPT];
-        int len[CPT];
-#pragma unroll
-        for (int k = 0; k < CPT; ++k) {
-            const bool live = t0 + k < L;
-            if (live && j[k] < 1) bad = min(bad, (unsigned long long)(t0 + k));
-            if (live && j[k] > N) over = 1;
-            vk[k] = live && j[k] >= 1 && j[k] <= N;
-        }
-        run_lengths(j, vk, len);
-#pragma unroll
-        for (int k = 0; k < CPT; ++k)
-            if (vk[k] && run_head(j, vk, k)) atomicAdd(&cnt[j[k] - 1], (uint32_t)len[k]);
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        bad = min(bad, __shfl_xor_sync(FULL, bad, o));
-        over |= __shfl_xor_sync(FULL, over, o);
-    }
-    if ((threadIdx.x & 31) == 0) {
-        if (bad != ~0ull) atomicMin(&err->bad_j, bad);
-        if (over) err->over_n = 1;
-    }
+    return vmask;
 }
 
 // ---------------------------------------------------------------------------
-// Window aggregation (k_colcount_win, k_scatter_win).  A CTA takes CHUNK
-// consecutive triplets; element-ordered input keeps a chunk's columns near
-// the chunk's first column, so the column runs (per thread) count into a
-// directly indexed shared-memory window of WB bins around it (one shared
-// atomic per run, no hashing).  The first touch of a bin lists it; after
-// the chunk, every listed bin issues one global atomic.  Columns outside
-// the window go to global memory directly.
+// k_colcount_win: column histogram + column-index validation.  Runs count
+// into a directly indexed shared-memory window of WB columns around the
+// chunk's first column (one shared atomic per run, no hashing); the first
+// touch of a window column lists it, and after the chunk every listed column
+// issues one global atomic.  Columns outside the window go to global memory
+// directly.
 // ---------------------------------------------------------------------------
 constexpr int WB = 8192;
 
 struct WinSmem {
-    uint32_t bin[WB];      // per window column: triplets of the chunk, then the cursor word
+    uint32_t bin[WB];      // per window column: triplets of the chunk
     int used[CHUNK];       // listed bins
     int nused;
 };
 
-__device__ __forceinline__ int window_base(const int32_t *__restrict__ jj, int64_t t) {
-    return __ldg(jj + t) - 1 - WB / 2;
-}
-
-__global__ void __launch_bounds__(AGG_NT) k_colcount_win(const int32_t *__restrict__ jj, int64_t L,
-                                                         int32_t N, uint32_t *__restrict__ cnt,
-                                                         ErrState *err, int vec) {
+__global__ void __launch_bounds__(AGG_NT) k_colcount_win(Segs S, int32_t N,
+                                                         uint32_t *__restrict__ cnt,
+                                                         ErrState *err) {
     __shared__ WinSmem W;
     const int tid = threadIdx.x;
     for (int k = tid; k < WB; k += AGG_NT) W.bin[k] = 0;
@@ -595,38 +515,25 @@ __global__ void __launch_bounds__(AGG_NT) k_colcount_win(const int32_t *__restri
     pdl_trigger();
     unsigned long long bad = ~0ull;
     unsigned over = 0;
-    const int64_t nchunk = (L + CHUNK - 1) / CHUNK;
+    const int64_t nchunk = S.ch0[S.nseg];
+    const bool skip = S.skip_foreign != 0;
     int jn[CPT];
-    if ((int64_t)blockIdx.x < nchunk)
-        load_run(jj, (int64_t)blockIdx.x * CHUNK + (int64_t)tid * CPT, L, vec, jn, 0x7fffffff);
+    if ((int64_t)blockIdx.x < nchunk) {
+        const SegChunk c = seg_chunk(S, blockIdx.x);
+        load_run(c.jj, c.t0 + (int64_t)tid * CPT, c.len, c.vec, jn, 0x7fffffff);
+    }
     for (int64_t ch = blockIdx.x; ch < nchunk; ch += gridDim.x) {
-        const int64_t t0 = ch * CHUNK + (int64_t)tid * CPT;
-        const int cb = window_base(jj, ch * CHUNK);
+        const SegChunk c = seg_chunk(S, ch);
+        const int64_t t0 = c.t0 + (int64_t)tid * CPT;
+        const int cb = __ldg(c.jj + c.t0) - S.col_lo - 1 - WB / 2;  // window base
         int j[CPT];
 #pragma unroll
-        for (int k = 0; k < CPT; ++k) j[k] = jn[k];
-        if (ch + gridDim.x < nchunk)  // prefetch the next chunk while this one is counted
-            load_run(jj, (ch + gridDim.x) * CHUNK + (int64_t)tid * CPT, L, vec, jn, 0x7fffffff);
-        // validity: one min/max over the run; per-slot checks only when needed
-        unsigned vmask = (1u << CPT) - 1;
-        {
-            int lo = j[0], hi = j[0];
-#pragma unroll
-            for (int k = 1; k < CPT; ++k) {
-                lo = min(lo, j[k]);
-                hi = max(hi, j[k]);
-            }
-            if (lo < 1 || hi > N || t0 + CPT > L) {
-                vmask = 0;
-#pragma unroll
-                for (int k = 0; k < CPT; ++k) {
-                    const bool live = t0 + k < L;
-                    if (live && j[k] < 1) bad = min(bad, (unsigned long long)(t0 + k));
-                    if (live && j[k] > N) over = 1;
-                    if (live && j[k] >= 1 && j[k] <= N) vmask |= 1u << k;
-                }
-            }
+        for (int k = 0; k < CPT; ++k) j[k] = jn[k] - S.col_lo;
+        if (ch + gridDim.x < nchunk) {  // prefetch the next chunk while this one is counted
+            const SegChunk cn = seg_chunk(S, ch + gridDim.x);
+            load_run(cn.jj, cn.t0 + (int64_t)tid * CPT, cn.len, cn.vec, jn, 0x7fffffff);
         }
+        const unsigned vmask = column_mask(j, t0, c.len, c.pos0, N, skip, bad, over);
         const Runs R = run_masks(j, vmask);
 #pragma unroll
         for (int k = 0; k < CPT; ++k) {
@@ -662,8 +569,6 @@ __global__ void __launch_bounds__(AGG_NT) k_colcount_win(const int32_t *__restri
     }
 }
 
-// Aggregation variants (measured on cfg2/cfg3/cfg4), chosen
-// by SA_COLCOUNT_MODE / SA_SCATTER_MODE = 0 direct, 1 hash, 2 window.
 bool pdl_enabled() {
     static int m = -1;
     if (m < 0) {
@@ -673,59 +578,28 @@ bool pdl_enabled() {
     return m == 1;
 }
 
-static int env_mode(const char *name, int dflt) {
-    const char *e = getenv(name);
-    return (e && e[0] >= '0' && e[0] <= '2') ? e[0] - '0' : dflt;
-}
-// 0 direct, 1 shared-memory hash, 2 shared-memory window
-static int colcount_mode() {
-    static int m = -1;
-    if (m < 0) m = env_mode("SA_COLCOUNT_MODE", 2);
-    return m;
-}
-static int scatter_mode() {
-    static int m = -1;
-    if (m < 0) m = env_mode("SA_SCATTER_MODE", 1);
-    return m;
-}
-
-cudaError_t launch_colcount(Launch &lc, const int32_t *jj, int64_t L, int32_t N, uint32_t *cnt,
-                            ErrState *err) {
-    if (L <= 0) return cudaSuccess;
-    const int vec = aligned16(jj);
-    const int64_t nchunk = (L + CHUNK - 1) / CHUNK;
-    int grid = (int)std::min<int64_t>(nchunk, (int64_t)lc.num_sms * 4);
-    if (colcount_mode() == 1) {
-        k_colcount<<<grid, AGG_NT, 0, lc.stream>>>(jj, L, N, cnt, err, vec);
-    } else if (colcount_mode() == 2) {
-        cudaError_t e = launch_pdl(k_colcount_win, dim3(grid), dim3(AGG_NT), 0, lc.stream, jj, L, N, cnt,
-                                   err, vec);
-        if (e != cudaSuccess) return e;
-    } else {
-        const int64_t want = ((L + CPT - 1) / CPT + AGG_NT - 1) / AGG_NT;
-        const int g = (int)std::min<int64_t>(want, (int64_t)lc.num_sms * 8);
-        k_colcount_direct<<<g, AGG_NT, 0, lc.stream>>>(jj, L, N, cnt, err, vec);
-    }
+cudaError_t launch_colcount(Launch &lc, const Segs &S, int32_t N, uint32_t *cnt, ErrState *err) {
+    const int64_t nchunk = S.ch0[S.nseg];
+    if (nchunk <= 0) return cudaSuccess;
+    const int grid = (int)std::min<int64_t>(nchunk, (int64_t)lc.num_sms * 4);
+    cudaError_t e = launch_pdl(k_colcount_win, dim3(grid), dim3(AGG_NT), 0, lc.stream, S, N, cnt, err);
     lc.launches++;
-    return cudaGetLastError();
+    return e;
 }
 
 // ---------------------------------------------------------------------------
-// k_scatter: counting-sort scatter by column of 8-byte entries {row,
-// input position} (the fold gathers the values by position, so the 8-byte
-// values are read once, by the fold).  Per chunk: (1) each column run gets
-// chunk-local slots from a shared-memory counter, (2) one global atomicAdd
-// per distinct column reserves the chunk's slots on the column cursor, (3)
-// entries are written.  Row indices are validated here for every triplet
-// (first bad position, rows above M).  The slot order inside a column is
-// arbitrary; the fold restores input order from the position.
+// k_scatter: counting-sort scatter by column of 8-byte entries {row, input
+// position} (the fold gathers the values by position, so the 8-byte values
+// are read once, by the fold).  Per chunk: (1) each column run gets
+// chunk-local slots from a shared-memory hash counter, (2) one global
+// atomicAdd per distinct column reserves the chunk's slots on the column
+// cursor, (3) entries are written.  Row indices are validated here for every
+// triplet (first bad position, rows above M).  The slot order inside a
+// column is arbitrary; the fold restores input order from the position.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(AGG_NT) k_scatter(const int32_t *__restrict__ ii,
-                                                    const int32_t *__restrict__ jj, int64_t L,
-                                                    int32_t M, int32_t N,
+__global__ void __launch_bounds__(AGG_NT) k_scatter(Segs S, int32_t M, int32_t N,
                                                     uint32_t *__restrict__ cur,
-                                                    uint2 *__restrict__ perm, int vec,
-                                                    ErrState *err) {
+                                                    uint2 *__restrict__ perm, ErrState *err) {
     __shared__ AggSmem A;
     const int tid = threadIdx.x;
     for (int k = tid; k < HT; k += AGG_NT) {
@@ -737,50 +611,49 @@ __global__ void __launch_bounds__(AGG_NT) k_scatter(const int32_t *__restrict__ 
     pdl_wait();
     pdl_trigger();
     const uint32_t lsmall = err->lsmall;
-    unsigned long long bad = ~0ull;
-    unsigned over = 0;
-    const int64_t nchunk = (L + CHUNK - 1) / CHUNK;
+    unsigned long long bad = ~0ull, badj = ~0ull;
+    unsigned over = 0, overj = 0;
+    const int64_t nchunk = S.ch0[S.nseg];
+    const bool skip = S.skip_foreign != 0;
     int in_[CPT], jn[CPT];
     if ((int64_t)blockIdx.x < nchunk) {
-        const int64_t t0 = (int64_t)blockIdx.x * CHUNK + (int64_t)tid * CPT;
-        load_run(ii, t0, L, vec, in_, 1);
-        load_run(jj, t0, L, vec, jn, 0);
+        const SegChunk c = seg_chunk(S, blockIdx.x);
+        const int64_t t0 = c.t0 + (int64_t)tid * CPT;
+        load_run(c.ii, t0, c.len, c.vec, in_, 1);
+        load_run(c.jj, t0, c.len, c.vec, jn, 0);
     }
     for (int64_t ch = blockIdx.x; ch < nchunk; ch += gridDim.x) {
-        const int64_t t0 = ch * CHUNK + (int64_t)tid * CPT;
+        const SegChunk c = seg_chunk(S, ch);
+        const int64_t t0 = c.t0 + (int64_t)tid * CPT;
         int i[CPT], j[CPT];
 #pragma unroll
         for (int k = 0; k < CPT; ++k) {
             i[k] = in_[k];
-            j[k] = jn[k];
+            j[k] = jn[k] - S.col_lo;
         }
         if (ch + gridDim.x < nchunk) {  // next chunk in flight
-            const int64_t t1 = (ch + gridDim.x) * CHUNK + (int64_t)tid * CPT;
-            load_run(ii, t1, L, vec, in_, 1);
-            load_run(jj, t1, L, vec, jn, 0);
+            const SegChunk cn = seg_chunk(S, ch + gridDim.x);
+            const int64_t t1 = cn.t0 + (int64_t)tid * CPT;
+            load_run(cn.ii, t1, cn.len, cn.vec, in_, 1);
+            load_run(cn.jj, t1, cn.len, cn.vec, jn, 0);
         }
-        // validity: min/max over the run; per-slot checks only when needed
-        unsigned vmask = (1u << CPT) - 1;
-        {
-            int jlo = j[0], jhi = j[0], ilo = i[0], ihi = i[0];
+        {  // rows: one min/max test, per-slot checks only when needed
+            int ilo = i[0], ihi = i[0];
 #pragma unroll
             for (int k = 1; k < CPT; ++k) {
-                jlo = min(jlo, j[k]);
-                jhi = max(jhi, j[k]);
                 ilo = min(ilo, i[k]);
                 ihi = max(ihi, i[k]);
             }
-            if (jlo < 1 || jhi > N || ilo < 1 || ihi > M || t0 + CPT > L) {
-                vmask = 0;
+            if (ilo < 1 || ihi > M || t0 + CPT > c.len) {
 #pragma unroll
                 for (int k = 0; k < CPT; ++k) {
-                    const bool live = t0 + k < L;
-                    if (live && i[k] < 1) bad = min(bad, (unsigned long long)(t0 + k));
+                    const bool live = t0 + k < c.len;
+                    if (live && i[k] < 1) bad = min(bad, (unsigned long long)(c.pos0 + t0 + k));
                     if (live && i[k] > M) over = 1;
-                    if (live && j[k] >= 1 && j[k] <= N) vmask |= 1u << k;
                 }
             }
         }
+        const unsigned vmask = column_mask(j, t0, c.len, c.pos0, N, true, badj, overj);
         const Runs R = run_masks(j, vmask);
         int hk[CPT], rk[CPT];
 #pragma unroll
@@ -807,7 +680,7 @@ __global__ void __launch_bounds__(AGG_NT) k_scatter(const int32_t *__restrict__ 
             if (hk[k] < 0) continue;
             const uint32_t bw = (uint32_t)A.ctr[hk[k]];
             const uint32_t pos = (bw & POSMASK) + ((bw & BIGFLAG) ? lsmall : 0u) + (uint32_t)rk[k];
-            perm[pos] = make_uint2((uint32_t)i[k], (uint32_t)(t0 + k));
+            perm[pos] = make_uint2((uint32_t)i[k], (uint32_t)(c.pos0 + t0 + k));
         }
         __syncthreads();
         for (int e = tid; e < nu; e += AGG_NT) {
@@ -818,6 +691,7 @@ __global__ void __launch_bounds__(AGG_NT) k_scatter(const int32_t *__restrict__ 
         if (tid == 0) A.nused = 0;
         __syncthreads();
     }
+    (void)skip;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         bad = min(bad, __shfl_xor_sync(FULL, bad, o));
@@ -829,188 +703,14 @@ __global__ void __launch_bounds__(AGG_NT) k_scatter(const int32_t *__restrict__ 
     }
 }
 
-// Direct variant: one global cursor reservation (atomicAdd with return) per
-// column run; all of a thread's reservations are in flight together.
-__global__ void __launch_bounds__(AGG_NT) k_scatter_direct(const int32_t *__restrict__ ii,
-                                                           const int32_t *__restrict__ jj,
-                                                           int64_t L, int32_t M, int32_t N,
-                                                           uint32_t *__restrict__ cur,
-                                                           uint2 *__restrict__ perm, int vec,
-                                                           ErrState *err) {
-    const uint32_t lsmall = err->lsmall;
-    unsigned long long bad = ~0ull;
-    unsigned over = 0;
-    const int64_t nrun = (L + CPT - 1) / CPT;
-    for (int64_t r = (int64_t)blockIdx.x * AGG_NT + threadIdx.x; r < nrun;
-         r += (int64_t)gridDim.x * AGG_NT) {
-        const int64_t t0 = r * CPT;
-        int i[CPT], j[CPT];
-        load_run(ii, t0, L, vec, i, 1);
-        load_run(jj, t0, L, vec, j, 0);
-        bool vk[CPT];
-        int len[CPT];
-#pragma unroll
-        for (int k = 0; k < CPT; ++k) {
-            const bool live = t0 + k < L;
-            if (live && i[k] < 1) bad = min(bad, (unsigned long long)(t0 + k));
-            if (live && i[k] > M) over = 1;
-            vk[k] = live && j[k] >= 1 && j[k] <= N;
-        }
-        run_lengths(j, vk, len);
-        uint32_t w[CPT];
-#pragma unroll
-        for (int k = 0; k < CPT; ++k) {
-            w[k] = 0;
-            if (vk[k] && run_head(j, vk, k)) w[k] = atomicAdd(&cur[j[k] - 1], (uint32_t)len[k]);
-        }
-        uint32_t slot = 0;
-#pragma unroll
-        for (int k = 0; k < CPT; ++k) {
-            if (!vk[k]) continue;
-            if (run_head(j, vk, k)) slot = (w[k] & POSMASK) + ((w[k] & BIGFLAG) ? lsmall : 0u);
-            else slot += 1;
-            perm[slot] = make_uint2((uint32_t)i[k], (uint32_t)(t0 + k));
-        }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        bad = min(bad, __shfl_xor_sync(FULL, bad, o));
-        over |= __shfl_xor_sync(FULL, over, o);
-    }
-    if ((threadIdx.x & 31) == 0) {
-        if (bad != ~0ull) atomicMin(&err->bad_i, bad);
-        if (over) err->over_m = 1;
-    }
-}
-
-__global__ void __launch_bounds__(AGG_NT, 4) k_scatter_win(const int32_t *__restrict__ ii,
-                                                        const int32_t *__restrict__ jj, int64_t L,
-                                                        int32_t M, int32_t N,
-                                                        uint32_t *__restrict__ cur,
-                                                        uint2 *__restrict__ perm, int vec,
-                                                        ErrState *err) {
-    __shared__ WinSmem W;
-    const int tid = threadIdx.x;
-    for (int k = tid; k < WB; k += AGG_NT) W.bin[k] = 0;
-    if (tid == 0) W.nused = 0;
-    __syncthreads();
-    const uint32_t lsmall = err->lsmall;
-    unsigned long long bad = ~0ull;
-    unsigned over = 0;
-    const int64_t nchunk = (L + CHUNK - 1) / CHUNK;
-    int in_[CPT], jn[CPT];
-    if ((int64_t)blockIdx.x < nchunk) {
-        const int64_t t0 = (int64_t)blockIdx.x * CHUNK + (int64_t)tid * CPT;
-        load_run(ii, t0, L, vec, in_, 1);
-        load_run(jj, t0, L, vec, jn, 0);
-    }
-    for (int64_t ch = blockIdx.x; ch < nchunk; ch += gridDim.x) {
-        const int64_t t0 = ch * CHUNK + (int64_t)tid * CPT;
-        const int cb = window_base(jj, ch * CHUNK);
-        int i[CPT], j[CPT];
-#pragma unroll
-        for (int k = 0; k < CPT; ++k) {
-            i[k] = in_[k];
-            j[k] = jn[k];
-        }
-        if (ch + gridDim.x < nchunk) {  // next chunk in flight
-            const int64_t t1 = (ch + gridDim.x) * CHUNK + (int64_t)tid * CPT;
-            load_run(ii, t1, L, vec, in_, 1);
-            load_run(jj, t1, L, vec, jn, 0);
-        }
-        unsigned vmask = (1u << CPT) - 1;
-        {
-            int jlo = j[0], jhi = j[0], ilo = i[0], ihi = i[0];
-#pragma unroll
-            for (int k = 1; k < CPT; ++k) {
-                jlo = min(jlo, j[k]);
-                jhi = max(jhi, j[k]);
-                ilo = min(ilo, i[k]);
-                ihi = max(ihi, i[k]);
-            }
-            if (jlo < 1 || jhi > N || ilo < 1 || ihi > M || t0 + CPT > L) {
-                vmask = 0;
-#pragma unroll
-                for (int k = 0; k < CPT; ++k) {
-                    const bool live = t0 + k < L;
-                    if (live && i[k] < 1) bad = min(bad, (unsigned long long)(t0 + k));
-                    if (live && i[k] > M) over = 1;
-                    if (live && j[k] >= 1 && j[k] <= N) vmask |= 1u << k;
-                }
-            }
-        }
-        const Runs R = run_masks(j, vmask);
-        uint32_t rk[CPT];
-        // heads: rank inside the window bin, or (outside the window) the
-        // global cursor word itself
-#pragma unroll
-        for (int k = 0; k < CPT; ++k) {
-            rk[k] = 0;
-            if (R.heads & (1u << k)) {
-                const unsigned b = (unsigned)(j[k] - 1 - cb);
-                if (b < (unsigned)WB) {
-                    rk[k] = atomicAdd(&W.bin[b], (uint32_t)run_len(R, k));
-                    if (rk[k] == 0u) W.used[atomicAdd(&W.nused, 1)] = (int)b;
-                } else {
-                    rk[k] = atomicAdd(&cur[j[k] - 1], (uint32_t)run_len(R, k));
-                }
-            }
-        }
-        __syncthreads();
-        const int nu = W.nused;
-        for (int e = tid; e < nu; e += AGG_NT) {
-            const int b = W.used[e];
-            W.bin[b] = atomicAdd(&cur[cb + b], W.bin[b]);
-        }
-        __syncthreads();
-        uint32_t slot = 0;
-#pragma unroll
-        for (int k = 0; k < CPT; ++k) {
-            if (!(vmask & (1u << k))) continue;
-            if (R.heads & (1u << k)) {
-                const unsigned b = (unsigned)(j[k] - 1 - cb);
-                const uint32_t w = (b < (unsigned)WB) ? W.bin[b] + rk[k] : rk[k];
-                slot = (w & POSMASK) + ((w & BIGFLAG) ? lsmall : 0u);
-            } else {
-                slot += 1;
-            }
-            perm[slot] = make_uint2((uint32_t)i[k], (uint32_t)(t0 + k));
-        }
-        __syncthreads();
-        for (int e = tid; e < nu; e += AGG_NT) W.bin[W.used[e]] = 0;
-        if (tid == 0) W.nused = 0;
-        __syncthreads();
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        bad = min(bad, __shfl_xor_sync(FULL, bad, o));
-        over |= __shfl_xor_sync(FULL, over, o);
-    }
-    if ((tid & 31) == 0) {
-        if (bad != ~0ull) atomicMin(&err->bad_i, bad);
-        if (over) err->over_m = 1;
-    }
-}
-
-cudaError_t launch_scatter(Launch &lc, const int32_t *ii, const int32_t *jj, int64_t L, int32_t M,
-                           int32_t N, uint32_t *cur, uint2 *perm, ErrState *err) {
-    if (L <= 0) return cudaSuccess;
-    const int vec = aligned16(ii) && aligned16(jj);
-    const int64_t nchunk = (L + CHUNK - 1) / CHUNK;
-    int grid = (int)std::min<int64_t>(nchunk, (int64_t)lc.num_sms * 4);
-    if (scatter_mode() == 1) {
-        cudaError_t e = launch_pdl(k_scatter, dim3(grid), dim3(AGG_NT), 0, lc.stream, ii, jj, L, M, N, cur,
-                                   perm, vec, err);
-        if (e != cudaSuccess) return e;
-    } else if (scatter_mode() == 2) {
-        k_scatter_win<<<grid, AGG_NT, 0, lc.stream>>>(ii, jj, L, M, N, cur, perm, vec, err);
-    } else {
-        const int64_t want = ((L + CPT - 1) / CPT + AGG_NT - 1) / AGG_NT;
-        const int g = (int)std::min<int64_t>(want, (int64_t)lc.num_sms * 8);
-        k_scatter_direct<<<g, AGG_NT, 0, lc.stream>>>(ii, jj, L, M, N, cur, perm, vec, err);
-    }
+cudaError_t launch_scatter(Launch &lc, const Segs &S, int32_t M, int32_t N, uint32_t *cur,
+                           uint2 *perm, ErrState *err) {
+    const int64_t nchunk = S.ch0[S.nseg];
+    if (nchunk <= 0) return cudaSuccess;
+    const int grid = (int)std::min<int64_t>(nchunk, (int64_t)lc.num_sms * 4);
+    cudaError_t e = launch_pdl(k_scatter, dim3(grid), dim3(AGG_NT), 0, lc.stream, S, M, N, cur, perm, err);
     lc.launches++;
-    return cudaGetLastError();
+    return e;
 }
 
 // ---------------------------------------------------------------------------
@@ -1077,8 +777,7 @@ __device__ __forceinline__ void big_radix_pass(const unsigned long long *src,
 
 __global__ void __launch_bounds__(BIG_NT) k_bigcol(BigCol *__restrict__ big_list,
                                                    const ErrState *err, int4 *rec,
-                                                   const uint2 *__restrict__ perm,
-                                                   const double *__restrict__ s, int64_t s_stride,
+                                                   const uint2 *__restrict__ perm, Segs S,
                                                    int idx_bits, int passes) {
     __shared__ uint32_t s_cnt[BIG_NW][256];
     __shared__ uint32_t s_warp[BIG_NW];
@@ -1123,7 +822,7 @@ __global__ void __launch_bounds__(BIG_NT) k_bigcol(BigCol *__restrict__ big_list
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
                 const int64_t p = p0 + u * BIG_NT + tid;
-                v[u] = (p < n) ? s[(src[p] & idx_mask) * s_stride] : 0.0;
+                v[u] = (p < n) ? *seg_value(S, (int64_t)(src[p] & idx_mask)) : 0.0;
             }
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
@@ -1188,11 +887,10 @@ __global__ void __launch_bounds__(BIG_NT) k_bigcol(BigCol *__restrict__ big_list
 }
 
 cudaError_t launch_bigcol(Launch &lc, BigCol *big_list, const ErrState *err, int4 *rec,
-                          const uint2 *perm, const double *s, int64_t s_stride, int idx_bits,
-                          int passes) {
+                          const uint2 *perm, const Segs &S, int idx_bits, int passes) {
     int grid = lc.num_sms;
-    cudaError_t e = launch_pdl(k_bigcol, dim3(grid), dim3(BIG_NT), 0, lc.stream, big_list, err, rec, perm, s,
-                               s_stride, idx_bits, passes);
+    cudaError_t e = launch_pdl(k_bigcol, dim3(grid), dim3(BIG_NT), 0, lc.stream, big_list, err, rec, perm, S,
+                               idx_bits, passes);
     if (e != cudaSuccess) return e;
     lc.launches++;
     return cudaGetLastError();

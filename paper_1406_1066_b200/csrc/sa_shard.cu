@@ -3,11 +3,14 @@
 //
 // The destination of a triplet is the rank owning its column block:
 // bounds[r] <= j-1 < bounds[r+1] (0-based column boundaries, world <= 8).
-// Output: the arrays {i}, {j - bounds[dest]}, {s} grouped by destination in
-// rank order and, inside a destination, in input order -- what the receiver
-// concatenates in source-rank order keeps the global input order, so the
-// per-rank assemblies stay bit-identical to one GPU.  The chunk's indices
-// are validated on the way (first bad row / column position, maxima).
+// Output: the arrays {i}, {j}, {s} of the triplets bound for other ranks,
+// grouped by destination in rank order and, inside a destination, in input
+// order (the rank's own triplets stay in place: its assembly reads its chunk
+// directly, sa_assemble_segments_async) -- the receiver places what it gets
+// from lower ranks before and from higher ranks after its own chunk, which
+// keeps the global input order, so the per-rank assemblies stay
+// bit-identical to one GPU.  The chunk's indices are validated on the way
+// (first bad row / column position, maxima).
 //
 // Three launches (a single pass over the triplets each):
 //   k_part_count    per tile (2048 triplets) and destination: counts
@@ -180,7 +183,7 @@ __global__ void __launch_bounds__(PT_NT) k_part_scatter(const int32_t *__restric
                                                         const int64_t *__restrict__ counts,
                                                         int32_t *__restrict__ out_i,
                                                         int32_t *__restrict__ out_j,
-                                                        double *__restrict__ out_s,
+                                                        double *__restrict__ out_s, int self,
                                                         TileCheck *__restrict__ chk_i) {
     __shared__ int s_cnt[PT_MAXW][PT_IPT * PT_NW];  // [dest][k*NW + w], then exclusive prefixes
     __shared__ TileCheck s_chk[PT_NW];
@@ -228,7 +231,8 @@ __global__ void __launch_bounds__(PT_NT) k_part_scatter(const int32_t *__restric
             if (lane >= o) x += y;
         }
         long long base = tile_off[t * B.world + w];
-        for (int r = 0; r < w; ++r) base += counts[r];  // destinations before w
+        for (int r = 0; r < w; ++r)  // destinations before w (the rank's own stay in place)
+            if (r != self) base += counts[r];
         const int ex = x - a0 - a1;
         s_cnt[w][2 * lane] = (int)ex;
         s_cnt[w][2 * lane + 1] = (int)(ex + a0);
@@ -242,7 +246,7 @@ __global__ void __launch_bounds__(PT_NT) k_part_scatter(const int32_t *__restric
     for (int k = 0; k < PT_IPT; ++k) {
         const int64_t e = t * PT_TILE + (int64_t)k * PT_NT + tid;
         const unsigned peers = pm[k];
-        if (d[k] < 0) continue;
+        if (d[k] < 0 || d[k] == self) continue;
         long long pos = 0;
         int pre = 0;
 #pragma unroll
@@ -253,7 +257,7 @@ __global__ void __launch_bounds__(PT_NT) k_part_scatter(const int32_t *__restric
             }
         pos += pre + __popc(peers & lt);
         out_i[pos] = iv[k];
-        out_j[pos] = j[k] - block_lo(B, d[k]);
+        out_j[pos] = j[k];
         out_s[pos] = sv[k];
     }
     __syncthreads();  // s_chk is reused below
@@ -293,7 +297,7 @@ int64_t partition_tiles(int64_t L) { return (L + PT_TILE - 1) / PT_TILE; }
 size_t partition_check_bytes(int64_t L) { return 2 * (size_t)partition_tiles(L) * sizeof(TileCheck); }
 
 cudaError_t launch_partition(Launch &lc, const int32_t *ii, const int32_t *jj, const double *s,
-                             int64_t s_stride, int64_t L, int world, const int32_t *bounds,
+                             int64_t s_stride, int64_t L, int world, int self, const int32_t *bounds,
                              int32_t *tile_cnt, int64_t *tile_off, int64_t *counts,
                              int32_t *out_i, int32_t *out_j, double *out_s, void *checks,
                              ErrState *err) {
@@ -308,7 +312,8 @@ cudaError_t launch_partition(Launch &lc, const int32_t *ii, const int32_t *jj, c
     k_part_count<<<(unsigned)ntiles, PT_NT, 0, lc.stream>>>(jj, L, B, tile_cnt, chk_j);
     k_part_scan<<<world, 1024, 0, lc.stream>>>(tile_cnt, ntiles, world, tile_off, counts);
     k_part_scatter<<<(unsigned)ntiles, PT_NT, 0, lc.stream>>>(ii, jj, s, s_stride, L, B, tile_off,
-                                                              counts, out_i, out_j, out_s, chk_i);
+                                                              counts, out_i, out_j, out_s, self,
+                                                              chk_i);
     k_part_reduce<<<1, 1024, 0, lc.stream>>>(chk_i, chk_j, ntiles, err);
     lc.launches += 4;
     return cudaGetLastError();

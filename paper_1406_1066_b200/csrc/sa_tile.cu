@@ -503,9 +503,7 @@ __global__ void __launch_bounds__(NT, 5) k_tile_fold(const uint32_t *__restrict_
                                                      const int2 *__restrict__ tile_info,
                                                      const uint8_t *__restrict__ tile_big,
                                                      int64_t ntiles,
-                                                     const int2 *__restrict__ entries,
-                                                     const double *__restrict__ sv,
-                                                     int64_t s_stride,
+                                                     const int2 *__restrict__ entries, Segs SG,
                                                      const int4 *__restrict__ rec,
                                                      const BigCol *__restrict__ big_list,
                                                      const uint32_t *__restrict__ bigk,
@@ -547,9 +545,18 @@ __global__ void __launch_bounds__(NT, 5) k_tile_fold(const uint32_t *__restrict_
     double *V = S.val;
     if (n > 0) mbar_wait(&S.mbar, 0u);
     FTRACE(b, 1);
-    for (int k = tid; k < n; k += NT) {
-        const uint32_t pos = (uint32_t)K[k].y;
-        if (pos != NOPOS) cp_async8(&V[k], sv + (int64_t)pos * s_stride);
+    if (SG.nseg == 1) {  // one input array (the single-GPU path)
+        const double *sv = SG.s[0];
+        const int64_t st = SG.stride[0];
+        for (int k = tid; k < n; k += NT) {
+            const uint32_t pos = (uint32_t)K[k].y;
+            if (pos != NOPOS) cp_async8(&V[k], sv + (int64_t)pos * st);
+        }
+    } else {
+        for (int k = tid; k < n; k += NT) {
+            const uint32_t pos = (uint32_t)K[k].y;
+            if (pos != NOPOS) cp_async8(&V[k], seg_value(SG, (int64_t)pos));
+        }
     }
     cp_async_commit();
     __syncthreads();  // every position is read before pass 1 reuses the field
@@ -792,8 +799,7 @@ __global__ void __launch_bounds__(NT, 5) k_tile_fold(const uint32_t *__restrict_
 
 cudaError_t launch_tile_fold(Launch &lc, const uint32_t *sstart, const int2 *tile_info,
                              const uint8_t *tile_big, int64_t ntiles, const int2 *entries,
-                             const double *s,
-                             int64_t s_stride, const int4 *rec, const BigCol *big_list,
+                             const Segs &SG, const int4 *rec, const BigCol *big_list,
                              const uint32_t *bigk, unsigned long long *tile_state, int32_t N,
                              int32_t *jc, int32_t *ir, double *pr, int64_t cap, ErrState *err) {
     if (ntiles <= 0) return cudaSuccess;
@@ -805,7 +811,7 @@ cudaError_t launch_tile_fold(Launch &lc, const uint32_t *sstart, const int2 *til
         attr = true;
     }
     cudaError_t e = launch_pdl(k_tile_fold, dim3((unsigned)ntiles), dim3(NT), sizeof(TileSmem), lc.stream,
-                               sstart, tile_info, tile_big, ntiles, entries, s, s_stride, rec, big_list,
+                               sstart, tile_info, tile_big, ntiles, entries, SG, rec, big_list,
                                bigk, tile_state, N, jc, ir, pr, cap, err);
     lc.launches++;
     return e;

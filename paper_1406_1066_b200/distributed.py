@@ -9,15 +9,17 @@ rank order = input order).  Per call:
 2. contiguous column ranges are assigned to ranks so that each receives about
    L / world triplets (block granularity);
 3. each rank partitions its chunk by destination rank, *stably* (the CUDA
-   kernels of sa_partition: per-tile counts, a scan, a block-scanned scatter
-   of (row, local column, value), validating the chunk on the way), and
-   ``all_to_all`` moves them to their owners;
+   kernels of sa_partition, validating the chunk on the way); only the
+   triplets bound for other ranks are written and moved by ``all_to_all``
+   (element-ordered FEM keeps ~99.9 % at home);
    a rank concatenates what it receives in source-rank order, which is the
    global input order restricted to its columns -- so duplicates are still
    folded in input order and the result is bit-identical to one GPU;
-4. the rank assembles its column block with the single-GPU pipeline (columns
-   relabelled to the block) and an ``all_gather`` of the per-rank nnz gives
-   the offset of its ``jc``.
+4. the rank assembles its column block with the single-GPU pipeline reading
+   three segments in place -- received from lower ranks, its own chunk
+   (other ranks' columns skipped), received from higher ranks -- which is
+   the global input order restricted to its columns (bit-identical to one
+   GPU); an ``all_gather`` of the per-rank nnz gives the offset of its ``jc``.
 
 The collectives are plain data movement (NCCL over NVLink for CUDA tensors,
 gloo for CPU tests); the local assembly is the caller-supplied assembler (the
@@ -66,34 +68,34 @@ def block_boundaries(block_hist: torch.Tensor, world: int, nblocks: int, n: int)
     return bounds
 
 
-def partition_torch(ii, jj, s, bounds, world):
+def partition_torch(ii, jj, s, bounds, world, self_rank=-1):
     """Host restatement of sa_partition (CPU tensors: the gloo tests).
-    Returns ((i, j - bounds[dest], s) grouped by destination rank, stably;
-    per-rank counts).  Columns outside [1, bounds[-1]] go nowhere."""
+    Returns ((i, j, s) of the triplets bound for ranks other than
+    `self_rank`, grouped by destination rank, stably; per-rank counts
+    including the rank's own).  Columns outside [1, bounds[-1]] go nowhere."""
     jj64 = jj.to(torch.int64)
     bt = torch.tensor(bounds[1:-1], dtype=torch.int64, device=jj.device)
     valid = (jj64 >= 1) & (jj64 <= bounds[-1])
     dest = torch.searchsorted(bt, jj64 - 1, right=True)
     dest = torch.where(valid, dest, torch.full_like(dest, world))
+    counts = torch.bincount(dest, minlength=world + 1)[:world]
+    if 0 <= self_rank < world:
+        dest = torch.where(dest == self_rank, torch.full_like(dest, world), dest)
     key = dest.to(torch.uint8) if world < 255 else dest
     order = torch.sort(key, stable=True).indices
-    counts = torch.bincount(dest, minlength=world + 1)[:world]
-    keep = order[: int(counts.sum())]
-    base = torch.tensor(bounds, dtype=torch.int64, device=jj.device)[dest[keep]]
+    keep = order[: int((dest < world).sum())]
     sv = s.expand(len(jj)) if s.numel() == 1 and len(jj) != 1 else s
-    out = (ii[keep].contiguous(), (jj64[keep] - base).to(torch.int32), sv[keep].contiguous())
+    out = (ii[keep].contiguous(), jj[keep].contiguous(), sv[keep].contiguous())
     return out, [int(c) for c in counts.tolist()]
 
 
-def _partition_cuda(ii, jj, s, m, n, bounds, world):
+def _partition_cuda(asm, ii, jj, s, m, n, bounds, world, self_rank):
     """sa_partition: the CUDA partition (validates the chunk on the way)."""
     import ctypes
 
-    from .assembly import _ptr, default_assembler
+    from .assembly import _ptr
 
     dev = ii.device
-    asm = default_assembler(dev.index if dev.index is not None else 0)
-    asm._bind_stream()
     L = len(ii)
     outs = (torch.empty(max(L, 1), dtype=torch.int32, device=dev),
             torch.empty(max(L, 1), dtype=torch.int32, device=dev),
@@ -101,33 +103,77 @@ def _partition_cuda(ii, jj, s, m, n, bounds, world):
     hb = (ctypes.c_int32 * (world + 1))(*bounds)
     hc = (ctypes.c_int64 * world)()
     bp, bw = ctypes.c_int64(-1), ctypes.c_int(-1)
-    sv = s.contiguous()
-    ii, jj = ii.contiguous(), jj.contiguous()
-    rc = asm.lib.sa_partition(asm.ctx, _ptr(ii), _ptr(jj), _ptr(sv),
-                              0 if (sv.numel() == 1 and L != 1) else 1, L, m, n, world, hb,
+    rc = asm.lib.sa_partition(asm.ctx, _ptr(ii), _ptr(jj), _ptr(s),
+                              0 if (s.numel() == 1 and L != 1) else 1, L, m, n, world, self_rank, hb,
                               _ptr(outs[0]), _ptr(outs[1]), _ptr(outs[2]), hc, ctypes.byref(bp),
                               ctypes.byref(bw))
     if rc:
         asm._raise_dev(rc, bp.value, bw.value, None, None, ii, jj)
     counts = [int(hc[r]) for r in range(world)]
-    k = sum(counts)
+    k = sum(c for r, c in enumerate(counts) if r != self_rank)
     return tuple(x[:k] for x in outs), counts
 
 
-def assemble_sharded(ii: torch.Tensor, jj: torch.Tensor, s: torch.Tensor, m: int, n: int,
-                     local_assemble, group=None, nblocks: int = 4096) -> ShardResult:
-    """Assemble the global matrix whose triplets are split across the ranks
-    of `group` (contiguous chunks in rank order).  `local_assemble(ii, jj, s,
-    m, n_local)` -> (jc int, ir int32, pr float64) tensors on ii's device.
+def _assemble_segments_cuda(asm, segs, col_lo, m, n_local):
+    """sa_assemble_segments_async over [(ii, jj, s), ...] read in place."""
+    import ctypes
 
-    CUDA tensors: the partition is the CUDA kernel set of sa_partition (which
-    also validates the chunk: BadIndex with the chunk-local position,
-    DimensionTooSmall); CPU tensors (gloo tests): its torch restatement."""
+    from .assembly import DeviceCsc, _ptr
+
+    dev = segs[0][0].device
+    k = len(segs)
+    pi = (ctypes.c_void_p * k)(*[_ptr(x[0]) for x in segs])
+    pj = (ctypes.c_void_p * k)(*[_ptr(x[1]) for x in segs])
+    ps = (ctypes.c_void_p * k)(*[_ptr(x[2]) for x in segs])
+    lens = [int(x[0].shape[0]) for x in segs]
+    st = (ctypes.c_int64 * k)(*[0 if (x[2].numel() == 1 and n_ != 1) else 1 for x, n_ in zip(segs, lens)])
+    ln = (ctypes.c_int64 * k)(*lens)
+    cap = max(sum(lens), 1)
+    jc = torch.empty(n_local + 1, dtype=torch.int32, device=dev)
+    ir = torch.empty(cap, dtype=torch.int32, device=dev)
+    pr = torch.empty(cap, dtype=torch.float64, device=dev)
+    asm._bind_stream()
+    rc = asm.lib.sa_assemble_segments_async(asm.ctx, k, pi, pj, ps, st, ln, col_lo, m, n_local,
+                                            _ptr(jc), _ptr(ir), _ptr(pr), cap)
+    if rc:
+        asm._raise(rc)
+    nnz = ctypes.c_int64(0)
+    bp, bw = ctypes.c_int64(-1), ctypes.c_int(-1)
+    rc = asm.lib.sa_finish(asm.ctx, ctypes.byref(nnz), ctypes.byref(bp), ctypes.byref(bw))
+    if rc:
+        asm._raise(rc)
+    return DeviceCsc(jc, ir[: nnz.value], pr[: nnz.value], m, n_local)
+
+
+def assemble_sharded(ii: torch.Tensor, jj: torch.Tensor, s: torch.Tensor, m: int, n: int,
+                     local_assemble=None, group=None, nblocks: int = 4096) -> ShardResult:
+    """Assemble the global matrix whose triplets are split across the ranks
+    of `group` (contiguous chunks in rank order).
+
+    CUDA tensors (local_assemble None or gpu_local_assembler): the CUDA
+    partition (sa_partition, which validates the chunk) moves only the
+    triplets bound for other ranks; the rank's assembly reads its own chunk
+    in place, between what it received from lower and from higher ranks
+    (sa_assemble_segments_async).  CPU tensors (gloo tests): the torch
+    restatement of the partition, the received and own triplets
+    concatenated, and `local_assemble(ii, jj, s, m, n_local)` -> (jc, ir, pr)."""
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     dev = ii.device
+    cuda = ii.is_cuda and (local_assemble is None or getattr(local_assemble, "cuda_segments", False))
+    asm = None
+    if cuda:
+        from .assembly import default_assembler
+
+        asm = default_assembler(dev.index if dev.index is not None else 0)
+        asm._bind_stream()
+        ii, jj, s = ii.contiguous(), jj.contiguous(), s.contiguous()
     if world == 1:  # one rank owns every column: no partition, no exchange
-        jc, ir, pr = local_assemble(ii, jj, s, m, n)
+        if cuda:
+            out = asm.assemble_device(ii, jj, s, m=m, n=n)
+            jc, ir, pr = out.jc, out.ir, out.pr
+        else:
+            jc, ir, pr = local_assemble(ii, jj, s, m, n)
         k = int(jc[-1]) if len(jc) else 0
         return ShardResult(0, n, jc.to(torch.int64), ir, pr, 0, k, m, n, int(ii.shape[0]), 0)
     nblocks = max(1, min(nblocks, n))
@@ -139,15 +185,16 @@ def assemble_sharded(ii: torch.Tensor, jj: torch.Tensor, s: torch.Tensor, m: int
     hist = torch.bincount(blk, minlength=nblocks).to(torch.int64) * step
     dist.all_reduce(hist, group=group)
     bounds = block_boundaries(hist, world, nblocks, n)
-    if ii.is_cuda:
-        parts, sc = _partition_cuda(ii, jj, s, m, n, bounds, world)
+    if cuda:
+        parts, counts = _partition_cuda(asm, ii, jj, s, m, n, bounds, world, rank)
     else:
-        parts, sc = partition_torch(ii, jj, s, bounds, world)
+        parts, counts = partition_torch(ii, jj, s, bounds, world, rank)
+    sc = [0 if r == rank else c for r, c in enumerate(counts)]  # the own triplets stay here
     send_counts = torch.tensor(sc, dtype=torch.int64, device=dev)
     recv_counts = torch.empty_like(send_counts)
     dist.all_to_all_single(recv_counts, send_counts, group=group)
     rc_ = recv_counts.cpu().tolist()
-    sent_remote = sum(c for r, c in enumerate(sc) if r != rank)
+    sent_remote = sum(sc)
 
     def exchange(x):
         out = torch.empty(sum(rc_), dtype=x.dtype, device=dev)
@@ -157,19 +204,34 @@ def assemble_sharded(ii: torch.Tensor, jj: torch.Tensor, s: torch.Tensor, m: int
     r_ii, r_jj, r_s = (exchange(x) for x in parts)
     col_lo, col_hi = bounds[rank], bounds[rank + 1]
     n_local = col_hi - col_lo
-    jc, ir, pr = local_assemble(r_ii, r_jj, r_s, m, n_local)
+    k_lo = sum(rc_[:rank])  # received from lower ranks precede the own chunk
+    lower = (r_ii[:k_lo], r_jj[:k_lo], r_s[:k_lo])
+    higher = (r_ii[k_lo:], r_jj[k_lo:], r_s[k_lo:])
+    if cuda:
+        segs = [x for x in (lower, (ii, jj, s), higher) if x[0].shape[0] > 0] or [(ii, jj, s)]
+        out = _assemble_segments_cuda(asm, segs, col_lo, m, n_local)
+        jc, ir, pr = out.jc, out.ir, out.pr
+    else:
+        mine = (jj.to(torch.int64) > col_lo) & (jj.to(torch.int64) <= col_hi)
+        sv = s.expand(len(jj)) if s.numel() == 1 and len(jj) != 1 else s
+        cat_i = torch.cat([lower[0], ii[mine], higher[0]])
+        cat_j = torch.cat([lower[1], jj[mine], higher[1]])
+        cat_s = torch.cat([lower[2], sv[mine], higher[2]])
+        jc, ir, pr = local_assemble(cat_i, (cat_j.to(torch.int64) - col_lo).to(torch.int32), cat_s, m,
+                                    n_local)
     nnz_local = torch.tensor([int(jc[-1]) if len(jc) else 0], dtype=torch.int64, device=dev)
     all_nnz = [torch.empty_like(nnz_local) for _ in range(world)]
     dist.all_gather(all_nnz, nnz_local, group=group)
-    counts = [int(x.item()) for x in all_nnz]
-    off = sum(counts[:rank])
+    nn = [int(x.item()) for x in all_nnz]
+    off = sum(nn[:rank])
     jc_global = jc.to(torch.int64) + off
-    return ShardResult(col_lo, col_hi, jc_global, ir, pr, off, sum(counts), m, n,
-                       int(r_ii.shape[0]), sent_remote)
+    return ShardResult(col_lo, col_hi, jc_global, ir, pr, off, sum(nn), m, n,
+                       int(r_ii.shape[0]) + counts[rank], sent_remote)
 
 
 def gpu_local_assembler(device: int = 0):
-    """The production local assembler: the CUDA pipeline (device tensors)."""
+    """The production local assembler marker: assemble_sharded then reads the
+    rank's own chunk in place (CUDA segments) instead of calling it."""
     from .assembly import default_assembler
 
     asm = default_assembler(device)
@@ -178,4 +240,5 @@ def gpu_local_assembler(device: int = 0):
         out = asm.assemble_device(ii.contiguous(), jj.contiguous(), s.contiguous(), m=m, n=n_local)
         return out.jc, out.ir, out.pr
 
+    run.cuda_segments = True
     return run

@@ -327,11 +327,11 @@ def test_matrixmarket_round_trip_bit_faithful(tmp_path):
         read_triplets_matrixmarket(p)
 
 
-@pytest.mark.parametrize("world", [1, 2, 3, 8])
-def test_partition_kernel_matches_torch_restatement(world):
+@pytest.mark.parametrize("world,self_rank", [(1, -1), (2, 0), (3, 2), (8, -1), (8, 5)])
+def test_partition_kernel_matches_torch_restatement(world, self_rank):
     """sa_partition (CUDA) == partition_torch: destinations in rank order,
-    stable inside each, out-of-block columns dropped, local columns; and the
-    chunk validation (first bad position, dimensions)."""
+    stable inside each, the own rank's triplets counted but left in place,
+    out-of-block columns dropped; and the chunk validation."""
     import ctypes
 
     from paper_1406_1066_b200.assembly import _ptr
@@ -354,16 +354,17 @@ def test_partition_kernel_matches_torch_restatement(world):
         hb = (ctypes.c_int32 * (world + 1))(*bounds)
         hc = (ctypes.c_int64 * world)()
         bp, bw = ctypes.c_int64(-1), ctypes.c_int(-1)
-        rc = a.lib.sa_partition(a.ctx, _ptr(ti), _ptr(tj), _ptr(ts), 1, L, m, nn, world, hb,
+        rc = a.lib.sa_partition(a.ctx, _ptr(ti), _ptr(tj), _ptr(ts), 1, L, m, nn, world, self_rank, hb,
                                 *(_ptr(x) for x in outs), hc, ctypes.byref(bp), ctypes.byref(bw))
         return rc, outs, [hc[r] for r in range(world)], bp.value, bw.value
 
     rc, outs, counts, _, _ = run(ii, jj, 900, n)
     assert rc == 0
     ref, rcounts = partition_torch(torch.from_numpy(ii), torch.from_numpy(jj), torch.from_numpy(s),
-                                   bounds, world)
-    k = sum(rcounts)
-    assert counts == rcounts and k == L
+                                   bounds, world, self_rank)
+    k = len(ref[0])
+    assert counts == rcounts and sum(rcounts) == L
+    assert k == L - (rcounts[self_rank] if self_rank >= 0 else 0)
     assert torch.equal(outs[0][:k].cpu(), ref[0]) and torch.equal(outs[1][:k].cpu(), ref[1])
     assert outs[2][:k].cpu().numpy().tobytes() == ref[2].numpy().tobytes()
     bad = jj.copy()
@@ -372,6 +373,44 @@ def test_partition_kernel_matches_torch_restatement(world):
     assert rc != 0 and bp == 10 and bw == 1  # SA_WHICH_COL
     rc, _, _, _, _ = run(ii, jj, 500, n)  # rows above M
     assert rc != 0
+
+
+@pytest.mark.parametrize("kind", ["fem2d", "heavy"])
+def test_segment_assembly_is_the_sharded_local_block(kind):
+    """sa_assemble_segments_async on [received from lower ranks, own chunk in
+    place (other columns skipped), received from higher ranks] == the
+    oracle's column block of the whole input, bit for bit (the 3-rank
+    sharded assembly simulated for each rank on one GPU)."""
+    from paper_1406_1066_b200 import workloads as W
+    from paper_1406_1066_b200.distributed import _assemble_segments_cuda
+
+    w = W.fem2d(30) if kind == "fem2d" else W.heavy_dup(m=400, positions=20_000, seed=4)
+    ii, jj, s = w.ii.numpy(), w.jj.numpy(), w.s.numpy()
+    L, m, n = len(ii), w.m, w.n
+    world = 3
+    chunks = [(L * r // world, L * (r + 1) // world) for r in range(world)]
+    bounds = [0, n // 3, (2 * n) // 3, n]
+    ref = O.assemble_counting(ii, jj, s, m, n)
+    dev = torch.device("cuda", 0)
+    a = sa.default_assembler(0)
+    for rank in range(world):
+        lo, hi = bounds[rank], bounds[rank + 1]
+
+        def block(c0, c1):
+            sel = (jj[c0:c1] > lo) & (jj[c0:c1] <= hi)
+            return tuple(torch.from_numpy(np.ascontiguousarray(x[c0:c1][sel])).to(dev) for x in (ii, jj, s))
+
+        lower = [block(*chunks[r]) for r in range(rank)]
+        higher = [block(*chunks[r]) for r in range(rank + 1, world)]
+        cat = lambda parts: tuple(torch.cat([p[q] for p in parts]) for q in range(3))  # noqa: E731
+        c0, c1 = chunks[rank]
+        own = tuple(torch.from_numpy(np.ascontiguousarray(x[c0:c1])).to(dev) for x in (ii, jj, s))
+        segs = ([cat(lower)] if lower else []) + [own] + ([cat(higher)] if higher else [])
+        got = _assemble_segments_cuda(a, segs, lo, m, hi - lo).to_host()
+        k0, k1 = ref.jc[lo], ref.jc[hi]
+        assert np.array_equal(got.jc, ref.jc[lo:hi + 1] - k0)
+        assert np.array_equal(got.ir, ref.ir[k0:k1])
+        assert got.pr.tobytes() == ref.pr[k0:k1].tobytes()
 
 
 def test_sharded_path_one_rank_nccl():
