@@ -21,12 +21,11 @@ constexpr int SCAN_IPT = 8;  // multiple of 4 (16-byte vectors)
 constexpr int SCAN_TILE = SCAN_NT * SCAN_IPT;
 
 // Fold geometry (k_tile_fold).  Tile b owns the columns whose small-space
-// start lies in [b*TILE, (b+1)*TILE); inside the CTA, thread t owns the
-// columns starting in its WIN-wide sub-window.  A tile holds at most
+// start lies in [b*TILE, (b+1)*TILE); inside the CTA every thread owns a
+// contiguous range of the tile's columns.  A tile holds at most
 // TILE + BIGCOL - 1 small records.
 constexpr int TILE = 1792;
 constexpr int TILE_THREADS = 128;
-constexpr int WIN = TILE / TILE_THREADS;  // 16 record positions per thread
 constexpr int BIGCOL = 256;
 constexpr int TCAP = TILE + BIGCOL;
 

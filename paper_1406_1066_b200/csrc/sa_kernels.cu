@@ -1,20 +1,26 @@
 // sa_kernels.cu -- hand-written sm_100a kernels for sparse(i,j,s,m,n).
 //
-// Pipeline (one stream, no host round trip):
-//   k_hist       column histogram of the triplets + index validation
-//                (types.py:121-165 semantics), warp-aggregated atomics
-//   k_col_scan   single-pass decoupled-look-back exclusive scan of the column
-//                counts -> column cursors; also the tile -> first-column map
-//                and the list of big columns
-//   k_scatter    counting-sort scatter by column: 16-byte records
-//                {row, input position, value} at cursor positions
-//   k_bigcol     columns longer than BIGCOL: in-place LSD radix sort by
-//                (row, input position), ordered fold
-//   k_tile_fold  per tile of columns, in shared memory: hash (column,row)
-//                groups, order each group by input position, fold from +0.0
-//                in input order (bit-exact with the reference scatter,
-//                _kernels.pyx:82-89), order groups by row, chained scan of
-//                the unique counts -> jc, ir, pr written once.
+// Pipeline (one stream, no host round trip, programmatic dependent launch):
+//   k_init          reset counters, look-back words, error state (sa_capi.cu)
+//   k_colcount_win  column histogram + column-index validation: runs of equal
+//                   columns per thread, a shared-memory window per 2048-triplet
+//                   chunk, one global atomic per touched column and chunk
+//   k_col_scan      single-pass decoupled-look-back exclusive scan of the column
+//                   counts -> column cursors; the tile -> first-column map and
+//                   the list of big columns
+//   k_scatter       counting-sort scatter by column of 8-byte entries {row,
+//                   input position} (shared-memory hash aggregation, one cursor
+//                   reservation per column and chunk) + row validation
+//   k_bigcol        columns longer than BIGCOL: LSD radix sort by (row, input
+//                   position) in one 1024-thread CTA, ordered fold
+//   k_tile_fold     (sa_tile.cu) per tile of columns: TMA entries, cp.async
+//                   value gather, per-column sort by (row, position), fold from
+//                   +0.0 in input order (bit-exact with the reference scatter,
+//                   _kernels.pyx:82-89), decoupled look-back of the unique
+//                   counts -> jc, ir, pr written once.
+// Helpers: k_hist (dimension inference / validation-only path), k_convert
+// (raw index arrays), k_prune (sa_prune.cu), the sharding partition
+// (sa_shard.cu).
 //
 // Reference algorithm: serial.py:111-168 / _kernels.pyx:20-89 (row-first
 // counting sort).  This pipeline is column-first; it produces the same CSC
