@@ -709,12 +709,179 @@ __global__ void __launch_bounds__(AGG_NT) k_scatter(Segs S, int32_t M, int32_t N
     }
 }
 
+// Staged variant (SA_SCATTER_STAGED=1): 128-thread CTAs on half chunks
+// (1024 triplets); after the reservation every entry is first placed in
+// shared memory grouped by column (each column's run of the half chunk is
+// contiguous there), then copied out so that consecutive lanes write
+// consecutive slots of one column.
+constexpr int SNT = 128;
+constexpr int SCH = SNT * CPT;   // 1024 triplets per half chunk
+constexpr int SHT = 2 * SCH;     // hash slots
+struct StgSmem {
+    int key[SHT];       // column + 1 (0 = empty); after the reservation: staging base
+    int ctr[SHT];       // triplets of the column in the half chunk, then the cursor word
+    int used[SCH];
+    uint2 ent[SCH];     // staged entries {row, position}
+    uint32_t dst[SCH];  // their slots
+    int nused;
+    int top;
+};
+
+__device__ __forceinline__ int stg_insert(StgSmem &A, int col) {
+    const int key = col + 1;
+    unsigned h = ((unsigned)key * 0x9E3779B1u) >> (32 - 11);  // SHT = 2048
+    bool fresh = false;
+    while (true) {
+        const int old = atomicCAS(&A.key[h], 0, key);
+        if (old == 0) {
+            fresh = true;
+            break;
+        }
+        if (old == key) break;
+        h = (h + 1) & (SHT - 1);
+    }
+    list_push(A.used, &A.nused, fresh, (int)h);
+    return (int)h;
+}
+
+__global__ void __launch_bounds__(SNT) k_scatter_staged(Segs S, int32_t M, int32_t N,
+                                                        uint32_t *__restrict__ cur,
+                                                        uint2 *__restrict__ perm, ErrState *err) {
+    __shared__ StgSmem A;
+    const int tid = threadIdx.x;
+    for (int k = tid; k < SHT; k += SNT) {
+        A.key[k] = 0;
+        A.ctr[k] = 0;
+    }
+    if (tid == 0) {
+        A.nused = 0;
+        A.top = 0;
+    }
+    __syncthreads();
+    pdl_wait();
+    pdl_trigger();
+    const uint32_t lsmall = err->lsmall;
+    unsigned long long bad = ~0ull, badj = ~0ull;
+    unsigned over = 0, overj = 0;
+    const int64_t nh = 2 * S.ch0[S.nseg];
+    int in_[CPT], jn[CPT];
+    auto prefetch = [&](int64_t hc) {
+        const SegChunk c = seg_chunk(S, hc >> 1);
+        const int64_t t = c.t0 + (hc & 1) * SCH + (int64_t)tid * CPT;
+        load_run(c.ii, t, c.len, c.vec, in_, 1);
+        load_run(c.jj, t, c.len, c.vec, jn, 0);
+    };
+    if ((int64_t)blockIdx.x < nh) prefetch(blockIdx.x);
+    for (int64_t hc = blockIdx.x; hc < nh; hc += gridDim.x) {
+        const SegChunk c = seg_chunk(S, hc >> 1);
+        const int64_t t0 = c.t0 + (hc & 1) * SCH + (int64_t)tid * CPT;
+        int i[CPT], j[CPT];
+#pragma unroll
+        for (int k = 0; k < CPT; ++k) {
+            i[k] = in_[k];
+            j[k] = jn[k] - S.col_lo;
+        }
+        if (hc + gridDim.x < nh) prefetch(hc + gridDim.x);
+        {
+            int ilo = i[0], ihi = i[0];
+#pragma unroll
+            for (int k = 1; k < CPT; ++k) {
+                ilo = min(ilo, i[k]);
+                ihi = max(ihi, i[k]);
+            }
+            if (ilo < 1 || ihi > M || t0 + CPT > c.len) {
+#pragma unroll
+                for (int k = 0; k < CPT; ++k) {
+                    const bool live = t0 + k < c.len;
+                    if (live && i[k] < 1) bad = min(bad, (unsigned long long)(c.pos0 + t0 + k));
+                    if (live && i[k] > M) over = 1;
+                }
+            }
+        }
+        const unsigned vmask = column_mask(j, t0, c.len, c.pos0, N, true, badj, overj);
+        const Runs R = run_masks(j, vmask);
+        int hk[CPT], rk[CPT];
+#pragma unroll
+        for (int k = 0; k < CPT; ++k) {
+            hk[k] = -1;
+            rk[k] = 0;
+            if (R.heads & (1u << k)) {
+                hk[k] = stg_insert(A, j[k] - 1);
+                rk[k] = atomicAdd(&A.ctr[hk[k]], run_len(R, k));
+            } else if (vmask & (1u << k)) {
+                hk[k] = hk[k > 0 ? k - 1 : 0];
+                rk[k] = rk[k > 0 ? k - 1 : 0] + 1;
+            }
+        }
+        __syncthreads();
+        const int nu = A.nused;
+        for (int e = tid; e < nu; e += SNT) {
+            const int h = A.used[e];
+            const int cnt = A.ctr[h];
+            A.ctr[h] = (int)atomicAdd(&cur[A.key[h] - 1], (uint32_t)cnt);
+            A.key[h] = atomicAdd(&A.top, cnt);  // the column's run in the staging area
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < CPT; ++k) {
+            if (hk[k] < 0) continue;
+            const uint32_t bw = (uint32_t)A.ctr[hk[k]];
+            const int x = A.key[hk[k]] + rk[k];
+            A.ent[x] = make_uint2((uint32_t)i[k], (uint32_t)(c.pos0 + t0 + k));
+            A.dst[x] = (bw & POSMASK) + ((bw & BIGFLAG) ? lsmall : 0u) + (uint32_t)rk[k];
+        }
+        __syncthreads();
+        const int nst = A.top;
+        for (int x = tid; x < nst; x += SNT) perm[A.dst[x]] = A.ent[x];
+        __syncthreads();
+        for (int e = tid; e < nu; e += SNT) {
+            const int h = A.used[e];
+            A.key[h] = 0;
+            A.ctr[h] = 0;
+        }
+        if (tid == 0) {
+            A.nused = 0;
+            A.top = 0;
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        bad = min(bad, __shfl_xor_sync(FULL, bad, o));
+        over |= __shfl_xor_sync(FULL, over, o);
+    }
+    if ((tid & 31) == 0) {
+        if (bad != ~0ull) atomicMin(&err->bad_i, bad);
+        if (over) err->over_m = 1;
+    }
+}
+
+// Staged writes pay off when the column cursors (4 N bytes) and the columns'
+// slot regions no longer stay in L2 between the chunks that fill them (cfg5,
+// N = 6.4e7: 14.3 -> 10.6 ms); with L2-resident cursors (cfg2 / cfg3) the
+// plain scatter is faster (110 vs 174 us on cfg2).  SA_SCATTER_STAGED=0/1
+// overrides.
+static bool scatter_staged(int32_t N) {
+    static int m = -2;
+    if (m == -2) {
+        const char *e = getenv("SA_SCATTER_STAGED");
+        m = (e && (e[0] == '0' || e[0] == '1')) ? e[0] - '0' : -1;
+    }
+    return m >= 0 ? m == 1 : N > (16 << 20);
+}
+
 cudaError_t launch_scatter(Launch &lc, const Segs &S, int32_t M, int32_t N, uint32_t *cur,
                            uint2 *perm, ErrState *err) {
     const int64_t nchunk = S.ch0[S.nseg];
     if (nchunk <= 0) return cudaSuccess;
-    const int grid = (int)std::min<int64_t>(nchunk, (int64_t)lc.num_sms * 4);
-    cudaError_t e = launch_pdl(k_scatter, dim3(grid), dim3(AGG_NT), 0, lc.stream, S, M, N, cur, perm, err);
+    cudaError_t e;
+    if (scatter_staged(N)) {
+        const int grid = (int)std::min<int64_t>(2 * nchunk, (int64_t)lc.num_sms * 7);
+        e = launch_pdl(k_scatter_staged, dim3(grid), dim3(SNT), 0, lc.stream, S, M, N, cur, perm, err);
+    } else {
+        const int grid = (int)std::min<int64_t>(nchunk, (int64_t)lc.num_sms * 4);
+        e = launch_pdl(k_scatter, dim3(grid), dim3(AGG_NT), 0, lc.stream, S, M, N, cur, perm, err);
+    }
     lc.launches++;
     return e;
 }
