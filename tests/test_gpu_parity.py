@@ -443,3 +443,32 @@ def test_sharded_path_one_rank_nccl():
             assemble_sharded(w.ii.to(dev), bad.to(dev), w.s.to(dev), w.m, w.n, gpu_local_assembler(0))
     finally:
         dist.destroy_process_group()
+
+
+def test_long_columns_with_spans_beyond_the_packed_key():
+    """Long columns (25..256 triplets) whose row span (rows 1 .. 2^31-1) and
+    position span (> 2^25) do not fit the packed 64-bit bitonic key take the
+    serial fallback; also long columns of every length class, duplicates
+    across the whole input, NaN values."""
+    rng = np.random.default_rng(21)
+    L = 34_000_000
+    ii = rng.integers(1, 1000, size=L).astype(np.int32)
+    jj = rng.integers(1, 2_000_001, size=L).astype(np.int32)  # short columns (~17 each)
+    s = rng.standard_normal(L)
+    # column 5: 100 triplets split between the start and the end of the input:
+    # 31 row bits + 26 position bits + 7 slot bits > 63
+    idx = np.concatenate([np.arange(0, 50), np.arange(L - 50, L)])
+    jj[idx] = 5
+    ii[idx] = rng.choice(np.array([1, 2, 2**31 - 1, 2**31 - 2], np.int64), size=100).astype(np.int32)
+    # columns 7 / 8 / 9: 40 / 100 / 200 triplets with ordinary spans and duplicates
+    for col, cnt in ((7, 40), (8, 100), (9, 200)):
+        sel = rng.choice(L // 2, size=cnt, replace=False) + (L // 4)
+        sel = sel[jj[sel] > 9]
+        jj[sel] = col
+        ii[sel] = rng.integers(1, 12, size=len(sel))
+    s[rng.random(L) < 1e-6] = np.nan
+    dev = torch.device("cuda", 0)
+    got = sa.default_assembler(0).assemble_device(*(torch.from_numpy(x).to(dev) for x in (ii, jj, s)),
+                                                  m=2**31 - 1, n=2_000_000).to_host()
+    ref = O.assemble_sorted(ii, jj, s, 2**31 - 1, 2_000_000)
+    _same(got, ref)
