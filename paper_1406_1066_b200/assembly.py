@@ -204,6 +204,12 @@ class Assembler:
             scalar = int(s.shape[0]) == 1 and L != 1
         if not scalar and int(s.shape[0]) != L:
             raise LengthMismatch(f"value array of length {int(s.shape[0])} vs index length {L}")
+        for name, t in (("ii", ii), ("jj", jj)):
+            if t.dtype != torch.int32 or not t.is_cuda:
+                raise TypeError(f"assemble_device: {name} must be an int32 CUDA tensor, got "
+                                f"{t.dtype} on {t.device} (assemble() converts other index types)")
+        if not s.is_cuda:
+            raise TypeError(f"assemble_device: s must be a CUDA tensor, got one on {s.device}")
         ii = ii.contiguous()
         jj = jj.contiguous()
         s = s.contiguous().to(torch.float64)

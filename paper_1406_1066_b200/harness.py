@@ -25,7 +25,7 @@ from __future__ import annotations
 
 import ctypes
 import time
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 from typing import Callable
 
 import numpy as np
@@ -113,3 +113,89 @@ def make_impl(kind: str = "b200", threads: int = 1, device: int = 0) -> Impl:
         raise ValueError(f"unknown implementation kind {kind!r}")
     return Impl(f"b200-cuda{device}", 1,
                 lambda req, pt=None: _run_b200(req, pt, device=device))
+
+
+@dataclass
+class BenchResult:
+    """One timed (dataset, implementation) row; the reference's fields
+    (bench.py:84-98) so ``mmio.write_bench_csv`` writes the same CSV."""
+
+    dataset_id: str
+    impl: str
+    threads: int
+    mean_seconds: float
+    min_seconds: float
+    reps: int
+    L: int
+    M: int
+    N: int
+    nnz: int
+    speedup_vs_serial: float | None = None
+    phase_means: dict = field(default_factory=dict)
+
+
+def run_bench(triplets, impls: list[Impl], reps: int = 40, dataset_id: str = "custom",
+              dims=None) -> list[BenchResult]:
+    """The reference's ``run_bench`` protocol (bench.py:132-196) over given
+    triplets ``(ii, jj, s)``: every implementation's output is cross-checked
+    bit-exactly against the first one's (``ResultMismatch`` otherwise), then
+    each gets one untimed warm-up and ``reps`` timed runs (mean, min, mean
+    phase times); ``speedup_vs_serial`` is filled when an implementation
+    named ``serial*`` is present."""
+    from types import SimpleNamespace
+
+    from .errors import ResultMismatch
+    from .types import Dimensions
+
+    if reps < 1:
+        raise ValueError("reps must be >= 1")
+    ii, jj, s = triplets
+    ii = np.ascontiguousarray(ii, dtype=np.int32)
+    jj = np.ascontiguousarray(jj, dtype=np.int32)
+    s = np.ascontiguousarray(s, dtype=np.float64)
+    # a reference-shaped request (validated triplets + dims), which both this
+    # package's Impl and the reference's accept
+    if dims is None:
+        dims = Dimensions(int(ii.max()) if len(ii) else 0, int(jj.max()) if len(jj) else 0)
+    req = SimpleNamespace(triplets=SimpleNamespace(ii=ii, jj=jj, sr=s), dims=dims,
+                          capacity_hint=None)
+    reference = None
+    for impl in impls:
+        out = impl.run(req)
+        if reference is None:
+            reference = (impl.name, out)
+        elif not _same(reference[1], out):
+            raise ResultMismatch(f"{impl.name} output differs from {reference[0]} "
+                                 f"(nnz {out.nnz} vs {reference[1].nnz})")
+    nnz = reference[1].nnz if reference else 0
+    results = []
+    serial_mean = None
+    for impl in impls:
+        impl.run(req)
+        times = []
+        acc: dict[str, float] = {}
+        for _ in range(reps):
+            phases: dict[str, float] = {}
+            t0 = time.perf_counter()
+            impl.run(req, phases)
+            times.append(time.perf_counter() - t0)
+            for k, v in phases.items():
+                acc[k] = acc.get(k, 0.0) + v
+        mean = sum(times) / len(times)
+        if impl.name.startswith("serial") and serial_mean is None:
+            serial_mean = mean
+        results.append(BenchResult(dataset_id, impl.name, impl.threads, mean, min(times), reps,
+                                   len(ii), dims.m, dims.n, nnz,
+                                   phase_means={k: v / reps for k, v in acc.items()}))
+    if serial_mean is not None:
+        for r in results:
+            r.speedup_vs_serial = serial_mean / r.mean_seconds
+    return results
+
+
+def _same(a, b) -> bool:
+    return (int(a.m) == int(b.m) and int(a.n) == int(b.n)
+            and np.array_equal(np.asarray(a.jc), np.asarray(b.jc))
+            and np.array_equal(np.asarray(a.ir), np.asarray(b.ir))
+            and np.asarray(a.pr, dtype=np.float64).tobytes()
+            == np.asarray(b.pr, dtype=np.float64).tobytes())

@@ -1,4 +1,5 @@
-"""MatrixMarket coordinate I/O for the assembly path.
+"""MatrixMarket coordinate I/O and the bench CSV writer
+(rank 2).
 
 Same file contract as the reference (mmio.py:43-137): header
 ``%%MatrixMarket matrix coordinate real|integer general``, a size line
@@ -111,3 +112,19 @@ def write_csc_matrixmarket(mat: CscMatrix, path) -> None:
                                                          np.asarray(mat.pr).tolist())]
     with open(path, "w") as fh:
         fh.write("\n".join([HEADER, f"{mat.m} {mat.n} {len(rows)}", *rows]) + "\n")
+
+
+# the reference's bench CSV schema (mmio.py:19-31, 140-146)
+BENCH_CSV_COLUMNS = ["dataset_id", "impl", "threads", "mean_seconds", "min_seconds", "reps", "L",
+                     "M", "N", "nnz", "speedup_vs_serial"]
+
+
+def write_bench_csv(results, path) -> None:
+    """One row per timed (dataset, implementation, threads) combination."""
+    import csv
+
+    with open(path, "w", newline="") as fh:
+        w = csv.DictWriter(fh, fieldnames=BENCH_CSV_COLUMNS)
+        w.writeheader()
+        for r in results:
+            w.writerow({c: getattr(r, c) for c in BENCH_CSV_COLUMNS})

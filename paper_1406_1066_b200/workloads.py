@@ -171,3 +171,42 @@ CONFIG_NAMES = {
     4: "cfg4 heavy-dup m=n=1e7, 1e8 positions x Poisson(5) (L~5e8)",
     5: "cfg5 sharded 2D P1 FEM N=8000 (L=1.152e9)",
 }
+
+
+# --- the reference's own benchmark datasets ---------------------------------
+# bench.py:27-32 (_DATASETS), 48-59 (dataset_config), 62-81 (gen_ransparse):
+# every row draws nnz_row uniform columns, the block is tiled nrep times,
+# one global permutation shuffles it, all values 1.0.  Same numpy Generator
+# calls in the same order, so the same seed gives the same bits.
+
+RANSPARSE_SEED = 20151023
+RANSPARSE_DATASETS = {1: (10_000, 50, 5), 2: (50_000, 50, 1), 3: (50_000, 10, 5)}
+
+
+def ransparse_spec(ds_id: int, scale: float = 1.0) -> tuple[int, int, int]:
+    """(siz, nnz_row, nrep) of standard dataset ``ds_id``; ``scale`` shrinks
+    the matrix size linearly (bench.py:48-59)."""
+    if ds_id not in RANSPARSE_DATASETS:
+        raise ValueError(f"dataset id {ds_id} not in {sorted(RANSPARSE_DATASETS)}")
+    if not 0.0 < scale <= 1.0:
+        raise ValueError(f"scale {scale} outside (0, 1]")
+    siz, nnz_row, nrep = RANSPARSE_DATASETS[ds_id]
+    return max(1, round(siz * scale)), nnz_row, nrep
+
+
+def ransparse(siz: int, nnz_row: int, nrep: int = 1, seed: int = RANSPARSE_SEED):
+    """Host (numpy) triplets ``(ii, jj, s)`` of the reference generator
+    (bench.py:62-81): int32, int32, float64 (all ones); ``siz`` x ``siz``."""
+    import numpy as np
+
+    if siz < 1 or nnz_row < 1 or nrep < 1:
+        raise ValueError(f"non-positive generator parameters ({siz}, {nnz_row}, {nrep})")
+    rng = np.random.default_rng(seed)
+    block = siz * nnz_row
+    rows = np.tile(np.arange(1, siz + 1, dtype=np.int32), nnz_row)
+    cols = rng.integers(1, siz + 1, size=block, dtype=np.int32)
+    rows = np.tile(rows, nrep)
+    cols = np.tile(cols, nrep)
+    perm = rng.permutation(len(rows))
+    return (np.ascontiguousarray(rows[perm]), np.ascontiguousarray(cols[perm]),
+            np.ones(len(rows), dtype=np.float64))

@@ -2,6 +2,8 @@
 outputs (golden fixtures) and the CPU oracle.  Bar: jc/ir bit-exact and pr
 bit-exact (ordered-sum contract), NaN payloads included."""
 
+import os
+
 import numpy as np
 import pytest
 
@@ -472,3 +474,95 @@ def test_long_columns_with_spans_beyond_the_packed_key():
                                                   m=2**31 - 1, n=2_000_000).to_host()
     ref = O.assemble_sorted(ii, jj, s, 2**31 - 1, 2_000_000)
     _same(got, ref)
+
+
+def _dataset_digests():
+    import json
+
+    with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden",
+                           "dataset_digests.json")) as f:
+        return json.load(f)
+
+
+@pytest.mark.parametrize("k", range(6))
+def test_reference_bench_datasets_bit_exact(k):
+    """The reference's own benchmark datasets (bench.py:27-81, values all 1.0,
+    heavy duplication): GPU output == the reference's assemble_serial output
+    (tests/golden/dataset_digests.json)."""
+    from paper_1406_1066_b200 import workloads as W
+
+    d = _dataset_digests()[k]
+    ii, jj, s = W.ransparse(d["siz"], d["nnz_row"], d["nrep"], d["seed"])
+    out = sa.assemble(ii, jj, s)
+    assert (out.m, out.n, out.nnz) == (d["m"], d["n"], d["nnz"])
+    assert output_digest(out.jc, out.ir, out.pr) == d["output"]
+
+
+def _oracle_checkers():
+    def check(ii, jj, s, m, n):
+        ii = np.asarray(ii)
+        jj = np.asarray(jj)
+        if m is None:
+            m = int(ii.max()) if len(ii) else 0
+            n = int(jj.max()) if len(jj) else 0
+        return O.assemble_counting(ii.astype(np.int32), jj.astype(np.int32),
+                                   np.asarray(s, dtype=np.float64), m, n)
+    return [("oracle", check)]
+
+
+def test_cli_assemble_verify_bench(tmp_path, monkeypatch, capsys):
+    """The CLI end to end on the GPU: gen -> assemble (+ --prune-zeros) ->
+    the written CSC equals the oracle's; verify --random / --input with the
+    test oracle standing in for the reference package (exit 0, and exit 2 on
+    a planted mismatch); bench writes the reference's CSV schema."""
+    import csv
+
+    from paper_1406_1066_b200 import cli
+    from paper_1406_1066_b200 import workloads as W
+    from paper_1406_1066_b200.mmio import BENCH_CSV_COLUMNS
+
+    t = tmp_path / "t.mtx"
+    a = tmp_path / "a.mtx"
+    assert cli.main(["gen", "--size", "300", "--nnz-row", "4", "--nrep", "3", "--out", str(t)]) == 0
+    assert cli.main(["assemble", "--input", str(t), "--output", str(a)]) == 0
+    ii, jj, s = W.ransparse(300, 4, 3)
+    ref = O.assemble_counting(ii, jj, s, 300, 300)
+    lines = a.read_text().splitlines()
+    assert lines[1] == f"300 300 {len(ref.ir)}"
+    rr = np.array([list(map(float, x.split())) for x in lines[2:]])
+    assert np.array_equal(rr[:, 0].astype(np.int64) - 1, ref.ir)
+    assert np.array_equal(rr[:, 1].astype(np.int64) - 1, np.repeat(np.arange(300), np.diff(ref.jc)))
+    assert np.array_equal(rr[:, 2], ref.pr)
+    # explicit larger shape and pruning (values are all >= 1: nothing dropped)
+    assert cli.main(["assemble", "--input", str(t), "--output", str(a), "--m", "310", "--n", "305",
+                     "--prune-zeros"]) == 0
+    assert a.read_text().splitlines()[1].startswith("310 305 ")
+    assert cli.main(["assemble", "--input", str(t), "--output", str(a), "--m", "10", "--n",
+                     "10"]) == 1  # DimensionTooSmall
+
+    dev = torch.device("cuda", 0)
+    with pytest.raises(TypeError):  # the device API takes int32 indices only
+        sa.default_assembler(0).assemble_device(torch.ones(3, dtype=torch.int64, device=dev),
+                                                torch.ones(3, dtype=torch.int32, device=dev),
+                                                torch.ones(3, dtype=torch.float64, device=dev))
+
+    monkeypatch.setattr(cli, "reference_checkers", lambda threads: _oracle_checkers())
+    assert cli.main(["verify", "--random", "12", "--seed", "3"]) == 0
+    assert cli.main(["verify", "--input", str(t)]) == 0
+
+    def wrong(ii, jj, s, m, n):
+        c = _oracle_checkers()[0][1](ii, jj, s, m, n)
+        pr = np.array(c.pr, copy=True)
+        pr[-1] += 1.0
+        return sa.CscMatrix(c.jc, c.ir, pr, c.m, c.n)
+
+    monkeypatch.setattr(cli, "reference_checkers", lambda threads: [("planted", wrong)])
+    assert cli.main(["verify", "--input", str(t)]) == 2
+    assert "first differing pr slot" in capsys.readouterr().err
+
+    b = tmp_path / "b.csv"
+    assert cli.main(["bench", "--dataset", "3", "--scale", "0.02", "--reps", "2", "--out",
+                     str(b)]) == 0
+    rows = list(csv.DictReader(open(b)))
+    assert list(rows[0].keys()) == BENCH_CSV_COLUMNS
+    assert rows[0]["impl"].startswith("b200") and int(rows[0]["nnz"]) == 9965
