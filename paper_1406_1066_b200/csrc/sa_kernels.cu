@@ -887,15 +887,19 @@ cudaError_t launch_scatter(Launch &lc, const Segs &S, int32_t M, int32_t N, uint
 }
 
 // ---------------------------------------------------------------------------
-// k_bigcol: one CTA per big column (grid-stride over the device-side list).
-// The column's entries {row, position} (big space) become keys
-// key = (row-1) << idx_bits | input position in two 8-byte buffers A|B
-// (the column's 16-byte slots of the big scratch).  Stable LSD radix
-// passes (8-bit digits, warp match + per-warp digit counts) sort by (row,
-// position); values are gathered from the input by position; each run of
-// equal rows is folded from +0.0 in position order.  Results: row-1 in the
-// key buffer, value bits in the other buffer, at index = run number;
-// bigu[c] = runs | (BIGFLAG if keys ended in buffer B).
+// k_bigcol: columns longer than BIGCOL (grid-stride over the device-side
+// list).  Results: row-1 in the key buffer, value bits in the other buffer,
+// at index = run number; bigu[c] = runs | (BIGFLAG if keys ended in buffer
+// B).  The column's two 8-byte buffers A|B are its 16-byte slots of the big
+// scratch.  Two paths by length:
+//  * medium (n <= MED_CAP): one 256-thread quarter of the CTA per column
+//    (named barrier per quarter), entirely in shared memory: keys
+//    (row-1) << idx_bits | input position, bitonic sort, values gathered by
+//    position, each run of equal rows folded from +0.0 in position order by
+//    the thread owning its head, heads compacted by a quarter-wide scan;
+//  * long: the whole CTA, keys in A|B, stable LSD radix passes (8-bit
+//    digits, warp match + per-warp digit counts), values gathered into the
+//    other buffer, runs folded and compacted in place.
 // ---------------------------------------------------------------------------
 constexpr int BIG_NT = 1024;
 constexpr int BIG_NW = BIG_NT / 32;
@@ -948,23 +952,123 @@ __device__ __forceinline__ void big_radix_pass(const unsigned long long *src,
     __syncthreads();
 }
 
-__global__ void __launch_bounds__(BIG_NT) k_bigcol(BigCol *__restrict__ big_list,
+constexpr int MED_NT = 256;                 // threads per medium-column quarter
+constexpr int MED_Q = BIG_NT / MED_NT;      // quarters per CTA
+constexpr int MED_CAP = 1024;               // longest medium column
+constexpr size_t BIG_DSMEM = (size_t)MED_Q * 2 * MED_CAP * sizeof(unsigned long long);
+
+__device__ __forceinline__ void quarter_sync(int q) {
+    asm volatile("bar.sync %0, %1;" ::"r"(q + 1), "n"(MED_NT) : "memory");
+}
+
+// One medium column (n <= MED_CAP) by quarter q (threads qt = 0..MED_NT-1).
+__device__ __forceinline__ void med_column(BigCol *bcp, uint32_t st, int n, unsigned long long *A,
+                                           const uint2 *__restrict__ perm, const Segs &S,
+                                           int idx_bits, unsigned long long *K,
+                                           unsigned long long *V, uint32_t *s_qw, int q, int qt) {
+    const unsigned long long idx_mask = (1ull << idx_bits) - 1;
+    int np2 = 32;
+    while (np2 < n) np2 <<= 1;
+    for (int p = qt; p < np2; p += MED_NT) {
+        unsigned long long key = ~0ull;
+        if (p < n) {
+            const uint2 e = perm[st + p];
+            key = ((unsigned long long)(e.x - 1u) << idx_bits) | e.y;
+        }
+        K[p] = key;
+    }
+    quarter_sync(q);
+    for (int k = 2; k <= np2; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int t = qt; t < (np2 >> 1); t += MED_NT) {
+                const int i = ((t & ~(j - 1)) << 1) | (t & (j - 1));
+                const unsigned long long a = K[i], b = K[i + j];
+                if ((a > b) == ((i & k) == 0)) {
+                    K[i] = b;
+                    K[i + j] = a;
+                }
+            }
+            quarter_sync(q);
+        }
+    }
+    for (int p = qt; p < n; p += MED_NT)
+        V[p] = (unsigned long long)__double_as_longlong(*seg_value(S, (int64_t)(K[p] & idx_mask)));
+    quarter_sync(q);
+    // thread qt owns entries [4 qt, 4 qt + 4) (MED_CAP = 4 * MED_NT)
+    constexpr int PER = MED_CAP / MED_NT;
+    const int p0 = PER * qt;
+    bool head[PER];
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+        const int p = p0 + u;
+        head[u] = p < n && (p == 0 || (K[p] >> idx_bits) != (K[p - 1] >> idx_bits));
+        cnt += head[u];
+    }
+    // quarter-wide exclusive scan of the head counts
+    const int lane = qt & 31, w = qt >> 5;
+    uint32_t incl = cnt;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t y = __shfl_up_sync(FULL, incl, d);
+        if (lane >= d) incl += y;
+    }
+    if (lane == 31) s_qw[w] = incl;
+    quarter_sync(q);
+    uint32_t run = incl - cnt;
+    for (int k = 0; k < w; ++k) run += s_qw[k];
+    unsigned long long *B = A + n;
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+        if (!head[u]) continue;
+        const int p = p0 + u;
+        const unsigned long long row = K[p] >> idx_bits;
+        double acc = fold_add(0.0, __longlong_as_double((long long)V[p]));
+        for (int r = p + 1; r < n && (K[r] >> idx_bits) == row; ++r)
+            acc = fold_add(acc, __longlong_as_double((long long)V[r]));
+        A[run] = row;
+        B[run] = (unsigned long long)__double_as_longlong(acc);
+        ++run;
+    }
+    if (qt == MED_NT - 1) {
+        bcp->start = st;  // absolute from here on
+        bcp->u = run;     // keys in A
+    }
+    quarter_sync(q);  // K, V and s_qw are free for the next column
+}
+
+__global__ void __launch_bounds__(BIG_NT, 2) k_bigcol(BigCol *__restrict__ big_list,
                                                    const ErrState *err, int4 *rec,
                                                    const uint2 *__restrict__ perm, Segs S,
-                                                   int idx_bits, int passes) {
+                                                   int idx_bits, int passes, int med_cap) {
     __shared__ uint32_t s_cnt[BIG_NW][256];
     __shared__ uint32_t s_warp[BIG_NW];
     __shared__ unsigned long long s_prevrow;
+    extern __shared__ unsigned long long s_med[];  // [MED_Q][2 * MED_CAP]
     const int tid = threadIdx.x;
     pdl_wait();
     pdl_trigger();
     const unsigned nbig = *((volatile const unsigned *)&err->nbig);
-    if (blockIdx.x >= nbig) return;
+    if (blockIdx.x >= nbig) return;  // no column for this CTA in either loop
     const unsigned lsmall = *((volatile const unsigned *)&err->lsmall);
     const unsigned long long idx_mask = (1ull << idx_bits) - 1;
+    {  // medium columns: one quarter each
+        const int q = tid / MED_NT, qt = tid % MED_NT;
+        unsigned long long *K = s_med + (size_t)q * 2 * MED_CAP;
+        uint32_t *s_qw = &s_cnt[0][0] + q * (MED_NT / 32);
+        for (unsigned kb = blockIdx.x * MED_Q + q; kb < nbig; kb += gridDim.x * MED_Q) {
+            const int n = (int)big_list[kb].n;
+            if (n > med_cap) continue;
+            const uint32_t st = big_list[kb].start + lsmall;
+            med_column(&big_list[kb], st, n, reinterpret_cast<unsigned long long *>(rec + st), perm,
+                       S, idx_bits, K, K + MED_CAP, s_qw, q, qt);
+        }
+    }
+    __syncthreads();
     for (unsigned kb = blockIdx.x; kb < nbig; kb += gridDim.x) {
-        const uint32_t st = big_list[kb].start + lsmall;
         const int64_t n = big_list[kb].n;
+        if (n <= med_cap) continue;
+        const uint32_t st = big_list[kb].start + lsmall;
         unsigned long long *A = reinterpret_cast<unsigned long long *>(rec + st);
         unsigned long long *B = A + n;
         // entries {row, position} -> keys in A (8 loads per thread in flight)
@@ -1061,9 +1165,18 @@ __global__ void __launch_bounds__(BIG_NT) k_bigcol(BigCol *__restrict__ big_list
 
 cudaError_t launch_bigcol(Launch &lc, BigCol *big_list, const ErrState *err, int4 *rec,
                           const uint2 *perm, const Segs &S, int idx_bits, int passes) {
-    int grid = lc.num_sms;
-    cudaError_t e = launch_pdl(k_bigcol, dim3(grid), dim3(BIG_NT), 0, lc.stream, big_list, err, rec, perm, S,
-                               idx_bits, passes);
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(k_bigcol, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)BIG_DSMEM);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    static int gmul = getenv("SA_BIG_GRID") ? atoi(getenv("SA_BIG_GRID")) : 2;
+    static int med = getenv("SA_BIG_MED") ? atoi(getenv("SA_BIG_MED")) : 1;
+    int grid = gmul * lc.num_sms;
+    cudaError_t e = launch_pdl(k_bigcol, dim3(grid), dim3(BIG_NT), med ? BIG_DSMEM : 0, lc.stream,
+                               big_list, err, rec, perm, S, idx_bits, passes, med ? MED_CAP : 0);
     if (e != cudaSuccess) return e;
     lc.launches++;
     return cudaGetLastError();

@@ -1,5 +1,5 @@
 """Per-tile timeline of k_tile_fold (library built with -DSA_TRACE).
-usage: python tools/fold_trace.py path/to/libsa_trace.so [config]
+usage: python tools/fold_trace.py path/to/libsa_trace.so [config | dsK]
 Stamps: 0 start, 1 entries in (TMA), 2 networks done, 3 values in, 4 count
 published, 5 values folded, 6 look-back done, 7 outputs written."""
 import ctypes, os, sys
@@ -10,7 +10,12 @@ lib = ctypes.CDLL(sys.argv[1])
 for name, (res, args) in _capi.SIGNATURES.items():
     f = getattr(lib, name); f.restype = res; f.argtypes = args
 ctx = ctypes.c_void_p(); lib.sa_create(0, ctypes.byref(ctx))
-w = W.config(int(sys.argv[2]) if len(sys.argv) > 2 else 2, device="cuda")
+cfg = sys.argv[2] if len(sys.argv) > 2 else "2"
+if cfg.startswith("ds"):
+    ii, jj, sv = W.ransparse(*W.ransparse_spec(int(cfg[2:])))
+    w = W.Workload(cfg, torch.from_numpy(ii).cuda(), torch.from_numpy(jj).cuda(), torch.from_numpy(sv).cuda(), int(ii.max()), int(jj.max()))
+else:
+    w = W.config(int(cfg), device="cuda")
 L, M, N = w.L, w.m, w.n
 jc = torch.empty(N + 1, dtype=torch.int32, device="cuda"); ir = torch.empty(L, dtype=torch.int32, device="cuda"); pr = torch.empty(L, dtype=torch.float64, device="cuda")
 s = torch.cuda.current_stream(); lib.sa_set_stream(ctx, ctypes.c_void_p(s.cuda_stream))

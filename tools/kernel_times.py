@@ -1,5 +1,6 @@
 """Per-kernel times (CUDA events inside the C ABI) through a given libsa .so.
-usage: python tools/kernel_times.py path/to/libsa.so [config]"""
+usage: python tools/kernel_times.py path/to/libsa.so [config | ds1 | ds2 | ds3]
+(config = BASELINE cfg 1-5; dsK = the reference's standard dataset K)"""
 import ctypes, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -8,8 +9,13 @@ lib = ctypes.CDLL(sys.argv[1])
 for name, (res, args) in _capi.SIGNATURES.items():
     f = getattr(lib, name); f.restype = res; f.argtypes = args
 ctx = ctypes.c_void_p(); lib.sa_create(0, ctypes.byref(ctx))
-cfg = int(sys.argv[2]) if len(sys.argv) > 2 else 2
-w = W.config(cfg, device="cuda")
+cfg = sys.argv[2] if len(sys.argv) > 2 else "2"
+if cfg.startswith("ds"):
+    ii, jj, sv = W.ransparse(*W.ransparse_spec(int(cfg[2:])))
+    w = W.Workload(cfg, torch.from_numpy(ii).cuda(), torch.from_numpy(jj).cuda(), torch.from_numpy(sv).cuda(), int(ii.max()), int(jj.max()))
+else:
+    cfg = int(cfg)
+    w = W.config(cfg, device="cuda")
 L, M, N = w.L, w.m, w.n
 jc = torch.empty(N + 1, dtype=torch.int32, device="cuda"); ir = torch.empty(L, dtype=torch.int32, device="cuda"); pr = torch.empty(L, dtype=torch.float64, device="cuda")
 s = torch.cuda.current_stream(); lib.sa_set_stream(ctx, ctypes.c_void_p(s.cuda_stream))
@@ -21,4 +27,4 @@ for it in range(12):
     n = lib.sa_last_kernel_times(ctx, 16, arr, names)
     if it >= 2:
         for k in range(n): tot.setdefault(names[k].decode(), []).append(arr[k])
-print(sys.argv[1].split('/')[-1], 'cfg%d' % cfg, {k: round(sum(v)/len(v)*1e3, 1) for k, v in tot.items()})
+print(sys.argv[1].split('/')[-1], 'cfg%s' % cfg, {k: round(sum(v)/len(v)*1e3, 1) for k, v in tot.items()})
