@@ -460,22 +460,22 @@ __device__ void fold_columns_group(int2 *K, double *V, const int *list, int coun
 
 // ---- hash-group fold of one long column by one warp ------------------------
 // Groups the column's entries by row in a per-warp hash table instead of
-// sorting them: distinct rows are ranked by counting (<= HU of them), each
-// group gets its output offset, the entries are placed by group and ranked
-// inside it by input position, and one lane per group folds it from +0.0 in
-// ascending position (the reference's order, _kernels.pyx:82-89).  About
-// 4x fewer instructions than the 64-bit bitonic for FEM-like columns (few
-// distinct rows, each repeated).  Returns false, leaving the column
+// sorting them: distinct rows are ranked by counting (at most HU of them),
+// each group gets its output offset, the entries are placed by group (as
+// {position, entry} in the column's own key slots, free once loaded) and
+// ranked inside it by input position, and one lane per group folds it from
+// +0.0 in ascending position (the reference's order, _kernels.pyx:82-89).
+// Far fewer instructions than the 64-bit bitonic for columns with few
+// distinct rows (FEM, repeated triplets).  Returns false, leaving the column
 // untouched, when it has more than HU distinct rows.
 constexpr int HT = 128;  // hash slots per warp
 constexpr int HU = 64;   // most distinct rows
 struct HashScratch {
-    int row[HT];                // slot -> row (0: empty; rows are >= 1)
-    int cnt[HT];                // slot -> entries
-    uint16_t off[HT];           // slot -> first entry of its group (sorted order)
-    int dl[HU];                 // distinct rows (compacted)
-    uint8_t ds[HU];             // their slots
-    uint8_t mem[LONGCAP];       // entry indices grouped by row, then sorted
+    int row[HT];       // slot -> row (0: empty; rows are >= 1)
+    int cnt[HT];       // slot -> entries
+    uint16_t off[HT];  // slot -> first entry of its group (sorted order)
+    int2 dl[HU];       // distinct rows (compacted): {row, entries}
+    uint8_t ds[HU];    // their slots
 };
 static_assert(sizeof(HashScratch) <= LONGCAP * sizeof(unsigned long long), "per-warp scratch");
 
@@ -483,6 +483,7 @@ __device__ __forceinline__ int row_hash(int r) { return (int)(((unsigned)r * 0x9
 
 __device__ bool fold_column_hash(int2 *Kc, double *Vc, int c, HashScratch &H) {
     constexpr int EPL = LONGCAP / 32;
+    constexpr int IM = LONGCAP - 1;
     const int lane = threadIdx.x & 31;
     const unsigned lt = lanemask_lt();
 #pragma unroll
@@ -506,6 +507,10 @@ __device__ bool fold_column_hash(int2 *Kc, double *Vc, int c, HashScratch &H) {
             pp[q] = e.y;
             const unsigned peers = __match_any_sync(FULL, v ? e.x : 0);
             const int leader = __ffs(peers) - 1;
+            // a short column whose first 32 rows are mostly distinct is
+            // cheaper in the 4-columns-per-warp bitonic
+            if (q == 0 && c <= 64 && __popc(__ballot_sync(FULL, v && lane == leader)) >= 24)
+                return false;
             int h = 0, a = 0;
             if (v && lane == leader) {
                 h = row_hash(e.x);
@@ -535,7 +540,7 @@ __device__ bool fold_column_hash(int2 *Kc, double *Vc, int c, HashScratch &H) {
         const unsigned bal = __ballot_sync(FULL, r != 0);
         const int k = D + __popc(bal & lt);
         if (r != 0 && k < HU) {
-            H.dl[k] = r;
+            H.dl[k] = make_int2(r, H.cnt[s]);
             H.ds[k] = (uint8_t)s;
         }
         D += __popc(bal);
@@ -543,32 +548,33 @@ __device__ bool fold_column_hash(int2 *Kc, double *Vc, int c, HashScratch &H) {
     if (__any_sync(FULL, over) || D > HU) return false;
     __syncwarp();
     // rank and group offset of distinct rows lane and lane + 32
-    const int ra = lane < D ? H.dl[lane] : 0x7fffffff;
-    const int rb = lane + 32 < D ? H.dl[lane + 32] : 0x7fffffff;
+    const int ra = lane < D ? H.dl[lane].x : 0x7fffffff;
+    const int rb = lane + 32 < D ? H.dl[lane + 32].x : 0x7fffffff;
     int ka = 0, kb = 0, oa = 0, ob = 0;
     for (int k = 0; k < D; ++k) {
-        const int x = H.dl[k];
-        const int n = H.cnt[H.ds[k]];
-        if (x < ra) {
+        const int2 x = H.dl[k];
+        if (x.x < ra) {
             ++ka;
-            oa += n;
+            oa += x.y;
         }
-        if (x < rb) {
+        if (x.x < rb) {
             ++kb;
-            ob += n;
+            ob += x.y;
         }
     }
     const int sa_ = lane < D ? H.ds[lane] : 0, sb_ = lane + 32 < D ? H.ds[lane + 32] : 0;
     if (lane < D) H.off[sa_] = (uint16_t)oa;
     if (lane + 32 < D) H.off[sb_] = (uint16_t)ob;
     __syncwarp();
-    // place the entries by group (arrival order), then rank them by position
+    // members grouped by row, {position, entry}, in the column's key slots
+    int2 *M = Kc;
 #pragma unroll
     for (int q = 0; q < EPL; ++q) {
         const int i = q * 32 + lane;
-        if (q < nb && i < c) H.mem[(H.off[hs[q] & 255] + (hs[q] >> 8)) & (LONGCAP - 1)] = (uint8_t)i;
+        if (q < nb && i < c) M[(H.off[hs[q] & 255] + (hs[q] >> 8)) & IM] = make_int2(pp[q], i);
     }
     __syncwarp();
+    // rank inside the group by input position
     int fi[EPL];
 #pragma unroll
     for (int q = 0; q < EPL; ++q) {
@@ -577,29 +583,33 @@ __device__ bool fold_column_hash(int2 *Kc, double *Vc, int c, HashScratch &H) {
         if (q < nb && i < c) {
             const int s = hs[q] & 255;
             const int b0 = H.off[s], n = H.cnt[s];
-            int r = 0;
-            for (int k = b0; k < b0 + n; ++k) r += Kc[H.mem[k & (LONGCAP - 1)]].y < pp[q];
-            fi[q] = (b0 + r) & (LONGCAP - 1);
+            const int me = pp[q];
+            int r = 0, k = b0;
+            for (; k + 4 <= b0 + n; k += 4)
+                r += (M[k & IM].x < me) + (M[(k + 1) & IM].x < me) + (M[(k + 2) & IM].x < me) +
+                     (M[(k + 3) & IM].x < me);
+            for (; k < b0 + n; ++k) r += M[k & IM].x < me;
+            fi[q] = (b0 + r) & IM;
         }
     }
     __syncwarp();
 #pragma unroll
     for (int q = 0; q < EPL; ++q) {
         const int i = q * 32 + lane;
-        if (q < nb && i < c) H.mem[fi[q]] = (uint8_t)i;
+        if (q < nb && i < c) M[fi[q]].y = i;
     }
     __syncwarp();
     // one lane per group folds it in position order
     double acc_a = 0.0, acc_b = 0.0;
     if (lane < D) {
-        const int n = H.cnt[sa_];
-        acc_a = fold_add(0.0, Vc[H.mem[oa & (LONGCAP - 1)]]);
-        for (int k = 1; k < n; ++k) acc_a = fold_add(acc_a, Vc[H.mem[(oa + k) & (LONGCAP - 1)]]);
+        const int n = H.dl[lane].y;
+        acc_a = fold_add(0.0, Vc[M[oa & IM].y & IM]);
+        for (int k = 1; k < n; ++k) acc_a = fold_add(acc_a, Vc[M[(oa + k) & IM].y & IM]);
     }
     if (lane + 32 < D) {
-        const int n = H.cnt[sb_];
-        acc_b = fold_add(0.0, Vc[H.mem[ob & (LONGCAP - 1)]]);
-        for (int k = 1; k < n; ++k) acc_b = fold_add(acc_b, Vc[H.mem[(ob + k) & (LONGCAP - 1)]]);
+        const int n = H.dl[lane + 32].y;
+        acc_b = fold_add(0.0, Vc[M[ob & IM].y & IM]);
+        for (int k = 1; k < n; ++k) acc_b = fold_add(acc_b, Vc[M[(ob + k) & IM].y & IM]);
     }
     __syncwarp();
     if (lane < D) {
@@ -775,13 +785,28 @@ __global__ void __launch_bounds__(NT, 5) k_tile_fold(const uint32_t *__restrict_
         const int n0 = min(S.ncls[0], LCAP), n1 = min(S.ncls[1], LCAP), n2 = min(S.ncls[2], LCAP);
         HashScratch &H = *reinterpret_cast<HashScratch *>(S.skey[warp]);
         for (int t = warp; t < n0 + n1 + n2; t += NWARP) {
-            const int *ent = (t < n0) ? &S.lcol[0][t] : (t < n0 + n1) ? &S.lcol[1][t - n0]
-                                                                     : &S.lcol[2][t - n0 - n1];
+            int *ent = (t < n0) ? &S.lcol[0][t] : (t < n0 + n1) ? &S.lcol[1][t - n0]
+                                                               : &S.lcol[2][t - n0 - n1];
             const int v = *ent;
-            if (!fold_column_hash(&K[v & 0xffff], &V[v & 0xffff], v >> 16, H))
-                fold_columns_group<32, 8>(K, V, ent, 1, S.skey[warp], S.lcol[3], &S.ncls[3]);
+            const bool ok = fold_column_hash(&K[v & 0xffff], &V[v & 0xffff], v >> 16, H);
+            if (!ok && lane == 0) *ent = v | (int)0x80000000u;  // left for the bitonic
         }
-    } else {
+        __syncthreads();
+        if (warp < 3) {  // keep only the marked entries, in order
+            const int n = min(S.ncls[warp], LCAP);
+            int kept = 0;
+            for (int base = 0; base < n; base += 32) {
+                const int e = (base + lane < n) ? S.lcol[warp][base + lane] : 0;
+                const unsigned bal = __ballot_sync(FULL, e < 0);
+                __syncwarp();
+                if (e < 0) S.lcol[warp][kept + __popc(bal & lanemask_lt())] = e & 0x7fffffff;
+                kept += __popc(bal);
+            }
+            if (lane == 0) S.ncls[warp] = kept;
+        }
+        __syncthreads();
+    }
+    {
         const int n0 = min(S.ncls[0], LCAP), n1 = min(S.ncls[1], LCAP), n2 = min(S.ncls[2], LCAP);
         const int b0 = (n0 + 3) / 4, b1 = (n1 + 1) / 2;
         for (int t = warp; t < b0 + b1 + n2; t += NWARP) {
