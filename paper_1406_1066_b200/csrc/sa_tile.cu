@@ -68,6 +68,7 @@ struct TileSmem {
     uint32_t scol[SCAP];               // sstart of the tile's columns (when they fit)
     unsigned long long mbar;
     int warp_u[NWARP];
+    int warp_b[NWARP];
     long long P;
 };
 
@@ -667,6 +668,7 @@ __device__ long long lookback_warp32(unsigned long long *st, long long b, unsign
 
 }  // namespace
 
+template <bool STAGED>
 __global__ void __launch_bounds__(NT, 5) k_tile_fold(const uint32_t *__restrict__ sstart,
                                                      const int2 *__restrict__ tile_info,
                                                      const uint8_t *__restrict__ tile_big,
@@ -679,7 +681,9 @@ __global__ void __launch_bounds__(NT, 5) k_tile_fold(const uint32_t *__restrict_
                                                      int32_t *__restrict__ jc,
                                                      int32_t *__restrict__ ir,
                                                      double *__restrict__ pr, int64_t cap,
-                                                     ErrState *err, int hash_fold) {
+                                                     ErrState *err, int hash_fold,
+                                                     int4 *__restrict__ stage,
+                                                     int2 *__restrict__ tile_cnt) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     TileSmem &S = *reinterpret_cast<TileSmem *>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -781,7 +785,7 @@ __global__ void __launch_bounds__(NT, 5) k_tile_fold(const uint32_t *__restrict_
     FTRACE(b, 3);
     // ---- pass 2: warps fold the long columns: hash groups, one column per warp;
     // columns with too many distinct rows by the group bitonic, 4 / 2 / 1 per warp
-    if (hash_fold) {
+    if (hash_fold && (S.ncls[0] | S.ncls[1] | S.ncls[2])) {
         const int n0 = min(S.ncls[0], LCAP), n1 = min(S.ncls[1], LCAP), n2 = min(S.ncls[2], LCAP);
         HashScratch &H = *reinterpret_cast<HashScratch *>(S.skey[warp]);
         for (int t = warp; t < n0 + n1 + n2; t += NWARP) {
@@ -832,25 +836,43 @@ __global__ void __launch_bounds__(NT, 5) k_tile_fold(const uint32_t *__restrict_
     __syncthreads();
 
     // ---- tile count and thread output bases; publish the aggregate early ------
-    int ut = 0;
+    int ut = 0, bt = 0;  // outputs of this thread's columns; of its big columns
     for (int c = k_lo; c < k_hi; ++c) {
         const uint32_t w0 = cs[c];
         const int s0 = (int)(w0 & POSMASK), s1 = (int)(cs[c + 1] & POSMASK);
-        if (w0 & BIGFLAG) ut += (int)(big_list[bigk[c_a + c]].u & POSMASK);
-        else if (s1 > s0) ut += K[s0 - r0].y;
+        if (w0 & BIGFLAG) {
+            const int ub = (int)(big_list[bigk[c_a + c]].u & POSMASK);
+            ut += ub;
+            if (STAGED) bt += ub;
+        } else if (s1 > s0) {
+            ut += K[s0 - r0].y;
+        }
     }
     const int inc = warp_incl_sum(ut);
-    if (lane == 31) S.warp_u[warp] = inc;
+    const int incb = (STAGED && has_big) ? warp_incl_sum(bt) : 0;
+    if (lane == 31) {
+        S.warp_u[warp] = inc;
+        S.warp_b[warp] = incb;
+    }
     __syncthreads();
-    int wpre = 0, U = 0;
+    int wpre = 0, U = 0, bpre = 0, UB = 0;
 #pragma unroll
     for (int k = 0; k < NWARP; ++k) {
-        const int v = S.warp_u[k];
-        if (k < warp) wpre += v;
+        const int v = S.warp_u[k], vb = S.warp_b[k];
+        if (k < warp) {
+            wpre += v;
+            bpre += vb;
+        }
         U += v;
+        UB += vb;
     }
     const int tbase = wpre + inc - ut;  // this thread's first output, tile-local
-    if (tid == 0) lookback_publish(tile_state, b, (unsigned long long)U);
+    // staged: this thread's first small-column output among the tile's staged ones
+    const int sbase = tbase - (bpre + incb - bt);
+    if (tid == 0) {
+        if (STAGED) tile_cnt[b] = make_int2(U, U - UB);
+        else lookback_publish(tile_state, b, (unsigned long long)U);
+    }
     FTRACE(b, 4);
 
     // ---- pass 3: fold the short columns' values; output map -------------------
@@ -875,8 +897,8 @@ __global__ void __launch_bounds__(NT, 5) k_tile_fold(const uint32_t *__restrict_
         }
     }
     FTRACE(b, 5);
-    if (warp == 0) {
-        const long long P = lookback_warp32(tile_state, b, (unsigned long long)U);
+    if (warp == 0) {  // staged: tile-local outputs, k_tile_emit adds the tile offset
+        const long long P = STAGED ? 0 : lookback_warp32(tile_state, b, (unsigned long long)U);
         if (lane == 0) S.P = P;
     }
     __syncthreads();
@@ -893,6 +915,7 @@ __global__ void __launch_bounds__(NT, 5) k_tile_fold(const uint32_t *__restrict_
     __syncthreads();
     {
         long long o = P + tbase;
+        int so = sbase;  // staged index of the next small-column output
         for (int c = k_lo; c < k_hi; ++c) {
             jc[c_a + c] = (int32_t)o;
             const uint32_t w0 = cs[c];
@@ -901,6 +924,10 @@ __global__ void __launch_bounds__(NT, 5) k_tile_fold(const uint32_t *__restrict_
                 const uint32_t kb = bigk[c_a + c];
                 const BigCol bc = big_list[kb];
                 const int ub = (int)(bc.u & POSMASK);
+                if (STAGED) {  // copied by k_tile_emit
+                    o += ub;
+                    continue;
+                }
                 const int e = atomicAdd(&S.ncls[0], 1);
                 if (e < BCAP) {
                     bcopy[2 * e] = (int)(o - P);
@@ -922,7 +949,16 @@ __global__ void __launch_bounds__(NT, 5) k_tile_fold(const uint32_t *__restrict_
             } else if (s1 > s0) {
                 const int off = s0 - r0;
                 const int u = K[off].y;
-                if (has_big) {
+                if (STAGED && has_big) {
+                    const bool shrt = s1 - s0 <= SHORT_COL;
+                    for (int k = 0; k < u; ++k) {
+                        const int sl = off + (shrt ? S.perm[off + k] : k);
+                        const long long vb = __double_as_longlong(V[sl]);
+                        stage[r0 + so + k] = make_int4(K[sl].x, (int)(unsigned)vb,
+                                                       (int)(unsigned)(vb >> 32), (int)(o + k));
+                    }
+                    so += u;
+                } else if (has_big) {
                     const bool shrt = s1 - s0 <= SHORT_COL;
                     for (int k = 0; k < u; ++k) {
                         const int sl = off + (shrt ? S.perm[off + k] : k);
@@ -971,7 +1007,13 @@ __global__ void __launch_bounds__(NT, 5) k_tile_fold(const uint32_t *__restrict_
         }
     }
     // ---- coalesced row indices and values ---------------------------------------
-    if (!has_big) {
+    if (STAGED && !has_big) {
+        for (int x = tid; x < U; x += NT) {
+            const int sl = S.omap[x];
+            const long long vb = __double_as_longlong(V[sl]);
+            stage[r0 + x] = make_int4(K[sl].x, (int)(unsigned)vb, (int)(unsigned)(vb >> 32), x);
+        }
+    } else if (!has_big) {
         for (int x = tid; x < U; x += NT) {
             const int sl = S.omap[x];
             if (P + x < cap) {
@@ -984,10 +1026,127 @@ __global__ void __launch_bounds__(NT, 5) k_tile_fold(const uint32_t *__restrict_
     }
     if (over) atomicExch(&err->cap_exceeded, 1u);
     FTRACE(b, 7);
-    if (b == ntiles - 1 && tid == 0) {
+    if (!STAGED && b == ntiles - 1 && tid == 0) {
         jc[N] = (int32_t)(P + U);
         err->nnz = P + U;
         if (P + U > cap) atomicExch(&err->cap_exceeded, 1u);
+    }
+}
+
+// ---- staged outputs (long-column inputs): no look-back in k_tile_fold ------
+// With many long columns a tile spends a fifth of its life waiting for its
+// predecessors' counts.  In staged mode k_tile_fold writes each tile's
+// small-column outputs as {row, value, tile-local index} records into the
+// free small space of the record scratch (tile b at its record start), and
+// its column pointers tile-local; k_tile_scan turns the tile counts into
+// offsets and k_tile_emit copies every tile to its place (and the big
+// columns from the big space), adding the offset to the column pointers.
+
+constexpr int TSCAN_NT = 1024;
+
+__global__ void __launch_bounds__(TSCAN_NT) k_tile_scan(const int2 *__restrict__ tile_cnt,
+                                                        int64_t ntiles,
+                                                        long long *__restrict__ tile_off) {
+    __shared__ long long s_warp[TSCAN_NT / 32];
+    __shared__ long long s_carry;
+    pdl_wait();
+    pdl_trigger();
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) s_carry = 0;
+    __syncthreads();
+    for (int64_t base = 0; base < ntiles; base += TSCAN_NT) {
+        const int64_t b = base + tid;
+        const long long v = (b < ntiles) ? (long long)tile_cnt[b].x : 0;
+        long long x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const long long y = __shfl_up_sync(FULL, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) s_warp[warp] = x;
+        __syncthreads();
+        long long pre = s_carry, tot = 0;
+        for (int k = 0; k < TSCAN_NT / 32; ++k) {
+            if (k < warp) pre += s_warp[k];
+            tot += s_warp[k];
+        }
+        if (b < ntiles) tile_off[b] = pre + x - v;
+        __syncthreads();
+        if (tid == 0) s_carry += tot;
+        __syncthreads();
+    }
+    if (tid == 0) tile_off[ntiles] = s_carry;
+}
+
+constexpr int EMIT_NT = 256;
+
+__global__ void __launch_bounds__(EMIT_NT) k_tile_emit(
+    const uint32_t *__restrict__ sstart, const int2 *__restrict__ tile_info,
+    const uint8_t *__restrict__ tile_big, int64_t ntiles, const int2 *__restrict__ tile_cnt,
+    const long long *__restrict__ tile_off, const int4 *__restrict__ stage,
+    const int4 *__restrict__ rec, const BigCol *__restrict__ big_list,
+    const uint32_t *__restrict__ bigk, int32_t N, int32_t *__restrict__ jc,
+    int32_t *__restrict__ ir, double *__restrict__ pr, int64_t cap, ErrState *err) {
+    __shared__ int2 s_big[TCAP];  // (tile-local output base, big-list index)
+    __shared__ int s_nbig;
+    pdl_wait();
+    pdl_trigger();
+    const int tid = threadIdx.x;
+    const long long b = blockIdx.x;
+    const int2 ti0 = tile_info[b], ti1 = tile_info[b + 1];
+    const int c_a = ti0.x, r0 = ti0.y, ncols = ti1.x - c_a;
+    const int2 uc = tile_cnt[b];
+    const long long P = tile_off[b];
+    bool over = false;
+    for (int k = tid; k < uc.y; k += EMIT_NT) {
+        const int4 r = stage[r0 + k];
+        const long long x = P + r.w;
+        if (x < cap) {
+            ir[x] = r.x;
+            pr[x] = __hiloint2double(r.z, r.y);
+        } else {
+            over = true;
+        }
+    }
+    const bool has_big = tile_big[b] != 0;
+    if (has_big) {
+        if (tid == 0) s_nbig = 0;
+        __syncthreads();
+    }
+    for (int c = tid; c < ncols; c += EMIT_NT) {
+        const int o = jc[c_a + c];
+        if (has_big && (sstart[c_a + c] & BIGFLAG)) {
+            const int e = atomicAdd(&s_nbig, 1);
+            if (e < TCAP) s_big[e] = make_int2(o, (int)bigk[c_a + c]);
+            else atomicExch(&err->internal, 1u);
+        }
+        jc[c_a + c] = (int32_t)(P + o);
+    }
+    if (has_big) {
+        __syncthreads();
+        const int nb = min(s_nbig, TCAP);
+        for (int e = 0; e < nb; ++e) {
+            const long long o = P + s_big[e].x;
+            const BigCol bc = big_list[s_big[e].y];
+            const int ub = (int)(bc.u & POSMASK);
+            const unsigned long long *RR = reinterpret_cast<const unsigned long long *>(rec + bc.start);
+            const unsigned long long *BK = (bc.u & BIGFLAG) ? RR + bc.n : RR;
+            const unsigned long long *BV = (bc.u & BIGFLAG) ? RR : RR + bc.n;
+            for (int q = tid; q < ub; q += EMIT_NT) {
+                if (o + q < cap) {
+                    ir[o + q] = (int32_t)BK[q];
+                    pr[o + q] = __longlong_as_double((long long)BV[q]);
+                } else {
+                    over = true;
+                }
+            }
+        }
+    }
+    if (over) atomicExch(&err->cap_exceeded, 1u);
+    if (b == ntiles - 1 && tid == 0) {
+        jc[N] = (int32_t)(P + uc.x);
+        err->nnz = P + uc.x;
+        if (P + uc.x > cap) atomicExch(&err->cap_exceeded, 1u);
     }
 }
 
@@ -995,19 +1154,38 @@ cudaError_t launch_tile_fold(Launch &lc, const uint32_t *sstart, const int2 *til
                              const uint8_t *tile_big, int64_t ntiles, const int2 *entries,
                              const Segs &SG, const int4 *rec, const BigCol *big_list,
                              const uint32_t *bigk, unsigned long long *tile_state, int32_t N,
-                             int32_t *jc, int32_t *ir, double *pr, int64_t cap, ErrState *err) {
+                             int32_t *jc, int32_t *ir, double *pr, int64_t cap, ErrState *err,
+                             int4 *stage, int2 *tile_cnt, long long *tile_off) {
     if (ntiles <= 0) return cudaSuccess;
     static const int hash_fold = getenv("SA_HASH_FOLD") ? atoi(getenv("SA_HASH_FOLD")) : 1;
     static bool attr = false;
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(k_tile_fold, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaError_t e = cudaFuncSetAttribute(k_tile_fold<false>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)sizeof(TileSmem));
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(k_tile_fold<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)sizeof(TileSmem));
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    cudaError_t e = launch_pdl(k_tile_fold, dim3((unsigned)ntiles), dim3(NT), sizeof(TileSmem), lc.stream,
-                               sstart, tile_info, tile_big, ntiles, entries, SG, rec, big_list,
-                               bigk, tile_state, N, jc, ir, pr, cap, err, hash_fold);
+    cudaError_t e = stage ? launch_pdl(k_tile_fold<true>, dim3((unsigned)ntiles), dim3(NT),
+                                       sizeof(TileSmem), lc.stream, sstart, tile_info, tile_big,
+                                       ntiles, entries, SG, rec, big_list, bigk, tile_state, N, jc,
+                                       ir, pr, cap, err, hash_fold, stage, tile_cnt)
+                          : launch_pdl(k_tile_fold<false>, dim3((unsigned)ntiles), dim3(NT),
+                                       sizeof(TileSmem), lc.stream, sstart, tile_info, tile_big,
+                                       ntiles, entries, SG, rec, big_list, bigk, tile_state, N, jc,
+                                       ir, pr, cap, err, hash_fold, stage, tile_cnt);
+    lc.launches++;
+    if (e != cudaSuccess || !stage) return e;
+    e = launch_pdl(k_tile_scan, dim3(1), dim3(TSCAN_NT), 0, lc.stream, (const int2 *)tile_cnt, ntiles,
+                   tile_off);
+    lc.launches++;
+    if (e != cudaSuccess) return e;
+    e = launch_pdl(k_tile_emit, dim3((unsigned)ntiles), dim3(EMIT_NT), 0, lc.stream, sstart, tile_info,
+                   tile_big, ntiles, (const int2 *)tile_cnt, (const long long *)tile_off,
+                   (const int4 *)stage, rec, big_list, bigk, N, jc, ir, pr, cap, err);
     lc.launches++;
     return e;
 }

@@ -566,3 +566,29 @@ def test_cli_assemble_verify_bench(tmp_path, monkeypatch, capsys):
     rows = list(csv.DictReader(open(b)))
     assert list(rows[0].keys()) == BENCH_CSV_COLUMNS
     assert rows[0]["impl"].startswith("b200") and int(rows[0]["nnz"]) == 9965
+
+
+@pytest.mark.parametrize("staged", ["0", "1"])
+def test_output_modes_bit_exact(staged, monkeypatch):
+    """Both output modes of the fold -- chained tile offsets (decoupled
+    look-back) and staged outputs (k_tile_scan + k_tile_emit, chosen for
+    long-column inputs) -- on the sweep subset with big columns, the
+    reference's datasets and scaled FEM / heavy-duplicate workloads."""
+    from paper_1406_1066_b200 import workloads as W
+
+    monkeypatch.setenv("SA_STAGED", staged)
+    kw, rows = sweep("acceptance")
+    for r in rows[:200]:
+        ii, jj, sr = random_triplets(r["seed"], **kw)
+        out = sa.assemble(ii.astype(np.int32), jj.astype(np.int32), sr)
+        assert output_digest(out.jc, out.ir, out.pr) == r["output"], r["seed"]
+    for d in _dataset_digests():
+        ii, jj, s = W.ransparse(d["siz"], d["nnz_row"], d["nrep"], d["seed"])
+        out = sa.assemble(ii, jj, s)
+        assert output_digest(out.jc, out.ir, out.pr) == d["output"], d
+    dev = torch.device("cuda", 0)
+    for w in (W.fem3d(30, device=dev), W.heavy_dup(m=20_000, positions=200_000, device=dev),
+              W.fem2d(64, device=dev)):
+        out = sa.default_assembler(0).assemble_device(w.ii, w.jj, w.s, m=w.m, n=w.n)
+        ref = O.assemble_counting(w.ii.cpu().numpy(), w.jj.cpu().numpy(), w.s.cpu().numpy(), w.m, w.n)
+        _same(out.to_host(), ref)
