@@ -113,7 +113,7 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // packed bitonic key: one lane, row selection (per distinct row, ascending:
 // gather its records to the front ordered by position, fold).  Outputs
 // (row-1, u) in K[0..u), values in V[0..u).
-__device__ int fold_column_serial(int2 *K, double *V, int c) {
+__device__ __noinline__ int fold_column_serial(int2 *K, double *V, int c) {
     int u = 0;
     int k = 0;
     while (k < c) {
@@ -361,7 +361,7 @@ __device__ __forceinline__ void group_bitonic(unsigned long long (&k)[E]) {
 // Outputs (row-1, u) in K[off..off+u), values in V[off..off+u).  A column
 // whose spans do not fit 64 bits is appended to `fb` instead.
 template <int G, int E>
-__device__ void fold_columns_group(int2 *K, double *V, const int *list, int count,
+__device__ __noinline__ void fold_columns_group(int2 *K, double *V, const int *list, int count,
                                    unsigned long long *skey, int *fb, int *nfb) {
     constexpr int P = G * E;
     constexpr int SB = (P <= 32) ? 5 : (P <= 64) ? 6 : (P <= 128) ? 7 : 8;
@@ -471,6 +471,7 @@ __device__ void fold_columns_group(int2 *K, double *V, const int *list, int coun
 // untouched, when it has more than HU distinct rows.
 constexpr int HT = 128;  // hash slots per warp
 constexpr int HU = 64;   // most distinct rows
+constexpr int BIGG = 16;  // groups above this size (up to 64) are sorted, not ranked
 struct HashScratch {
     int row[HT];       // slot -> row (0: empty; rows are >= 1)
     int cnt[HT];       // slot -> entries
@@ -481,6 +482,52 @@ struct HashScratch {
 static_assert(sizeof(HashScratch) <= LONGCAP * sizeof(unsigned long long), "per-warp scratch");
 
 __device__ __forceinline__ int row_hash(int r) { return (int)(((unsigned)r * 0x9E3779B1u) >> 25); }
+
+// Groups of BIGG < n <= 64 members of a hash-folded column (ballots bga /
+// bgb over the distinct rows lane / lane + 32): each sorted by input
+// position with one warp-wide bitonic of {position, entry}.  Out of line:
+// rarely taken, and the fold kernel's code is large.
+__device__ __noinline__ void sort_big_groups(int2 *M, unsigned bga, unsigned bgb, int oa, int ob,
+                                             int na, int nb2) {
+    constexpr int IM = LONGCAP - 1;
+    const int lane = threadIdx.x & 31;
+    while (bga | bgb) {
+        int gb0, g;
+        if (bga) {
+            const int src = __ffs(bga) - 1;
+            bga &= bga - 1;
+            gb0 = __shfl_sync(FULL, oa, src);
+            g = __shfl_sync(FULL, na, src);
+        } else {
+            const int src = __ffs(bgb) - 1;
+            bgb &= bgb - 1;
+            gb0 = __shfl_sync(FULL, ob, src);
+            g = __shfl_sync(FULL, nb2, src);
+        }
+        if (g <= 32) {
+            unsigned long long k1[1];
+            const int2 m = lane < g ? M[(gb0 + lane) & IM] : make_int2(0, 0);
+            k1[0] = lane < g ? ((unsigned long long)(unsigned)m.x << 8) | (unsigned)m.y : ~0ull;
+            group_bitonic<32, 1>(k1);
+            if (lane < g) M[(gb0 + lane) & IM] = make_int2((int)(k1[0] >> 8), (int)(k1[0] & 255));
+        } else {
+            unsigned long long k2[2];
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int x = 2 * lane + e;
+                const int2 m = x < g ? M[(gb0 + x) & IM] : make_int2(0, 0);
+                k2[e] = x < g ? ((unsigned long long)(unsigned)m.x << 8) | (unsigned)m.y : ~0ull;
+            }
+            group_bitonic<32, 2>(k2);
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int x = 2 * lane + e;
+                if (x < g) M[(gb0 + x) & IM] = make_int2((int)(k2[e] >> 8), (int)(k2[e] & 255));
+            }
+        }
+        __syncwarp();
+    }
+}
 
 __device__ bool fold_column_hash(int2 *Kc, double *Vc, int c, HashScratch &H) {
     constexpr int EPL = LONGCAP / 32;
@@ -575,15 +622,22 @@ __device__ bool fold_column_hash(int2 *Kc, double *Vc, int c, HashScratch &H) {
         if (q < nb && i < c) M[(H.off[hs[q] & 255] + (hs[q] >> 8)) & IM] = make_int2(pp[q], i);
     }
     __syncwarp();
-    // rank inside the group by input position
+    // groups of BIGG < n <= 64 members: one warp-wide bitonic of {position, entry} each
+    const int na = lane < D ? H.dl[lane].y : 0, nb2 = lane + 32 < D ? H.dl[lane + 32].y : 0;
+    unsigned bga = __ballot_sync(FULL, na > BIGG && na <= 64);
+    unsigned bgb = __ballot_sync(FULL, nb2 > BIGG && nb2 <= 64);
+    const bool sorted_groups = (bga | bgb) != 0;
+    if (sorted_groups) sort_big_groups(M, bga, bgb, oa, ob, na, nb2);
+    // the other groups: rank inside the group by input position
     int fi[EPL];
 #pragma unroll
     for (int q = 0; q < EPL; ++q) {
-        fi[q] = 0;
+        fi[q] = -1;
         const int i = q * 32 + lane;
         if (q < nb && i < c) {
             const int s = hs[q] & 255;
             const int b0 = H.off[s], n = H.cnt[s];
+            if (sorted_groups && n > BIGG && n <= 64) continue;  // sorted above
             const int me = pp[q];
             int r = 0, k = b0;
             for (; k + 4 <= b0 + n; k += 4)
@@ -597,18 +651,18 @@ __device__ bool fold_column_hash(int2 *Kc, double *Vc, int c, HashScratch &H) {
 #pragma unroll
     for (int q = 0; q < EPL; ++q) {
         const int i = q * 32 + lane;
-        if (q < nb && i < c) M[fi[q]].y = i;
+        if (q < nb && i < c && (!sorted_groups || fi[q] >= 0)) M[fi[q] & IM].y = i;
     }
     __syncwarp();
     // one lane per group folds it in position order
     double acc_a = 0.0, acc_b = 0.0;
     if (lane < D) {
-        const int n = H.dl[lane].y;
+        const int n = na;
         acc_a = fold_add(0.0, Vc[M[oa & IM].y & IM]);
         for (int k = 1; k < n; ++k) acc_a = fold_add(acc_a, Vc[M[(oa + k) & IM].y & IM]);
     }
     if (lane + 32 < D) {
-        const int n = H.dl[lane + 32].y;
+        const int n = nb2;
         acc_b = fold_add(0.0, Vc[M[ob & IM].y & IM]);
         for (int k = 1; k < n; ++k) acc_b = fold_add(acc_b, Vc[M[(ob + k) & IM].y & IM]);
     }
