@@ -555,10 +555,12 @@ __device__ bool fold_column_hash(int2 *Kc, double *Vc, int c, HashScratch &H) {
             pp[q] = e.y;
             const unsigned peers = __match_any_sync(FULL, v ? e.x : 0);
             const int leader = __ffs(peers) - 1;
-            // a short column whose first 32 rows are mostly distinct is
-            // cheaper in the 4-columns-per-warp bitonic
-            if (q == 0 && c <= 64 && __popc(__ballot_sync(FULL, v && lane == leader)) >= 24)
-                return false;
+            // first 32 rows mostly distinct: a short column is cheaper in the
+            // 4-columns-per-warp bitonic, a longer one will exceed HU rows
+            if (q == 0 && c > 32) {
+                const int nd = __popc(__ballot_sync(FULL, v && lane == leader));
+                if (nd >= (c <= 64 ? 24 : 30)) return false;
+            }
             int h = 0, a = 0;
             if (v && lane == leader) {
                 h = row_hash(e.x);
