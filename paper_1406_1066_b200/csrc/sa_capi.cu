@@ -34,7 +34,6 @@ struct sa_ctx {
     uint8_t *tile_big = nullptr;          size_t tb_cap = 0;      // ntiles
     unsigned long long *tile_state = nullptr; size_t ts_cap = 0;  // ntiles
     int2 *tile_cnt = nullptr;             size_t tc_cap = 0;      // staged fold: {U, small U} per tile
-    long long *tile_off = nullptr;        size_t to_cap = 0;      // staged fold: tile offsets (+1)
     unsigned long long *scan_state = nullptr; size_t ss_cap = 0;  // scan CTAs
     BigCol *big_list = nullptr;           size_t bl_cap = 0;      // L/(BIGCOL+1)+1
     uint32_t *bigk = nullptr;             size_t bk_cap = 0;      // N
@@ -296,7 +295,6 @@ void sa_destroy(sa_ctx *ctx) {
     cudaFree(ctx->tile_big);
     cudaFree(ctx->tile_state);
     cudaFree(ctx->tile_cnt);
-    cudaFree(ctx->tile_off);
     cudaFree(ctx->scan_state);
     cudaFree(ctx->big_list);
     cudaFree(ctx->bigk);
@@ -436,14 +434,12 @@ int assemble_segments(sa_ctx *ctx, const Segs &S, int64_t L, int32_t M, int32_t 
     const bool staged = env ? atoi(env) != 0 : (L >= 64 * (int64_t)N && ntiles >= 16 * ctx->num_sms);
     if (staged) {
         SA_CUDA(ctx, ensure(ctx->tile_cnt, ctx->tc_cap, (size_t)ntiles));
-        SA_CUDA(ctx, ensure(ctx->tile_off, ctx->to_cap, (size_t)ntiles + 1));
     }
     if ((rc = mark(ctx, "k_tile_fold"))) return rc;
     SA_CUDA(ctx, launch_tile_fold(lc, ctx->sstart, ctx->tile_info, ctx->tile_big, ntiles,
                                   reinterpret_cast<const int2 *>(ctx->perm), S, ctx->rec,
                                   ctx->big_list, ctx->bigk, ctx->tile_state, N, d_jc, d_ir, d_pr,
-                                  cap, ctx->err, staged ? ctx->rec : nullptr, ctx->tile_cnt,
-                                  ctx->tile_off));
+                                  cap, ctx->err, staged ? ctx->rec : nullptr, ctx->tile_cnt));
     if ((rc = mark(ctx, nullptr))) return rc;
     ctx->launches = lc.launches;
     return SA_OK;

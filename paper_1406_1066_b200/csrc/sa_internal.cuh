@@ -344,7 +344,7 @@ cudaError_t launch_tile_fold(Launch &lc, const uint32_t *sstart, const int2 *til
                              const BigCol *big_list, const uint32_t *bigk,
                              unsigned long long *tile_state, int32_t N, int32_t *jc, int32_t *ir,
                              double *pr, int64_t cap, ErrState *err, int4 *stage,
-                             int2 *tile_cnt, long long *tile_off);
+                             int2 *tile_cnt);
 
 cudaError_t launch_prune(Launch &lc, const int32_t *jc, const int32_t *ir, const double *pr,
                          int32_t N, int64_t nnz, int32_t *jc_out, int32_t *ir_out,

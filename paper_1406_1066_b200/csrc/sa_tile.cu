@@ -927,7 +927,7 @@ __global__ void __launch_bounds__(NT, 5) k_tile_fold(const uint32_t *__restrict_
     const int sbase = tbase - (bpre + incb - bt);
     if (tid == 0) {
         if (STAGED) tile_cnt[b] = make_int2(U, U - UB);
-        else lookback_publish(tile_state, b, (unsigned long long)U);
+        lookback_publish(tile_state, b, (unsigned long long)U);
     }
     FTRACE(b, 4);
 
@@ -1094,52 +1094,17 @@ __global__ void __launch_bounds__(NT, 5) k_tile_fold(const uint32_t *__restrict_
 // predecessors' counts.  In staged mode k_tile_fold writes each tile's
 // small-column outputs as {row, value, tile-local index} records into the
 // free small space of the record scratch (tile b at its record start), and
-// its column pointers tile-local; k_tile_scan turns the tile counts into
-// offsets and k_tile_emit copies every tile to its place (and the big
+// its column pointers tile-local, and publishes its count; k_tile_emit
+// chains the tile offsets (decoupled look-back over counts that are all
+// already published) and copies every tile to its place (and the big
 // columns from the big space), adding the offset to the column pointers.
-
-constexpr int TSCAN_NT = 1024;
-
-__global__ void __launch_bounds__(TSCAN_NT) k_tile_scan(const int2 *__restrict__ tile_cnt,
-                                                        int64_t ntiles,
-                                                        long long *__restrict__ tile_off) {
-    __shared__ long long s_warp[TSCAN_NT / 32];
-    __shared__ long long s_carry;
-    pdl_wait();
-    pdl_trigger();
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid == 0) s_carry = 0;
-    __syncthreads();
-    for (int64_t base = 0; base < ntiles; base += TSCAN_NT) {
-        const int64_t b = base + tid;
-        const long long v = (b < ntiles) ? (long long)tile_cnt[b].x : 0;
-        long long x = v;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const long long y = __shfl_up_sync(FULL, x, o);
-            if (lane >= o) x += y;
-        }
-        if (lane == 31) s_warp[warp] = x;
-        __syncthreads();
-        long long pre = s_carry, tot = 0;
-        for (int k = 0; k < TSCAN_NT / 32; ++k) {
-            if (k < warp) pre += s_warp[k];
-            tot += s_warp[k];
-        }
-        if (b < ntiles) tile_off[b] = pre + x - v;
-        __syncthreads();
-        if (tid == 0) s_carry += tot;
-        __syncthreads();
-    }
-    if (tid == 0) tile_off[ntiles] = s_carry;
-}
 
 constexpr int EMIT_NT = 256;
 
 __global__ void __launch_bounds__(EMIT_NT) k_tile_emit(
     const uint32_t *__restrict__ sstart, const int2 *__restrict__ tile_info,
     const uint8_t *__restrict__ tile_big, int64_t ntiles, const int2 *__restrict__ tile_cnt,
-    const long long *__restrict__ tile_off, const int4 *__restrict__ stage,
+    unsigned long long *tile_state, const int4 *__restrict__ stage,
     const int4 *__restrict__ rec, const BigCol *__restrict__ big_list,
     const uint32_t *__restrict__ bigk, int32_t N, int32_t *__restrict__ jc,
     int32_t *__restrict__ ir, double *__restrict__ pr, int64_t cap, ErrState *err) {
@@ -1151,8 +1116,14 @@ __global__ void __launch_bounds__(EMIT_NT) k_tile_emit(
     const long long b = blockIdx.x;
     const int2 ti0 = tile_info[b], ti1 = tile_info[b + 1];
     const int c_a = ti0.x, r0 = ti0.y, ncols = ti1.x - c_a;
+    __shared__ long long s_P;
     const int2 uc = tile_cnt[b];
-    const long long P = tile_off[b];
+    if (tid < 32) {  // every tile's count is already published: no waiting on slow tiles
+        const long long p = lookback_warp32(tile_state, b, (unsigned long long)uc.x);
+        if (tid == 0) s_P = p;
+    }
+    __syncthreads();
+    const long long P = s_P;
     bool over = false;
     for (int k = tid; k < uc.y; k += EMIT_NT) {
         const int4 r = stage[r0 + k];
@@ -1211,7 +1182,7 @@ cudaError_t launch_tile_fold(Launch &lc, const uint32_t *sstart, const int2 *til
                              const Segs &SG, const int4 *rec, const BigCol *big_list,
                              const uint32_t *bigk, unsigned long long *tile_state, int32_t N,
                              int32_t *jc, int32_t *ir, double *pr, int64_t cap, ErrState *err,
-                             int4 *stage, int2 *tile_cnt, long long *tile_off) {
+                             int4 *stage, int2 *tile_cnt) {
     if (ntiles <= 0) return cudaSuccess;
     static const int hash_fold = getenv("SA_HASH_FOLD") ? atoi(getenv("SA_HASH_FOLD")) : 1;
     static bool attr = false;
@@ -1235,13 +1206,9 @@ cudaError_t launch_tile_fold(Launch &lc, const uint32_t *sstart, const int2 *til
                                        ir, pr, cap, err, hash_fold, stage, tile_cnt);
     lc.launches++;
     if (e != cudaSuccess || !stage) return e;
-    e = launch_pdl(k_tile_scan, dim3(1), dim3(TSCAN_NT), 0, lc.stream, (const int2 *)tile_cnt, ntiles,
-                   tile_off);
-    lc.launches++;
-    if (e != cudaSuccess) return e;
     e = launch_pdl(k_tile_emit, dim3((unsigned)ntiles), dim3(EMIT_NT), 0, lc.stream, sstart, tile_info,
-                   tile_big, ntiles, (const int2 *)tile_cnt, (const long long *)tile_off,
-                   (const int4 *)stage, rec, big_list, bigk, N, jc, ir, pr, cap, err);
+                   tile_big, ntiles, (const int2 *)tile_cnt, tile_state, (const int4 *)stage, rec,
+                   big_list, bigk, N, jc, ir, pr, cap, err);
     lc.launches++;
     return e;
 }
