@@ -505,8 +505,7 @@ constexpr int WB = 8192;
 
 struct WinSmem {
     uint32_t bin[WB];      // per window column: triplets of the chunk
-    int used[CHUNK];       // listed bins
-    int nused;
+    int lo[2], hi[2];      // touched bin range of the chunk (by chunk parity)
 };
 
 __global__ void __launch_bounds__(AGG_NT) k_colcount_win(Segs S, int32_t N,
@@ -515,7 +514,10 @@ __global__ void __launch_bounds__(AGG_NT) k_colcount_win(Segs S, int32_t N,
     __shared__ WinSmem W;
     const int tid = threadIdx.x;
     for (int k = tid; k < WB; k += AGG_NT) W.bin[k] = 0;
-    if (tid == 0) W.nused = 0;
+    if (tid < 2) {
+        W.lo[tid] = WB;
+        W.hi[tid] = -1;
+    }
     __syncthreads();
     pdl_wait();
     pdl_trigger();
@@ -523,6 +525,7 @@ __global__ void __launch_bounds__(AGG_NT) k_colcount_win(Segs S, int32_t N,
     unsigned over = 0;
     const int64_t nchunk = S.ch0[S.nseg];
     const bool skip = S.skip_foreign != 0;
+    int par = 0;
     int jn[CPT];
     if ((int64_t)blockIdx.x < nchunk) {
         const SegChunk c = seg_chunk(S, blockIdx.x);
@@ -541,27 +544,46 @@ __global__ void __launch_bounds__(AGG_NT) k_colcount_win(Segs S, int32_t N,
         }
         const unsigned vmask = column_mask(j, t0, c.len, c.pos0, N, skip, bad, over);
         const Runs R = run_masks(j, vmask);
+        // non-returning shared adds; the chunk's touched bin range is scanned
+        // at flush time instead of listing first touches (a returning atomic)
+        int blo = WB, bhi = -1;
 #pragma unroll
         for (int k = 0; k < CPT; ++k) {
             if (R.heads & (1u << k)) {
                 const int len = run_len(R, k);
                 const unsigned b = (unsigned)(j[k] - 1 - cb);
                 if (b < (unsigned)WB) {
-                    if (atomicAdd(&W.bin[b], (uint32_t)len) == 0u) W.used[atomicAdd(&W.nused, 1)] = (int)b;
+                    atomicAdd(&W.bin[b], (uint32_t)len);
+                    blo = min(blo, (int)b);
+                    bhi = max(bhi, (int)b);
                 } else {
                     atomicAdd(&cnt[j[k] - 1], (uint32_t)len);
                 }
             }
         }
-        __syncthreads();
-        const int nu = W.nused;
-        for (int e = tid; e < nu; e += AGG_NT) {
-            const int b = W.used[e];
-            atomicAdd(&cnt[cb + b], W.bin[b]);
-            W.bin[b] = 0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            blo = min(blo, __shfl_xor_sync(FULL, blo, o));
+            bhi = max(bhi, __shfl_xor_sync(FULL, bhi, o));
+        }
+        if ((tid & 31) == 0 && bhi >= 0) {
+            atomicMin(&W.lo[par], blo);
+            atomicMax(&W.hi[par], bhi);
         }
         __syncthreads();
-        if (tid == 0) W.nused = 0;
+        const int lo = W.lo[par], hi = W.hi[par];
+        for (int b = lo + tid; b <= hi; b += AGG_NT) {
+            const uint32_t v = W.bin[b];
+            if (v) {
+                atomicAdd(&cnt[cb + b], v);
+                W.bin[b] = 0;
+            }
+        }
+        if (tid == 0) {  // the next chunk's range (its adds start after the barrier)
+            W.lo[par ^ 1] = WB;
+            W.hi[par ^ 1] = -1;
+        }
+        par ^= 1;
         __syncthreads();
     }
 #pragma unroll
