@@ -606,10 +606,19 @@ bool pdl_enabled() {
     return m == 1;
 }
 
+static int colcount_ctas() {  // resident CTAs per SM (SA_COLCOUNT_CTAS for A/B)
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("SA_COLCOUNT_CTAS");
+        v = e ? std::max(1, atoi(e)) : 5;
+    }
+    return v;
+}
+
 cudaError_t launch_colcount(Launch &lc, const Segs &S, int32_t N, uint32_t *cnt, ErrState *err) {
     const int64_t nchunk = S.ch0[S.nseg];
     if (nchunk <= 0) return cudaSuccess;
-    const int grid = (int)std::min<int64_t>(nchunk, (int64_t)lc.num_sms * 4);
+    const int grid = (int)std::min<int64_t>(nchunk, (int64_t)lc.num_sms * colcount_ctas());
     cudaError_t e = launch_pdl(k_colcount_win, dim3(grid), dim3(AGG_NT), 0, lc.stream, S, N, cnt, err);
     lc.launches++;
     return e;
