@@ -44,6 +44,10 @@ __device__ unsigned long long g_ftrace[1 << 15][8];
 #define FTRACE(b, k)
 #endif
 
+#ifndef SA_FOLD_MINB
+#define SA_FOLD_MINB 5  // resident CTAs per SM the fold is compiled for (96 registers)
+#endif
+
 namespace {
 
 constexpr int NT = TILE_THREADS;
@@ -725,7 +729,7 @@ __device__ long long lookback_warp32(unsigned long long *st, long long b, unsign
 }  // namespace
 
 template <bool STAGED>
-__global__ void __launch_bounds__(NT, 5) k_tile_fold(const uint32_t *__restrict__ sstart,
+__global__ void __launch_bounds__(NT, SA_FOLD_MINB) k_tile_fold(const uint32_t *__restrict__ sstart,
                                                      const int2 *__restrict__ tile_info,
                                                      const uint8_t *__restrict__ tile_big,
                                                      int64_t ntiles,
