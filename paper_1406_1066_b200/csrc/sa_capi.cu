@@ -42,7 +42,6 @@ struct sa_ctx {
     int32_t *pt_cnt = nullptr;            size_t ptc_cap = 0;    // partition: tile x rank counts
     int64_t *pt_off = nullptr;            size_t pto_cap = 0;    // partition: tile x rank offsets
     int64_t *pt_counts = nullptr;         // partition: per-rank counts and bases (16)
-    unsigned char *pt_chk = nullptr;      size_t ptk_cap = 0;    // partition: per-tile index checks
     ErrState *err = nullptr;              // device
     ErrState *err_host = nullptr;         // pinned mirror
 
@@ -303,7 +302,6 @@ void sa_destroy(sa_ctx *ctx) {
     cudaFree(ctx->pt_cnt);
     cudaFree(ctx->pt_off);
     cudaFree(ctx->pt_counts);
-    cudaFree(ctx->pt_chk);
     cudaFree(ctx->pr_nnz);
     cudaFree(ctx->h_ii);
     cudaFree(ctx->h_jj);
@@ -621,22 +619,19 @@ int sa_partition(sa_ctx *ctx, const int32_t *d_ii, const int32_t *d_jj, const do
     const size_t nt = (size_t)std::max<int64_t>(partition_tiles(L), 1) * (size_t)world;
     SA_CUDA(ctx, ensure(ctx->pt_cnt, ctx->ptc_cap, nt));
     SA_CUDA(ctx, ensure(ctx->pt_off, ctx->pto_cap, nt));
-    SA_CUDA(ctx, ensure(ctx->pt_chk, ctx->ptk_cap, std::max<size_t>(partition_check_bytes(L), 16)));
     if (!ctx->pt_counts) SA_CUDA(ctx, cudaMalloc(reinterpret_cast<void **>(&ctx->pt_counts), 16 * sizeof(int64_t)));
     int rc = launch_init(ctx, lc, 0, 0, 0);  // error state
     if (rc) return rc;
-    SA_CUDA(ctx, launch_partition(lc, d_ii, d_jj, d_s, s_stride, L, world, self, h_bounds, ctx->pt_cnt,
-                                  ctx->pt_off, ctx->pt_counts, d_ii_out, d_jj_out, d_s_out, ctx->pt_chk,
-                                  ctx->err));
+    SA_CUDA(ctx, launch_partition(lc, d_ii, d_jj, d_s, s_stride, L, world, self, h_bounds, M,
+                                  ctx->pt_cnt, ctx->pt_off, ctx->pt_counts, d_ii_out, d_jj_out,
+                                  d_s_out, ctx->err));
     int64_t h[16];
     SA_CUDA(ctx, cudaMemcpyAsync(h, ctx->pt_counts, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
     SA_CUDA(ctx, cudaMemcpyAsync(ctx->err_host, ctx->err, sizeof(ErrState), cudaMemcpyDeviceToHost, ctx->stream));
     SA_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     for (int r = 0; r < world; ++r) h_counts[r] = h[r];
     ctx->launches = lc.launches;
-    ErrState e = *ctx->err_host;
-    if (e.bad_i == ~0ull && e.bad_j == ~0ull && ((int64_t)e.max_i > M || (int64_t)e.max_j > N))
-        e.over_m = 1;  // a valid index beyond the global dimensions
+    ErrState e = *ctx->err_host;  // over_m / over_n: an index beyond the global dimensions
     e.nnz = 0;
     return decode(ctx, e, nullptr, bad_pos, bad_which);
 }

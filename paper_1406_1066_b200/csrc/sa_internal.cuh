@@ -352,10 +352,8 @@ cudaError_t launch_prune(Launch &lc, const int32_t *jc, const int32_t *ir, const
 int64_t prune_tiles(int64_t nnz);
 cudaError_t launch_partition(Launch &lc, const int32_t *ii, const int32_t *jj, const double *s,
                              int64_t s_stride, int64_t L, int world, int self, const int32_t *bounds,
-                             int32_t *tile_cnt, int64_t *tile_off, int64_t *counts,
-                             int32_t *out_i, int32_t *out_j, double *out_s, void *checks,
-                             ErrState *err);
+                             int32_t M, int32_t *tile_cnt, int64_t *tile_off, int64_t *counts,
+                             int32_t *out_i, int32_t *out_j, double *out_s, ErrState *err);
 int64_t partition_tiles(int64_t L);
-size_t partition_check_bytes(int64_t L);
 
 }  // namespace sa

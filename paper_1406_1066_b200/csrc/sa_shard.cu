@@ -12,13 +12,16 @@
 // bit-identical to one GPU.  The chunk's indices are validated on the way
 // (first bad row / column position, maxima).
 //
-// Three launches (a single pass over the triplets each):
-//   k_part_count    per tile (2048 triplets) and destination: counts
-//   k_part_scan     one CTA: exclusive scan over tiles per destination
-//   k_part_scatter  per tile: block scan of packed per-thread counts (4 x
-//                   16-bit fields per 64-bit word), entries written
+// Three launches (values are read only for the triplets that leave):
+//   k_part_count    per tile (2048 triplets, 8 consecutive per thread) and
+//                   destination: counts; column checks
+//   k_part_scan     one CTA per destination: exclusive scan over tiles
+//   k_part_scatter  per tile: lane / warp prefixes of packed per-thread
+//                   counts (16-bit fields), leaving triplets written; row
+//                   checks; tiles whose triplets all stay exit early
 // Invalid columns (outside [1, bounds[world]]) go to no destination; the
-// validation reports them (bad_j, or max_j above the global N).
+// checks report them (first bad position, or an index beyond the global
+// dimensions).
 
 #include "sa_internal.cuh"
 
@@ -28,7 +31,7 @@ namespace {
 
 constexpr int PT_NT = 256;
 constexpr int PT_NW = PT_NT / 32;
-constexpr int PT_IPT = 8;                 // rows of a tile: element (k, tid) = tile + k*PT_NT + tid
+constexpr int PT_IPT = 8;                 // triplets per thread: element k of thread tid = tile + tid*PT_IPT + k
 constexpr int PT_TILE = PT_NT * PT_IPT;   // 2048 triplets
 constexpr int PT_MAXW = 8;
 
@@ -42,265 +45,283 @@ __device__ __forceinline__ int dest_of(const Bounds &B, int j) {
     const int c = j - 1;
     if (c < 0 || c >= B.n) return -1;
     int d = 0;
-    for (int r = 1; r < B.world; ++r)  // warp-uniform trip count
-        if (c >= B.b[r]) d = r;
+#pragma unroll
+    for (int r = 1; r < PT_MAXW; ++r)  // static indices: the bounds stay in the parameter bank
+        if (r < B.world && c >= B.b[r]) d = r;
     return d;
 }
 
-// first column of destination d (no dynamic indexing into the parameter)
-__device__ __forceinline__ int block_lo(const Bounds &B, int d) {
+
+// Element k of thread tid of a tile is the tile's (tid * PT_IPT + k)-th
+// triplet (thread-contiguous: two 16-byte loads per index array); the stable
+// order inside a tile is (thread, k).  Index checks go straight to the error
+// state with rare atomics: a warp reports only when it saw a bad index (first
+// position, atomicMin) or one beyond the global dimensions (a flag).
+
+__device__ __forceinline__ void load8(const int32_t *__restrict__ p, int64_t e0, int64_t L, bool vec,
+                                      int (&v)[PT_IPT], int fill) {
+    if (vec && e0 + PT_IPT <= L) {
+        const int4 a = __ldg(reinterpret_cast<const int4 *>(p + e0));
+        const int4 b = __ldg(reinterpret_cast<const int4 *>(p + e0) + 1);
+        v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+        v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+    } else {
+#pragma unroll
+        for (int k = 0; k < PT_IPT; ++k) v[k] = (e0 + k < L) ? __ldg(p + e0 + k) : fill;
+    }
+}
+
+__device__ __forceinline__ void report(unsigned long long bad, bool over,
+                                       unsigned long long *err_bad, unsigned *err_over) {
+    if (!__any_sync(FULL, bad != ~0ull || over)) return;  // the common case
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) bad = min(bad, __shfl_xor_sync(FULL, bad, o));
+    const bool ov = __any_sync(FULL, over);
+    if ((threadIdx.x & 31) == 0) {
+        if (bad != ~0ull) atomicMin(err_bad, bad);
+        if (ov) atomicExch(err_over, 1u);
+    }
+}
+
+// A thread's destination counts (<= PT_IPT = 8 each) as 4-bit fields of one
+// word, widened to 16-bit fields, two destinations per word (sums over a
+// whole tile fit).
+__device__ __forceinline__ void widen(unsigned c4, unsigned (&w)[PT_MAXW / 2]) {
+#pragma unroll
+    for (int q = 0; q < PT_MAXW / 2; ++q)
+        w[q] = ((c4 >> (8 * q)) & 15u) | (((c4 >> (8 * q + 4)) & 15u) << 16);
+}
+__device__ __forceinline__ int field(const unsigned (&w)[PT_MAXW / 2], int d) {
     int v = 0;
 #pragma unroll
-    for (int r = 1; r < PT_MAXW; ++r)
-        if (r == d) v = B.b[r];
+    for (int q = 0; q < PT_MAXW / 2; ++q)
+        if (q == (d >> 1)) v = (int)((w[q] >> (16 * (d & 1))) & 0xffffu);
     return v;
 }
 
-// first bad position (< 1) and maximum of the CTA's indices -> one slot per
-// tile (no same-address atomics across the grid; k_part_reduce folds them)
-struct TileCheck {
-    unsigned long long bad;
-    unsigned mx;
-    unsigned pad;
-};
-
-__device__ __forceinline__ void check_finish(unsigned long long b, unsigned m, TileCheck *out,
-                                             TileCheck *s_chk) {
+// Destinations of a thread's PT_IPT consecutive triplets.  The destination
+// is monotone in the column, so when the smallest and largest column of the
+// run go to the same rank (FEM element order: nearly always) the per-triplet
+// search is skipped.  Returns the 4-bit per-destination counts.
+__device__ __forceinline__ unsigned run_dests(const Bounds &B, const int (&j)[PT_IPT], int64_t e0,
+                                              int64_t L, int (&d)[PT_IPT]) {
+    int lo = j[0], hi = j[0];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        b = min(b, __shfl_xor_sync(FULL, b, o));
-        m = max(m, __shfl_xor_sync(FULL, m, o));
+    for (int k = 1; k < PT_IPT; ++k) {
+        lo = min(lo, j[k]);
+        hi = max(hi, j[k]);
     }
-    const int w = threadIdx.x >> 5;
-    if ((threadIdx.x & 31) == 0) s_chk[w] = TileCheck{b, m, 0u};
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        TileCheck c = s_chk[0];
-        for (int k = 1; k < PT_NW; ++k) {
-            c.bad = min(c.bad, s_chk[k].bad);
-            c.mx = max(c.mx, s_chk[k].mx);
+    if (e0 + PT_IPT <= L && lo >= 1 && hi <= B.n) {
+        const int dl = dest_of(B, lo);
+        if (dl == dest_of(B, hi)) {
+#pragma unroll
+            for (int k = 0; k < PT_IPT; ++k) d[k] = dl;
+            return (unsigned)PT_IPT << (4 * dl);
         }
-        *out = c;
     }
-}
-
-// Per (row k, warp w) and destination d: triplets of the warp's 32 consecutive
-// elements that go to d; lane d of the warp writes cnt[k][w][d].
-__device__ __forceinline__ void warp_dest_counts(int dk, int world, int *cnt_kw) {
-    const int lane = threadIdx.x & 31;
+    unsigned c4 = 0;
 #pragma unroll
-    for (int r = 0; r < PT_MAXW; ++r) {
-        const unsigned m = __ballot_sync(FULL, dk == r);
-        if (lane == r && r < world) cnt_kw[r] = __popc(m);
+    for (int k = 0; k < PT_IPT; ++k) {
+        d[k] = (e0 + k < L) ? dest_of(B, j[k]) : -1;
+        if (d[k] >= 0) c4 += 1u << (4 * d[k]);
     }
+    return c4;
 }
 
 __global__ void __launch_bounds__(PT_NT) k_part_count(const int32_t *__restrict__ jj, int64_t L,
-                                                      Bounds B, int32_t *__restrict__ tile_cnt,
-                                                      TileCheck *__restrict__ chk_j) {
-    __shared__ int s_cnt[PT_NW][PT_MAXW];
-    __shared__ TileCheck s_chk[PT_NW];
-    const long long t = blockIdx.x;
+                                                      Bounds B, int vec,
+                                                      int32_t *__restrict__ tile_cnt, ErrState *err) {
+    __shared__ unsigned s_w[PT_NW][PT_MAXW / 2];
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int64_t ntiles = (L + PT_TILE - 1) / PT_TILE;
     unsigned long long bad = ~0ull;
-    unsigned mx = 0;
-    // per-thread counts in 4-bit fields (<= PT_IPT = 8 per destination)
-    unsigned long long acc = 0;
-    int jv[PT_IPT];
+    bool over = false;
+    int jn[PT_IPT];  // the next tile's columns, in flight while this one is counted
+    if ((int64_t)blockIdx.x < ntiles) load8(jj, (int64_t)blockIdx.x * PT_TILE + (int64_t)tid * PT_IPT, L, vec != 0, jn, 1);
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int64_t e0 = t * PT_TILE + (int64_t)tid * PT_IPT;
+        int jv[PT_IPT];
 #pragma unroll
-    for (int k = 0; k < PT_IPT; ++k) {  // all loads in flight before any use
-        const int64_t e = t * PT_TILE + (int64_t)k * PT_NT + tid;
-        jv[k] = (e < L) ? __ldg(jj + e) : 0;
-    }
+        for (int k = 0; k < PT_IPT; ++k) jv[k] = jn[k];
+        if (t + gridDim.x < ntiles) load8(jj, e0 + (int64_t)gridDim.x * PT_TILE, L, vec != 0, jn, 1);
+        int d[PT_IPT];
+        const unsigned c4 = run_dests(B, jv, e0, L, d);
 #pragma unroll
-    for (int k = 0; k < PT_IPT; ++k) {
-        const int64_t e = t * PT_TILE + (int64_t)k * PT_NT + tid;
-        const int j = jv[k];
-        const int d = (e < L) ? dest_of(B, j) : -1;
-        if (e < L) {
-            if (j < 1) bad = min(bad, (unsigned long long)e);
-            else mx = max(mx, (unsigned)j);
+        for (int k = 0; k < PT_IPT; ++k) {
+            const bool live = e0 + k < L;
+            if (live && jv[k] < 1) bad = min(bad, (unsigned long long)(e0 + k));
+            if (live && jv[k] > B.n) over = true;
         }
-        if (d >= 0) acc += 1ull << (4 * d);
-    }
-    // widen to 16-bit fields (4 destinations per word) and reduce over the warp
-    unsigned long long lo = 0, hi = 0;
+        unsigned wd[PT_MAXW / 2];
+        widen(c4, wd);
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
-        lo |= ((acc >> (4 * r)) & 15ull) << (16 * r);
-        hi |= ((acc >> (4 * (r + 4))) & 15ull) << (16 * r);
-    }
+        for (int q = 0; q < PT_MAXW / 2; ++q)
+            if (2 * q < B.world) wd[q] = __reduce_add_sync(FULL, wd[q]);
+        if (lane == 0)
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        lo += __shfl_xor_sync(FULL, lo, o);
-        hi += __shfl_xor_sync(FULL, hi, o);
+            for (int q = 0; q < PT_MAXW / 2; ++q) s_w[w][q] = wd[q];
+        __syncthreads();
+        if (tid < B.world) {
+            int tot = 0;
+            for (int q = 0; q < PT_NW; ++q) tot += (int)((s_w[q][tid >> 1] >> (16 * (tid & 1))) & 0xffffu);
+            tile_cnt[(int64_t)tid * ntiles + t] = tot;  // destination-major
+        }
+        __syncthreads();  // s_w is rewritten by the next tile
     }
-    const int acc_l = (lane < 4) ? (int)((lo >> (16 * lane)) & 0xffff)
-                                 : (int)((hi >> (16 * (lane & 3))) & 0xffff);
-    if (lane < PT_MAXW) s_cnt[w][lane] = acc_l;
-    check_finish(bad, mx, &chk_j[t], s_chk);  // ends with a barrier
-    if (tid < B.world) {
-        int tot = 0;
-        for (int q = 0; q < PT_NW; ++q) tot += s_cnt[q][tid];
-        tile_cnt[t * B.world + tid] = tot;
-    }
+    report(bad, over, &err->bad_j, &err->over_n);
 }
 
-// CTA d: tile_off[t][d] = sum over tiles < t of tile_cnt[.][d]; counts[d] =
-// records for destination d (the scatter derives the destination bases)
+// CTA d: tile_off[d][t] = sum over tiles < t of tile_cnt[d][.]
+// (destination-major rows; every thread scans a contiguous run of up to
+// SC_RUN tiles held in registers, more in a second pass); counts[d] =
+// records for destination d
+constexpr int SC_RUN = 12;
 __global__ void __launch_bounds__(1024) k_part_scan(const int32_t *__restrict__ tile_cnt,
                                                     int64_t ntiles, int world,
                                                     int64_t *__restrict__ tile_off,
                                                     int64_t *__restrict__ counts) {
     __shared__ long long s_warp[32];
-    __shared__ long long s_carry;
     const int d = blockIdx.x;
-    if (threadIdx.x == 0) s_carry = 0;
-    __syncthreads();
-    for (int64_t base = 0; base < ntiles; base += 1024) {
-        const int64_t t = base + threadIdx.x;
-        const long long v = (t < ntiles) ? tile_cnt[t * world + d] : 0;
-        long long total;
-        const long long pre = block_excl_sum<1024, long long>(v, s_warp, total);
-        if (t < ntiles) tile_off[t * world + d] = s_carry + pre;
-        __syncthreads();
-        if (threadIdx.x == 0) s_carry += total;
-        __syncthreads();
+    const int32_t *row = tile_cnt + (int64_t)d * ntiles;
+    int64_t *orow = tile_off + (int64_t)d * ntiles;
+    const int64_t per = (ntiles + 1023) / 1024;
+    const int64_t t0 = min(ntiles, (int64_t)threadIdx.x * per), t1 = min(ntiles, t0 + per);
+    int v[SC_RUN];
+    long long sum = 0;
+#pragma unroll
+    for (int k = 0; k < SC_RUN; ++k) {
+        v[k] = (t0 + k < t1) ? row[t0 + k] : 0;
+        sum += v[k];
     }
-    if (threadIdx.x == 0) counts[d] = s_carry;
+    for (int64_t t = t0 + SC_RUN; t < t1; ++t) sum += row[t];
+    long long total;
+    long long run = block_excl_sum<1024, long long>(sum, s_warp, total);
+#pragma unroll
+    for (int k = 0; k < SC_RUN; ++k)
+        if (t0 + k < t1) {
+            orow[t0 + k] = run;
+            run += v[k];
+        }
+    for (int64_t t = t0 + SC_RUN; t < t1; ++t) {
+        orow[t] = run;
+        run += row[t];
+    }
+    if (threadIdx.x == 0) counts[d] = total;
 }
 
-// Element (k, tid) of a tile is its k*PT_NT + tid-th triplet; the stable
-// order inside the tile is (k, warp, lane).  The per-(k, warp) destination
-// counts are scanned in that order (one warp per destination), and every
-// lane adds its rank among the warp's lanes with the same destination:
-// lanes writing one destination write consecutive slots.
-__global__ void __launch_bounds__(PT_NT) k_part_scatter(const int32_t *__restrict__ ii,
+// Stable scatter of the triplets bound for other ranks.  A thread's base
+// for destination d = tile offset + the counts of the warps and lanes before
+// it (16-bit fields); its own triplets to d follow in k order.  Values are
+// loaded only for triplets that leave (element-ordered FEM keeps ~99.9 %
+// of them at home).
+__global__ void __launch_bounds__(PT_NT, 3) k_part_scatter(const int32_t *__restrict__ ii,
                                                         const int32_t *__restrict__ jj,
                                                         const double *__restrict__ s,
                                                         int64_t s_stride, int64_t L, Bounds B,
+                                                        int vec, int32_t M,
                                                         const int64_t *__restrict__ tile_off,
                                                         const int64_t *__restrict__ counts,
                                                         int32_t *__restrict__ out_i,
                                                         int32_t *__restrict__ out_j,
                                                         double *__restrict__ out_s, int self,
-                                                        TileCheck *__restrict__ chk_i) {
-    __shared__ int s_cnt[PT_MAXW][PT_IPT * PT_NW];  // [dest][k*NW + w], then exclusive prefixes
-    __shared__ TileCheck s_chk[PT_NW];
-    const long long t = blockIdx.x;
+                                                        ErrState *err) {
+    __shared__ unsigned s_w[PT_NW][PT_MAXW / 2];
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-    const unsigned lt = lanemask_lt();
-    int d[PT_IPT], j[PT_IPT], iv[PT_IPT];
+    const int64_t ntiles = (L + PT_TILE - 1) / PT_TILE;
     unsigned long long bad = ~0ull;
-    unsigned mx = 0;
-    double sv[PT_IPT];
-    unsigned pm[PT_IPT];
-    for (int x = tid; x < PT_MAXW * PT_IPT * PT_NW; x += PT_NT) (&s_cnt[0][0])[x] = 0;
-#pragma unroll
-    for (int k = 0; k < PT_IPT; ++k) {  // all loads in flight before any use
-        const int64_t e = t * PT_TILE + (int64_t)k * PT_NT + tid;
-        j[k] = (e < L) ? __ldg(jj + e) : 0;
-        iv[k] = (e < L) ? __ldg(ii + e) : 1;
-        sv[k] = (e < L) ? __ldg(s + e * s_stride) : 0.0;
+    bool over = false;
+    int jn[PT_IPT], in_[PT_IPT];  // the next tile's indices, in flight
+    if ((int64_t)blockIdx.x < ntiles) {
+        const int64_t e1 = (int64_t)blockIdx.x * PT_TILE + (int64_t)tid * PT_IPT;
+        load8(jj, e1, L, vec != 0, jn, 1);
+        load8(ii, e1, L, vec != 0, in_, 1);
     }
-    __syncthreads();  // counters zeroed
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int64_t e0 = t * PT_TILE + (int64_t)tid * PT_IPT;
+        int jv[PT_IPT], iv[PT_IPT], d[PT_IPT];
 #pragma unroll
-    for (int k = 0; k < PT_IPT; ++k) {
-        const int64_t e = t * PT_TILE + (int64_t)k * PT_NT + tid;
-        d[k] = (e < L) ? dest_of(B, j[k]) : -1;
-        if (e < L) {
-            if (iv[k] < 1) bad = min(bad, (unsigned long long)e);
-            else mx = max(mx, (unsigned)iv[k]);
+        for (int k = 0; k < PT_IPT; ++k) {
+            jv[k] = jn[k];
+            iv[k] = in_[k];
         }
-        pm[k] = __match_any_sync(FULL, d[k]);  // lanes with the same destination
-        if (d[k] >= 0 && (pm[k] & lt) == 0u) {  // group leader
+        if (t + gridDim.x < ntiles) {
+            load8(jj, e0 + (int64_t)gridDim.x * PT_TILE, L, vec != 0, jn, 1);
+            load8(ii, e0 + (int64_t)gridDim.x * PT_TILE, L, vec != 0, in_, 1);
+        }
+        const unsigned c4 = run_dests(B, jv, e0, L, d);
+        unsigned leave = 0;
 #pragma unroll
-            for (int r = 0; r < PT_MAXW; ++r)
-                if (r == d[k]) s_cnt[r][k * PT_NW + w] = __popc(pm[k]);
+        for (int k = 0; k < PT_IPT; ++k) {
+            const bool live = e0 + k < L;
+            if (live && iv[k] < 1) bad = min(bad, (unsigned long long)(e0 + k));
+            if (live && iv[k] > M) over = true;
+            if (d[k] >= 0 && d[k] != self) leave |= 1u << k;
         }
-    }
-    __syncthreads();
-    // exclusive scan of s_cnt[d][0..64) in (k, w) order: warp d, 2 entries per lane
-    if (w < B.world) {
-        static_assert(PT_IPT * PT_NW == 64, "two (k, warp) entries per lane");
-        const int a0 = s_cnt[w][2 * lane], a1 = s_cnt[w][2 * lane + 1];
-        int x = a0 + a1;
+        if (!__syncthreads_or(leave != 0u)) continue;  // nothing leaves this tile
+        double sv[PT_IPT];
+#pragma unroll
+        for (int k = 0; k < PT_IPT; ++k) sv[k] = (leave >> k & 1u) ? __ldg(s + (e0 + k) * s_stride) : 0.0;
+        // exclusive prefix of the fields over the lanes, then over the warps
+        unsigned own[PT_MAXW / 2], x[PT_MAXW / 2];
+        widen(c4, own);
+#pragma unroll
+        for (int q = 0; q < PT_MAXW / 2; ++q) x[q] = own[q];
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(FULL, x, o);
-            if (lane >= o) x += y;
-        }
-        long long base = tile_off[t * B.world + w];
-        for (int r = 0; r < w; ++r)  // destinations before w (the rank's own stay in place)
-            if (r != self) base += counts[r];
-        const int ex = x - a0 - a1;
-        s_cnt[w][2 * lane] = (int)ex;
-        s_cnt[w][2 * lane + 1] = (int)(ex + a0);
-        if (lane == 0) s_chk[w].bad = (unsigned long long)base;  // stash the base
-    }
-    __syncthreads();
-    long long dbase[PT_MAXW];
 #pragma unroll
-    for (int r = 0; r < PT_MAXW; ++r) dbase[r] = (r < B.world) ? (long long)s_chk[r].bad : 0;
-#pragma unroll
-    for (int k = 0; k < PT_IPT; ++k) {
-        const int64_t e = t * PT_TILE + (int64_t)k * PT_NT + tid;
-        const unsigned peers = pm[k];
-        if (d[k] < 0 || d[k] == self) continue;
-        long long pos = 0;
-        int pre = 0;
-#pragma unroll
-        for (int r = 0; r < PT_MAXW; ++r)
-            if (r == d[k]) {
-                pos = dbase[r];
-                pre = s_cnt[r][k * PT_NW + w];
+            for (int q = 0; q < PT_MAXW / 2; ++q) {
+                const unsigned y = __shfl_up_sync(FULL, x[q], o);
+                if (lane >= o) x[q] += y;
             }
-        pos += pre + __popc(peers & lt);
-        out_i[pos] = iv[k];
-        out_j[pos] = j[k];
-        out_s[pos] = sv[k];
-    }
-    __syncthreads();  // s_chk is reused below
-    check_finish(bad, mx, &chk_i[t], s_chk);
-}
-
-// one CTA: the tiles' index checks -> the context's error state
-__global__ void __launch_bounds__(1024) k_part_reduce(const TileCheck *__restrict__ chk_i,
-                                                      const TileCheck *__restrict__ chk_j,
-                                                      int64_t ntiles, ErrState *err) {
-    unsigned long long bi = ~0ull, bj = ~0ull;
-    unsigned mi = 0, mj = 0;
-    for (int64_t t = threadIdx.x; t < ntiles; t += 1024) {
-        bi = min(bi, chk_i[t].bad);
-        bj = min(bj, chk_j[t].bad);
-        mi = max(mi, chk_i[t].mx);
-        mj = max(mj, chk_j[t].mx);
-    }
+        }
+        if (lane == 31)
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        bi = min(bi, __shfl_xor_sync(FULL, bi, o));
-        bj = min(bj, __shfl_xor_sync(FULL, bj, o));
-        mi = max(mi, __shfl_xor_sync(FULL, mi, o));
-        mj = max(mj, __shfl_xor_sync(FULL, mj, o));
+            for (int q = 0; q < PT_MAXW / 2; ++q) s_w[w][q] = x[q];
+#pragma unroll
+        for (int q = 0; q < PT_MAXW / 2; ++q) x[q] -= own[q];
+        __syncthreads();
+        for (int p = 0; p < w; ++p)
+#pragma unroll
+            for (int q = 0; q < PT_MAXW / 2; ++q) x[q] += s_w[p][q];
+        if (!leave) continue;  // (s_w is rewritten only after the next tile's barrier)
+        long long base[PT_MAXW];
+        {
+            long long acc = 0;  // destinations before r (the rank's own stay in place)
+#pragma unroll
+            for (int r = 0; r < PT_MAXW; ++r) {
+                base[r] = 0;
+                if (r < B.world) {
+                    base[r] = acc + tile_off[(int64_t)r * ntiles + t] + field(x, r);
+                    if (r != self) acc += counts[r];
+                }
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < PT_IPT; ++k) {
+            if (!(leave >> k & 1u)) continue;  // (every triplet to a destination r != self leaves)
+            long long pos = 0;
+#pragma unroll
+            for (int r = 0; r < PT_MAXW; ++r) {  // predicated: base stays in registers
+                const bool m = r == d[k];
+                pos = m ? base[r] : pos;
+                base[r] += m ? 1 : 0;
+            }
+            out_i[pos] = iv[k];
+            out_j[pos] = jv[k];
+            out_s[pos] = sv[k];
+        }
     }
-    if ((threadIdx.x & 31) == 0) {
-        if (bi != ~0ull) atomicMin(&err->bad_i, bi);
-        if (bj != ~0ull) atomicMin(&err->bad_j, bj);
-        if (mi) atomicMax(&err->max_i, mi);
-        if (mj) atomicMax(&err->max_j, mj);
-    }
+    report(bad, over, &err->bad_i, &err->over_m);
 }
 
 }  // namespace
 
 int64_t partition_tiles(int64_t L) { return (L + PT_TILE - 1) / PT_TILE; }
-size_t partition_check_bytes(int64_t L) { return 2 * (size_t)partition_tiles(L) * sizeof(TileCheck); }
 
 cudaError_t launch_partition(Launch &lc, const int32_t *ii, const int32_t *jj, const double *s,
                              int64_t s_stride, int64_t L, int world, int self, const int32_t *bounds,
-                             int32_t *tile_cnt, int64_t *tile_off, int64_t *counts,
-                             int32_t *out_i, int32_t *out_j, double *out_s, void *checks,
-                             ErrState *err) {
+                             int32_t M, int32_t *tile_cnt, int64_t *tile_off, int64_t *counts,
+                             int32_t *out_i, int32_t *out_j, double *out_s, ErrState *err) {
     if (world < 1 || world > PT_MAXW) return cudaErrorInvalidValue;
     Bounds B;
     for (int r = 0; r <= PT_MAXW; ++r) B.b[r] = (r <= world) ? bounds[r] : bounds[world];
@@ -308,14 +329,14 @@ cudaError_t launch_partition(Launch &lc, const int32_t *ii, const int32_t *jj, c
     B.n = bounds[world];
     const int64_t ntiles = partition_tiles(L);
     if (ntiles == 0) return cudaMemsetAsync(counts, 0, 2 * PT_MAXW * sizeof(int64_t), lc.stream);
-    TileCheck *chk_j = reinterpret_cast<TileCheck *>(checks), *chk_i = chk_j + ntiles;
-    k_part_count<<<(unsigned)ntiles, PT_NT, 0, lc.stream>>>(jj, L, B, tile_cnt, chk_j);
+    const int vec = ((reinterpret_cast<uintptr_t>(ii) | reinterpret_cast<uintptr_t>(jj)) & 15) == 0;
+    const unsigned grid = (unsigned)std::min<int64_t>(ntiles, (int64_t)lc.num_sms * 8);
+    k_part_count<<<grid, PT_NT, 0, lc.stream>>>(jj, L, B, vec, tile_cnt, err);
     k_part_scan<<<world, 1024, 0, lc.stream>>>(tile_cnt, ntiles, world, tile_off, counts);
-    k_part_scatter<<<(unsigned)ntiles, PT_NT, 0, lc.stream>>>(ii, jj, s, s_stride, L, B, tile_off,
-                                                              counts, out_i, out_j, out_s, self,
-                                                              chk_i);
-    k_part_reduce<<<1, 1024, 0, lc.stream>>>(chk_i, chk_j, ntiles, err);
-    lc.launches += 4;
+    k_part_scatter<<<grid, PT_NT, 0, lc.stream>>>(ii, jj, s, s_stride, L, B, vec, M,
+                                                              tile_off, counts, out_i, out_j, out_s,
+                                                              self, err);
+    lc.launches += 3;
     return cudaGetLastError();
 }
 
