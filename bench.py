@@ -185,6 +185,8 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sharded", action="store_true",
+                    help="use the multi-GPU (sharded, NCCL) step even with one rank (under torchrun)")
     args = ap.parse_args()
     world, rank, local = _dist()
     if args.warmup < 3:
@@ -231,7 +233,9 @@ def main():
     import paper_1406_1066_b200 as sa
     from paper_1406_1066_b200 import _capi
 
-    if world > 1:
+    shard = world > 1 or args.sharded
+
+    if shard:
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -249,17 +253,20 @@ def main():
     asm._bind_stream()
     stream = torch.cuda.current_stream(dev)
 
-    if world > 1:
+    if shard:
         # column-block sharding: histogram + all_reduce, stable partition,
         # NCCL all_to_all of the triplets, local CUDA assembly, nnz all_gather
         from paper_1406_1066_b200.distributed import assemble_sharded, gpu_local_assembler
 
-        local = gpu_local_assembler(local)
+        local_asm = gpu_local_assembler(local)
         shard_info = {}
 
         def step():
-            res = assemble_sharded(w.ii, w.jj, w.s, M, N, local)
+            res = assemble_sharded(w.ii, w.jj, w.s, M, N, local_asm)
             shard_info["nnz"] = res.nnz_total
+            shard_info["nnz_local"] = int(res.ir.numel())
+            shard_info["n_local"] = res.col_hi - res.col_lo
+            shard_info["launches"] = res.launches
             shard_info["sent_remote"] = res.sent_remote
             shard_info["recv"] = res.recv_triplets
     else:
@@ -273,9 +280,9 @@ def main():
     step()
     import ctypes
 
-    if world > 1:
+    if shard:
         nnz = shard_info["nnz"]
-        launches_per_step = lib.sa_last_launch_count(ctx)
+        launches_per_step = shard_info["launches"]  # partition + local assembly
     else:
         nnz_c = ctypes.c_int64(0)
         rc = lib.sa_finish(ctx, ctypes.byref(nnz_c), None, None)
@@ -287,7 +294,7 @@ def main():
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    if world > 1:
+    if shard:
         dist.barrier()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
@@ -298,7 +305,7 @@ def main():
         ev1.record(stream)
         torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1) / args.steps
-    if world > 1:
+    if shard:
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
@@ -319,19 +326,25 @@ def main():
     lib.sa_enable_timing(ctx, 0)
     kern_ms = {k: sum(v) / len(v) for k, v in kt.items()}
     dom = max(kern_ms, key=kern_ms.get)
-    # algorithmic bytes per launch of each kernel ("kernels")
+    # algorithmic bytes per launch of each kernel ("kernels"); at
+    # N > 1 the rank's own assembly: its chunk, its column block, its nnz
+    # (received triplets are few for the element-ordered meshes)
+    nl = shard_info["nnz_local"] if shard else nnz
+    Nl = shard_info["n_local"] if shard else N
     alg = {
-        "k_init": 4 * (N + 1),
+        "k_init": 4 * (Nl + 1),
         "k_colcount": 4 * L,
-        "k_col_scan": 8 * N,
+        "k_col_scan": 8 * Nl,
         "k_scatter": 16 * L,
         "k_bigcol": 0,
-        "k_tile_fold": 16 * L + 8 * N + 12 * nnz + 4 * (N + 1),
+        "k_tile_fold": 16 * L + 8 * Nl + 12 * nl + 4 * (Nl + 1),
     }
     peak_gbs, peak_kind = _peaks()
     dom_gbs = alg.get(dom, 0) / (kern_ms[dom] * 1e-3) / 1e9
-    compulsory = 16 * L + 12 * nnz + 4 * (N + 1)
-    path_gbs = compulsory / (ms * 1e-3) / 1e9
+    # whole job: every rank's triplets read, the global CSC written, over
+    # world x the per-GPU peak
+    compulsory = 16 * L * world + 12 * nnz + 4 * (N + 1)
+    path_gbs = compulsory / (ms * 1e-3) / 1e9 / world
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "dram_traffic.json")
     if os.path.exists(tpath):
@@ -351,16 +364,30 @@ def main():
     hs.copy_(w.s)
     hin, hjn, hsn = hi.numpy(), hj.numpy(), hs.numpy()
     d2h = 4 * (N + 1) + 12 * nnz
-    if world > 1:
+    if shard:
         # host chunk -> device, sharded assembly, the rank's column block -> host
+        pinned = {}
+
+        def to_pinned(name, x):  # page-locked result buffers, reused across calls
+            buf = pinned.get(name)
+            if buf is None or buf.numel() < x.numel():
+                buf = pinned[name] = torch.empty(int(x.numel() * 1.25) + 16, dtype=x.dtype,
+                                                 pin_memory=True)
+            out_ = buf[: x.numel()]
+            out_.copy_(x, non_blocking=True)
+            return out_
+
         def e2e_call():
             di = hi.to(dev, non_blocking=True)
             dj = hj.to(dev, non_blocking=True)
             ds = hs.to(dev, non_blocking=True)
-            res = assemble_sharded(di, dj, ds, M, N, local)
-            return res.jc.cpu(), res.ir.cpu(), res.pr.cpu()
+            res = assemble_sharded(di, dj, ds, M, N, local_asm)
+            outs = (to_pinned("jc", res.jc), to_pinned("ir", res.ir), to_pinned("pr", res.pr))
+            torch.cuda.current_stream(dev).synchronize()
+            return outs
 
-        jc_h, ir_h, pr_h = e2e_call()
+        for _ in range(2):  # warm-up (allocator, page-locked buffers)
+            jc_h, ir_h, pr_h = e2e_call()
         d2h = 8 * len(jc_h) + 12 * len(ir_h)
         out = None
     else:
@@ -372,22 +399,22 @@ def main():
     e2e_t = []
     for _ in range(max(1, args.e2e_steps)):
         torch.cuda.synchronize()
-        if world > 1:
+        if shard:
             dist.barrier()
         t0 = time.perf_counter()
         r = e2e_call()
         e2e_t.append(time.perf_counter() - t0)
-        if world == 1:
+        if not shard:
             out = r
     e2e_s = sum(e2e_t) / len(e2e_t)
-    if world > 1:
+    if shard:
         t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
 
     cpu = None
     parity = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and not shard and not args.no_cpu_baseline:
         info, ref = cpu_reference_run(hin, hjn, hsn, M, N)
         parity = bool(out.same_as(ref))
         cpu = {"value": L / info["mean_s"], "unit": UNIT, "cores": info["cores"], "kind": info["kind"],
@@ -395,7 +422,7 @@ def main():
                          f"mean {info['mean_s'] * 1e3:.1f} ms"}
 
     if rank != 0:
-        if world > 1:
+        if shard:
             dist.destroy_process_group()
         return
     value = L * world / (ms * 1e-3)
@@ -405,7 +432,7 @@ def main():
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": w.name, "L": L, "m": M, "n": N, "nnz": nnz,
                    "l2": "inputs (16 B x L) and workspace exceed the 126 MB L2; no explicit flush",
-                   "parallelism": f"dp{world}" if world > 1 else "single"},
+                   "parallelism": f"dp{world}" if shard else "single"},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": dom_gbs, "peak": peak_gbs,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": dom_gbs / peak_gbs,
                      "traffic": traffic, "alg_bytes_per_launch": alg.get(dom),
@@ -421,13 +448,13 @@ def main():
         "cpu_baseline": cpu,
         "parity_vs_cpu_reference": parity,
     }
-    if world > 1:
+    if shard:
         line["exchange"] = {"sent_remote_triplets_rank0": shard_info.get("sent_remote"),
                             "received_triplets_rank0": shard_info.get("recv"),
                             "collectives": "all_reduce(block histogram), all_to_all(triplets), "
                                            "all_gather(nnz) over NCCL"}
     print(json.dumps(line), flush=True)
-    if world > 1:
+    if shard:
         dist.destroy_process_group()
 
 

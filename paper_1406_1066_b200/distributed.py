@@ -49,6 +49,7 @@ class ShardResult:
     n: int
     recv_triplets: int      # triplets assembled here after the exchange
     sent_remote: int        # triplets this rank sent to other ranks
+    launches: int = 0       # CUDA kernels this rank launched (partition + assembly)
 
 
 def block_boundaries(block_hist: torch.Tensor, world: int, nblocks: int, n: int):
@@ -175,7 +176,8 @@ def assemble_sharded(ii: torch.Tensor, jj: torch.Tensor, s: torch.Tensor, m: int
         else:
             jc, ir, pr = local_assemble(ii, jj, s, m, n)
         k = int(jc[-1]) if len(jc) else 0
-        return ShardResult(0, n, jc.to(torch.int64), ir, pr, 0, k, m, n, int(ii.shape[0]), 0)
+        nl = asm.lib.sa_last_launch_count(asm.ctx) if cuda else 0
+        return ShardResult(0, n, jc.to(torch.int64), ir, pr, 0, k, m, n, int(ii.shape[0]), 0, nl)
     nblocks = max(1, min(nblocks, n))
     bsize = (n + nblocks - 1) // nblocks
     # the boundaries only balance the ranks' work: a strided sample of the
@@ -185,8 +187,10 @@ def assemble_sharded(ii: torch.Tensor, jj: torch.Tensor, s: torch.Tensor, m: int
     hist = torch.bincount(blk, minlength=nblocks).to(torch.int64) * step
     dist.all_reduce(hist, group=group)
     bounds = block_boundaries(hist, world, nblocks, n)
+    launches = 0
     if cuda:
         parts, counts = _partition_cuda(asm, ii, jj, s, m, n, bounds, world, rank)
+        launches += asm.lib.sa_last_launch_count(asm.ctx)
     else:
         parts, counts = partition_torch(ii, jj, s, bounds, world, rank)
     sc = [0 if r == rank else c for r, c in enumerate(counts)]  # the own triplets stay here
@@ -210,6 +214,7 @@ def assemble_sharded(ii: torch.Tensor, jj: torch.Tensor, s: torch.Tensor, m: int
     if cuda:
         segs = [x for x in (lower, (ii, jj, s), higher) if x[0].shape[0] > 0] or [(ii, jj, s)]
         out = _assemble_segments_cuda(asm, segs, col_lo, m, n_local)
+        launches += asm.lib.sa_last_launch_count(asm.ctx)
         jc, ir, pr = out.jc, out.ir, out.pr
     else:
         mine = (jj.to(torch.int64) > col_lo) & (jj.to(torch.int64) <= col_hi)
@@ -226,7 +231,7 @@ def assemble_sharded(ii: torch.Tensor, jj: torch.Tensor, s: torch.Tensor, m: int
     off = sum(nn[:rank])
     jc_global = jc.to(torch.int64) + off
     return ShardResult(col_lo, col_hi, jc_global, ir, pr, off, sum(nn), m, n,
-                       int(r_ii.shape[0]) + counts[rank], sent_remote)
+                       int(r_ii.shape[0]) + counts[rank], sent_remote, launches)
 
 
 def gpu_local_assembler(device: int = 0):
