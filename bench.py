@@ -238,7 +238,19 @@ def main():
     if shard:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # stdout carries only the JSON line: the communicator is created (and
+        # NCCL prints its version banner, NCCL_DEBUG=VERSION in this image)
+        # with fd 1 pointing at stderr
+        sys.stdout.flush()
+        saved = os.dup(1)
+        os.dup2(2, 1)
+        try:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            dist.barrier()
+        finally:
+            sys.stdout.flush()
+            os.dup2(saved, 1)
+            os.close(saved)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     w = build_workload(args.config, dev, rank, world)
@@ -260,9 +272,10 @@ def main():
 
         local_asm = gpu_local_assembler(local)
         shard_info = {}
+        shard_out = {}  # result buffers reused across steps (as the single-GPU step's jc / ir / pr)
 
         def step():
-            res = assemble_sharded(w.ii, w.jj, w.s, M, N, local_asm)
+            res = assemble_sharded(w.ii, w.jj, w.s, M, N, local_asm, out=shard_out)
             shard_info["nnz"] = res.nnz_total
             shard_info["nnz_local"] = int(res.ir.numel())
             shard_info["n_local"] = res.col_hi - res.col_lo
@@ -381,7 +394,7 @@ def main():
             di = hi.to(dev, non_blocking=True)
             dj = hj.to(dev, non_blocking=True)
             ds = hs.to(dev, non_blocking=True)
-            res = assemble_sharded(di, dj, ds, M, N, local_asm)
+            res = assemble_sharded(di, dj, ds, M, N, local_asm, out=shard_out)
             outs = (to_pinned("jc", res.jc), to_pinned("ir", res.ir), to_pinned("pr", res.pr))
             torch.cuda.current_stream(dev).synchronize()
             return outs

@@ -19,6 +19,8 @@
  *                                     _kernels.validate_chunk     _kernels.pyx:92-110
  *   sa_infer_dims                  <- AssemblyRequest.effective_dims (inferred) types.py:102-118
  *   sa_prune_zeros                 <- types.prune_explicit_zeros types.py:204-213
+ *   sa_block_histogram             <- (new: the sampled column-block histogram that sets
+ *                                     the multi-GPU rank boundaries)
  *   sa_partition                   <- (new: multi-GPU column-block sharding, SURVEY 8(e);
  *                                     the reference's threaded driver partitions by
  *                                     element range, parallel.py:28-35, 267-358)
@@ -175,6 +177,15 @@ void sa_host_buffer_release(void *ptr);
 int sa_prune_zeros(sa_ctx *ctx, const int32_t *d_jc, const int32_t *d_ir, const double *d_pr,
                    int32_t N, int64_t nnz, int32_t *d_jc_out, int32_t *d_ir_out,
                    double *d_pr_out, int64_t *nnz_out);
+
+/*
+ * Sampled column-block histogram (multi-GPU rank boundaries): d_hist[b]
+ * (nblocks <= 8192 entries, zeroed here) += step for every step-th triplet
+ * whose column j falls in block b = (j-1) / bsize (clamped to [0, nblocks)).
+ * Asynchronous on the context's stream.
+ */
+int sa_block_histogram(sa_ctx *ctx, const int32_t *d_jj, int64_t L, int64_t step, int32_t nblocks,
+                       int64_t bsize, uint64_t *d_hist);
 
 /*
  * Multi-GPU column-block sharding (one process per GPU).  sa_partition

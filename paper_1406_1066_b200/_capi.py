@@ -53,6 +53,7 @@ SIGNATURES = {
     "sa_host_assemble": (_int, [_vp, _i32, _i32, _pi64, _pi64, _pint]),
     "sa_host_fetch": (_int, [_vp, _vp, _vp, _vp]),
     "sa_prune_zeros": (_int, [_vp, _vp, _vp, _vp, _i32, _i64, _vp, _vp, _vp, _pi64]),
+    "sa_block_histogram": (_int, [_vp, _vp, _i64, _i64, _i32, _i64, _vp]),
     "sa_partition": (_int, [_vp, _vp, _vp, _vp, _i64, _i64, _i32, _i32, _i32, _i32, ctypes.POINTER(_i32),
                             _vp, _vp, _vp, _pi64, _pi64, _pint]),
     "sa_assemble_segments_async": (_int, [_vp, _int, ctypes.POINTER(_vp), ctypes.POINTER(_vp),

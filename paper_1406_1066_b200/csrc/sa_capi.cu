@@ -604,6 +604,19 @@ int sa_prune_zeros(sa_ctx *ctx, const int32_t *d_jc, const int32_t *d_ir, const 
     return SA_OK;
 }
 
+int sa_block_histogram(sa_ctx *ctx, const int32_t *d_jj, int64_t L, int64_t step, int32_t nblocks,
+                       int64_t bsize, uint64_t *d_hist) {
+    if (!ctx) return SA_ERR_INVALID_ARG;
+    if (L < 0 || step < 1 || nblocks < 1 || nblocks > 8192 || bsize < 1 || !d_hist || (L > 0 && !d_jj))
+        return fail(ctx, SA_ERR_INVALID_ARG, "sa_block_histogram: bad arguments");
+    SA_CUDA(ctx, cudaSetDevice(ctx->device));
+    Launch lc{ctx->stream, ctx->num_sms, 0};
+    SA_CUDA(ctx, launch_block_hist(lc, d_jj, L, step, nblocks, bsize,
+                                   reinterpret_cast<unsigned long long *>(d_hist)));
+    ctx->launches = lc.launches;
+    return SA_OK;
+}
+
 int sa_partition(sa_ctx *ctx, const int32_t *d_ii, const int32_t *d_jj, const double *d_s,
                  int64_t s_stride, int64_t L, int32_t M, int32_t N, int32_t world, int32_t self,
                  const int32_t *h_bounds, int32_t *d_ii_out, int32_t *d_jj_out, double *d_s_out,

@@ -355,5 +355,7 @@ cudaError_t launch_partition(Launch &lc, const int32_t *ii, const int32_t *jj, c
                              int32_t M, int32_t *tile_cnt, int64_t *tile_off, int64_t *counts,
                              int32_t *out_i, int32_t *out_j, double *out_s, ErrState *err);
 int64_t partition_tiles(int64_t L);
+cudaError_t launch_block_hist(Launch &lc, const int32_t *jj, int64_t L, int64_t step, int nblocks,
+                              int64_t bsize, unsigned long long *hist);
 
 }  // namespace sa

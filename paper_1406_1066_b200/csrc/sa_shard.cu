@@ -314,9 +314,44 @@ __global__ void __launch_bounds__(PT_NT, 3) k_part_scatter(const int32_t *__rest
     report(bad, over, &err->bad_i, &err->over_m);
 }
 
+// Sampled column-block histogram for the rank boundaries (distributed.py):
+// every `step`-th triplet's column, in `nblocks` blocks of `bsize` columns
+// (columns outside [1, N] clamped into the end blocks), counts scaled by
+// `step`.  Shared-memory bins per CTA, one global add per touched bin.
+constexpr int BH_NT = 256;
+constexpr int BH_MAXB = 8192;
+__global__ void __launch_bounds__(BH_NT) k_block_hist(const int32_t *__restrict__ jj, int64_t L,
+                                                      int64_t step, int nblocks, int64_t bsize,
+                                                      unsigned long long *__restrict__ hist) {
+    __shared__ unsigned bins[BH_MAXB];
+    for (int b = threadIdx.x; b < nblocks; b += BH_NT) bins[b] = 0;
+    __syncthreads();
+    const int64_t ns = (L + step - 1) / step;
+    for (int64_t q = (int64_t)blockIdx.x * BH_NT + threadIdx.x; q < ns; q += (int64_t)gridDim.x * BH_NT) {
+        int64_t b = ((int64_t)__ldg(jj + q * step) - 1) / bsize;
+        b = b < 0 ? 0 : (b >= nblocks ? nblocks - 1 : b);
+        atomicAdd(&bins[b], 1u);
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < nblocks; b += BH_NT)
+        if (bins[b]) atomicAdd(&hist[b], (unsigned long long)bins[b] * (unsigned long long)step);
+}
+
 }  // namespace
 
 int64_t partition_tiles(int64_t L) { return (L + PT_TILE - 1) / PT_TILE; }
+
+cudaError_t launch_block_hist(Launch &lc, const int32_t *jj, int64_t L, int64_t step, int nblocks,
+                              int64_t bsize, unsigned long long *hist) {
+    if (nblocks < 1 || nblocks > BH_MAXB || step < 1 || bsize < 1) return cudaErrorInvalidValue;
+    cudaError_t e = cudaMemsetAsync(hist, 0, (size_t)nblocks * sizeof(unsigned long long), lc.stream);
+    if (e != cudaSuccess || L <= 0) return e;
+    const int64_t ns = (L + step - 1) / step;
+    const int grid = (int)std::min<int64_t>((ns + BH_NT - 1) / BH_NT, (int64_t)lc.num_sms * 2);
+    k_block_hist<<<grid, BH_NT, 0, lc.stream>>>(jj, L, step, nblocks, bsize, hist);
+    lc.launches++;
+    return cudaGetLastError();
+}
 
 cudaError_t launch_partition(Launch &lc, const int32_t *ii, const int32_t *jj, const double *s,
                              int64_t s_stride, int64_t L, int world, int self, const int32_t *bounds,

@@ -55,15 +55,17 @@ class ShardResult:
 def block_boundaries(block_hist: torch.Tensor, world: int, nblocks: int, n: int):
     """Split nblocks column blocks into `world` contiguous ranges with about
     equal triplet counts.  Returns (world+1) column boundaries (int list)."""
-    cum = torch.cumsum(block_hist.to(torch.int64).cpu(), 0)
+    import numpy as np
+
+    cum = np.cumsum(block_hist.to(torch.int64).cpu().numpy())
     total = int(cum[-1]) if len(cum) else 0
     bsize = (n + nblocks - 1) // nblocks
+    targets = np.array([(total * r) // world for r in range(1, world)], dtype=np.int64)
+    # first block whose cumulative count reaches each target
+    ks = np.searchsorted(cum, targets, side="left") if len(cum) else np.zeros(0, dtype=np.int64)
     bounds = [0]
     for r in range(1, world):
-        target = (total * r) // world
-        # first block index whose cumulative count reaches the target
-        k = int(torch.searchsorted(cum, torch.tensor(target, dtype=torch.int64), right=False))
-        col = min(n, (k + 1) * bsize) if total else (n * r) // world
+        col = min(n, (int(ks[r - 1]) + 1) * bsize) if total else (n * r) // world
         bounds.append(max(bounds[-1], col))
     bounds.append(n)
     return bounds
@@ -90,17 +92,39 @@ def partition_torch(ii, jj, s, bounds, world, self_rank=-1):
     return out, [int(c) for c in counts.tolist()]
 
 
+def _scratch(asm, name, n, dtype, dev):
+    """A reusable device buffer of at least n elements kept on the assembler
+    (allocating 10^8-byte tensors per call costs ~0.1 ms of host time)."""
+    cache = asm.__dict__.setdefault("_shard_scratch", {})
+    buf = cache.get(name)
+    if buf is None or buf.numel() < n or buf.dtype != dtype or buf.device != dev:
+        buf = cache[name] = torch.empty(max(int(n * 1.25), 1), dtype=dtype, device=dev)
+    return buf[:n]
+
+
+def _block_hist_cuda(asm, jj, nblocks, bsize, step):
+    """sa_block_histogram: the sampled column-block histogram in one launch."""
+    from .assembly import _ptr
+
+    hist = _scratch(asm, "hist", nblocks, torch.int64, jj.device)
+    rc = asm.lib.sa_block_histogram(asm.ctx, _ptr(jj), int(jj.shape[0]), step, nblocks, bsize, _ptr(hist))
+    if rc:
+        asm._raise(rc)
+    return hist
+
+
 def _partition_cuda(asm, ii, jj, s, m, n, bounds, world, self_rank):
-    """sa_partition: the CUDA partition (validates the chunk on the way)."""
+    """sa_partition: the CUDA partition (validates the chunk on the way);
+    the outputs are views of buffers reused across calls (valid until the
+    next call on this assembler)."""
     import ctypes
 
     from .assembly import _ptr
 
     dev = ii.device
     L = len(ii)
-    outs = (torch.empty(max(L, 1), dtype=torch.int32, device=dev),
-            torch.empty(max(L, 1), dtype=torch.int32, device=dev),
-            torch.empty(max(L, 1), dtype=torch.float64, device=dev))
+    outs = (_scratch(asm, "pi", max(L, 1), torch.int32, dev), _scratch(asm, "pj", max(L, 1), torch.int32, dev),
+            _scratch(asm, "ps", max(L, 1), torch.float64, dev))
     hb = (ctypes.c_int32 * (world + 1))(*bounds)
     hc = (ctypes.c_int64 * world)()
     bp, bw = ctypes.c_int64(-1), ctypes.c_int(-1)
@@ -115,8 +139,9 @@ def _partition_cuda(asm, ii, jj, s, m, n, bounds, world, self_rank):
     return tuple(x[:k] for x in outs), counts
 
 
-def _assemble_segments_cuda(asm, segs, col_lo, m, n_local):
-    """sa_assemble_segments_async over [(ii, jj, s), ...] read in place."""
+def _assemble_segments_cuda(asm, segs, col_lo, m, n_local, out=None):
+    """sa_assemble_segments_async over [(ii, jj, s), ...] read in place.
+    `out` (a dict) keeps the jc / ir / pr buffers across calls."""
     import ctypes
 
     from .assembly import DeviceCsc, _ptr
@@ -130,9 +155,17 @@ def _assemble_segments_cuda(asm, segs, col_lo, m, n_local):
     st = (ctypes.c_int64 * k)(*[0 if (x[2].numel() == 1 and n_ != 1) else 1 for x, n_ in zip(segs, lens)])
     ln = (ctypes.c_int64 * k)(*lens)
     cap = max(sum(lens), 1)
-    jc = torch.empty(n_local + 1, dtype=torch.int32, device=dev)
-    ir = torch.empty(cap, dtype=torch.int32, device=dev)
-    pr = torch.empty(cap, dtype=torch.float64, device=dev)
+    if out is not None:
+        def buf(name, k, dt):
+            b = out.get(name)
+            if b is None or b.numel() < k or b.device != dev:
+                b = out[name] = torch.empty(max(int(k * 1.25), 1), dtype=dt, device=dev)
+            return b[:k]
+        jc, ir, pr = buf("jc", n_local + 1, torch.int32), buf("ir", cap, torch.int32), buf("pr", cap, torch.float64)
+    else:
+        jc = torch.empty(n_local + 1, dtype=torch.int32, device=dev)
+        ir = torch.empty(cap, dtype=torch.int32, device=dev)
+        pr = torch.empty(cap, dtype=torch.float64, device=dev)
     asm._bind_stream()
     rc = asm.lib.sa_assemble_segments_async(asm.ctx, k, pi, pj, ps, st, ln, col_lo, m, n_local,
                                             _ptr(jc), _ptr(ir), _ptr(pr), cap)
@@ -147,7 +180,8 @@ def _assemble_segments_cuda(asm, segs, col_lo, m, n_local):
 
 
 def assemble_sharded(ii: torch.Tensor, jj: torch.Tensor, s: torch.Tensor, m: int, n: int,
-                     local_assemble=None, group=None, nblocks: int = 4096) -> ShardResult:
+                     local_assemble=None, group=None, nblocks: int = 4096,
+                     out: dict | None = None) -> ShardResult:
     """Assemble the global matrix whose triplets are split across the ranks
     of `group` (contiguous chunks in rank order).
 
@@ -157,7 +191,9 @@ def assemble_sharded(ii: torch.Tensor, jj: torch.Tensor, s: torch.Tensor, m: int
     in place, between what it received from lower and from higher ranks
     (sa_assemble_segments_async).  CPU tensors (gloo tests): the torch
     restatement of the partition, the received and own triplets
-    concatenated, and `local_assemble(ii, jj, s, m, n_local)` -> (jc, ir, pr)."""
+    concatenated, and `local_assemble(ii, jj, s, m, n_local)` -> (jc, ir, pr).
+    `out` (CUDA path, a dict kept by the caller): the result tensors are
+    written into buffers reused across calls (valid until the next call)."""
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     dev = ii.device
@@ -183,8 +219,11 @@ def assemble_sharded(ii: torch.Tensor, jj: torch.Tensor, s: torch.Tensor, m: int
     # the boundaries only balance the ranks' work: a strided sample of the
     # columns (<= 2^20 per rank) is enough and keeps this off the critical path
     step = max(1, len(jj) >> 20)
-    blk = torch.clamp((jj[::step].to(torch.int64) - 1) // bsize, 0, nblocks - 1)
-    hist = torch.bincount(blk, minlength=nblocks).to(torch.int64) * step
+    if cuda:
+        hist = _block_hist_cuda(asm, jj, nblocks, bsize, step)
+    else:
+        blk = torch.clamp((jj[::step].to(torch.int64) - 1) // bsize, 0, nblocks - 1)
+        hist = torch.bincount(blk, minlength=nblocks).to(torch.int64) * step
     dist.all_reduce(hist, group=group)
     bounds = block_boundaries(hist, world, nblocks, n)
     launches = 0
@@ -213,9 +252,9 @@ def assemble_sharded(ii: torch.Tensor, jj: torch.Tensor, s: torch.Tensor, m: int
     higher = (r_ii[k_lo:], r_jj[k_lo:], r_s[k_lo:])
     if cuda:
         segs = [x for x in (lower, (ii, jj, s), higher) if x[0].shape[0] > 0] or [(ii, jj, s)]
-        out = _assemble_segments_cuda(asm, segs, col_lo, m, n_local)
+        res = _assemble_segments_cuda(asm, segs, col_lo, m, n_local, out)
         launches += asm.lib.sa_last_launch_count(asm.ctx)
-        jc, ir, pr = out.jc, out.ir, out.pr
+        jc, ir, pr = res.jc, res.ir, res.pr
     else:
         mine = (jj.to(torch.int64) > col_lo) & (jj.to(torch.int64) <= col_hi)
         sv = s.expand(len(jj)) if s.numel() == 1 and len(jj) != 1 else s
@@ -229,7 +268,13 @@ def assemble_sharded(ii: torch.Tensor, jj: torch.Tensor, s: torch.Tensor, m: int
     dist.all_gather(all_nnz, nnz_local, group=group)
     nn = [int(x.item()) for x in all_nnz]
     off = sum(nn[:rank])
-    jc_global = jc.to(torch.int64) + off
+    if out is not None and cuda:
+        b = out.get("jc64")
+        if b is None or b.numel() < jc.numel() or b.device != dev:
+            b = out["jc64"] = torch.empty(max(int(jc.numel() * 1.25), 1), dtype=torch.int64, device=dev)
+        jc_global = torch.add(jc, off, out=b[: jc.numel()])
+    else:
+        jc_global = jc.to(torch.int64) + off
     return ShardResult(col_lo, col_hi, jc_global, ir, pr, off, sum(nn), m, n,
                        int(r_ii.shape[0]) + counts[rank], sent_remote, launches)
 

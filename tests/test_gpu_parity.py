@@ -329,11 +329,15 @@ def test_matrixmarket_round_trip_bit_faithful(tmp_path):
         read_triplets_matrixmarket(p)
 
 
-@pytest.mark.parametrize("world,self_rank", [(1, -1), (2, 0), (3, 2), (8, -1), (8, 5)])
-def test_partition_kernel_matches_torch_restatement(world, self_rank):
+@pytest.mark.parametrize("world,self_rank,banded", [(1, -1, False), (2, 0, False), (3, 2, False),
+                                                     (8, -1, False), (8, 5, False), (4, 1, True),
+                                                     (8, 7, True)])
+def test_partition_kernel_matches_torch_restatement(world, self_rank, banded):
     """sa_partition (CUDA) == partition_torch: destinations in rank order,
     stable inside each, the own rank's triplets counted but left in place,
-    out-of-block columns dropped; and the chunk validation."""
+    out-of-block columns dropped; and the chunk validation.  `banded`:
+    columns nearly sorted (element-ordered meshes), so most threads take
+    the one-destination shortcut and whole tiles stay home."""
     import ctypes
 
     from paper_1406_1066_b200.assembly import _ptr
@@ -343,6 +347,9 @@ def test_partition_kernel_matches_torch_restatement(world, self_rank):
     L, n = 70_001, 5_000
     ii = rng.integers(1, 900, size=L).astype(np.int32)
     jj = rng.integers(1, n + 1, size=L).astype(np.int32)
+    if banded:
+        jj = np.sort(jj)
+        jj[::97] = rng.integers(1, n + 1, size=len(jj[::97]))  # a few far columns
     s = rng.standard_normal(L)
     cuts = sorted(rng.choice(np.arange(1, n), size=world - 1, replace=False).tolist())
     bounds = [0] + cuts + [n]
@@ -375,6 +382,27 @@ def test_partition_kernel_matches_torch_restatement(world, self_rank):
     assert rc != 0 and bp == 10 and bw == 1  # SA_WHICH_COL
     rc, _, _, _, _ = run(ii, jj, 500, n)  # rows above M
     assert rc != 0
+
+
+@pytest.mark.parametrize("L,step,nblocks", [(0, 1, 16), (1, 1, 1), (100_003, 7, 4096), (2_000_000, 1, 333)])
+def test_block_histogram_matches_bincount(L, step, nblocks):
+    """sa_block_histogram == the torch restatement (distributed.py CPU path):
+    every step-th column, clamped blocks, counts scaled by step."""
+    from paper_1406_1066_b200.assembly import _ptr
+
+    rng = np.random.default_rng(L)
+    n = 50_000
+    jj = rng.integers(-3, n + 10, size=L).astype(np.int32)  # out-of-range columns clamp
+    bsize = (n + nblocks - 1) // nblocks
+    a = sa.default_assembler(0)
+    a._bind_stream()
+    dev = torch.device("cuda", 0)
+    tj = torch.from_numpy(jj).to(dev)
+    hist = torch.full((nblocks,), -1, dtype=torch.int64, device=dev)
+    assert a.lib.sa_block_histogram(a.ctx, _ptr(tj) if L else None, L, step, nblocks, bsize, _ptr(hist)) == 0
+    blk = torch.clamp((torch.from_numpy(jj[::step]).to(torch.int64) - 1) // bsize, 0, nblocks - 1)
+    ref = torch.bincount(blk, minlength=nblocks).to(torch.int64) * step
+    assert torch.equal(hist.cpu(), ref)
 
 
 @pytest.mark.parametrize("kind", ["fem2d", "heavy"])
