@@ -109,3 +109,94 @@ def test_block_boundaries_balance():
     assert b[0] == 0 and b[-1] == 80 and all(x <= y for x, y in zip(b, b[1:]))
     b1 = block_boundaries(torch.zeros(8, dtype=torch.int64), 2, 8, 80)
     assert b1 == [0, 40, 80]
+
+
+def _bounce_collectives():
+    """gloo collectives for CUDA tensors, bounced through host memory (the
+    CUDA-path test below runs several ranks on the one GPU; NCCL refuses two
+    ranks on one device).  Only the transport changes; the CUDA kernels of
+    each rank run on their own and never wait on another rank's."""
+    orig = {k: getattr(dist, k) for k in ("all_reduce", "all_to_all_single", "all_gather")}
+
+    def all_reduce(t, *a, **k):
+        c = t.cpu()
+        r = orig["all_reduce"](c, *a, **k)
+        t.copy_(c)
+        return r
+
+    def all_to_all_single(out, inp, *a, **k):
+        c = out.cpu()
+        r = orig["all_to_all_single"](c, inp.cpu(), *a, **k)
+        out.copy_(c)
+        return r
+
+    def all_gather(lst, t, *a, **k):
+        cl = [x.cpu() for x in lst]
+        r = orig["all_gather"](cl, t.cpu(), *a, **k)
+        for x, c in zip(lst, cl):
+            x.copy_(c)
+        return r
+
+    dist.all_reduce, dist.all_to_all_single, dist.all_gather = all_reduce, all_to_all_single, all_gather
+
+
+def _gpu_worker(rank, world, port, kind, result_q):
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path[:0] = [root, os.path.join(root, "tests")]
+    from paper_1406_1066_b200.distributed import assemble_sharded, gpu_local_assembler
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    _bounce_collectives()
+    try:
+        ii, jj, s, m, n = _case(kind)
+        L = len(ii)
+        lo, hi = L * rank // world, L * (rank + 1) // world
+        dev = torch.device("cuda", 0)
+        t = [torch.from_numpy(x[lo:hi].copy()).to(dev) for x in (ii, jj, s)]
+        out = {}
+        for _ in range(2):  # the second call reuses the scratch and result buffers
+            res = assemble_sharded(*t, m, n, gpu_local_assembler(0), nblocks=64, out=out)
+        result_q.put((rank, res.col_lo, res.col_hi, res.jc.cpu().numpy(), res.ir.cpu().numpy(),
+                      res.pr.cpu().numpy(), res.nnz_offset, res.nnz_total, res.sent_remote))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind,world", [("fem2d", 2), ("fem3d", 3), ("heavy", 2), ("heavy", 3),
+                                        ("random", 2)])
+def test_cuda_sharded_path_matches_single_process(kind, world):
+    """assemble_sharded's CUDA branch (sa_block_histogram, sa_partition,
+    exchange, sa_assemble_segments_async over the received and own
+    segments, jc offsets) with `world` ranks on the one GPU: the stitched
+    column blocks equal the single-process oracle bit for bit."""
+    from oracle import oracle as O
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gpu_worker, args=(r, world, port, kind, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = sorted([q.get(timeout=300) for _ in range(world)])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    ii, jj, s, m, n = _case(kind)
+    ref = O.assemble_counting(ii, jj, s, m, n)
+    jc = [0]
+    ir, pr = [], []
+    assert got[0][1] == 0 and got[-1][2] == n
+    for rank, lo, hi, bjc, bir, bpr, off, tot, _ in got:
+        assert bjc[0] == off and tot == ref.nnz
+        jc.extend(bjc[1:].tolist())
+        ir.append(bir)
+        pr.append(bpr)
+    assert np.array_equal(np.array(jc), ref.jc)
+    assert np.array_equal(np.concatenate(ir), ref.ir)
+    assert np.concatenate(pr).tobytes() == ref.pr.tobytes()
+    if kind == "heavy":  # shuffled input: the exchange moved triplets both ways
+        assert all(g[-1] > 0 for g in got)
