@@ -502,19 +502,57 @@ __device__ __forceinline__ unsigned column_mask(const int (&j)[CPT], int64_t t0,
 }
 
 // ---------------------------------------------------------------------------
-// k_colcount_win: column histogram + column-index validation.  Runs count
-// into a directly indexed shared-memory window of WB columns around the
-// chunk's first column (one shared atomic per run, no hashing); the first
-// touch of a window column lists it, and after the chunk every listed column
-// issues one global atomic.  Columns outside the window go to global memory
-// directly.
+// k_colcount_win: column histogram + column-index validation.  Each CTA
+// takes a contiguous range of chunks (element-ordered input keeps the
+// range's columns within a few mesh rows) and counts runs into a directly
+// indexed shared-memory window of WB columns with non-returning shared adds.
+// The window starts just behind the range's first column and is flushed to
+// global memory (the touched bin range only: one global atomic per touched
+// column) at the end of the range, or when a chunk's first column has left
+// the window's first half -- at most every RECENTER chunks, so shuffled
+// input does not flush every chunk.  Columns outside the window go to
+// global memory directly.
 // ---------------------------------------------------------------------------
 constexpr int WB = 8192;
+constexpr int WBACK = 512;    // window bins behind the first column
+constexpr int RECENTER = 4;   // chunks between window moves, at least
 
 struct WinSmem {
-    uint32_t bin[WB];      // per window column: triplets of the chunk
-    int lo[2], hi[2];      // touched bin range of the chunk (by chunk parity)
+    uint32_t bin[WB];  // per window column: triplets of the CTA's range
+    int lo, hi;        // touched bin range
 };
+
+// Window bins [lo, hi] touched since the last flush -> global counts; the
+// bins are zeroed and the touched range reset.  Called by the whole CTA.
+__device__ __forceinline__ void flush_window(WinSmem &W, int &blo, int &bhi, int cb,
+                                             uint32_t *__restrict__ cnt) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        blo = min(blo, __shfl_xor_sync(FULL, blo, o));
+        bhi = max(bhi, __shfl_xor_sync(FULL, bhi, o));
+    }
+    if ((threadIdx.x & 31) == 0 && bhi >= 0) {
+        atomicMin(&W.lo, blo);
+        atomicMax(&W.hi, bhi);
+    }
+    __syncthreads();
+    const int lo = W.lo, hi = W.hi;
+    for (int b = lo + (int)threadIdx.x; b <= hi; b += AGG_NT) {
+        const uint32_t v = W.bin[b];
+        if (v) {
+            atomicAdd(&cnt[cb + b], v);
+            W.bin[b] = 0;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        W.lo = WB;
+        W.hi = -1;
+    }
+    __syncthreads();
+    blo = WB;
+    bhi = -1;
+}
 
 __global__ void __launch_bounds__(AGG_NT) k_colcount_win(Segs S, int32_t N,
                                                          uint32_t *__restrict__ cnt,
@@ -522,9 +560,9 @@ __global__ void __launch_bounds__(AGG_NT) k_colcount_win(Segs S, int32_t N,
     __shared__ WinSmem W;
     const int tid = threadIdx.x;
     for (int k = tid; k < WB; k += AGG_NT) W.bin[k] = 0;
-    if (tid < 2) {
-        W.lo[tid] = WB;
-        W.hi[tid] = -1;
+    if (tid == 0) {
+        W.lo = WB;
+        W.hi = -1;
     }
     __syncthreads();
     pdl_wait();
@@ -533,28 +571,37 @@ __global__ void __launch_bounds__(AGG_NT) k_colcount_win(Segs S, int32_t N,
     unsigned over = 0;
     const int64_t nchunk = S.ch0[S.nseg];
     const bool skip = S.skip_foreign != 0;
-    int par = 0;
-    int jn[CPT];
-    if ((int64_t)blockIdx.x < nchunk) {
-        const SegChunk c = seg_chunk_1(S, blockIdx.x);
+    const int64_t per = (nchunk + gridDim.x - 1) / gridDim.x;
+    const int64_t c_begin = (int64_t)blockIdx.x * per, c_end = min(nchunk, c_begin + per);
+    int blo = WB, bhi = -1;
+    int cb = 0;  // window base (column index of bin 0)
+    int64_t moved = c_begin;
+    int jn[CPT], fn = 0;  // the next chunk's columns and first column, in flight
+    if (c_begin < c_end) {
+        const SegChunk c = seg_chunk_1(S, c_begin);
+        fn = __ldg(c.jj + c.t0);
+        cb = fn - S.col_lo - 1 - WBACK;  // the range runs forward in the mesh
         load_run(c.jj, c.t0 + (int64_t)tid * CPT, c.len, c.vec, jn, 0x7fffffff);
     }
-    for (int64_t ch = blockIdx.x; ch < nchunk; ch += gridDim.x) {
+    for (int64_t ch = c_begin; ch < c_end; ++ch) {
         const SegChunk c = seg_chunk_1(S, ch);
         const int64_t t0 = c.t0 + (int64_t)tid * CPT;
-        const int cb = __ldg(c.jj + c.t0) - S.col_lo - 1 - WB / 2;  // window base
+        const int first = fn - S.col_lo - 1;
+        if (ch - moved >= RECENTER && (first < cb || first >= cb + WB / 2)) {  // CTA-uniform
+            flush_window(W, blo, bhi, cb, cnt);
+            cb = first - WBACK;
+            moved = ch;
+        }
         int j[CPT];
 #pragma unroll
         for (int k = 0; k < CPT; ++k) j[k] = jn[k] - S.col_lo;
-        if (ch + gridDim.x < nchunk) {  // prefetch the next chunk while this one is counted
-            const SegChunk cn = seg_chunk_1(S, ch + gridDim.x);
+        if (ch + 1 < c_end) {  // prefetch the next chunk while this one is counted
+            const SegChunk cn = seg_chunk_1(S, ch + 1);
+            fn = __ldg(cn.jj + cn.t0);
             load_run(cn.jj, cn.t0 + (int64_t)tid * CPT, cn.len, cn.vec, jn, 0x7fffffff);
         }
         const unsigned vmask = column_mask(j, t0, c.len, c.pos0, N, skip, bad, over);
         const Runs R = run_masks(j, vmask);
-        // non-returning shared adds; the chunk's touched bin range is scanned
-        // at flush time instead of listing first touches (a returning atomic)
-        int blo = WB, bhi = -1;
 #pragma unroll
         for (int k = 0; k < CPT; ++k) {
             if (R.heads & (1u << k)) {
@@ -569,31 +616,8 @@ __global__ void __launch_bounds__(AGG_NT) k_colcount_win(Segs S, int32_t N,
                 }
             }
         }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            blo = min(blo, __shfl_xor_sync(FULL, blo, o));
-            bhi = max(bhi, __shfl_xor_sync(FULL, bhi, o));
-        }
-        if ((tid & 31) == 0 && bhi >= 0) {
-            atomicMin(&W.lo[par], blo);
-            atomicMax(&W.hi[par], bhi);
-        }
-        __syncthreads();
-        const int lo = W.lo[par], hi = W.hi[par];
-        for (int b = lo + tid; b <= hi; b += AGG_NT) {
-            const uint32_t v = W.bin[b];
-            if (v) {
-                atomicAdd(&cnt[cb + b], v);
-                W.bin[b] = 0;
-            }
-        }
-        if (tid == 0) {  // the next chunk's range (its adds start after the barrier)
-            W.lo[par ^ 1] = WB;
-            W.hi[par ^ 1] = -1;
-        }
-        par ^= 1;
-        __syncthreads();
     }
+    flush_window(W, blo, bhi, cb, cnt);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         bad = min(bad, __shfl_xor_sync(FULL, bad, o));
