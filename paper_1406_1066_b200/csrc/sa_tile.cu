@@ -647,30 +647,29 @@ __device__ bool fold_column_hash(int2 *Kc, double *Vc, int c, HashScratch &H) {
             const int me = pp[q];
             int r = 0, k = b0;
             for (; k + 4 <= b0 + n; k += 4)
-                r += (M[k & IM].x < me) + (M[(k + 1) & IM].x < me) + (M[(k + 2) & IM].x < me) +
-                     (M[(k + 3) & IM].x < me);
-            for (; k < b0 + n; ++k) r += M[k & IM].x < me;
-            fi[q] = (b0 + r) & IM;
+                r += (M[k].x < me) + (M[k + 1].x < me) + (M[k + 2].x < me) + (M[k + 3].x < me);
+            for (; k < b0 + n; ++k) r += M[k].x < me;
+            fi[q] = b0 + r;  // (member indices stay below the column length)
         }
     }
     __syncwarp();
 #pragma unroll
     for (int q = 0; q < EPL; ++q) {
         const int i = q * 32 + lane;
-        if (q < nb && i < c && (!sorted_groups || fi[q] >= 0)) M[fi[q] & IM].y = i;
+        if (q < nb && i < c && (!sorted_groups || fi[q] >= 0)) M[fi[q]].y = i;
     }
     __syncwarp();
     // one lane per group folds it in position order
     double acc_a = 0.0, acc_b = 0.0;
     if (lane < D) {
         const int n = na;
-        acc_a = fold_add(0.0, Vc[M[oa & IM].y & IM]);
-        for (int k = 1; k < n; ++k) acc_a = fold_add(acc_a, Vc[M[(oa + k) & IM].y & IM]);
+        acc_a = fold_add(0.0, Vc[M[oa].y]);
+        for (int k = 1; k < n; ++k) acc_a = fold_add(acc_a, Vc[M[oa + k].y]);
     }
     if (lane + 32 < D) {
         const int n = nb2;
-        acc_b = fold_add(0.0, Vc[M[ob & IM].y & IM]);
-        for (int k = 1; k < n; ++k) acc_b = fold_add(acc_b, Vc[M[(ob + k) & IM].y & IM]);
+        acc_b = fold_add(0.0, Vc[M[ob].y]);
+        for (int k = 1; k < n; ++k) acc_b = fold_add(acc_b, Vc[M[ob + k].y]);
     }
     __syncwarp();
     if (lane < D) {
