@@ -533,6 +533,21 @@ __device__ __noinline__ void sort_big_groups(int2 *M, unsigned bga, unsigned bgb
     }
 }
 
+// Ordered fold of one row group (members M[m0 .. m0+n), value slots in .y)
+// from +0.0.  Plain adds give the bits of fold_add's x86 rule unless the sum
+// turns NaN (only then can two NaN payloads meet), so the rule's select is
+// kept off the dependent chain and the fold is redone exactly in that case.
+__device__ __forceinline__ double fold_group_exact(const double *Vc, const int2 *M, int m0, int n) {
+    double a = fold_add(0.0, Vc[M[m0].y]);
+    for (int k = 1; k < n; ++k) a = fold_add(a, Vc[M[m0 + k].y]);
+    return a;
+}
+__device__ __forceinline__ double fold_group(const double *Vc, const int2 *M, int m0, int n) {
+    double a = __dadd_rn(0.0, Vc[M[m0].y]);
+    for (int k = 1; k < n; ++k) a = __dadd_rn(a, Vc[M[m0 + k].y]);
+    return (a != a) ? fold_group_exact(Vc, M, m0, n) : a;
+}
+
 __device__ bool fold_column_hash(int2 *Kc, double *Vc, int c, HashScratch &H) {
     constexpr int EPL = LONGCAP / 32;
     constexpr int IM = LONGCAP - 1;
@@ -663,13 +678,11 @@ __device__ bool fold_column_hash(int2 *Kc, double *Vc, int c, HashScratch &H) {
     double acc_a = 0.0, acc_b = 0.0;
     if (lane < D) {
         const int n = na;
-        acc_a = fold_add(0.0, Vc[M[oa].y]);
-        for (int k = 1; k < n; ++k) acc_a = fold_add(acc_a, Vc[M[oa + k].y]);
+        acc_a = fold_group(Vc, M, oa, n);
     }
     if (lane + 32 < D) {
         const int n = nb2;
-        acc_b = fold_add(0.0, Vc[M[ob].y]);
-        for (int k = 1; k < n; ++k) acc_b = fold_add(acc_b, Vc[M[ob + k].y]);
+        acc_b = fold_group(Vc, M, ob, n);
     }
     __syncwarp();
     if (lane < D) {
