@@ -640,7 +640,7 @@ __device__ bool fold_column_hash(int2 *Kc, double *Vc, int c, HashScratch &H) {
 #pragma unroll
     for (int q = 0; q < EPL; ++q) {
         const int i = q * 32 + lane;
-        if (q < nb && i < c) M[(H.off[hs[q] & 255] + (hs[q] >> 8)) & IM] = make_int2(pp[q], i);
+        if (q < nb && i < c) M[H.off[hs[q] & 255] + (hs[q] >> 8)] = make_int2(pp[q], i);
     }
     __syncwarp();
     // groups of BIGG < n <= 64 members: one warp-wide bitonic of {position, entry} each
