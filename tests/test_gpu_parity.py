@@ -620,3 +620,31 @@ def test_output_modes_bit_exact(staged, monkeypatch):
         out = sa.default_assembler(0).assemble_device(w.ii, w.jj, w.s, m=w.m, n=w.n)
         ref = O.assemble_counting(w.ii.cpu().numpy(), w.jj.cpu().numpy(), w.s.cpu().numpy(), w.m, w.n)
         _same(out.to_host(), ref)
+
+
+@pytest.mark.parametrize("width", [40, 90, 200])
+def test_nan_payloads_in_hash_folded_columns(width):
+    """Columns of `width` triplets over few distinct rows (the hash-group
+    fold) whose row groups mix several NaN payloads, +-inf (inf - inf),
+    -0.0 and ordinary values: every group's sum must carry the x86 payload
+    rule (the first NaN the ordered sum meets), bit for bit with the C
+    oracle.  The plain-add chain re-folds exactly only for NaN sums."""
+    rng = np.random.default_rng(width)
+    n, rows = 300, 12
+    jj = np.repeat(np.arange(1, n + 1, dtype=np.int32), width)
+    ii = rng.integers(1, rows + 1, size=len(jj)).astype(np.int32)
+    perm = rng.permutation(len(jj))
+    ii, jj = ii[perm], jj[perm]
+    s = rng.standard_normal(len(jj))
+    payloads = np.array([0x7FF8000000000001, 0x7FF8000000000ABC, 0xFFF8000000000123,
+                         0x7FF0000000000007], dtype=np.uint64).view(np.float64)  # last: signalling
+    pick = rng.random(len(jj))
+    s[pick < 0.02] = rng.choice(payloads, size=int((pick < 0.02).sum()))
+    s[(pick >= 0.02) & (pick < 0.03)] = np.inf
+    s[(pick >= 0.03) & (pick < 0.04)] = -np.inf
+    s[(pick >= 0.04) & (pick < 0.05)] = -0.0
+    got = sa.assemble(ii, jj, s, m=rows, n=n)
+    ref = O.assemble_counting(ii, jj, s, rows, n)
+    assert np.array_equal(got.jc, ref.jc) and np.array_equal(got.ir, ref.ir)
+    assert got.pr.tobytes() == ref.pr.tobytes()
+    assert np.isnan(ref.pr).sum() > 10  # the case does exercise NaN groups
