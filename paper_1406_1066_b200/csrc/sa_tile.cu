@@ -475,7 +475,6 @@ __device__ __noinline__ void fold_columns_group(int2 *K, double *V, const int *l
 // untouched, when it has more than HU distinct rows.
 constexpr int HT = 128;  // hash slots per warp
 constexpr int HU = 64;   // most distinct rows
-constexpr int BIGG = 16;  // groups above this size (up to 64) are sorted, not ranked
 struct HashScratch {
     int row[HT];       // slot -> row (0: empty; rows are >= 1)
     int cnt[HT];       // slot -> entries
@@ -486,52 +485,6 @@ struct HashScratch {
 static_assert(sizeof(HashScratch) <= LONGCAP * sizeof(unsigned long long), "per-warp scratch");
 
 __device__ __forceinline__ int row_hash(int r) { return (int)(((unsigned)r * 0x9E3779B1u) >> 25); }
-
-// Groups of BIGG < n <= 64 members of a hash-folded column (ballots bga /
-// bgb over the distinct rows lane / lane + 32): each sorted by input
-// position with one warp-wide bitonic of {position, entry}.  Out of line:
-// rarely taken, and the fold kernel's code is large.
-__device__ __noinline__ void sort_big_groups(int2 *M, unsigned bga, unsigned bgb, int oa, int ob,
-                                             int na, int nb2) {
-    constexpr int IM = LONGCAP - 1;
-    const int lane = threadIdx.x & 31;
-    while (bga | bgb) {
-        int gb0, g;
-        if (bga) {
-            const int src = __ffs(bga) - 1;
-            bga &= bga - 1;
-            gb0 = __shfl_sync(FULL, oa, src);
-            g = __shfl_sync(FULL, na, src);
-        } else {
-            const int src = __ffs(bgb) - 1;
-            bgb &= bgb - 1;
-            gb0 = __shfl_sync(FULL, ob, src);
-            g = __shfl_sync(FULL, nb2, src);
-        }
-        if (g <= 32) {
-            unsigned long long k1[1];
-            const int2 m = lane < g ? M[(gb0 + lane) & IM] : make_int2(0, 0);
-            k1[0] = lane < g ? ((unsigned long long)(unsigned)m.x << 8) | (unsigned)m.y : ~0ull;
-            group_bitonic<32, 1>(k1);
-            if (lane < g) M[(gb0 + lane) & IM] = make_int2((int)(k1[0] >> 8), (int)(k1[0] & 255));
-        } else {
-            unsigned long long k2[2];
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                const int x = 2 * lane + e;
-                const int2 m = x < g ? M[(gb0 + x) & IM] : make_int2(0, 0);
-                k2[e] = x < g ? ((unsigned long long)(unsigned)m.x << 8) | (unsigned)m.y : ~0ull;
-            }
-            group_bitonic<32, 2>(k2);
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                const int x = 2 * lane + e;
-                if (x < g) M[(gb0 + x) & IM] = make_int2((int)(k2[e] >> 8), (int)(k2[e] & 255));
-            }
-        }
-        __syncwarp();
-    }
-}
 
 // Ordered fold of one row group (members M[m0 .. m0+n), value slots in .y)
 // from +0.0.  Plain adds give the bits of fold_add's x86 rule unless the sum
@@ -550,7 +503,6 @@ __device__ __forceinline__ double fold_group(const double *Vc, const int2 *M, in
 
 __device__ bool fold_column_hash(int2 *Kc, double *Vc, int c, HashScratch &H) {
     constexpr int EPL = LONGCAP / 32;
-    constexpr int IM = LONGCAP - 1;
     const int lane = threadIdx.x & 31;
     const unsigned lt = lanemask_lt();
 #pragma unroll
@@ -640,38 +592,38 @@ __device__ bool fold_column_hash(int2 *Kc, double *Vc, int c, HashScratch &H) {
 #pragma unroll
     for (int q = 0; q < EPL; ++q) {
         const int i = q * 32 + lane;
-        if (q < nb && i < c) M[H.off[hs[q] & 255] + (hs[q] >> 8)] = make_int2(pp[q], i);
+        if (q < nb && i < c) M[H.off[hs[q] & 255] + (hs[q] >> 8)] = make_int2(pp[q], i | (int)((hs[q] & 255) << 8));
     }
     __syncwarp();
-    // groups of BIGG < n <= 64 members: one warp-wide bitonic of {position, entry} each
     const int na = lane < D ? H.dl[lane].y : 0, nb2 = lane + 32 < D ? H.dl[lane + 32].y : 0;
-    unsigned bga = __ballot_sync(FULL, na > BIGG && na <= 64);
-    unsigned bgb = __ballot_sync(FULL, nb2 > BIGG && nb2 <= 64);
-    const bool sorted_groups = (bga | bgb) != 0;
-    if (sorted_groups) sort_big_groups(M, bga, bgb, oa, ob, na, nb2);
-    // the other groups: rank inside the group by input position
-    int fi[EPL];
+    // rank inside the group by input position, members taken in grouped
+    // order (M[x] = {position, slot | group slot << 8}): consecutive lanes
+    // hold members of one group, so a warp iterates about as long as its
+    // own groups, and no group needs a sort
+    int mp[EPL], mw[EPL];
 #pragma unroll
     for (int q = 0; q < EPL; ++q) {
-        fi[q] = -1;
-        const int i = q * 32 + lane;
-        if (q < nb && i < c) {
-            const int s = hs[q] & 255;
-            const int b0 = H.off[s], n = H.cnt[s];
-            if (sorted_groups && n > BIGG && n <= 64) continue;  // sorted above
-            const int me = pp[q];
-            int r = 0, k = b0;
-            for (; k + 4 <= b0 + n; k += 4)
-                r += (M[k].x < me) + (M[k + 1].x < me) + (M[k + 2].x < me) + (M[k + 3].x < me);
-            for (; k < b0 + n; ++k) r += M[k].x < me;
-            fi[q] = b0 + r;  // (member indices stay below the column length)
+        const int x = q * 32 + lane;
+        mp[q] = 0;
+        mw[q] = -1;
+        if (q < nb && x < c) {
+            const int2 w = M[x];
+            mp[q] = w.x;
+            mw[q] = w.y;
         }
     }
-    __syncwarp();
+    __syncwarp();  // every member word is read before the slots are written
 #pragma unroll
     for (int q = 0; q < EPL; ++q) {
-        const int i = q * 32 + lane;
-        if (q < nb && i < c && (!sorted_groups || fi[q] >= 0)) M[fi[q]].y = i;
+        if (mw[q] < 0) continue;
+        const int s = mw[q] >> 8;
+        const int b0 = H.off[s], n = H.cnt[s];
+        const int me = mp[q];
+        int r = 0, k = b0;
+        for (; k + 4 <= b0 + n; k += 4)
+            r += (M[k].x < me) + (M[k + 1].x < me) + (M[k + 2].x < me) + (M[k + 3].x < me);
+        for (; k < b0 + n; ++k) r += M[k].x < me;
+        M[b0 + r].y = mw[q] & 255;  // (positions in .x are only read)
     }
     __syncwarp();
     // one lane per group folds it in position order
