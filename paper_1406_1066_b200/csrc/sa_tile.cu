@@ -497,6 +497,7 @@ __device__ __forceinline__ double fold_group_exact(const double *Vc, const int2 
 }
 __device__ __forceinline__ double fold_group(const double *Vc, const int2 *M, int m0, int n) {
     double a = __dadd_rn(0.0, Vc[M[m0].y]);
+#pragma unroll 4
     for (int k = 1; k < n; ++k) a = __dadd_rn(a, Vc[M[m0 + k].y]);
     return (a != a) ? fold_group_exact(Vc, M, m0, n) : a;
 }
