@@ -620,10 +620,11 @@ __device__ bool fold_column_hash(int2 *Kc, double *Vc, int c, HashScratch &H) {
         const int s = mw[q] >> 8;
         const int b0 = H.off[s], n = H.cnt[s];
         const int me = mp[q];
-        int r = 0, k = b0;
-        for (; k + 4 <= b0 + n; k += 4)
-            r += (M[k].x < me) + (M[k + 1].x < me) + (M[k + 2].x < me) + (M[k + 3].x < me);
-        for (; k < b0 + n; ++k) r += M[k].x < me;
+        const int e = b0 + n;
+        int r = 0;
+        for (int k = b0; k < e; k += 4)  // 4 per step, the tail predicated (groups of 4-6 are common)
+            r += (M[k].x < me) + (k + 1 < e && M[k + 1].x < me) + (k + 2 < e && M[k + 2].x < me) +
+                 (k + 3 < e && M[k + 3].x < me);
         M[b0 + r].y = mw[q] & 255;  // (positions in .x are only read)
     }
     __syncwarp();
