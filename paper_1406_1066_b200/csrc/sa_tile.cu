@@ -573,6 +573,7 @@ __device__ bool fold_column_hash(int2 *Kc, double *Vc, int c, HashScratch &H) {
     const int ra = lane < D ? H.dl[lane].x : 0x7fffffff;
     const int rb = lane + 32 < D ? H.dl[lane + 32].x : 0x7fffffff;
     int ka = 0, kb = 0, oa = 0, ob = 0;
+#pragma unroll 4
     for (int k = 0; k < D; ++k) {
         const int2 x = H.dl[k];
         if (x.x < ra) {
