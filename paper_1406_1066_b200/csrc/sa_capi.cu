@@ -429,7 +429,7 @@ int assemble_segments(sa_ctx *ctx, const Segs &S, int64_t L, int32_t M, int32_t 
     }
     // long columns dominate: stage the outputs instead of chaining tile offsets
     const char *env = getenv("SA_STAGED");
-    const bool staged = env ? atoi(env) != 0 : (L >= 64 * (int64_t)N && ntiles >= 16 * ctx->num_sms);
+    const bool staged = env ? atoi(env) != 0 : (L >= 40 * (int64_t)N && ntiles >= 16 * ctx->num_sms);
     if (staged) {
         SA_CUDA(ctx, ensure(ctx->tile_cnt, ctx->tc_cap, (size_t)ntiles));
     }
