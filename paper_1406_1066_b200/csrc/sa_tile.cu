@@ -219,10 +219,11 @@ __device__ int fold_short_net(const int2 *K, int c, uint8_t *perm) {
                                         (((unsigned)posv[w] - pmin) << 5) | w)
                            : 0xffffffffu;
         run_network<W, unsigned>(k);
+        const unsigned rmask = (sh >= 32) ? 0u : (~0u << sh);  // the row bits of a key
 #pragma unroll
         for (int w = 0; w < W; ++w) {
             if (w < c) perm[w] = (uint8_t)(k[w] & 31u);
-            if (w > 0 && w < c && ((unsigned long long)k[w] >> sh) != ((unsigned long long)k[w - 1] >> sh)) ++u;
+            if (w > 0 && w < c && ((k[w] ^ k[w - 1]) & rmask)) ++u;
         }
     } else if (pb <= 27) {
         unsigned long long k[W];
