@@ -284,8 +284,10 @@ __device__ int fold_short_net(const int2 *K, int c, uint8_t *perm) {
 // Fold a short column from its sorted order: each run of equal rows from
 // +0.0 in input-position order.  A run's output (row-1, u) / value is stored
 // in the slot of the run's first record (already read, never read again),
-// and perm[j] becomes the slot of output j.
-__device__ void fold_from_perm(int2 *K, double *V, uint8_t *perm, int c, int un) {
+// and perm[j] becomes the slot of output j; with an output map `om`, its
+// tile-local slot (off + slot) goes to om[j] as well.
+__device__ void fold_from_perm(int2 *K, double *V, uint8_t *perm, int c, int un, uint16_t *om,
+                               int off) {
     int head = perm[0];
     int prev = K[head].x;
     double acc = fold_add(0.0, V[head]);
@@ -297,6 +299,7 @@ __device__ void fold_from_perm(int2 *K, double *V, uint8_t *perm, int c, int un)
         if (row != prev) {
             K[head] = make_int2(prev - 1, un);
             V[head] = acc;
+            if (om) om[u] = (uint16_t)(off + head);
             perm[u++] = (uint8_t)head;
             head = sl;
             prev = row;
@@ -307,6 +310,7 @@ __device__ void fold_from_perm(int2 *K, double *V, uint8_t *perm, int c, int un)
     }
     K[head] = make_int2(prev - 1, un);
     V[head] = acc;
+    if (om) om[u] = (uint16_t)(off + head);
     perm[u] = (uint8_t)head;
 }
 
@@ -914,13 +918,10 @@ __global__ void __launch_bounds__(NT, SA_FOLD_MINB) k_tile_fold(const uint32_t *
             if (cnt <= 0) continue;
             const int off = s0 - r0;
             const int u = K[off].y;
-            if (cnt <= SHORT_COL) fold_from_perm(&K[off], &V[off], &S.perm[off], cnt, u);
-            if (!has_big) {
-                if (cnt <= SHORT_COL)
-                    for (int k = 0; k < u; ++k) S.omap[o + k] = (uint16_t)(off + S.perm[off + k]);
-                else
-                    for (int k = 0; k < u; ++k) S.omap[o + k] = (uint16_t)(off + k);
-            }
+            if (cnt <= SHORT_COL)  // (writes the output map itself)
+                fold_from_perm(&K[off], &V[off], &S.perm[off], cnt, u, has_big ? nullptr : &S.omap[o], off);
+            else if (!has_big)
+                for (int k = 0; k < u; ++k) S.omap[o + k] = (uint16_t)(off + k);
             o += u;
         }
     }
