@@ -648,3 +648,39 @@ def test_nan_payloads_in_hash_folded_columns(width):
     assert np.array_equal(got.jc, ref.jc) and np.array_equal(got.ir, ref.ir)
     assert got.pr.tobytes() == ref.pr.tobytes()
     assert np.isnan(ref.pr).sum() > 10  # the case does exercise NaN groups
+
+
+@pytest.mark.parametrize("world,self_rank", [(2, 1), (5, 0)])
+def test_partition_unaligned_inputs(world, self_rank):
+    """sa_partition on index arrays that are not 16-byte aligned (views one
+    element into a buffer): the scalar-load path, same result as the torch
+    restatement."""
+    import ctypes
+
+    from paper_1406_1066_b200.assembly import _ptr
+    from paper_1406_1066_b200.distributed import partition_torch
+
+    rng = np.random.default_rng(world + 10)
+    L, n = 50_003, 4_000
+    ii = rng.integers(1, 700, size=L + 1).astype(np.int32)
+    jj = np.sort(rng.integers(1, n + 1, size=L + 1)).astype(np.int32)
+    s = rng.standard_normal(L + 1)
+    bounds = [n * r // world for r in range(world + 1)]
+    dev = torch.device("cuda", 0)
+    ti, tj, ts = (torch.from_numpy(x).to(dev)[1:] for x in (ii, jj, s))  # 4 / 8-byte offsets
+    assert ti.data_ptr() % 16 and tj.data_ptr() % 16
+    a = sa.default_assembler(0)
+    a._bind_stream()
+    outs = [torch.empty(L, dtype=dt, device=dev) for dt in (torch.int32, torch.int32, torch.float64)]
+    hb = (ctypes.c_int32 * (world + 1))(*bounds)
+    hc = (ctypes.c_int64 * world)()
+    bp, bw = ctypes.c_int64(-1), ctypes.c_int(-1)
+    rc = a.lib.sa_partition(a.ctx, _ptr(ti), _ptr(tj), _ptr(ts), 1, L, 700, n, world, self_rank, hb,
+                            *(_ptr(x) for x in outs), hc, ctypes.byref(bp), ctypes.byref(bw))
+    assert rc == 0
+    ref, rcounts = partition_torch(torch.from_numpy(ii[1:]), torch.from_numpy(jj[1:]), torch.from_numpy(s[1:]),
+                                   bounds, world, self_rank)
+    k = len(ref[0])
+    assert [hc[r] for r in range(world)] == rcounts
+    assert torch.equal(outs[0][:k].cpu(), ref[0]) and torch.equal(outs[1][:k].cpu(), ref[1])
+    assert outs[2][:k].cpu().numpy().tobytes() == ref[2].numpy().tobytes()
