@@ -28,6 +28,9 @@ constexpr int TILE = 1792;
 constexpr int TILE_THREADS = 128;
 constexpr int BIGCOL = 256;
 constexpr int TCAP = TILE + BIGCOL;
+// Columns of at most SHORT_COL triplets are sorted by one thread's register
+// network in the fold; longer small columns go to its warp-level long pass.
+constexpr int SHORT_COL = 24;
 
 // One big column (k_col_scan appends, k_bigcol folds, k_tile_fold copies out).
 struct BigCol {
@@ -79,6 +82,7 @@ struct ErrState {
     unsigned int scan_ticket;
     unsigned int nbig;          // number of big columns
     unsigned int lsmall;        // triplets in small columns (small record space)
+    unsigned int long_cols;     // some small column is long (> SHORT_COL): the fold's long pass runs
 };
 
 __device__ __forceinline__ unsigned lanemask_lt() {

@@ -262,8 +262,13 @@ __global__ void __launch_bounds__(SCAN_NT) k_col_scan(const uint32_t *cnt,
         for (int k = 0; k < SCAN_IPT; ++k) loc[k] = (c0 + k < N) ? cnt[c0 + k] : 0u;
     }
     unsigned long long sum = 0;
+    bool long_col = false;
 #pragma unroll
-    for (int k = 0; k < SCAN_IPT; ++k) sum += scan_word(loc[k]);
+    for (int k = 0; k < SCAN_IPT; ++k) {
+        sum += scan_word(loc[k]);
+        long_col |= loc[k] > (uint32_t)SHORT_COL && loc[k] <= (uint32_t)BIGCOL;
+    }
+    if (__any_sync(FULL, long_col) && (threadIdx.x & 31) == 0) err->long_cols = 1u;
     unsigned long long total;
     const unsigned long long pre = block_excl_sum<SCAN_NT, unsigned long long>(sum, s_warp, total);
     TRACE(b, 1);

@@ -51,7 +51,6 @@ __device__ unsigned long long g_ftrace[1 << 15][8];
 namespace {
 
 constexpr int NT = TILE_THREADS;
-constexpr int SHORT_COL = 24;
 constexpr int NWARP = NT / 32;
 constexpr int LCAP = TILE / (SHORT_COL + 1) + 2;  // long columns per tile
 constexpr int SCAP = 256;                         // staged column starts per tile
@@ -700,8 +699,12 @@ __device__ long long lookback_warp32(unsigned long long *st, long long b, unsign
 
 }  // namespace
 
-template <bool STAGED>
-__global__ void __launch_bounds__(NT, SA_FOLD_MINB) k_tile_fold(const uint32_t *__restrict__ sstart,
+// The fold of one tile.  LONGP: the input has long small columns (the
+// column scan's flag); the body without the long pass is compiled on its
+// own, so short-column inputs (2D FEM) run code free of its registers and
+// instructions.
+template <bool STAGED, bool LONGP>
+__device__ __forceinline__ void tile_fold_body(const uint32_t *__restrict__ sstart,
                                                      const int2 *__restrict__ tile_info,
                                                      const uint8_t *__restrict__ tile_big,
                                                      int64_t ntiles,
@@ -720,8 +723,6 @@ __global__ void __launch_bounds__(NT, SA_FOLD_MINB) k_tile_fold(const uint32_t *
     TileSmem &S = *reinterpret_cast<TileSmem *>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const long long b = blockIdx.x;
-    pdl_wait();
-    pdl_trigger();
     FTRACE(b, 0);
     const int2 ti0 = tile_info[b], ti1 = tile_info[b + 1];
     const int c_a = ti0.x, r0 = ti0.y;
@@ -815,6 +816,7 @@ __global__ void __launch_bounds__(NT, SA_FOLD_MINB) k_tile_fold(const uint32_t *
     cp_async_wait_all();
     __syncthreads();  // values in; long-column list complete
     FTRACE(b, 3);
+    if constexpr (LONGP) {
     // ---- pass 2: warps fold the long columns: hash groups, one column per warp;
     // columns with too many distinct rows by the group bitonic, 4 / 2 / 1 per warp
     if (hash_fold && (S.ncls[0] | S.ncls[1] | S.ncls[2])) {
@@ -867,6 +869,7 @@ __global__ void __launch_bounds__(NT, SA_FOLD_MINB) k_tile_fold(const uint32_t *
     }
     __syncthreads();
 
+    }  // LONGP
     // ---- tile count and thread output bases; publish the aggregate early ------
     int ut = 0, bt = 0;  // outputs of this thread's columns; of its big columns
     for (int c = k_lo; c < k_hi; ++c) {
@@ -1060,6 +1063,26 @@ __global__ void __launch_bounds__(NT, SA_FOLD_MINB) k_tile_fold(const uint32_t *
         err->nnz = P + U;
         if (P + U > cap) atomicExch(&err->cap_exceeded, 1u);
     }
+}
+
+template <bool STAGED>
+__global__ void __launch_bounds__(NT, SA_FOLD_MINB) k_tile_fold(
+    const uint32_t *__restrict__ sstart, const int2 *__restrict__ tile_info,
+    const uint8_t *__restrict__ tile_big, int64_t ntiles, const int2 *__restrict__ entries, Segs SG,
+    const int4 *__restrict__ rec, const BigCol *__restrict__ big_list,
+    const uint32_t *__restrict__ bigk, unsigned long long *tile_state, int32_t N,
+    int32_t *__restrict__ jc, int32_t *__restrict__ ir, double *__restrict__ pr, int64_t cap,
+    ErrState *err, int hash_fold, int4 *__restrict__ stage, int2 *__restrict__ tile_cnt) {
+    pdl_wait();
+    pdl_trigger();
+    if (err->long_cols)
+        tile_fold_body<STAGED, true>(sstart, tile_info, tile_big, ntiles, entries, SG, rec, big_list,
+                                     bigk, tile_state, N, jc, ir, pr, cap, err, hash_fold, stage,
+                                     tile_cnt);
+    else
+        tile_fold_body<STAGED, false>(sstart, tile_info, tile_big, ntiles, entries, SG, rec, big_list,
+                                      bigk, tile_state, N, jc, ir, pr, cap, err, hash_fold, stage,
+                                      tile_cnt);
 }
 
 // ---- staged outputs (long-column inputs): no look-back in k_tile_fold ------
