@@ -1065,6 +1065,20 @@ __device__ __forceinline__ void tile_fold_body(const uint32_t *__restrict__ ssta
     }
 }
 
+// The long-column body out of line: the short body stays on the kernel's
+// fall-through path with its own code layout.
+template <bool STAGED>
+__device__ __noinline__ void tile_fold_long(
+    const uint32_t *__restrict__ sstart, const int2 *__restrict__ tile_info,
+    const uint8_t *__restrict__ tile_big, int64_t ntiles, const int2 *__restrict__ entries, Segs SG,
+    const int4 *__restrict__ rec, const BigCol *__restrict__ big_list,
+    const uint32_t *__restrict__ bigk, unsigned long long *tile_state, int32_t N,
+    int32_t *__restrict__ jc, int32_t *__restrict__ ir, double *__restrict__ pr, int64_t cap,
+    ErrState *err, int hash_fold, int4 *__restrict__ stage, int2 *__restrict__ tile_cnt) {
+    tile_fold_body<STAGED, true>(sstart, tile_info, tile_big, ntiles, entries, SG, rec, big_list, bigk,
+                                 tile_state, N, jc, ir, pr, cap, err, hash_fold, stage, tile_cnt);
+}
+
 template <bool STAGED>
 __global__ void __launch_bounds__(NT, SA_FOLD_MINB) k_tile_fold(
     const uint32_t *__restrict__ sstart, const int2 *__restrict__ tile_info,
@@ -1075,14 +1089,13 @@ __global__ void __launch_bounds__(NT, SA_FOLD_MINB) k_tile_fold(
     ErrState *err, int hash_fold, int4 *__restrict__ stage, int2 *__restrict__ tile_cnt) {
     pdl_wait();
     pdl_trigger();
-    if (err->long_cols)
-        tile_fold_body<STAGED, true>(sstart, tile_info, tile_big, ntiles, entries, SG, rec, big_list,
-                                     bigk, tile_state, N, jc, ir, pr, cap, err, hash_fold, stage,
-                                     tile_cnt);
-    else
+    if (!err->long_cols)  // (the short body first: the fall-through path)
         tile_fold_body<STAGED, false>(sstart, tile_info, tile_big, ntiles, entries, SG, rec, big_list,
                                       bigk, tile_state, N, jc, ir, pr, cap, err, hash_fold, stage,
                                       tile_cnt);
+    else
+        tile_fold_long<STAGED>(sstart, tile_info, tile_big, ntiles, entries, SG, rec, big_list, bigk,
+                               tile_state, N, jc, ir, pr, cap, err, hash_fold, stage, tile_cnt);
 }
 
 // ---- staged outputs (long-column inputs): no look-back in k_tile_fold ------
