@@ -5,24 +5,30 @@
 // (| BIGFLAG for a big column, which occupies one placeholder slot);
 // tile_info[t] = {first column of tile t, its start}.  Output: jc, ir, pr.
 //
-// One CTA (128 threads) per tile of TILE = 2048 record positions:
+// One CTA (128 threads) per tile of TILE = 1792 record positions (plus the
+// last column's overhang, TCAP):
 //   1. one TMA bulk copy (cp.async.bulk) brings the tile's entries into
 //      shared memory (keys K[k] = {row, position}); the values are gathered
 //      by position with cp.async (8 bytes each, no register staging) into
 //      V[k] while the short columns are already being sorted;
 //   2. every thread owns a contiguous range of the tile's columns; a short
-//      column (<= 24 triplets) is sorted by (row, position) with a register
-//      sorting network (sa_network.cuh), a longer one by a warp-wide bitonic
-//      sort of packed 64-bit keys (row, position, slot);
+//      column (<= SHORT_COL triplets) is sorted by (row, position) with a
+//      register sorting network (sa_network.cuh); longer ones go to a warp
+//      each: a hash-group fold (rows grouped in a per-warp hash table,
+//      members ranked by position in grouped order) when they have <= 64
+//      distinct rows, else a sub-warp bitonic sort of packed 64-bit keys;
 //   3. each run of equal rows is folded from +0.0 in ascending input
 //      position -- the reference's scatter order (_kernels.pyx:82-89, x86 NaN
 //      rule in fold_add) -- so pr is bit-exact;
 //   4. a block scan of the per-thread unique counts gives the tile count U,
-//      published for the decoupled look-back before the values are folded;
+//      published for the decoupled look-back before the values are folded
+//      (or, for long-column inputs, staged outputs chained by k_tile_emit);
 //   5. an output map (tile-local CSC index -> slot) lets all threads write
 //      jc / ir / pr with coalesced stores.
-// Tiles holding a big column (folded by k_bigcol) copy its results from the
-// big space.
+// The kernel dispatches on the column scan's flag: inputs without long small
+// columns run a body compiled without step 2's warp paths (inline, the
+// fall-through code); the long-column body is out of line.  Tiles holding a
+// big column (folded by k_bigcol) copy its results from the big space.
 
 #include <cstdlib>
 
