@@ -51,7 +51,8 @@ def _peaks():
 
 class ClockSampler:
     """Clock / throttle-reason sampling during the timed region: NVML
-    (pynvml, ~1 ms per query, every 2 ms) when importable, else nvidia-smi."""
+    (pynvml: SM clock + throttle reasons, ~1.4 ms per sample, back to back)
+    when importable, else nvidia-smi."""
 
     NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
 
@@ -71,15 +72,16 @@ class ClockSampler:
                           pynvml.nvmlClocksEventReasonHwThermalSlowdown,
                           pynvml.nvmlClocksEventReasonSwThermalSlowdown,
                           pynvml.nvmlClocksEventReasonSwPowerCap)
+            # the max clock does not change: queried once (an NVML query is ~0.7 ms)
+            self._max = float(pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM))
         except Exception:
             self._nvml = None
 
     def _sample_nvml(self):
         nv = self._nvml
         sm = nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM)
-        mx = nv.nvmlDeviceGetMaxClockInfo(self._h, nv.NVML_CLOCK_SM)
         r = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
-        self.samples.append((float(sm), float(mx), [n for n, bit in zip(self.NAMES, self._bits) if r & bit]))
+        self.samples.append((float(sm), self._max, [n for n, bit in zip(self.NAMES, self._bits) if r & bit]))
 
     def _sample_smi(self):
         fields = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
@@ -101,7 +103,7 @@ class ClockSampler:
                     self._sample_smi()
             except Exception:
                 pass
-            self._stop.wait(0.002 if self._nvml is not None else 0.1)
+            self._stop.wait(0.0002 if self._nvml is not None else 0.1)  # NVML: back to back
 
     def __enter__(self):
         self._t.start()
