@@ -804,14 +804,14 @@ __device__ __forceinline__ void tile_fold_body(const uint32_t *__restrict__ ssta
             for (int o = 16; o > 0; o >>= 1) wmax = max(wmax, __shfl_xor_sync(FULL, wmax, o));
             if (wmax == 0) continue;
             int u = 0;
-            if (wmax <= 8) {
+            if (wmax > 16 && wmax <= 18) {  // 2D FEM columns first (the fall-through code)
+                if (cnt) u = fold_short_net<18>(&K[off], cnt, &S.perm[off]);
+            } else if (wmax <= 8) {
                 if (cnt) u = fold_short_net<8>(&K[off], cnt, &S.perm[off]);
             } else if (wmax <= 12) {
                 if (cnt) u = fold_short_net<12>(&K[off], cnt, &S.perm[off]);
             } else if (wmax <= 16) {
                 if (cnt) u = fold_short_net<16>(&K[off], cnt, &S.perm[off]);
-            } else if (wmax <= 18) {
-                if (cnt) u = fold_short_net<18>(&K[off], cnt, &S.perm[off]);
             } else {
                 if (cnt) u = fold_short_net<24>(&K[off], cnt, &S.perm[off]);
             }
