@@ -10,7 +10,7 @@
 // from lower ranks before and from higher ranks after its own chunk, which
 // keeps the global input order, so the per-rank assemblies stay
 // bit-identical to one GPU.  The chunk's indices are validated on the way
-// (first bad row / column position, maxima).
+// (first bad row / column position, indices beyond the global dimensions).
 //
 // Three launches (values are read only for the triplets that leave):
 //   k_part_count    per tile (2048 triplets, 8 consecutive per thread) and
@@ -50,7 +50,6 @@ __device__ __forceinline__ int dest_of(const Bounds &B, int j) {
         if (r < B.world && c >= B.b[r]) d = r;
     return d;
 }
-
 
 // Element k of thread tid of a tile is the tile's (tid * PT_IPT + k)-th
 // triplet (thread-contiguous: two 16-byte loads per index array); the stable
