@@ -1116,6 +1116,8 @@ __global__ void __launch_bounds__(NT, SA_FOLD_MINB) k_tile_fold(
 
 constexpr int EMIT_NT = 256;
 
+constexpr int EMIT_TILES = 8;  // tiles per k_tile_emit CTA
+
 __global__ void __launch_bounds__(EMIT_NT) k_tile_emit(
     const uint32_t *__restrict__ sstart, const int2 *__restrict__ tile_info,
     const uint8_t *__restrict__ tile_big, int64_t ntiles, const int2 *__restrict__ tile_cnt,
@@ -1125,71 +1127,90 @@ __global__ void __launch_bounds__(EMIT_NT) k_tile_emit(
     int32_t *__restrict__ ir, double *__restrict__ pr, int64_t cap, ErrState *err) {
     __shared__ int2 s_big[TCAP];  // (tile-local output base, big-list index)
     __shared__ int s_nbig;
+    __shared__ long long s_P[EMIT_TILES];
     pdl_wait();
     pdl_trigger();
-    const int tid = threadIdx.x;
-    const long long b = blockIdx.x;
-    const int2 ti0 = tile_info[b], ti1 = tile_info[b + 1];
-    const int c_a = ti0.x, r0 = ti0.y, ncols = ti1.x - c_a;
-    __shared__ long long s_P;
-    const int2 uc = tile_cnt[b];
-    if (tid < 32) {  // every tile's count is already published: no waiting on slow tiles
-        const long long p = lookback_warp32(tile_state, b, (unsigned long long)uc.x);
-        if (tid == 0) s_P = p;
+    const int tid = threadIdx.x, lane = tid & 31;
+    const long long b0 = (long long)blockIdx.x * EMIT_TILES;
+    const int nt = (int)min((long long)EMIT_TILES, ntiles - b0);
+    if (tid < 32) {  // every count is published already: one look-back for the first tile,
+                     // the others by a prefix over their counts (and published as inclusive)
+        const int cv = lane < nt ? tile_cnt[b0 + lane].x : 0;
+        int incl = cv;
+#pragma unroll
+        for (int o = 1; o < EMIT_TILES; o <<= 1) {
+            const int y = __shfl_up_sync(FULL, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const long long p0 = lookback_warp32(tile_state, b0, (unsigned long long)__shfl_sync(FULL, cv, 0));
+        const long long P = p0 + incl - cv;
+        if (lane < nt) {
+            s_P[lane] = P;
+            if (lane > 0)
+                reinterpret_cast<volatile unsigned long long *>(tile_state)[(b0 + lane) * LB_STRIDE] =
+                    lb_pack(2, (unsigned long long)(P + cv));
+        }
     }
     __syncthreads();
-    const long long P = s_P;
     bool over = false;
-    for (int k = tid; k < uc.y; k += EMIT_NT) {
-        const int4 r = stage[r0 + k];
-        const long long x = P + r.w;
-        if (x < cap) {
-            ir[x] = r.x;
-            pr[x] = __hiloint2double(r.z, r.y);
-        } else {
-            over = true;
+    for (int t = 0; t < nt; ++t) {
+        const long long b = b0 + t;
+        const int2 ti0 = tile_info[b], ti1 = tile_info[b + 1];
+        const int c_a = ti0.x, r0 = ti0.y, ncols = ti1.x - c_a;
+        const long long P = s_P[t];
+        const int2 uc = tile_cnt[b];
+        for (int k = tid; k < uc.y; k += EMIT_NT) {
+            const int4 r = stage[r0 + k];
+            const long long x = P + r.w;
+            if (x < cap) {
+                ir[x] = r.x;
+                pr[x] = __hiloint2double(r.z, r.y);
+            } else {
+                over = true;
+            }
         }
-    }
-    const bool has_big = tile_big[b] != 0;
-    if (has_big) {
-        if (tid == 0) s_nbig = 0;
-        __syncthreads();
-    }
-    for (int c = tid; c < ncols; c += EMIT_NT) {
-        const int o = jc[c_a + c];
-        if (has_big && (sstart[c_a + c] & BIGFLAG)) {
-            const int e = atomicAdd(&s_nbig, 1);
-            if (e < TCAP) s_big[e] = make_int2(o, (int)bigk[c_a + c]);
-            else atomicExch(&err->internal, 1u);
+        const bool has_big = tile_big[b] != 0;
+        if (has_big) {
+            if (tid == 0) s_nbig = 0;
+            __syncthreads();
         }
-        jc[c_a + c] = (int32_t)(P + o);
-    }
-    if (has_big) {
-        __syncthreads();
-        const int nb = min(s_nbig, TCAP);
-        for (int e = 0; e < nb; ++e) {
-            const long long o = P + s_big[e].x;
-            const BigCol bc = big_list[s_big[e].y];
-            const int ub = (int)(bc.u & POSMASK);
-            const unsigned long long *RR = reinterpret_cast<const unsigned long long *>(rec + bc.start);
-            const unsigned long long *BK = (bc.u & BIGFLAG) ? RR + bc.n : RR;
-            const unsigned long long *BV = (bc.u & BIGFLAG) ? RR : RR + bc.n;
-            for (int q = tid; q < ub; q += EMIT_NT) {
-                if (o + q < cap) {
-                    ir[o + q] = (int32_t)BK[q];
-                    pr[o + q] = __longlong_as_double((long long)BV[q]);
-                } else {
-                    over = true;
+        for (int c = tid; c < ncols; c += EMIT_NT) {
+            const int o = jc[c_a + c];
+            if (has_big && (sstart[c_a + c] & BIGFLAG)) {
+                const int e = atomicAdd(&s_nbig, 1);
+                if (e < TCAP) s_big[e] = make_int2(o, (int)bigk[c_a + c]);
+                else atomicExch(&err->internal, 1u);
+            }
+            jc[c_a + c] = (int32_t)(P + o);
+        }
+        if (has_big) {
+            __syncthreads();
+            const int nb = min(s_nbig, TCAP);
+            for (int e = 0; e < nb; ++e) {
+                const long long o = P + s_big[e].x;
+                const BigCol bc = big_list[s_big[e].y];
+                const int ub = (int)(bc.u & POSMASK);
+                const unsigned long long *RR = reinterpret_cast<const unsigned long long *>(rec + bc.start);
+                const unsigned long long *BK = (bc.u & BIGFLAG) ? RR + bc.n : RR;
+                const unsigned long long *BV = (bc.u & BIGFLAG) ? RR : RR + bc.n;
+                for (int q = tid; q < ub; q += EMIT_NT) {
+                    if (o + q < cap) {
+                        ir[o + q] = (int32_t)BK[q];
+                        pr[o + q] = __longlong_as_double((long long)BV[q]);
+                    } else {
+                        over = true;
+                    }
                 }
             }
+            __syncthreads();  // s_big / s_nbig are reused by the next tile
+        }
+        if (b == ntiles - 1 && tid == 0) {
+            jc[N] = (int32_t)(P + uc.x);
+            err->nnz = P + uc.x;
+            if (P + uc.x > cap) atomicExch(&err->cap_exceeded, 1u);
         }
     }
     if (over) atomicExch(&err->cap_exceeded, 1u);
-    if (b == ntiles - 1 && tid == 0) {
-        jc[N] = (int32_t)(P + uc.x);
-        err->nnz = P + uc.x;
-        if (P + uc.x > cap) atomicExch(&err->cap_exceeded, 1u);
-    }
 }
 
 cudaError_t launch_tile_fold(Launch &lc, const uint32_t *sstart, const int2 *tile_info,
@@ -1221,7 +1242,8 @@ cudaError_t launch_tile_fold(Launch &lc, const uint32_t *sstart, const int2 *til
                                        ir, pr, cap, err, hash_fold, stage, tile_cnt);
     lc.launches++;
     if (e != cudaSuccess || !stage) return e;
-    e = launch_pdl(k_tile_emit, dim3((unsigned)ntiles), dim3(EMIT_NT), 0, lc.stream, sstart, tile_info,
+    e = launch_pdl(k_tile_emit, dim3((unsigned)((ntiles + EMIT_TILES - 1) / EMIT_TILES)), dim3(EMIT_NT), 0,
+                   lc.stream, sstart, tile_info,
                    tile_big, ntiles, (const int2 *)tile_cnt, tile_state, (const int4 *)stage, rec,
                    big_list, bigk, N, jc, ir, pr, cap, err);
     lc.launches++;
