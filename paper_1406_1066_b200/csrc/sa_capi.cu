@@ -393,7 +393,12 @@ int assemble_segments(sa_ctx *ctx, const Segs &S, int64_t L, int32_t M, int32_t 
     }
 
     const int64_t nbig_max = L / (BIGCOL + 1) + 1;
-    const int64_t ntiles = (L + nbig_max + TILE - 1) / TILE;
+    // fold tile size: TILE, or smaller so that a small input still gives every
+    // SM two tiles (cfg1: 56 tiles of 1792 slots would leave 92 SMs idle)
+    int tile_sz = TILE;
+    if ((L + nbig_max + TILE - 1) / TILE < 2 * (int64_t)ctx->num_sms)
+        tile_sz = (int)std::max<int64_t>(256, (L + nbig_max + 2 * ctx->num_sms - 1) / (2 * ctx->num_sms));
+    const int64_t ntiles = (L + nbig_max + tile_sz - 1) / tile_sz;
     const int64_t nscan = (N + SCAN_TILE - 1) / SCAN_TILE;
     SA_CUDA(ctx, ensure(ctx->cur, ctx->cur_cap, (size_t)N + 4));
     SA_CUDA(ctx, ensure(ctx->sstart, ctx->st_cap, (size_t)N + 1));
@@ -416,7 +421,7 @@ int assemble_segments(sa_ctx *ctx, const Segs &S, int64_t L, int32_t M, int32_t 
     if ((rc = mark(ctx, "k_col_scan"))) return rc;
     SA_CUDA(ctx, launch_col_scan(lc, ctx->cur, ctx->sstart, ctx->cur, N, ctx->tile_info,
                                  ctx->tile_big, ntiles, ctx->big_list, ctx->bigk, ctx->scan_state,
-                                 ctx->perm, ctx->err));
+                                 ctx->perm, ctx->err, tile_sz));
     if ((rc = mark(ctx, "k_scatter"))) return rc;
     SA_CUDA(ctx, launch_scatter(lc, S, M, N, ctx->cur, ctx->perm, ctx->err));
     if (L > BIGCOL) {

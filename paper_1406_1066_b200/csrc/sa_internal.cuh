@@ -336,7 +336,8 @@ cudaError_t launch_hist(Launch &lc, const int32_t *ii, const int32_t *jj, int64_
 cudaError_t launch_col_scan(Launch &lc, const uint32_t *cnt, uint32_t *sstart, uint32_t *cur,
                             int32_t N, int2 *tile_info, uint8_t *tile_big,
                             int64_t ntiles, BigCol *big_list, uint32_t *bigk,
-                            unsigned long long *scan_state, uint2 *perm, ErrState *err);
+                            unsigned long long *scan_state, uint2 *perm, ErrState *err,
+                            int tile_sz);
 cudaError_t launch_colcount(Launch &lc, const Segs &S, int32_t N, uint32_t *cnt, ErrState *err);
 cudaError_t launch_scatter(Launch &lc, const Segs &S, int32_t M, int32_t N, uint32_t *cur,
                            uint2 *perm, ErrState *err);

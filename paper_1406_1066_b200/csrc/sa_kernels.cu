@@ -196,7 +196,8 @@ cudaError_t launch_hist(Launch &lc, const int32_t *ii, const int32_t *jj, int64_
 //   sstart[c]     small-space start of column c (| BIGFLAG if big; a big
 //                 column sits at the start of the next small column)
 //   cur[c]        scatter cursor (small start, or big-space start | BIGFLAG)
-//   tile_info[t]  {min{c : sstart(c) >= t*TILE}, its sstart}, 0 <= t <= ntiles
+//   tile_info[t]  {min{c : sstart(c) >= t*tile}, its sstart}, 0 <= t <= ntiles
+//                 (tile = the call's tile size, TILE or smaller for small inputs)
 //                 (the fold tile t owns the columns starting in its range)
 //   tile_big[b]   tile b owns a big column
 //   big_list[]    big columns {col, big-space start, n}; bigk[c] = list index
@@ -228,6 +229,13 @@ __device__ __forceinline__ unsigned long long scan_word(uint32_t n) {
 // Each thread owns SCAN_IPT = 8 consecutive columns: 16-byte loads of the
 // counts, 16-byte stores of sstart / cur, so the kernel streams at HBM speed;
 // small CTAs keep many of them resident per SM for memory parallelism.
+// Tile index of small-space offset x for the runtime tile size d: the high
+// half of x * ceil(2^64 / d), exact for x < 2^32 (the error x * (m/2^64 -
+// 1/d) < 2^-32 stays below the distance 1/d to the next integer).
+__device__ __forceinline__ int64_t tile_of(uint64_t x, uint64_t tmagic) {
+    return (int64_t)__umul64hi(x, tmagic);
+}
+
 __global__ void __launch_bounds__(SCAN_NT) k_col_scan(const uint32_t *cnt,
                                                       uint32_t *__restrict__ sstart,
                                                       uint32_t *cur, int32_t N,
@@ -237,7 +245,7 @@ __global__ void __launch_bounds__(SCAN_NT) k_col_scan(const uint32_t *cnt,
                                                       uint32_t *__restrict__ bigk,
                                                       unsigned long long *scan_state,
                                                       uint2 *__restrict__ perm,
-                                                      ErrState *err) {
+                                                      ErrState *err, uint64_t tmagic) {
     __shared__ unsigned long long s_warp[SCAN_NT / 32];
     __shared__ long long s_b;
     __shared__ unsigned long long s_excl;
@@ -295,22 +303,22 @@ __global__ void __launch_bounds__(SCAN_NT) k_col_scan(const uint32_t *cnt,
                 big_list[slot] = BigCol{(uint32_t)c, (uint32_t)bigp, n, 0u};
                 bigk[c] = slot;
                 perm[small] = make_uint2(0u, 0xffffffffu);  // placeholder slot: nothing to gather
-                int64_t tb = (int64_t)(small / TILE);
+                int64_t tb = tile_of(small, tmagic);
                 if (tb > ntiles - 1) tb = ntiles - 1;
                 tile_big[tb] = 1;
             }
-            // fold tiles t with small < t*TILE <= small + extent start at column c+1
+            // fold tiles t with small < t*tile <= small + extent start at column c+1
             const uint32_t ext = big ? 1u : n;
             if (ext) {
-                int64_t t = (int64_t)(small / TILE) + 1;
-                const int64_t last = min((int64_t)((small + ext) / TILE), ntiles - 1);
+                int64_t t = tile_of(small, tmagic) + 1;
+                const int64_t last = min(tile_of(small + ext, tmagic), ntiles - 1);
                 for (; t <= last; ++t) tile_info[t] = make_int2((int)(c + 1), (int)(small + ext));
             }
             if (c == N - 1) {
                 const uint64_t tot_small = small + ext;
                 err->lsmall = (unsigned)tot_small;
                 sstart[N] = (uint32_t)tot_small;
-                s_tail = (long long)(tot_small / TILE) + 1;
+                s_tail = (long long)tile_of(tot_small, tmagic) + 1;
                 s_tot = (int)tot_small;
             }
         }
@@ -351,11 +359,14 @@ __global__ void __launch_bounds__(SCAN_NT) k_col_scan(const uint32_t *cnt,
 cudaError_t launch_col_scan(Launch &lc, const uint32_t *cnt, uint32_t *sstart, uint32_t *cur,
                             int32_t N, int2 *tile_info, uint8_t *tile_big,
                             int64_t ntiles, BigCol *big_list, uint32_t *bigk,
-                            unsigned long long *scan_state, uint2 *perm, ErrState *err) {
+                            unsigned long long *scan_state, uint2 *perm, ErrState *err,
+                            int tile_sz) {
     if (N <= 0) return cudaSuccess;
+    const uint64_t tmagic = ~0ull / (uint64_t)tile_sz + 1;  // ceil(2^64 / tile_sz)
     int grid = (int)((N + SCAN_TILE - 1) / SCAN_TILE);
     cudaError_t e = launch_pdl(k_col_scan, dim3(grid), dim3(SCAN_NT), 0, lc.stream, cnt, sstart, cur, N,
-                               tile_info, tile_big, ntiles, big_list, bigk, scan_state, perm, err);
+                               tile_info, tile_big, ntiles, big_list, bigk, scan_state, perm, err,
+                               tmagic);
     if (e != cudaSuccess) return e;
     lc.launches++;
     return cudaGetLastError();
