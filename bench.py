@@ -3,9 +3,11 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl reference]
 
 A step is one full assembly S = sparse(i, j, s, m, n) of the workload
-(default: BASELINE configs[1], the 2D P1 FEM stiffness with N=1000 cells per
-side, L = 18e6 triplets).  Inputs (288 MB) and the workspace exceed the
-126 MB L2, so consecutive steps stream from HBM (no explicit flush).
+(default: BASELINE configs[3], the heavy-duplicate random input, m = n = 1e7,
+1e8 positions x Poisson(5) repeats, L ~ 5e8 triplets: the largest config
+that fits one GPU; --config 1..5 picks another).  Inputs (8 GB) and the
+workspace exceed the 126 MB L2, so consecutive steps stream from HBM (no
+explicit flush; inputs that fit in L2 are timed step by step after a flush).
 
 Prints ONE JSON line (rank 0):
   value        whole-job triplets/s, device-resident inputs, CUDA events on
@@ -17,9 +19,12 @@ Prints ONE JSON line (rank 0):
                duration vs MEASURED_PEAKS.json hbm_gbs
   path_roofline  compulsory bytes of the whole assembly (16 L + 12 nnz +
                4 (N+1)) / step time
-  cpu_baseline the reference's own compiled kernels (oracle/_ref, threaded
-               driver) on this host, same workload
---impl reference runs only that CPU implementation and prints its line.
+  cpu_baseline the UNMODIFIED reference package (oracle/_ref: stock
+               sparseasm.assemble_parallel over its compiled kernels, all
+               host threads) on a bounded sample of the same workload (the
+               first Ls triplets, ~1 s per run)
+--impl reference runs only that CPU implementation (one sample per step) and
+prints its line, with the same `config` as this arm.
 """
 
 from __future__ import annotations
@@ -37,6 +42,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "input triplets/sec assembled to CSC"
+L2_BYTES = 126 << 20
 UNIT = "triplets/s"
 
 
@@ -130,24 +136,37 @@ def _dist():
     return world, rank, local
 
 
-def cpu_reference_run(ii, jj, s, m, n, budget_s=12.0, max_reps=20, threads=None):
-    """Time the reference's CPU implementation: its own compiled kernels
-    (oracle/_ref) under the restated threaded driver (parallel.py:267-358)
-    with all host threads; falls back to the C restatement (1 core)."""
-    from oracle import oracle as O
-    from oracle import ref_driver
+REF_STEP_S = 1.0  # target duration of one timed reference step (bounded sample)
 
-    p = threads or len(os.sched_getaffinity(0))
-    if ref_driver.available():
-        kind = "reference"
-        run = (lambda: ref_driver.assemble_parallel(ii, jj, s, m, n, p)) if p > 1 else \
-            (lambda: ref_driver.assemble_serial(ii, jj, s, m, n))
-        cores = p
-    else:
-        kind = "port"
-        run = lambda: O.assemble_counting(ii, jj, s, m, n)  # noqa: E731
-        cores = 1
-    out = run()  # warm-up (untimed), also the parity reference
+
+def reference_sample(ii, jj, s, m, n, target_s=REF_STEP_S):
+    """Size a bounded sample of the workload for the reference's CPU path:
+    the first Ls triplets (same m, n) such that one stock
+    ``assemble_parallel`` on all host threads takes about ``target_s``.
+    Returns (Ls, req, run) with the reference's request built once, outside
+    any timing (its run_bench protocol, bench.py:146-160)."""
+    from oracle import stock
+
+    p = stock.host_threads()
+    L = len(ii)
+    Ls = min(L, 1 << 22)
+    req = stock.request(ii[:Ls], jj[:Ls], s[:Ls], m, n)
+    t0 = time.perf_counter()
+    stock.parallel(req, p)  # untimed probe run (also a warm-up)
+    dt = max(time.perf_counter() - t0, 1e-6)
+    want = int(min(L, max(Ls, Ls * target_s / dt)))
+    if want > Ls * 1.2 or (want == L and Ls != L):
+        Ls = want
+        req = stock.request(ii[:Ls], jj[:Ls], s[:Ls], m, n)
+    return Ls, req, (lambda: stock.parallel(req, p)), p
+
+
+def cpu_reference_run(ii, jj, s, m, n, budget_s=15.0, max_reps=20):
+    """cpu_baseline: the UNMODIFIED reference package (oracle/_ref: its
+    threaded driver over its compiled kernels, parallel.py:361-389) with all
+    host threads, on a bounded sample of the workload."""
+    Ls, req, run, p = reference_sample(ii, jj, s, m, n)
+    out = run()  # warm-up (untimed), also the parity reference for the sample
     times = []
     t_start = time.perf_counter()
     while len(times) < max_reps and (time.perf_counter() - t_start) < budget_s:
@@ -155,7 +174,17 @@ def cpu_reference_run(ii, jj, s, m, n, budget_s=12.0, max_reps=20, threads=None)
         run()
         times.append(time.perf_counter() - t0)
     mean = sum(times) / len(times)
-    return dict(kind=kind, cores=cores, mean_s=mean, min_s=min(times), reps=len(times)), out
+    return dict(kind="reference", cores=p, mean_s=mean, min_s=min(times), reps=len(times), Ls=Ls), out
+
+
+def bench_config(w, world: int, shard: bool) -> dict:
+    """The workload description both arms print (identical keys)."""
+    small = 16 * w.L < L2_BYTES
+    return {"workload": w.name, "L": w.L, "m": w.m, "n": w.n,
+            "l2": ("inputs fit in the 126 MB L2: each step timed alone after a 256 MB flush"
+                   if small else
+                   "inputs (16 B x L) and workspace exceed the 126 MB L2; no explicit flush"),
+            "parallelism": f"dp{world}" if shard else "single"}
 
 
 def build_workload(cfg: int, device, rank: int, world: int):
@@ -183,7 +212,9 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", type=int, default=2)
+    # default: configs[3], the largest single-GPU BASELINE config (heavy-duplicate
+    # random, L ~ 5e8); configs[4] is the 8-GPU sharded one
+    ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -200,34 +231,32 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        w = build_workload(args.config, "cpu", 0, 1)
-        ii, jj, s = w.ii.numpy(), w.jj.numpy(), w.s.numpy()
-        from oracle import oracle as O
-        from oracle import ref_driver
-
-        p = len(os.sched_getaffinity(0))
-        if ref_driver.available():
-            info = {"kind": "reference", "cores": p}
-            run = lambda: ref_driver.assemble_parallel(ii, jj, s, w.m, w.n, p)  # noqa: E731
-        else:
-            info = {"kind": "port", "cores": 1}
-            run = lambda: O.assemble_counting(ii, jj, s, w.m, w.n)  # noqa: E731
+        # the same bits as the GPU arm's workload (generated on the GPU when
+        # there is one; input generation is not part of either timed path)
+        gen_dev = torch.device("cuda", local) if torch.cuda.is_available() else "cpu"
+        w = build_workload(args.config, gen_dev, 0, 1)
+        ii, jj, s = w.ii.cpu().numpy(), w.jj.cpu().numpy(), w.s.cpu().numpy()
+        cfg_line, wL = bench_config(w, args.gpus, args.gpus > 1), w.L
+        del w.ii, w.jj, w.s  # device copies
+        Ls, req, run, p = reference_sample(ii, jj, s, w.m, w.n)
         for _ in range(args.warmup):
-            out = run()
+            run()
         times = []
         for _ in range(args.steps):
             t0 = time.perf_counter()
             run()
             times.append(time.perf_counter() - t0)
         mean = sum(times) / len(times)
-        val = w.L / mean
+        val = Ls / mean
+        sample = (f"first {Ls} of the workload's {wL} triplets (same m, n) per step, "
+                  f"stock sparseasm.assemble_parallel(req, p={p}) from oracle/_ref")
         line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": mean * 1e3,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic",
-                "config": {"workload": w.name, "L": w.L, "m": w.m, "n": w.n, "nnz": out.nnz},
-                "cpu_baseline": {"value": val, "unit": UNIT, "cores": info["cores"], "kind": info["kind"],
-                                 "sample": f"full workload, {args.steps} timed runs"},
+                "config": cfg_line,
+                "cpu_baseline": {"value": val, "unit": UNIT, "cores": p, "kind": "reference",
+                                 "sample": sample},
                 "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
         return
@@ -314,7 +343,6 @@ def main():
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     # inputs that fit in the 126 MB L2 (cfg1): every step timed on its own,
     # the L2 flushed between steps (a 256 MB write outside the timed events)
-    L2_BYTES = 126 << 20
     small = 16 * L < L2_BYTES
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev) if small else None
     with ClockSampler(local) as clk:
@@ -447,10 +475,14 @@ def main():
     parity = None
     if rank == 0 and not shard and not args.no_cpu_baseline:
         info, ref = cpu_reference_run(hin, hjn, hsn, M, N)
-        parity = bool(out.same_as(ref))
-        cpu = {"value": L / info["mean_s"], "unit": UNIT, "cores": info["cores"], "kind": info["kind"],
-               "sample": f"full workload ({L} triplets), {info['reps']} timed runs after 1 warm-up, "
-                         f"mean {info['mean_s'] * 1e3:.1f} ms"}
+        Ls = info["Ls"]
+        # parity on the sample: the public API on the same Ls triplets
+        mine = out if Ls == L else sa.assemble(hin[:Ls], hjn[:Ls], hsn[:Ls], m=M, n=N, device=local)
+        parity = bool(mine.same_as(ref))
+        cpu = {"value": Ls / info["mean_s"], "unit": UNIT, "cores": info["cores"], "kind": info["kind"],
+               "sample": f"first {Ls} of {L} triplets (same m, n), stock sparseasm.assemble_parallel "
+                         f"(oracle/_ref) on {info['cores']} threads, {info['reps']} timed runs after "
+                         f"1 warm-up, mean {info['mean_s'] * 1e3:.1f} ms"}
 
     if rank != 0:
         if shard:
@@ -461,11 +493,8 @@ def main():
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": w.name, "L": L, "m": M, "n": N, "nnz": nnz,
-                   "l2": ("inputs fit in the 126 MB L2: each step timed alone after a 256 MB flush"
-                          if small else
-                          "inputs (16 B x L) and workspace exceed the 126 MB L2; no explicit flush"),
-                   "parallelism": f"dp{world}" if shard else "single"},
+        "config": bench_config(w, world, shard),
+        "nnz": nnz,
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": dom_gbs, "peak": peak_gbs,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": dom_gbs / peak_gbs,
                      "traffic": traffic, "alg_bytes_per_launch": alg.get(dom),

@@ -67,6 +67,14 @@ enum { SA_DTYPE_INT32 = 0, SA_DTYPE_INT64 = 1, SA_DTYPE_FLOAT64 = 2 };
 /* which array a SA_ERR_BAD_INDEX refers to */
 enum { SA_WHICH_ROW = 0, SA_WHICH_COL = 1 };
 
+/* context options (sa_set_option); value -1 = automatic (the default), 0 or 1
+ * forces a pipeline variant.  They select between code paths that produce the
+ * SAME bits (tests force each variant); none changes a result. */
+enum {
+    SA_OPT_FOLD_STAGED = 0,     /* fold outputs staged + k_tile_emit pass       */
+    SA_OPT_SCATTER_STAGED = 1   /* column scatter through shared-memory staging */
+};
+
 /* ABI version (bumped on any signature change). */
 int sa_version(void);
 
@@ -77,6 +85,9 @@ void sa_destroy(sa_ctx *ctx);
 /* Run subsequent work on `stream` (a cudaStream_t; 0/NULL = the legacy
  * default stream).  A new context starts on its own non-blocking stream. */
 int sa_set_stream(sa_ctx *ctx, void *stream);
+/* Set a context option (SA_OPT_*) to -1 (automatic), 0 or 1.  Replaces no
+ * reference interface: the reference has one code path per backend. */
+int sa_set_option(sa_ctx *ctx, int option, int value);
 /* Message describing the last failure on this context ("" if none). */
 const char *sa_last_error(const sa_ctx *ctx);
 

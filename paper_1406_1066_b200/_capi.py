@@ -28,6 +28,9 @@ SA_DTYPE_FLOAT64 = 2
 SA_WHICH_ROW = 0
 SA_WHICH_COL = 1
 
+SA_OPT_FOLD_STAGED = 0
+SA_OPT_SCATTER_STAGED = 1
+
 # every symbol include/sparse_assembly.h declares, with (restype, argtypes)
 _vp = ctypes.c_void_p
 _i32 = ctypes.c_int32
@@ -42,6 +45,7 @@ SIGNATURES = {
     "sa_create": (_int, [_int, ctypes.POINTER(_vp)]),
     "sa_destroy": (None, [_vp]),
     "sa_set_stream": (_int, [_vp, _vp]),
+    "sa_set_option": (_int, [_vp, _int, _int]),
     "sa_last_error": (ctypes.c_char_p, [_vp]),
     "sa_convert_indices": (_int, [_vp, _vp, _int, _i64, _vp, _pi64, _pi32]),
     "sa_infer_dims": (_int, [_vp, _vp, _vp, _i64, _pi32, _pi32, _pi64, _pint]),

@@ -91,6 +91,13 @@ class Assembler:
         s = torch.cuda.current_stream(self.device)
         self.lib.sa_set_stream(self.ctx, ctypes.c_void_p(s.cuda_stream))
 
+    def set_option(self, option: int, value: int) -> None:
+        """Force a pipeline variant (_capi.SA_OPT_*: -1 automatic, 0, 1).
+        Every variant produces the same bits; tests use this to cover each."""
+        rc = self.lib.sa_set_option(self.ctx, int(option), int(value))
+        if rc:
+            raise ValueError(self._msg())
+
     def launch_count(self) -> int:
         return int(self.lib.sa_last_launch_count(self.ctx))
 

@@ -59,6 +59,10 @@ struct sa_ctx {
     cudaEvent_t ev[MAXEV + 1] = {};
     const char *ev_name[MAXEV] = {};
 
+    // options (sa_set_option); -1 = automatic
+    int opt_fold_staged = -1;
+    int opt_scatter_staged = -1;
+
     int64_t host_L = -1;
     int64_t host_stride = 1;
     int32_t host_N = 0;
@@ -316,6 +320,16 @@ void sa_destroy(sa_ctx *ctx) {
     delete ctx;
 }
 
+int sa_set_option(sa_ctx *ctx, int option, int value) {
+    if (!ctx) return SA_ERR_INVALID_ARG;
+    if (value < -1 || value > 1) return fail(ctx, SA_ERR_INVALID_ARG, "sa_set_option: value must be -1, 0 or 1");
+    switch (option) {
+        case SA_OPT_FOLD_STAGED: ctx->opt_fold_staged = value; return SA_OK;
+        case SA_OPT_SCATTER_STAGED: ctx->opt_scatter_staged = value; return SA_OK;
+        default: return fail(ctx, SA_ERR_INVALID_ARG, "sa_set_option: unknown option");
+    }
+}
+
 int sa_set_stream(sa_ctx *ctx, void *stream) {
     if (!ctx) return SA_ERR_INVALID_ARG;
     ctx->stream = reinterpret_cast<cudaStream_t>(stream);  // 0 = the legacy default stream
@@ -376,6 +390,8 @@ int assemble_segments(sa_ctx *ctx, const Segs &S, int64_t L, int32_t M, int32_t 
                       int32_t *d_ir, double *d_pr, int64_t cap) {
     SA_CUDA(ctx, cudaSetDevice(ctx->device));
     Launch lc{ctx->stream, ctx->num_sms, 0};
+    lc.fold_staged = ctx->opt_fold_staged;
+    lc.scatter_staged = ctx->opt_scatter_staged;
 
     if (L == 0 || N == 0) {
         // nothing to assemble (L > 0 with N == 0 means every column index is
@@ -433,8 +449,9 @@ int assemble_segments(sa_ctx *ctx, const Segs &S, int64_t L, int32_t M, int32_t 
                                    passes));
     }
     // long columns dominate: stage the outputs instead of chaining tile offsets
-    const char *env = getenv("SA_STAGED");
-    const bool staged = env ? atoi(env) != 0 : (L >= 40 * (int64_t)N && ntiles >= 16 * ctx->num_sms);
+    const bool staged = ctx->opt_fold_staged >= 0
+                            ? ctx->opt_fold_staged == 1
+                            : (L >= 40 * (int64_t)N && ntiles >= 16 * ctx->num_sms);
     if (staged) {
         SA_CUDA(ctx, ensure(ctx->tile_cnt, ctx->tc_cap, (size_t)ntiles));
     }

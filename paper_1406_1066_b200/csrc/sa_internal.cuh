@@ -304,7 +304,9 @@ __device__ __forceinline__ void smem_incl_max(int *arr, int n, int *s_warp) {
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
-bool pdl_enabled();  // SA_PDL=0 disables (A/B measurement)
+// cudaFuncAttributeMaxDynamicSharedMemorySize for `fn` on the CURRENT device
+// (the attribute is per device): set once per (kernel, device), thread-safe.
+cudaError_t ensure_smem_attr(const void *fn, int bytes);
 
 template <typename... KArgs, typename... Args>
 cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
@@ -316,7 +318,7 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
     cfg.stream = stream;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
@@ -327,6 +329,9 @@ struct Launch {
     cudaStream_t stream;
     int num_sms;
     int launches;  // incremented per kernel launch
+    // context options (sa_set_option): -1 = automatic choice
+    int fold_staged = -1;     // SA_OPT_FOLD_STAGED: staged fold outputs + k_tile_emit
+    int scatter_staged = -1;  // SA_OPT_SCATTER_STAGED: k_scatter_staged
 };
 
 cudaError_t launch_convert(Launch &lc, const void *raw, int dtype, int64_t L, int32_t *out,

@@ -28,6 +28,9 @@
 // ascending input order.
 
 #include <cstdlib>
+#include <mutex>
+#include <set>
+#include <utility>
 
 #include "sa_internal.cuh"
 
@@ -645,28 +648,25 @@ __global__ void __launch_bounds__(AGG_NT) k_colcount_win(Segs S, int32_t N,
     }
 }
 
-bool pdl_enabled() {
-    static int m = -1;
-    if (m < 0) {
-        const char *e = getenv("SA_PDL");
-        m = (e && e[0] == '0') ? 0 : 1;
-    }
-    return m == 1;
+cudaError_t ensure_smem_attr(const void *fn, int bytes) {
+    static std::mutex mu;
+    static std::set<std::pair<const void *, int>> done;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> g(mu);
+    if (done.count({fn, dev})) return cudaSuccess;
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess) done.insert({fn, dev});
+    return e;
 }
 
-static int colcount_ctas() {  // resident CTAs per SM (SA_COLCOUNT_CTAS for A/B)
-    static int v = -1;
-    if (v < 0) {
-        const char *e = getenv("SA_COLCOUNT_CTAS");
-        v = e ? std::max(1, atoi(e)) : 5;
-    }
-    return v;
-}
+constexpr int COLCOUNT_CTAS = 5;  // resident CTAs per SM of the column pass
 
 cudaError_t launch_colcount(Launch &lc, const Segs &S, int32_t N, uint32_t *cnt, ErrState *err) {
     const int64_t nchunk = S.ch0[S.nseg];
     if (nchunk <= 0) return cudaSuccess;
-    const int grid = (int)std::min<int64_t>(nchunk, (int64_t)lc.num_sms * colcount_ctas());
+    const int grid = (int)std::min<int64_t>(nchunk, (int64_t)lc.num_sms * COLCOUNT_CTAS);
     cudaError_t e = launch_pdl(k_colcount_win, dim3(grid), dim3(AGG_NT), 0, lc.stream, S, N, cnt, err);
     lc.launches++;
     return e;
@@ -938,15 +938,10 @@ __global__ void __launch_bounds__(SNT) k_scatter_staged(Segs S, int32_t M, int32
 // Staged writes pay off when the column cursors (4 N bytes) and the columns'
 // slot regions no longer stay in L2 between the chunks that fill them (cfg5,
 // N = 6.4e7: 14.3 -> 10.6 ms); with L2-resident cursors (cfg2 / cfg3) the
-// plain scatter is faster (110 vs 174 us on cfg2).  SA_SCATTER_STAGED=0/1
-// overrides.
-static bool scatter_staged(int32_t N) {
-    static int m = -2;
-    if (m == -2) {
-        const char *e = getenv("SA_SCATTER_STAGED");
-        m = (e && (e[0] == '0' || e[0] == '1')) ? e[0] - '0' : -1;
-    }
-    return m >= 0 ? m == 1 : N > (16 << 20);
+// plain scatter is faster (110 vs 174 us on cfg2).  The context option
+// SA_OPT_SCATTER_STAGED overrides the choice (tests force both variants).
+static bool scatter_staged(const Launch &lc, int32_t N) {
+    return lc.scatter_staged >= 0 ? lc.scatter_staged == 1 : N > (16 << 20);
 }
 
 cudaError_t launch_scatter(Launch &lc, const Segs &S, int32_t M, int32_t N, uint32_t *cur,
@@ -954,7 +949,7 @@ cudaError_t launch_scatter(Launch &lc, const Segs &S, int32_t M, int32_t N, uint
     const int64_t nchunk = S.ch0[S.nseg];
     if (nchunk <= 0) return cudaSuccess;
     cudaError_t e;
-    if (scatter_staged(N)) {
+    if (scatter_staged(lc, N)) {
         const int grid = (int)std::min<int64_t>(2 * nchunk, (int64_t)lc.num_sms * 7);
         e = launch_pdl(k_scatter_staged, dim3(grid), dim3(SNT), 0, lc.stream, S, M, N, cur, perm, err);
     } else {
@@ -1244,18 +1239,11 @@ __global__ void __launch_bounds__(BIG_NT, 2) k_bigcol(BigCol *__restrict__ big_l
 
 cudaError_t launch_bigcol(Launch &lc, BigCol *big_list, const ErrState *err, int4 *rec,
                           const uint2 *perm, const Segs &S, int idx_bits, int passes) {
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(k_bigcol, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)BIG_DSMEM);
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
-    static int gmul = getenv("SA_BIG_GRID") ? atoi(getenv("SA_BIG_GRID")) : 2;
-    static int med = getenv("SA_BIG_MED") ? atoi(getenv("SA_BIG_MED")) : 1;
-    int grid = gmul * lc.num_sms;
-    cudaError_t e = launch_pdl(k_bigcol, dim3(grid), dim3(BIG_NT), med ? BIG_DSMEM : 0, lc.stream,
-                               big_list, err, rec, perm, S, idx_bits, passes, med ? MED_CAP : 0);
+    cudaError_t e = ensure_smem_attr((const void *)k_bigcol, (int)BIG_DSMEM);
+    if (e != cudaSuccess) return e;
+    const int grid = 2 * lc.num_sms;
+    e = launch_pdl(k_bigcol, dim3(grid), dim3(BIG_NT), BIG_DSMEM, lc.stream, big_list, err, rec,
+                   perm, S, idx_bits, passes, MED_CAP);
     if (e != cudaSuccess) return e;
     lc.launches++;
     return cudaGetLastError();

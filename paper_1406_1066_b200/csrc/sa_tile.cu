@@ -1220,19 +1220,11 @@ cudaError_t launch_tile_fold(Launch &lc, const uint32_t *sstart, const int2 *til
                              int32_t *jc, int32_t *ir, double *pr, int64_t cap, ErrState *err,
                              int4 *stage, int2 *tile_cnt) {
     if (ntiles <= 0) return cudaSuccess;
-    static const int hash_fold = getenv("SA_HASH_FOLD") ? atoi(getenv("SA_HASH_FOLD")) : 1;
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(k_tile_fold<false>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)sizeof(TileSmem));
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(k_tile_fold<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)sizeof(TileSmem));
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
-    cudaError_t e = stage ? launch_pdl(k_tile_fold<true>, dim3((unsigned)ntiles), dim3(NT),
+    constexpr int hash_fold = 1;
+    cudaError_t e = ensure_smem_attr((const void *)k_tile_fold<false>, (int)sizeof(TileSmem));
+    if (e == cudaSuccess) e = ensure_smem_attr((const void *)k_tile_fold<true>, (int)sizeof(TileSmem));
+    if (e != cudaSuccess) return e;
+    e = stage ? launch_pdl(k_tile_fold<true>, dim3((unsigned)ntiles), dim3(NT),
                                        sizeof(TileSmem), lc.stream, sstart, tile_info, tile_big,
                                        ntiles, entries, SG, rec, big_list, bigk, tile_state, N, jc,
                                        ir, pr, cap, err, hash_fold, stage, tile_cnt)

@@ -134,14 +134,29 @@ class BenchResult:
     phase_means: dict = field(default_factory=dict)
 
 
+def _timed(impl: Impl, req, reps: int):
+    """One untimed warm-up, then ``reps`` timed calls: (mean, min, mean phases)."""
+    impl.run(req)
+    times, phases = [], {}
+    for _ in range(reps):
+        pt: dict[str, float] = {}
+        t0 = time.perf_counter()
+        impl.run(req, pt)
+        times.append(time.perf_counter() - t0)
+        for k, v in pt.items():
+            phases[k] = phases.get(k, 0.0) + v / reps
+    return sum(times) / reps, min(times), phases
+
+
 def run_bench(triplets, impls: list[Impl], reps: int = 40, dataset_id: str = "custom",
               dims=None) -> list[BenchResult]:
-    """The reference's ``run_bench`` protocol (bench.py:132-196) over given
-    triplets ``(ii, jj, s)``: every implementation's output is cross-checked
-    bit-exactly against the first one's (``ResultMismatch`` otherwise), then
-    each gets one untimed warm-up and ``reps`` timed runs (mean, min, mean
-    phase times); ``speedup_vs_serial`` is filled when an implementation
-    named ``serial*`` is present."""
+    """Cross-check, then time (the protocol of the reference's run_bench,
+    bench.py:132-196) over given triplets ``(ii, jj, s)``.  When the
+    reference package is importable, use its own ``bench.run_bench`` instead
+    (INTEGRATION.md); this is the self-contained version for the CLI.
+    Outputs must agree bit for bit with the first implementation's
+    (``ResultMismatch`` otherwise); ``speedup_vs_serial`` is relative to the
+    first implementation named ``serial*``."""
     from types import SimpleNamespace
 
     from .errors import ResultMismatch
@@ -149,48 +164,28 @@ def run_bench(triplets, impls: list[Impl], reps: int = 40, dataset_id: str = "cu
 
     if reps < 1:
         raise ValueError("reps must be >= 1")
-    ii, jj, s = triplets
-    ii = np.ascontiguousarray(ii, dtype=np.int32)
-    jj = np.ascontiguousarray(jj, dtype=np.int32)
-    s = np.ascontiguousarray(s, dtype=np.float64)
-    # a reference-shaped request (validated triplets + dims), which both this
-    # package's Impl and the reference's accept
+    ii, jj, s = (np.ascontiguousarray(a, dtype=d) for a, d in
+                 zip(triplets, (np.int32, np.int32, np.float64)))
     if dims is None:
-        dims = Dimensions(int(ii.max()) if len(ii) else 0, int(jj.max()) if len(jj) else 0)
+        dims = Dimensions(int(ii.max(initial=0)), int(jj.max(initial=0)))
+    # reference-shaped request: validated triplets + dims (both Impl kinds accept it)
     req = SimpleNamespace(triplets=SimpleNamespace(ii=ii, jj=jj, sr=s), dims=dims,
                           capacity_hint=None)
-    reference = None
+    outs = [(impl.name, impl.run(req)) for impl in impls]
+    for name, out in outs[1:]:
+        if not _same(outs[0][1], out):
+            raise ResultMismatch(f"{name} output differs from {outs[0][0]} "
+                                 f"(nnz {out.nnz} vs {outs[0][1].nnz})")
+    nnz = outs[0][1].nnz if outs else 0
+    rows = []
     for impl in impls:
-        out = impl.run(req)
-        if reference is None:
-            reference = (impl.name, out)
-        elif not _same(reference[1], out):
-            raise ResultMismatch(f"{impl.name} output differs from {reference[0]} "
-                                 f"(nnz {out.nnz} vs {reference[1].nnz})")
-    nnz = reference[1].nnz if reference else 0
-    results = []
-    serial_mean = None
-    for impl in impls:
-        impl.run(req)
-        times = []
-        acc: dict[str, float] = {}
-        for _ in range(reps):
-            phases: dict[str, float] = {}
-            t0 = time.perf_counter()
-            impl.run(req, phases)
-            times.append(time.perf_counter() - t0)
-            for k, v in phases.items():
-                acc[k] = acc.get(k, 0.0) + v
-        mean = sum(times) / len(times)
-        if impl.name.startswith("serial") and serial_mean is None:
-            serial_mean = mean
-        results.append(BenchResult(dataset_id, impl.name, impl.threads, mean, min(times), reps,
-                                   len(ii), dims.m, dims.n, nnz,
-                                   phase_means={k: v / reps for k, v in acc.items()}))
-    if serial_mean is not None:
-        for r in results:
-            r.speedup_vs_serial = serial_mean / r.mean_seconds
-    return results
+        mean, best, phases = _timed(impl, req, reps)
+        rows.append(BenchResult(dataset_id, impl.name, impl.threads, mean, best, reps, len(ii),
+                                dims.m, dims.n, nnz, phase_means=phases))
+    base = next((r.mean_seconds for r in rows if r.impl.startswith("serial")), None)
+    for r in rows:
+        r.speedup_vs_serial = base / r.mean_seconds if base else None
+    return rows
 
 
 def _same(a, b) -> bool:

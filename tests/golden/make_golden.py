@@ -4,10 +4,9 @@ Run in the build container (where /root/reference exists):
 
     python tests/golden/make_golden.py
 
-It imports the reference package ``sparseasm`` from
-/root/reference/pkg/src with its compiled Cython kernels (built from the
-reference's own _kernels.pyx by oracle/Makefile into oracle/_ref/) and
-writes, next to this script:
+It imports the reference package ``sparseasm`` installed unmodified into
+oracle/_ref/ (its drivers plus its Cython kernels compiled from its own
+sources: oracle/Makefile target ``ref``) and writes, next to this script:
 
   sweep_digests.json    the acceptance sweep (reference
                         test_acceptance.py:33-35, 50-51): for seeds
@@ -35,7 +34,6 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(os.path.dirname(HERE))
-REF_SRC = "/root/reference/pkg/src"
 REF_TESTS = "/root/reference/pkg/tests"
 
 sys.path.insert(0, ROOT)
@@ -43,12 +41,9 @@ sys.path.insert(0, os.path.join(ROOT, "tests"))
 
 
 def _import_reference():
-    from oracle import ref_driver
+    from oracle import stock
 
-    kernels = ref_driver.kernels()  # the reference's own compiled kernels
-    sys.modules["sparseasm._kernels"] = kernels
-    sys.path.insert(0, REF_SRC)
-    import sparseasm
+    sparseasm = stock.module()  # the unmodified reference package (oracle/_ref)
 
     assert sparseasm.backend.name() == "c", "reference compiled kernels not active"
     sys.path.insert(0, REF_TESTS)

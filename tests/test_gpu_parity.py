@@ -15,6 +15,7 @@ import paper_1406_1066_b200 as sa  # noqa: E402
 from golden_io import error_cases, small_cases, sweep, workloads  # noqa: E402
 from instances import input_digest, output_digest, random_triplets  # noqa: E402
 from oracle import oracle as O  # noqa: E402
+from oracle import stock  # noqa: E402
 
 CASES = small_cases()
 ERRS = error_cases()
@@ -596,30 +597,73 @@ def test_cli_assemble_verify_bench(tmp_path, monkeypatch, capsys):
     assert rows[0]["impl"].startswith("b200") and int(rows[0]["nnz"]) == 9965
 
 
-@pytest.mark.parametrize("staged", ["0", "1"])
-def test_output_modes_bit_exact(staged, monkeypatch):
-    """Both output modes of the fold -- chained tile offsets (decoupled
-    look-back) and staged outputs (k_tile_scan + k_tile_emit, chosen for
-    long-column inputs) -- on the sweep subset with big columns, the
-    reference's datasets and scaled FEM / heavy-duplicate workloads."""
+@pytest.mark.parametrize("opt,val", [("FOLD_STAGED", 0), ("FOLD_STAGED", 1),
+                                     ("SCATTER_STAGED", 0), ("SCATTER_STAGED", 1)])
+def test_pipeline_variants_bit_exact(opt, val):
+    """Every variant a context option can force gives the reference's bits:
+    the fold's chained tile offsets vs staged outputs (k_tile_emit), and the
+    plain vs shared-memory-staged column scatter (k_scatter_staged, chosen
+    automatically only for N > 2^24, i.e. cfg5).  Whole acceptance sweep,
+    the reference's datasets, scaled FEM / heavy-duplicate workloads and
+    full-size cfg2 / cfg3."""
+    from paper_1406_1066_b200 import _capi
     from paper_1406_1066_b200 import workloads as W
 
-    monkeypatch.setenv("SA_STAGED", staged)
-    kw, rows = sweep("acceptance")
-    for r in rows[:200]:
-        ii, jj, sr = random_triplets(r["seed"], **kw)
-        out = sa.assemble(ii.astype(np.int32), jj.astype(np.int32), sr)
-        assert output_digest(out.jc, out.ir, out.pr) == r["output"], r["seed"]
-    for d in _dataset_digests():
-        ii, jj, s = W.ransparse(d["siz"], d["nnz_row"], d["nrep"], d["seed"])
-        out = sa.assemble(ii, jj, s)
-        assert output_digest(out.jc, out.ir, out.pr) == d["output"], d
+    a = sa.default_assembler(0)
+    a.set_option(getattr(_capi, "SA_OPT_" + opt), val)
+    try:
+        kw, rows = sweep("acceptance")
+        bad = []
+        for r in rows:
+            ii, jj, sr = random_triplets(r["seed"], **kw)
+            out = sa.assemble(ii.astype(np.int32), jj.astype(np.int32), sr)
+            if output_digest(out.jc, out.ir, out.pr) != r["output"]:
+                bad.append(r["seed"])
+        assert bad == []
+        for d in _dataset_digests():
+            ii, jj, s = W.ransparse(d["siz"], d["nnz_row"], d["nrep"], d["seed"])
+            out = sa.assemble(ii, jj, s)
+            assert output_digest(out.jc, out.ir, out.pr) == d["output"], d
+        dev = torch.device("cuda", 0)
+        for w in (W.fem3d(30, device=dev), W.heavy_dup(m=20_000, positions=200_000, device=dev),
+                  W.fem2d(64, device=dev), W.config(2, device=dev), W.config(3, device=dev)):
+            out = a.assemble_device(w.ii, w.jj, w.s, m=w.m, n=w.n)
+            ref = O.assemble_counting(w.ii.cpu().numpy(), w.jj.cpu().numpy(), w.s.cpu().numpy(),
+                                      w.m, w.n)
+            _same(out.to_host(), ref)
+            del w, out, ref
+    finally:
+        a.set_option(getattr(_capi, "SA_OPT_" + opt), -1)
+
+
+@pytest.mark.skipif(not stock.available(), reason="oracle/_ref (stock reference) not installed")
+@pytest.mark.parametrize("k", [4, 5])
+def test_full_size_bit_exact_vs_stock_reference(k):
+    """north_star: bit-exact CSC on all five configs.  cfg4 (heavy-duplicate,
+    L ~ 5e8) and cfg5 (2D FEM N = 8000, L = 1.152e9) at FULL size against the
+    unmodified reference package (oracle/_ref: stock assemble_parallel over
+    its compiled kernels, all host threads; bit-identical to its serial
+    driver for every p, test_acceptance.py:135-154): jc / ir equal, pr equal
+    byte for byte."""
+    from paper_1406_1066_b200 import workloads as W
+
     dev = torch.device("cuda", 0)
-    for w in (W.fem3d(30, device=dev), W.heavy_dup(m=20_000, positions=200_000, device=dev),
-              W.fem2d(64, device=dev)):
-        out = sa.default_assembler(0).assemble_device(w.ii, w.jj, w.s, m=w.m, n=w.n)
-        ref = O.assemble_counting(w.ii.cpu().numpy(), w.jj.cpu().numpy(), w.s.cpu().numpy(), w.m, w.n)
-        _same(out.to_host(), ref)
+    w = W.config(k, device=dev)
+    m, n, L = w.m, w.n, w.L
+    out = sa.default_assembler(0).assemble_device(w.ii, w.jj, w.s, m=m, n=n)
+    ii, jj, s = w.ii.cpu().numpy(), w.jj.cpu().numpy(), w.s.cpu().numpy()
+    del w
+    jc, ir, pr = out.jc.cpu().numpy(), out.ir.cpu().numpy(), out.pr.cpu().numpy()
+    del out
+    torch.cuda.empty_cache()
+    ref = stock.parallel(stock.request(ii, jj, s, m, n), stock.host_threads())
+    del ii, jj, s
+    assert (ref.m, ref.n) == (m, n)
+    assert np.array_equal(jc, ref.jc)
+    assert np.array_equal(ir, ref.ir)
+    assert pr.tobytes() == np.asarray(ref.pr).tobytes()
+    if k == 5:
+        assert len(ir) == 448_048_001 and L == 1_152_000_000
 
 
 @pytest.mark.parametrize("width", [40, 90, 200])

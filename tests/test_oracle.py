@@ -7,7 +7,7 @@ import pytest
 from golden_io import error_cases, small_cases, sweep, workloads
 from instances import input_digest, output_digest, random_triplets
 from oracle import oracle as O
-from oracle import ref_driver
+from oracle import stock
 
 CASES = small_cases()
 
@@ -116,17 +116,18 @@ def test_workload_digests_c_oracle():
         assert output_digest(out.jc, out.ir, out.pr) == r["output"], r
 
 
-@pytest.mark.skipif(not ref_driver.available(), reason="oracle/_ref not built")
-def test_reference_kernels_serial_and_threaded():
-    """The reference's own compiled kernels (oracle/_ref) under the restated
-    serial and threaded drivers reproduce the reference digests."""
+@pytest.mark.skipif(not stock.available(), reason="oracle/_ref (stock reference) not installed")
+def test_stock_reference_serial_and_threaded():
+    """The unmodified reference package (oracle/_ref: its drivers and its
+    compiled kernels) reproduces the committed reference digests, serially
+    and with its threaded driver (parallel.py:361-389)."""
     kw, rows = sweep("acceptance")
     for r in rows[::25]:
         ii, jj, sr = random_triplets(r["seed"], **kw)
         ii32, jj32 = ii.astype(np.int32), jj.astype(np.int32)
-        M, N = int(ii32.max(initial=0)), int(jj32.max(initial=0))
-        a = ref_driver.assemble_serial(ii32, jj32, sr, M, N)
+        req = stock.request(ii32, jj32, sr, None, None)
+        a = stock.serial(req)
         assert output_digest(a.jc, a.ir, a.pr) == r["output"]
         for p in (2, 3, 8):
-            b = ref_driver.assemble_parallel(ii32, jj32, sr, M, N, p)
+            b = stock.parallel(req, p)
             assert b.same_as(a)
