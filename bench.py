@@ -136,28 +136,43 @@ def _dist():
     return world, rank, local
 
 
-REF_STEP_S = 1.0  # target duration of one timed reference step (bounded sample)
+REF_STEP_S = 5.0  # longest timed reference step before the workload is sampled
 
 
 def reference_sample(ii, jj, s, m, n, target_s=REF_STEP_S):
-    """Size a bounded sample of the workload for the reference's CPU path:
-    the first Ls triplets (same m, n) such that one stock
-    ``assemble_parallel`` on all host threads takes about ``target_s``.
-    Returns (Ls, req, run) with the reference's request built once, outside
-    any timing (its run_bench protocol, bench.py:146-160)."""
+    """Size the bounded sample of the workload for the reference's CPU path:
+    the first Ls triplets (same m, n).  Its run time is fitted as a + b Ls
+    from two untimed probe runs (the O((m + n) p) merges of the threaded
+    driver are a fixed cost, so a small prefix alone would understate its
+    throughput); the whole workload is used when one run fits in
+    ``target_s``.  Returns (Ls, req, run, p) with the reference's request
+    built once, outside any timing (its run_bench protocol,
+    bench.py:146-160)."""
     from oracle import stock
 
     p = stock.host_threads()
     L = len(ii)
-    Ls = min(L, 1 << 22)
-    req = stock.request(ii[:Ls], jj[:Ls], s[:Ls], m, n)
-    t0 = time.perf_counter()
-    stock.parallel(req, p)  # untimed probe run (also a warm-up)
-    dt = max(time.perf_counter() - t0, 1e-6)
-    want = int(min(L, max(Ls, Ls * target_s / dt)))
-    if want > Ls * 1.2 or (want == L and Ls != L):
-        Ls = want
-        req = stock.request(ii[:Ls], jj[:Ls], s[:Ls], m, n)
+
+    def timed(k):
+        req = stock.request(ii[:k], jj[:k], s[:k], m, n)
+        t0 = time.perf_counter()
+        stock.parallel(req, p)
+        return req, time.perf_counter() - t0
+
+    k0 = min(L, 1 << 22)
+    req, t0 = timed(k0)
+    Ls = k0
+    if k0 < L:
+        k1 = min(L, 1 << 24)
+        req, t1 = timed(k1)
+        Ls = k1
+        if k1 < L:
+            b_ = max((t1 - t0) / (k1 - k0), 1e-12)
+            a_ = max(t1 - b_ * k1, 0.0)
+            want = int(min(L, max(k1, (target_s - a_) / b_)))
+            if want > k1:
+                Ls = want
+                req = stock.request(ii[:Ls], jj[:Ls], s[:Ls], m, n)
     return Ls, req, (lambda: stock.parallel(req, p)), p
 
 

@@ -72,7 +72,9 @@ enum { SA_WHICH_ROW = 0, SA_WHICH_COL = 1 };
  * SAME bits (tests force each variant); none changes a result. */
 enum {
     SA_OPT_FOLD_STAGED = 0,     /* fold outputs staged + k_tile_emit pass       */
-    SA_OPT_SCATTER_STAGED = 1   /* column scatter through shared-memory staging */
+    SA_OPT_SCATTER_STAGED = 1,  /* column scatter through shared-memory staging */
+    SA_OPT_PATH = 2             /* 0: column-cursor pipeline, 1: column-block radix
+                                   path (sa_radix.cu), -1: chosen per input    */
 };
 
 /* ABI version (bumped on any signature change). */

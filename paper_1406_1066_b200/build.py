@@ -15,7 +15,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "lib")
 LIBNAME = "libsa_b200.so"
-SOURCES = ["sa_kernels.cu", "sa_tile.cu", "sa_prune.cu", "sa_shard.cu", "sa_capi.cu"]
+SOURCES = ["sa_kernels.cu", "sa_tile.cu", "sa_radix.cu", "sa_prune.cu", "sa_shard.cu", "sa_capi.cu"]
 HEADERS = ["sa_internal.cuh", "sa_network.cuh", os.path.join("..", "..", "include", "sparse_assembly.h")]
 
 NVCC_FLAGS = [

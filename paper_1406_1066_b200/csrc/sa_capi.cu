@@ -42,6 +42,16 @@ struct sa_ctx {
     int32_t *pt_cnt = nullptr;            size_t ptc_cap = 0;    // partition: tile x rank counts
     int64_t *pt_off = nullptr;            size_t pto_cap = 0;    // partition: tile x rank offsets
     int64_t *pt_counts = nullptr;         // partition: per-rank counts and bases (16)
+    // radix path (sa_radix.cu): partition buffers X / Y, histograms, look-back words
+    int32_t *rx_i = nullptr, *rx_j = nullptr; double *rx_s = nullptr;  size_t rx_cap = 0;
+    int32_t *ry_i = nullptr, *ry_j = nullptr; double *ry_s = nullptr;  size_t ry_cap = 0;
+    uint32_t *rhist = nullptr;                                         // RP_MAXPASS x RP_MAXD
+    unsigned long long *rlb = nullptr;    size_t rlb_cap = 0;          // nchunk x RP_MAXD
+    unsigned long long *rlbf = nullptr;   size_t rlbf_cap = 0;         // nsub x LB_STRIDE
+    uint32_t *rbnd = nullptr;             size_t rbnd_cap = 0;         // nsub + 1
+    uint32_t *rbig = nullptr;             size_t rbig_cap = 0;         // nsub (oversize list)
+    uint32_t *rbigu = nullptr;            size_t rbigu_cap = 0;        // nsub
+    unsigned rp_epoch = 0;                                             // look-back tag epoch
     ErrState *err = nullptr;              // device
     ErrState *err_host = nullptr;         // pinned mirror
 
@@ -62,6 +72,7 @@ struct sa_ctx {
     // options (sa_set_option); -1 = automatic
     int opt_fold_staged = -1;
     int opt_scatter_staged = -1;
+    int opt_path = -1;
 
     int64_t host_L = -1;
     int64_t host_stride = 1;
@@ -110,7 +121,8 @@ int bits_for(uint64_t v) {  // bits needed to represent v (0 -> 0)
 
 // One launch that resets the per-call device state.
 __global__ void k_init(ErrState *err, uint32_t *cur, int64_t ncur, unsigned long long *ts,
-                       int64_t nts, unsigned long long *ss, int64_t nss, uint8_t *tb) {
+                       int64_t nts, unsigned long long *ss, int64_t nss, uint8_t *tb,
+                       uint32_t *z, int nz) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     pdl_wait();  // the previous call's fold may still read the look-back words
@@ -132,13 +144,15 @@ __global__ void k_init(ErrState *err, uint32_t *cur, int64_t ncur, unsigned long
         tb[k] = 0;
     }
     for (int64_t k = t0; k < nss; k += stride) ss[k * LB_STRIDE] = 0ull;
+    for (int64_t k = t0; k < nz; k += stride) z[k] = 0u;
 }
 
-int launch_init(sa_ctx *ctx, Launch &lc, int64_t ncur, int64_t nts, int64_t nss) {
-    int64_t work = std::max<int64_t>({ncur / 4, nts, nss, 1});
+int launch_init(sa_ctx *ctx, Launch &lc, int64_t ncur, int64_t nts, int64_t nss,
+                uint32_t *z = nullptr, int nz = 0) {
+    int64_t work = std::max<int64_t>({ncur / 4, nts, nss, (int64_t)nz, 1});
     int grid = (int)std::min<int64_t>((work + 255) / 256, (int64_t)ctx->num_sms * 4);
     SA_CUDA(ctx, launch_pdl(k_init, dim3(grid), dim3(256), 0, lc.stream, ctx->err, ctx->cur, ncur,
-                            ctx->tile_state, nts, ctx->scan_state, nss, ctx->tile_big));
+                            ctx->tile_state, nts, ctx->scan_state, nss, ctx->tile_big, z, nz));
     lc.launches++;
     return SA_OK;
 }
@@ -307,6 +321,10 @@ void sa_destroy(sa_ctx *ctx) {
     cudaFree(ctx->pt_off);
     cudaFree(ctx->pt_counts);
     cudaFree(ctx->pr_nnz);
+    for (void *p : {(void *)ctx->rx_i, (void *)ctx->rx_j, (void *)ctx->rx_s, (void *)ctx->ry_i,
+                    (void *)ctx->ry_j, (void *)ctx->ry_s, (void *)ctx->rhist, (void *)ctx->rlb,
+                    (void *)ctx->rlbf, (void *)ctx->rbnd, (void *)ctx->rbig, (void *)ctx->rbigu})
+        cudaFree(p);
     cudaFree(ctx->h_ii);
     cudaFree(ctx->h_jj);
     cudaFree(ctx->h_s);
@@ -326,6 +344,7 @@ int sa_set_option(sa_ctx *ctx, int option, int value) {
     switch (option) {
         case SA_OPT_FOLD_STAGED: ctx->opt_fold_staged = value; return SA_OK;
         case SA_OPT_SCATTER_STAGED: ctx->opt_scatter_staged = value; return SA_OK;
+        case SA_OPT_PATH: ctx->opt_path = value; return SA_OK;
         default: return fail(ctx, SA_ERR_INVALID_ARG, "sa_set_option: unknown option");
     }
 }
@@ -385,10 +404,179 @@ int sa_infer_dims(sa_ctx *ctx, const int32_t *d_ii, const int32_t *d_jj, int64_t
 
 namespace {
 
+// ---- radix path (sa_radix.cu) -------------------------------------------------
+struct RadixPlan {
+    bool ok = false;
+    int w = 0, rbits = 0, npass = 0;
+    int shift[RP_MAXPASS] = {}, bits[RP_MAXPASS] = {};
+    int32_t nsub = 0;
+    int64_t nchunk = 0;
+};
+
+// Sub-buckets of W = 2^w columns: the largest w whose expected sub-bucket
+// (L W / N triplets) stays within 4/5 of the fold's shared-memory capacity and
+// whose (column-local, row) key fits 31 bits; the remaining column bits are
+// split over at most RP_MAXPASS passes of at most RP_MAXBITS bits.
+RadixPlan radix_plan(int64_t L, int32_t M, int32_t N) {
+    RadixPlan P;
+    if (L <= 0 || N <= 0 || M <= 0) return P;
+    P.rbits = bits_for((uint64_t)(M - 1));
+    const int cbits = bits_for((uint64_t)(N - 1));
+    int w = 0;
+    while (w < 8 && w < cbits && w + 1 + P.rbits <= 31 &&
+           (L << (w + 1)) <= (int64_t)(4 * RF_CAP / 5) * (int64_t)N)
+        ++w;
+    if (w + P.rbits > 31) return P;
+    const int R = cbits - w;
+    const int npass = std::max(1, (R + RP_MAXBITS - 1) / RP_MAXBITS);
+    if (npass > RP_MAXPASS) return P;
+    int sh = w;
+    for (int p = 0; p < npass; ++p) {
+        P.bits[p] = R / npass + (p < R % npass ? 1 : 0);
+        P.shift[p] = sh;
+        sh += P.bits[p];
+    }
+    P.w = w;
+    P.npass = npass;
+    P.nsub = (int32_t)(((int64_t)N + (1ll << w) - 1) >> w);
+    P.nchunk = (L + RP_CHUNK - 1) / RP_CHUNK;
+    P.ok = true;
+    return P;
+}
+
+// One partition buffer: ii, jj (int32) and s (float64) for `need` triplets.
+cudaError_t ensure_trip(int32_t *&i, int32_t *&j, double *&v, size_t &cap, size_t need) {
+    if (need <= cap && i) return cudaSuccess;
+    cudaFree(i);
+    cudaFree(j);
+    cudaFree(v);
+    i = j = nullptr;
+    v = nullptr;
+    cap = 0;
+    need = std::max<size_t>(need, 1);
+    cudaError_t e = cudaMalloc(reinterpret_cast<void **>(&i), need * 4);
+    if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void **>(&j), need * 4);
+    if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void **>(&v), need * 8);
+    if (e == cudaSuccess) cap = need;
+    return e;
+}
+
+// ensure() for look-back word arrays: fresh memory is zeroed (tag 0 = never
+// published); returns true in `fresh` when the array was (re)allocated.
+cudaError_t ensure_lb(unsigned long long *&p, size_t &cap, size_t need, cudaStream_t st, bool &fresh) {
+    fresh = false;
+    if (need <= cap && p) return cudaSuccess;
+    cudaError_t e = ensure(p, cap, need);
+    if (e == cudaSuccess) e = cudaMemsetAsync(p, 0, cap * sizeof(unsigned long long), st);
+    fresh = true;
+    return e;
+}
+
+int assemble_radix(sa_ctx *ctx, const RadixPlan &P, const int32_t *ii, const int32_t *jj,
+                   const double *s, int64_t s_stride, int64_t L, int32_t M, int32_t N,
+                   int32_t *d_jc, int32_t *d_ir, double *d_pr, int64_t cap) {
+    Launch lc{ctx->stream, ctx->num_sms, 0};
+    const size_t nl = (size_t)L;
+    const size_t nsub = (size_t)P.nsub;
+    SA_CUDA(ctx, ensure_trip(ctx->rx_i, ctx->rx_j, ctx->rx_s, ctx->rx_cap, nl));
+    if (P.npass > 1) SA_CUDA(ctx, ensure_trip(ctx->ry_i, ctx->ry_j, ctx->ry_s, ctx->ry_cap, nl));
+    else SA_CUDA(ctx, ensure_trip(ctx->ry_i, ctx->ry_j, ctx->ry_s, ctx->ry_cap, 1));
+    SA_CUDA(ctx, ensure(ctx->perm, ctx->perm_cap, nl + 2));  // oversize scratch A
+    if (!ctx->rhist) SA_CUDA(ctx, cudaMalloc(reinterpret_cast<void **>(&ctx->rhist), RP_MAXPASS * RP_MAXD * 4));
+    bool f1 = false, f2 = false;
+    SA_CUDA(ctx, ensure_lb(ctx->rlb, ctx->rlb_cap, (size_t)P.nchunk * RP_MAXD, ctx->stream, f1));
+    SA_CUDA(ctx, ensure_lb(ctx->rlbf, ctx->rlbf_cap, nsub * LB_STRIDE, ctx->stream, f2));
+    SA_CUDA(ctx, ensure(ctx->rbnd, ctx->rbnd_cap, nsub + 1));
+    SA_CUDA(ctx, ensure(ctx->rbig, ctx->rbig_cap, nsub));
+    SA_CUDA(ctx, ensure(ctx->rbigu, ctx->rbigu_cap, nsub));
+    // look-back tags: (epoch << 2 | pass), epoch in [1, 16383]; on wrap-around
+    // every word is cleared once so no stale word can carry a live tag
+    if (++ctx->rp_epoch >= 16384) {
+        if (!f1) SA_CUDA(ctx, cudaMemsetAsync(ctx->rlb, 0, ctx->rlb_cap * 8, ctx->stream));
+        if (!f2) SA_CUDA(ctx, cudaMemsetAsync(ctx->rlbf, 0, ctx->rlbf_cap * 8, ctx->stream));
+        ctx->rp_epoch = 1;
+    }
+    const unsigned ep = ctx->rp_epoch << 2;
+
+    ctx->nev = 0;
+    int rc = mark(ctx, "k_init");
+    if (rc) return rc;
+    if ((rc = launch_init(ctx, lc, 0, 0, 0, ctx->rhist, RP_MAXPASS * RP_MAXD))) return rc;
+    if ((rc = mark(ctx, "k_rhist"))) return rc;
+    SA_CUDA(ctx, launch_rhist(lc, jj, L, N, P.shift[0], P.bits[0], ctx->rhist, ctx->err));
+    int32_t *bi[2] = {ctx->rx_i, ctx->ry_i}, *bj[2] = {ctx->rx_j, ctx->ry_j};
+    double *bs[2] = {ctx->rx_s, ctx->ry_s};
+    static const char *pname[RP_MAXPASS] = {"k_rpass0", "k_rpass1", "k_rpass2"};
+    for (int p = 0; p < P.npass; ++p) {
+        RadixPassArgs A{};
+        A.ii_in = p ? bi[(p - 1) & 1] : ii;
+        A.jj_in = p ? bj[(p - 1) & 1] : jj;
+        A.s_in = p ? bs[(p - 1) & 1] : s;
+        A.s_stride = p ? 1 : s_stride;
+        A.ii_out = bi[p & 1];
+        A.jj_out = bj[p & 1];
+        A.s_out = bs[p & 1];
+        A.L = L;
+        A.M = M;
+        A.N = N;
+        A.shift = P.shift[p];
+        A.bits = P.bits[p];
+        const bool last = p + 1 == P.npass;
+        A.nshift = last ? 0 : P.shift[p + 1];
+        A.nbits = last ? 0 : P.bits[p + 1];
+        A.hist = ctx->rhist + p * RP_MAXD;
+        A.hist_next = last ? nullptr : ctx->rhist + (p + 1) * RP_MAXD;
+        A.lb = ctx->rlb;
+        A.tag = ep | (unsigned)p;
+        A.pass = p;
+        if ((rc = mark(ctx, pname[p]))) return rc;
+        SA_CUDA(ctx, launch_rpass(lc, A, p == 0, P.nchunk, ctx->err));
+    }
+    const int fb = (P.npass - 1) & 1;  // buffer holding the partitioned triplets
+    RadixFoldArgs F{};
+    F.ii = bi[fb];
+    F.jj = bj[fb];
+    F.s = bs[fb];
+    F.bnd = ctx->rbnd;
+    F.biglist = ctx->rbig;
+    F.bigu = ctx->rbigu;
+    F.scrA = reinterpret_cast<unsigned long long *>(ctx->perm);
+    F.scrB = reinterpret_cast<unsigned long long *>(fb ? ctx->rx_s : ctx->ry_s);
+    if (P.npass == 1) {  // Y is a 1-entry stub: scratch B must hold L words
+        SA_CUDA(ctx, ensure_trip(ctx->ry_i, ctx->ry_j, ctx->ry_s, ctx->ry_cap, nl));
+        F.scrB = reinterpret_cast<unsigned long long *>(ctx->ry_s);
+    }
+    F.lbf = ctx->rlbf;
+    F.tag = ep | 3u;
+    F.w = P.w;
+    F.rbits = P.rbits;
+    F.N = N;
+    F.nsub = P.nsub;
+    F.jc = d_jc;
+    F.ir = d_ir;
+    F.pr = d_pr;
+    F.cap = cap;
+    if ((rc = mark(ctx, "k_rbounds"))) return rc;
+    SA_CUDA(ctx, launch_rbounds(lc, F.jj, P.w, P.nsub, ctx->rbnd, ctx->rbig, ctx->err));
+    if ((rc = mark(ctx, "k_rbig"))) return rc;
+    SA_CUDA(ctx, launch_rbig(lc, F, ctx->err));
+    if ((rc = mark(ctx, "k_rfold"))) return rc;
+    SA_CUDA(ctx, launch_rfold(lc, F, ctx->err));
+    if ((rc = mark(ctx, nullptr))) return rc;
+    ctx->launches = lc.launches;
+    return SA_OK;
+}
+
 // The assembly pipeline over a segment table (Ltot triplets in total).
 int assemble_segments(sa_ctx *ctx, const Segs &S, int64_t L, int32_t M, int32_t N, int32_t *d_jc,
                       int32_t *d_ir, double *d_pr, int64_t cap) {
     SA_CUDA(ctx, cudaSetDevice(ctx->device));
+    if (S.nseg == 1 && L > 0 && N > 0 && M > 0 && ctx->opt_path != 0) {
+        const RadixPlan P = radix_plan(L, M, N);
+        if (P.ok && ctx->opt_path == 1)
+            return assemble_radix(ctx, P, S.ii[0], S.jj[0], S.s[0], S.stride[0], L, M, N, d_jc, d_ir,
+                                  d_pr, cap);
+    }
     Launch lc{ctx->stream, ctx->num_sms, 0};
     lc.fold_staged = ctx->opt_fold_staged;
     lc.scatter_staged = ctx->opt_scatter_staged;

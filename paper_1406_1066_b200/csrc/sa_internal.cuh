@@ -83,6 +83,11 @@ struct ErrState {
     unsigned int nbig;          // number of big columns
     unsigned int lsmall;        // triplets in small columns (small record space)
     unsigned int long_cols;     // some small column is long (> SHORT_COL): the fold's long pass runs
+    // radix path (sa_radix.cu)
+    unsigned int rp_ticket[3];  // chunk tickets of the partition passes
+    unsigned int rf_ticket;     // sub-bucket tickets of the fold
+    unsigned int rbig_n;        // oversize sub-buckets listed by k_rbounds
+    unsigned int rvalid;        // triplets with a valid column (partitioned)
 };
 
 __device__ __forceinline__ unsigned lanemask_lt() {
@@ -295,6 +300,57 @@ __device__ __forceinline__ void smem_incl_max(int *arr, int n, int *s_warp) {
     __syncthreads();
 }
 
+constexpr int BIG_NT = 1024;
+constexpr int BIG_NW = BIG_NT / 32;
+
+// One stable LSD radix pass (8-bit digit at `shift`) of n keys src -> dst by
+// one CTA: every warp owns a contiguous segment; per-warp digit counts, one
+// block scan over (digit, warp), then each warp places its segment in order
+// (match.any ranks + a warp-private running counter per digit) -- no block
+// barrier inside the loops.
+__device__ __forceinline__ void big_radix_pass(const unsigned long long *src,
+                                               unsigned long long *dst, int64_t n, int shift,
+                                               uint32_t (*s_cnt)[256], uint32_t *s_warp) {
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const unsigned lt = lanemask_lt();
+    for (int k = tid; k < BIG_NW * 256; k += BIG_NT) (&s_cnt[0][0])[k] = 0;
+    __syncthreads();
+    const int64_t lo = (int64_t)w * n / BIG_NW, hi = (int64_t)(w + 1) * n / BIG_NW;
+    for (int64_t p = lo + lane; p < hi; p += 32) atomicAdd(&s_cnt[w][(src[p] >> shift) & 255], 1u);
+    __syncthreads();
+    {  // digit-major exclusive scan: thread t owns entries 8t .. 8t+7 of (digit, warp)
+        uint32_t v[8], sum = 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int q = 8 * tid + k;
+            v[k] = s_cnt[q % BIG_NW][q / BIG_NW];
+            sum += v[k];
+        }
+        uint32_t tot;
+        uint32_t pre = block_excl_sum<BIG_NT, uint32_t>(sum, s_warp, tot);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int q = 8 * tid + k;
+            s_cnt[q % BIG_NW][q / BIG_NW] = pre;
+            pre += v[k];
+        }
+    }
+    __syncthreads();
+    for (int64_t b0 = lo; b0 < hi; b0 += 32) {
+        const int64_t p = b0 + lane;
+        const bool valid = p < hi;
+        const unsigned long long key = valid ? src[p] : 0ull;
+        const int d = valid ? (int)((key >> shift) & 255) : 256;
+        const unsigned peers = __match_any_sync(FULL, d);
+        const uint32_t base = valid ? s_cnt[w][d] : 0u;
+        if (valid) dst[base + __popc(peers & lt)] = key;
+        __syncwarp();
+        if (valid && (peers & lt) == 0u) s_cnt[w][d] = base + __popc(peers);
+        __syncwarp();
+    }
+    __syncthreads();
+}
+
 // ---- programmatic dependent launch -------------------------------------------
 // Every kernel of the assembly chain is launched with programmatic stream
 // serialisation: it may start (smem set-up) while its predecessor drains,
@@ -355,6 +411,59 @@ cudaError_t launch_tile_fold(Launch &lc, const uint32_t *sstart, const int2 *til
                              unsigned long long *tile_state, int32_t N, int32_t *jc, int32_t *ir,
                              double *pr, int64_t cap, ErrState *err, int4 *stage,
                              int2 *tile_cnt);
+
+// ---- radix path (sa_radix.cu) -------------------------------------------------
+constexpr int RP_NT = 512;                  // partition pass: threads per CTA
+constexpr int RP_NW = RP_NT / 32;
+constexpr int RP_IPT = 16;                  // triplets per thread
+constexpr int RP_CHUNK = RP_NT * RP_IPT;    // triplets per chunk (CTA)
+constexpr int RP_MAXBITS = 9;               // digit bits per pass
+constexpr int RP_MAXD = 1 << RP_MAXBITS;
+constexpr int RP_MAXPASS = 3;
+constexpr int RF_CAP = 4096;                // fold: largest sub-bucket held in shared memory
+constexpr int RF_WMAX = 256;                // fold: columns per sub-bucket (2^w)
+
+struct RadixPassArgs {
+    const int32_t *ii_in, *jj_in;
+    const double *s_in;
+    int64_t s_stride;
+    int32_t *ii_out, *jj_out;
+    double *s_out;
+    int64_t L;
+    int32_t M, N;
+    int shift, bits;    // this pass's digit: ((col - 1) >> shift) & (2^bits - 1)
+    int nshift, nbits;  // the next pass's digit (nbits = 0: last pass)
+    const uint32_t *hist;
+    uint32_t *hist_next;
+    unsigned long long *lb;  // look-back words, nchunk x 2^bits
+    unsigned tag;
+    int pass;
+};
+
+struct RadixFoldArgs {
+    const int32_t *ii, *jj;  // partitioned triplets (sorted by sub-bucket, stable)
+    const double *s;
+    const uint32_t *bnd;     // nsub + 1 sub-bucket starts
+    const uint32_t *biglist; // oversize sub-buckets
+    uint32_t *bigu;          // per oversize sub-bucket: results | BIGFLAG (keys in scrB)
+    unsigned long long *scrA, *scrB;  // oversize scratch (L entries each)
+    unsigned long long *lbf; // look-back words, nsub x LB_STRIDE
+    unsigned tag;
+    int w, rbits;
+    int32_t N, nsub;
+    int32_t *jc, *ir;
+    double *pr;
+    int64_t cap;
+};
+
+cudaError_t launch_rhist(Launch &lc, const int32_t *jj, int64_t L, int32_t N, int shift, int bits,
+                         uint32_t *hist, ErrState *err);
+cudaError_t launch_rpass(Launch &lc, const RadixPassArgs &A, bool first, int64_t nchunk,
+                         ErrState *err);
+cudaError_t launch_rbounds(Launch &lc, const int32_t *jj, int w, int32_t nsub, uint32_t *bnd,
+                           uint32_t *biglist, ErrState *err);
+cudaError_t launch_rbig(Launch &lc, const RadixFoldArgs &F, ErrState *err);
+cudaError_t launch_rfold(Launch &lc, const RadixFoldArgs &F, ErrState *err);
 
 cudaError_t launch_prune(Launch &lc, const int32_t *jc, const int32_t *ir, const double *pr,
                          int32_t N, int64_t nnz, int32_t *jc_out, int32_t *ir_out,

@@ -975,57 +975,6 @@ cudaError_t launch_scatter(Launch &lc, const Segs &S, int32_t M, int32_t N, uint
 //    digits, warp match + per-warp digit counts), values gathered into the
 //    other buffer, runs folded and compacted in place.
 // ---------------------------------------------------------------------------
-constexpr int BIG_NT = 1024;
-constexpr int BIG_NW = BIG_NT / 32;
-
-// One stable LSD radix pass (8-bit digit at `shift`) of n keys src -> dst by
-// one CTA: every warp owns a contiguous segment; per-warp digit counts, one
-// block scan over (digit, warp), then each warp places its segment in order
-// (match.any ranks + a warp-private running counter per digit) -- no block
-// barrier inside the loops.
-__device__ __forceinline__ void big_radix_pass(const unsigned long long *src,
-                                               unsigned long long *dst, int64_t n, int shift,
-                                               uint32_t (*s_cnt)[256], uint32_t *s_warp) {
-    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-    const unsigned lt = lanemask_lt();
-    for (int k = tid; k < BIG_NW * 256; k += BIG_NT) (&s_cnt[0][0])[k] = 0;
-    __syncthreads();
-    const int64_t lo = (int64_t)w * n / BIG_NW, hi = (int64_t)(w + 1) * n / BIG_NW;
-    for (int64_t p = lo + lane; p < hi; p += 32) atomicAdd(&s_cnt[w][(src[p] >> shift) & 255], 1u);
-    __syncthreads();
-    {  // digit-major exclusive scan: thread t owns entries 8t .. 8t+7 of (digit, warp)
-        uint32_t v[8], sum = 0;
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            const int q = 8 * tid + k;
-            v[k] = s_cnt[q % BIG_NW][q / BIG_NW];
-            sum += v[k];
-        }
-        uint32_t tot;
-        uint32_t pre = block_excl_sum<BIG_NT, uint32_t>(sum, s_warp, tot);
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            const int q = 8 * tid + k;
-            s_cnt[q % BIG_NW][q / BIG_NW] = pre;
-            pre += v[k];
-        }
-    }
-    __syncthreads();
-    for (int64_t b0 = lo; b0 < hi; b0 += 32) {
-        const int64_t p = b0 + lane;
-        const bool valid = p < hi;
-        const unsigned long long key = valid ? src[p] : 0ull;
-        const int d = valid ? (int)((key >> shift) & 255) : 256;
-        const unsigned peers = __match_any_sync(FULL, d);
-        const uint32_t base = valid ? s_cnt[w][d] : 0u;
-        if (valid) dst[base + __popc(peers & lt)] = key;
-        __syncwarp();
-        if (valid && (peers & lt) == 0u) s_cnt[w][d] = base + __popc(peers);
-        __syncwarp();
-    }
-    __syncthreads();
-}
-
 constexpr int MED_NT = 256;                 // threads per medium-column quarter
 constexpr int MED_Q = BIG_NT / MED_NT;      // quarters per CTA
 constexpr int MED_CAP = 1024;               // longest medium column
