@@ -45,8 +45,9 @@ struct sa_ctx {
     // radix path (sa_radix.cu): partition buffers X / Y, histograms, look-back words
     int32_t *rx_i = nullptr, *rx_j = nullptr; double *rx_s = nullptr;  size_t rx_cap = 0;
     int32_t *ry_i = nullptr, *ry_j = nullptr; double *ry_s = nullptr;  size_t ry_cap = 0;
-    uint32_t *rhist = nullptr;                                         // RP_MAXPASS x RP_MAXD
-    unsigned long long *rlb = nullptr;    size_t rlb_cap = 0;          // nchunk x RP_MAXD
+    uint16_t *rcnt = nullptr;             size_t rcnt_cap = 0;         // nchunk x RP_MAXD chunk histograms
+    uint32_t *roff = nullptr;             size_t roff_cap = 0;         // nchunk x RP_MAXD chunk bases
+    uint32_t *rbsum = nullptr;            size_t rbsum_cap = 0;        // nblk x RP_MAXD block bases
     unsigned long long *rlbf = nullptr;   size_t rlbf_cap = 0;         // nsub x LB_STRIDE
     uint32_t *rbnd = nullptr;             size_t rbnd_cap = 0;         // nsub + 1
     uint32_t *rbig = nullptr;             size_t rbig_cap = 0;         // nsub (oversize list)
@@ -322,7 +323,7 @@ void sa_destroy(sa_ctx *ctx) {
     cudaFree(ctx->pt_counts);
     cudaFree(ctx->pr_nnz);
     for (void *p : {(void *)ctx->rx_i, (void *)ctx->rx_j, (void *)ctx->rx_s, (void *)ctx->ry_i,
-                    (void *)ctx->ry_j, (void *)ctx->ry_s, (void *)ctx->rhist, (void *)ctx->rlb,
+                    (void *)ctx->ry_j, (void *)ctx->ry_s, (void *)ctx->rcnt, (void *)ctx->roff, (void *)ctx->rbsum,
                     (void *)ctx->rlbf, (void *)ctx->rbnd, (void *)ctx->rbig, (void *)ctx->rbigu})
         cudaFree(p);
     cudaFree(ctx->h_ii);
@@ -482,9 +483,13 @@ int assemble_radix(sa_ctx *ctx, const RadixPlan &P, const int32_t *ii, const int
     if (P.npass > 1) SA_CUDA(ctx, ensure_trip(ctx->ry_i, ctx->ry_j, ctx->ry_s, ctx->ry_cap, nl));
     else SA_CUDA(ctx, ensure_trip(ctx->ry_i, ctx->ry_j, ctx->ry_s, ctx->ry_cap, 1));
     SA_CUDA(ctx, ensure(ctx->perm, ctx->perm_cap, nl + 2));  // oversize scratch A
-    if (!ctx->rhist) SA_CUDA(ctx, cudaMalloc(reinterpret_cast<void **>(&ctx->rhist), RP_MAXPASS * RP_MAXD * 4));
-    bool f1 = false, f2 = false;
-    SA_CUDA(ctx, ensure_lb(ctx->rlb, ctx->rlb_cap, (size_t)P.nchunk * RP_MAXD, ctx->stream, f1));
+    // partition CTAs: the resident ones (2 per SM), walking the chunks with that stride
+    const int nseg = (int)std::max<int64_t>(1, std::min<int64_t>(P.nchunk, (int64_t)ctx->num_sms * (2048 / RP_NT)));
+    const int64_t nblk = (P.nchunk + RP_BLK - 1) / RP_BLK;
+    SA_CUDA(ctx, ensure(ctx->rcnt, ctx->rcnt_cap, (size_t)P.nchunk * RP_MAXD));
+    SA_CUDA(ctx, ensure(ctx->roff, ctx->roff_cap, (size_t)P.nchunk * RP_MAXD));
+    SA_CUDA(ctx, ensure(ctx->rbsum, ctx->rbsum_cap, (size_t)std::max<int64_t>(nblk, 1) * RP_MAXD));
+    bool f2 = false;
     SA_CUDA(ctx, ensure_lb(ctx->rlbf, ctx->rlbf_cap, nsub * LB_STRIDE, ctx->stream, f2));
     SA_CUDA(ctx, ensure(ctx->rbnd, ctx->rbnd_cap, nsub + 1));
     SA_CUDA(ctx, ensure(ctx->rbig, ctx->rbig_cap, nsub));
@@ -492,7 +497,6 @@ int assemble_radix(sa_ctx *ctx, const RadixPlan &P, const int32_t *ii, const int
     // look-back tags: (epoch << 2 | pass), epoch in [1, 16383]; on wrap-around
     // every word is cleared once so no stale word can carry a live tag
     if (++ctx->rp_epoch >= 16384) {
-        if (!f1) SA_CUDA(ctx, cudaMemsetAsync(ctx->rlb, 0, ctx->rlb_cap * 8, ctx->stream));
         if (!f2) SA_CUDA(ctx, cudaMemsetAsync(ctx->rlbf, 0, ctx->rlbf_cap * 8, ctx->stream));
         ctx->rp_epoch = 1;
     }
@@ -501,12 +505,11 @@ int assemble_radix(sa_ctx *ctx, const RadixPlan &P, const int32_t *ii, const int
     ctx->nev = 0;
     int rc = mark(ctx, "k_init");
     if (rc) return rc;
-    if ((rc = launch_init(ctx, lc, 0, 0, 0, ctx->rhist, RP_MAXPASS * RP_MAXD))) return rc;
-    if ((rc = mark(ctx, "k_rhist"))) return rc;
-    SA_CUDA(ctx, launch_rhist(lc, jj, L, N, P.shift[0], P.bits[0], ctx->rhist, ctx->err));
+    if ((rc = launch_init(ctx, lc, 0, 0, 0))) return rc;
     int32_t *bi[2] = {ctx->rx_i, ctx->ry_i}, *bj[2] = {ctx->rx_j, ctx->ry_j};
     double *bs[2] = {ctx->rx_s, ctx->ry_s};
     static const char *pname[RP_MAXPASS] = {"k_rpass0", "k_rpass1", "k_rpass2"};
+    static const char *uname[RP_MAXPASS] = {"k_rup0", "k_rup1", "k_rup2"};
     for (int p = 0; p < P.npass; ++p) {
         RadixPassArgs A{};
         A.ii_in = p ? bi[(p - 1) & 1] : ii;
@@ -521,16 +524,12 @@ int assemble_radix(sa_ctx *ctx, const RadixPlan &P, const int32_t *ii, const int
         A.N = N;
         A.shift = P.shift[p];
         A.bits = P.bits[p];
-        const bool last = p + 1 == P.npass;
-        A.nshift = last ? 0 : P.shift[p + 1];
-        A.nbits = last ? 0 : P.bits[p + 1];
-        A.hist = ctx->rhist + p * RP_MAXD;
-        A.hist_next = last ? nullptr : ctx->rhist + (p + 1) * RP_MAXD;
-        A.lb = ctx->rlb;
-        A.tag = ep | (unsigned)p;
-        A.pass = p;
+        A.off = ctx->roff;
+        if ((rc = mark(ctx, uname[p]))) return rc;
+        SA_CUDA(ctx, launch_rup(lc, p == 0, A.jj_in, L, N, A.shift, A.bits, ctx->rcnt, ctx->rbsum,
+                                ctx->roff, ctx->err));
         if ((rc = mark(ctx, pname[p]))) return rc;
-        SA_CUDA(ctx, launch_rpass(lc, A, p == 0, P.nchunk, ctx->err));
+        SA_CUDA(ctx, launch_rpass(lc, A, p == 0, nseg, ctx->err));
     }
     const int fb = (P.npass - 1) & 1;  // buffer holding the partitioned triplets
     RadixFoldArgs F{};

@@ -84,7 +84,6 @@ struct ErrState {
     unsigned int lsmall;        // triplets in small columns (small record space)
     unsigned int long_cols;     // some small column is long (> SHORT_COL): the fold's long pass runs
     // radix path (sa_radix.cu)
-    unsigned int rp_ticket[3];  // chunk tickets of the partition passes
     unsigned int rf_ticket;     // sub-bucket tickets of the fold
     unsigned int rbig_n;        // oversize sub-buckets listed by k_rbounds
     unsigned int rvalid;        // triplets with a valid column (partitioned)
@@ -413,13 +412,14 @@ cudaError_t launch_tile_fold(Launch &lc, const uint32_t *sstart, const int2 *til
                              int2 *tile_cnt);
 
 // ---- radix path (sa_radix.cu) -------------------------------------------------
-constexpr int RP_NT = 512;                  // partition pass: threads per CTA
+constexpr int RP_NT = 1024;                 // partition pass: threads per CTA (one CTA per SM)
 constexpr int RP_NW = RP_NT / 32;
-constexpr int RP_IPT = 16;                  // triplets per thread
+constexpr int RP_IPT = 8;                   // triplets per thread
 constexpr int RP_CHUNK = RP_NT * RP_IPT;    // triplets per chunk (CTA)
 constexpr int RP_MAXBITS = 9;               // digit bits per pass
 constexpr int RP_MAXD = 1 << RP_MAXBITS;
 constexpr int RP_MAXPASS = 3;
+constexpr int RP_BLK = 64;                  // chunks per upsweep block
 constexpr int RF_CAP = 4096;                // fold: largest sub-bucket held in shared memory
 constexpr int RF_WMAX = 256;                // fold: columns per sub-bucket (2^w)
 
@@ -431,13 +431,8 @@ struct RadixPassArgs {
     double *s_out;
     int64_t L;
     int32_t M, N;
-    int shift, bits;    // this pass's digit: ((col - 1) >> shift) & (2^bits - 1)
-    int nshift, nbits;  // the next pass's digit (nbits = 0: last pass)
-    const uint32_t *hist;
-    uint32_t *hist_next;
-    unsigned long long *lb;  // look-back words, nchunk x 2^bits
-    unsigned tag;
-    int pass;
+    int shift, bits;          // this pass's digit: ((col - 1) >> shift) & (2^bits - 1)
+    const uint32_t *off;      // nchunk x RP_MAXD: global position of every chunk's digits
 };
 
 struct RadixFoldArgs {
@@ -456,10 +451,9 @@ struct RadixFoldArgs {
     int64_t cap;
 };
 
-cudaError_t launch_rhist(Launch &lc, const int32_t *jj, int64_t L, int32_t N, int shift, int bits,
-                         uint32_t *hist, ErrState *err);
-cudaError_t launch_rpass(Launch &lc, const RadixPassArgs &A, bool first, int64_t nchunk,
-                         ErrState *err);
+cudaError_t launch_rup(Launch &lc, bool first, const int32_t *jj, int64_t L, int32_t N, int shift,
+                       int bits, uint16_t *cnt, uint32_t *bsum, uint32_t *off, ErrState *err);
+cudaError_t launch_rpass(Launch &lc, const RadixPassArgs &A, bool first, int nseg, ErrState *err);
 cudaError_t launch_rbounds(Launch &lc, const int32_t *jj, int w, int32_t nsub, uint32_t *bnd,
                            uint32_t *biglist, ErrState *err);
 cudaError_t launch_rbig(Launch &lc, const RadixFoldArgs &F, ErrState *err);

@@ -10,12 +10,16 @@
 // column block ("sub-bucket", W = 2^w columns, ~3k triplets):
 //
 //   k_init     error state, tickets, digit histograms reset (sa_capi.cu)
-//   k_rhist    histogram of the first pass's digit + column validation
-//   k_rpass    one stable partition pass (onesweep: chunk-local stable rank
-//              by warp match + per-warp running counters, decoupled
-//              look-back per digit across chunks, coalesced scatter through
-//              shared memory), 16 B per triplet in and out; the first pass
-//              validates rows, every pass histograms the next pass's digit
+//   per pass (stable LSD partition on one digit of the column):
+//   k_rup      per-segment digit histograms of the pass input (S contiguous
+//              segments, one per resident partition CTA); the first also
+//              validates the columns
+//   k_rscan    every segment's global base per digit
+//   k_rpass    the partition: CTA s walks its segment's chunks in order
+//              (chunk-local stable rank from per-warp running counters over
+//              digit ballots, a running base per digit in shared memory,
+//              coalesced scatter through shared memory), 16 B per triplet
+//              in and out; the first pass validates the rows
 //   k_rbounds  sub-bucket boundaries in the partitioned arrays (binary search)
 //              and the list of oversize sub-buckets
 //   k_rbig     oversize sub-buckets (> RF_CAP triplets: skewed input), one
@@ -81,237 +85,291 @@ __device__ __forceinline__ unsigned long long ep_walk_warp(const unsigned long l
 }
 
 // ---------------------------------------------------------------------------
-// k_rhist: histogram of the first pass's digit over the valid triplets and
-// column validation (first column index < 1, any index > N).
+// Partition passes without a look-back chain ("reduce, then scan").  The
+// upsweep histograms the pass input chunk by chunk (RP_CHUNK triplets) --
+// one CTA per block of RP_BLK chunks, which also sums its block -- a small
+// scan turns the block sums into every block's global base per digit, and a
+// third kernel turns them into every chunk's base per digit.  The
+// partition CTAs then need no look-back: concurrently running CTAs take
+// adjacent chunks (chunk = CTA + k x grid), so the output digit runs of
+// neighbouring chunks are written at about the same time and L2 completes
+// their sectors before they leave it.  (A decoupled look-back per digit spent
+// a quarter of the pass's instructions spinning; contiguous per-CTA segments
+// without it left ~150k partially written write fronts in L2 and cost 50 %
+// extra DRAM traffic in read-modify-writes.)
 // ---------------------------------------------------------------------------
-constexpr int RH_NT = 256;
-constexpr int RH_U = 8;
+constexpr int RU_NT = 512;
 
-__global__ void __launch_bounds__(RH_NT) k_rhist(const int32_t *__restrict__ jj, int64_t L,
-                                                 int32_t N, int shift, int bits,
-                                                 uint32_t *__restrict__ hist, ErrState *err) {
+// k_rup: per-chunk digit histograms cnt[c][d] (16-bit) of the pass input (jj)
+// and the block's sums bsum[B][d].  The first pass also validates the
+// columns (first index < 1, any index > N) and counts the valid triplets
+// (err->rvalid, the length the later passes read).
+template <bool FIRST>
+__global__ void __launch_bounds__(RU_NT) k_rup(const int32_t *__restrict__ jj, int64_t L, int32_t N,
+                                               int shift, int bits, uint16_t *__restrict__ cnt,
+                                               uint32_t *__restrict__ bsum, ErrState *err) {
     __shared__ uint32_t h[RP_MAXD];
-    for (int k = threadIdx.x; k < RP_MAXD; k += RH_NT) h[k] = 0;
-    __syncthreads();
     pdl_wait();
+    const int64_t Lp = FIRST ? L : (int64_t)*((volatile const unsigned *)&err->rvalid);
+    const int64_t nchunk = (Lp + RP_CHUNK - 1) / RP_CHUNK;
     const unsigned dmask = (1u << bits) - 1u;
+    const int ndig = 1 << bits;
     unsigned long long bad = ~0ull;
-    unsigned over = 0;
-    const int64_t step = (int64_t)gridDim.x * RH_NT * RH_U;
-    for (int64_t t0 = (int64_t)blockIdx.x * RH_NT * RH_U + threadIdx.x; t0 < L; t0 += step) {
-        int v[RH_U];
+    unsigned over = 0, nval = 0;
+    uint32_t bs = 0;  // block sum of digit threadIdx.x
+    const int64_t cb = (int64_t)blockIdx.x * RP_BLK;
+    for (int64_t c = cb; c < min(nchunk, cb + RP_BLK); ++c) {
+        for (int k = threadIdx.x; k < ndig; k += RU_NT) h[k] = 0;
+        __syncthreads();
+        const int64_t lo = c * RP_CHUNK, hi = min(Lp, lo + RP_CHUNK);
+        int v[RP_CHUNK / RU_NT];
 #pragma unroll
-        for (int u = 0; u < RH_U; ++u) {
-            const int64_t t = t0 + (int64_t)u * RH_NT;
-            v[u] = (t < L) ? __ldg(jj + t) : 1;
+        for (int u = 0; u < RP_CHUNK / RU_NT; ++u) {
+            const int64_t t = lo + threadIdx.x + (int64_t)u * RU_NT;
+            v[u] = (t < hi) ? __ldcs(jj + t) : 0;
         }
 #pragma unroll
-        for (int u = 0; u < RH_U; ++u) {
-            const int64_t t = t0 + (int64_t)u * RH_NT;
-            if (t >= L) continue;
-            const int c = v[u];
-            if (c < 1) bad = min(bad, (unsigned long long)t);
-            else if (c > N) over = 1;
-            else atomicAdd(&h[((unsigned)(c - 1) >> shift) & dmask], 1u);
+        for (int u = 0; u < RP_CHUNK / RU_NT; ++u) {
+            const int64_t t = lo + threadIdx.x + (int64_t)u * RU_NT;
+            if (t >= hi) continue;
+            const int cc = v[u];
+            if (FIRST && cc < 1) bad = min(bad, (unsigned long long)t);
+            else if (FIRST && cc > N) over = 1;
+            else {
+                atomicAdd(&h[((unsigned)(cc - 1) >> shift) & dmask], 1u);
+                ++nval;
+            }
         }
+        __syncthreads();
+        for (int k = threadIdx.x; k < ndig; k += RU_NT) {
+            cnt[c * RP_MAXD + k] = (uint16_t)h[k];
+            bs += h[k];  // RU_NT == RP_MAXD: thread k owns digit k
+        }
+        __syncthreads();
     }
-    __syncthreads();
-    for (int k = threadIdx.x; k <= (int)dmask; k += RH_NT)
-        if (h[k]) atomicAdd(&hist[k], h[k]);
+    if (threadIdx.x < ndig) bsum[(int64_t)blockIdx.x * RP_MAXD + threadIdx.x] = bs;
+    if (FIRST) {
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        bad = min(bad, __shfl_xor_sync(FULL, bad, o));
-        over |= __shfl_xor_sync(FULL, over, o);
-    }
-    if ((threadIdx.x & 31) == 0) {
-        if (bad != ~0ull) atomicMin(&err->bad_j, bad);
-        if (over) err->over_n = 1;
+        for (int o = 16; o > 0; o >>= 1) {
+            bad = min(bad, __shfl_xor_sync(FULL, bad, o));
+            over |= __shfl_xor_sync(FULL, over, o);
+            nval += __shfl_xor_sync(FULL, nval, o);
+        }
+        if ((threadIdx.x & 31) == 0) {
+            if (bad != ~0ull) atomicMin(&err->bad_j, bad);
+            if (over) err->over_n = 1;
+            if (nval) atomicAdd(&err->rvalid, nval);
+        }
     }
     pdl_trigger();
 }
 
-// ---------------------------------------------------------------------------
-// k_rpass: one stable LSD partition pass by the digit (col-1) >> shift.
-// A chunk of RP_CHUNK consecutive triplets per CTA (ticket order); warp w
-// owns the chunk's w-th run of RP_IPT x 32 triplets and walks it in order,
-// 32 at a time: __match_any_sync groups equal digits, a per-warp running
-// counter per digit gives every triplet its rank -- stable by construction.
-// A block scan over (digit, warp) makes the ranks chunk-local; a decoupled
-// look-back per digit (one thread each) over the previous chunks gives the
-// chunk's global base per digit.  The triplets are then reordered in shared
-// memory by digit and written out so that consecutive threads write
-// consecutive addresses of one digit run.
-// ---------------------------------------------------------------------------
-struct PassSmem {
-    uint16_t cnt[RP_NW][RP_MAXD];      // per warp and digit: running count, then chunk-local base
-    unsigned long long buf[RP_CHUNK];  // reorder buffer (values, then row << 32 | col)
-    uint16_t sdig[RP_CHUNK];           // digit of the reordered triplet
-    uint32_t cbase[RP_MAXD];           // global position of the digit's chunk-local slot 0
-    uint32_t hnext[RP_MAXD];           // histogram of the next pass's digit
-    uint32_t red[RP_NW];
-    int b;
-};
-
-template <bool FIRST>
-__global__ void __launch_bounds__(RP_NT, 2) k_rpass(RadixPassArgs A, ErrState *err) {
-    extern __shared__ __align__(16) unsigned char rp_smem[];
-    PassSmem &S = *reinterpret_cast<PassSmem *>(rp_smem);
-    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-    const int ndig = 1 << A.bits;
-    const unsigned dmask = (unsigned)ndig - 1u;
-    const unsigned nmask = (1u << A.nbits) - 1u;
-    const unsigned lt = lanemask_lt();
-    {
-        uint32_t *c32 = reinterpret_cast<uint32_t *>(&S.cnt[0][0]);
-        for (int k = tid; k < RP_NW * RP_MAXD / 2; k += RP_NT) c32[k] = 0;
-        for (int k = tid; k < RP_MAXD; k += RP_NT) S.hnext[k] = 0;
-    }
+// k_rscan: bsum[B][d] := (exclusive prefix of the digit totals)[d] + the count
+// of digit d in blocks < B.  One CTA, a thread per digit.
+__global__ void __launch_bounds__(RP_MAXD) k_rscan(uint32_t *__restrict__ bsum, int nblk, int bits) {
+    __shared__ uint32_t red[RP_MAXD / 32];
+    const int d = threadIdx.x;
     pdl_wait();
-    // global start of every digit: exclusive scan of this pass's histogram
-    uint32_t htot;
-    const uint32_t gstart =
-        block_excl_sum<RP_NT, uint32_t>((tid < ndig) ? A.hist[tid] : 0u, S.red, htot);
-    if (tid == 0) S.b = (int)atomicAdd(&err->rp_ticket[A.pass], 1u);
-    __syncthreads();
-    const int64_t b = S.b;
-    const int64_t base = b * RP_CHUNK + (int64_t)w * (RP_IPT * 32) + lane;
-    {  // the chunk's rows and values into L2 now; they are read after the ranking
-        const int64_t c0 = b * RP_CHUNK;
-        const int64_t nrow = max((int64_t)0, min((int64_t)RP_CHUNK, A.L - c0));  // upper bound (Lp <= L)
-        if (A.s_stride) {
-            const char *vb = reinterpret_cast<const char *>(A.s_in + c0);
-            for (int64_t o = (int64_t)tid * 128; o < nrow * 8; o += RP_NT * 128)
-                asm volatile("prefetch.global.L2 [%0];" ::"l"(vb + o));
+    const bool live = d < (1 << bits);
+    uint32_t run = 0;
+    if (live)
+        for (int q = 0; q < nblk; ++q) {
+            const uint32_t c = bsum[(int64_t)q * RP_MAXD + d];
+            bsum[(int64_t)q * RP_MAXD + d] = run;
+            run += c;
         }
-        const char *rb = reinterpret_cast<const char *>(A.ii_in + c0);
-        for (int64_t o = (int64_t)tid * 128; o < nrow * 4; o += RP_NT * 128)
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(rb + o));
-    }
+    uint32_t tot;
+    const uint32_t g = block_excl_sum<RP_MAXD, uint32_t>(live ? run : 0u, red, tot);
+    if (live)
+        for (int q = 0; q < nblk; ++q) bsum[(int64_t)q * RP_MAXD + d] += g;
+    pdl_trigger();
+}
 
-    // passes after the first read the valid triplets the first one wrote
-    const int64_t Lp = FIRST ? A.L : (int64_t)*((volatile const unsigned *)&err->rvalid);
-    int col[RP_IPT];
-#pragma unroll
-    for (int r = 0; r < RP_IPT; ++r) {
-        const int64_t idx = base + r * 32;
-        col[r] = (idx < Lp) ? __ldg(A.jj_in + idx) : 0;
-    }
-    unsigned long long bad = ~0ull;
-    unsigned over = 0, nval = 0;
-    uint32_t rk[RP_IPT / 2];  // ranks, two 16-bit halves per word
-#pragma unroll
-    for (int r = 0; r < RP_IPT; ++r) {
-        const int64_t idx = base + r * 32;
-        const bool live = idx < Lp;
-        const bool valid = live && col[r] >= 1 && col[r] <= A.N;
-        const unsigned c0 = (unsigned)(col[r] - 1);
-        const unsigned d = valid ? ((c0 >> A.shift) & dmask) : (unsigned)ndig;
-        if (A.nbits && valid) atomicAdd(&S.hnext[(c0 >> A.nshift) & nmask], 1u);
-        nval += valid;
-        const unsigned peers = __match_any_sync(FULL, d);
-        unsigned c = 0;
-        if (valid) c = S.cnt[w][d];
-        __syncwarp();
-        if (valid && (peers & lt) == 0u) S.cnt[w][d] = (uint16_t)(c + __popc(peers));
-        __syncwarp();
-        const unsigned rr = c + __popc(peers & lt);
-        if (r & 1) rk[r >> 1] |= rr << 16;
-        else rk[r >> 1] = rr;
-    }
-    __syncthreads();
-    // (digit, warp) digit-major scan: chunk-local base of every warp's run of a digit
-    uint32_t tot = 0;
-    if (tid < ndig) {
-#pragma unroll
-        for (int ww = 0; ww < RP_NW; ++ww) {
-            const uint32_t c = S.cnt[ww][tid];
-            S.cnt[ww][tid] = (uint16_t)tot;
-            tot += c;
+// k_roff: off[c][d] = the global position of chunk c's first digit-d triplet.
+__global__ void __launch_bounds__(RP_MAXD) k_roff(const uint16_t *__restrict__ cnt,
+                                                  const uint32_t *__restrict__ bsum, int bits,
+                                                  uint32_t *__restrict__ off, ErrState *err, int64_t L,
+                                                  int first) {
+    const int d = threadIdx.x;
+    pdl_wait();
+    const int64_t Lp = first ? L : (int64_t)*((volatile const unsigned *)&err->rvalid);
+    const int64_t nchunk = (Lp + RP_CHUNK - 1) / RP_CHUNK;
+    if (d < (1 << bits)) {
+        uint32_t run = bsum[(int64_t)blockIdx.x * RP_MAXD + d];
+        const int64_t cb = (int64_t)blockIdx.x * RP_BLK;
+        for (int64_t c = cb; c < min(nchunk, cb + RP_BLK); ++c) {
+            off[c * RP_MAXD + d] = run;
+            run += cnt[c * RP_MAXD + d];
         }
-    }
-    uint32_t ctot;
-    const uint32_t dstart = block_excl_sum<RP_NT, uint32_t>(tot, S.red, ctot);
-    if (tid < ndig) {
-#pragma unroll
-        for (int ww = 0; ww < RP_NW; ++ww) S.cnt[ww][tid] = (uint16_t)(S.cnt[ww][tid] + dstart);
-        // decoupled look-back of this digit's count across the chunks
-        volatile unsigned long long *vlb = A.lb + b * ndig;
-        unsigned long long excl = 0;
-        if (b == 0) {
-            vlb[tid] = ep_pack(A.tag, 2, tot);
-        } else {
-            vlb[tid] = ep_pack(A.tag, 1, tot);
-            const volatile unsigned long long *p = A.lb + (b - 1) * ndig + tid;
-            while (true) {
-                unsigned long long wd;
-                unsigned f;
-                do {
-                    wd = *p;
-                    f = ep_flag(wd, A.tag);
-                } while (f == 0);
-                excl += wd & EP_VMASK;
-                if (f == 2) break;
-                p -= ndig;
-            }
-            vlb[tid] = ep_pack(A.tag, 2, excl + tot);
-        }
-        S.cbase[tid] = (uint32_t)(gstart + excl) - dstart;
-    }
-    __syncthreads();
-    // values -> reorder buffer
-#pragma unroll
-    for (int r = 0; r < RP_IPT; ++r) {
-        const int64_t idx = base + r * 32;
-        const bool valid = idx < Lp && col[r] >= 1 && col[r] <= A.N;
-        if (valid) {
-            const unsigned d = ((unsigned)(col[r] - 1) >> A.shift) & dmask;
-            const unsigned pos = S.cnt[w][d] + ((rk[r >> 1] >> ((r & 1) * 16)) & 0xffffu);
-            S.buf[pos] = (unsigned long long)__double_as_longlong(__ldg(A.s_in + idx * A.s_stride));
-            S.sdig[pos] = (uint16_t)d;
-        }
-    }
-    __syncthreads();
-    for (int k = tid; k < (int)ctot; k += RP_NT)
-        A.s_out[S.cbase[S.sdig[k]] + (uint32_t)k] = __longlong_as_double((long long)S.buf[k]);
-    __syncthreads();
-#pragma unroll
-    for (int r = 0; r < RP_IPT; ++r) {  // rows (re-read: the chunk is still in L2), validated once
-        const int64_t idx = base + r * 32;
-        const bool live = idx < Lp;
-        const int row = live ? __ldg(A.ii_in + idx) : 1;
-        if (FIRST && live) {
-            if (row < 1) bad = min(bad, (unsigned long long)idx);
-            else if (row > A.M) over = 1;
-        }
-        if (live && col[r] >= 1 && col[r] <= A.N) {
-            const unsigned d = ((unsigned)(col[r] - 1) >> A.shift) & dmask;
-            const unsigned pos = S.cnt[w][d] + ((rk[r >> 1] >> ((r & 1) * 16)) & 0xffffu);
-            S.buf[pos] = ((unsigned long long)(uint32_t)row << 32) | (uint32_t)col[r];
-        }
-    }
-    __syncthreads();
-    for (int k = tid; k < (int)ctot; k += RP_NT) {
-        const unsigned long long v = S.buf[k];
-        const uint32_t o = S.cbase[S.sdig[k]] + (uint32_t)k;
-        A.ii_out[o] = (int32_t)(v >> 32);
-        A.jj_out[o] = (int32_t)(uint32_t)v;
     }
     pdl_trigger();
-    if (A.nbits)
-        for (int k = tid; k <= (int)nmask; k += RP_NT)
-            if (S.hnext[k]) atomicAdd(&A.hist_next[k], S.hnext[k]);
+}
+
+// L2 eviction priority "last" for the partition's output stores: a digit run
+// of a chunk fills only part of a sector, the neighbouring chunk's run the
+// rest; keeping the lines in L2 until both arrive avoids a DRAM
+// read-modify-write of the sector.
+__device__ __forceinline__ unsigned long long l2_evict_last() {
+    unsigned long long p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ void st_last(int32_t *a, int32_t v, unsigned long long pol) {
+    asm volatile("st.global.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(a), "r"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void st_last(double *a, double v, unsigned long long pol) {
+    asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(a), "d"(v), "l"(pol) : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// k_rpass: one stable LSD partition pass by the digit (col-1) >> shift (the
+// downsweep).  CTA s walks the RP_CHUNK-triplet chunks of segment s in order;
+// warp w owns the chunk's w-th run of RP_IPT x 32 triplets.  All of a
+// thread's triplets (row, column, value) are loaded up front.  The warp walks
+// its run in order, 32 at a time: lanes of equal digit are found by one
+// ballot per digit bit, and a per-warp running counter per digit (a shared
+// atomic by the group's first lane) gives every triplet its rank -- stable by
+// construction.  A scan over (digit, warp) makes the ranks chunk-local; the
+// segment's running base per digit places the chunk.  Each triplet is then
+// put, as one 16-byte record with its output index, at its sorted slot in
+// shared memory, and the chunk is written out so that consecutive threads
+// write consecutive addresses of one digit run.
+// ---------------------------------------------------------------------------
+struct PassSmem {
+    uint4 rec[RP_CHUNK];              // reordered {row, col, value}
+    uint32_t oidx[RP_CHUNK];          // output index of reordered slot k
+    uint32_t cnt[RP_NW][RP_MAXD / 2]; // per warp, digit pair (16-bit halves): running count, then base
+    uint32_t dtot[RP_MAXD];           // digit totals of the chunk
+    uint32_t run[RP_MAXD];            // the chunk's global base per digit
+    uint32_t red[RP_NW];
+};
+
+template <bool FIRST, int BITS>
+__global__ void __launch_bounds__(RP_NT, 1) k_rpass(RadixPassArgs A, ErrState *err) {
+    extern __shared__ __align__(16) unsigned char rp_smem[];
+    PassSmem &S = *reinterpret_cast<PassSmem *>(rp_smem);
+    constexpr int ndig = 1 << BITS;
+    constexpr unsigned dmask = (unsigned)ndig - 1u;
+    constexpr int npair = (ndig + 1) >> 1;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const unsigned lt = lanemask_lt();
+    pdl_wait();
+    // passes after the first read the valid triplets the first one wrote
+    const int64_t Lp = FIRST ? A.L : (int64_t)*((volatile const unsigned *)&err->rvalid);
+    const int64_t nchunk = (Lp + RP_CHUNK - 1) / RP_CHUNK;
+    const int shift = A.shift;
+    const int32_t M = A.M, N = A.N;
+    unsigned long long bad = ~0ull;
+    unsigned over = 0;
+    for (int64_t c = blockIdx.x; c < nchunk; c += gridDim.x) {
+        const int64_t c0 = c * RP_CHUNK;
+        const int64_t seg_hi = min(Lp, c0 + RP_CHUNK);
+        {
+            uint32_t *c32 = &S.cnt[0][0];
+            for (int k = tid; k < RP_NW * npair; k += RP_NT) c32[(k / npair) * (RP_MAXD / 2) + k % npair] = 0;
+            for (int k = tid; k < ndig; k += RP_NT) S.run[k] = A.off[c * RP_MAXD + k];
+        }
+        const int64_t base = c0 + (int64_t)w * (RP_IPT * 32) + lane;
+        const int nlive = (int)max((int64_t)0, min((int64_t)(RP_IPT * 32), seg_hi - (base - lane)));  // warp-uniform
+        const int32_t *jp = A.jj_in + base, *ip = A.ii_in + base;
+        const double *sp = A.s_in + (A.s_stride ? base : 0);
+        const int sstep = A.s_stride ? 32 : 0;
+        int col[RP_IPT], row[RP_IPT];
+        double val[RP_IPT];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        bad = min(bad, __shfl_xor_sync(FULL, bad, o));
-        over |= __shfl_xor_sync(FULL, over, o);
-        nval += __shfl_xor_sync(FULL, nval, o);
+        for (int r = 0; r < RP_IPT; ++r) {
+            const bool live = r * 32 + lane < nlive;
+            // streaming loads (evict-first): the input must not push the
+            // partially written output lines out of L2
+            col[r] = live ? __ldcs(jp + r * 32) : 0;
+            row[r] = live ? __ldcs(ip + r * 32) : 1;
+            val[r] = live ? __ldcs(sp + r * sstep) : 0.0;
+        }
+        __syncthreads();  // counters cleared (and the previous chunk's buffers drained)
+        uint32_t rk[RP_IPT / 2];  // ranks: two 16-bit halves per word
+#pragma unroll
+        for (int r = 0; r < RP_IPT; ++r) {
+            const bool live = r * 32 + lane < nlive;
+            if (FIRST && live) {
+                if (row[r] < 1) bad = min(bad, (unsigned long long)(base + r * 32));
+                else if (row[r] > M) over = 1;
+            }
+            const bool valid = live && (unsigned)(col[r] - 1) < (unsigned)N;
+            const unsigned d = ((unsigned)(col[r] - 1) >> shift) & dmask;
+            // lanes with the same digit: one ballot per digit bit
+            // (__match_any_sync runs on the slow ADU pipe)
+            unsigned peers = __ballot_sync(FULL, valid);
+#pragma unroll
+            for (int i = 0; i < BITS; ++i) {
+                const unsigned bb = __ballot_sync(FULL, (d >> i) & 1u);
+                peers &= bb ^ (((d >> i) & 1u) - 1u);  // bit set: bb; clear: ~bb
+            }
+            // rank = the warp's running count of digit d (returned by the
+            // group's first lane's shared atomic; one warp's shared atomics
+            // complete in program order)
+            const int leader = __ffs(peers) - 1;
+            const unsigned sh = (d & 1u) * 16u;
+            unsigned old = 0;
+            if (lane == leader && valid) old = atomicAdd(&S.cnt[w][d >> 1], (unsigned)__popc(peers) << sh);
+            const unsigned rr = ((__shfl_sync(FULL, old, leader & 31) >> sh) & 0xffffu) + __popc(peers & lt);
+            if (r & 1) rk[r >> 1] |= rr << 16;
+            else rk[r >> 1] = rr;
+        }
+        __syncthreads();
+        // (digit, warp) digit-major scan: thread t owns the digit pair (2t, 2t+1)
+        uint32_t t0 = 0, t1 = 0;
+        if (tid < npair) {
+#pragma unroll 8
+            for (int ww = 0; ww < RP_NW; ++ww) {
+                const uint32_t c = S.cnt[ww][tid];
+                S.cnt[ww][tid] = t0 | (t1 << 16);
+                t0 += c & 0xffffu;
+                t1 += c >> 16;
+            }
+        }
+        uint32_t ctot;
+        const uint32_t ex = block_excl_sum<RP_NT, uint32_t>(t0 + t1, S.red, ctot);
+        if (tid < npair) {
+            const uint32_t add = ex | ((ex + t0) << 16);  // chunk-local starts of digits 2t, 2t+1
+#pragma unroll 8
+            for (int ww = 0; ww < RP_NW; ++ww) S.cnt[ww][tid] += add;
+            // global position of chunk-local slot 0 of each digit: run - local start
+            S.run[2 * tid] -= ex;
+            if (2 * tid + 1 < ndig) S.run[2 * tid + 1] -= ex + t0;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int r = 0; r < RP_IPT; ++r) {  // records to their sorted slots
+            if (r * 32 + lane < nlive && (unsigned)(col[r] - 1) < (unsigned)N) {
+                const unsigned d = ((unsigned)(col[r] - 1) >> shift) & dmask;
+                const unsigned pos = ((S.cnt[w][d >> 1] >> ((d & 1u) * 16u)) & 0xffffu) +
+                                     ((rk[r >> 1] >> ((r & 1) * 16)) & 0xffffu);
+                const unsigned long long vb = (unsigned long long)__double_as_longlong(val[r]);
+                S.rec[pos] = make_uint4((uint32_t)row[r], (uint32_t)col[r], (uint32_t)vb, (uint32_t)(vb >> 32));
+                S.oidx[pos] = S.run[d] + pos;
+            }
+        }
+        __syncthreads();
+        const unsigned long long pol = l2_evict_last();
+        for (int k = tid; k < (int)ctot; k += RP_NT) {
+            const uint4 v = S.rec[k];
+            const uint32_t o = S.oidx[k];
+            st_last(A.ii_out + o, (int32_t)v.x, pol);
+            st_last(A.jj_out + o, (int32_t)v.y, pol);
+            st_last(A.s_out + o, __longlong_as_double((long long)(((unsigned long long)v.w << 32) | v.z)), pol);
+        }
     }
-    if (lane == 0) {
-        if (FIRST) {
+    pdl_trigger();
+    if (FIRST) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            bad = min(bad, __shfl_xor_sync(FULL, bad, o));
+            over |= __shfl_xor_sync(FULL, over, o);
+        }
+        if (lane == 0) {
             if (bad != ~0ull) atomicMin(&err->bad_i, bad);
             if (over) err->over_m = 1;
         }
-        if (A.pass == 0 && nval) atomicAdd(&err->rvalid, nval);
     }
 }
 
@@ -758,26 +816,54 @@ __global__ void __launch_bounds__(RF_NT, 2) k_rfold(RadixFoldArgs F, ErrState *e
 }
 
 // ---- launchers -----------------------------------------------------------------
-cudaError_t launch_rhist(Launch &lc, const int32_t *jj, int64_t L, int32_t N, int shift, int bits,
-                         uint32_t *hist, ErrState *err) {
-    if (L <= 0) return cudaSuccess;
-    const int64_t want = (L + RH_NT * RH_U - 1) / (RH_NT * RH_U);
-    const int grid = (int)std::min<int64_t>(want, (int64_t)lc.num_sms * 8);
-    cudaError_t e = launch_pdl(k_rhist, dim3(grid), dim3(RH_NT), 0, lc.stream, jj, L, N, shift, bits,
-                               hist, err);
+cudaError_t launch_rup(Launch &lc, bool first, const int32_t *jj, int64_t L, int32_t N, int shift,
+                       int bits, uint16_t *cnt, uint32_t *bsum, uint32_t *off, ErrState *err) {
+    // grid sized for L (an upper bound of the valid count the later passes read)
+    const int64_t nchunk = (L + RP_CHUNK - 1) / RP_CHUNK;
+    const int nblk = (int)std::max<int64_t>(1, (nchunk + RP_BLK - 1) / RP_BLK);
+    cudaError_t e = first ? launch_pdl(k_rup<true>, dim3((unsigned)nblk), dim3(RU_NT), 0, lc.stream, jj, L,
+                                       N, shift, bits, cnt, bsum, err)
+                          : launch_pdl(k_rup<false>, dim3((unsigned)nblk), dim3(RU_NT), 0, lc.stream, jj, L,
+                                       N, shift, bits, cnt, bsum, err);
+    lc.launches++;
+    if (e != cudaSuccess) return e;
+    e = launch_pdl(k_rscan, dim3(1), dim3(RP_MAXD), 0, lc.stream, bsum, nblk, bits);
+    lc.launches++;
+    if (e != cudaSuccess) return e;
+    e = launch_pdl(k_roff, dim3((unsigned)nblk), dim3(RP_MAXD), 0, lc.stream, (const uint16_t *)cnt,
+                   (const uint32_t *)bsum, bits, off, err, L, first ? 1 : 0);
     lc.launches++;
     return e;
 }
 
-cudaError_t launch_rpass(Launch &lc, const RadixPassArgs &A, bool first, int64_t nchunk,
-                         ErrState *err) {
-    if (nchunk <= 0) return cudaSuccess;
+template <bool FIRST, int BITS>
+static cudaError_t launch_rpass_t(Launch &lc, const RadixPassArgs &A, int nseg, ErrState *err) {
     const int smem = (int)sizeof(PassSmem);
-    cudaError_t e = first ? ensure_smem_attr((const void *)k_rpass<true>, smem)
-                          : ensure_smem_attr((const void *)k_rpass<false>, smem);
+    cudaError_t e = ensure_smem_attr((const void *)k_rpass<FIRST, BITS>, smem);
     if (e != cudaSuccess) return e;
-    e = first ? launch_pdl(k_rpass<true>, dim3((unsigned)nchunk), dim3(RP_NT), smem, lc.stream, A, err)
-              : launch_pdl(k_rpass<false>, dim3((unsigned)nchunk), dim3(RP_NT), smem, lc.stream, A, err);
+    return launch_pdl(k_rpass<FIRST, BITS>, dim3((unsigned)nseg), dim3(RP_NT), smem, lc.stream, A, err);
+    // (nseg = the number of resident partition CTAs; they walk the chunks with stride nseg)
+}
+
+template <bool FIRST>
+static cudaError_t launch_rpass_b(Launch &lc, const RadixPassArgs &A, int nseg, ErrState *err) {
+    switch (A.bits) {  // the digit width is a compile-time constant of the kernel
+        case 0: return launch_rpass_t<FIRST, 0>(lc, A, nseg, err);
+        case 1: return launch_rpass_t<FIRST, 1>(lc, A, nseg, err);
+        case 2: return launch_rpass_t<FIRST, 2>(lc, A, nseg, err);
+        case 3: return launch_rpass_t<FIRST, 3>(lc, A, nseg, err);
+        case 4: return launch_rpass_t<FIRST, 4>(lc, A, nseg, err);
+        case 5: return launch_rpass_t<FIRST, 5>(lc, A, nseg, err);
+        case 6: return launch_rpass_t<FIRST, 6>(lc, A, nseg, err);
+        case 7: return launch_rpass_t<FIRST, 7>(lc, A, nseg, err);
+        case 8: return launch_rpass_t<FIRST, 8>(lc, A, nseg, err);
+        case 9: return launch_rpass_t<FIRST, 9>(lc, A, nseg, err);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+cudaError_t launch_rpass(Launch &lc, const RadixPassArgs &A, bool first, int nseg, ErrState *err) {
+    cudaError_t e = first ? launch_rpass_b<true>(lc, A, nseg, err) : launch_rpass_b<false>(lc, A, nseg, err);
     lc.launches++;
     return e;
 }
