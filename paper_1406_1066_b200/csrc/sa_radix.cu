@@ -509,13 +509,15 @@ __global__ void __launch_bounds__(BIG_NT, 1) k_rbig(RadixFoldArgs F, ErrState *e
 //      members sorted by k (insertion sort, <= 32) and folded from +0.0;
 //      ir / pr / jc written coalesced.
 // ---------------------------------------------------------------------------
-constexpr int RF_NT = 256;
+constexpr int RF_NT = 512;
 constexpr int RF_HS = 2 * RF_CAP;
 constexpr int RF_BIGG = 128;  // groups of > 32 members per sub-bucket (<= RF_CAP / 33)
 
 struct FoldSmem {
-    uint32_t key[RF_HS];          // hash keys (key + 1; 0 = empty); sort items in the fallback
-    uint32_t cnt[RF_HS];          // members per slot, then member cursor
+    uint32_t key[RF_HS];          // hash keys (key + 1; 0 = empty); then the column lists' keys
+                                  // (ckey), or the fallback's sort items
+    uint32_t cnt2[RF_HS / 2];     // per slot (16-bit halves): members, then member cursor
+    uint32_t gkey[RF_CAP];        // key + 1 of group g
     uint16_t gid[RF_CAP];         // slot of record k; then: group of output entry p
     uint16_t memb[RF_CAP];        // member records, grouped
     uint16_t glist[RF_CAP];       // slot of group g
@@ -626,10 +628,8 @@ __global__ void __launch_bounds__(RF_NT, 2) k_rfold(RadixFoldArgs F, ErrState *e
     int hbits = 6;
     while ((1u << hbits) < 2 * n) ++hbits;
     const int hs = 1 << hbits;
-    for (int k = tid; k < hs; k += RF_NT) {
-        S.key[k] = 0u;
-        S.cnt[k] = 0;
-    }
+    for (int k = tid; k < hs; k += RF_NT) S.key[k] = 0u;
+    for (int k = tid; k < hs / 2; k += RF_NT) S.cnt2[k] = 0u;
     for (int c = tid; c <= ncol; c += RF_NT) S.colst[c] = 0;
     if (tid == 0) {
         S.U = 0;
@@ -655,9 +655,11 @@ __global__ void __launch_bounds__(RF_NT, 2) k_rfold(RadixFoldArgs F, ErrState *e
             bool fresh;
             const unsigned h = rf_insert(S.key, hbits, kk[u], fresh);
             S.gid[k] = (uint16_t)h;
-            atomicAdd(&S.cnt[h], 1u);
+            atomicAdd(&S.cnt2[h >> 1], 1u << ((h & 1u) * 16u));
             if (fresh) {
-                S.glist[atomicAdd(&S.U, 1)] = (uint16_t)h;
+                const int g = atomicAdd(&S.U, 1);
+                S.glist[g] = (uint16_t)h;
+                S.gkey[g] = kk[u];
                 atomicAdd(&S.colst[(kk[u] - 1u) >> F.rbits], 1u);
             }
         }
@@ -667,32 +669,38 @@ __global__ void __launch_bounds__(RF_NT, 2) k_rfold(RadixFoldArgs F, ErrState *e
     if (tid == 0) ((volatile unsigned long long *)lbs)[0] = ep_pack(F.tag, s == 0 ? 2 : 1, (unsigned)U);
 
     // ---- 2. member starts, column starts ------------------------------------
-    {  // exclusive scan of the member counts in group order -> gstart
+    {  // exclusive scan of the member counts in group order -> gstart; the slot's
+       // count becomes its member cursor
         const int g0 = tid * RIPT;
         uint32_t loc[RIPT], sum = 0;
 #pragma unroll
         for (int u = 0; u < RIPT; ++u) {
-            loc[u] = (g0 + u < U) ? S.cnt[S.glist[g0 + u]] : 0u;
+            loc[u] = 0u;
+            if (g0 + u < U) {
+                const unsigned h = S.glist[g0 + u];
+                loc[u] = (S.cnt2[h >> 1] >> ((h & 1u) * 16u)) & 0xffffu;
+            }
             sum += loc[u];
         }
         uint32_t tot;
         uint32_t pre = block_excl_sum<RF_NT, uint32_t>(sum, S.red, tot);
 #pragma unroll
         for (int u = 0; u < RIPT; ++u) {
-            if (g0 + u < U) S.gstart[g0 + u] = (uint16_t)pre;
+            const int g = g0 + u;
+            if (g < U) {
+                S.gstart[g] = (uint16_t)pre;
+                const unsigned h = S.glist[g], sh = (h & 1u) * 16u;
+                atomicAnd(&S.cnt2[h >> 1], ~(0xffffu << sh));
+                atomicOr(&S.cnt2[h >> 1], pre << sh);
+                if (loc[u] > 32u) {
+                    const int q = atomicAdd(&S.nbigg, 1);
+                    if (q < RF_BIGG) S.bigg[q] = (uint16_t)g;
+                }
+            }
             pre += loc[u];
         }
     }
     smem_excl_scan<RF_NT, 1, uint32_t>(S.colst, ncol, S.red);
-    for (int g = tid; g < U; g += RF_NT) {
-        const unsigned h = S.glist[g];
-        const int m = S.cnt[h];
-        S.cnt[h] = S.gstart[g];  // member cursor
-        if (m > 32) {
-            const int q = atomicAdd(&S.nbigg, 1);
-            if (q < RF_BIGG) S.bigg[q] = (uint16_t)g;
-        }
-    }
     for (int c = tid; c < ncol; c += RF_NT) S.colcur[c] = S.colst[c];
     if (tid == 0) {
         S.gstart[U] = (uint16_t)n;
@@ -700,14 +708,20 @@ __global__ void __launch_bounds__(RF_NT, 2) k_rfold(RadixFoldArgs F, ErrState *e
     }
     __syncthreads();
     // ---- 3. members (unordered), groups per column ---------------------------------
+    uint32_t *ckey = S.key;  // the hash table is dead: column lists' keys
 #pragma unroll
     for (int u = 0; u < RIPT; ++u) {
         const uint32_t k = tid + u * RF_NT;
-        if (k < n) S.memb[atomicAdd(&S.cnt[S.gid[k]], 1u)] = (uint16_t)k;
+        if (k < n) {
+            const unsigned h = S.gid[k], sh = (h & 1u) * 16u;
+            S.memb[(atomicAdd(&S.cnt2[h >> 1], 1u << sh) >> sh) & 0xffffu] = (uint16_t)k;
+        }
     }
     for (int g = tid; g < U; g += RF_NT) {
-        const uint32_t cl = (S.key[S.glist[g]] - 1u) >> F.rbits;
-        S.ord[atomicAdd(&S.colcur[cl], 1u)] = (uint16_t)g;  // column lists (unordered)
+        const uint32_t kx = S.gkey[g];
+        const uint32_t q = atomicAdd(&S.colcur[(kx - 1u) >> F.rbits], 1u);
+        S.ord[q] = (uint16_t)g;  // column lists (unordered)
+        ckey[q] = kx;
     }
     __syncthreads();
     for (int q = warp; q < min(S.nbigg, RF_BIGG); q += RF_NT / 32) {  // big groups: rebuilt in order
@@ -729,20 +743,20 @@ __global__ void __launch_bounds__(RF_NT, 2) k_rfold(RadixFoldArgs F, ErrState *e
         const int g = tid + u * RF_NT;
         opos[u] = 0;
         if (g < U) {
-            const uint32_t kx = S.key[S.glist[g]];
-            const int st = S.colst[(kx - 1u) >> F.rbits], en = S.colst[((kx - 1u) >> F.rbits) + 1];
+            const uint32_t kx = S.gkey[g];
+            const uint32_t cl = (kx - 1u) >> F.rbits;
+            const int st = S.colst[cl], en = S.colst[cl + 1];
             if (en - st > 64) {
                 S.sortall = 1;
             } else {
                 int r = st;
-                for (int q = st; q < en; ++q) r += S.key[S.glist[S.ord[q]]] < kx;
+                for (int q = st; q < en; ++q) r += ckey[q] < kx;
                 opos[u] = (uint16_t)r;
             }
         }
     }
     __syncthreads();
     const bool sortall = S.sortall != 0;
-    unsigned long long *items = reinterpret_cast<unsigned long long *>(S.key);  // fallback only
     if (!sortall) {
 #pragma unroll
         for (int u = 0; u < RIPT; ++u) {
@@ -750,20 +764,11 @@ __global__ void __launch_bounds__(RF_NT, 2) k_rfold(RadixFoldArgs F, ErrState *e
             if (g < U) S.gid[opos[u]] = (uint16_t)g;  // gid := group of output entry
         }
     } else {  // CTA bitonic sort of all groups by key (a column with > 64 distinct rows)
+        unsigned long long *items = reinterpret_cast<unsigned long long *>(S.key);
         int np2 = 1;
         while (np2 < U) np2 <<= 1;
-        unsigned long long it[RIPT];
-#pragma unroll
-        for (int u = 0; u < RIPT; ++u) {
-            const int g = tid + u * RF_NT;
-            it[u] = (g < U) ? (((unsigned long long)S.key[S.glist[g]] << 16) | (unsigned)g) : ~0ull;
-        }
-        __syncthreads();
-#pragma unroll
-        for (int u = 0; u < RIPT; ++u) {
-            const int g = tid + u * RF_NT;
-            if (g < np2) items[g] = it[u];
-        }
+        for (int g = tid; g < np2; g += RF_NT)
+            items[g] = (g < U) ? (((unsigned long long)S.gkey[g] << 16) | (unsigned)g) : ~0ull;
         __syncthreads();
         for (int k = 2; k <= np2; k <<= 1) {
             for (int j = k >> 1; j > 0; j >>= 1) {
@@ -794,7 +799,7 @@ __global__ void __launch_bounds__(RF_NT, 2) k_rfold(RadixFoldArgs F, ErrState *e
     for (int p = tid; p < U; p += RF_NT) {
         const int g = S.gid[p];
         const int st = S.gstart[g], en = S.gstart[g + 1];
-        const uint32_t kx = sortall ? (uint32_t)(items[p] >> 16) : S.key[S.glist[g]];
+        const uint32_t kx = S.gkey[g];
         if (en - st <= 32) rf_isort16(S.memb + st, en - st);
         double acc = 0.0;
         for (int q = st; q < en; ++q) acc = fold_add(acc, __ldg(sv + S.memb[q]));
