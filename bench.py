@@ -405,13 +405,22 @@ def main():
     # (received triplets are few for the element-ordered meshes)
     nl = shard_info["nnz_local"] if shard else nnz
     Nl = shard_info["n_local"] if shard else N
+    Lv = L  # valid triplets (every index is valid in the BASELINE workloads)
     alg = {
+        # column-cursor pipeline (sa_kernels.cu, sa_tile.cu)
         "k_init": 4 * (Nl + 1),
         "k_colcount": 4 * L,
         "k_col_scan": 8 * Nl,
         "k_scatter": 16 * L,
         "k_bigcol": 0,
         "k_tile_fold": 16 * L + 8 * Nl + 12 * nl + 4 * (Nl + 1),
+        # column-block radix path (sa_radix.cu): per pass an upsweep over the
+        # columns and a 16 B in / 16 B out partition; the fold reads every
+        # partitioned triplet once and writes the CSC
+        "k_rup0": 4 * L, "k_rup1": 4 * Lv, "k_rup2": 4 * Lv,
+        "k_rpass0": 32 * Lv, "k_rpass1": 32 * Lv, "k_rpass2": 32 * Lv,
+        "k_rbounds": 0, "k_rbig": 0,
+        "k_rfold": 16 * Lv + 12 * nl + 4 * (Nl + 1),
     }
     peak_gbs, peak_kind = _peaks()
     dom_gbs = alg.get(dom, 0) / (kern_ms[dom] * 1e-3) / 1e9

@@ -9,6 +9,7 @@
 #include <map>
 #include <mutex>
 #include <string>
+#include <tuple>
 #include <unordered_map>
 #include <vector>
 
@@ -74,8 +75,10 @@ struct sa_ctx {
     int opt_fold_staged = -1;
     int opt_scatter_staged = -1;
     int opt_path = -1;
+    std::map<std::tuple<const void *, int64_t, int32_t, int32_t>, bool> path_cache;  // choose_radix
 
     int64_t host_L = -1;
+    int host_radix = -1;  // path choice made at sa_host_upload from the host columns
     int64_t host_stride = 1;
     int32_t host_N = 0;
     int64_t host_nnz = -1;
@@ -566,13 +569,73 @@ int assemble_radix(sa_ctx *ctx, const RadixPlan &P, const int32_t *ii, const int
     return SA_OK;
 }
 
+// ---- path choice -----------------------------------------------------------------
+// The column-cursor pipeline wins when consecutive triplets touch nearby
+// columns (element-ordered FEM input: its scatter write front and its value
+// gathers stay in L2); the radix path wins when they do not (shuffled input:
+// cfg4 70.7 vs 25.7 ms; cfg2 0.32 vs 1.1 ms the other way).  The choice looks
+// at RADIX_WIN windows of RADIX_WLEN consecutive column indices spread over
+// the input: the median number of distinct 64-column blocks per window.
+// The sample costs one small synchronous copy, so the decision is cached per
+// (input pointer, L, M, N): re-assembling the same buffers reuses it (a stale
+// choice after the caller rewrites the buffers only costs speed -- both paths
+// give the same bits).
+constexpr int64_t RADIX_MIN_L = 1 << 21;
+constexpr int RADIX_WIN = 8;
+constexpr int RADIX_WLEN = 1024;
+constexpr int RADIX_BLOCKS = RADIX_WLEN / 4;  // more distinct blocks per window: no locality
+
+int64_t window_at(int64_t L, int wdx) {
+    return std::max<int64_t>(0, std::min<int64_t>(L - RADIX_WLEN, L * (2 * wdx + 1) / (2 * RADIX_WIN)));
+}
+bool sample_says_radix(const std::vector<int32_t> &smp);
+
+int choose_radix(sa_ctx *ctx, const int32_t *jj, int64_t L, int32_t M, int32_t N, bool &radix) {
+    const std::tuple<const void *, int64_t, int32_t, int32_t> key{jj, L, M, N};
+    auto it = ctx->path_cache.find(key);
+    if (it != ctx->path_cache.end()) {
+        radix = it->second;
+        return SA_OK;
+    }
+    std::vector<int32_t> smp((size_t)RADIX_WIN * RADIX_WLEN);
+    for (int wdx = 0; wdx < RADIX_WIN; ++wdx)
+        SA_CUDA(ctx, cudaMemcpyAsync(smp.data() + (size_t)wdx * RADIX_WLEN, jj + window_at(L, wdx),
+                                     RADIX_WLEN * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    SA_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    radix = sample_says_radix(smp);
+    if (ctx->path_cache.size() > 64) ctx->path_cache.clear();
+    ctx->path_cache[key] = radix;
+    return SA_OK;
+}
+
+bool sample_says_radix(const std::vector<int32_t> &smp) {
+    std::vector<int> distinct(RADIX_WIN);
+    for (int wdx = 0; wdx < RADIX_WIN; ++wdx) {
+        std::vector<int32_t> b(smp.begin() + (size_t)wdx * RADIX_WLEN, smp.begin() + (size_t)(wdx + 1) * RADIX_WLEN);
+        for (auto &x : b) x >>= 6;
+        std::sort(b.begin(), b.end());
+        distinct[wdx] = (int)(std::unique(b.begin(), b.end()) - b.begin());
+    }
+    std::nth_element(distinct.begin(), distinct.begin() + RADIX_WIN / 2, distinct.end());
+    return distinct[RADIX_WIN / 2] > RADIX_BLOCKS;
+}
+
 // The assembly pipeline over a segment table (Ltot triplets in total).
 int assemble_segments(sa_ctx *ctx, const Segs &S, int64_t L, int32_t M, int32_t N, int32_t *d_jc,
                       int32_t *d_ir, double *d_pr, int64_t cap) {
     SA_CUDA(ctx, cudaSetDevice(ctx->device));
     if (S.nseg == 1 && L > 0 && N > 0 && M > 0 && ctx->opt_path != 0) {
         const RadixPlan P = radix_plan(L, M, N);
-        if (P.ok && ctx->opt_path == 1)
+        bool radix = P.ok && ctx->opt_path == 1;
+        if (P.ok && ctx->opt_path == -1 && L >= RADIX_MIN_L) {
+            if (S.jj[0] == ctx->h_jj && ctx->host_radix >= 0) {
+                radix = ctx->host_radix == 1;  // host protocol: chosen at upload
+            } else {
+                int rc = choose_radix(ctx, S.jj[0], L, M, N, radix);
+                if (rc) return rc;
+            }
+        }
+        if (radix)
             return assemble_radix(ctx, P, S.ii[0], S.jj[0], S.s[0], S.stride[0], L, M, N, d_jc, d_ir,
                                   d_pr, cap);
     }
@@ -736,6 +799,13 @@ int sa_host_upload(sa_ctx *ctx, const int32_t *h_ii, const int32_t *h_jj, const 
     ctx->host_nnz = -1;
     ctx->host_L = L;
     ctx->host_stride = s_stride;
+    ctx->host_radix = -1;
+    if (L >= RADIX_MIN_L) {  // the path choice from the host copy of the columns
+        std::vector<int32_t> smp((size_t)RADIX_WIN * RADIX_WLEN);
+        for (int wdx = 0; wdx < RADIX_WIN; ++wdx)
+            memcpy(smp.data() + (size_t)wdx * RADIX_WLEN, h_jj + window_at(L, wdx), RADIX_WLEN * 4);
+        ctx->host_radix = sample_says_radix(smp) ? 1 : 0;
+    }
     const size_t nl = (size_t)std::max<int64_t>(L, 1);
     const size_t ns = s_stride ? nl : 1;
     SA_CUDA(ctx, ensure(ctx->h_ii, ctx->hii_cap, nl));

@@ -598,14 +598,18 @@ def test_cli_assemble_verify_bench(tmp_path, monkeypatch, capsys):
 
 
 @pytest.mark.parametrize("opt,val", [("FOLD_STAGED", 0), ("FOLD_STAGED", 1),
-                                     ("SCATTER_STAGED", 0), ("SCATTER_STAGED", 1)])
+                                     ("SCATTER_STAGED", 0), ("SCATTER_STAGED", 1),
+                                     ("PATH", 0), ("PATH", 1)])
 def test_pipeline_variants_bit_exact(opt, val):
     """Every variant a context option can force gives the reference's bits:
-    the fold's chained tile offsets vs staged outputs (k_tile_emit), and the
+    the fold's chained tile offsets vs staged outputs (k_tile_emit), the
     plain vs shared-memory-staged column scatter (k_scatter_staged, chosen
-    automatically only for N > 2^24, i.e. cfg5).  Whole acceptance sweep,
-    the reference's datasets, scaled FEM / heavy-duplicate workloads and
-    full-size cfg2 / cfg3."""
+    automatically only for N > 2^24, i.e. cfg5), and the two pipelines
+    (column-cursor vs column-block radix path, sa_radix.cu; with the radix
+    path the sweep's 1x1..7x7 matrices with ~50k-long runs go through its
+    oversize sub-bucket kernel).  Whole acceptance sweep, the reference's
+    datasets, scaled FEM / heavy-duplicate workloads and full-size cfg2 /
+    cfg3."""
     from paper_1406_1066_b200 import _capi
     from paper_1406_1066_b200 import workloads as W
 
@@ -644,26 +648,38 @@ def test_full_size_bit_exact_vs_stock_reference(k):
     unmodified reference package (oracle/_ref: stock assemble_parallel over
     its compiled kernels, all host threads; bit-identical to its serial
     driver for every p, test_acceptance.py:135-154): jc / ir equal, pr equal
-    byte for byte."""
+    byte for byte -- through the automatically chosen pipeline and through
+    the other one (cfg4: radix path chosen, column-cursor path forced;
+    cfg5: the other way round)."""
+    from paper_1406_1066_b200 import _capi
     from paper_1406_1066_b200 import workloads as W
 
     dev = torch.device("cuda", 0)
+    a = sa.default_assembler(0)
     w = W.config(k, device=dev)
     m, n, L = w.m, w.n, w.L
-    out = sa.default_assembler(0).assemble_device(w.ii, w.jj, w.s, m=m, n=n)
+    outs = []
+    for path in (-1, 1 if k == 5 else 0):
+        a.set_option(_capi.SA_OPT_PATH, path)
+        try:
+            out = a.assemble_device(w.ii, w.jj, w.s, m=m, n=n)
+            outs.append((out.jc.cpu().numpy(), out.ir.cpu().numpy(), out.pr.cpu().numpy()))
+            del out
+        finally:
+            a.set_option(_capi.SA_OPT_PATH, -1)
+        torch.cuda.empty_cache()
     ii, jj, s = w.ii.cpu().numpy(), w.jj.cpu().numpy(), w.s.cpu().numpy()
     del w
-    jc, ir, pr = out.jc.cpu().numpy(), out.ir.cpu().numpy(), out.pr.cpu().numpy()
-    del out
     torch.cuda.empty_cache()
     ref = stock.parallel(stock.request(ii, jj, s, m, n), stock.host_threads())
     del ii, jj, s
     assert (ref.m, ref.n) == (m, n)
-    assert np.array_equal(jc, ref.jc)
-    assert np.array_equal(ir, ref.ir)
-    assert pr.tobytes() == np.asarray(ref.pr).tobytes()
+    for jc, ir, pr in outs:
+        assert np.array_equal(jc, ref.jc)
+        assert np.array_equal(ir, ref.ir)
+        assert pr.tobytes() == np.asarray(ref.pr).tobytes()
     if k == 5:
-        assert len(ir) == 448_048_001 and L == 1_152_000_000
+        assert len(outs[0][1]) == 448_048_001 and L == 1_152_000_000
 
 
 @pytest.mark.parametrize("width", [40, 90, 200])
