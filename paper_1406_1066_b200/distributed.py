@@ -71,11 +71,28 @@ def block_boundaries(block_hist: torch.Tensor, world: int, nblocks: int, n: int)
     return bounds
 
 
+def validate_torch(ii, jj, m, n):
+    """Host restatement of sa_partition's index checks (CPU tensors): the
+    first row index < 1, else the first column index < 1 (rows before
+    columns, reference types.py:161-162), else whether any index exceeds the
+    explicit dimensions (DimensionTooSmall, types.py:113-117).  Returns
+    (which, local position, value) or ("dim", -1, None) or None."""
+    for which, x in (("row", ii), ("col", jj)):
+        bad = torch.nonzero(x < 1)
+        if len(bad):
+            k = int(bad[0, 0])
+            return which, k, int(x[k])
+    if (len(ii) and int(ii.max()) > m) or (len(jj) and int(jj.max()) > n):
+        return "dim", -1, None
+    return None
+
+
 def partition_torch(ii, jj, s, bounds, world, self_rank=-1):
-    """Host restatement of sa_partition (CPU tensors: the gloo tests).
-    Returns ((i, j, s) of the triplets bound for ranks other than
-    `self_rank`, grouped by destination rank, stably; per-rank counts
-    including the rank's own).  Columns outside [1, bounds[-1]] go nowhere."""
+    """Host restatement of sa_partition (CPU tensors: the gloo tests; the
+    index checks are validate_torch).  Returns ((i, j, s) of the triplets
+    bound for ranks other than `self_rank`, grouped by destination rank,
+    stably; per-rank counts including the rank's own).  Columns outside
+    [1, bounds[-1]] go nowhere."""
     jj64 = jj.to(torch.int64)
     bt = torch.tensor(bounds[1:-1], dtype=torch.int64, device=jj.device)
     valid = (jj64 >= 1) & (jj64 <= bounds[-1])
@@ -90,6 +107,42 @@ def partition_torch(ii, jj, s, bounds, world, self_rank=-1):
     sv = s.expand(len(jj)) if s.numel() == 1 and len(jj) != 1 else s
     out = (ii[keep].contiguous(), jj[keep].contiguous(), sv[keep].contiguous())
     return out, [int(c) for c in counts.tolist()]
+
+
+# error words exchanged with the counts: [kind, which, global position, value]
+_OK, _BAD, _DIM, _DEV = 0, 1, 2, 3
+_NONE = 1 << 62
+
+
+def _error_word(err, chunk_off):
+    """The rank's validation outcome as 4 int64: kind, which (0 row, 1 col),
+    GLOBAL position (chunk offset + local position), offending value."""
+    if err is None:
+        return [_OK, 0, _NONE, 0]
+    which, pos, val = err
+    if which == "dim":
+        return [_DIM, 0, _NONE, 0]
+    if which == "dev":
+        return [_DEV, 0, _NONE, int(pos)]
+    return [_BAD, 0 if which == "row" else 1, chunk_off + int(pos), int(val)]
+
+
+def _raise_agreed(words):
+    """Every rank gets every rank's error word and raises the same exception
+    the one-process call would: the first bad row over the whole input, else
+    the first bad column, else DimensionTooSmall (reference validation order,
+    types.py:141-165 then effective_dims 113-117)."""
+    from .errors import BadIndex, DeviceError, DimensionTooSmall
+
+    bad = [w for w in words if w[0] == _BAD]
+    if bad:
+        w = min(bad, key=lambda w: (w[1], w[2]))
+        raise BadIndex(int(w[2]), int(w[3]))
+    if any(w[0] == _DIM for w in words):
+        raise DimensionTooSmall("indices exceed the explicit dimensions")
+    dev = [w for w in words if w[0] == _DEV]
+    if dev:
+        raise DeviceError(int(dev[0][3]), "sa_partition failed on a peer rank")
 
 
 def _scratch(asm, name, n, dtype, dev):
@@ -114,11 +167,16 @@ def _block_hist_cuda(asm, jj, nblocks, bsize, step):
 
 
 def _partition_cuda(asm, ii, jj, s, m, n, bounds, world, self_rank):
-    """sa_partition: the CUDA partition (validates the chunk on the way);
-    the outputs are views of buffers reused across calls (valid until the
-    next call on this assembler)."""
+    """sa_partition: the CUDA partition, validating the chunk on the way.
+    Returns (outputs, counts, err): the outputs are views of buffers reused
+    across calls (valid until the next call on this assembler); err is None
+    or (which, chunk-local position, value) / ("dim", -1, None) -- not
+    raised here, so that every rank can raise the same exception after the
+    count exchange (a rank raising alone would leave its peers blocked in
+    the collective)."""
     import ctypes
 
+    from . import _capi
     from .assembly import _ptr
 
     dev = ii.device
@@ -132,11 +190,18 @@ def _partition_cuda(asm, ii, jj, s, m, n, bounds, world, self_rank):
                               0 if (s.numel() == 1 and L != 1) else 1, L, m, n, world, self_rank, hb,
                               _ptr(outs[0]), _ptr(outs[1]), _ptr(outs[2]), hc, ctypes.byref(bp),
                               ctypes.byref(bw))
-    if rc:
-        asm._raise_dev(rc, bp.value, bw.value, None, None, ii, jj)
-    counts = [int(hc[r]) for r in range(world)]
+    err = None
+    if rc == _capi.SA_ERR_BAD_INDEX:
+        row = bw.value == _capi.SA_WHICH_ROW
+        arr = ii if row else jj
+        err = ("row" if row else "col", bp.value, int(arr[bp.value].item()))
+    elif rc == _capi.SA_ERR_DIM_TOO_SMALL:
+        err = ("dim", -1, None)
+    elif rc:
+        err = ("dev", rc, None)
+    counts = [0] * world if err else [int(hc[r]) for r in range(world)]
     k = sum(c for r, c in enumerate(counts) if r != self_rank)
-    return tuple(x[:k] for x in outs), counts
+    return tuple(x[:k] for x in outs), counts, err
 
 
 def _assemble_segments_cuda(asm, segs, col_lo, m, n_local, out=None):
@@ -224,19 +289,35 @@ def assemble_sharded(ii: torch.Tensor, jj: torch.Tensor, s: torch.Tensor, m: int
     else:
         blk = torch.clamp((jj[::step].to(torch.int64) - 1) // bsize, 0, nblocks - 1)
         hist = torch.bincount(blk, minlength=nblocks).to(torch.int64) * step
-    dist.all_reduce(hist, group=group)
+    # one all_reduce: the block histogram and every rank's chunk length (the
+    # chunk offsets turn chunk-local error positions into global ones)
+    lens = torch.zeros(world, dtype=torch.int64, device=dev)
+    lens[rank] = int(jj.shape[0])
+    red = torch.cat([hist.to(torch.int64), lens])
+    dist.all_reduce(red, group=group)
+    hist = red[:nblocks]
+    chunk_off = int(red[nblocks:nblocks + rank].sum().item()) if rank else 0
     bounds = block_boundaries(hist, world, nblocks, n)
     launches = 0
     if cuda:
-        parts, counts = _partition_cuda(asm, ii, jj, s, m, n, bounds, world, rank)
+        parts, counts, err = _partition_cuda(asm, ii, jj, s, m, n, bounds, world, rank)
         launches += asm.lib.sa_last_launch_count(asm.ctx)
     else:
+        err = validate_torch(ii, jj, m, n)
         parts, counts = partition_torch(ii, jj, s, bounds, world, rank)
+        if err:
+            counts = [0] * world
     sc = [0 if r == rank else c for r, c in enumerate(counts)]  # the own triplets stay here
-    send_counts = torch.tensor(sc, dtype=torch.int64, device=dev)
-    recv_counts = torch.empty_like(send_counts)
-    dist.all_to_all_single(recv_counts, send_counts, group=group)
-    rc_ = recv_counts.cpu().tolist()
+    # one all_to_all: per destination its count and this rank's error word
+    word = _error_word(err, chunk_off)
+    send = torch.tensor([[c] + word for c in sc], dtype=torch.int64, device=dev)
+    recv = torch.empty_like(send)
+    dist.all_to_all_single(recv, send, group=group)
+    recv = recv.cpu()
+    words = recv[:, 1:].tolist()
+    if any(w[0] != _OK for w in words):
+        _raise_agreed(words)
+    rc_ = recv[:, 0].tolist()
     sent_remote = sum(sc)
 
     def exchange(x):

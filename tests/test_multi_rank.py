@@ -200,3 +200,103 @@ def test_cuda_sharded_path_matches_single_process(kind, world):
     assert np.concatenate(pr).tobytes() == ref.pr.tobytes()
     if kind == "heavy":  # shuffled input: the exchange moved triplets both ways
         assert all(g[-1] > 0 for g in got)
+
+
+def _err_case(kind):
+    """A fem2d input with one invalid index planted in the LAST rank's chunk
+    (and, for "both", a bad column earlier in rank 0's chunk as well)."""
+    from paper_1406_1066_b200 import workloads as W
+
+    w = W.fem2d(24)
+    ii, jj, s = w.ii.numpy().copy(), w.jj.numpy().copy(), w.s.numpy().copy()
+    L = len(ii)
+    m, n = w.m, w.n
+    if kind == "row":
+        ii[L - 7] = 0
+    elif kind == "both":  # rows are checked before columns, over the whole input
+        jj[5] = -3
+        ii[L - 7] = 0
+    elif kind == "col":
+        jj[L - 100] = 0
+    elif kind == "dim":
+        jj[L - 3] = n + 5
+    return ii, jj, s, m, n
+
+
+def _err_worker(rank, world, port, kind, cuda, result_q):
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path[:0] = [root, os.path.join(root, "tests")]
+    from paper_1406_1066_b200.distributed import assemble_sharded, gpu_local_assembler
+    from paper_1406_1066_b200.errors import BadIndex, DimensionTooSmall
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    if cuda:
+        _bounce_collectives()
+    try:
+        ii, jj, s, m, n = _err_case(kind)
+        L = len(ii)
+        lo, hi = L * rank // world, L * (rank + 1) // world
+        t = [torch.from_numpy(x[lo:hi].copy()) for x in (ii, jj, s)]
+        if cuda:
+            t = [x.to(torch.device("cuda", 0)) for x in t]
+            local = gpu_local_assembler(0)
+        else:
+            local = _oracle_local
+        try:
+            assemble_sharded(*t, m, n, local, nblocks=64)
+            result_q.put((rank, "none", None, None))
+        except BadIndex as e:
+            result_q.put((rank, "BadIndex", e.position, e.value))
+        except DimensionTooSmall:
+            result_q.put((rank, "DimensionTooSmall", None, None))
+    finally:
+        dist.destroy_process_group()
+
+
+def _run_err(kind, world, cuda):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_err_worker, args=(r, world, port, kind, cuda, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = sorted([q.get(timeout=300) for _ in range(world)])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    return got
+
+
+def _expected_err(kind):
+    """What the one-process reference validation raises (types.py:141-165)."""
+    ii, jj, s, m, n = _err_case(kind)
+    bad_i = np.flatnonzero(ii < 1)
+    bad_j = np.flatnonzero(jj < 1)
+    if len(bad_i):
+        return ("BadIndex", int(bad_i[0]), int(ii[bad_i[0]]))
+    if len(bad_j):
+        return ("BadIndex", int(bad_j[0]), int(jj[bad_j[0]]))
+    return ("DimensionTooSmall", None, None)
+
+
+@pytest.mark.parametrize("kind", ["row", "both", "col", "dim"])
+def test_validation_error_raised_on_every_rank(kind):
+    """an invalid index in one rank's chunk must not leave the
+    other ranks blocked in the exchange.  Every rank raises the exception the
+    one-process call raises, with the GLOBAL position (rows before columns,
+    reference types.py:161-162) and the offending value."""
+    got = _run_err(kind, 2, cuda=False)
+    exp = _expected_err(kind)
+    assert [g[1:] for g in got] == [exp, exp]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind", ["row", "both", "dim"])
+def test_cuda_validation_error_raised_on_every_rank(kind):
+    """The same through sa_partition (the CUDA branch, ranks on one GPU)."""
+    got = _run_err(kind, 2, cuda=True)
+    exp = _expected_err(kind)
+    assert [g[1:] for g in got] == [exp, exp]
