@@ -548,6 +548,26 @@ __device__ __forceinline__ unsigned rf_insert(uint32_t *key, int hbits, uint32_t
     }
 }
 
+__device__ __forceinline__ void rf_cp_async8(void *dst, const void *src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
+                 "l"(src) : "memory");
+}
+
+// Batcher's odd-even merge network on 8 keys (19 compare-exchanges), ascending.
+__device__ __forceinline__ void rf_cx(uint32_t &a, uint32_t &b) {
+    const uint32_t lo = min(a, b), hi = max(a, b);
+    a = lo;
+    b = hi;
+}
+__device__ __forceinline__ void rf_net8(uint32_t (&m)[8]) {
+    rf_cx(m[0], m[1]); rf_cx(m[2], m[3]); rf_cx(m[4], m[5]); rf_cx(m[6], m[7]);
+    rf_cx(m[0], m[2]); rf_cx(m[1], m[3]); rf_cx(m[4], m[6]); rf_cx(m[5], m[7]);
+    rf_cx(m[1], m[2]); rf_cx(m[5], m[6]);
+    rf_cx(m[0], m[4]); rf_cx(m[1], m[5]); rf_cx(m[2], m[6]); rf_cx(m[3], m[7]);
+    rf_cx(m[2], m[4]); rf_cx(m[3], m[5]);
+    rf_cx(m[1], m[2]); rf_cx(m[3], m[4]); rf_cx(m[5], m[6]);
+}
+
 __device__ __forceinline__ void rf_isort16(uint16_t *a, int n) {  // ascending, in place
     for (int i = 1; i < n; ++i) {
         const uint16_t x = a[i];
@@ -757,12 +777,20 @@ __global__ void __launch_bounds__(RF_NT, 2) k_rfold(RadixFoldArgs F, ErrState *e
     }
     __syncthreads();
     const bool sortall = S.sortall != 0;
+    // the sub-bucket's values into shared memory (the upper half of the dead
+    // hash table and the member counts: ckey uses key[0, U), U <= RF_CAP),
+    // in flight while the offset is looked back; the fallback sort below
+    // needs the whole table, so it reads the values from global memory
+    double *Vs = reinterpret_cast<double *>(&S.key[RF_CAP]);
     if (!sortall) {
 #pragma unroll
         for (int u = 0; u < RIPT; ++u) {
             const int g = tid + u * RF_NT;
             if (g < U) S.gid[opos[u]] = (uint16_t)g;  // gid := group of output entry
         }
+        const double *sg = F.s + a;
+        for (uint32_t k = tid; k < n; k += RF_NT) rf_cp_async8(&Vs[k], sg + k);
+        asm volatile("cp.async.commit_group;" ::: "memory");
     } else {  // CTA bitonic sort of all groups by key (a column with > 64 distinct rows)
         unsigned long long *items = reinterpret_cast<unsigned long long *>(S.key);
         int np2 = 1;
@@ -794,15 +822,34 @@ __global__ void __launch_bounds__(RF_NT, 2) k_rfold(RadixFoldArgs F, ErrState *e
         }
     }
     __syncthreads();
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
     const long long off = S.off;
-    const double *__restrict__ sv = F.s + a;
+    const double *__restrict__ sv = sortall ? F.s + a : Vs;
     for (int p = tid; p < U; p += RF_NT) {
         const int g = S.gid[p];
         const int st = S.gstart[g], en = S.gstart[g + 1];
         const uint32_t kx = S.gkey[g];
-        if (en - st <= 32) rf_isort16(S.memb + st, en - st);
         double acc = 0.0;
-        for (int q = st; q < en; ++q) acc = fold_add(acc, __ldg(sv + S.memb[q]));
+        const int nm = en - st;
+        if (nm <= 8) {
+            // up to 8 members (Poisson(5) repeats: 93 % of groups): member
+            // indices sorted by a register network, then every value load in
+            // flight at once before the ordered chain of adds
+            uint32_t m[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) m[q] = (q < nm) ? (uint32_t)S.memb[st + q] : 0xffffu;
+            rf_net8(m);
+            double v[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) v[q] = (q < nm) ? sv[m[q]] : 0.0;
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                if (q < nm) acc = fold_add(acc, v[q]);
+        } else {
+            if (nm <= 32) rf_isort16(S.memb + st, nm);
+            for (int q = st; q < en; ++q) acc = fold_add(acc, sv[S.memb[q]]);
+        }
         if (off + p < F.cap) {
             F.ir[off + p] = (int32_t)((kx - 1u) & rmask);
             F.pr[off + p] = acc;
