@@ -73,8 +73,10 @@ enum { SA_WHICH_ROW = 0, SA_WHICH_COL = 1 };
 enum {
     SA_OPT_FOLD_STAGED = 0,     /* fold outputs staged + k_tile_emit pass       */
     SA_OPT_SCATTER_STAGED = 1,  /* column scatter through shared-memory staging */
-    SA_OPT_PATH = 2             /* 0: column-cursor pipeline, 1: column-block radix
+    SA_OPT_PATH = 2,            /* 0: column-cursor pipeline, 1: column-block radix
                                    path (sa_radix.cu), -1: chosen per input    */
+    SA_OPT_RPASS_TMA = 3        /* radix partition passes with TMA-staged input
+                                   (k_rpass_tma) or register loads (k_rpass)   */
 };
 
 /* ABI version (bumped on any signature change). */

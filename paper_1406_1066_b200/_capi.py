@@ -31,6 +31,7 @@ SA_WHICH_COL = 1
 SA_OPT_FOLD_STAGED = 0
 SA_OPT_SCATTER_STAGED = 1
 SA_OPT_PATH = 2
+SA_OPT_RPASS_TMA = 3
 
 # every symbol include/sparse_assembly.h declares, with (restype, argtypes)
 _vp = ctypes.c_void_p

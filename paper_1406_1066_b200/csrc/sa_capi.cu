@@ -75,6 +75,7 @@ struct sa_ctx {
     int opt_fold_staged = -1;
     int opt_scatter_staged = -1;
     int opt_path = -1;
+    int opt_rpass_tma = -1;
     std::map<std::tuple<const void *, int64_t, int32_t, int32_t>, bool> path_cache;  // choose_radix
 
     int64_t host_L = -1;
@@ -349,6 +350,7 @@ int sa_set_option(sa_ctx *ctx, int option, int value) {
         case SA_OPT_FOLD_STAGED: ctx->opt_fold_staged = value; return SA_OK;
         case SA_OPT_SCATTER_STAGED: ctx->opt_scatter_staged = value; return SA_OK;
         case SA_OPT_PATH: ctx->opt_path = value; return SA_OK;
+        case SA_OPT_RPASS_TMA: ctx->opt_rpass_tma = value; return SA_OK;
         default: return fail(ctx, SA_ERR_INVALID_ARG, "sa_set_option: unknown option");
     }
 }
@@ -480,6 +482,7 @@ int assemble_radix(sa_ctx *ctx, const RadixPlan &P, const int32_t *ii, const int
                    const double *s, int64_t s_stride, int64_t L, int32_t M, int32_t N,
                    int32_t *d_jc, int32_t *d_ir, double *d_pr, int64_t cap) {
     Launch lc{ctx->stream, ctx->num_sms, 0};
+    lc.rpass_tma = ctx->opt_rpass_tma;
     const size_t nl = (size_t)L;
     const size_t nsub = (size_t)P.nsub;
     SA_CUDA(ctx, ensure_trip(ctx->rx_i, ctx->rx_j, ctx->rx_s, ctx->rx_cap, nl));

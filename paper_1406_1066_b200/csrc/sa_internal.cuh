@@ -387,6 +387,7 @@ struct Launch {
     // context options (sa_set_option): -1 = automatic choice
     int fold_staged = -1;     // SA_OPT_FOLD_STAGED: staged fold outputs + k_tile_emit
     int scatter_staged = -1;  // SA_OPT_SCATTER_STAGED: k_scatter_staged
+    int rpass_tma = -1;       // SA_OPT_RPASS_TMA: radix passes with TMA-staged input (k_rpass_tma)
 };
 
 cudaError_t launch_convert(Launch &lc, const void *raw, int dtype, int64_t L, int32_t *out,

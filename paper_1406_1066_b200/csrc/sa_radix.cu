@@ -374,6 +374,218 @@ __global__ void __launch_bounds__(RP_NT, 1) k_rpass(RadixPassArgs A, ErrState *e
 }
 
 // ---------------------------------------------------------------------------
+// k_rpass_tma: the same stable partition pass with the input staged by TMA.
+// A chunk (RP_CHUNK triplets, the unit of the histograms and bases) is
+// processed as two halves of RT_HALF; each half's rows, columns and values
+// arrive by cp.async.bulk into one of two shared-memory buffers while the
+// previous half is ranked, placed and written out, so the loads never stall
+// the CTA (k_rpass holds a whole chunk in registers and waits for it).  The
+// records are then placed in sorted order in the same buffer (every thread
+// has its triplets in registers by then) and written out as in k_rpass.
+// Needs 16-byte aligned input arrays (the host checks; k_rpass otherwise).
+// ---------------------------------------------------------------------------
+constexpr int RT_HALF = RP_CHUNK / 2;
+constexpr int RT_IPT = RT_HALF / RP_NT;
+struct PassTmaSmem {
+    uint4 buf[2][RT_HALF];            // staged {ii[], jj[], s[]} of a half, then its sorted records
+    uint32_t oidx[RT_HALF];           // output index of sorted slot k
+    uint32_t cnt[RP_NW][RP_MAXD / 2]; // per warp, digit pair (16-bit halves)
+    uint32_t hb[RP_MAXD];             // the half's global base per digit
+    uint32_t run[RP_MAXD];
+    uint32_t red[RP_NW];
+    unsigned long long mbar[2];
+};
+
+__device__ __forceinline__ unsigned rt_smem(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+// Stage half h (triplets [h0, h0 + nh)) into buffer `b` (thread 0).
+__device__ __forceinline__ void rt_issue(PassTmaSmem &S, int b, const RadixPassArgs &A, int64_t h0, int nh) {
+    int32_t *si = reinterpret_cast<int32_t *>(&S.buf[b][0]);
+    int32_t *sj = si + RT_HALF;
+    double *ss = reinterpret_cast<double *>(sj + RT_HALF);
+    const unsigned bi = (unsigned)nh * 4u, bs = A.s_stride ? (unsigned)nh * 8u : 0u;
+    const unsigned bar = rt_smem(&S.mbar[b]);
+    // the buffer was last written by the generic proxy (sorted records)
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(2 * bi + bs) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(rt_smem(si)), "l"(A.ii_in + h0), "r"(bi), "r"(bar) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(rt_smem(sj)), "l"(A.jj_in + h0), "r"(bi), "r"(bar) : "memory");
+    if (bs)
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                     ::"r"(rt_smem(ss)), "l"(A.s_in + h0), "r"(bs), "r"(bar) : "memory");
+}
+
+__device__ __forceinline__ void rt_wait(unsigned long long *bar, unsigned parity) {
+    unsigned done = 0;
+    while (!done) {
+        asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                     "selp.u32 %0, 1, 0, p;\n\t}"
+                     : "=r"(done) : "r"(rt_smem(bar)), "r"(parity) : "memory");
+    }
+}
+
+template <bool FIRST, int BITS>
+__global__ void __launch_bounds__(RP_NT, 1) k_rpass_tma(RadixPassArgs A, ErrState *err) {
+    extern __shared__ __align__(128) unsigned char rt_smem_raw[];
+    PassTmaSmem &S = *reinterpret_cast<PassTmaSmem *>(rt_smem_raw);
+    constexpr int ndig = 1 << BITS;
+    constexpr unsigned dmask = (unsigned)ndig - 1u;
+    constexpr int npair = (ndig + 1) >> 1;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const unsigned lt = lanemask_lt();
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(rt_smem(&S.mbar[0])) : "memory");
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(rt_smem(&S.mbar[1])) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    pdl_wait();
+    const int64_t Lp = FIRST ? A.L : (int64_t)*((volatile const unsigned *)&err->rvalid);
+    const int64_t nchunk = (Lp + RP_CHUNK - 1) / RP_CHUNK;
+    const int shift = A.shift;
+    const int32_t M = A.M, N = A.N;
+    const double sc = A.s_stride ? 0.0 : A.s_in[0];
+    unsigned long long bad = ~0ull;
+    unsigned over = 0;
+    // this CTA's halves: chunks blockIdx.x + i * grid, two halves each
+    const int64_t nmine = (nchunk > blockIdx.x) ? 2 * ((nchunk - 1 - blockIdx.x) / gridDim.x + 1) : 0;
+    auto half_start = [&](int64_t k) -> int64_t {
+        return ((int64_t)blockIdx.x + (k >> 1) * gridDim.x) * RP_CHUNK + (k & 1) * RT_HALF;
+    };
+    auto half_len = [&](int64_t k) -> int { return (int)max((int64_t)0, min((int64_t)RT_HALF, Lp - half_start(k))); };
+    // TMA only for whole halves (16-byte multiples); a partial tail half is
+    // loaded by the threads
+    if (tid == 0 && nmine > 0 && half_len(0) == RT_HALF) rt_issue(S, 0, A, half_start(0), RT_HALF);
+    for (int64_t k = 0; k < nmine; ++k) {
+        const int b = (int)(k & 1);
+        const int64_t h0 = half_start(k);
+        const int nh = half_len(k);
+        const int64_t c = blockIdx.x + (k >> 1) * gridDim.x;
+        if (tid == 0 && k + 1 < nmine && half_len(k + 1) == RT_HALF)
+            rt_issue(S, b ^ 1, A, half_start(k + 1), RT_HALF);
+        {
+            uint32_t *c32 = &S.cnt[0][0];
+            for (int q = tid; q < RP_NW * npair; q += RP_NT) c32[(q / npair) * (RP_MAXD / 2) + q % npair] = 0;
+            if ((k & 1) == 0)
+                for (int q = tid; q < ndig; q += RP_NT) S.hb[q] = A.off[c * RP_MAXD + q];
+        }
+        int32_t *si = reinterpret_cast<int32_t *>(&S.buf[b][0]);
+        int32_t *sj = si + RT_HALF;
+        double *ss = reinterpret_cast<double *>(sj + RT_HALF);
+        if (nh == RT_HALF) {
+            rt_wait(&S.mbar[b], (unsigned)((k >> 1) & 1));
+        } else {  // tail half: plain loads into the buffer
+            for (int q = tid; q < nh; q += RP_NT) {
+                si[q] = A.ii_in[h0 + q];
+                sj[q] = A.jj_in[h0 + q];
+                if (A.s_stride) ss[q] = A.s_in[h0 + q];
+            }
+            __syncthreads();
+        }
+        // warp w owns the half's w-th run of RT_IPT x 32 triplets, striped
+        const int o0 = w * (RT_IPT * 32) + lane;
+        int col[RT_IPT], row[RT_IPT];
+        double val[RT_IPT];
+#pragma unroll
+        for (int r = 0; r < RT_IPT; ++r) {
+            const int q = o0 + r * 32;
+            const bool live = q < nh;
+            col[r] = live ? sj[q] : 0;
+            row[r] = live ? si[q] : 1;
+            val[r] = live ? (A.s_stride ? ss[q] : sc) : 0.0;
+        }
+        __syncthreads();  // counters cleared; the buffer is read (it now takes the sorted records)
+        uint32_t rk[(RT_IPT + 1) / 2];
+#pragma unroll
+        for (int r = 0; r < RT_IPT; ++r) {
+            const bool live = o0 + r * 32 < nh;
+            if (FIRST && live) {
+                if (row[r] < 1) bad = min(bad, (unsigned long long)(h0 + o0 + r * 32));
+                else if (row[r] > M) over = 1;
+            }
+            const bool valid = live && (unsigned)(col[r] - 1) < (unsigned)N;
+            const unsigned d = ((unsigned)(col[r] - 1) >> shift) & dmask;
+            unsigned peers = __ballot_sync(FULL, valid);
+#pragma unroll
+            for (int i = 0; i < BITS; ++i) {
+                const unsigned bb = __ballot_sync(FULL, (d >> i) & 1u);
+                peers &= bb ^ (((d >> i) & 1u) - 1u);
+            }
+            const int leader = __ffs(peers) - 1;
+            const unsigned sh = (d & 1u) * 16u;
+            unsigned old = 0;
+            if (lane == leader && valid) old = atomicAdd(&S.cnt[w][d >> 1], (unsigned)__popc(peers) << sh);
+            const unsigned rr = ((__shfl_sync(FULL, old, leader & 31) >> sh) & 0xffffu) + __popc(peers & lt);
+            if (r & 1) rk[r >> 1] |= rr << 16;
+            else rk[r >> 1] = rr;
+        }
+        __syncthreads();
+        uint32_t t0 = 0, t1 = 0;
+        if (tid < npair) {
+#pragma unroll 8
+            for (int ww = 0; ww < RP_NW; ++ww) {
+                const uint32_t cc = S.cnt[ww][tid];
+                S.cnt[ww][tid] = t0 | (t1 << 16);
+                t0 += cc & 0xffffu;
+                t1 += cc >> 16;
+            }
+        }
+        uint32_t ctot;
+        const uint32_t ex = block_excl_sum<RP_NT, uint32_t>(t0 + t1, S.red, ctot);
+        if (tid < npair) {
+            const uint32_t add = ex | ((ex + t0) << 16);
+#pragma unroll 8
+            for (int ww = 0; ww < RP_NW; ++ww) S.cnt[ww][tid] += add;
+            // global position of the half-local slot 0 of each digit; the next
+            // half of the chunk starts where this one ends
+            S.run[2 * tid] = S.hb[2 * tid] - ex;
+            S.hb[2 * tid] += t0;
+            if (2 * tid + 1 < ndig) {
+                S.run[2 * tid + 1] = S.hb[2 * tid + 1] - (ex + t0);
+                S.hb[2 * tid + 1] += t1;
+            }
+        }
+        __syncthreads();
+        uint4 *rec = &S.buf[b][0];
+#pragma unroll
+        for (int r = 0; r < RT_IPT; ++r) {
+            if (o0 + r * 32 < nh && (unsigned)(col[r] - 1) < (unsigned)N) {
+                const unsigned d = ((unsigned)(col[r] - 1) >> shift) & dmask;
+                const unsigned pos = ((S.cnt[w][d >> 1] >> ((d & 1u) * 16u)) & 0xffffu) +
+                                     ((rk[r >> 1] >> ((r & 1) * 16)) & 0xffffu);
+                const unsigned long long vb = (unsigned long long)__double_as_longlong(val[r]);
+                rec[pos] = make_uint4((uint32_t)row[r], (uint32_t)col[r], (uint32_t)vb, (uint32_t)(vb >> 32));
+                S.oidx[pos] = S.run[d] + pos;
+            }
+        }
+        __syncthreads();
+        const unsigned long long pol = l2_evict_last();
+        for (int q = tid; q < (int)ctot; q += RP_NT) {
+            const uint4 v = rec[q];
+            const uint32_t o = S.oidx[q];
+            st_last(A.ii_out + o, (int32_t)v.x, pol);
+            st_last(A.jj_out + o, (int32_t)v.y, pol);
+            st_last(A.s_out + o, __longlong_as_double((long long)(((unsigned long long)v.w << 32) | v.z)), pol);
+        }
+        __syncthreads();  // the buffer and the counters are reused by the half after next
+    }
+    pdl_trigger();
+    if (FIRST) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            bad = min(bad, __shfl_xor_sync(FULL, bad, o));
+            over |= __shfl_xor_sync(FULL, over, o);
+        }
+        if (lane == 0) {
+            if (bad != ~0ull) atomicMin(&err->bad_i, bad);
+            if (over) err->over_m = 1;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // k_rbounds: start of every sub-bucket s = (col-1) >> w in the partitioned
 // column array (lower bound; the array is sorted by sub-bucket), and the
 // list of sub-buckets longer than RF_CAP.
@@ -890,6 +1102,17 @@ cudaError_t launch_rup(Launch &lc, bool first, const int32_t *jj, int64_t L, int
 
 template <bool FIRST, int BITS>
 static cudaError_t launch_rpass_t(Launch &lc, const RadixPassArgs &A, int nseg, ErrState *err) {
+    auto al16 = [](const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+    // TMA-staged input: measured faster for the later passes (cfg4 pass 2:
+    // 7.0 -> 6.0 ms) and slower for the first (8.3 -> 9.7 ms)
+    const bool tma = lc.rpass_tma >= 0 ? lc.rpass_tma == 1 : !FIRST;
+    if (tma && al16(A.ii_in) && al16(A.jj_in) && (A.s_stride == 0 || al16(A.s_in))) {
+        const int smem = (int)sizeof(PassTmaSmem);
+        cudaError_t e = ensure_smem_attr((const void *)k_rpass_tma<FIRST, BITS>, smem);
+        if (e != cudaSuccess) return e;
+        return launch_pdl(k_rpass_tma<FIRST, BITS>, dim3((unsigned)lc.num_sms), dim3(RP_NT), smem, lc.stream,
+                          A, err);
+    }
     const int smem = (int)sizeof(PassSmem);
     cudaError_t e = ensure_smem_attr((const void *)k_rpass<FIRST, BITS>, smem);
     if (e != cudaSuccess) return e;

@@ -599,7 +599,7 @@ def test_cli_assemble_verify_bench(tmp_path, monkeypatch, capsys):
 
 @pytest.mark.parametrize("opt,val", [("FOLD_STAGED", 0), ("FOLD_STAGED", 1),
                                      ("SCATTER_STAGED", 0), ("SCATTER_STAGED", 1),
-                                     ("PATH", 0), ("PATH", 1)])
+                                     ("PATH", 0), ("PATH", 1), ("RPASS_TMA", 0), ("RPASS_TMA", 1)])
 def test_pipeline_variants_bit_exact(opt, val):
     """Every variant a context option can force gives the reference's bits:
     the fold's chained tile offsets vs staged outputs (k_tile_emit), the
@@ -607,7 +607,9 @@ def test_pipeline_variants_bit_exact(opt, val):
     automatically only for N > 2^24, i.e. cfg5), and the two pipelines
     (column-cursor vs column-block radix path, sa_radix.cu; with the radix
     path the sweep's 1x1..7x7 matrices with ~50k-long runs go through its
-    oversize sub-bucket kernel).  Whole acceptance sweep, the reference's
+    oversize sub-bucket kernel), and the radix passes with register-loaded
+    or TMA-staged input (k_rpass / k_rpass_tma; RPASS_TMA applies when the
+    radix path runs, so these two variants also force it).  Whole acceptance sweep, the reference's
     datasets, scaled FEM / heavy-duplicate workloads and full-size cfg2 /
     cfg3."""
     from paper_1406_1066_b200 import _capi
@@ -615,6 +617,8 @@ def test_pipeline_variants_bit_exact(opt, val):
 
     a = sa.default_assembler(0)
     a.set_option(getattr(_capi, "SA_OPT_" + opt), val)
+    if opt == "RPASS_TMA":
+        a.set_option(_capi.SA_OPT_PATH, 1)
     try:
         kw, rows = sweep("acceptance")
         bad = []
@@ -638,6 +642,7 @@ def test_pipeline_variants_bit_exact(opt, val):
             del w, out, ref
     finally:
         a.set_option(getattr(_capi, "SA_OPT_" + opt), -1)
+        a.set_option(_capi.SA_OPT_PATH, -1)
 
 
 @pytest.mark.skipif(not stock.available(), reason="oracle/_ref (stock reference) not installed")
