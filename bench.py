@@ -193,30 +193,31 @@ def cpu_reference_run(ii, jj, s, m, n, budget_s=15.0, max_reps=20):
 
 
 def bench_config(w, world: int, shard: bool) -> dict:
-    """The workload description both arms print (identical keys)."""
-    small = 16 * w.L < L2_BYTES
-    return {"workload": w.name, "L": w.L, "m": w.m, "n": w.n,
+    """The workload description both arms print (identical keys): the whole
+    job's workload (a sharded run's chunks carry the global name and L)."""
+    name = getattr(w, "global_name", w.name)
+    L = getattr(w, "global_L", w.L)
+    small = 16 * L < L2_BYTES
+    return {"workload": name, "L": L, "m": w.m, "n": w.n,
             "l2": ("inputs fit in the 126 MB L2: each step timed alone after a 256 MB flush"
                    if small else
                    "inputs (16 B x L) and workspace exceed the 126 MB L2; no explicit flush"),
-            "parallelism": f"dp{world}" if shard else "single"}
+            "parallelism": (f"column-block shards over {world} GPUs (contiguous triplet chunk per "
+                            "rank, NCCL all-to-all exchange)") if shard else "single"}
 
 
 def build_workload(cfg: int, device, rank: int, world: int):
     from paper_1406_1066_b200 import workloads as W
 
-    if cfg == 5 or world > 1:
-        # sharded 2D FEM: rank r takes a contiguous cell chunk (weak scaling:
-        # each rank holds a cfg2-sized chunk of an N_mesh = 1000*sqrt(world) mesh)
-        import math
-
-        if cfg == 5:
-            Nm = 8000
-        else:
-            Nm = int(round(1000 * math.sqrt(world)))
+    if world > 1 or cfg == 5:
+        # BASELINE configs[4], the sharded config: the N = 8000 triangulated
+        # mesh (L = 1.152e9), rank r holding a contiguous chunk of its element
+        # stream (strong scaling: the whole job is the same at every N)
+        Nm = 8000
         cells = Nm * Nm
         c0, c1 = cells * rank // world, cells * (rank + 1) // world
         w = W.fem2d(Nm, device=device, cell_range=(c0, c1))
+        w.global_name, w.global_L = f"fem2d_N{Nm}", 18 * cells
         w.name = f"fem2d_N{Nm}_chunk{rank}of{world}"
         return w
     return W.config(cfg, device=device)
@@ -228,7 +229,8 @@ def main():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     # default: configs[3], the largest single-GPU BASELINE config (heavy-duplicate
-    # random, L ~ 5e8); configs[4] is the 8-GPU sharded one
+    # random, L ~ 5e8); under torchrun with N > 1 ranks: configs[4], the
+    # sharded config, split over the ranks (its N = 1 point: --config 5)
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=5)
@@ -249,7 +251,8 @@ def main():
         # the same bits as the GPU arm's workload (generated on the GPU when
         # there is one; input generation is not part of either timed path)
         gen_dev = torch.device("cuda", local) if torch.cuda.is_available() else "cpu"
-        w = build_workload(args.config, gen_dev, 0, 1)
+        # N > 1: the sharded config as the GPU arm runs it, whole (rank 0 holds it)
+        w = build_workload(5 if args.gpus > 1 else args.config, gen_dev, 0, 1)
         ii, jj, s = w.ii.cpu().numpy(), w.jj.cpu().numpy(), w.s.cpu().numpy()
         cfg_line, wL = bench_config(w, args.gpus, args.gpus > 1), w.L
         del w.ii, w.jj, w.s  # device copies
@@ -267,8 +270,8 @@ def main():
                   f"stock sparseasm.assemble_parallel(req, p={p}) from oracle/_ref")
         line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": mean * 1e3,
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-                "data": "synthetic",
+                "higher_is_better": True, "scaling": "strong" if args.gpus > 1 else "weak",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": cfg_line,
                 "cpu_baseline": {"value": val, "unit": UNIT, "cores": p, "kind": "reference",
                                  "sample": sample},
@@ -283,6 +286,12 @@ def main():
 
     if shard:
         import torch.distributed as dist
+
+        # communicator set-up lines (nranks, transport) on stderr for the record
+        # (the image's NCCL_DEBUG=VERSION prints only the banner)
+        if os.environ.get("NCCL_DEBUG", "VERSION").upper() in ("", "VERSION", "WARN"):
+            os.environ["NCCL_DEBUG"] = "INFO"
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
 
         # stdout carries only the JSON line: the communicator is created (and
         # NCCL prints its version banner, NCCL_DEBUG=VERSION in this image)
@@ -426,7 +435,7 @@ def main():
     dom_gbs = alg.get(dom, 0) / (kern_ms[dom] * 1e-3) / 1e9
     # whole job: every rank's triplets read, the global CSC written, over
     # world x the per-GPU peak
-    compulsory = 16 * L * world + 12 * nnz + 4 * (N + 1)
+    compulsory = 16 * getattr(w, "global_L", L * world) + 12 * nnz + 4 * (N + 1)
     path_gbs = compulsory / (ms * 1e-3) / 1e9 / world
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "dram_traffic.json")
@@ -512,10 +521,12 @@ def main():
         if shard:
             dist.destroy_process_group()
         return
-    value = L * world / (ms * 1e-3)
+    Ltot = getattr(w, "global_L", L) if shard else L  # every rank's triplets
+    value = Ltot / (ms * 1e-3)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong" if shard else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": bench_config(w, world, shard),
         "nnz": nnz,
@@ -526,7 +537,7 @@ def main():
         "path_roofline": {"compulsory_bytes": compulsory, "achieved": path_gbs, "peak": peak_gbs,
                           "unit": "GB/s", "frac": path_gbs / peak_gbs},
         "kernel_ms": kern_ms,
-        "e2e": {"value": L * world / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 16 * L,
+        "e2e": {"value": (getattr(w, "global_L", L * world) if shard else L) / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 16 * L,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3},
         "gpu_launches": launches_per_step * args.steps,
         "launches_per_step": launches_per_step,

@@ -276,7 +276,7 @@ def assemble_sharded(ii: torch.Tensor, jj: torch.Tensor, s: torch.Tensor, m: int
             jc, ir, pr = out.jc, out.ir, out.pr
         else:
             jc, ir, pr = local_assemble(ii, jj, s, m, n)
-        k = int(jc[-1]) if len(jc) else 0
+        k = int(ir.shape[0])  # nnz (the assembly already synchronised for it)
         nl = asm.lib.sa_last_launch_count(asm.ctx) if cuda else 0
         return ShardResult(0, n, jc.to(torch.int64), ir, pr, 0, k, m, n, int(ii.shape[0]), 0, nl)
     nblocks = max(1, min(nblocks, n))
