@@ -413,38 +413,51 @@ namespace {
 // ---- radix path (sa_radix.cu) -------------------------------------------------
 struct RadixPlan {
     bool ok = false;
-    int w = 0, rbits = 0, npass = 0;
+    int z = 0, rbits = 0, npass = 0;
     int shift[RP_MAXPASS] = {}, bits[RP_MAXPASS] = {};
     int32_t nsub = 0;
     int64_t nchunk = 0;
 };
 
-// Sub-buckets of W = 2^w columns: the largest w whose expected sub-bucket
-// (L W / N triplets) stays within 4/5 of the fold's shared-memory capacity and
-// whose (column-local, row) key fits 31 bits; the remaining column bits are
-// split over at most RP_MAXPASS passes of at most RP_MAXBITS bits.
+// The sort key of a triplet is (col - 1) << rbits | (row - 1); sub-bucket s
+// holds the keys [s << z, (s + 1) << z) and the passes partition on the key
+// bits above z (at most RP_MAXPASS passes of at most RP_MAXBITS bits).
+// Column-block plan: z = rbits + w, sub-buckets of W = 2^w whole columns --
+// the largest w whose expected sub-bucket (L W / N triplets) stays within 4/5
+// of the fold's shared-memory capacity, with the local key inside 31 bits.
+// Row-split plan, when even single columns are longer than that on average
+// (few, long columns: L > 4/5 RF_CAP N): z < rbits, sub-buckets of 2^z rows
+// of one column, expected (L / N) 2^z / M triplets.
 RadixPlan radix_plan(int64_t L, int32_t M, int32_t N) {
     RadixPlan P;
     if (L <= 0 || N <= 0 || M <= 0) return P;
     P.rbits = bits_for((uint64_t)(M - 1));
     const int cbits = bits_for((uint64_t)(N - 1));
-    int w = 0;
-    while (w < 8 && w < cbits && w + 1 + P.rbits <= 31 &&
-           (L << (w + 1)) <= (int64_t)(4 * RF_CAP / 5) * (int64_t)N)
-        ++w;
-    if (w + P.rbits > 31) return P;
-    const int R = cbits - w;
+    const int64_t cap = 4 * RF_CAP / 5;
+    int z;
+    if (L <= cap * (int64_t)N || P.rbits == 0) {
+        int w = 0;
+        while (w < 8 && w < cbits && w + 1 + P.rbits <= 31 && (L << (w + 1)) <= cap * (int64_t)N) ++w;
+        z = w + P.rbits;
+    } else {
+        z = 0;
+        while (z + 1 < P.rbits && (double)L / N * (double)(1ll << (z + 1)) / M <= (double)cap) ++z;
+    }
+    if (z > 31) return P;
+    const int R = cbits + P.rbits - z;
     const int npass = std::max(1, (R + RP_MAXBITS - 1) / RP_MAXBITS);
     if (npass > RP_MAXPASS) return P;
-    int sh = w;
+    int sh = z;
     for (int p = 0; p < npass; ++p) {
         P.bits[p] = R / npass + (p < R % npass ? 1 : 0);
         P.shift[p] = sh;
         sh += P.bits[p];
     }
-    P.w = w;
+    const uint64_t kmax = ((uint64_t)(N - 1) << P.rbits) | (uint64_t)(M - 1);
+    if ((kmax >> z) >= (uint64_t)INT32_MAX) return P;
+    P.z = z;
     P.npass = npass;
-    P.nsub = (int32_t)(((int64_t)N + (1ll << w) - 1) >> w);
+    P.nsub = (int32_t)((kmax >> z) + 1);
     P.nchunk = (L + RP_CHUNK - 1) / RP_CHUNK;
     P.ok = true;
     return P;
@@ -491,7 +504,8 @@ int assemble_radix(sa_ctx *ctx, const RadixPlan &P, const int32_t *ii, const int
     SA_CUDA(ctx, ensure(ctx->perm, ctx->perm_cap, nl + 2));  // oversize scratch A
     // partition CTAs: the resident ones (2 per SM), walking the chunks with that stride
     const int nseg = (int)std::max<int64_t>(1, std::min<int64_t>(P.nchunk, (int64_t)ctx->num_sms * (2048 / RP_NT)));
-    const int64_t nblk = (P.nchunk + RP_BLK - 1) / RP_BLK;
+    const int cpb = rup_cpb(P.nchunk, ctx->num_sms);
+    const int64_t nblk = (P.nchunk + cpb - 1) / cpb;
     SA_CUDA(ctx, ensure(ctx->rcnt, ctx->rcnt_cap, (size_t)P.nchunk * RP_MAXD));
     SA_CUDA(ctx, ensure(ctx->roff, ctx->roff_cap, (size_t)P.nchunk * RP_MAXD));
     SA_CUDA(ctx, ensure(ctx->rbsum, ctx->rbsum_cap, (size_t)std::max<int64_t>(nblk, 1) * RP_MAXD));
@@ -514,8 +528,8 @@ int assemble_radix(sa_ctx *ctx, const RadixPlan &P, const int32_t *ii, const int
     if ((rc = launch_init(ctx, lc, 0, 0, 0))) return rc;
     int32_t *bi[2] = {ctx->rx_i, ctx->ry_i}, *bj[2] = {ctx->rx_j, ctx->ry_j};
     double *bs[2] = {ctx->rx_s, ctx->ry_s};
-    static const char *pname[RP_MAXPASS] = {"k_rpass0", "k_rpass1", "k_rpass2"};
-    static const char *uname[RP_MAXPASS] = {"k_rup0", "k_rup1", "k_rup2"};
+    static const char *pname[RP_MAXPASS] = {"k_rpass0", "k_rpass1", "k_rpass2", "k_rpass3"};
+    static const char *uname[RP_MAXPASS] = {"k_rup0", "k_rup1", "k_rup2", "k_rup3"};
     for (int p = 0; p < P.npass; ++p) {
         RadixPassArgs A{};
         A.ii_in = p ? bi[(p - 1) & 1] : ii;
@@ -530,10 +544,11 @@ int assemble_radix(sa_ctx *ctx, const RadixPlan &P, const int32_t *ii, const int
         A.N = N;
         A.shift = P.shift[p];
         A.bits = P.bits[p];
+        A.rbits = P.rbits;
         A.off = ctx->roff;
         if ((rc = mark(ctx, uname[p]))) return rc;
-        SA_CUDA(ctx, launch_rup(lc, p == 0, A.jj_in, L, N, A.shift, A.bits, ctx->rcnt, ctx->rbsum,
-                                ctx->roff, ctx->err));
+        SA_CUDA(ctx, launch_rup(lc, p == 0, A.ii_in, A.jj_in, L, N, A.shift, A.bits, P.rbits, ctx->rcnt,
+                                ctx->rbsum, ctx->roff, ctx->err));
         if ((rc = mark(ctx, pname[p]))) return rc;
         SA_CUDA(ctx, launch_rpass(lc, A, p == 0, nseg, ctx->err));
     }
@@ -553,7 +568,7 @@ int assemble_radix(sa_ctx *ctx, const RadixPlan &P, const int32_t *ii, const int
     }
     F.lbf = ctx->rlbf;
     F.tag = ep | 3u;
-    F.w = P.w;
+    F.z = P.z;
     F.rbits = P.rbits;
     F.N = N;
     F.nsub = P.nsub;
@@ -562,7 +577,7 @@ int assemble_radix(sa_ctx *ctx, const RadixPlan &P, const int32_t *ii, const int
     F.pr = d_pr;
     F.cap = cap;
     if ((rc = mark(ctx, "k_rbounds"))) return rc;
-    SA_CUDA(ctx, launch_rbounds(lc, F.jj, P.w, P.nsub, ctx->rbnd, ctx->rbig, ctx->err));
+    SA_CUDA(ctx, launch_rbounds(lc, F.ii, F.jj, P.z, P.rbits, P.nsub, ctx->rbnd, ctx->rbig, ctx->err));
     if ((rc = mark(ctx, "k_rbig"))) return rc;
     SA_CUDA(ctx, launch_rbig(lc, F, ctx->err));
     if ((rc = mark(ctx, "k_rfold"))) return rc;
@@ -584,6 +599,7 @@ int assemble_radix(sa_ctx *ctx, const RadixPlan &P, const int32_t *ii, const int
 // choice after the caller rewrites the buffers only costs speed -- both paths
 // give the same bits).
 constexpr int64_t RADIX_MIN_L = 1 << 21;
+constexpr int64_t RADIX_LONG_L = 1 << 16;  // long-column inputs take the radix path from this size
 constexpr int RADIX_WIN = 8;
 constexpr int RADIX_WLEN = 1024;
 constexpr int RADIX_BLOCKS = RADIX_WLEN / 4;  // more distinct blocks per window: no locality
@@ -630,7 +646,12 @@ int assemble_segments(sa_ctx *ctx, const Segs &S, int64_t L, int32_t M, int32_t 
     if (S.nseg == 1 && L > 0 && N > 0 && M > 0 && ctx->opt_path != 0) {
         const RadixPlan P = radix_plan(L, M, N);
         bool radix = P.ok && ctx->opt_path == 1;
-        if (P.ok && ctx->opt_path == -1 && L >= RADIX_MIN_L) {
+        if (P.ok && ctx->opt_path == -1 && L >= RADIX_LONG_L && P.z < P.rbits) {
+            // columns longer than a fold sub-bucket on average: the row-split
+            // plan spreads each column over many CTAs (the column-cursor
+            // pipeline folds a big column in one CTA)
+            radix = true;
+        } else if (P.ok && ctx->opt_path == -1 && L >= RADIX_MIN_L) {
             if (S.jj[0] == ctx->h_jj && ctx->host_radix >= 0) {
                 radix = ctx->host_radix == 1;  // host protocol: chosen at upload
             } else {

@@ -419,7 +419,7 @@ constexpr int RP_IPT = 8;                   // triplets per thread
 constexpr int RP_CHUNK = RP_NT * RP_IPT;    // triplets per chunk (CTA)
 constexpr int RP_MAXBITS = 9;               // digit bits per pass
 constexpr int RP_MAXD = 1 << RP_MAXBITS;
-constexpr int RP_MAXPASS = 3;
+constexpr int RP_MAXPASS = 4;
 constexpr int RP_BLK = 64;                  // chunks per upsweep block
 constexpr int RF_CAP = 4096;                // fold: largest sub-bucket held in shared memory
 constexpr int RF_WMAX = 256;                // fold: columns per sub-bucket (2^w)
@@ -432,7 +432,8 @@ struct RadixPassArgs {
     double *s_out;
     int64_t L;
     int32_t M, N;
-    int shift, bits;          // this pass's digit: ((col - 1) >> shift) & (2^bits - 1)
+    int shift, bits;          // this pass's digit: (key >> shift) & (2^bits - 1) of the key
+    int rbits;                // key = (col - 1) << rbits | (row - 1)
     const uint32_t *off;      // nchunk x RP_MAXD: global position of every chunk's digits
 };
 
@@ -445,18 +446,20 @@ struct RadixFoldArgs {
     unsigned long long *scrA, *scrB;  // oversize scratch (L entries each)
     unsigned long long *lbf; // look-back words, nsub x LB_STRIDE
     unsigned tag;
-    int w, rbits;
+    int z, rbits;            // sub-bucket s = the keys [s << z, (s + 1) << z), key as above
     int32_t N, nsub;
     int32_t *jc, *ir;
     double *pr;
     int64_t cap;
 };
 
-cudaError_t launch_rup(Launch &lc, bool first, const int32_t *jj, int64_t L, int32_t N, int shift,
-                       int bits, uint16_t *cnt, uint32_t *bsum, uint32_t *off, ErrState *err);
+cudaError_t launch_rup(Launch &lc, bool first, const int32_t *ii, const int32_t *jj, int64_t L, int32_t N,
+                       int shift, int bits, int rbits, uint16_t *cnt, uint32_t *bsum, uint32_t *off,
+                       ErrState *err);
+int rup_cpb(int64_t nchunk, int num_sms);  // chunks per upsweep block
 cudaError_t launch_rpass(Launch &lc, const RadixPassArgs &A, bool first, int nseg, ErrState *err);
-cudaError_t launch_rbounds(Launch &lc, const int32_t *jj, int w, int32_t nsub, uint32_t *bnd,
-                           uint32_t *biglist, ErrState *err);
+cudaError_t launch_rbounds(Launch &lc, const int32_t *ii, const int32_t *jj, int z, int rbits,
+                           int32_t nsub, uint32_t *bnd, uint32_t *biglist, ErrState *err);
 cudaError_t launch_rbig(Launch &lc, const RadixFoldArgs &F, ErrState *err);
 cudaError_t launch_rfold(Launch &lc, const RadixFoldArgs &F, ErrState *err);
 

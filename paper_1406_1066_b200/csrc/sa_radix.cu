@@ -100,14 +100,43 @@ __device__ __forceinline__ unsigned long long ep_walk_warp(const unsigned long l
 // ---------------------------------------------------------------------------
 constexpr int RU_NT = 512;
 
+// Digit of the sort key (col - 1) << rbits | (row - 1) at bit `shift`.  The
+// column-block plan only uses digits of the column bits (shift >= rbits);
+// the row-split plan (few, long columns) also the row bits.
+__device__ __forceinline__ unsigned key_digit(int col, int row, int shift, int rbits, unsigned dmask) {
+    if (shift >= rbits) return ((unsigned)(col - 1) >> (shift - rbits)) & dmask;
+    const unsigned long long key = ((unsigned long long)(unsigned)(col - 1) << rbits) | (unsigned)(row - 1);
+    return (unsigned)(key >> shift) & dmask;
+}
+
+// Sort key of a (valid) triplet.
+__device__ __forceinline__ unsigned long long tkey(int col, int row, int rbits) {
+    return ((unsigned long long)(unsigned)(col - 1) << rbits) | (unsigned)(row - 1);
+}
+
+// Key relative to the first key of its sub-bucket (K0 = c0 << rbits | roff),
+// in 32 bits: column-block plan (z >= rbits, roff = 0) the local column and
+// the row; row-split plan (one column) the row offset.
+__device__ __forceinline__ uint32_t lkey(int col, int row, int z, int rbits, uint32_t c0, uint32_t roff) {
+    return z >= rbits ? (((uint32_t)(col - 1) - c0) << rbits) | (uint32_t)(row - 1)
+                      : (uint32_t)(row - 1) - roff;
+}
+
+// Any index error: the call fails, the fold's work is moot (and rows beyond
+// M would spill into the column bits of the fold's keys).
+__device__ __forceinline__ bool call_failed(const ErrState *err) {
+    return err->bad_i != ~0ull || err->bad_j != ~0ull || err->over_m || err->over_n;
+}
+
 // k_rup: per-chunk digit histograms cnt[c][d] (16-bit) of the pass input (jj)
 // and the block's sums bsum[B][d].  The first pass also validates the
 // columns (first index < 1, any index > N) and counts the valid triplets
 // (err->rvalid, the length the later passes read).
-template <bool FIRST>
-__global__ void __launch_bounds__(RU_NT) k_rup(const int32_t *__restrict__ jj, int64_t L, int32_t N,
-                                               int shift, int bits, uint16_t *__restrict__ cnt,
-                                               uint32_t *__restrict__ bsum, ErrState *err) {
+template <bool FIRST, bool ROWKEY>
+__global__ void __launch_bounds__(RU_NT) k_rup(const int32_t *__restrict__ ii, const int32_t *__restrict__ jj,
+                                               int64_t L, int32_t N, int shift, int bits, int rbits, int cpb,
+                                               uint16_t *__restrict__ cnt, uint32_t *__restrict__ bsum,
+                                               ErrState *err) {
     __shared__ uint32_t h[RP_MAXD];
     pdl_wait();
     const int64_t Lp = FIRST ? L : (int64_t)*((volatile const unsigned *)&err->rvalid);
@@ -117,8 +146,8 @@ __global__ void __launch_bounds__(RU_NT) k_rup(const int32_t *__restrict__ jj, i
     unsigned long long bad = ~0ull;
     unsigned over = 0, nval = 0;
     uint32_t bs = 0;  // block sum of digit threadIdx.x
-    const int64_t cb = (int64_t)blockIdx.x * RP_BLK;
-    for (int64_t c = cb; c < min(nchunk, cb + RP_BLK); ++c) {
+    const int64_t cb = (int64_t)blockIdx.x * cpb;
+    for (int64_t c = cb; c < min(nchunk, cb + cpb); ++c) {
         for (int k = threadIdx.x; k < ndig; k += RU_NT) h[k] = 0;
         __syncthreads();
         const int64_t lo = c * RP_CHUNK, hi = min(Lp, lo + RP_CHUNK);
@@ -136,7 +165,10 @@ __global__ void __launch_bounds__(RU_NT) k_rup(const int32_t *__restrict__ jj, i
             if (FIRST && cc < 1) bad = min(bad, (unsigned long long)t);
             else if (FIRST && cc > N) over = 1;
             else {
-                atomicAdd(&h[((unsigned)(cc - 1) >> shift) & dmask], 1u);
+                if (ROWKEY)  // the digit takes row bits (row-split plan)
+                    atomicAdd(&h[key_digit(cc, __ldcs(ii + t), shift, rbits, dmask)], 1u);
+                else
+                    atomicAdd(&h[((unsigned)(cc - 1) >> (shift - rbits)) & dmask], 1u);
                 ++nval;
             }
         }
@@ -189,15 +221,15 @@ __global__ void __launch_bounds__(RP_MAXD) k_rscan(uint32_t *__restrict__ bsum, 
 __global__ void __launch_bounds__(RP_MAXD) k_roff(const uint16_t *__restrict__ cnt,
                                                   const uint32_t *__restrict__ bsum, int bits,
                                                   uint32_t *__restrict__ off, ErrState *err, int64_t L,
-                                                  int first) {
+                                                  int first, int cpb) {
     const int d = threadIdx.x;
     pdl_wait();
     const int64_t Lp = first ? L : (int64_t)*((volatile const unsigned *)&err->rvalid);
     const int64_t nchunk = (Lp + RP_CHUNK - 1) / RP_CHUNK;
     if (d < (1 << bits)) {
         uint32_t run = bsum[(int64_t)blockIdx.x * RP_MAXD + d];
-        const int64_t cb = (int64_t)blockIdx.x * RP_BLK;
-        for (int64_t c = cb; c < min(nchunk, cb + RP_BLK); ++c) {
+        const int64_t cb = (int64_t)blockIdx.x * cpb;
+        for (int64_t c = cb; c < min(nchunk, cb + cpb); ++c) {
             off[c * RP_MAXD + d] = run;
             run += cnt[c * RP_MAXD + d];
         }
@@ -295,7 +327,7 @@ __global__ void __launch_bounds__(RP_NT, 1) k_rpass(RadixPassArgs A, ErrState *e
                 else if (row[r] > M) over = 1;
             }
             const bool valid = live && (unsigned)(col[r] - 1) < (unsigned)N;
-            const unsigned d = ((unsigned)(col[r] - 1) >> shift) & dmask;
+            const unsigned d = key_digit(col[r], row[r], shift, A.rbits, dmask);
             // lanes with the same digit: one ballot per digit bit
             // (__match_any_sync runs on the slow ADU pipe)
             unsigned peers = __ballot_sync(FULL, valid);
@@ -341,7 +373,7 @@ __global__ void __launch_bounds__(RP_NT, 1) k_rpass(RadixPassArgs A, ErrState *e
 #pragma unroll
         for (int r = 0; r < RP_IPT; ++r) {  // records to their sorted slots
             if (r * 32 + lane < nlive && (unsigned)(col[r] - 1) < (unsigned)N) {
-                const unsigned d = ((unsigned)(col[r] - 1) >> shift) & dmask;
+                const unsigned d = key_digit(col[r], row[r], shift, A.rbits, dmask);
                 const unsigned pos = ((S.cnt[w][d >> 1] >> ((d & 1u) * 16u)) & 0xffffu) +
                                      ((rk[r >> 1] >> ((r & 1) * 16)) & 0xffffu);
                 const unsigned long long vb = (unsigned long long)__double_as_longlong(val[r]);
@@ -506,7 +538,7 @@ __global__ void __launch_bounds__(RP_NT, 1) k_rpass_tma(RadixPassArgs A, ErrStat
                 else if (row[r] > M) over = 1;
             }
             const bool valid = live && (unsigned)(col[r] - 1) < (unsigned)N;
-            const unsigned d = ((unsigned)(col[r] - 1) >> shift) & dmask;
+            const unsigned d = key_digit(col[r], row[r], shift, A.rbits, dmask);
             unsigned peers = __ballot_sync(FULL, valid);
 #pragma unroll
             for (int i = 0; i < BITS; ++i) {
@@ -552,7 +584,7 @@ __global__ void __launch_bounds__(RP_NT, 1) k_rpass_tma(RadixPassArgs A, ErrStat
 #pragma unroll
         for (int r = 0; r < RT_IPT; ++r) {
             if (o0 + r * 32 < nh && (unsigned)(col[r] - 1) < (unsigned)N) {
-                const unsigned d = ((unsigned)(col[r] - 1) >> shift) & dmask;
+                const unsigned d = key_digit(col[r], row[r], shift, A.rbits, dmask);
                 const unsigned pos = ((S.cnt[w][d >> 1] >> ((d & 1u) * 16u)) & 0xffffu) +
                                      ((rk[r >> 1] >> ((r & 1) * 16)) & 0xffffu);
                 const unsigned long long vb = (unsigned long long)__double_as_longlong(val[r]);
@@ -586,32 +618,41 @@ __global__ void __launch_bounds__(RP_NT, 1) k_rpass_tma(RadixPassArgs A, ErrStat
 }
 
 // ---------------------------------------------------------------------------
-// k_rbounds: start of every sub-bucket s = (col-1) >> w in the partitioned
-// column array (lower bound; the array is sorted by sub-bucket), and the
-// list of sub-buckets longer than RF_CAP.
+// k_rbounds: start of every sub-bucket s = key >> z in the partitioned
+// arrays (lower bound; the arrays are sorted by sub-bucket), and the list of
+// sub-buckets longer than RF_CAP.  Column-block plan (z >= rbits): s =
+// (col - 1) >> (z - rbits), the columns alone decide.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t sub_lower_bound(const int32_t *__restrict__ jj, uint32_t n,
-                                                    int w, uint32_t s) {
+__device__ __forceinline__ unsigned long long sub_of(const int32_t *__restrict__ ii,
+                                                     const int32_t *__restrict__ jj, uint32_t k, int z,
+                                                     int rbits) {
+    if (z >= rbits) return (unsigned long long)((uint32_t)(__ldg(jj + k) - 1) >> (z - rbits));
+    return tkey(__ldg(jj + k), __ldg(ii + k), rbits) >> z;
+}
+
+__device__ __forceinline__ uint32_t sub_lower_bound(const int32_t *__restrict__ ii,
+                                                    const int32_t *__restrict__ jj, uint32_t n, int z,
+                                                    int rbits, uint32_t s) {
     uint32_t lo = 0, hi = n;
     while (lo < hi) {
         const uint32_t mid = (lo + hi) >> 1;
-        if (((uint32_t)(__ldg(jj + mid) - 1) >> w) < s) lo = mid + 1;
+        if (sub_of(ii, jj, mid, z, rbits) < s) lo = mid + 1;
         else hi = mid;
     }
     return lo;
 }
 
-__global__ void k_rbounds(const int32_t *__restrict__ jj, int w, int32_t nsub,
-                          uint32_t *__restrict__ bnd, uint32_t *__restrict__ biglist,
+__global__ void k_rbounds(const int32_t *__restrict__ ii, const int32_t *__restrict__ jj, int z, int rbits,
+                          int32_t nsub, uint32_t *__restrict__ bnd, uint32_t *__restrict__ biglist,
                           ErrState *err) {
     const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     pdl_wait();
     if (s <= nsub) {
         const uint32_t n = *((volatile const unsigned *)&err->rvalid);
-        const uint32_t a = (s == 0) ? 0u : (s == nsub ? n : sub_lower_bound(jj, n, w, (uint32_t)s));
+        const uint32_t a = (s == 0) ? 0u : (s == nsub ? n : sub_lower_bound(ii, jj, n, z, rbits, (uint32_t)s));
         bnd[s] = a;
         if (s < nsub) {
-            const uint32_t e = (s + 1 == nsub) ? n : sub_lower_bound(jj, n, w, (uint32_t)s + 1);
+            const uint32_t e = (s + 1 == nsub) ? n : sub_lower_bound(ii, jj, n, z, rbits, (uint32_t)s + 1);
             if (e - a > (uint32_t)RF_CAP) biglist[atomicAdd(&err->rbig_n, 1u)] = (uint32_t)s;
         }
     }
@@ -620,7 +661,7 @@ __global__ void k_rbounds(const int32_t *__restrict__ jj, int w, int32_t nsub,
 
 // ---------------------------------------------------------------------------
 // k_rbig: oversize sub-buckets, one 1024-thread CTA each (grid-stride over
-// the list).  Keys (col_local << rbits | row-1) << 32 | k in scratch A, a
+// the list).  Keys (key - the sub-bucket's first key) << 32 | k in scratch A, a
 // stable LSD radix sort on the key bits (big_radix_pass, 8-bit digits, A <->
 // B), values gathered in sorted order, each run of equal keys folded from
 // +0.0 in k (= input) order, heads compacted.  Result: keys (high 32 bits)
@@ -634,16 +675,21 @@ __global__ void __launch_bounds__(BIG_NT, 1) k_rbig(RadixFoldArgs F, ErrState *e
     const int tid = threadIdx.x;
     pdl_wait();
     const unsigned nbig = *((volatile const unsigned *)&err->rbig_n);
-    const int kbits = F.w + F.rbits;
-    const int passes = (kbits + 7) / 8;
+    if (call_failed(err)) {
+        pdl_trigger();
+        return;
+    }
+    const int passes = (F.z + 7) / 8;
     for (unsigned q = blockIdx.x; q < nbig; q += gridDim.x) {
         const uint32_t s = F.biglist[q];
         const uint32_t a = F.bnd[s], n = F.bnd[s + 1] - a;
-        const uint32_t c0 = s << F.w;
+        const unsigned long long K0 = (unsigned long long)s << F.z;
+        const uint32_t c0 = (uint32_t)(K0 >> F.rbits);
+        const uint32_t roff = (uint32_t)K0 & ((F.rbits >= 32) ? 0xffffffffu : ((1u << F.rbits) - 1u));
         unsigned long long *A = F.scrA + a;
         unsigned long long *B = F.scrB + a;
         for (uint32_t k = tid; k < n; k += BIG_NT) {
-            const uint32_t key = ((uint32_t)(F.jj[a + k] - 1) - c0) << F.rbits | (uint32_t)(F.ii[a + k] - 1);
+            const uint32_t key = lkey(F.jj[a + k], F.ii[a + k], F.z, F.rbits, c0, roff);
             A[k] = ((unsigned long long)key << 32) | k;
         }
         __syncthreads();
@@ -798,13 +844,27 @@ __global__ void __launch_bounds__(RF_NT, 2) k_rfold(RadixFoldArgs F, ErrState *e
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const unsigned lt = lanemask_lt();
     pdl_wait();
+    if (call_failed(err)) {
+        pdl_trigger();
+        return;
+    }
     if (tid == 0) S.b = (int)atomicAdd(&err->rf_ticket, 1u);
     __syncthreads();
     const int64_t s = S.b;
     const uint32_t a = F.bnd[s], n = F.bnd[s + 1] - a;
-    const int64_t c0 = s << F.w;
-    const int ncol = (int)min((int64_t)1 << F.w, (int64_t)F.N - c0);
+    // sub-bucket keys [K0, K0 + 2^z): column-block plan (z >= rbits) -- the
+    // columns c0 .. c0 + 2^(z - rbits) - 1, whole; row-split plan (z < rbits)
+    // -- rows roff .. roff + 2^z - 1 of column c0 (it starts the column when
+    // roff == 0).  A local key kl = key - K0 belongs to local column
+    // (roff + kl) >> rbits and row (roff + kl) & rmask.
+    const unsigned long long K0 = (unsigned long long)s << F.z;
+    const int64_t c0 = (int64_t)(K0 >> F.rbits);
     const uint32_t rmask = (F.rbits >= 32) ? 0xffffffffu : ((1u << F.rbits) - 1u);
+    const uint32_t roff = (uint32_t)K0 & rmask;
+    // local columns (group bookkeeping) and the columns whose jc this
+    // sub-bucket writes (a row-split sub-bucket only if it starts its column)
+    const int ncol = F.z >= F.rbits ? (int)min((int64_t)1 << (F.z - F.rbits), (int64_t)F.N - c0) : 1;
+    const int njc = (F.z >= F.rbits || roff == 0) ? ncol : 0;
     unsigned long long *lbs = F.lbf + s * LB_STRIDE;
     bool over = false;
 
@@ -823,18 +883,18 @@ __global__ void __launch_bounds__(RF_NT, 2) k_rfold(RadixFoldArgs F, ErrState *e
         }
         __syncthreads();
         const long long off = S.off;
-        for (int c = tid; c < ncol; c += RF_NT) {  // first result of column c
+        for (int c = tid; c < njc; c += RF_NT) {  // first result of column c
             uint32_t lo = 0, hi = U;
             while (lo < hi) {
                 const uint32_t mid = (lo + hi) >> 1;
-                if ((uint32_t)(RK[mid] >> 32) >> F.rbits < (uint32_t)c) lo = mid + 1;
+                if ((roff + (uint32_t)(RK[mid] >> 32)) >> F.rbits < (uint32_t)c) lo = mid + 1;
                 else hi = mid;
             }
             F.jc[c0 + c] = (int32_t)(off + lo);
         }
         for (uint32_t p = tid; p < U; p += RF_NT) {
             if (off + p < F.cap) {
-                F.ir[off + p] = (int32_t)((uint32_t)(RK[p] >> 32) & rmask);
+                F.ir[off + p] = (int32_t)((roff + (uint32_t)(RK[p] >> 32)) & rmask);
                 F.pr[off + p] = __longlong_as_double((long long)RV[p]);
             } else {
                 over = true;
@@ -869,15 +929,12 @@ __global__ void __launch_bounds__(RF_NT, 2) k_rfold(RadixFoldArgs F, ErrState *e
         S.sortall = 0;
     }
     constexpr int RIPT = RF_CAP / RF_NT;
-    uint32_t kk[RIPT];  // (col_local << rbits | row-1) + 1 of records tid + u * RF_NT
+    uint32_t kk[RIPT];  // local key + 1 of records tid + u * RF_NT
 #pragma unroll
     for (int u = 0; u < RIPT; ++u) {
         const uint32_t k = tid + u * RF_NT;
         kk[u] = 0u;
-        if (k < n) {
-            const uint32_t cl = (uint32_t)(__ldg(F.jj + a + k) - 1) - (uint32_t)c0;
-            kk[u] = ((cl << F.rbits) | (uint32_t)(__ldg(F.ii + a + k) - 1)) + 1u;
-        }
+        if (k < n) kk[u] = (uint32_t)(tkey(__ldg(F.jj + a + k), __ldg(F.ii + a + k), F.rbits) - K0) + 1u;
     }
     __syncthreads();
 #pragma unroll
@@ -892,7 +949,7 @@ __global__ void __launch_bounds__(RF_NT, 2) k_rfold(RadixFoldArgs F, ErrState *e
                 const int g = atomicAdd(&S.U, 1);
                 S.glist[g] = (uint16_t)h;
                 S.gkey[g] = kk[u];
-                atomicAdd(&S.colst[(kk[u] - 1u) >> F.rbits], 1u);
+                atomicAdd(&S.colst[(roff + kk[u] - 1u) >> F.rbits], 1u);
             }
         }
     }
@@ -951,7 +1008,7 @@ __global__ void __launch_bounds__(RF_NT, 2) k_rfold(RadixFoldArgs F, ErrState *e
     }
     for (int g = tid; g < U; g += RF_NT) {
         const uint32_t kx = S.gkey[g];
-        const uint32_t q = atomicAdd(&S.colcur[(kx - 1u) >> F.rbits], 1u);
+        const uint32_t q = atomicAdd(&S.colcur[(roff + kx - 1u) >> F.rbits], 1u);
         S.ord[q] = (uint16_t)g;  // column lists (unordered)
         ckey[q] = kx;
     }
@@ -976,7 +1033,7 @@ __global__ void __launch_bounds__(RF_NT, 2) k_rfold(RadixFoldArgs F, ErrState *e
         opos[u] = 0;
         if (g < U) {
             const uint32_t kx = S.gkey[g];
-            const uint32_t cl = (kx - 1u) >> F.rbits;
+            const uint32_t cl = (roff + kx - 1u) >> F.rbits;
             const int st = S.colst[cl], en = S.colst[cl + 1];
             if (en - st > 64) {
                 S.sortall = 1;
@@ -1063,13 +1120,13 @@ __global__ void __launch_bounds__(RF_NT, 2) k_rfold(RadixFoldArgs F, ErrState *e
             for (int q = st; q < en; ++q) acc = fold_add(acc, sv[S.memb[q]]);
         }
         if (off + p < F.cap) {
-            F.ir[off + p] = (int32_t)((kx - 1u) & rmask);
+            F.ir[off + p] = (int32_t)((roff + kx - 1u) & rmask);
             F.pr[off + p] = acc;
         } else {
             over = true;
         }
     }
-    for (int c = tid; c < ncol; c += RF_NT) F.jc[c0 + c] = (int32_t)(off + S.colst[c]);
+    for (int c = tid; c < njc; c += RF_NT) F.jc[c0 + c] = (int32_t)(off + S.colst[c]);
     if (s == F.nsub - 1 && tid == 0) {
         F.jc[F.N] = (int32_t)(off + U);
         err->nnz = off + U;
@@ -1080,22 +1137,31 @@ __global__ void __launch_bounds__(RF_NT, 2) k_rfold(RadixFoldArgs F, ErrState *e
 }
 
 // ---- launchers -----------------------------------------------------------------
-cudaError_t launch_rup(Launch &lc, bool first, const int32_t *jj, int64_t L, int32_t N, int shift,
-                       int bits, uint16_t *cnt, uint32_t *bsum, uint32_t *off, ErrState *err) {
+// Chunks per upsweep block: RP_BLK, fewer for small inputs so that every SM
+// gets about four blocks.
+int rup_cpb(int64_t nchunk, int num_sms) {
+    return (int)std::max<int64_t>(1, std::min<int64_t>(RP_BLK, nchunk / (4 * (int64_t)num_sms)));
+}
+
+cudaError_t launch_rup(Launch &lc, bool first, const int32_t *ii, const int32_t *jj, int64_t L, int32_t N,
+                       int shift, int bits, int rbits, uint16_t *cnt, uint32_t *bsum, uint32_t *off,
+                       ErrState *err) {
     // grid sized for L (an upper bound of the valid count the later passes read)
     const int64_t nchunk = (L + RP_CHUNK - 1) / RP_CHUNK;
-    const int nblk = (int)std::max<int64_t>(1, (nchunk + RP_BLK - 1) / RP_BLK);
-    cudaError_t e = first ? launch_pdl(k_rup<true>, dim3((unsigned)nblk), dim3(RU_NT), 0, lc.stream, jj, L,
-                                       N, shift, bits, cnt, bsum, err)
-                          : launch_pdl(k_rup<false>, dim3((unsigned)nblk), dim3(RU_NT), 0, lc.stream, jj, L,
-                                       N, shift, bits, cnt, bsum, err);
+    const int cpb = rup_cpb(nchunk, lc.num_sms);
+    const int nblk = (int)std::max<int64_t>(1, (nchunk + cpb - 1) / cpb);
+    const bool rowkey = shift < rbits;
+    auto kern = first ? (rowkey ? k_rup<true, true> : k_rup<true, false>)
+                      : (rowkey ? k_rup<false, true> : k_rup<false, false>);
+    cudaError_t e = launch_pdl(kern, dim3((unsigned)nblk), dim3(RU_NT), 0, lc.stream, ii, jj, L, N, shift, bits,
+                               rbits, cpb, cnt, bsum, err);
     lc.launches++;
     if (e != cudaSuccess) return e;
     e = launch_pdl(k_rscan, dim3(1), dim3(RP_MAXD), 0, lc.stream, bsum, nblk, bits);
     lc.launches++;
     if (e != cudaSuccess) return e;
     e = launch_pdl(k_roff, dim3((unsigned)nblk), dim3(RP_MAXD), 0, lc.stream, (const uint16_t *)cnt,
-                   (const uint32_t *)bsum, bits, off, err, L, first ? 1 : 0);
+                   (const uint32_t *)bsum, bits, off, err, L, first ? 1 : 0, cpb);
     lc.launches++;
     return e;
 }
@@ -1143,11 +1209,11 @@ cudaError_t launch_rpass(Launch &lc, const RadixPassArgs &A, bool first, int nse
     return e;
 }
 
-cudaError_t launch_rbounds(Launch &lc, const int32_t *jj, int w, int32_t nsub, uint32_t *bnd,
-                           uint32_t *biglist, ErrState *err) {
+cudaError_t launch_rbounds(Launch &lc, const int32_t *ii, const int32_t *jj, int z, int rbits,
+                           int32_t nsub, uint32_t *bnd, uint32_t *biglist, ErrState *err) {
     const int64_t n = (int64_t)nsub + 1;
     cudaError_t e = launch_pdl(k_rbounds, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, lc.stream,
-                               jj, w, nsub, bnd, biglist, err);
+                               ii, jj, z, rbits, nsub, bnd, biglist, err);
     lc.launches++;
     return e;
 }

@@ -749,3 +749,21 @@ def test_partition_unaligned_inputs(world, self_rank):
     assert [hc[r] for r in range(world)] == rcounts
     assert torch.equal(outs[0][:k].cpu(), ref[0]) and torch.equal(outs[1][:k].cpu(), ref[1])
     assert outs[2][:k].cpu().numpy().tobytes() == ref[2].numpy().tobytes()
+
+
+@pytest.mark.parametrize("m,n,L", [(1_000_000, 1, 2_000_000), (1_000_000, 20, 3_000_000), (1000, 1, 2_000_000),
+                                   (5_000_000, 3, 1_500_000), (300, 7, 200_000)])
+def test_long_columns_row_split_bit_exact(m, n, L):
+    """Few, long columns (the reference's long-run instances, conftest.py:43-45,
+    at scale): the automatic choice takes the radix path's row-split plan
+    (sub-buckets of 2^z rows of one column, spread over all SMs; a column
+    longer than a sub-bucket's capacity per key range goes to k_rbig) --
+    bit-exact against the C oracle, jc included for the columns whose start
+    lies inside a sub-bucket."""
+    from paper_1406_1066_b200 import workloads as W
+
+    w = W.random_coo(m=m, n=n, L=L, seed=m + n)
+    got = sa.assemble(w.ii.numpy(), w.jj.numpy(), w.s.numpy(), m=m, n=n)
+    ref = O.assemble_counting(w.ii.numpy(), w.jj.numpy(), w.s.numpy(), m, n)
+    _same(got, ref)
+    assert sa.default_assembler(0).launch_count() > 6  # the radix pipeline ran

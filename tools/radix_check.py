@@ -84,6 +84,10 @@ def main():
     ok &= check(asm, W.heavy_dup(m=20_000, positions=200_000), "heavy_dup small")
     ok &= check(asm, W.fem2d(64), "fem2d 64")
     ok &= check(asm, W.fem3d(20), "fem3d 20")
+    ok &= check(asm, W.random_coo(m=1_000_000, n=1, L=2_000_000, seed=6), "one long column (row split)")
+    ok &= check(asm, W.random_coo(m=1_000_000, n=20, L=3_000_000, seed=7), "20 long columns (row split)")
+    ok &= check(asm, W.random_coo(m=1000, n=1, L=2_000_000, seed=8), "one column, 1000 rows")
+    ok &= check(asm, W.random_coo(m=5_000_000, n=3, L=1_500_000, seed=9), "3 columns, sparse rows")
     ok &= check(asm, W.config(4, scale=0.02), "cfg4 x0.02")
     ok &= check(asm, W.config(2, device=dev), "cfg2 full")
     ok &= check(asm, W.config(3, device=dev), "cfg3 full")
