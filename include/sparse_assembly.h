@@ -178,7 +178,9 @@ int sa_host_fetch(sa_ctx *ctx, int32_t *h_jc, int32_t *h_ir, double *h_pr);
 /*
  * Page-locked host buffers from a process-wide cache (size classes of powers
  * of two), for host outputs that the device->host copies fill at full link
- * bandwidth.  sa_host_buffer returns NULL on failure.
+ * bandwidth.  The process keeps at most 2 GB of released blocks for reuse and
+ * hands out at most 16 GB at a time; sa_host_buffer returns NULL beyond that
+ * or on failure (callers then use pageable memory).
  */
 void *sa_host_buffer(uint64_t bytes);
 void sa_host_buffer_release(void *ptr);

@@ -308,7 +308,7 @@ class _PinnedBlock:
         nbytes = max(int(n), 1) * np.dtype(dtype).itemsize
         self._ptr = lib.sa_host_buffer(nbytes)
         if not self._ptr:
-            raise MemoryError(f"page-locked host allocation of {nbytes} bytes failed")
+            raise MemoryError(f"page-locked host allocation of {nbytes} bytes failed or over the cap")
         self.__array_interface__ = {"data": (self._ptr, False), "shape": (int(n),),
                                     "typestr": np.dtype(dtype).str, "version": 3}
 
@@ -320,8 +320,14 @@ class _PinnedBlock:
 
 def _pinned_empty(n, dtype):
     """numpy array in page-locked memory (returned to the cache when the
-    array and all its views are gone)."""
-    return np.asarray(_PinnedBlock(_capi.load(), n, dtype))
+    array and all its views are gone), so the device->host copy runs at full
+    PCIe bandwidth.  The library bounds what it keeps page-locked (2 GB of
+    free blocks, 16 GB of live results, sa_capi.cu PinnedCache); beyond that,
+    or if pinning fails, an ordinary (pageable) array."""
+    try:
+        return np.asarray(_PinnedBlock(_capi.load(), n, dtype))
+    except MemoryError:
+        return np.empty(max(int(n), 0), dtype=dtype)
 
 
 def _bad_value(arr, k):

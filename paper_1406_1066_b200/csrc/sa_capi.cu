@@ -206,8 +206,13 @@ struct PinnedCache {
     std::mutex mu;
     std::map<uint64_t, std::vector<void *>> free_by_class;  // class bytes -> blocks
     std::unordered_map<void *, uint64_t> live;               // block -> class bytes
-    uint64_t cached = 0;
-    static constexpr uint64_t kMaxCached = 8ull << 30;
+    uint64_t cached = 0;      // bytes in free blocks
+    uint64_t live_bytes = 0;  // bytes handed out and not yet released
+    // bounds on the host RAM this library keeps page-locked: free blocks kept
+    // for reuse, and results handed out (beyond it callers get nullptr and
+    // fall back to pageable memory)
+    static constexpr uint64_t kMaxCached = 2ull << 30;
+    static constexpr uint64_t kMaxLive = 16ull << 30;
 };
 PinnedCache &pinned_cache() {
     static PinnedCache *c = new PinnedCache();  // leaked on purpose (process lifetime)
@@ -233,13 +238,16 @@ void *sa_host_buffer(uint64_t bytes) {
             it->second.pop_back();
             pc.cached -= cls;
             pc.live[p] = cls;
+            pc.live_bytes += cls;
             return p;
         }
+        if (pc.live_bytes + cls > PinnedCache::kMaxLive) return nullptr;
     }
     void *p = nullptr;
     if (cudaHostAlloc(&p, cls, cudaHostAllocPortable) != cudaSuccess) return nullptr;
     std::lock_guard<std::mutex> g(pc.mu);
     pc.live[p] = cls;
+    pc.live_bytes += cls;
     return p;
 }
 
@@ -253,6 +261,7 @@ void sa_host_buffer_release(void *ptr) {
         if (it == pc.live.end()) return;
         cls = it->second;
         pc.live.erase(it);
+        pc.live_bytes -= cls;
         if (pc.cached + cls <= PinnedCache::kMaxCached) {
             pc.free_by_class[cls].push_back(ptr);
             pc.cached += cls;
