@@ -162,9 +162,14 @@ const int64_t *sa_device_nnz(sa_ctx *ctx);
  * arrays in, a fresh host CSC out).  nnz is unknown until the device has
  * assembled, so -- as in the reference, which sizes ir/pr after Part 4
  * (serial.py:153-158) -- the caller allocates its outputs between steps:
- *   1. sa_host_upload   : enqueue host->device copies of the triplets
- *                         (pinned host memory gives full PCIe bandwidth)
- *   2. sa_host_dims     : optional, infer M = max(i), N = max(j) (sync)
+ *   1. sa_host_upload   : enqueue host->device copies of the triplets in
+ *                         chunks (pinned host memory gives full PCIe
+ *                         bandwidth); the validation / maxima pass of each
+ *                         chunk runs on a second stream as soon as the
+ *                         chunk has landed, overlapped with the next copy
+ *                         (types.py:121-138, 163-165 fused into the upload)
+ *   2. sa_host_dims     : optional, M = max(i), N = max(j) or the first bad
+ *                         index from that pass (sync; no further pass)
  *   3. sa_host_assemble : assemble the uploaded triplets (sync), -> nnz
  *   4. sa_host_fetch    : copy jc[N+1], ir[nnz], pr[nnz] to the host (sync)
  */

@@ -56,6 +56,15 @@ struct sa_ctx {
     unsigned rp_epoch = 0;                                             // look-back tag epoch
     ErrState *err = nullptr;              // device
     ErrState *err_host = nullptr;         // pinned mirror
+    // host protocol: the dimension / validation pass runs on up_stream over
+    // each uploaded chunk while the next one is copied (sa_host_upload), its
+    // outcome in err_up; up_done marks its end
+    cudaStream_t up_stream = nullptr;
+    ErrState *err_up = nullptr;
+    ErrState *err_up_host = nullptr;
+    cudaEvent_t up_done = nullptr;
+    static constexpr int MAXUP = 64;
+    cudaEvent_t up_ev[MAXUP] = {};
 
     // buffers of the host-pointer entry point
     int32_t *h_ii = nullptr;                   size_t hii_cap = 0;
@@ -304,6 +313,12 @@ int sa_create(int device, sa_ctx **out) {
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void **>(&ctx->err), sizeof(ErrState));
     if (e == cudaSuccess) e = cudaMallocHost(reinterpret_cast<void **>(&ctx->err_host), sizeof(ErrState));
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->up_stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void **>(&ctx->err_up), sizeof(ErrState));
+    if (e == cudaSuccess) e = cudaMallocHost(reinterpret_cast<void **>(&ctx->err_up_host), sizeof(ErrState));
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->up_done, cudaEventDisableTiming);
+    for (int k = 0; k < sa_ctx::MAXUP && e == cudaSuccess; ++k)
+        e = cudaEventCreateWithFlags(&ctx->up_ev[k], cudaEventDisableTiming);
     if (e != cudaSuccess) {
         int rc = cuda_fail(ctx, e, "sa_create");
         sa_destroy(ctx);
@@ -318,6 +333,15 @@ void sa_destroy(sa_ctx *ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    if (ctx->up_stream) {
+        cudaStreamSynchronize(ctx->up_stream);
+        cudaStreamDestroy(ctx->up_stream);
+    }
+    cudaFree(ctx->err_up);
+    cudaFreeHost(ctx->err_up_host);
+    if (ctx->up_done) cudaEventDestroy(ctx->up_done);
+    for (auto ev : ctx->up_ev)
+        if (ev) cudaEventDestroy(ev);
     cudaFree(ctx->cur);
     cudaFree(ctx->sstart);
     cudaFree(ctx->rec);
@@ -685,7 +709,8 @@ int assemble_segments(sa_ctx *ctx, const Segs &S, int64_t L, int32_t M, int32_t 
         // exceeds N and k_hist flags DimensionTooSmall (no histogram writes)
         if (L > 0 && !S.skip_foreign)
             for (int g = 0; g < S.nseg; ++g)
-                SA_CUDA(ctx, launch_hist(lc, S.ii[g], S.jj[g], S.len[g], M, N, ctx->cur, ctx->err, false));
+                SA_CUDA(ctx, launch_hist(lc, S.ii[g], S.jj[g], S.len[g], M, N, ctx->cur, ctx->err, false,
+                                         S.pos0[g]));
         SA_CUDA(ctx, cudaMemsetAsync(d_jc, 0, ((size_t)N + 1) * sizeof(int32_t), ctx->stream));
         ctx->launches = lc.launches;
         return SA_OK;
@@ -841,21 +866,58 @@ int sa_host_upload(sa_ctx *ctx, const int32_t *h_ii, const int32_t *h_jj, const 
     }
     const size_t nl = (size_t)std::max<int64_t>(L, 1);
     const size_t ns = s_stride ? nl : 1;
+    // the previous upload's dimension pass may still read the buffers (the
+    // assembly itself never waits for it)
+    SA_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->up_done, 0));
+    SA_CUDA(ctx, cudaStreamSynchronize(ctx->up_stream));
     SA_CUDA(ctx, ensure(ctx->h_ii, ctx->hii_cap, nl));
     SA_CUDA(ctx, ensure(ctx->h_jj, ctx->hjj_cap, nl));
     SA_CUDA(ctx, ensure(ctx->h_s, ctx->hs_cap, ns));
-    if (L > 0) {
-        SA_CUDA(ctx, cudaMemcpyAsync(ctx->h_ii, h_ii, (size_t)L * 4, cudaMemcpyHostToDevice, ctx->stream));
-        SA_CUDA(ctx, cudaMemcpyAsync(ctx->h_jj, h_jj, (size_t)L * 4, cudaMemcpyHostToDevice, ctx->stream));
-        SA_CUDA(ctx, cudaMemcpyAsync(ctx->h_s, h_s, ns * 8, cudaMemcpyHostToDevice, ctx->stream));
+    // the dimension / validation pass (types.py:121-138, 163-165: maxima and
+    // first bad positions) is fused into the upload: it runs on up_stream
+    // over each chunk as soon as it has landed, overlapped with the copy of
+    // the next one, so sa_host_dims only reads its outcome
+    {
+        ErrState z{};
+        z.bad_i = ~0ull;
+        z.bad_j = ~0ull;
+        *ctx->err_up_host = z;
     }
+    SA_CUDA(ctx, cudaMemcpyAsync(ctx->err_up, ctx->err_up_host, sizeof(ErrState), cudaMemcpyHostToDevice,
+                                 ctx->stream));
+    if (L > 0) {
+        const int64_t nch = std::min<int64_t>(sa_ctx::MAXUP, std::max<int64_t>(1, L >> 24));  // >= 16M per chunk
+        Launch lc{ctx->up_stream, ctx->num_sms, 0};
+        for (int64_t k = 0; k < nch; ++k) {
+            const int64_t a = (L * k / nch) & ~(int64_t)3, b = (k + 1 == nch) ? L : ((L * (k + 1) / nch) & ~(int64_t)3);
+            if (b <= a) continue;
+            SA_CUDA(ctx, cudaMemcpyAsync(ctx->h_ii + a, h_ii + a, (size_t)(b - a) * 4, cudaMemcpyHostToDevice, ctx->stream));
+            SA_CUDA(ctx, cudaMemcpyAsync(ctx->h_jj + a, h_jj + a, (size_t)(b - a) * 4, cudaMemcpyHostToDevice, ctx->stream));
+            if (s_stride)
+                SA_CUDA(ctx, cudaMemcpyAsync(ctx->h_s + a, h_s + a, (size_t)(b - a) * 8, cudaMemcpyHostToDevice, ctx->stream));
+            SA_CUDA(ctx, cudaEventRecord(ctx->up_ev[k], ctx->stream));
+            SA_CUDA(ctx, cudaStreamWaitEvent(ctx->up_stream, ctx->up_ev[k], 0));
+            SA_CUDA(ctx, launch_hist(lc, ctx->h_ii + a, ctx->h_jj + a, b - a, 0, 0, nullptr, ctx->err_up, true, a));
+        }
+        if (!s_stride) SA_CUDA(ctx, cudaMemcpyAsync(ctx->h_s, h_s, 8, cudaMemcpyHostToDevice, ctx->stream));
+    }
+    SA_CUDA(ctx, cudaEventRecord(ctx->up_done, ctx->up_stream));
     return SA_OK;
 }
 
 int sa_host_dims(sa_ctx *ctx, int32_t *M, int32_t *N, int64_t *bad_pos, int *bad_which) {
     if (!ctx) return SA_ERR_INVALID_ARG;
     if (ctx->host_L < 0) return fail(ctx, SA_ERR_INVALID_ARG, "sa_host_dims: nothing uploaded");
-    return sa_infer_dims(ctx, ctx->h_ii, ctx->h_jj, ctx->host_L, M, N, bad_pos, bad_which);
+    SA_CUDA(ctx, cudaSetDevice(ctx->device));
+    // the outcome of the pass the upload ran (no further pass over the data)
+    SA_CUDA(ctx, cudaMemcpyAsync(ctx->err_up_host, ctx->err_up, sizeof(ErrState), cudaMemcpyDeviceToHost,
+                                 ctx->up_stream));
+    SA_CUDA(ctx, cudaStreamSynchronize(ctx->up_stream));
+    ErrState e = *ctx->err_up_host;
+    if (M) *M = (int32_t)e.max_i;
+    if (N) *N = (int32_t)e.max_j;
+    e.nnz = 0;
+    return decode(ctx, e, nullptr, bad_pos, bad_which);
 }
 
 int sa_host_assemble(sa_ctx *ctx, int32_t M, int32_t N, int64_t *nnz, int64_t *bad_pos,

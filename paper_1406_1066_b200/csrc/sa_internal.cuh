@@ -393,7 +393,8 @@ struct Launch {
 cudaError_t launch_convert(Launch &lc, const void *raw, int dtype, int64_t L, int32_t *out,
                            ErrState *err);
 cudaError_t launch_hist(Launch &lc, const int32_t *ii, const int32_t *jj, int64_t L,
-                        int32_t M, int32_t N, uint32_t *cnt, ErrState *err, bool infer);
+                        int32_t M, int32_t N, uint32_t *cnt, ErrState *err, bool infer,
+                        int64_t pos0 = 0);
 cudaError_t launch_col_scan(Launch &lc, const uint32_t *cnt, uint32_t *sstart, uint32_t *cur,
                             int32_t N, int2 *tile_info, uint8_t *tile_big,
                             int64_t ntiles, BigCol *big_list, uint32_t *bigk,

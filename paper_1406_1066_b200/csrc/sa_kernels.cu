@@ -125,7 +125,7 @@ __device__ __forceinline__ void hist_one(int64_t t, int32_t i, int32_t j, bool l
 __global__ void __launch_bounds__(256) k_hist(const int32_t *__restrict__ ii,
                                               const int32_t *__restrict__ jj, int64_t L,
                                               int32_t M, int32_t N, uint32_t *__restrict__ cnt,
-                                              ErrState *err, int vec, int infer) {
+                                              ErrState *err, int vec, int infer, int64_t pos0) {
     HistAcc a;
     if (infer) cnt = nullptr;
     const int lane = threadIdx.x & 31;
@@ -166,9 +166,9 @@ __global__ void __launch_bounds__(256) k_hist(const int32_t *__restrict__ ii,
         a.over_m |= __shfl_xor_sync(FULL, a.over_m, o);
         a.over_n |= __shfl_xor_sync(FULL, a.over_n, o);
     }
-    if (lane == 0) {
-        if (a.bad_i != ~0ull) atomicMin(&err->bad_i, a.bad_i);
-        if (a.bad_j != ~0ull) atomicMin(&err->bad_j, a.bad_j);
+    if (lane == 0) {  // (positions of this array slice + pos0: global input positions)
+        if (a.bad_i != ~0ull) atomicMin(&err->bad_i, a.bad_i + (unsigned long long)pos0);
+        if (a.bad_j != ~0ull) atomicMin(&err->bad_j, a.bad_j + (unsigned long long)pos0);
         if (infer) {
             if (a.maxi) atomicMax(&err->max_i, a.maxi);
             if (a.maxj) atomicMax(&err->max_j, a.maxj);
@@ -181,12 +181,12 @@ __global__ void __launch_bounds__(256) k_hist(const int32_t *__restrict__ ii,
 static inline bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 cudaError_t launch_hist(Launch &lc, const int32_t *ii, const int32_t *jj, int64_t L, int32_t M,
-                        int32_t N, uint32_t *cnt, ErrState *err, bool infer) {
+                        int32_t N, uint32_t *cnt, ErrState *err, bool infer, int64_t pos0) {
     if (L <= 0) return cudaSuccess;
     const int vec = aligned16(ii) && aligned16(jj);
     int64_t want = ((vec ? (L >> 2) : L) + 255) / 256 + 1;
     int grid = (int)std::min<int64_t>(want, (int64_t)lc.num_sms * 8);
-    k_hist<<<grid, 256, 0, lc.stream>>>(ii, jj, L, M, N, cnt, err, vec, infer ? 1 : 0);
+    k_hist<<<grid, 256, 0, lc.stream>>>(ii, jj, L, M, N, cnt, err, vec, infer ? 1 : 0, pos0);
     lc.launches++;
     return cudaGetLastError();
 }

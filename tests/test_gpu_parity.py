@@ -767,3 +767,30 @@ def test_long_columns_row_split_bit_exact(m, n, L):
     ref = O.assemble_counting(w.ii.numpy(), w.jj.numpy(), w.s.numpy(), m, n)
     _same(got, ref)
     assert sa.default_assembler(0).launch_count() > 6  # the radix pipeline ran
+
+
+def test_host_dims_inferred_during_chunked_upload():
+    """Dimension inference fused into the upload (sa_host_upload runs the
+    validation / maxima pass over each landed chunk while the next one is
+    copied; sa_host_dims only reads it): inferred m, n over a multi-chunk
+    input, and a bad index in a later chunk reported at its GLOBAL position
+    (reference types.py:121-138, 161-165)."""
+    rng = np.random.default_rng(11)
+    L = 40_000_000
+    ii = rng.integers(1, 70_001, size=L, dtype=np.int32)
+    jj = rng.integers(1, 50_001, size=L, dtype=np.int32)
+    s = np.ones(L)
+    ii[123] = 90_000  # the row maximum, in the first chunk
+    jj[L - 5] = 60_000  # the column maximum, in the last chunk
+    out = sa.assemble(ii, jj, s)
+    assert (out.m, out.n) == (90_000, 60_000)
+    assert int(out.jc[-1]) == len(out.ir) and float(out.pr.sum()) == float(L)
+    jj[35_000_001] = 0
+    ii[39_000_002] = -2
+    with pytest.raises(sa.BadIndex) as e:  # rows before columns
+        sa.assemble(ii, jj, s)
+    assert (e.value.position, e.value.value) == (39_000_002, -2)
+    ii[39_000_002] = 5
+    with pytest.raises(sa.BadIndex) as e:
+        sa.assemble(ii, jj, s)
+    assert (e.value.position, e.value.value) == (35_000_001, 0)
