@@ -1169,14 +1169,19 @@ cudaError_t launch_rup(Launch &lc, bool first, const int32_t *ii, const int32_t 
 template <bool FIRST, int BITS>
 static cudaError_t launch_rpass_t(Launch &lc, const RadixPassArgs &A, int nseg, ErrState *err) {
     auto al16 = [](const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
-    // TMA-staged input: measured faster for the later passes (cfg4 pass 2:
-    // 7.0 -> 6.0 ms) and slower for the first (8.3 -> 9.7 ms)
-    const bool tma = lc.rpass_tma >= 0 ? lc.rpass_tma == 1 : !FIRST;
+    // TMA-staged input (cfg4: pass 1 8.3 -> 7.0 ms, pass 2 7.0 -> 6.1 ms)
+    const bool tma = lc.rpass_tma != 0;
     if (tma && al16(A.ii_in) && al16(A.jj_in) && (A.s_stride == 0 || al16(A.s_in))) {
         const int smem = (int)sizeof(PassTmaSmem);
         cudaError_t e = ensure_smem_attr((const void *)k_rpass_tma<FIRST, BITS>, smem);
         if (e != cudaSuccess) return e;
-        return launch_pdl(k_rpass_tma<FIRST, BITS>, dim3((unsigned)lc.num_sms), dim3(RP_NT), smem, lc.stream,
+        // grid: the first pass runs best with many short-lived CTAs (about 8
+        // chunks each; cfg4: 8.8 ms at one CTA per SM, 7.0 ms at 64 waves),
+        // the later ones with one CTA per SM (6.1 ms; 3 waves: 7.0 ms) --
+        // measured, tools/variant_time.py
+        const int64_t nch = (A.L + RP_CHUNK - 1) / RP_CHUNK;
+        const int64_t grid = FIRST ? std::max<int64_t>(lc.num_sms, (nch + 7) / 8) : lc.num_sms;
+        return launch_pdl(k_rpass_tma<FIRST, BITS>, dim3((unsigned)grid), dim3(RP_NT), smem, lc.stream,
                           A, err);
     }
     const int smem = (int)sizeof(PassSmem);

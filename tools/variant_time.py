@@ -1,6 +1,6 @@
 """Step time and per-kernel times of BASELINE configs under context-option
 variants (dev A/B tool).  usage: python tools/variant_time.py CFG[,CFG..] [OPT=VAL ...]
-e.g. python tools/variant_time.py 5 SCATTER_STAGED=0 SCATTER_STAGED=1"""
+e.g. python tools/variant_time.py 5 SCATTER_STAGED=0 SCATTER_STAGED=1 PATH=1,RPASS_TMA=1"""
 import ctypes, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -10,7 +10,7 @@ from paper_1406_1066_b200 import _capi, workloads as W
 asm = sa.default_assembler(0)
 lib, ctx = asm.lib, asm.ctx
 dev = torch.device("cuda", 0)
-variants = [None] + [v.split("=") for v in sys.argv[2:]]
+variants = [None] + [[kv.split("=") for kv in v.split(",")] for v in sys.argv[2:]]
 for cfg in [int(c) for c in sys.argv[1].split(",")]:
     w = W.config(cfg, device=dev)
     L = w.L
@@ -19,8 +19,8 @@ for cfg in [int(c) for c in sys.argv[1].split(",")]:
     pr = torch.empty(L, dtype=torch.float64, device=dev)
     asm._bind_stream()
     for var in variants:
-        if var:
-            asm.set_option(getattr(_capi, "SA_OPT_" + var[0]), int(var[1]))
+        for o, v in (var or []):
+            asm.set_option(getattr(_capi, "SA_OPT_" + o), int(v))
         def step():
             rc = lib.sa_assemble_async(ctx, w.ii.data_ptr(), w.jj.data_ptr(), w.s.data_ptr(), 1, L, w.m, w.n,
                                        jc.data_ptr(), ir.data_ptr(), pr.data_ptr(), L)
@@ -47,10 +47,10 @@ for cfg in [int(c) for c in sys.argv[1].split(",")]:
         lib.sa_enable_timing(ctx, 0)
         nnz = ctypes.c_int64(0)
         rc = lib.sa_finish(ctx, ctypes.byref(nnz), None, None)
-        tag = "=".join(var) if var else "auto"
+        tag = ",".join("=".join(x) for x in var) if var else "auto"
         print(f"cfg{cfg} {tag:22s} {ms:8.3f} ms  nnz={nnz.value} rc={rc} "
               + " ".join(f"{k}={sum(v)/len(v):.3f}" for k, v in kt.items()), flush=True)
-        if var:
-            asm.set_option(getattr(_capi, "SA_OPT_" + var[0]), -1)
+        for o, v in (var or []):
+            asm.set_option(getattr(_capi, "SA_OPT_" + o), -1)
     del w, jc, ir, pr
     torch.cuda.empty_cache()
