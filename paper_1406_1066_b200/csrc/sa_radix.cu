@@ -911,11 +911,11 @@ __global__ void __launch_bounds__(RF_NT, 2) k_rfold(RadixFoldArgs F, ErrState *e
     }
 
     // ---- 1. groups -------------------------------------------------------
-    {  // the sub-bucket's values into L1 while the groups are built (the fold reads them)
+    {  // the sub-bucket's values into L2 while the groups are built (staged later)
         const char *vb = reinterpret_cast<const char *>(F.s + a);
         const uint32_t nb = n * 8u;
         for (uint32_t o = (uint32_t)tid * 128u; o < nb; o += RF_NT * 128u)
-            asm volatile("prefetch.global.L1 [%0];" ::"l"(vb + o));
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(vb + o));
     }
     int hbits = 6;
     while ((1u << hbits) < 2 * n) ++hbits;
