@@ -183,7 +183,7 @@ int sa_host_fetch(sa_ctx *ctx, int32_t *h_jc, int32_t *h_ir, double *h_pr);
 /*
  * Page-locked host buffers from a process-wide cache (size classes of powers
  * of two), for host outputs that the device->host copies fill at full link
- * bandwidth.  The process keeps at most 2 GB of released blocks for reuse and
+ * bandwidth.  The process keeps at most 8 GB of released blocks for reuse and
  * hands out at most 16 GB at a time; sa_host_buffer returns NULL beyond that
  * or on failure (callers then use pageable memory).
  */

@@ -321,7 +321,7 @@ class _PinnedBlock:
 def _pinned_empty(n, dtype):
     """numpy array in page-locked memory (returned to the cache when the
     array and all its views are gone), so the device->host copy runs at full
-    PCIe bandwidth.  The library bounds what it keeps page-locked (2 GB of
+    PCIe bandwidth.  The library bounds what it keeps page-locked (8 GB of
     free blocks, 16 GB of live results, sa_capi.cu PinnedCache); beyond that,
     or if pinning fails, an ordinary (pageable) array."""
     try:

@@ -220,7 +220,7 @@ struct PinnedCache {
     // bounds on the host RAM this library keeps page-locked: free blocks kept
     // for reuse, and results handed out (beyond it callers get nullptr and
     // fall back to pageable memory)
-    static constexpr uint64_t kMaxCached = 2ull << 30;
+    static constexpr uint64_t kMaxCached = 8ull << 30;
     static constexpr uint64_t kMaxLive = 16ull << 30;
 };
 PinnedCache &pinned_cache() {

@@ -295,8 +295,9 @@ def assemble_sharded(ii: torch.Tensor, jj: torch.Tensor, s: torch.Tensor, m: int
     lens[rank] = int(jj.shape[0])
     red = torch.cat([hist.to(torch.int64), lens])
     dist.all_reduce(red, group=group)
+    red = red.cpu()  # one host read: the boundaries and the chunk offset
     hist = red[:nblocks]
-    chunk_off = int(red[nblocks:nblocks + rank].sum().item()) if rank else 0
+    chunk_off = int(red[nblocks:nblocks + rank].sum()) if rank else 0
     bounds = block_boundaries(hist, world, nblocks, n)
     launches = 0
     if cuda:
@@ -344,10 +345,12 @@ def assemble_sharded(ii: torch.Tensor, jj: torch.Tensor, s: torch.Tensor, m: int
         cat_s = torch.cat([lower[2], sv[mine], higher[2]])
         jc, ir, pr = local_assemble(cat_i, (cat_j.to(torch.int64) - col_lo).to(torch.int32), cat_s, m,
                                     n_local)
-    nnz_local = torch.tensor([int(jc[-1]) if len(jc) else 0], dtype=torch.int64, device=dev)
+    # the rank's nnz is known on the host already (the local assembly
+    # synchronised for it); one all_gather and one host read for all ranks'
+    nnz_local = torch.tensor([int(ir.shape[0])], dtype=torch.int64, device=dev)
     all_nnz = [torch.empty_like(nnz_local) for _ in range(world)]
     dist.all_gather(all_nnz, nnz_local, group=group)
-    nn = [int(x.item()) for x in all_nnz]
+    nn = torch.cat(all_nnz).cpu().tolist()
     off = sum(nn[:rank])
     if out is not None and cuda:
         b = out.get("jc64")
