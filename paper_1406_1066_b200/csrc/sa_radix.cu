@@ -137,7 +137,11 @@ __global__ void __launch_bounds__(RU_NT) k_rup(const int32_t *__restrict__ ii, c
                                                int64_t L, int32_t N, int shift, int bits, int rbits, int cpb,
                                                uint16_t *__restrict__ cnt, uint32_t *__restrict__ bsum,
                                                ErrState *err) {
-    __shared__ uint32_t h[RP_MAXD];
+    // two histograms: chunk c counts into h[c & 1] while the loads of chunk
+    // c + 1 are in flight; one barrier per chunk (the owner of digit k writes
+    // out and clears its counter for chunk c + 2)
+    __shared__ uint32_t h[2][RP_MAXD];
+    for (int k = threadIdx.x; k < 2 * RP_MAXD; k += RU_NT) h[k >> RP_MAXBITS][k & (RP_MAXD - 1)] = 0;
     pdl_wait();
     const int64_t Lp = FIRST ? L : (int64_t)*((volatile const unsigned *)&err->rvalid);
     const int64_t nchunk = (Lp + RP_CHUNK - 1) / RP_CHUNK;
@@ -146,19 +150,26 @@ __global__ void __launch_bounds__(RU_NT) k_rup(const int32_t *__restrict__ ii, c
     unsigned long long bad = ~0ull;
     unsigned over = 0, nval = 0;
     uint32_t bs = 0;  // block sum of digit threadIdx.x
-    const int64_t cb = (int64_t)blockIdx.x * cpb;
-    for (int64_t c = cb; c < min(nchunk, cb + cpb); ++c) {
-        for (int k = threadIdx.x; k < ndig; k += RU_NT) h[k] = 0;
-        __syncthreads();
+    constexpr int UPT = RP_CHUNK / RU_NT;
+    const int64_t cb = (int64_t)blockIdx.x * cpb, ce = min(nchunk, cb + cpb);
+    int v[UPT];
+    auto load = [&](int64_t c, int (&x)[UPT]) {
         const int64_t lo = c * RP_CHUNK, hi = min(Lp, lo + RP_CHUNK);
-        int v[RP_CHUNK / RU_NT];
 #pragma unroll
-        for (int u = 0; u < RP_CHUNK / RU_NT; ++u) {
+        for (int u = 0; u < UPT; ++u) {
             const int64_t t = lo + threadIdx.x + (int64_t)u * RU_NT;
-            v[u] = (t < hi) ? __ldcs(jj + t) : 0;
+            x[u] = (t < hi) ? __ldcs(jj + t) : 0;
         }
+    };
+    if (cb < ce) load(cb, v);
+    __syncthreads();
+    for (int64_t c = cb; c < ce; ++c) {
+        int vn[UPT];
+        if (c + 1 < ce) load(c + 1, vn);
+        uint32_t *hc = h[c & 1];
+        const int64_t lo = c * RP_CHUNK, hi = min(Lp, lo + RP_CHUNK);
 #pragma unroll
-        for (int u = 0; u < RP_CHUNK / RU_NT; ++u) {
+        for (int u = 0; u < UPT; ++u) {
             const int64_t t = lo + threadIdx.x + (int64_t)u * RU_NT;
             if (t >= hi) continue;
             const int cc = v[u];
@@ -166,18 +177,20 @@ __global__ void __launch_bounds__(RU_NT) k_rup(const int32_t *__restrict__ ii, c
             else if (FIRST && cc > N) over = 1;
             else {
                 if (ROWKEY)  // the digit takes row bits (row-split plan)
-                    atomicAdd(&h[key_digit(cc, __ldcs(ii + t), shift, rbits, dmask)], 1u);
+                    atomicAdd(&hc[key_digit(cc, __ldcs(ii + t), shift, rbits, dmask)], 1u);
                 else
-                    atomicAdd(&h[((unsigned)(cc - 1) >> (shift - rbits)) & dmask], 1u);
+                    atomicAdd(&hc[((unsigned)(cc - 1) >> (shift - rbits)) & dmask], 1u);
                 ++nval;
             }
         }
         __syncthreads();
         for (int k = threadIdx.x; k < ndig; k += RU_NT) {
-            cnt[c * RP_MAXD + k] = (uint16_t)h[k];
-            bs += h[k];  // RU_NT == RP_MAXD: thread k owns digit k
+            cnt[c * RP_MAXD + k] = (uint16_t)hc[k];
+            bs += hc[k];  // RU_NT == RP_MAXD: thread k owns digit k
+            hc[k] = 0;
         }
-        __syncthreads();
+#pragma unroll
+        for (int u = 0; u < UPT; ++u) v[u] = vn[u];
     }
     if (threadIdx.x < ndig) bsum[(int64_t)blockIdx.x * RP_MAXD + threadIdx.x] = bs;
     if (FIRST) {
