@@ -780,20 +780,30 @@ __global__ void __launch_bounds__(BIG_NT, 1) k_rbig(RadixFoldArgs F, ErrState *e
 //      members sorted by k (insertion sort, <= 32) and folded from +0.0;
 //      ir / pr / jc written coalesced.
 // ---------------------------------------------------------------------------
-constexpr int RF_NT = 512;
-constexpr int RF_HS = 2 * RF_CAP;
+#ifndef SA_RF_NT
+#define SA_RF_NT 512
+#endif
+// 512 threads, two sub-buckets in flight per SM (8192 hash slots, 98 KB of
+// shared memory); 256 threads fit three (4096 slots, 74 KB) but measured
+// slower (cfg4 fold 8.5 -> 8.9 ms)
+constexpr int RF_NT = SA_RF_NT;
+constexpr int RF_MINB = RF_NT == 256 ? 3 : 2;
+constexpr int RF_HS = RF_NT == 256 ? RF_CAP : 2 * RF_CAP;
+constexpr int RF_HS_BITS = RF_NT == 256 ? 12 : 13;
+static_assert((1 << RF_HS_BITS) == RF_HS, "hash table size");
 constexpr int RF_BIGG = 128;  // groups of > 32 members per sub-bucket (<= RF_CAP / 33)
 
 struct FoldSmem {
+    // key, cnt2 and glist are dead by the output phase: together (>= 8 RF_CAP
+    // bytes) they take the staged values (or the fallback's sort items)
     uint32_t key[RF_HS];          // hash keys (key + 1; 0 = empty); then the column lists' keys
-                                  // (ckey), or the fallback's sort items
+                                  // (ckey)
     uint32_t cnt2[RF_HS / 2];     // per slot (16-bit halves): members, then member cursor
+    uint16_t glist[RF_CAP];       // slot of group g
     uint32_t gkey[RF_CAP];        // key + 1 of group g
     uint16_t gid[RF_CAP];         // slot of record k; then: group of output entry p
     uint16_t memb[RF_CAP];        // member records, grouped
-    uint16_t glist[RF_CAP];       // slot of group g
     uint16_t gstart[RF_CAP + 1];  // first member of group g
-    uint16_t ord[RF_CAP];         // groups listed per column (unordered)
     uint32_t colst[RF_WMAX + 1];  // distinct groups per column -> column start
     uint32_t colcur[RF_WMAX];
     uint16_t bigg[RF_BIGG];       // groups of more than 32 members
@@ -851,7 +861,7 @@ __device__ __forceinline__ void rf_isort16(uint16_t *a, int n) {  // ascending, 
     }
 }
 
-__global__ void __launch_bounds__(RF_NT, 2) k_rfold(RadixFoldArgs F, ErrState *err) {
+__global__ void __launch_bounds__(RF_NT, RF_MINB) k_rfold(RadixFoldArgs F, ErrState *err) {
     extern __shared__ __align__(16) unsigned char rf_smem[];
     FoldSmem &S = *reinterpret_cast<FoldSmem *>(rf_smem);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -931,7 +941,7 @@ __global__ void __launch_bounds__(RF_NT, 2) k_rfold(RadixFoldArgs F, ErrState *e
             asm volatile("prefetch.global.L2 [%0];" ::"l"(vb + o));
     }
     int hbits = 6;
-    while ((1u << hbits) < 2 * n) ++hbits;
+    while (hbits < RF_HS_BITS && (1u << hbits) < 2 * n) ++hbits;
     const int hs = 1 << hbits;
     for (int k = tid; k < hs; k += RF_NT) S.key[k] = 0u;
     for (int k = tid; k < hs / 2; k += RF_NT) S.cnt2[k] = 0u;
@@ -1022,8 +1032,7 @@ __global__ void __launch_bounds__(RF_NT, 2) k_rfold(RadixFoldArgs F, ErrState *e
     for (int g = tid; g < U; g += RF_NT) {
         const uint32_t kx = S.gkey[g];
         const uint32_t q = atomicAdd(&S.colcur[(roff + kx - 1u) >> F.rbits], 1u);
-        S.ord[q] = (uint16_t)g;  // column lists (unordered)
-        ckey[q] = kx;
+        ckey[q] = kx;  // column lists of the groups' keys (unordered)
     }
     __syncthreads();
     for (int q = warp; q < min(S.nbigg, RF_BIGG); q += RF_NT / 32) {  // big groups: rebuilt in order
@@ -1059,11 +1068,13 @@ __global__ void __launch_bounds__(RF_NT, 2) k_rfold(RadixFoldArgs F, ErrState *e
     }
     __syncthreads();
     const bool sortall = S.sortall != 0;
-    // the sub-bucket's values into shared memory (the upper half of the dead
-    // hash table and the member counts: ckey uses key[0, U), U <= RF_CAP),
+    // the sub-bucket's values into shared memory (the dead hash table, member
+    // counts and group slots: the ranking above was the last reader of ckey),
     // in flight while the offset is looked back; the fallback sort below
-    // needs the whole table, so it reads the values from global memory
-    double *Vs = reinterpret_cast<double *>(&S.key[RF_CAP]);
+    // uses the same space, so it reads the values from global memory
+    static_assert(sizeof(uint32_t) * (RF_HS + RF_HS / 2) + sizeof(uint16_t) * RF_CAP >= 8 * RF_CAP,
+                  "staged values");
+    double *Vs = reinterpret_cast<double *>(&S.key[0]);
     if (!sortall) {
 #pragma unroll
         for (int u = 0; u < RIPT; ++u) {
