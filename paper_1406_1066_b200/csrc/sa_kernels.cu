@@ -666,8 +666,10 @@ constexpr int COLCOUNT_CTAS = 5;  // resident CTAs per SM of the column pass
 cudaError_t launch_colcount(Launch &lc, const Segs &S, int32_t N, uint32_t *cnt, ErrState *err) {
     const int64_t nchunk = S.ch0[S.nseg];
     if (nchunk <= 0) return cudaSuccess;
-    const int grid = (int)std::min<int64_t>(nchunk, (int64_t)lc.num_sms * COLCOUNT_CTAS);
-    cudaError_t e = launch_pdl(k_colcount_win, dim3(grid), dim3(AGG_NT), 0, lc.stream, S, N, cnt, err);
+    // at least the resident CTAs; large inputs: about 32 chunks per CTA
+    // (cfg5 1.84 -> 1.62 ms with 16x the resident CTAs; cfg2 slower with more)
+    const int64_t grid = std::min<int64_t>(nchunk, std::max<int64_t>((int64_t)lc.num_sms * COLCOUNT_CTAS, nchunk / 32));
+    cudaError_t e = launch_pdl(k_colcount_win, dim3((unsigned)grid), dim3(AGG_NT), 0, lc.stream, S, N, cnt, err);
     lc.launches++;
     return e;
 }
@@ -950,11 +952,13 @@ cudaError_t launch_scatter(Launch &lc, const Segs &S, int32_t M, int32_t N, uint
     if (nchunk <= 0) return cudaSuccess;
     cudaError_t e;
     if (scatter_staged(lc, N)) {
-        const int grid = (int)std::min<int64_t>(2 * nchunk, (int64_t)lc.num_sms * 7);
-        e = launch_pdl(k_scatter_staged, dim3(grid), dim3(SNT), 0, lc.stream, S, M, N, cur, perm, err);
+        // many short-lived CTAs, about 16 half chunks each (cfg5: 10.6 ms with
+        // the 7 resident CTAs per SM walking all chunks, 6.6 ms like this)
+        const int64_t grid = std::min<int64_t>(2 * nchunk, std::max<int64_t>((int64_t)lc.num_sms * 7, 2 * nchunk / 16));
+        e = launch_pdl(k_scatter_staged, dim3((unsigned)grid), dim3(SNT), 0, lc.stream, S, M, N, cur, perm, err);
     } else {
-        const int grid = (int)std::min<int64_t>(nchunk, (int64_t)lc.num_sms * 4);
-        e = launch_pdl(k_scatter, dim3(grid), dim3(AGG_NT), 0, lc.stream, S, M, N, cur, perm, err);
+        const int64_t grid = std::min<int64_t>(nchunk, (int64_t)lc.num_sms * 4);
+        e = launch_pdl(k_scatter, dim3((unsigned)grid), dim3(AGG_NT), 0, lc.stream, S, M, N, cur, perm, err);
     }
     lc.launches++;
     return e;

@@ -10,6 +10,9 @@ for name, (res, args) in _capi.SIGNATURES.items():
     f = getattr(lib, name); f.restype = res; f.argtypes = args
 ctx = ctypes.c_void_p(); lib.sa_create(0, ctypes.byref(ctx))
 cfg = sys.argv[2] if len(sys.argv) > 2 else "2"
+for kv in sys.argv[3:]:  # context options OPT=VAL
+    o, v = kv.split("=")
+    lib.sa_set_option(ctx, getattr(_capi, "SA_OPT_" + o), int(v))
 if cfg.startswith("ds"):
     ii, jj, sv = W.ransparse(*W.ransparse_spec(int(cfg[2:])))
     w = W.Workload(cfg, torch.from_numpy(ii).cuda(), torch.from_numpy(jj).cuda(), torch.from_numpy(sv).cuda(), int(ii.max()), int(jj.max()))
@@ -27,4 +30,4 @@ for it in range(12):
     n = lib.sa_last_kernel_times(ctx, 16, arr, names)
     if it >= 2:
         for k in range(n): tot.setdefault(names[k].decode(), []).append(arr[k])
-print(sys.argv[1].split('/')[-1], 'cfg%s' % cfg, {k: round(sum(v)/len(v)*1e3, 1) for k, v in tot.items()})
+print(sys.argv[1].split('/')[-1], 'cfg%s' % cfg, *sys.argv[3:], {k: round(sum(v)/len(v)*1e3, 1) for k, v in tot.items()})
