@@ -84,7 +84,6 @@ struct ErrState {
     unsigned int lsmall;        // triplets in small columns (small record space)
     unsigned int long_cols;     // some small column is long (> SHORT_COL): the fold's long pass runs
     // radix path (sa_radix.cu)
-    unsigned int rf_ticket;     // sub-bucket tickets of the fold
     unsigned int rbig_n;        // oversize sub-buckets listed by k_rbounds
     unsigned int rvalid;        // triplets with a valid column (partitioned)
 };

@@ -849,6 +849,23 @@ __device__ __forceinline__ void rf_net8(uint32_t (&m)[8]) {
     rf_cx(m[1], m[2]); rf_cx(m[3], m[4]); rf_cx(m[5], m[6]);
 }
 
+// 16 keys: two sorted halves (rf_net8), then merged -- compare k with 15 - k
+// (every key of the low half is then <= every key of the high half and both
+// halves are bitonic) and a bitonic clean-up of each half (70 compare-exchanges).
+__device__ __forceinline__ void rf_net16(uint32_t (&m)[16]) {
+    uint32_t(&lo)[8] = *reinterpret_cast<uint32_t(*)[8]>(&m[0]);
+    uint32_t(&hi)[8] = *reinterpret_cast<uint32_t(*)[8]>(&m[8]);
+    rf_net8(lo);
+    rf_net8(hi);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) rf_cx(m[k], m[15 - k]);
+#pragma unroll
+    for (int d = 4; d >= 1; d >>= 1)
+#pragma unroll
+        for (int k = 0; k < 16; ++k)
+            if ((k & d) == 0) rf_cx(m[k], m[k + d]);
+}
+
 __device__ __forceinline__ void rf_isort16(uint16_t *a, int n) {  // ascending, in place
     for (int i = 1; i < n; ++i) {
         const uint16_t x = a[i];
@@ -867,14 +884,16 @@ __global__ void __launch_bounds__(RF_NT, RF_MINB) k_rfold(RadixFoldArgs F, ErrSt
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const unsigned lt = lanemask_lt();
     pdl_wait();
-    if (call_failed(err)) {
+    // sub-bucket = block index (blocks are dispatched in index order, so the
+    // look-back below only waits on started predecessors, as in the tile fold);
+    // the error flags and the bounds are read concurrently
+    const int64_t s = blockIdx.x;
+    const bool failed = call_failed(err);
+    const uint32_t a = F.bnd[s], n = F.bnd[s + 1] - a;
+    if (failed) {
         pdl_trigger();
         return;
     }
-    if (tid == 0) S.b = (int)atomicAdd(&err->rf_ticket, 1u);
-    __syncthreads();
-    const int64_t s = S.b;
-    const uint32_t a = F.bnd[s], n = F.bnd[s + 1] - a;
     // sub-bucket keys [K0, K0 + 2^z): column-block plan (z >= rbits) -- the
     // columns c0 .. c0 + 2^(z - rbits) - 1, whole; row-split plan (z < rbits)
     // -- rows roff .. roff + 2^z - 1 of column c0 (it starts the column when
@@ -1139,6 +1158,14 @@ __global__ void __launch_bounds__(RF_NT, RF_MINB) k_rfold(RadixFoldArgs F, ErrSt
 #pragma unroll
             for (int q = 0; q < 8; ++q)
                 if (q < nm) acc = fold_add(acc, v[q]);
+        } else if (nm <= 16) {  // (7 % of the groups)
+            uint32_t m[16];
+#pragma unroll
+            for (int q = 0; q < 16; ++q) m[q] = (q < nm) ? (uint32_t)S.memb[st + q] : 0xffffu;
+            rf_net16(m);
+#pragma unroll
+            for (int q = 0; q < 16; ++q)
+                if (q < nm) acc = fold_add(acc, sv[m[q]]);
         } else {
             if (nm <= 32) rf_isort16(S.memb + st, nm);
             for (int q = st; q < en; ++q) acc = fold_add(acc, sv[S.memb[q]]);
