@@ -794,3 +794,37 @@ def test_host_dims_inferred_during_chunked_upload():
     with pytest.raises(sa.BadIndex) as e:
         sa.assemble(ii, jj, s)
     assert (e.value.position, e.value.value) == (35_000_001, 0)
+
+
+def test_concurrent_contexts_on_one_device():
+    """Several contexts (one per host thread, sa_create each; the kernels'
+    shared-memory attributes are set per (kernel, device) under a lock) run
+    assemblies concurrently on device 0 -- column-cursor inputs with big
+    columns (k_bigcol's 64 KB dynamic shared memory), shuffled inputs on the
+    radix path and long columns on its row-split plan -- each bit-exact."""
+    import threading
+
+    from paper_1406_1066_b200 import workloads as W
+
+    cases = [W.heavy_dup(m=30_000, positions=600_000, seed=21), W.fem3d(12),
+             W.random_coo(m=200_000, n=3, L=400_000, seed=22), W.random_coo(m=2000, n=50, L=120_000, seed=23)]
+    refs = [O.assemble_counting(w.ii.numpy(), w.jj.numpy(), w.s.numpy(), w.m, w.n) for w in cases]
+    errors = []
+
+    def run(k):
+        try:
+            a = sa.Assembler(0)  # a fresh context in this thread
+            for _ in range(3):
+                for w, ref in zip(cases[k:] + cases[:k], refs[k:] + refs[:k]):
+                    got = a.assemble(w.ii.numpy(), w.jj.numpy(), w.s.numpy(), m=w.m, n=w.n)
+                    _same(got, ref)
+            a.close()
+        except Exception as e:  # noqa: BLE001
+            errors.append(e)
+
+    threads = [threading.Thread(target=run, args=(k,)) for k in range(4)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert errors == []
