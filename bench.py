@@ -256,7 +256,10 @@ def main():
         ii, jj, s = w.ii.cpu().numpy(), w.jj.cpu().numpy(), w.s.cpu().numpy()
         cfg_line, wL = bench_config(w, args.gpus, args.gpus > 1), w.L
         del w.ii, w.jj, w.s  # device copies
-        Ls, req, run, p = reference_sample(ii, jj, s, w.m, w.n)
+        # each step a bounded sample: at most REF_STEP_S, and the whole
+        # warm-up + timed run within about two minutes
+        step_s = max(0.25, min(REF_STEP_S, 120.0 / (args.steps + args.warmup)))
+        Ls, req, run, p = reference_sample(ii, jj, s, w.m, w.n, target_s=step_s)
         for _ in range(args.warmup):
             run()
         times = []
