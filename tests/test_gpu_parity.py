@@ -828,3 +828,52 @@ def test_concurrent_contexts_on_one_device():
     for t in threads:
         t.join()
     assert errors == []
+
+
+def _fuzz_case(seed):
+    """A random shape: dimensions from 1 to 3e6, lengths up to 6e5, with
+    duplication, skew (a few heavy columns / rows), scalar values, NaN and
+    signed zeros, sometimes column-ordered (FEM-like) runs."""
+    rng = np.random.default_rng(seed)
+    m = int(rng.choice([1, 3, 17, 1000, 65_537, 3_000_000]))
+    n = int(rng.choice([1, 2, 29, 1000, 65_535, 2_000_000]))
+    L = int(rng.integers(0, 600_000))
+    ii = rng.integers(1, m + 1, size=L)
+    jj = rng.integers(1, n + 1, size=L)
+    kind = seed % 5
+    if kind == 1 and L:  # heavy duplicates
+        k = max(1, L // 7)
+        pick = rng.integers(0, k, size=L)
+        ii, jj = ii[:k][pick], jj[:k][pick]
+    elif kind == 2 and L:  # a few heavy columns
+        heavy = rng.random(L) < 0.6
+        jj[heavy] = rng.integers(1, min(n, 4) + 1, size=int(heavy.sum()))
+    elif kind == 3 and L:  # column-ordered runs
+        jj = np.sort(jj)
+    s = rng.standard_normal(L)
+    if L:
+        s[rng.random(L) < 0.01] = np.nan
+        s[rng.random(L) < 0.01] = -0.0
+    if seed % 7 == 0:
+        s = np.array([0.1])  # scalar value
+    return ii.astype(np.int32), jj.astype(np.int32), s, m, n
+
+
+@pytest.mark.parametrize("seed", list(range(64)))
+def test_fuzz_both_pipelines_bit_exact(seed):
+    """Random shapes through both pipelines (column-cursor and radix, each
+    forced; the radix path picks its column-block or row-split plan by
+    shape) against the C oracle, bit for bit."""
+    from paper_1406_1066_b200 import _capi
+
+    ii, jj, s, m, n = _fuzz_case(seed)
+    sv = np.full(len(ii), s[0]) if len(s) == 1 and len(ii) != 1 else s
+    ref = O.assemble_counting(ii, jj, sv, m, n)
+    a = sa.default_assembler(0)
+    for path in (0, 1):
+        a.set_option(_capi.SA_OPT_PATH, path)
+        try:
+            got = a.assemble(ii, jj, s, m=m, n=n)
+        finally:
+            a.set_option(_capi.SA_OPT_PATH, -1)
+        _same(got, ref)
