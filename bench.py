@@ -189,7 +189,23 @@ def cpu_reference_run(ii, jj, s, m, n, budget_s=15.0, max_reps=20):
         run()
         times.append(time.perf_counter() - t0)
     mean = sum(times) / len(times)
-    return dict(kind="reference", cores=p, mean_s=mean, min_s=min(times), reps=len(times), Ls=Ls), out
+    # the reference's serial driver too, one run on a prefix of
+    # the sample sized for about 3 s (its throughput is flat in L)
+    from oracle import stock
+
+    Lser = min(Ls, 1 << 22)
+    rq = stock.request(ii[:Lser], jj[:Lser], s[:Lser], m, n)
+    t0 = time.perf_counter()
+    stock.serial(rq)
+    ts = time.perf_counter() - t0
+    if ts < 1.0 and Lser < Ls:
+        Lser = int(min(Ls, Lser * max(1.0, 3.0 / max(ts, 1e-3))))
+        rq = stock.request(ii[:Lser], jj[:Lser], s[:Lser], m, n)
+        t0 = time.perf_counter()
+        stock.serial(rq)
+        ts = time.perf_counter() - t0
+    return dict(kind="reference", cores=p, mean_s=mean, min_s=min(times), reps=len(times), Ls=Ls,
+                serial_value=Lser / ts, serial_Ls=Lser), out
 
 
 def bench_config(w, world: int, shard: bool) -> dict:
@@ -516,6 +532,8 @@ def main():
         mine = out if Ls == L else sa.assemble(hin[:Ls], hjn[:Ls], hsn[:Ls], m=M, n=N, device=local)
         parity = bool(mine.same_as(ref))
         cpu = {"value": Ls / info["mean_s"], "unit": UNIT, "cores": info["cores"], "kind": info["kind"],
+               "serial": {"value": info["serial_value"], "unit": UNIT, "cores": 1,
+                          "sample": f"first {info['serial_Ls']} triplets, stock sparseasm.assemble_serial"},
                "sample": f"first {Ls} of {L} triplets (same m, n), stock sparseasm.assemble_parallel "
                          f"(oracle/_ref) on {info['cores']} threads, {info['reps']} timed runs after "
                          f"1 warm-up, mean {info['mean_s'] * 1e3:.1f} ms"}
