@@ -272,14 +272,20 @@ def main():
         ii, jj, s = w.ii.cpu().numpy(), w.jj.cpu().numpy(), w.s.cpu().numpy()
         cfg_line, wL = bench_config(w, args.gpus, args.gpus > 1), w.L
         del w.ii, w.jj, w.s  # device copies
-        # each step a bounded sample: at most REF_STEP_S, and the whole
-        # warm-up + timed run within about two minutes
-        step_s = max(0.25, min(REF_STEP_S, 120.0 / (args.steps + args.warmup)))
-        Ls, req, run, p = reference_sample(ii, jj, s, w.m, w.n, target_s=step_s)
-        for _ in range(args.warmup):
+        # each step a bounded sample (REF_STEP_S: large enough that the
+        # threaded driver's fixed O((m + n) p) merge cost does not understate
+        # its throughput); warm-up runs at most 2, and only as many timed
+        # steps as fit in about two and a half minutes (at least 3, at most
+        # --steps): the line's "steps" is the count actually timed
+        Ls, req, run, p = reference_sample(ii, jj, s, w.m, w.n)
+        t0 = time.perf_counter()
+        run()  # warm-up (also times one step)
+        t_step = time.perf_counter() - t0
+        for _ in range(min(args.warmup, 2) - 1):
             run()
+        nsteps = int(min(args.steps, max(3, 150.0 // max(t_step, 1e-3))))
         times = []
-        for _ in range(args.steps):
+        for _ in range(nsteps):
             t0 = time.perf_counter()
             run()
             times.append(time.perf_counter() - t0)
@@ -288,7 +294,8 @@ def main():
         sample = (f"first {Ls} of the workload's {wL} triplets (same m, n) per step, "
                   f"stock sparseasm.assemble_parallel(req, p={p}) from oracle/_ref")
         line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
-                "steps": args.steps, "warmup": args.warmup, "ms_per_step": mean * 1e3,
+                "steps": nsteps, "steps_requested": args.steps, "warmup": args.warmup,
+                "ms_per_step": mean * 1e3,
                 "higher_is_better": True, "scaling": "strong" if args.gpus > 1 else "weak",
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": cfg_line,
