@@ -239,6 +239,43 @@ def build_workload(cfg: int, device, rank: int, world: int):
     return W.config(cfg, device=device)
 
 
+def sharded_config_point(w, lib, ctx, asm, dev, stream, steps, warmup):
+    """cfg5 (the sharded config) assembled whole on this GPU, device-resident,
+    CUDA events on the library's stream: the N = 1 point of the scaling runs
+    (which split cfg5 over the ranks)."""
+    import torch
+
+    for name in ("ii", "jj", "s"):  # the headline workload's inputs are no longer needed
+        setattr(w, name, None)
+    torch.cuda.empty_cache()
+    w5 = build_workload(5, dev, 0, 1)
+    L5, M5, N5 = w5.L, w5.m, w5.n
+    jc = torch.empty(N5 + 1, dtype=torch.int32, device=dev)
+    ir = torch.empty(L5, dtype=torch.int32, device=dev)
+    pr = torch.empty(L5, dtype=torch.float64, device=dev)
+
+    def step():
+        rc = lib.sa_assemble_async(ctx, w5.ii.data_ptr(), w5.jj.data_ptr(), w5.s.data_ptr(), 1, L5, M5, N5,
+                                   jc.data_ptr(), ir.data_ptr(), pr.data_ptr(), L5)
+        if rc:
+            raise RuntimeError(asm._msg())
+
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    del w5, jc, ir, pr
+    torch.cuda.empty_cache()
+    return {"workload": f"fem2d_N8000", "L": L5, "m": M5, "n": N5, "steps": steps,
+            "ms_per_step": ms, "value": L5 / (ms * 1e-3), "unit": UNIT}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -251,6 +288,8 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-sharded-point", action="store_true",
+                    help="skip the sharded config's one-GPU point (cfg4 runs only)")
     ap.add_argument("--sharded", action="store_true",
                     help="use the multi-GPU (sharded, NCCL) step even with one rank (under torchrun)")
     args = ap.parse_args()
@@ -545,6 +584,14 @@ def main():
                          f"(oracle/_ref) on {info['cores']} threads, {info['reps']} timed runs after "
                          f"1 warm-up, mean {info['mean_s'] * 1e3:.1f} ms"}
 
+    # the sharded config's one-GPU point (the N > 1 runs split it over the
+    # ranks): measured here too, so a scaling curve has its N = 1 reference
+    sharded_1gpu = None
+    cfg_line = bench_config(w, world, shard)
+    if rank == 0 and not shard and args.config == 4 and not args.no_sharded_point:
+        sharded_1gpu = sharded_config_point(w, lib, ctx, asm, dev, stream, max(3, min(args.steps, 10)),
+                                            args.warmup)
+
     if rank != 0:
         if shard:
             dist.destroy_process_group()
@@ -556,7 +603,7 @@ def main():
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "strong" if shard else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": bench_config(w, world, shard),
+        "config": cfg_line,
         "nnz": nnz,
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": dom_gbs, "peak": peak_gbs,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": dom_gbs / peak_gbs,
@@ -573,6 +620,8 @@ def main():
         "cpu_baseline": cpu,
         "parity_vs_cpu_reference": parity,
     }
+    if sharded_1gpu is not None:
+        line["sharded_config_1gpu"] = sharded_1gpu
     if shard:
         line["exchange"] = {"sent_remote_triplets_rank0": shard_info.get("sent_remote"),
                             "received_triplets_rank0": shard_info.get("recv"),
