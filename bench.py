@@ -23,6 +23,10 @@ Prints ONE JSON line (rank 0):
                sparseasm.assemble_parallel over its compiled kernels, all
                host threads) on a bounded sample of the same workload (the
                first Ls triplets, ~1 s per run)
+  sharded_config_1gpu  (default cfg4 line) cfg5, the sharded config, whole
+               on this GPU: the N = 1 point of the multi-GPU runs
+Under torchrun with N > 1 ranks: cfg5 split over the ranks (strong scaling),
+column-block sharding with one NCCL exchange.
 --impl reference runs only that CPU implementation (one sample per step) and
 prints its line, with the same `config` as this arm.
 """
