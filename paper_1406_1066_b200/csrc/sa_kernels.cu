@@ -939,11 +939,13 @@ __global__ void __launch_bounds__(SNT) k_scatter_staged(Segs S, int32_t M, int32
 
 // Staged writes pay off when the column cursors (4 N bytes) and the columns'
 // slot regions no longer stay in L2 between the chunks that fill them (cfg5,
-// N = 6.4e7: 14.3 -> 10.6 ms); with L2-resident cursors (cfg2 / cfg3) the
-// plain scatter is faster (110 vs 174 us on cfg2).  The context option
+// N = 6.4e7: 14.3 -> 6.7 ms with its grid below; a rank's cfg5 block at 8
+// GPUs, N = 8e6: 2.92 -> 2.48 ms for its local assembly); with L2-resident
+// cursors (cfg2 / cfg3, N = 1e6) the plain scatter is faster (109 vs 166 us
+// on cfg2, 459 vs 619 us on cfg3).  The context option
 // SA_OPT_SCATTER_STAGED overrides the choice (tests force both variants).
 static bool scatter_staged(const Launch &lc, int32_t N) {
-    return lc.scatter_staged >= 0 ? lc.scatter_staged == 1 : N > (16 << 20);
+    return lc.scatter_staged >= 0 ? lc.scatter_staged == 1 : N > (4 << 20);
 }
 
 cudaError_t launch_scatter(Launch &lc, const Segs &S, int32_t M, int32_t N, uint32_t *cur,

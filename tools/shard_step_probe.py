@@ -4,7 +4,7 @@ histogram gives for these meshes): rank `rank` of `world` on the weak-scaling me
 chunk bench.py uses.  Phases: sampled block histogram, boundaries (host),
 sa_partition (+ host read of the counts), segment assembly of the own chunk
 (+ sa_finish).  The NCCL exchange is replaced by "nothing received".
-usage: python tools/shard_step_probe.py [world] [rank]"""
+usage: python tools/shard_step_probe.py [world] [rank] [OPT=VAL ...]"""
 import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -16,6 +16,10 @@ rank = int(sys.argv[2]) if len(sys.argv) > 2 else 3
 w = bench.build_workload(2, "cuda", rank, world)
 M, N = w.m, w.n
 asm = default_assembler(0); asm._bind_stream()
+from paper_1406_1066_b200 import _capi
+for kv in sys.argv[3:]:
+    o, v = kv.split("=")
+    asm.set_option(getattr(_capi, "SA_OPT_" + o), int(v))
 ii, jj, s = w.ii, w.jj, w.s
 OUT = {}
 EV = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
@@ -30,7 +34,7 @@ def step(t):
     bounds = [N * r // world for r in range(world + 1)]
     t.append(("hist+bounds", time.perf_counter()))
     EV[1].record()
-    parts, counts = D._partition_cuda(asm, ii, jj, s, M, N, bounds, world, rank)
+    parts, counts, _err = D._partition_cuda(asm, ii, jj, s, M, N, bounds, world, rank)
     t.append(("partition", time.perf_counter()))
     EV[2].record()
     col_lo, col_hi = bounds[rank], bounds[rank + 1]
