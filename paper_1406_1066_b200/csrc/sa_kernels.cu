@@ -790,8 +790,9 @@ __global__ void __launch_bounds__(AGG_NT) k_scatter(Segs S, int32_t M, int32_t N
     }
 }
 
-// Staged variant (SA_SCATTER_STAGED=1): 128-thread CTAs on half chunks
-// (1024 triplets); after the reservation every entry is first placed in
+// Staged variant (chosen for N > 4M columns; SA_OPT_SCATTER_STAGED forces
+// either): 128-thread CTAs on half chunks (1024 triplets); after the
+// reservation every entry is first placed in
 // shared memory grouped by column (each column's run of the half chunk is
 // contiguous there), then copied out so that consecutive lanes write
 // consecutive slots of one column.
