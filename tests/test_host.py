@@ -276,3 +276,28 @@ def test_run_bench_protocol_and_csv(tmp_path):
     write_bench_csv(res, p)
     rows = list(csv.DictReader(open(p)))
     assert list(rows[0].keys()) == BENCH_CSV_COLUMNS and rows[1]["impl"] == "b200"
+
+
+def test_bench_reference_arm_contract():
+    """bench.py --impl reference (runs on the host CPU, no GPU needed): one
+    JSON line with the driver's keys, the same `config` dictionary the GPU
+    arm prints, and a cpu_baseline describing the stock reference run."""
+    import json
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--impl", "reference",
+                          "--config", "1", "--steps", "3", "--warmup", "3"],
+                         capture_output=True, text=True, timeout=600, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+              "scaling", "vs_baseline", "dtype", "data", "config", "cpu_baseline", "e2e"):
+        assert k in d, k
+    assert d["impl"] == "reference" and d["value"] > 0 and d["higher_is_better"] is True
+    assert d["config"]["workload"].startswith("random_coo") and d["config"]["L"] == 100_000
+    assert d["cpu_baseline"]["kind"] == "reference" and d["cpu_baseline"]["cores"] >= 1
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and 3 <= d["steps"] <= 3
