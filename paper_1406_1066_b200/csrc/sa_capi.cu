@@ -43,9 +43,11 @@ struct sa_ctx {
     int32_t *pt_cnt = nullptr;            size_t ptc_cap = 0;    // partition: tile x rank counts
     int64_t *pt_off = nullptr;            size_t pto_cap = 0;    // partition: tile x rank offsets
     int64_t *pt_counts = nullptr;         // partition: per-rank counts and bases (16)
-    // radix path (sa_radix.cu): partition buffers X / Y, histograms, look-back words
-    int32_t *rx_i = nullptr, *rx_j = nullptr; double *rx_s = nullptr;  size_t rx_cap = 0;
-    int32_t *ry_i = nullptr, *ry_j = nullptr; double *ry_s = nullptr;  size_t ry_cap = 0;
+    // radix path (sa_radix.cu): partition buffers X / Y (one 16-byte-per-triplet
+    // block each: the arrays ii | jj | s of the passes before the last, the
+    // last pass's {row, col} pairs | s), histograms, look-back words
+    uint4 *rx = nullptr; int32_t *rx_i = nullptr, *rx_j = nullptr; double *rx_s = nullptr;  size_t rx_cap = 0;
+    uint4 *ry = nullptr; int32_t *ry_i = nullptr, *ry_j = nullptr; double *ry_s = nullptr;  size_t ry_cap = 0;
     uint16_t *rcnt = nullptr;             size_t rcnt_cap = 0;         // nchunk x RP_MAXD chunk histograms
     uint32_t *roff = nullptr;             size_t roff_cap = 0;         // nchunk x RP_MAXD chunk bases
     uint32_t *rbsum = nullptr;            size_t rbsum_cap = 0;        // nblk x RP_MAXD block bases
@@ -359,8 +361,7 @@ void sa_destroy(sa_ctx *ctx) {
     cudaFree(ctx->pt_off);
     cudaFree(ctx->pt_counts);
     cudaFree(ctx->pr_nnz);
-    for (void *p : {(void *)ctx->rx_i, (void *)ctx->rx_j, (void *)ctx->rx_s, (void *)ctx->ry_i,
-                    (void *)ctx->ry_j, (void *)ctx->ry_s, (void *)ctx->rcnt, (void *)ctx->roff, (void *)ctx->rbsum,
+    for (void *p : {(void *)ctx->rx, (void *)ctx->ry, (void *)ctx->rcnt, (void *)ctx->roff, (void *)ctx->rbsum,
                     (void *)ctx->rlbf, (void *)ctx->rbnd, (void *)ctx->rbig, (void *)ctx->rbigu})
         cudaFree(p);
     cudaFree(ctx->h_ii);
@@ -496,20 +497,23 @@ RadixPlan radix_plan(int64_t L, int32_t M, int32_t N) {
     return P;
 }
 
-// One partition buffer: ii, jj (int32) and s (float64) for `need` triplets.
-cudaError_t ensure_trip(int32_t *&i, int32_t *&j, double *&v, size_t &cap, size_t need) {
-    if (need <= cap && i) return cudaSuccess;
-    cudaFree(i);
-    cudaFree(j);
-    cudaFree(v);
+// One partition buffer of 16 bytes per triplet for `need` triplets: viewed as
+// the column arrays ii, jj (int32) and s (float64), each 16-byte aligned, or
+// as `need` records.
+cudaError_t ensure_trip(uint4 *&blk, int32_t *&i, int32_t *&j, double *&v, size_t &cap, size_t need) {
+    if (need <= cap && blk) return cudaSuccess;
+    cudaFree(blk);
+    blk = nullptr;
     i = j = nullptr;
     v = nullptr;
     cap = 0;
-    need = std::max<size_t>(need, 1);
-    cudaError_t e = cudaMalloc(reinterpret_cast<void **>(&i), need * 4);
-    if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void **>(&j), need * 4);
-    if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void **>(&v), need * 8);
-    if (e == cudaSuccess) cap = need;
+    need = (std::max<size_t>(need, 1) + 3) & ~size_t(3);
+    cudaError_t e = cudaMalloc(reinterpret_cast<void **>(&blk), need * 16);
+    if (e != cudaSuccess) return e;
+    cap = need;
+    i = reinterpret_cast<int32_t *>(blk);
+    j = i + need;
+    v = reinterpret_cast<double *>(j + need);
     return e;
 }
 
@@ -531,9 +535,10 @@ int assemble_radix(sa_ctx *ctx, const RadixPlan &P, const int32_t *ii, const int
     lc.rpass_tma = ctx->opt_rpass_tma;
     const size_t nl = (size_t)L;
     const size_t nsub = (size_t)P.nsub;
-    SA_CUDA(ctx, ensure_trip(ctx->rx_i, ctx->rx_j, ctx->rx_s, ctx->rx_cap, nl));
-    if (P.npass > 1) SA_CUDA(ctx, ensure_trip(ctx->ry_i, ctx->ry_j, ctx->ry_s, ctx->ry_cap, nl));
-    else SA_CUDA(ctx, ensure_trip(ctx->ry_i, ctx->ry_j, ctx->ry_s, ctx->ry_cap, 1));
+    // X and Y: the passes alternate X, Y, X, ...; the last one writes records.
+    // (With one pass Y is the oversize scratch B.)
+    SA_CUDA(ctx, ensure_trip(ctx->rx, ctx->rx_i, ctx->rx_j, ctx->rx_s, ctx->rx_cap, nl));
+    SA_CUDA(ctx, ensure_trip(ctx->ry, ctx->ry_i, ctx->ry_j, ctx->ry_s, ctx->ry_cap, nl));
     SA_CUDA(ctx, ensure(ctx->perm, ctx->perm_cap, nl + 2));  // oversize scratch A
     // partition CTAs: the resident ones (2 per SM), walking the chunks with that stride
     const int nseg = (int)std::max<int64_t>(1, std::min<int64_t>(P.nchunk, (int64_t)ctx->num_sms * (2048 / RP_NT)));
@@ -561,6 +566,7 @@ int assemble_radix(sa_ctx *ctx, const RadixPlan &P, const int32_t *ii, const int
     if ((rc = launch_init(ctx, lc, 0, 0, 0))) return rc;
     int32_t *bi[2] = {ctx->rx_i, ctx->ry_i}, *bj[2] = {ctx->rx_j, ctx->ry_j};
     double *bs[2] = {ctx->rx_s, ctx->ry_s};
+    uint4 *br[2] = {ctx->rx, ctx->ry};
     static const char *pname[RP_MAXPASS] = {"k_rpass0", "k_rpass1", "k_rpass2", "k_rpass3"};
     static const char *uname[RP_MAXPASS] = {"k_rup0", "k_rup1", "k_rup2", "k_rup3"};
     for (int p = 0; p < P.npass; ++p) {
@@ -572,6 +578,7 @@ int assemble_radix(sa_ctx *ctx, const RadixPlan &P, const int32_t *ii, const int
         A.ii_out = bi[p & 1];
         A.jj_out = bj[p & 1];
         A.s_out = bs[p & 1];
+        A.rc_out = reinterpret_cast<int2 *>(bi[p & 1]);  // the ii | jj regions of the block
         A.L = L;
         A.M = M;
         A.N = N;
@@ -583,22 +590,17 @@ int assemble_radix(sa_ctx *ctx, const RadixPlan &P, const int32_t *ii, const int
         SA_CUDA(ctx, launch_rup(lc, p == 0, A.ii_in, A.jj_in, L, N, A.shift, A.bits, P.rbits, ctx->rcnt,
                                 ctx->rbsum, ctx->roff, ctx->err));
         if ((rc = mark(ctx, pname[p]))) return rc;
-        SA_CUDA(ctx, launch_rpass(lc, A, p == 0, nseg, ctx->err));
+        SA_CUDA(ctx, launch_rpass(lc, A, p == 0, p == P.npass - 1, nseg, ctx->err));
     }
-    const int fb = (P.npass - 1) & 1;  // buffer holding the partitioned triplets
+    const int fb = (P.npass - 1) & 1;  // buffer holding the partitioned records
     RadixFoldArgs F{};
-    F.ii = bi[fb];
-    F.jj = bj[fb];
+    F.rc = reinterpret_cast<const int2 *>(bi[fb]);
     F.s = bs[fb];
     F.bnd = ctx->rbnd;
     F.biglist = ctx->rbig;
     F.bigu = ctx->rbigu;
     F.scrA = reinterpret_cast<unsigned long long *>(ctx->perm);
-    F.scrB = reinterpret_cast<unsigned long long *>(fb ? ctx->rx_s : ctx->ry_s);
-    if (P.npass == 1) {  // Y is a 1-entry stub: scratch B must hold L words
-        SA_CUDA(ctx, ensure_trip(ctx->ry_i, ctx->ry_j, ctx->ry_s, ctx->ry_cap, nl));
-        F.scrB = reinterpret_cast<unsigned long long *>(ctx->ry_s);
-    }
+    F.scrB = reinterpret_cast<unsigned long long *>(br[fb ^ 1]);
     F.lbf = ctx->rlbf;
     F.tag = ep | 3u;
     F.z = P.z;
@@ -610,7 +612,7 @@ int assemble_radix(sa_ctx *ctx, const RadixPlan &P, const int32_t *ii, const int
     F.pr = d_pr;
     F.cap = cap;
     if ((rc = mark(ctx, "k_rbounds"))) return rc;
-    SA_CUDA(ctx, launch_rbounds(lc, F.ii, F.jj, P.z, P.rbits, P.nsub, ctx->rbnd, ctx->rbig, ctx->err));
+    SA_CUDA(ctx, launch_rbounds(lc, F.rc, P.z, P.rbits, P.nsub, ctx->rbnd, ctx->rbig, ctx->err));
     if ((rc = mark(ctx, "k_rbig"))) return rc;
     SA_CUDA(ctx, launch_rbig(lc, F, ctx->err));
     if ((rc = mark(ctx, "k_rfold"))) return rc;

@@ -428,8 +428,9 @@ struct RadixPassArgs {
     const int32_t *ii_in, *jj_in;
     const double *s_in;
     int64_t s_stride;
-    int32_t *ii_out, *jj_out;
-    double *s_out;
+    int32_t *ii_out, *jj_out;  // output rows / columns (every pass but the last)
+    double *s_out;             // output values
+    int2 *rc_out;              // the last pass: {row, col} pairs (8 B each) instead of ii / jj
     int64_t L;
     int32_t M, N;
     int shift, bits;          // this pass's digit: (key >> shift) & (2^bits - 1) of the key
@@ -438,8 +439,8 @@ struct RadixPassArgs {
 };
 
 struct RadixFoldArgs {
-    const int32_t *ii, *jj;  // partitioned triplets (sorted by sub-bucket, stable)
-    const double *s;
+    const int2 *rc;          // partitioned triplets: {row, col} pairs and values (sorted by
+    const double *s;         // sub-bucket, stable)
     const uint32_t *bnd;     // nsub + 1 sub-bucket starts
     const uint32_t *biglist; // oversize sub-buckets
     uint32_t *bigu;          // per oversize sub-bucket: results | BIGFLAG (keys in scrB)
@@ -457,9 +458,9 @@ cudaError_t launch_rup(Launch &lc, bool first, const int32_t *ii, const int32_t 
                        int shift, int bits, int rbits, uint16_t *cnt, uint32_t *bsum, uint32_t *off,
                        ErrState *err);
 int rup_cpb(int64_t nchunk, int num_sms);  // chunks per upsweep block
-cudaError_t launch_rpass(Launch &lc, const RadixPassArgs &A, bool first, int nseg, ErrState *err);
-cudaError_t launch_rbounds(Launch &lc, const int32_t *ii, const int32_t *jj, int z, int rbits,
-                           int32_t nsub, uint32_t *bnd, uint32_t *biglist, ErrState *err);
+cudaError_t launch_rpass(Launch &lc, const RadixPassArgs &A, bool first, bool last, int nseg, ErrState *err);
+cudaError_t launch_rbounds(Launch &lc, const int2 *rc, int z, int rbits, int32_t nsub, uint32_t *bnd,
+                           uint32_t *biglist, ErrState *err);
 cudaError_t launch_rbig(Launch &lc, const RadixFoldArgs &F, ErrState *err);
 cudaError_t launch_rfold(Launch &lc, const RadixFoldArgs &F, ErrState *err);
 

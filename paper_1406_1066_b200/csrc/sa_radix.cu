@@ -265,6 +265,25 @@ __device__ __forceinline__ void st_last(int32_t *a, int32_t v, unsigned long lon
 __device__ __forceinline__ void st_last(double *a, double v, unsigned long long pol) {
     asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(a), "d"(v), "l"(pol) : "memory");
 }
+__device__ __forceinline__ void st_last(int2 *a, int2 v, unsigned long long pol) {
+    asm volatile("st.global.L2::cache_hint.v2.b32 [%0], {%1, %2}, %3;" ::"l"(a), "r"(v.x), "r"(v.y), "l"(pol)
+                 : "memory");
+}
+
+// One sorted record {row, col, value bits} out: the last pass writes the
+// {row, col} pair as one 8-byte store (what the fold and the bounds read),
+// the others separate row and column arrays (the next upsweep reads the
+// columns alone); the values go to their own array either way.
+template <bool LAST>
+__device__ __forceinline__ void put_rec(const RadixPassArgs &A, uint32_t o, uint4 v, unsigned long long pol) {
+    if (LAST) {
+        st_last(A.rc_out + o, make_int2((int)v.x, (int)v.y), pol);
+    } else {
+        st_last(A.ii_out + o, (int32_t)v.x, pol);
+        st_last(A.jj_out + o, (int32_t)v.y, pol);
+    }
+    st_last(A.s_out + o, __longlong_as_double((long long)(((unsigned long long)v.w << 32) | v.z)), pol);
+}
 
 // ---------------------------------------------------------------------------
 // k_rpass: one stable LSD partition pass by the digit (col-1) >> shift (the
@@ -289,7 +308,7 @@ struct PassSmem {
     uint32_t red[RP_NW];
 };
 
-template <bool FIRST, int BITS>
+template <bool FIRST, bool LAST, int BITS>
 __global__ void __launch_bounds__(RP_NT, 1) k_rpass(RadixPassArgs A, ErrState *err) {
     extern __shared__ __align__(16) unsigned char rp_smem[];
     PassSmem &S = *reinterpret_cast<PassSmem *>(rp_smem);
@@ -396,13 +415,7 @@ __global__ void __launch_bounds__(RP_NT, 1) k_rpass(RadixPassArgs A, ErrState *e
         }
         __syncthreads();
         const unsigned long long pol = l2_evict_last();
-        for (int k = tid; k < (int)ctot; k += RP_NT) {
-            const uint4 v = S.rec[k];
-            const uint32_t o = S.oidx[k];
-            st_last(A.ii_out + o, (int32_t)v.x, pol);
-            st_last(A.jj_out + o, (int32_t)v.y, pol);
-            st_last(A.s_out + o, __longlong_as_double((long long)(((unsigned long long)v.w << 32) | v.z)), pol);
-        }
+        for (int k = tid; k < (int)ctot; k += RP_NT) put_rec<LAST>(A, S.oidx[k], S.rec[k], pol);
     }
     pdl_trigger();
     if (FIRST) {
@@ -471,7 +484,7 @@ __device__ __forceinline__ void rt_wait(unsigned long long *bar, unsigned parity
     }
 }
 
-template <bool FIRST, int BITS>
+template <bool FIRST, bool LAST, int BITS>
 __global__ void __launch_bounds__(RP_NT, 1) k_rpass_tma(RadixPassArgs A, ErrState *err) {
     extern __shared__ __align__(128) unsigned char rt_smem_raw[];
     PassTmaSmem &S = *reinterpret_cast<PassTmaSmem *>(rt_smem_raw);
@@ -607,13 +620,7 @@ __global__ void __launch_bounds__(RP_NT, 1) k_rpass_tma(RadixPassArgs A, ErrStat
         }
         __syncthreads();
         const unsigned long long pol = l2_evict_last();
-        for (int q = tid; q < (int)ctot; q += RP_NT) {
-            const uint4 v = rec[q];
-            const uint32_t o = S.oidx[q];
-            st_last(A.ii_out + o, (int32_t)v.x, pol);
-            st_last(A.jj_out + o, (int32_t)v.y, pol);
-            st_last(A.s_out + o, __longlong_as_double((long long)(((unsigned long long)v.w << 32) | v.z)), pol);
-        }
+        for (int q = tid; q < (int)ctot; q += RP_NT) put_rec<LAST>(A, S.oidx[q], rec[q], pol);
         __syncthreads();  // the buffer and the counters are reused by the half after next
     }
     pdl_trigger();
@@ -636,36 +643,34 @@ __global__ void __launch_bounds__(RP_NT, 1) k_rpass_tma(RadixPassArgs A, ErrStat
 // sub-buckets longer than RF_CAP.  Column-block plan (z >= rbits): s =
 // (col - 1) >> (z - rbits), the columns alone decide.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ unsigned long long sub_of(const int32_t *__restrict__ ii,
-                                                     const int32_t *__restrict__ jj, uint32_t k, int z,
+__device__ __forceinline__ unsigned long long sub_of(const int2 *__restrict__ rcp, uint32_t k, int z,
                                                      int rbits) {
-    if (z >= rbits) return (unsigned long long)((uint32_t)(__ldg(jj + k) - 1) >> (z - rbits));
-    return tkey(__ldg(jj + k), __ldg(ii + k), rbits) >> z;
+    const int2 rc = __ldg(rcp + k);  // {row, col}
+    if (z >= rbits) return (unsigned long long)((uint32_t)(rc.y - 1) >> (z - rbits));
+    return tkey(rc.y, rc.x, rbits) >> z;
 }
 
-__device__ __forceinline__ uint32_t sub_lower_bound(const int32_t *__restrict__ ii,
-                                                    const int32_t *__restrict__ jj, uint32_t n, int z,
+__device__ __forceinline__ uint32_t sub_lower_bound(const int2 *__restrict__ rec, uint32_t n, int z,
                                                     int rbits, uint32_t s) {
     uint32_t lo = 0, hi = n;
     while (lo < hi) {
         const uint32_t mid = (lo + hi) >> 1;
-        if (sub_of(ii, jj, mid, z, rbits) < s) lo = mid + 1;
+        if (sub_of(rec, mid, z, rbits) < s) lo = mid + 1;
         else hi = mid;
     }
     return lo;
 }
 
-__global__ void k_rbounds(const int32_t *__restrict__ ii, const int32_t *__restrict__ jj, int z, int rbits,
-                          int32_t nsub, uint32_t *__restrict__ bnd, uint32_t *__restrict__ biglist,
-                          ErrState *err) {
+__global__ void k_rbounds(const int2 *__restrict__ rec, int z, int rbits, int32_t nsub,
+                          uint32_t *__restrict__ bnd, uint32_t *__restrict__ biglist, ErrState *err) {
     const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     pdl_wait();
     if (s <= nsub) {
         const uint32_t n = *((volatile const unsigned *)&err->rvalid);
-        const uint32_t a = (s == 0) ? 0u : (s == nsub ? n : sub_lower_bound(ii, jj, n, z, rbits, (uint32_t)s));
+        const uint32_t a = (s == 0) ? 0u : (s == nsub ? n : sub_lower_bound(rec, n, z, rbits, (uint32_t)s));
         bnd[s] = a;
         if (s < nsub) {
-            const uint32_t e = (s + 1 == nsub) ? n : sub_lower_bound(ii, jj, n, z, rbits, (uint32_t)s + 1);
+            const uint32_t e = (s + 1 == nsub) ? n : sub_lower_bound(rec, n, z, rbits, (uint32_t)s + 1);
             if (e - a > (uint32_t)RF_CAP) biglist[atomicAdd(&err->rbig_n, 1u)] = (uint32_t)s;
         }
     }
@@ -702,7 +707,8 @@ __global__ void __launch_bounds__(BIG_NT, 1) k_rbig(RadixFoldArgs F, ErrState *e
         unsigned long long *A = F.scrA + a;
         unsigned long long *B = F.scrB + a;
         for (uint32_t k = tid; k < n; k += BIG_NT) {
-            const uint32_t key = lkey(F.jj[a + k], F.ii[a + k], F.z, F.rbits, c0, roff);
+            const int2 rc = __ldg(F.rc + a + k);
+            const uint32_t key = lkey(rc.y, rc.x, F.z, F.rbits, c0, roff);
             A[k] = ((unsigned long long)key << 32) | k;
         }
         __syncthreads();
@@ -976,7 +982,10 @@ __global__ void __launch_bounds__(RF_NT, RF_MINB) k_rfold(RadixFoldArgs F, ErrSt
     for (int u = 0; u < RIPT; ++u) {
         const uint32_t k = tid + u * RF_NT;
         kk[u] = 0u;
-        if (k < n) kk[u] = (uint32_t)(tkey(__ldg(F.jj + a + k), __ldg(F.ii + a + k), F.rbits) - K0) + 1u;
+        if (k < n) {
+            const int2 rc = __ldg(F.rc + a + k);  // {row, col}
+            kk[u] = (uint32_t)(tkey(rc.y, rc.x, F.rbits) - K0) + 1u;
+        }
     }
     __syncthreads();
 #pragma unroll
@@ -1217,14 +1226,14 @@ cudaError_t launch_rup(Launch &lc, bool first, const int32_t *ii, const int32_t 
     return e;
 }
 
-template <bool FIRST, int BITS>
+template <bool FIRST, bool LAST, int BITS>
 static cudaError_t launch_rpass_t(Launch &lc, const RadixPassArgs &A, int nseg, ErrState *err) {
     auto al16 = [](const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
     // TMA-staged input (cfg4: pass 1 8.3 -> 7.0 ms, pass 2 7.0 -> 6.1 ms)
     const bool tma = lc.rpass_tma != 0;
     if (tma && al16(A.ii_in) && al16(A.jj_in) && (A.s_stride == 0 || al16(A.s_in))) {
         const int smem = (int)sizeof(PassTmaSmem);
-        cudaError_t e = ensure_smem_attr((const void *)k_rpass_tma<FIRST, BITS>, smem);
+        cudaError_t e = ensure_smem_attr((const void *)k_rpass_tma<FIRST, LAST, BITS>, smem);
         if (e != cudaSuccess) return e;
         // grid: the first pass runs best with many short-lived CTAs (about 8
         // chunks each; cfg4: 8.8 ms at one CTA per SM, 7.0 ms at 64 waves),
@@ -1232,44 +1241,47 @@ static cudaError_t launch_rpass_t(Launch &lc, const RadixPassArgs &A, int nseg, 
         // measured, tools/variant_time.py
         const int64_t nch = (A.L + RP_CHUNK - 1) / RP_CHUNK;
         const int64_t grid = FIRST ? std::max<int64_t>(lc.num_sms, (nch + 7) / 8) : lc.num_sms;
-        return launch_pdl(k_rpass_tma<FIRST, BITS>, dim3((unsigned)grid), dim3(RP_NT), smem, lc.stream,
+        return launch_pdl(k_rpass_tma<FIRST, LAST, BITS>, dim3((unsigned)grid), dim3(RP_NT), smem, lc.stream,
                           A, err);
     }
     const int smem = (int)sizeof(PassSmem);
-    cudaError_t e = ensure_smem_attr((const void *)k_rpass<FIRST, BITS>, smem);
+    cudaError_t e = ensure_smem_attr((const void *)k_rpass<FIRST, LAST, BITS>, smem);
     if (e != cudaSuccess) return e;
-    return launch_pdl(k_rpass<FIRST, BITS>, dim3((unsigned)nseg), dim3(RP_NT), smem, lc.stream, A, err);
+    return launch_pdl(k_rpass<FIRST, LAST, BITS>, dim3((unsigned)nseg), dim3(RP_NT), smem, lc.stream, A, err);
     // (nseg = the number of resident partition CTAs; they walk the chunks with stride nseg)
 }
 
-template <bool FIRST>
+template <bool FIRST, bool LAST>
 static cudaError_t launch_rpass_b(Launch &lc, const RadixPassArgs &A, int nseg, ErrState *err) {
     switch (A.bits) {  // the digit width is a compile-time constant of the kernel
-        case 0: return launch_rpass_t<FIRST, 0>(lc, A, nseg, err);
-        case 1: return launch_rpass_t<FIRST, 1>(lc, A, nseg, err);
-        case 2: return launch_rpass_t<FIRST, 2>(lc, A, nseg, err);
-        case 3: return launch_rpass_t<FIRST, 3>(lc, A, nseg, err);
-        case 4: return launch_rpass_t<FIRST, 4>(lc, A, nseg, err);
-        case 5: return launch_rpass_t<FIRST, 5>(lc, A, nseg, err);
-        case 6: return launch_rpass_t<FIRST, 6>(lc, A, nseg, err);
-        case 7: return launch_rpass_t<FIRST, 7>(lc, A, nseg, err);
-        case 8: return launch_rpass_t<FIRST, 8>(lc, A, nseg, err);
-        case 9: return launch_rpass_t<FIRST, 9>(lc, A, nseg, err);
+        case 0: return launch_rpass_t<FIRST, LAST, 0>(lc, A, nseg, err);
+        case 1: return launch_rpass_t<FIRST, LAST, 1>(lc, A, nseg, err);
+        case 2: return launch_rpass_t<FIRST, LAST, 2>(lc, A, nseg, err);
+        case 3: return launch_rpass_t<FIRST, LAST, 3>(lc, A, nseg, err);
+        case 4: return launch_rpass_t<FIRST, LAST, 4>(lc, A, nseg, err);
+        case 5: return launch_rpass_t<FIRST, LAST, 5>(lc, A, nseg, err);
+        case 6: return launch_rpass_t<FIRST, LAST, 6>(lc, A, nseg, err);
+        case 7: return launch_rpass_t<FIRST, LAST, 7>(lc, A, nseg, err);
+        case 8: return launch_rpass_t<FIRST, LAST, 8>(lc, A, nseg, err);
+        case 9: return launch_rpass_t<FIRST, LAST, 9>(lc, A, nseg, err);
         default: return cudaErrorInvalidValue;
     }
 }
 
-cudaError_t launch_rpass(Launch &lc, const RadixPassArgs &A, bool first, int nseg, ErrState *err) {
-    cudaError_t e = first ? launch_rpass_b<true>(lc, A, nseg, err) : launch_rpass_b<false>(lc, A, nseg, err);
+cudaError_t launch_rpass(Launch &lc, const RadixPassArgs &A, bool first, bool last, int nseg, ErrState *err) {
+    cudaError_t e = first ? (last ? launch_rpass_b<true, true>(lc, A, nseg, err)
+                                  : launch_rpass_b<true, false>(lc, A, nseg, err))
+                          : (last ? launch_rpass_b<false, true>(lc, A, nseg, err)
+                                  : launch_rpass_b<false, false>(lc, A, nseg, err));
     lc.launches++;
     return e;
 }
 
-cudaError_t launch_rbounds(Launch &lc, const int32_t *ii, const int32_t *jj, int z, int rbits,
-                           int32_t nsub, uint32_t *bnd, uint32_t *biglist, ErrState *err) {
+cudaError_t launch_rbounds(Launch &lc, const int2 *rec, int z, int rbits, int32_t nsub, uint32_t *bnd,
+                           uint32_t *biglist, ErrState *err) {
     const int64_t n = (int64_t)nsub + 1;
     cudaError_t e = launch_pdl(k_rbounds, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, lc.stream,
-                               ii, jj, z, rbits, nsub, bnd, biglist, err);
+                               rec, z, rbits, nsub, bnd, biglist, err);
     lc.launches++;
     return e;
 }

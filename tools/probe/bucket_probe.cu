@@ -148,6 +148,51 @@ __global__ void k_colred(const int32_t *jj, int64_t L, uint32_t *cnt) {
     }
 }
 
+
+// bucket count by global reductions (one RED per triplet, no shared histogram)
+__global__ void k_bred(const int32_t *jj, int64_t L, int shift, uint32_t *cnt) {
+    const int4 *j4 = reinterpret_cast<const int4 *>(jj);
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < L / 4; q += (int64_t)gridDim.x * blockDim.x) {
+        int4 v = __ldcs(j4 + q);
+        atomicAdd(&cnt[(v.x - 1) >> shift], 1u); atomicAdd(&cnt[(v.y - 1) >> shift], 1u);
+        atomicAdd(&cnt[(v.z - 1) >> shift], 1u); atomicAdd(&cnt[(v.w - 1) >> shift], 1u);
+    }
+}
+// record scatter: one returning global atomic per triplet (no aggregation), one
+// 16-byte record {local key, position, value} per triplet; Q quads per thread
+template <int Q>
+__global__ void __launch_bounds__(256) k_rscatter(const int32_t *ii, const int32_t *jj, const double *s, int64_t L,
+                                                  int shift, uint32_t *gcur, int rb, uint4 *rec) {
+    const int4 *i4 = reinterpret_cast<const int4 *>(ii);
+    const int4 *j4 = reinterpret_cast<const int4 *>(jj);
+    const double2 *s2 = reinterpret_cast<const double2 *>(s);
+    const int64_t q0 = ((int64_t)blockIdx.x * 256) * Q + threadIdx.x;
+    int I[4 * Q], J[4 * Q];
+    double S[4 * Q];
+#pragma unroll
+    for (int u = 0; u < Q; ++u) {
+        const int64_t q = q0 + u * 256;
+        int4 vi = make_int4(1, 1, 1, 1), vj = make_int4(0, 0, 0, 0);
+        double2 sa = make_double2(0, 0), sb = sa;
+        if (q < L / 4) { vi = __ldcs(i4 + q); vj = __ldcs(j4 + q); sa = __ldcs(s2 + 2 * q); sb = __ldcs(s2 + 2 * q + 1); }
+        I[4*u] = vi.x; I[4*u+1] = vi.y; I[4*u+2] = vi.z; I[4*u+3] = vi.w;
+        J[4*u] = vj.x; J[4*u+1] = vj.y; J[4*u+2] = vj.z; J[4*u+3] = vj.w;
+        S[4*u] = sa.x; S[4*u+1] = sa.y; S[4*u+2] = sb.x; S[4*u+3] = sb.y;
+    }
+    uint32_t slot[4 * Q];
+#pragma unroll
+    for (int k = 0; k < 4 * Q; ++k) slot[k] = J[k] > 0 ? atomicAdd(&gcur[(J[k] - 1) >> shift], 1u) : 0u;
+    const uint32_t cm = (1u << shift) - 1u;
+#pragma unroll
+    for (int k = 0; k < 4 * Q; ++k) {
+        if (J[k] <= 0) continue;
+        const int64_t pos = 4 * (q0 + (k >> 2) * 256) + (k & 3);
+        const unsigned long long vb = (unsigned long long)__double_as_longlong(S[k]);
+        rec[slot[k]] = make_uint4((((uint32_t)(J[k] - 1) & cm) << rb) | (uint32_t)(I[k] - 1), (uint32_t)pos,
+                                  (uint32_t)vb, (uint32_t)(vb >> 32));
+    }
+}
+
 int main(int argc, char **argv) {
     const int64_t L = argc > 1 ? atoll(argv[1]) : 500000000LL;
     const int M = 10000000, N = 10000000;
@@ -176,6 +221,31 @@ int main(int argc, char **argv) {
     double2 *zz; CK(cudaMalloc(&zz, L * 8));
     tm("copy 16B/16B", [&] { k_copy<<<sms * 4, 512>>>((const int4 *)ii, (const int4 *)jj, (const double2 *)s, x, (int4 *)cp_j, zz, L / 4); }, 32.0 * L);
     CK(cudaFree(cp_j)); CK(cudaFree(zz));
+
+    {
+        uint32_t *bc, *gcur; uint4 *rec;
+        CK(cudaMalloc(&bc, (size_t)B * 4)); CK(cudaMalloc(&gcur, (size_t)B * 4)); CK(cudaMalloc(&rec, (size_t)L * 16));
+        char nm[64];
+        for (int gm : {8, 32}) {
+            snprintf(nm, 64, "bucket RED count grid=%dx", gm);
+            tm(nm, [&] { cudaMemsetAsync(bc, 0, (size_t)B * 4); k_bred<<<sms * gm, 256>>>(jj, L, shift, bc); }, 4.0 * L);
+        }
+        std::vector<uint32_t> h(B);
+        CK(cudaMemcpy(h.data(), bc, B * 4, cudaMemcpyDeviceToHost));
+        uint32_t r = 0, mx = 0;
+        for (int b = 0; b < B; ++b) { uint32_t v = h[b]; h[b] = r; r += v; mx = v > mx ? v : mx; }
+        printf("   B=%d max bucket %u\n", B, mx);
+        uint32_t *base; CK(cudaMalloc(&base, (size_t)B * 4));
+        CK(cudaMemcpy(base, h.data(), B * 4, cudaMemcpyHostToDevice));
+        tm("record scatter Q=1", [&] { cudaMemcpyAsync(gcur, base, B * 4, cudaMemcpyDeviceToDevice);
+             k_rscatter<1><<<(unsigned)((L / 4 + 255) / 256), 256>>>(ii, jj, s, L, shift, gcur, 24, rec); }, 32.0 * L);
+        tm("record scatter Q=2", [&] { cudaMemcpyAsync(gcur, base, B * 4, cudaMemcpyDeviceToDevice);
+             k_rscatter<2><<<(unsigned)((L / 4 + 511) / 512), 256>>>(ii, jj, s, L, shift, gcur, 24, rec); }, 32.0 * L);
+        tm("record scatter Q=4", [&] { cudaMemcpyAsync(gcur, base, B * 4, cudaMemcpyDeviceToDevice);
+             k_rscatter<4><<<(unsigned)((L / 4 + 1023) / 1024), 256>>>(ii, jj, s, L, shift, gcur, 24, rec); }, 32.0 * L);
+        CK(cudaFree(bc)); CK(cudaFree(gcur)); CK(cudaFree(rec)); CK(cudaFree(base));
+    }
+    if (argc > 3) { printf("done\n"); return 0; }
     const int rb = 24, pb = 29;
     for (int gmul : {1}) {
         const int G = sms * gmul;
