@@ -286,6 +286,95 @@ __device__ __forceinline__ void put_rec(const RadixPassArgs &A, uint32_t o, uint
 }
 
 // ---------------------------------------------------------------------------
+// Pass building blocks shared by k_rpass and k_rpass_tma.
+//
+// Per-warp digit counters: RP_NW rows of RP_MAXD / 2 words (digits 2p and
+// 2p + 1 in the 16-bit halves of word p), row stride RP_CS = 257 words so that
+// the block-wide scan below (4 adjacent lanes per digit pair, 8 rows each)
+// reads 32 distinct banks.
+// ---------------------------------------------------------------------------
+#ifndef SA_PASS_V2
+#define SA_PASS_V2 1
+#endif
+#if SA_PASS_V2
+constexpr int RP_CS = RP_MAXD / 2 + 1;
+#else
+constexpr int RP_CS = RP_MAXD / 2;
+#endif
+
+// Stable rank of a triplet among its warp's triplets of digit d so far (the
+// running counter of (warp, d) advances by the step's group size).  Optimistic:
+// every valid lane reads the counter, then takes a slot with its own shared
+// atomic (one warp's shared-memory operations complete in program order, so
+// all lanes of a step read the count from before the step).  A lane whose
+// atomic returned something else shares its digit with another lane of this
+// step; only those digits are re-ranked in lane order (a ballot per distinct
+// conflicting digit) -- with 2^9 digits about one pair per step, against one
+// ballot per digit bit for every step.
+__device__ __forceinline__ unsigned rp_rank(uint32_t *cntw, unsigned d, bool valid, unsigned lt) {
+    const unsigned sh = (d & 1u) * 16u;
+    const unsigned addr = (unsigned)__cvta_generic_to_shared(cntw + (d >> 1));
+    unsigned c0 = 0, rr = 0;
+    if (valid) {
+        unsigned w0, w1;
+        asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(w0) : "r"(addr) : "memory");
+        asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(w1) : "r"(addr), "r"(1u << sh) : "memory");
+        c0 = (w0 >> sh) & 0xffffu;
+        rr = (w1 >> sh) & 0xffffu;
+    }
+    unsigned fl = __ballot_sync(FULL, rr != c0);
+    while (fl) {
+        const int f = __ffs(fl) - 1;
+        const unsigned df = __shfl_sync(FULL, d, f);
+        const bool mine = valid && d == df;
+        const unsigned same = __ballot_sync(FULL, mine);
+        if (mine) rr = c0 + __popc(same & lt);
+        fl &= ~same;
+    }
+    return rr;
+}
+
+// (digit, warp) digit-major exclusive scan of the per-warp counters, all
+// RP_NT threads: thread (p = tid / 4, q = tid % 4) owns digit pair p in the
+// warp rows 8 q .. 8 q + 7 (packed 16-bit adds; a half never exceeds the chunk
+// size).  Every counter becomes the chunk-local start of its (digit, warp)
+// run; returns through t0 / t1 / ex (valid for q == 0, p < npair) the pair's
+// digit totals and the chunk-local start of digit 2p, and the chunk total.
+template <int BITS>
+__device__ __forceinline__ void rp_scan(uint32_t *cnt, uint32_t *red, uint32_t &t0, uint32_t &t1, uint32_t &ex,
+                                        uint32_t &ctot) {
+    static_assert(RP_NT == 1024 && RP_NW == 32, "rp_scan layout");
+    constexpr int npair = ((1 << BITS) + 1) >> 1;
+    const int tid = threadIdx.x, lane = tid & 31, p = tid >> 2, q = tid & 3;
+    uint32_t c[8], part = 0;
+    uint32_t *cp = cnt + (q * 8) * RP_CS + p;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) c[i] = (p < npair) ? cp[i * RP_CS] : 0u;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const uint32_t x = c[i];
+        c[i] = part;
+        part += x;
+    }
+    uint32_t inc = part;
+    uint32_t y = __shfl_up_sync(FULL, inc, 1);
+    if (q >= 1) inc += y;
+    y = __shfl_up_sync(FULL, inc, 2);
+    if (q >= 2) inc += y;
+    const uint32_t before = inc - part;  // rows of lower q (packed)
+    const uint32_t totp = __shfl_sync(FULL, inc, lane | 3);
+    t0 = totp & 0xffffu;
+    t1 = totp >> 16;
+    const uint32_t exq = block_excl_sum<RP_NT, uint32_t>(q == 0 ? t0 + t1 : 0u, red, ctot);
+    ex = __shfl_sync(FULL, exq, lane & ~3);
+    if (p < npair) {
+        const uint32_t add = (ex + (before & 0xffffu)) | ((ex + t0 + (before >> 16)) << 16);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) cp[i * RP_CS] = c[i] + add;
+    }
+}
+
+// ---------------------------------------------------------------------------
 // k_rpass: one stable LSD partition pass by the digit (col-1) >> shift (the
 // downsweep).  CTA s walks the RP_CHUNK-triplet chunks of segment s in order;
 // warp w owns the chunk's w-th run of RP_IPT x 32 triplets.  All of a
@@ -302,7 +391,7 @@ __device__ __forceinline__ void put_rec(const RadixPassArgs &A, uint32_t o, uint
 struct PassSmem {
     uint4 rec[RP_CHUNK];              // reordered {row, col, value}
     uint32_t oidx[RP_CHUNK];          // output index of reordered slot k
-    uint32_t cnt[RP_NW][RP_MAXD / 2]; // per warp, digit pair (16-bit halves): running count, then base
+    uint32_t cnt[RP_NW][RP_CS];       // per warp, digit pair (16-bit halves): running count, then base
     uint32_t dtot[RP_MAXD];           // digit totals of the chunk
     uint32_t run[RP_MAXD];            // the chunk's global base per digit
     uint32_t red[RP_NW];
@@ -330,7 +419,7 @@ __global__ void __launch_bounds__(RP_NT, 1) k_rpass(RadixPassArgs A, ErrState *e
         const int64_t seg_hi = min(Lp, c0 + RP_CHUNK);
         {
             uint32_t *c32 = &S.cnt[0][0];
-            for (int k = tid; k < RP_NW * npair; k += RP_NT) c32[(k / npair) * (RP_MAXD / 2) + k % npair] = 0;
+            for (int k = tid; k < RP_NW * npair; k += RP_NT) c32[(k / npair) * RP_CS + k % npair] = 0;
             for (int k = tid; k < ndig; k += RP_NT) S.run[k] = A.off[c * RP_MAXD + k];
         }
         const int64_t base = c0 + (int64_t)w * (RP_IPT * 32) + lane;
@@ -360,6 +449,9 @@ __global__ void __launch_bounds__(RP_NT, 1) k_rpass(RadixPassArgs A, ErrState *e
             }
             const bool valid = live && (unsigned)(col[r] - 1) < (unsigned)N;
             const unsigned d = key_digit(col[r], row[r], shift, A.rbits, dmask);
+#if SA_PASS_V2
+            const unsigned rr = rp_rank(&S.cnt[w][0], d, valid, lt);
+#else
             // lanes with the same digit: one ballot per digit bit
             // (__match_any_sync runs on the slow ADU pipe)
             unsigned peers = __ballot_sync(FULL, valid);
@@ -376,10 +468,21 @@ __global__ void __launch_bounds__(RP_NT, 1) k_rpass(RadixPassArgs A, ErrState *e
             unsigned old = 0;
             if (lane == leader && valid) old = atomicAdd(&S.cnt[w][d >> 1], (unsigned)__popc(peers) << sh);
             const unsigned rr = ((__shfl_sync(FULL, old, leader & 31) >> sh) & 0xffffu) + __popc(peers & lt);
+#endif
             if (r & 1) rk[r >> 1] |= rr << 16;
             else rk[r >> 1] = rr;
         }
         __syncthreads();
+#if SA_PASS_V2
+        uint32_t t0, t1, ex, ctot;
+        rp_scan<BITS>(&S.cnt[0][0], S.red, t0, t1, ex, ctot);
+        if ((tid & 3) == 0 && (tid >> 2) < npair) {
+            // global position of chunk-local slot 0 of each digit: run - local start
+            const int pp = tid >> 2;
+            S.run[2 * pp] -= ex;
+            if (2 * pp + 1 < ndig) S.run[2 * pp + 1] -= ex + t0;
+        }
+#else
         // (digit, warp) digit-major scan: thread t owns the digit pair (2t, 2t+1)
         uint32_t t0 = 0, t1 = 0;
         if (tid < npair) {
@@ -401,6 +504,7 @@ __global__ void __launch_bounds__(RP_NT, 1) k_rpass(RadixPassArgs A, ErrState *e
             S.run[2 * tid] -= ex;
             if (2 * tid + 1 < ndig) S.run[2 * tid + 1] -= ex + t0;
         }
+#endif
         __syncthreads();
 #pragma unroll
         for (int r = 0; r < RP_IPT; ++r) {  // records to their sorted slots
@@ -447,7 +551,7 @@ constexpr int RT_IPT = RT_HALF / RP_NT;
 struct PassTmaSmem {
     uint4 buf[2][RT_HALF];            // staged {ii[], jj[], s[]} of a half, then its sorted records
     uint32_t oidx[RT_HALF];           // output index of sorted slot k
-    uint32_t cnt[RP_NW][RP_MAXD / 2]; // per warp, digit pair (16-bit halves)
+    uint32_t cnt[RP_NW][RP_CS];       // per warp, digit pair (16-bit halves)
     uint32_t hb[RP_MAXD];             // the half's global base per digit
     uint32_t run[RP_MAXD];
     uint32_t red[RP_NW];
@@ -525,7 +629,7 @@ __global__ void __launch_bounds__(RP_NT, 1) k_rpass_tma(RadixPassArgs A, ErrStat
             rt_issue(S, b ^ 1, A, half_start(k + 1), RT_HALF);
         {
             uint32_t *c32 = &S.cnt[0][0];
-            for (int q = tid; q < RP_NW * npair; q += RP_NT) c32[(q / npair) * (RP_MAXD / 2) + q % npair] = 0;
+            for (int q = tid; q < RP_NW * npair; q += RP_NT) c32[(q / npair) * RP_CS + q % npair] = 0;
             if ((k & 1) == 0)
                 for (int q = tid; q < ndig; q += RP_NT) S.hb[q] = A.off[c * RP_MAXD + q];
         }
@@ -565,6 +669,9 @@ __global__ void __launch_bounds__(RP_NT, 1) k_rpass_tma(RadixPassArgs A, ErrStat
             }
             const bool valid = live && (unsigned)(col[r] - 1) < (unsigned)N;
             const unsigned d = key_digit(col[r], row[r], shift, A.rbits, dmask);
+#if SA_PASS_V2
+            const unsigned rr = rp_rank(&S.cnt[w][0], d, valid, lt);
+#else
             unsigned peers = __ballot_sync(FULL, valid);
 #pragma unroll
             for (int i = 0; i < BITS; ++i) {
@@ -576,10 +683,26 @@ __global__ void __launch_bounds__(RP_NT, 1) k_rpass_tma(RadixPassArgs A, ErrStat
             unsigned old = 0;
             if (lane == leader && valid) old = atomicAdd(&S.cnt[w][d >> 1], (unsigned)__popc(peers) << sh);
             const unsigned rr = ((__shfl_sync(FULL, old, leader & 31) >> sh) & 0xffffu) + __popc(peers & lt);
+#endif
             if (r & 1) rk[r >> 1] |= rr << 16;
             else rk[r >> 1] = rr;
         }
         __syncthreads();
+#if SA_PASS_V2
+        uint32_t t0, t1, ex, ctot;
+        rp_scan<BITS>(&S.cnt[0][0], S.red, t0, t1, ex, ctot);
+        if ((tid & 3) == 0 && (tid >> 2) < npair) {
+            // global position of the half-local slot 0 of each digit; the next
+            // half of the chunk starts where this one ends
+            const int pp = tid >> 2;
+            S.run[2 * pp] = S.hb[2 * pp] - ex;
+            S.hb[2 * pp] += t0;
+            if (2 * pp + 1 < ndig) {
+                S.run[2 * pp + 1] = S.hb[2 * pp + 1] - (ex + t0);
+                S.hb[2 * pp + 1] += t1;
+            }
+        }
+#else
         uint32_t t0 = 0, t1 = 0;
         if (tid < npair) {
 #pragma unroll 8
@@ -605,6 +728,7 @@ __global__ void __launch_bounds__(RP_NT, 1) k_rpass_tma(RadixPassArgs A, ErrStat
                 S.hb[2 * tid + 1] += t1;
             }
         }
+#endif
         __syncthreads();
         uint4 *rec = &S.buf[b][0];
 #pragma unroll
