@@ -41,6 +41,7 @@
 // Look-back words carry a 16-bit tag (call epoch << 2 | pass) so the state
 // arrays never need resetting between calls.
 
+#include <cstddef>
 #include <cstdint>
 
 #include "sa_internal.cuh"
@@ -620,18 +621,26 @@ __global__ void __launch_bounds__(RP_NT, 1) k_rpass_tma(RadixPassArgs A, ErrStat
     // TMA only for whole halves (16-byte multiples); a partial tail half is
     // loaded by the threads
     if (tid == 0 && nmine > 0 && half_len(0) == RT_HALF) rt_issue(S, 0, A, half_start(0), RT_HALF);
+    // the chunk's digit bases, fetched one chunk ahead (thread d holds digit d)
+    static_assert(RP_MAXD <= RP_NT, "one digit base per thread");
+    uint32_t hbn = (tid < ndig && nmine > 0) ? A.off[(int64_t)blockIdx.x * RP_MAXD + tid] : 0u;
     for (int64_t k = 0; k < nmine; ++k) {
         const int b = (int)(k & 1);
         const int64_t h0 = half_start(k);
         const int nh = half_len(k);
         const int64_t c = blockIdx.x + (k >> 1) * gridDim.x;
-        if (tid == 0 && k + 1 < nmine && half_len(k + 1) == RT_HALF)
-            rt_issue(S, b ^ 1, A, half_start(k + 1), RT_HALF);
         {
-            uint32_t *c32 = &S.cnt[0][0];
-            for (int q = tid; q < RP_NW * npair; q += RP_NT) c32[(q / npair) * RP_CS + q % npair] = 0;
-            if ((k & 1) == 0)
-                for (int q = tid; q < ndig; q += RP_NT) S.hb[q] = A.off[c * RP_MAXD + q];
+            // (no barrier closes an iteration: the counters were last read
+            // before the previous half's write-out barrier)
+            static_assert(sizeof(S.cnt) % 16 == 0 && offsetof(PassTmaSmem, cnt) % 16 == 0, "vector clear");
+            uint4 *c128 = reinterpret_cast<uint4 *>(&S.cnt[0][0]);
+            for (int q = tid; q < (int)(sizeof(S.cnt) / 16); q += RP_NT) c128[q] = make_uint4(0u, 0u, 0u, 0u);
+            if ((k & 1) == 0) {
+                if (tid < ndig) {
+                    S.hb[tid] = hbn;
+                    if (k + 2 < nmine) hbn = A.off[(c + gridDim.x) * RP_MAXD + tid];
+                }
+            }
         }
         int32_t *si = reinterpret_cast<int32_t *>(&S.buf[b][0]);
         int32_t *sj = si + RT_HALF;
@@ -659,6 +668,10 @@ __global__ void __launch_bounds__(RP_NT, 1) k_rpass_tma(RadixPassArgs A, ErrStat
             val[r] = live ? (A.s_stride ? ss[q] : sc) : 0.0;
         }
         __syncthreads();  // counters cleared; the buffer is read (it now takes the sorted records)
+        // every thread is past the previous half's write-out: its buffer
+        // takes the next half while this one is ranked, placed and written
+        if (tid == 0 && k + 1 < nmine && half_len(k + 1) == RT_HALF)
+            rt_issue(S, b ^ 1, A, half_start(k + 1), RT_HALF);
         uint32_t rk[(RT_IPT + 1) / 2];
 #pragma unroll
         for (int r = 0; r < RT_IPT; ++r) {
@@ -745,7 +758,6 @@ __global__ void __launch_bounds__(RP_NT, 1) k_rpass_tma(RadixPassArgs A, ErrStat
         __syncthreads();
         const unsigned long long pol = l2_evict_last();
         for (int q = tid; q < (int)ctot; q += RP_NT) put_rec<LAST>(A, S.oidx[q], rec[q], pol);
-        __syncthreads();  // the buffer and the counters are reused by the half after next
     }
     pdl_trigger();
     if (FIRST) {
