@@ -297,6 +297,9 @@ __device__ __forceinline__ void put_rec(const RadixPassArgs &A, uint32_t o, uint
 #ifndef SA_PASS_V2
 #define SA_PASS_V2 1
 #endif
+#ifndef SA_PASS_NOIDX
+#define SA_PASS_NOIDX 1
+#endif
 #if SA_PASS_V2
 constexpr int RP_CS = RP_MAXD / 2 + 1;
 #else
@@ -752,12 +755,24 @@ __global__ void __launch_bounds__(RP_NT, 1) k_rpass_tma(RadixPassArgs A, ErrStat
                                      ((rk[r >> 1] >> ((r & 1) * 16)) & 0xffffu);
                 const unsigned long long vb = (unsigned long long)__double_as_longlong(val[r]);
                 rec[pos] = make_uint4((uint32_t)row[r], (uint32_t)col[r], (uint32_t)vb, (uint32_t)(vb >> 32));
+#if !SA_PASS_NOIDX
                 S.oidx[pos] = S.run[d] + pos;
+#endif
             }
         }
         __syncthreads();
         const unsigned long long pol = l2_evict_last();
+#if SA_PASS_NOIDX
+        // output index from the record's own digit: consecutive slots share a
+        // digit, so the base reads are near-broadcasts (a stored index per slot
+        // cost a scattered store and a scattered base read in the loop above)
+        for (int q = tid; q < (int)ctot; q += RP_NT) {
+            const uint4 v = rec[q];
+            put_rec<LAST>(A, S.run[key_digit((int)v.y, (int)v.x, shift, A.rbits, dmask)] + (uint32_t)q, v, pol);
+        }
+#else
         for (int q = tid; q < (int)ctot; q += RP_NT) put_rec<LAST>(A, S.oidx[q], rec[q], pol);
+#endif
     }
     pdl_trigger();
     if (FIRST) {
