@@ -937,6 +937,18 @@ __global__ void __launch_bounds__(BIG_NT, 1) k_rbig(RadixFoldArgs F, ErrState *e
 //      members sorted by k (insertion sort, <= 32) and folded from +0.0;
 //      ir / pr / jc written coalesced.
 // ---------------------------------------------------------------------------
+#ifndef SA_FOLD_GBAL
+#define SA_FOLD_GBAL 1
+#endif
+#ifndef SA_FOLD_CWARP
+#define SA_FOLD_CWARP 1
+#endif
+#ifndef SA_FOLD_XOR
+#define SA_FOLD_XOR 1
+#endif
+#ifndef SA_FOLD_LRANK
+#define SA_FOLD_LRANK 1
+#endif
 #ifndef SA_RF_NT
 #define SA_RF_NT 512
 #endif
@@ -964,6 +976,7 @@ struct FoldSmem {
     uint32_t colst[RF_WMAX + 1];  // distinct groups per column -> column start
     uint32_t colcur[RF_WMAX];
     uint16_t bigg[RF_BIGG];       // groups of more than 32 members
+    uint16_t cgrp[RF_CAP];        // group of column-list entry q
     uint32_t red[RF_NT / 32];
     int U, nbigg, sortall, b;
     long long off;
@@ -1142,17 +1155,18 @@ __global__ void __launch_bounds__(RF_NT, RF_MINB) k_rfold(RadixFoldArgs F, ErrSt
 #pragma unroll
     for (int u = 0; u < RIPT; ++u) {
         const uint32_t k = tid + u * RF_NT;
+        bool fresh = false;
+        unsigned h = 0;
         if (k < n) {
-            bool fresh;
-            const unsigned h = rf_insert(S.key, hbits, kk[u], fresh);
+            h = rf_insert(S.key, hbits, kk[u], fresh);
             S.gid[k] = (uint16_t)h;
             atomicAdd(&S.cnt2[h >> 1], 1u << ((h & 1u) * 16u));
-            if (fresh) {
-                const int g = atomicAdd(&S.U, 1);
-                S.glist[g] = (uint16_t)h;
-                S.gkey[g] = kk[u];
-                atomicAdd(&S.colst[(roff + kk[u] - 1u) >> F.rbits], 1u);
-            }
+        }
+        if (fresh) {
+            const int g = atomicAdd(&S.U, 1);
+            S.glist[g] = (uint16_t)h;
+            S.gkey[g] = kk[u];
+            atomicAdd(&S.colst[(roff + kk[u] - 1u) >> F.rbits], 1u);
         }
     }
     __syncthreads();
@@ -1160,14 +1174,48 @@ __global__ void __launch_bounds__(RF_NT, RF_MINB) k_rfold(RadixFoldArgs F, ErrSt
     if (tid == 0) ((volatile unsigned long long *)lbs)[0] = ep_pack(F.tag, s == 0 ? 2 : 1, (unsigned)U);
 
     // ---- 2. member starts, column starts ------------------------------------
+#if SA_FOLD_CWARP
+    if (warp == RF_NT / 32 - 1) {  // column starts: one warp's scan (no block-wide barriers)
+        constexpr int CPL = RF_WMAX / 32;
+        uint32_t v[CPL], sum = 0;
+#pragma unroll
+        for (int i = 0; i < CPL; ++i) {
+            const int c = lane * CPL + i;
+            v[i] = (c < ncol) ? S.colst[c] : 0u;
+            sum += v[i];
+        }
+        uint32_t x = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(FULL, x, o);
+            if (lane >= o) x += y;
+        }
+        uint32_t ex = x - sum;
+#pragma unroll
+        for (int i = 0; i < CPL; ++i) {
+            const int c = lane * CPL + i;
+            if (c < ncol) {
+                S.colst[c] = ex;
+                S.colcur[c] = ex;
+            }
+            ex += v[i];
+        }
+        if (lane == 31) S.colst[ncol] = ex;  // = U
+    }
+#endif
     {  // exclusive scan of the member counts in group order -> gstart; the slot's
        // count becomes its member cursor
-        const int g0 = tid * RIPT;
+#if SA_FOLD_GBAL
+        const int G = (U + RF_NT - 1) / RF_NT;  // groups per thread (<= RIPT)
+#else
+        const int G = RIPT;
+#endif
+        const int g0 = tid * G;
         uint32_t loc[RIPT], sum = 0;
 #pragma unroll
         for (int u = 0; u < RIPT; ++u) {
             loc[u] = 0u;
-            if (g0 + u < U) {
+            if (u < G && g0 + u < U) {
                 const unsigned h = S.glist[g0 + u];
                 loc[u] = (S.cnt2[h >> 1] >> ((h & 1u) * 16u)) & 0xffffu;
             }
@@ -1178,11 +1226,15 @@ __global__ void __launch_bounds__(RF_NT, RF_MINB) k_rfold(RadixFoldArgs F, ErrSt
 #pragma unroll
         for (int u = 0; u < RIPT; ++u) {
             const int g = g0 + u;
-            if (g < U) {
+            if (u < G && g < U) {
                 S.gstart[g] = (uint16_t)pre;
                 const unsigned h = S.glist[g], sh = (h & 1u) * 16u;
+#if SA_FOLD_XOR
+                atomicXor(&S.cnt2[h >> 1], (loc[u] ^ pre) << sh);  // count -> first member
+#else
                 atomicAnd(&S.cnt2[h >> 1], ~(0xffffu << sh));
                 atomicOr(&S.cnt2[h >> 1], pre << sh);
+#endif
                 if (loc[u] > 32u) {
                     const int q = atomicAdd(&S.nbigg, 1);
                     if (q < RF_BIGG) S.bigg[q] = (uint16_t)g;
@@ -1191,12 +1243,12 @@ __global__ void __launch_bounds__(RF_NT, RF_MINB) k_rfold(RadixFoldArgs F, ErrSt
             pre += loc[u];
         }
     }
+#if !SA_FOLD_CWARP
     smem_excl_scan<RF_NT, 1, uint32_t>(S.colst, ncol, S.red);
     for (int c = tid; c < ncol; c += RF_NT) S.colcur[c] = S.colst[c];
-    if (tid == 0) {
-        S.gstart[U] = (uint16_t)n;
-        S.colst[ncol] = (uint32_t)U;
-    }
+    if (tid == 0) S.colst[ncol] = (uint32_t)U;
+#endif
+    if (tid == 0) S.gstart[U] = (uint16_t)n;
     __syncthreads();
     // ---- 3. members (unordered), groups per column ---------------------------------
     uint32_t *ckey = S.key;  // the hash table is dead: column lists' keys
@@ -1212,6 +1264,7 @@ __global__ void __launch_bounds__(RF_NT, RF_MINB) k_rfold(RadixFoldArgs F, ErrSt
         const uint32_t kx = S.gkey[g];
         const uint32_t q = atomicAdd(&S.colcur[(roff + kx - 1u) >> F.rbits], 1u);
         ckey[q] = kx;  // column lists of the groups' keys (unordered)
+        S.cgrp[q] = (uint16_t)g;
     }
     __syncthreads();
     for (int q = warp; q < min(S.nbigg, RF_BIGG); q += RF_NT / 32) {  // big groups: rebuilt in order
@@ -1227,13 +1280,20 @@ __global__ void __launch_bounds__(RF_NT, RF_MINB) k_rfold(RadixFoldArgs F, ErrSt
         }
     }
     // ---- 4. output order: rank of every group among its column's groups ----------
-    uint16_t opos[RIPT];
+    // (walked in list order: the lanes of a warp share a few columns, so the
+    // list reads below are near-broadcasts; in group order every lane walked
+    // its own column's list)
+    uint32_t opos[RIPT];  // output position | group << 16
 #pragma unroll
     for (int u = 0; u < RIPT; ++u) {
-        const int g = tid + u * RF_NT;
+        const int t = tid + u * RF_NT;
         opos[u] = 0;
-        if (g < U) {
-            const uint32_t kx = S.gkey[g];
+        if (t < U) {
+#if SA_FOLD_LRANK
+            const uint32_t kx = ckey[t];
+#else
+            const uint32_t kx = S.gkey[t];
+#endif
             const uint32_t cl = (roff + kx - 1u) >> F.rbits;
             const int st = S.colst[cl], en = S.colst[cl + 1];
             if (en - st > 64) {
@@ -1241,7 +1301,11 @@ __global__ void __launch_bounds__(RF_NT, RF_MINB) k_rfold(RadixFoldArgs F, ErrSt
             } else {
                 int r = st;
                 for (int q = st; q < en; ++q) r += ckey[q] < kx;
-                opos[u] = (uint16_t)r;
+#if SA_FOLD_LRANK
+                opos[u] = (uint32_t)r | ((uint32_t)S.cgrp[t] << 16);
+#else
+                opos[u] = (uint32_t)r | ((uint32_t)t << 16);
+#endif
             }
         }
     }
@@ -1257,8 +1321,7 @@ __global__ void __launch_bounds__(RF_NT, RF_MINB) k_rfold(RadixFoldArgs F, ErrSt
     if (!sortall) {
 #pragma unroll
         for (int u = 0; u < RIPT; ++u) {
-            const int g = tid + u * RF_NT;
-            if (g < U) S.gid[opos[u]] = (uint16_t)g;  // gid := group of output entry
+            if (tid + u * RF_NT < U) S.gid[opos[u] & 0xffffu] = (uint16_t)(opos[u] >> 16);  // gid := group of output entry
         }
         const double *sg = F.s + a;
         for (uint32_t k = tid; k < n; k += RF_NT) rf_cp_async8(&Vs[k], sg + k);
