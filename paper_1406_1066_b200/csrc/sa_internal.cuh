@@ -449,6 +449,7 @@ struct RadixFoldArgs {
     unsigned tag;
     int z, rbits;            // sub-bucket s = the keys [s << z, (s + 1) << z), key as above
     int32_t N, nsub;
+    int32_t nres;            // fold CTAs in flight (set by launch_rfold)
     int32_t *jc, *ir;
     double *pr;
     int64_t cap;

@@ -943,6 +943,9 @@ __global__ void __launch_bounds__(BIG_NT, 1) k_rbig(RadixFoldArgs F, ErrState *e
 #ifndef SA_FOLD_CWARP
 #define SA_FOLD_CWARP 1
 #endif
+#ifndef SA_FOLD_PF
+#define SA_FOLD_PF 1
+#endif
 #ifndef SA_FOLD_XOR
 #define SA_FOLD_XOR 1
 #endif
@@ -1151,6 +1154,17 @@ __global__ void __launch_bounds__(RF_NT, RF_MINB) k_rfold(RadixFoldArgs F, ErrSt
             kk[u] = (uint32_t)(tkey(rc.y, rc.x, F.rbits) - K0) + 1u;
         }
     }
+#if SA_FOLD_PF
+    {  // the keys of the sub-bucket that takes this CTA's place when it retires: into L2
+        const int64_t sp = s + F.nres;
+        if (sp < F.nsub) {
+            const uint32_t a2 = F.bnd[sp], n2 = min(F.bnd[sp + 1] - a2, (uint32_t)RF_CAP);
+            const char *kb = reinterpret_cast<const char *>(F.rc + a2);
+            for (uint32_t o = (uint32_t)tid * 128u; o < n2 * 8u; o += RF_NT * 128u)
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(kb + o));
+        }
+    }
+#endif
     __syncthreads();
 #pragma unroll
     for (int u = 0; u < RIPT; ++u) {
@@ -1510,7 +1524,9 @@ cudaError_t launch_rfold(Launch &lc, const RadixFoldArgs &F, ErrState *err) {
     const int smem = (int)sizeof(FoldSmem);
     cudaError_t e = ensure_smem_attr((const void *)k_rfold, smem);
     if (e != cudaSuccess) return e;
-    e = launch_pdl(k_rfold, dim3((unsigned)F.nsub), dim3(RF_NT), smem, lc.stream, F, err);
+    RadixFoldArgs G = F;
+    G.nres = lc.num_sms * RF_MINB;  // CTAs in flight
+    e = launch_pdl(k_rfold, dim3((unsigned)F.nsub), dim3(RF_NT), smem, lc.stream, G, err);
     lc.launches++;
     return e;
 }
