@@ -153,13 +153,34 @@ __global__ void __launch_bounds__(RU_NT) k_rup(const int32_t *__restrict__ ii, c
     uint32_t bs = 0;  // block sum of digit threadIdx.x
     constexpr int UPT = RP_CHUNK / RU_NT;
     const int64_t cb = (int64_t)blockIdx.x * cpb, ce = min(nchunk, cb + cpb);
+    // Whole chunks of a 16-byte aligned array are read with 16-byte loads
+    // (thread t holds the elements 4 (t + 512 u) .. + 3: a histogram does not
+    // care which thread counts what), a partial last chunk or an unaligned
+    // array element by element.  Valid columns take the short way (one
+    // unsigned compare); the position of a bad one is worked out only then.
+    const bool al16 = (reinterpret_cast<uintptr_t>(jj) & 15) == 0;
+    const int csh = shift - rbits;
     int v[UPT];
+    auto vecmode = [&](int64_t c) { return al16 && (c + 1) * RP_CHUNK <= Lp; };
     auto load = [&](int64_t c, int (&x)[UPT]) {
-        const int64_t lo = c * RP_CHUNK, hi = min(Lp, lo + RP_CHUNK);
+        const int64_t lo = c * RP_CHUNK;
+        if (vecmode(c)) {
+            const int4 *p4 = reinterpret_cast<const int4 *>(jj + lo) + threadIdx.x;
 #pragma unroll
-        for (int u = 0; u < UPT; ++u) {
-            const int64_t t = lo + threadIdx.x + (int64_t)u * RU_NT;
-            x[u] = (t < hi) ? __ldcs(jj + t) : 0;
+            for (int u = 0; u < UPT / 4; ++u) {
+                const int4 q = __ldcs(p4 + u * RU_NT);
+                x[4 * u] = q.x;
+                x[4 * u + 1] = q.y;
+                x[4 * u + 2] = q.z;
+                x[4 * u + 3] = q.w;
+            }
+        } else {
+            const int64_t hi = min(Lp, lo + RP_CHUNK);
+#pragma unroll
+            for (int u = 0; u < UPT; ++u) {
+                const int64_t t = lo + threadIdx.x + (int64_t)u * RU_NT;
+                x[u] = (t < hi) ? __ldcs(jj + t) : 1;  // (padding: a valid column, not counted)
+            }
         }
     };
     if (cb < ce) load(cb, v);
@@ -169,19 +190,24 @@ __global__ void __launch_bounds__(RU_NT) k_rup(const int32_t *__restrict__ ii, c
         if (c + 1 < ce) load(c + 1, vn);
         uint32_t *hc = h[c & 1];
         const int64_t lo = c * RP_CHUNK, hi = min(Lp, lo + RP_CHUNK);
+        const bool vec = vecmode(c);
+        // element index of v[u] within the chunk
+        auto eidx = [&](int u) -> int {
+            return vec ? 4 * ((int)threadIdx.x + (u >> 2) * RU_NT) + (u & 3) : (int)threadIdx.x + u * RU_NT;
+        };
 #pragma unroll
         for (int u = 0; u < UPT; ++u) {
-            const int64_t t = lo + threadIdx.x + (int64_t)u * RU_NT;
-            if (t >= hi) continue;
             const int cc = v[u];
-            if (FIRST && cc < 1) bad = min(bad, (unsigned long long)t);
-            else if (FIRST && cc > N) over = 1;
-            else {
+            if (!FIRST || (unsigned)(cc - 1) < (unsigned)N) {
+                if (!vec && lo + eidx(u) >= hi) continue;  // padding of a partial chunk
                 if (ROWKEY)  // the digit takes row bits (row-split plan)
-                    atomicAdd(&hc[key_digit(cc, __ldcs(ii + t), shift, rbits, dmask)], 1u);
+                    atomicAdd(&hc[key_digit(cc, __ldcs(ii + lo + eidx(u)), shift, rbits, dmask)], 1u);
                 else
-                    atomicAdd(&hc[((unsigned)(cc - 1) >> (shift - rbits)) & dmask], 1u);
+                    atomicAdd(&hc[((unsigned)(cc - 1) >> csh) & dmask], 1u);
                 ++nval;
+            } else {
+                if (cc < 1) bad = min(bad, (unsigned long long)(lo + eidx(u)));
+                else over = 1;
             }
         }
         __syncthreads();
