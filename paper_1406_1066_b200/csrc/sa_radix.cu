@@ -1489,12 +1489,20 @@ static cudaError_t launch_rpass_t(Launch &lc, const RadixPassArgs &A, int nseg, 
         const int smem = (int)sizeof(PassTmaSmem);
         cudaError_t e = ensure_smem_attr((const void *)k_rpass_tma<FIRST, LAST, BITS>, smem);
         if (e != cudaSuccess) return e;
-        // grid: the first pass runs best with many short-lived CTAs (about 8
-        // chunks each; cfg4: 8.8 ms at one CTA per SM, 7.0 ms at 64 waves),
-        // the later ones with one CTA per SM (6.1 ms; 3 waves: 7.0 ms) --
-        // measured, tools/variant_time.py
+        // grid: the first pass runs best with many short-lived CTAs (cfg4:
+        // 9.6 ms at one CTA per SM, 6.75 / 6.19 / 5.95 / 5.94 / 5.92 / 6.22 ms
+        // at 16 / 8 / 4 / 3 / 2 / 1 chunks per CTA), the later ones with one
+        // CTA per SM (4.67 ms; 4 / 2 / 1 chunks per CTA: 4.75 / 4.85 / 5.30
+        // ms) -- measured, tools/abn.sh
+#ifndef SA_RP_FIRST_CPC
+#define SA_RP_FIRST_CPC 3
+#endif
+#ifndef SA_RP_LATER_CPC
+#define SA_RP_LATER_CPC 0
+#endif
         const int64_t nch = (A.L + RP_CHUNK - 1) / RP_CHUNK;
-        const int64_t grid = FIRST ? std::max<int64_t>(lc.num_sms, (nch + 7) / 8) : lc.num_sms;
+        const int cpc = FIRST ? SA_RP_FIRST_CPC : SA_RP_LATER_CPC;  // chunks per CTA (0: one CTA per SM)
+        const int64_t grid = cpc ? std::max<int64_t>(lc.num_sms, (nch + cpc - 1) / cpc) : lc.num_sms;
         return launch_pdl(k_rpass_tma<FIRST, LAST, BITS>, dim3((unsigned)grid), dim3(RP_NT), smem, lc.stream,
                           A, err);
     }
