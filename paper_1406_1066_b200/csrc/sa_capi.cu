@@ -50,7 +50,7 @@ struct sa_ctx {
     uint4 *ry = nullptr; int32_t *ry_i = nullptr, *ry_j = nullptr; double *ry_s = nullptr;  size_t ry_cap = 0;
     uint16_t *rcnt = nullptr;             size_t rcnt_cap = 0;         // nchunk x RP_MAXD chunk histograms
     uint32_t *roff = nullptr;             size_t roff_cap = 0;         // nchunk x RP_MAXD chunk bases
-    uint32_t *rbsum = nullptr;            size_t rbsum_cap = 0;        // nblk x RP_MAXD block bases
+    uint32_t *rbsum = nullptr;            size_t rbsum_cap = 0;        // (nblk + 1) x RP_MAXD: block bases, digit totals
     unsigned long long *rlbf = nullptr;   size_t rlbf_cap = 0;         // nsub x LB_STRIDE
     uint32_t *rbnd = nullptr;             size_t rbnd_cap = 0;         // nsub + 1
     uint32_t *rbig = nullptr;             size_t rbig_cap = 0;         // nsub (oversize list)
@@ -546,7 +546,7 @@ int assemble_radix(sa_ctx *ctx, const RadixPlan &P, const int32_t *ii, const int
     const int64_t nblk = (P.nchunk + cpb - 1) / cpb;
     SA_CUDA(ctx, ensure(ctx->rcnt, ctx->rcnt_cap, (size_t)P.nchunk * RP_MAXD));
     SA_CUDA(ctx, ensure(ctx->roff, ctx->roff_cap, (size_t)P.nchunk * RP_MAXD));
-    SA_CUDA(ctx, ensure(ctx->rbsum, ctx->rbsum_cap, (size_t)std::max<int64_t>(nblk, 1) * RP_MAXD));
+    SA_CUDA(ctx, ensure(ctx->rbsum, ctx->rbsum_cap, (size_t)(std::max<int64_t>(nblk, 1) + 1) * RP_MAXD));  // + the digit totals
     bool f2 = false;
     SA_CUDA(ctx, ensure_lb(ctx->rlbf, ctx->rlbf_cap, nsub * LB_STRIDE, ctx->stream, f2));
     SA_CUDA(ctx, ensure(ctx->rbnd, ctx->rbnd_cap, nsub + 1));

@@ -236,38 +236,50 @@ __global__ void __launch_bounds__(RU_NT) k_rup(const int32_t *__restrict__ ii, c
     pdl_trigger();
 }
 
-// k_rscan: bsum[B][d] := (exclusive prefix of the digit totals)[d] + the count
-// of digit d in blocks < B.  One CTA, a thread per digit.
-__global__ void __launch_bounds__(RP_MAXD) k_rscan(uint32_t *__restrict__ bsum, int nblk, int bits) {
-    __shared__ uint32_t red[RP_MAXD / 32];
-    const int d = threadIdx.x;
+// k_rscan: bsum[B][d] := the count of digit d in blocks < B; tot[d] := the
+// digit's total.  One warp per digit (lane q takes blocks q, q + 32, ...).
+__global__ void __launch_bounds__(256) k_rscan(uint32_t *__restrict__ bsum, uint32_t *__restrict__ tot, int nblk,
+                                               int bits) {
+    const int lane = threadIdx.x & 31;
+    const int d = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     pdl_wait();
-    const bool live = d < (1 << bits);
-    uint32_t run = 0;
-    if (live)
-        for (int q = 0; q < nblk; ++q) {
-            const uint32_t c = bsum[(int64_t)q * RP_MAXD + d];
-            bsum[(int64_t)q * RP_MAXD + d] = run;
-            run += c;
+    if (d < (1 << bits)) {
+        uint32_t run = 0;
+        for (int q0 = 0; q0 < nblk; q0 += 32) {
+            const int q = q0 + lane;
+            const uint32_t c = (q < nblk) ? bsum[(int64_t)q * RP_MAXD + d] : 0u;
+            uint32_t x = c;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(FULL, x, o);
+                if (lane >= o) x += y;
+            }
+            if (q < nblk) bsum[(int64_t)q * RP_MAXD + d] = run + x - c;
+            run += __shfl_sync(FULL, x, 31);
         }
-    uint32_t tot;
-    const uint32_t g = block_excl_sum<RP_MAXD, uint32_t>(live ? run : 0u, red, tot);
-    if (live)
-        for (int q = 0; q < nblk; ++q) bsum[(int64_t)q * RP_MAXD + d] += g;
+        if (lane == 0) tot[d] = run;
+    }
     pdl_trigger();
 }
 
-// k_roff: off[c][d] = the global position of chunk c's first digit-d triplet.
+// k_roff: off[c][d] = the global position of chunk c's first digit-d triplet
+// (the digit's base -- an exclusive scan of the digit totals, redone by
+// every CTA -- plus the digit's count in earlier blocks and chunks).
 __global__ void __launch_bounds__(RP_MAXD) k_roff(const uint16_t *__restrict__ cnt,
-                                                  const uint32_t *__restrict__ bsum, int bits,
+                                                  const uint32_t *__restrict__ bsum,
+                                                  const uint32_t *__restrict__ tot, int bits,
                                                   uint32_t *__restrict__ off, ErrState *err, int64_t L,
                                                   int first, int cpb) {
+    __shared__ uint32_t red[RP_MAXD / 32];
     const int d = threadIdx.x;
     pdl_wait();
     const int64_t Lp = first ? L : (int64_t)*((volatile const unsigned *)&err->rvalid);
     const int64_t nchunk = (Lp + RP_CHUNK - 1) / RP_CHUNK;
-    if (d < (1 << bits)) {
-        uint32_t run = bsum[(int64_t)blockIdx.x * RP_MAXD + d];
+    const bool live = d < (1 << bits);
+    uint32_t total;
+    const uint32_t g = block_excl_sum<RP_MAXD, uint32_t>(live ? tot[d] : 0u, red, total);
+    if (live) {
+        uint32_t run = g + bsum[(int64_t)blockIdx.x * RP_MAXD + d];
         const int64_t cb = (int64_t)blockIdx.x * cpb;
         for (int64_t c = cb; c < min(nchunk, cb + cpb); ++c) {
             off[c * RP_MAXD + d] = run;
@@ -1471,11 +1483,13 @@ cudaError_t launch_rup(Launch &lc, bool first, const int32_t *ii, const int32_t 
                                rbits, cpb, cnt, bsum, err);
     lc.launches++;
     if (e != cudaSuccess) return e;
-    e = launch_pdl(k_rscan, dim3(1), dim3(RP_MAXD), 0, lc.stream, bsum, nblk, bits);
+    // (the digit totals live behind the block sums: bsum has room for nblk + 1 rows)
+    uint32_t *tot = bsum + (int64_t)nblk * RP_MAXD;
+    e = launch_pdl(k_rscan, dim3((unsigned)((RP_MAXD + 7) / 8)), dim3(256), 0, lc.stream, bsum, tot, nblk, bits);
     lc.launches++;
     if (e != cudaSuccess) return e;
     e = launch_pdl(k_roff, dim3((unsigned)nblk), dim3(RP_MAXD), 0, lc.stream, (const uint16_t *)cnt,
-                   (const uint32_t *)bsum, bits, off, err, L, first ? 1 : 0, cpb);
+                   (const uint32_t *)bsum, (const uint32_t *)tot, bits, off, err, L, first ? 1 : 0, cpb);
     lc.launches++;
     return e;
 }
