@@ -425,12 +425,13 @@ constexpr int RF_CAP = 4096;                // fold: largest sub-bucket held in 
 constexpr int RF_WMAX = 256;                // fold: columns per sub-bucket (2^w)
 
 struct RadixPassArgs {
-    const int32_t *ii_in, *jj_in;
+    const int32_t *ii_in, *jj_in;  // the first pass's input (the caller's arrays)
+    const int2 *rc_in;             // the later passes' input: {row, col} pairs
     const double *s_in;
     int64_t s_stride;
-    int32_t *ii_out, *jj_out;  // output rows / columns (every pass but the last)
+    int32_t *ii_out, *jj_out;  // (SA_PAIRS == 0: output rows / columns of every pass but the last)
     double *s_out;             // output values
-    int2 *rc_out;              // the last pass: {row, col} pairs (8 B each) instead of ii / jj
+    int2 *rc_out;              // output {row, col} pairs (8 B each)
     int64_t L;
     int32_t M, N;
     int shift, bits;          // this pass's digit: (key >> shift) & (2^bits - 1) of the key

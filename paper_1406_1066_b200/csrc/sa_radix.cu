@@ -313,9 +313,12 @@ __device__ __forceinline__ void st_last(int2 *a, int2 v, unsigned long long pol)
 // {row, col} pair as one 8-byte store (what the fold and the bounds read),
 // the others separate row and column arrays (the next upsweep reads the
 // columns alone); the values go to their own array either way.
+#ifndef SA_PAIRS
+#define SA_PAIRS 0
+#endif
 template <bool LAST>
 __device__ __forceinline__ void put_rec(const RadixPassArgs &A, uint32_t o, uint4 v, unsigned long long pol) {
-    if (LAST) {
+    if (LAST || SA_PAIRS) {
         st_last(A.rc_out + o, make_int2((int)v.x, (int)v.y), pol);
     } else {
         st_last(A.ii_out + o, (int32_t)v.x, pol);
@@ -476,8 +479,14 @@ __global__ void __launch_bounds__(RP_NT, 1) k_rpass(RadixPassArgs A, ErrState *e
             const bool live = r * 32 + lane < nlive;
             // streaming loads (evict-first): the input must not push the
             // partially written output lines out of L2
-            col[r] = live ? __ldcs(jp + r * 32) : 0;
-            row[r] = live ? __ldcs(ip + r * 32) : 1;
+            if (!FIRST && SA_PAIRS) {
+                const int2 pr2 = live ? __ldcs(A.rc_in + base + r * 32) : make_int2(1, 0);
+                row[r] = pr2.x;
+                col[r] = pr2.y;
+            } else {
+                col[r] = live ? __ldcs(jp + r * 32) : 0;
+                row[r] = live ? __ldcs(ip + r * 32) : 1;
+            }
             val[r] = live ? __ldcs(sp + r * sstep) : 0.0;
         }
         __syncthreads();  // counters cleared (and the previous chunk's buffers drained)
@@ -603,6 +612,7 @@ struct PassTmaSmem {
 __device__ __forceinline__ unsigned rt_smem(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
 
 // Stage half h (triplets [h0, h0 + nh)) into buffer `b` (thread 0).
+template <bool PAIRS>
 __device__ __forceinline__ void rt_issue(PassTmaSmem &S, int b, const RadixPassArgs &A, int64_t h0, int nh) {
     int32_t *si = reinterpret_cast<int32_t *>(&S.buf[b][0]);
     int32_t *sj = si + RT_HALF;
@@ -612,10 +622,15 @@ __device__ __forceinline__ void rt_issue(PassTmaSmem &S, int b, const RadixPassA
     // the buffer was last written by the generic proxy (sorted records)
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(2 * bi + bs) : "memory");
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                 ::"r"(rt_smem(si)), "l"(A.ii_in + h0), "r"(bi), "r"(bar) : "memory");
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                 ::"r"(rt_smem(sj)), "l"(A.jj_in + h0), "r"(bi), "r"(bar) : "memory");
+    if (PAIRS) {  // {row, col} pairs: one copy into the si | sj regions
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                     ::"r"(rt_smem(si)), "l"(A.rc_in + h0), "r"(2 * bi), "r"(bar) : "memory");
+    } else {
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                     ::"r"(rt_smem(si)), "l"(A.ii_in + h0), "r"(bi), "r"(bar) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                     ::"r"(rt_smem(sj)), "l"(A.jj_in + h0), "r"(bi), "r"(bar) : "memory");
+    }
     if (bs)
         asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                      ::"r"(rt_smem(ss)), "l"(A.s_in + h0), "r"(bs), "r"(bar) : "memory");
@@ -637,6 +652,7 @@ __global__ void __launch_bounds__(RP_NT, 1) k_rpass_tma(RadixPassArgs A, ErrStat
     constexpr int ndig = 1 << BITS;
     constexpr unsigned dmask = (unsigned)ndig - 1u;
     constexpr int npair = (ndig + 1) >> 1;
+    constexpr bool PAIRS = !FIRST && SA_PAIRS;  // input: {row, col} pairs
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const unsigned lt = lanemask_lt();
     if (tid == 0) {
@@ -661,7 +677,7 @@ __global__ void __launch_bounds__(RP_NT, 1) k_rpass_tma(RadixPassArgs A, ErrStat
     auto half_len = [&](int64_t k) -> int { return (int)max((int64_t)0, min((int64_t)RT_HALF, Lp - half_start(k))); };
     // TMA only for whole halves (16-byte multiples); a partial tail half is
     // loaded by the threads
-    if (tid == 0 && nmine > 0 && half_len(0) == RT_HALF) rt_issue(S, 0, A, half_start(0), RT_HALF);
+    if (tid == 0 && nmine > 0 && half_len(0) == RT_HALF) rt_issue<PAIRS>(S, 0, A, half_start(0), RT_HALF);
     // the chunk's digit bases, fetched one chunk ahead (thread d holds digit d)
     static_assert(RP_MAXD <= RP_NT, "one digit base per thread");
     uint32_t hbn = (tid < ndig && nmine > 0) ? A.off[(int64_t)blockIdx.x * RP_MAXD + tid] : 0u;
@@ -690,8 +706,12 @@ __global__ void __launch_bounds__(RP_NT, 1) k_rpass_tma(RadixPassArgs A, ErrStat
             rt_wait(&S.mbar[b], (unsigned)((k >> 1) & 1));
         } else {  // tail half: plain loads into the buffer
             for (int q = tid; q < nh; q += RP_NT) {
-                si[q] = A.ii_in[h0 + q];
-                sj[q] = A.jj_in[h0 + q];
+                if (PAIRS) {
+                    reinterpret_cast<int2 *>(si)[q] = A.rc_in[h0 + q];
+                } else {
+                    si[q] = A.ii_in[h0 + q];
+                    sj[q] = A.jj_in[h0 + q];
+                }
                 if (A.s_stride) ss[q] = A.s_in[h0 + q];
             }
             __syncthreads();
@@ -704,15 +724,21 @@ __global__ void __launch_bounds__(RP_NT, 1) k_rpass_tma(RadixPassArgs A, ErrStat
         for (int r = 0; r < RT_IPT; ++r) {
             const int q = o0 + r * 32;
             const bool live = q < nh;
-            col[r] = live ? sj[q] : 0;
-            row[r] = live ? si[q] : 1;
+            if (PAIRS) {
+                const int2 pr2 = live ? reinterpret_cast<const int2 *>(si)[q] : make_int2(1, 0);
+                row[r] = pr2.x;
+                col[r] = pr2.y;
+            } else {
+                col[r] = live ? sj[q] : 0;
+                row[r] = live ? si[q] : 1;
+            }
             val[r] = live ? (A.s_stride ? ss[q] : sc) : 0.0;
         }
         __syncthreads();  // counters cleared; the buffer is read (it now takes the sorted records)
         // every thread is past the previous half's write-out: its buffer
         // takes the next half while this one is ranked, placed and written
         if (tid == 0 && k + 1 < nmine && half_len(k + 1) == RT_HALF)
-            rt_issue(S, b ^ 1, A, half_start(k + 1), RT_HALF);
+            rt_issue<PAIRS>(S, b ^ 1, A, half_start(k + 1), RT_HALF);
         uint32_t rk[(RT_IPT + 1) / 2];
 #pragma unroll
         for (int r = 0; r < RT_IPT; ++r) {
@@ -1003,6 +1029,15 @@ constexpr int RF_HS_BITS = RF_NT == 256 ? 12 : 13;
 static_assert((1 << RF_HS_BITS) == RF_HS, "hash table size");
 constexpr int RF_BIGG = 128;  // groups of > 32 members per sub-bucket (<= RF_CAP / 33)
 
+#ifdef SA_RTRACE
+// per-sub-bucket phase stamps of k_rfold (tools/rfold_trace.py): SM cycles
+__device__ long long g_rtrace[1 << 15][10];
+#define RTRACE(k) \
+    if (threadIdx.x == 0 && blockIdx.x < (1 << 15)) g_rtrace[blockIdx.x][k] = clock64();
+#else
+#define RTRACE(k)
+#endif
+
 struct FoldSmem {
     // key, cnt2 and glist are dead by the output phase: together (>= 8 RF_CAP
     // bytes) they take the staged values (or the fallback's sort items)
@@ -1019,7 +1054,7 @@ struct FoldSmem {
     uint16_t bigg[RF_BIGG];       // groups of more than 32 members
     uint16_t cgrp[RF_CAP];        // group of column-list entry q
     uint32_t red[RF_NT / 32];
-    int U, nbigg, sortall, b;
+    int U, nbigg, sortall, ndef;
     long long off;
 };
 
@@ -1098,6 +1133,7 @@ __global__ void __launch_bounds__(RF_NT, RF_MINB) k_rfold(RadixFoldArgs F, ErrSt
     // sub-bucket = block index (blocks are dispatched in index order, so the
     // look-back below only waits on started predecessors, as in the tile fold);
     // the error flags and the bounds are read concurrently
+    RTRACE(0)
     const int64_t s = blockIdx.x;
     const bool failed = call_failed(err);
     const uint32_t a = F.bnd[s], n = F.bnd[s + 1] - a;
@@ -1170,16 +1206,21 @@ __global__ void __launch_bounds__(RF_NT, RF_MINB) k_rfold(RadixFoldArgs F, ErrSt
         for (uint32_t o = (uint32_t)tid * 128u; o < nb; o += RF_NT * 128u)
             asm volatile("prefetch.global.L2 [%0];" ::"l"(vb + o));
     }
-    int hbits = 6;
-    while (hbits < RF_HS_BITS && (1u << hbits) < 2 * n) ++hbits;
+    // table of 2^hbits >= 2 n slots (64 .. RF_HS), cleared with 16-byte stores
+    const int hbits = n ? min(RF_HS_BITS, max(6, 32 - __clz((int)(2u * n) - 1))) : 6;
     const int hs = 1 << hbits;
-    for (int k = tid; k < hs; k += RF_NT) S.key[k] = 0u;
-    for (int k = tid; k < hs / 2; k += RF_NT) S.cnt2[k] = 0u;
+    static_assert(offsetof(FoldSmem, key) % 16 == 0 && offsetof(FoldSmem, cnt2) % 16 == 0, "vector clear");
+    {
+        uint4 *k4 = reinterpret_cast<uint4 *>(S.key), *c4 = reinterpret_cast<uint4 *>(S.cnt2);
+        for (int k = tid; k < hs / 4; k += RF_NT) k4[k] = make_uint4(0u, 0u, 0u, 0u);
+        for (int k = tid; k < hs / 8; k += RF_NT) c4[k] = make_uint4(0u, 0u, 0u, 0u);
+    }
     for (int c = tid; c <= ncol; c += RF_NT) S.colst[c] = 0;
     if (tid == 0) {
         S.U = 0;
         S.nbigg = 0;
         S.sortall = 0;
+        S.ndef = 0;
     }
     constexpr int RIPT = RF_CAP / RF_NT;
     uint32_t kk[RIPT];  // local key + 1 of records tid + u * RF_NT
@@ -1204,6 +1245,7 @@ __global__ void __launch_bounds__(RF_NT, RF_MINB) k_rfold(RadixFoldArgs F, ErrSt
     }
 #endif
     __syncthreads();
+    RTRACE(1)
 #pragma unroll
     for (int u = 0; u < RIPT; ++u) {
         const uint32_t k = tid + u * RF_NT;
@@ -1222,6 +1264,7 @@ __global__ void __launch_bounds__(RF_NT, RF_MINB) k_rfold(RadixFoldArgs F, ErrSt
         }
     }
     __syncthreads();
+    RTRACE(2)
     const int U = S.U;
     if (tid == 0) ((volatile unsigned long long *)lbs)[0] = ep_pack(F.tag, s == 0 ? 2 : 1, (unsigned)U);
 
@@ -1302,6 +1345,7 @@ __global__ void __launch_bounds__(RF_NT, RF_MINB) k_rfold(RadixFoldArgs F, ErrSt
 #endif
     if (tid == 0) S.gstart[U] = (uint16_t)n;
     __syncthreads();
+    RTRACE(3)
     // ---- 3. members (unordered), groups per column ---------------------------------
     uint32_t *ckey = S.key;  // the hash table is dead: column lists' keys
 #pragma unroll
@@ -1319,6 +1363,7 @@ __global__ void __launch_bounds__(RF_NT, RF_MINB) k_rfold(RadixFoldArgs F, ErrSt
         S.cgrp[q] = (uint16_t)g;
     }
     __syncthreads();
+    RTRACE(4)
     for (int q = warp; q < min(S.nbigg, RF_BIGG); q += RF_NT / 32) {  // big groups: rebuilt in order
         const int g = S.bigg[q];
         const unsigned h = S.glist[g];
@@ -1336,6 +1381,9 @@ __global__ void __launch_bounds__(RF_NT, RF_MINB) k_rfold(RadixFoldArgs F, ErrSt
     // list reads below are near-broadcasts; in group order every lane walked
     // its own column's list)
     uint32_t opos[RIPT];  // output position | group << 16
+    // output entries whose group has more than 8 members, listed over the
+    // dead member cursors (folded by the last threads of the CTA, below)
+    uint16_t *dl = reinterpret_cast<uint16_t *>(S.cnt2);
 #pragma unroll
     for (int u = 0; u < RIPT; ++u) {
         const int t = tid + u * RF_NT;
@@ -1354,7 +1402,9 @@ __global__ void __launch_bounds__(RF_NT, RF_MINB) k_rfold(RadixFoldArgs F, ErrSt
                 int r = st;
                 for (int q = st; q < en; ++q) r += ckey[q] < kx;
 #if SA_FOLD_LRANK
-                opos[u] = (uint32_t)r | ((uint32_t)S.cgrp[t] << 16);
+                const uint32_t g = S.cgrp[t];
+                opos[u] = (uint32_t)r | (g << 16);
+                if (S.gstart[g + 1] - S.gstart[g] > 8) dl[atomicAdd(&S.ndef, 1)] = (uint16_t)r;
 #else
                 opos[u] = (uint32_t)r | ((uint32_t)t << 16);
 #endif
@@ -1362,6 +1412,7 @@ __global__ void __launch_bounds__(RF_NT, RF_MINB) k_rfold(RadixFoldArgs F, ErrSt
         }
     }
     __syncthreads();
+    RTRACE(5)
     const bool sortall = S.sortall != 0;
     // the sub-bucket's values into shared memory (the dead hash table, member
     // counts and group slots: the ranking above was the last reader of ckey),
@@ -1399,6 +1450,12 @@ __global__ void __launch_bounds__(RF_NT, RF_MINB) k_rfold(RadixFoldArgs F, ErrSt
             }
         }
         for (int p = tid; p < U; p += RF_NT) S.gid[p] = (uint16_t)(items[p] & 0xffffu);
+        if (tid == 0) S.ndef = 0;  // (the ranking above listed some entries before it gave up)
+        __syncthreads();
+        for (int p = tid; p < U; p += RF_NT) {
+            const int g = S.gid[p];
+            if (S.gstart[g + 1] - S.gstart[g] > 8) dl[atomicAdd(&S.ndef, 1)] = (uint16_t)p;
+        }
     }
     // ---- 5. offset, fold, outputs -------------------------------------------------
     if (warp == 0) {
@@ -1409,20 +1466,53 @@ __global__ void __launch_bounds__(RF_NT, RF_MINB) k_rfold(RadixFoldArgs F, ErrSt
         }
     }
     __syncthreads();
+    RTRACE(6)
     asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
+    RTRACE(7)
     const long long off = S.off;
     const double *__restrict__ sv = sortall ? F.s + a : Vs;
+    // groups of more than 8 members (Poisson(5) repeats: 7 % of the groups)
+    // were listed by the ranking: folded one per thread, taken from the last
+    // thread down -- the warps with the fewest entries of the loop below -- so
+    // the 16-key network and the general loop run in a warp or two instead
+    // of in every warp for a few lanes each, and beside the small groups
+    // instead of after them
+    {
+        const int ndef = S.ndef;
+        for (int t = RF_NT - 1 - tid; t < ndef; t += RF_NT) {
+            const int p = dl[t];
+            const int g = S.gid[p];
+            const int st = S.gstart[g], en = S.gstart[g + 1];
+            const int nm = en - st;
+            double acc = 0.0;
+            if (nm <= 16) {
+                uint32_t m[16];
+#pragma unroll
+                for (int q = 0; q < 16; ++q) m[q] = (q < nm) ? (uint32_t)S.memb[st + q] : 0xffffu;
+                rf_net16(m);
+#pragma unroll
+                for (int q = 0; q < 16; ++q)
+                    if (q < nm) acc = fold_add(acc, sv[m[q]]);
+            } else {
+                if (nm <= 32) rf_isort16(S.memb + st, nm);
+                for (int q = st; q < en; ++q) acc = fold_add(acc, sv[S.memb[q]]);
+            }
+            if (off + p < F.cap) {
+                F.ir[off + p] = (int32_t)((roff + S.gkey[g] - 1u) & rmask);
+                F.pr[off + p] = acc;
+            } else {
+                over = true;
+            }
+        }
+    }
     for (int p = tid; p < U; p += RF_NT) {
         const int g = S.gid[p];
         const int st = S.gstart[g], en = S.gstart[g + 1];
-        const uint32_t kx = S.gkey[g];
-        double acc = 0.0;
         const int nm = en - st;
         if (nm <= 8) {
-            // up to 8 members (Poisson(5) repeats: 93 % of groups): member
-            // indices sorted by a register network, then every value load in
-            // flight at once before the ordered chain of adds
+            // member indices sorted by a register network, then every value
+            // load in flight at once before the ordered chain of adds
             uint32_t m[8];
 #pragma unroll
             for (int q = 0; q < 8; ++q) m[q] = (q < nm) ? (uint32_t)S.memb[st + q] : 0xffffu;
@@ -1430,26 +1520,16 @@ __global__ void __launch_bounds__(RF_NT, RF_MINB) k_rfold(RadixFoldArgs F, ErrSt
             double v[8];
 #pragma unroll
             for (int q = 0; q < 8; ++q) v[q] = (q < nm) ? sv[m[q]] : 0.0;
+            double acc = 0.0;
 #pragma unroll
             for (int q = 0; q < 8; ++q)
                 if (q < nm) acc = fold_add(acc, v[q]);
-        } else if (nm <= 16) {  // (7 % of the groups)
-            uint32_t m[16];
-#pragma unroll
-            for (int q = 0; q < 16; ++q) m[q] = (q < nm) ? (uint32_t)S.memb[st + q] : 0xffffu;
-            rf_net16(m);
-#pragma unroll
-            for (int q = 0; q < 16; ++q)
-                if (q < nm) acc = fold_add(acc, sv[m[q]]);
-        } else {
-            if (nm <= 32) rf_isort16(S.memb + st, nm);
-            for (int q = st; q < en; ++q) acc = fold_add(acc, sv[S.memb[q]]);
-        }
-        if (off + p < F.cap) {
-            F.ir[off + p] = (int32_t)((roff + kx - 1u) & rmask);
-            F.pr[off + p] = acc;
-        } else {
-            over = true;
+            if (off + p < F.cap) {
+                F.ir[off + p] = (int32_t)((roff + S.gkey[g] - 1u) & rmask);
+                F.pr[off + p] = acc;
+            } else {
+                over = true;
+            }
         }
     }
     for (int c = tid; c < njc; c += RF_NT) F.jc[c0 + c] = (int32_t)(off + S.colst[c]);
@@ -1459,8 +1539,17 @@ __global__ void __launch_bounds__(RF_NT, RF_MINB) k_rfold(RadixFoldArgs F, ErrSt
         if (off + U > F.cap) atomicExch(&err->cap_exceeded, 1u);
     }
     if (over) atomicExch(&err->cap_exceeded, 1u);
+    RTRACE(9)
     pdl_trigger();
 }
+
+#ifdef SA_RTRACE
+}  // namespace sa
+extern "C" int sa_debug_rtrace(void *host, int n) {
+    return (int)cudaMemcpyFromSymbol(host, sa::g_rtrace, (size_t)n * 80);
+}
+namespace sa {
+#endif
 
 // ---- launchers -----------------------------------------------------------------
 // Chunks per upsweep block: RP_BLK, fewer for small inputs so that every SM
