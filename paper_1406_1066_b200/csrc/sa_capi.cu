@@ -573,6 +573,7 @@ int assemble_radix(sa_ctx *ctx, const RadixPlan &P, const int32_t *ii, const int
         RadixPassArgs A{};
         A.ii_in = p ? bi[(p - 1) & 1] : ii;
         A.jj_in = p ? bj[(p - 1) & 1] : jj;
+        A.rc_in = p ? reinterpret_cast<const int2 *>(bi[(p - 1) & 1]) : nullptr;  // (the ii | jj regions)
         A.s_in = p ? bs[(p - 1) & 1] : s;
         A.s_stride = p ? 1 : s_stride;
         A.ii_out = bi[p & 1];
@@ -587,7 +588,7 @@ int assemble_radix(sa_ctx *ctx, const RadixPlan &P, const int32_t *ii, const int
         A.rbits = P.rbits;
         A.off = ctx->roff;
         if ((rc = mark(ctx, uname[p]))) return rc;
-        SA_CUDA(ctx, launch_rup(lc, p == 0, A.ii_in, A.jj_in, L, N, A.shift, A.bits, P.rbits, ctx->rcnt,
+        SA_CUDA(ctx, launch_rup(lc, p == 0, A.ii_in, A.jj_in, A.rc_in, L, N, A.shift, A.bits, P.rbits, ctx->rcnt,
                                 ctx->rbsum, ctx->roff, ctx->err));
         if ((rc = mark(ctx, pname[p]))) return rc;
         SA_CUDA(ctx, launch_rpass(lc, A, p == 0, p == P.npass - 1, nseg, ctx->err));

@@ -456,7 +456,8 @@ struct RadixFoldArgs {
     int64_t cap;
 };
 
-cudaError_t launch_rup(Launch &lc, bool first, const int32_t *ii, const int32_t *jj, int64_t L, int32_t N,
+cudaError_t launch_rup(Launch &lc, bool first, const int32_t *ii, const int32_t *jj, const int2 *rc, int64_t L,
+                       int32_t N,
                        int shift, int bits, int rbits, uint16_t *cnt, uint32_t *bsum, uint32_t *off,
                        ErrState *err);
 int rup_cpb(int64_t nchunk, int num_sms);  // chunks per upsweep block

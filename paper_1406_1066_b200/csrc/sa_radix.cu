@@ -129,13 +129,19 @@ __device__ __forceinline__ bool call_failed(const ErrState *err) {
     return err->bad_i != ~0ull || err->bad_j != ~0ull || err->over_m || err->over_n;
 }
 
+// Intermediate partition buffers hold {row, col} pairs (as the last pass's
+// output) instead of separate row and column arrays.
+#ifndef SA_PAIRS
+#define SA_PAIRS 1
+#endif
+
 // k_rup: per-chunk digit histograms cnt[c][d] (16-bit) of the pass input (jj)
 // and the block's sums bsum[B][d].  The first pass also validates the
 // columns (first index < 1, any index > N) and counts the valid triplets
 // (err->rvalid, the length the later passes read).
 template <bool FIRST, bool ROWKEY>
 __global__ void __launch_bounds__(RU_NT) k_rup(const int32_t *__restrict__ ii, const int32_t *__restrict__ jj,
-                                               int64_t L, int32_t N, int shift, int bits, int rbits, int cpb,
+                                               const int2 *__restrict__ rc, int64_t L, int32_t N, int shift, int bits, int rbits, int cpb,
                                                uint16_t *__restrict__ cnt, uint32_t *__restrict__ bsum,
                                                ErrState *err) {
     // two histograms: chunk c counts into h[c & 1] while the loads of chunk
@@ -158,9 +164,71 @@ __global__ void __launch_bounds__(RU_NT) k_rup(const int32_t *__restrict__ ii, c
     // care which thread counts what), a partial last chunk or an unaligned
     // array element by element.  Valid columns take the short way (one
     // unsigned compare); the position of a bad one is worked out only then.
-    const bool al16 = (reinterpret_cast<uintptr_t>(jj) & 15) == 0;
+    constexpr bool PAIRS = !FIRST && SA_PAIRS;  // input: {row, col} pairs (rc)
+    const bool al16 = ((PAIRS ? reinterpret_cast<uintptr_t>(rc) : reinterpret_cast<uintptr_t>(jj)) & 15) == 0;
     const int csh = shift - rbits;
     int v[UPT];
+#if SA_PAIRS
+    if (PAIRS) {
+        // thread t holds the pairs 2 (t + RU_NT u), + 1 of a whole chunk (one
+        // 16-byte load each), or t + RU_NT u of a partial / unaligned one
+        int vr[ROWKEY ? UPT : 1], vnr[ROWKEY ? UPT : 1];
+        auto vecmode = [&](int64_t c) { return al16 && (c + 1) * RP_CHUNK <= Lp; };
+        auto load = [&](int64_t c, int (&x)[UPT], int (&xr)[ROWKEY ? UPT : 1]) {
+            const int64_t lo = c * RP_CHUNK;
+            if (vecmode(c)) {
+                const int4 *p4 = reinterpret_cast<const int4 *>(rc + lo) + threadIdx.x;
+#pragma unroll
+                for (int u = 0; u < UPT / 2; ++u) {
+                    const int4 q = __ldcs(p4 + u * RU_NT);
+                    x[2 * u] = q.y;
+                    x[2 * u + 1] = q.w;
+                    if (ROWKEY) {
+                        xr[2 * u] = q.x;
+                        xr[2 * u + 1] = q.z;
+                    }
+                }
+            } else {
+                const int64_t hi = min(Lp, lo + RP_CHUNK);
+#pragma unroll
+                for (int u = 0; u < UPT; ++u) {
+                    const int64_t t = lo + threadIdx.x + (int64_t)u * RU_NT;
+                    const int2 q = (t < hi) ? __ldcs(rc + t) : make_int2(1, 0);  // (column 0: padding)
+                    x[u] = q.y;
+                    if (ROWKEY) xr[u] = q.x;
+                }
+            }
+        };
+        if (cb < ce) load(cb, v, vr);
+        __syncthreads();
+        for (int64_t c = cb; c < ce; ++c) {
+            int vn[UPT];
+            if (c + 1 < ce) load(c + 1, vn, vnr);
+            uint32_t *hc = h[c & 1];
+#pragma unroll
+            for (int u = 0; u < UPT; ++u) {
+                const int cc = v[u];
+                if (cc < 1) continue;  // padding of a partial chunk (stored columns are valid)
+                if (ROWKEY) atomicAdd(&hc[key_digit(cc, vr[ROWKEY ? u : 0], shift, rbits, dmask)], 1u);
+                else atomicAdd(&hc[((unsigned)(cc - 1) >> csh) & dmask], 1u);
+            }
+            __syncthreads();
+            for (int k = threadIdx.x; k < ndig; k += RU_NT) {
+                cnt[c * RP_MAXD + k] = (uint16_t)hc[k];
+                bs += hc[k];  // RU_NT == RP_MAXD: thread k owns digit k
+                hc[k] = 0;
+            }
+#pragma unroll
+            for (int u = 0; u < UPT; ++u) {
+                v[u] = vn[u];
+                if (ROWKEY) vr[u] = vnr[u];
+            }
+        }
+        if (threadIdx.x < ndig) bsum[(int64_t)blockIdx.x * RP_MAXD + threadIdx.x] = bs;
+        pdl_trigger();
+        return;
+    }
+#endif
     auto vecmode = [&](int64_t c) { return al16 && (c + 1) * RP_CHUNK <= Lp; };
     auto load = [&](int64_t c, int (&x)[UPT]) {
         const int64_t lo = c * RP_CHUNK;
@@ -313,9 +381,6 @@ __device__ __forceinline__ void st_last(int2 *a, int2 v, unsigned long long pol)
 // {row, col} pair as one 8-byte store (what the fold and the bounds read),
 // the others separate row and column arrays (the next upsweep reads the
 // columns alone); the values go to their own array either way.
-#ifndef SA_PAIRS
-#define SA_PAIRS 0
-#endif
 template <bool LAST>
 __device__ __forceinline__ void put_rec(const RadixPassArgs &A, uint32_t o, uint4 v, unsigned long long pol) {
     if (LAST || SA_PAIRS) {
@@ -1558,7 +1623,8 @@ int rup_cpb(int64_t nchunk, int num_sms) {
     return (int)std::max<int64_t>(1, std::min<int64_t>(RP_BLK, nchunk / (4 * (int64_t)num_sms)));
 }
 
-cudaError_t launch_rup(Launch &lc, bool first, const int32_t *ii, const int32_t *jj, int64_t L, int32_t N,
+cudaError_t launch_rup(Launch &lc, bool first, const int32_t *ii, const int32_t *jj, const int2 *rc, int64_t L,
+                       int32_t N,
                        int shift, int bits, int rbits, uint16_t *cnt, uint32_t *bsum, uint32_t *off,
                        ErrState *err) {
     // grid sized for L (an upper bound of the valid count the later passes read)
@@ -1568,7 +1634,7 @@ cudaError_t launch_rup(Launch &lc, bool first, const int32_t *ii, const int32_t 
     const bool rowkey = shift < rbits;
     auto kern = first ? (rowkey ? k_rup<true, true> : k_rup<true, false>)
                       : (rowkey ? k_rup<false, true> : k_rup<false, false>);
-    cudaError_t e = launch_pdl(kern, dim3((unsigned)nblk), dim3(RU_NT), 0, lc.stream, ii, jj, L, N, shift, bits,
+    cudaError_t e = launch_pdl(kern, dim3((unsigned)nblk), dim3(RU_NT), 0, lc.stream, ii, jj, rc, L, N, shift, bits,
                                rbits, cpb, cnt, bsum, err);
     lc.launches++;
     if (e != cudaSuccess) return e;
@@ -1588,7 +1654,8 @@ static cudaError_t launch_rpass_t(Launch &lc, const RadixPassArgs &A, int nseg, 
     auto al16 = [](const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
     // TMA-staged input (cfg4: pass 1 8.3 -> 7.0 ms, pass 2 7.0 -> 6.1 ms)
     const bool tma = lc.rpass_tma != 0;
-    if (tma && al16(A.ii_in) && al16(A.jj_in) && (A.s_stride == 0 || al16(A.s_in))) {
+    const bool in16 = (!FIRST && SA_PAIRS) ? al16(A.rc_in) : (al16(A.ii_in) && al16(A.jj_in));
+    if (tma && in16 && (A.s_stride == 0 || al16(A.s_in))) {
         const int smem = (int)sizeof(PassTmaSmem);
         cudaError_t e = ensure_smem_attr((const void *)k_rpass_tma<FIRST, LAST, BITS>, smem);
         if (e != cudaSuccess) return e;
