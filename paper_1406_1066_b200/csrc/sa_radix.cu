@@ -1078,6 +1078,9 @@ __global__ void __launch_bounds__(BIG_NT, 1) k_rbig(RadixFoldArgs F, ErrState *e
 #ifndef SA_FOLD_XOR
 #define SA_FOLD_XOR 1
 #endif
+#ifndef SA_FOLD_K32
+#define SA_FOLD_K32 1
+#endif
 #ifndef SA_FOLD_LRANK
 #define SA_FOLD_LRANK 1
 #endif
@@ -1288,6 +1291,9 @@ __global__ void __launch_bounds__(RF_NT, RF_MINB) k_rfold(RadixFoldArgs F, ErrSt
         S.ndef = 0;
     }
     constexpr int RIPT = RF_CAP / RF_NT;
+#if SA_FOLD_K32
+    const int ksh = min(F.rbits, 31);  // (rbits == 32 only with one column block: the shifted term is 0)
+#endif
     uint32_t kk[RIPT];  // local key + 1 of records tid + u * RF_NT
 #pragma unroll
     for (int u = 0; u < RIPT; ++u) {
@@ -1295,7 +1301,13 @@ __global__ void __launch_bounds__(RF_NT, RF_MINB) k_rfold(RadixFoldArgs F, ErrSt
         kk[u] = 0u;
         if (k < n) {
             const int2 rc = __ldg(F.rc + a + k);  // {row, col}
+#if SA_FOLD_K32
+            // local key + 1 in 32 bits: ((col - 1 - c0) << rbits) + row - roff
+            // (column-block plan: roff = 0; row-split plan: col - 1 == c0)
+            kk[u] = (((uint32_t)(rc.y - 1) - (uint32_t)c0) << ksh) + (uint32_t)rc.x - roff;
+#else
             kk[u] = (uint32_t)(tkey(rc.y, rc.x, F.rbits) - K0) + 1u;
+#endif
         }
     }
 #if SA_FOLD_PF

@@ -1,3 +1,4 @@
-O=gpurun_out/w7; mkdir -p $O
-timeout 1500 python -m pytest tests -m gpu -x -q > $O/pytest.log 2>&1; echo rc=$? >> $O/pytest.log
-python bench.py --steps 10 --warmup 3 > $O/bench_cfg4.json 2> $O/bench_cfg4.err
+O=gpurun_out/w9; mkdir -p $O
+bash tools/abn.sh w9 4 k0 k1
+cp paper_1406_1066_b200/lib/libsa_k1.so paper_1406_1066_b200/lib/libsa_b200.so
+python tools/radix_check.py > $O/check.txt 2>&1
