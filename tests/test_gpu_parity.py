@@ -769,6 +769,44 @@ def test_long_columns_row_split_bit_exact(m, n, L):
     assert sa.default_assembler(0).launch_count() > 6  # the radix pipeline ran
 
 
+@pytest.mark.parametrize("tma", [1, 0])
+def test_three_pass_radix_plan_bit_exact(tma):
+    """2e8 columns: the radix plan needs three partition passes (28 column
+    bits above 256-column sub-buckets), so the middle pass both reads and
+    writes the {row, col} pair buffers and the second and third upsweeps read
+    their columns out of the pairs -- with TMA-staged and register-loaded
+    passes, bit-exact against the C oracle."""
+    import ctypes
+
+    from paper_1406_1066_b200 import _capi
+
+    m, n, P, reps = 50_000, 200_000_000, 1_000_000, 4
+    rng = np.random.default_rng(77)
+    pi = rng.integers(1, m + 1, size=P).astype(np.int32)
+    pj = rng.integers(1, n + 1, size=P).astype(np.int32)
+    pj[:1000] = n  # the last column, repeated
+    sel = rng.permutation(np.repeat(np.arange(P), reps))
+    ii, jj = pi[sel], pj[sel]
+    s = rng.standard_normal(len(ii))
+    ref = O.assemble_counting(ii, jj, s, m, n)
+    a = sa.default_assembler(0)
+    a.set_option(_capi.SA_OPT_PATH, 1)
+    a.set_option(_capi.SA_OPT_RPASS_TMA, tma)
+    a.lib.sa_enable_timing(a.ctx, 1)
+    try:
+        got = a.assemble(ii, jj, s, m=m, n=n)
+        arr = (ctypes.c_float * 16)()
+        names = (ctypes.c_char_p * 16)()
+        nk = a.lib.sa_last_kernel_times(a.ctx, 16, arr, names)
+        ran = [names[k].decode() for k in range(nk)]
+    finally:
+        a.lib.sa_enable_timing(a.ctx, 0)
+        a.set_option(_capi.SA_OPT_PATH, -1)
+        a.set_option(_capi.SA_OPT_RPASS_TMA, -1)
+    _same(got, ref)
+    assert "k_rpass2" in ran and "k_rpass3" not in ran, ran
+
+
 def test_host_dims_inferred_during_chunked_upload():
     """Dimension inference fused into the upload (sa_host_upload runs the
     validation / maxima pass over each landed chunk while the next one is
