@@ -978,6 +978,42 @@ __global__ void __launch_bounds__(BIG_NT, 1) k_rbig(RadixFoldArgs F, ErrState *e
         return;
     }
     const int passes = (F.z + 7) / 8;
+    if (passes == 0) {
+        // z == 0: a sub-bucket is one (row, col) key, i.e. one run of n > RF_CAP
+        // repeats already in input order (the partition is stable).  Nothing to
+        // sort: one warp per sub-bucket reads the values 32 at a time (the next
+        // 32 in flight) and every lane folds them in order through shuffles --
+        // the chain of n ordered adds is the floor; with a CTA per sub-bucket
+        // one thread walked the run through global memory (1e7 triplets on
+        // 1000 keys: 7.7 ms).
+        const int lane = tid & 31;
+        const unsigned wpg = gridDim.x * (BIG_NT / 32);
+        for (unsigned q = blockIdx.x * (BIG_NT / 32) + (tid >> 5); q < nbig; q += wpg) {
+            const uint32_t s = F.biglist[q];
+            const uint32_t a = F.bnd[s], n = F.bnd[s + 1] - a;
+            const double *v = F.s + a;
+            double acc = 0.0;
+            double x = (uint32_t)lane < n ? __ldg(v + lane) : 0.0;
+            for (uint32_t k0 = 0; k0 < n; k0 += 32) {
+                const double xn = (k0 + 32 + lane < n) ? __ldg(v + k0 + 32 + lane) : 0.0;
+                const int cnt = (int)min(32u, n - k0);
+                if (cnt == 32) {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) acc = fold_add(acc, __shfl_sync(FULL, x, j));
+                } else {
+                    for (int j = 0; j < cnt; ++j) acc = fold_add(acc, __shfl_sync(FULL, x, j));
+                }
+                x = xn;
+            }
+            if (lane == 0) {  // one result: local key 0 in A, its value in B
+                F.scrA[a] = 0ull;
+                F.scrB[a] = (unsigned long long)__double_as_longlong(acc);
+                F.bigu[s] = 1u;
+            }
+        }
+        pdl_trigger();
+        return;
+    }
     for (unsigned q = blockIdx.x; q < nbig; q += gridDim.x) {
         const uint32_t s = F.biglist[q];
         const uint32_t a = F.bnd[s], n = F.bnd[s + 1] - a;

@@ -769,6 +769,34 @@ def test_long_columns_row_split_bit_exact(m, n, L):
     assert sa.default_assembler(0).launch_count() > 6  # the radix pipeline ran
 
 
+@pytest.mark.parametrize("m,n,L", [(5, 5, 400_000), (1000, 1, 6_000_000), (1, 1, 300_000)])
+def test_single_key_oversize_sub_buckets_bit_exact(m, n, L):
+    """So many repeats per (row, col) that the row-split plan reaches z = 0 (a
+    sub-bucket is one key) and every sub-bucket exceeds the fold's capacity:
+    k_rbig folds each run in input order with one warp (no sort) -- the
+    reference's long-run instances (conftest.py:43-45) at scale, with NaN and
+    -0.0 among the values; bit-exact against the C oracle."""
+    rng = np.random.default_rng(L + m)
+    ii = rng.integers(1, m + 1, size=L).astype(np.int32)
+    jj = rng.integers(1, n + 1, size=L).astype(np.int32)
+    s = rng.standard_normal(L)
+    s[rng.random(L) < 1e-4] = -0.0
+    if m == 5:
+        s[(ii == 2) & (jj == 3) & (rng.random(L) < 1e-3)] = np.nan
+    from paper_1406_1066_b200 import _capi
+
+    ref = O.assemble_counting(ii, jj, s, m, n)
+    a = sa.default_assembler(0)
+    for path in (-1, 1):  # the automatic choice, and the radix path forced
+        a.set_option(_capi.SA_OPT_PATH, path)
+        try:
+            got = a.assemble(ii, jj, s, m=m, n=n)
+        finally:
+            a.set_option(_capi.SA_OPT_PATH, -1)
+        _same(got, ref)
+    assert a.launch_count() > 6  # the radix pipeline ran
+
+
 @pytest.mark.parametrize("tma", [1, 0])
 def test_three_pass_radix_plan_bit_exact(tma):
     """2e8 columns: the radix plan needs three partition passes (28 column
