@@ -103,6 +103,40 @@ __device__ __forceinline__ double fold_add(double acc, double v) {
     return (acc != acc) ? acc : __dadd_rn(acc, v);
 }
 
+// Ordered fold, from +0.0, of the n values (bit patterns) at v by one warp:
+// the values are read 32 at a time (the next 32 in flight) and handed round
+// by shuffles, every lane running the same chain of adds -- the chain is
+// the floor of a long run of repeats.  Whole blocks of 32 use plain adds
+// (fold_add's bits unless the sum turns NaN: NaN is sticky, so a non-NaN
+// result met no NaN on the way; the block is redone by the rule otherwise),
+// which keeps the rule's compare and select off the dependent chain.
+__device__ __forceinline__ double warp_fold_run(const unsigned long long *v, int64_t n) {
+    const int lane = threadIdx.x & 31;
+    double acc = 0.0;
+    unsigned long long x = (lane < n) ? v[lane] : 0ull;
+    for (int64_t k0 = 0; k0 < n; k0 += 32) {
+        const unsigned long long xn = (k0 + 32 + lane < n) ? v[k0 + 32 + lane] : 0ull;
+        if (n - k0 >= 32) {
+            double t = acc;
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+                t = __dadd_rn(t, __longlong_as_double((long long)__shfl_sync(0xffffffffu, x, j)));
+            if (t != t) {
+                t = acc;
+                for (int j = 0; j < 32; ++j)
+                    t = fold_add(t, __longlong_as_double((long long)__shfl_sync(0xffffffffu, x, j)));
+            }
+            acc = t;
+        } else {
+            const int cnt = (int)(n - k0);
+            for (int j = 0; j < cnt; ++j)
+                acc = fold_add(acc, __longlong_as_double((long long)__shfl_sync(0xffffffffu, x, j)));
+        }
+        x = xn;
+    }
+    return acc;
+}
+
 // ---- decoupled look-back (single-pass chained scan) ----------------------
 // status word: bits 63:62 flag (0 empty, 1 aggregate, 2 inclusive prefix),
 // bits 61:0 value.

@@ -1067,6 +1067,8 @@ __device__ __forceinline__ void med_column(BigCol *bcp, uint32_t st, int n, unsi
     quarter_sync(q);  // K, V and s_qw are free for the next column
 }
 
+constexpr int BIGC_LONGRUN = 256;  // runs of equal rows longer than this are folded by a warp
+constexpr int BIGC_NLONG = 256;    // listed long runs per column (more: walked by their thread)
 __global__ void __launch_bounds__(BIG_NT, 2) k_bigcol(BigCol *__restrict__ big_list,
                                                    const ErrState *err, int4 *rec,
                                                    const uint2 *__restrict__ perm, Segs S,
@@ -1074,6 +1076,8 @@ __global__ void __launch_bounds__(BIG_NT, 2) k_bigcol(BigCol *__restrict__ big_l
     __shared__ uint32_t s_cnt[BIG_NW][256];
     __shared__ uint32_t s_warp[BIG_NW];
     __shared__ unsigned long long s_prevrow;
+    __shared__ uint2 s_long[BIGC_NLONG];  // long runs of the column: [first, end)
+    __shared__ int s_nlong;
     extern __shared__ unsigned long long s_med[];  // [MED_Q][2 * MED_CAP]
     const int tid = threadIdx.x;
     pdl_wait();
@@ -1141,6 +1145,12 @@ __global__ void __launch_bounds__(BIG_NT, 2) k_bigcol(BigCol *__restrict__ big_l
         // ordered fold of runs of equal rows, all runs at once: thread t folds
         // the runs whose head lies in its segment (a run may extend past it);
         // the result lands at the run's head (row in src, value in dst)
+        // A run longer than BIGC_LONGRUN (a heavy hitter: one entry repeated
+        // over and over) is only listed (its end by binary search: the rows are
+        // sorted) and folded by a warp afterwards (warp_fold_run): one thread
+        // walking it through global memory costs ~100+ cycles per repeat.
+        if (tid == 0) s_nlong = 0;
+        __syncthreads();
         {
             const int64_t lo = (int64_t)tid * n / BIG_NT, hi = (int64_t)(tid + 1) * n / BIG_NT;
             int64_t p = lo;
@@ -1150,6 +1160,20 @@ __global__ void __launch_bounds__(BIG_NT, 2) k_bigcol(BigCol *__restrict__ big_l
                     ++p;
                     continue;
                 }
+                if (p + BIGC_LONGRUN < n && (src[p + BIGC_LONGRUN] >> idx_bits) == row) {
+                    int64_t a2 = p + BIGC_LONGRUN + 1, b2 = n;  // first index in [a2, b2] of another row
+                    while (a2 < b2) {
+                        const int64_t mid = (a2 + b2) >> 1;
+                        if ((src[mid] >> idx_bits) == row) a2 = mid + 1;
+                        else b2 = mid;
+                    }
+                    const int e = atomicAdd(&s_nlong, 1);
+                    if (e < BIGC_NLONG) {
+                        s_long[e] = make_uint2((uint32_t)p, (uint32_t)a2);
+                        p = a2;
+                        continue;
+                    }
+                }
                 double acc = fold_add(0.0, __longlong_as_double((long long)dst[p]));
                 int64_t q = p + 1;
                 while (q < n && (src[q] >> idx_bits) == row) {
@@ -1158,6 +1182,16 @@ __global__ void __launch_bounds__(BIG_NT, 2) k_bigcol(BigCol *__restrict__ big_l
                 }
                 dst[p] = (unsigned long long)__double_as_longlong(acc);
                 p = q;
+            }
+        }
+        __syncthreads();
+        {
+            const int nl = min(s_nlong, BIGC_NLONG);
+            for (int e = tid >> 5; e < nl; e += BIG_NT / 32) {
+                const uint32_t q0 = s_long[e].x, q1 = s_long[e].y;
+                const double acc = warp_fold_run(dst + q0, (int64_t)q1 - q0);
+                __syncwarp();
+                if ((tid & 31) == 0) dst[q0] = (unsigned long long)__double_as_longlong(acc);
             }
         }
         __syncthreads();

@@ -966,10 +966,14 @@ __global__ void k_rbounds(const int2 *__restrict__ rec, int z, int rbits, int32_
 // in one buffer, value bits in the other, bigu[s] = U | BIGFLAG if the keys
 // ended in B.
 // ---------------------------------------------------------------------------
+constexpr int BIG_LONGRUN = 256;  // runs longer than this are folded by a warp
+constexpr int BIG_NLONG = 512;    // listed long runs per sub-bucket (more: walked by their thread)
 __global__ void __launch_bounds__(BIG_NT, 1) k_rbig(RadixFoldArgs F, ErrState *err) {
     __shared__ uint32_t s_cnt[BIG_NW][256];
     __shared__ uint32_t s_warp[BIG_NW];
     __shared__ unsigned long long s_prev;
+    __shared__ uint2 s_long[BIG_NLONG];  // long runs of the sub-bucket: [first, end)
+    __shared__ int s_nlong;
     const int tid = threadIdx.x;
     pdl_wait();
     const unsigned nbig = *((volatile const unsigned *)&err->rbig_n);
@@ -991,20 +995,7 @@ __global__ void __launch_bounds__(BIG_NT, 1) k_rbig(RadixFoldArgs F, ErrState *e
         for (unsigned q = blockIdx.x * (BIG_NT / 32) + (tid >> 5); q < nbig; q += wpg) {
             const uint32_t s = F.biglist[q];
             const uint32_t a = F.bnd[s], n = F.bnd[s + 1] - a;
-            const double *v = F.s + a;
-            double acc = 0.0;
-            double x = (uint32_t)lane < n ? __ldg(v + lane) : 0.0;
-            for (uint32_t k0 = 0; k0 < n; k0 += 32) {
-                const double xn = (k0 + 32 + lane < n) ? __ldg(v + k0 + 32 + lane) : 0.0;
-                const int cnt = (int)min(32u, n - k0);
-                if (cnt == 32) {
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) acc = fold_add(acc, __shfl_sync(FULL, x, j));
-                } else {
-                    for (int j = 0; j < cnt; ++j) acc = fold_add(acc, __shfl_sync(FULL, x, j));
-                }
-                x = xn;
-            }
+            const double acc = warp_fold_run(reinterpret_cast<const unsigned long long *>(F.s + a), n);
             if (lane == 0) {  // one result: local key 0 in A, its value in B
                 F.scrA[a] = 0ull;
                 F.scrB[a] = (unsigned long long)__double_as_longlong(acc);
@@ -1038,7 +1029,13 @@ __global__ void __launch_bounds__(BIG_NT, 1) k_rbig(RadixFoldArgs F, ErrState *e
         for (uint32_t k = tid; k < n; k += BIG_NT)
             dst[k] = (unsigned long long)__double_as_longlong(__ldg(F.s + a + (uint32_t)src[k]));
         __syncthreads();
-        {  // ordered fold of every run; the result lands at the run's head
+        if (tid == 0) s_nlong = 0;
+        __syncthreads();
+        {  // ordered fold of every run; the result lands at the run's head.  A
+           // run longer than BIG_LONGRUN is only listed here (its end found by
+           // binary search: the keys are sorted) and folded by a warp below --
+           // one thread walking a heavy hitter's run through global memory
+           // costs ~100 cycles per repeat, the warp ~12
             const uint32_t lo = (uint32_t)((uint64_t)tid * n / BIG_NT);
             const uint32_t hi = (uint32_t)((uint64_t)(tid + 1) * n / BIG_NT);
             uint32_t p = lo;
@@ -1048,6 +1045,20 @@ __global__ void __launch_bounds__(BIG_NT, 1) k_rbig(RadixFoldArgs F, ErrState *e
                     ++p;
                     continue;
                 }
+                if (p + BIG_LONGRUN < n && (uint32_t)(src[p + BIG_LONGRUN] >> 32) == key) {
+                    uint32_t a2 = p + BIG_LONGRUN + 1, b2 = n;  // first index in [a2, b2] of another key
+                    while (a2 < b2) {
+                        const uint32_t mid = (a2 + b2) >> 1;
+                        if ((uint32_t)(src[mid] >> 32) == key) a2 = mid + 1;
+                        else b2 = mid;
+                    }
+                    const int e = atomicAdd(&s_nlong, 1);
+                    if (e < BIG_NLONG) {
+                        s_long[e] = make_uint2(p, a2);
+                        p = a2;
+                        continue;
+                    }
+                }
                 double acc = fold_add(0.0, __longlong_as_double((long long)dst[p]));
                 uint32_t r = p + 1;
                 while (r < n && (uint32_t)(src[r] >> 32) == key) {
@@ -1056,6 +1067,18 @@ __global__ void __launch_bounds__(BIG_NT, 1) k_rbig(RadixFoldArgs F, ErrState *e
                 }
                 dst[p] = (unsigned long long)__double_as_longlong(acc);
                 p = r;
+            }
+        }
+        __syncthreads();
+        {  // the listed long runs: one warp each, values 32 at a time (the next
+           // 32 in flight), every lane folding them in order through shuffles
+            const int lane = tid & 31;
+            const int nl = min(s_nlong, BIG_NLONG);
+            for (int e = tid >> 5; e < nl; e += BIG_NT / 32) {
+                const uint32_t p0 = s_long[e].x, p1 = s_long[e].y;
+                const double acc = warp_fold_run(dst + p0, (int64_t)p1 - p0);
+                __syncwarp();
+                if (lane == 0) dst[p0] = (unsigned long long)__double_as_longlong(acc);
             }
         }
         __syncthreads();

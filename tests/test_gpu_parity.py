@@ -797,6 +797,42 @@ def test_single_key_oversize_sub_buckets_bit_exact(m, n, L):
     assert a.launch_count() > 6  # the radix pipeline ran
 
 
+@pytest.mark.parametrize("nan_at", [None, 100_000, 5])
+@pytest.mark.parametrize("m,n", [(200_000, 200_000), (300, 300)])
+def test_heavy_hitter_entry_bit_exact(m, n, nan_at):
+    """One (row, col) entry holds half of 600 000 triplets among random ones:
+    its run of repeats is folded in input order by one warp (warp_fold_run:
+    plain adds per block of 32, redone by the x86 NaN rule when the sum turns
+    NaN) in k_rbig (radix path) and k_bigcol (column-cursor path); NaNs with
+    distinct payloads inside the run pin the rule.  Both pipelines forced,
+    bit-exact against the C oracle."""
+    from paper_1406_1066_b200 import _capi
+
+    L = 600_000
+    rng = np.random.default_rng(m + (nan_at or 0))
+    ii = rng.integers(1, m + 1, size=L).astype(np.int32)
+    jj = rng.integers(1, n + 1, size=L).astype(np.int32)
+    hot = np.flatnonzero(rng.random(L) < 0.5)
+    ii[hot] = 7
+    jj[hot] = n - 1
+    s = rng.standard_normal(L)
+    s[hot[::1000]] = -0.0
+    if nan_at is not None:
+        pay = np.array([0x7FF8000000000123, 0xFFF8000000000456, 0x7FF0000000000789], dtype=np.uint64).view(np.float64)
+        s[hot[nan_at]] = pay[0]
+        s[hot[nan_at + 40]] = pay[1]
+        s[hot[nan_at + 3000]] = pay[2]  # (signalling: quieted by the first add that meets it)
+    ref = O.assemble_counting(ii, jj, s, m, n)
+    a = sa.default_assembler(0)
+    for path in (0, 1):
+        a.set_option(_capi.SA_OPT_PATH, path)
+        try:
+            got = a.assemble(ii, jj, s, m=m, n=n)
+        finally:
+            a.set_option(_capi.SA_OPT_PATH, -1)
+        _same(got, ref)
+
+
 @pytest.mark.parametrize("tma", [1, 0])
 def test_three_pass_radix_plan_bit_exact(tma):
     """2e8 columns: the radix plan needs three partition passes (28 column
