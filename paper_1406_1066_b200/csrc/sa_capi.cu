@@ -596,7 +596,8 @@ int assemble_radix(sa_ctx *ctx, const RadixPlan &P, const int32_t *ii, const int
     const int fb = (P.npass - 1) & 1;  // buffer holding the partitioned records
     RadixFoldArgs F{};
     F.rc = reinterpret_cast<const int2 *>(bi[fb]);
-    F.s = bs[fb];
+    // (16-byte records: the value sits behind its {row, col} pair)
+    F.s = SA_AOS ? reinterpret_cast<const double *>(br[fb]) + 1 : bs[fb];
     F.bnd = ctx->rbnd;
     F.biglist = ctx->rbig;
     F.bigu = ctx->rbigu;

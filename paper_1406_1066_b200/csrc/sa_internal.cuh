@@ -110,12 +110,12 @@ __device__ __forceinline__ double fold_add(double acc, double v) {
 // (fold_add's bits unless the sum turns NaN: NaN is sticky, so a non-NaN
 // result met no NaN on the way; the block is redone by the rule otherwise),
 // which keeps the rule's compare and select off the dependent chain.
-__device__ __forceinline__ double warp_fold_run(const unsigned long long *v, int64_t n) {
+__device__ __forceinline__ double warp_fold_run(const unsigned long long *v, int64_t n, int stride = 1) {
     const int lane = threadIdx.x & 31;
     double acc = 0.0;
-    unsigned long long x = (lane < n) ? v[lane] : 0ull;
+    unsigned long long x = (lane < n) ? v[(int64_t)lane * stride] : 0ull;
     for (int64_t k0 = 0; k0 < n; k0 += 32) {
-        const unsigned long long xn = (k0 + 32 + lane < n) ? v[k0 + 32 + lane] : 0ull;
+        const unsigned long long xn = (k0 + 32 + lane < n) ? v[(k0 + 32 + lane) * stride] : 0ull;
         if (n - k0 >= 32) {
             double t = acc;
 #pragma unroll
@@ -473,9 +473,20 @@ struct RadixPassArgs {
     const uint32_t *off;      // nchunk x RP_MAXD: global position of every chunk's digits
 };
 
+// SA_AOS = 1: the last pass writes 16-byte {row, col, value} records (one
+// store per triplet, one write stream of 128-byte digit runs) and the fold's
+// views rc / s of the record array step by RF_STRIDE = 2 elements per
+// triplet.  Measured on cfg4: last pass 4.66 -> 4.30 ms, but the fold reads
+// keys and values in separate phases and then pulls every line twice from
+// L2: 6.13 -> 6.62 ms.  Off.
+#ifndef SA_AOS
+#define SA_AOS 0
+#endif
+constexpr int RF_STRIDE = SA_AOS ? 2 : 1;
+
 struct RadixFoldArgs {
-    const int2 *rc;          // partitioned triplets: {row, col} pairs and values (sorted by
-    const double *s;         // sub-bucket, stable)
+    const int2 *rc;          // partitioned triplets (sorted by sub-bucket, stable): {row, col} of
+    const double *s;         // triplet k at rc[k * RF_STRIDE], its value at s[k * RF_STRIDE]
     const uint32_t *bnd;     // nsub + 1 sub-bucket starts
     const uint32_t *biglist; // oversize sub-buckets
     uint32_t *bigu;          // per oversize sub-bucket: results | BIGFLAG (keys in scrB)

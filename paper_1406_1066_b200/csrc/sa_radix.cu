@@ -372,6 +372,10 @@ __device__ __forceinline__ void st_last(int32_t *a, int32_t v, unsigned long lon
 __device__ __forceinline__ void st_last(double *a, double v, unsigned long long pol) {
     asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(a), "d"(v), "l"(pol) : "memory");
 }
+__device__ __forceinline__ void st_last(uint4 *a, uint4 v, unsigned long long pol) {
+    asm volatile("st.global.L2::cache_hint.v4.b32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(a), "r"(v.x), "r"(v.y),
+                 "r"(v.z), "r"(v.w), "l"(pol) : "memory");
+}
 __device__ __forceinline__ void st_last(int2 *a, int2 v, unsigned long long pol) {
     asm volatile("st.global.L2::cache_hint.v2.b32 [%0], {%1, %2}, %3;" ::"l"(a), "r"(v.x), "r"(v.y), "l"(pol)
                  : "memory");
@@ -383,6 +387,10 @@ __device__ __forceinline__ void st_last(int2 *a, int2 v, unsigned long long pol)
 // columns alone); the values go to their own array either way.
 template <bool LAST>
 __device__ __forceinline__ void put_rec(const RadixPassArgs &A, uint32_t o, uint4 v, unsigned long long pol) {
+    if (LAST && SA_AOS) {  // one 16-byte record (the fold's and the bounds' input)
+        st_last(reinterpret_cast<uint4 *>(A.rc_out) + o, v, pol);
+        return;
+    }
     if (LAST || SA_PAIRS) {
         st_last(A.rc_out + o, make_int2((int)v.x, (int)v.y), pol);
     } else {
@@ -925,7 +933,7 @@ __global__ void __launch_bounds__(RP_NT, 1) k_rpass_tma(RadixPassArgs A, ErrStat
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ unsigned long long sub_of(const int2 *__restrict__ rcp, uint32_t k, int z,
                                                      int rbits) {
-    const int2 rc = __ldg(rcp + k);  // {row, col}
+    const int2 rc = __ldg(rcp + (size_t)k * RF_STRIDE);  // {row, col}
     if (z >= rbits) return (unsigned long long)((uint32_t)(rc.y - 1) >> (z - rbits));
     return tkey(rc.y, rc.x, rbits) >> z;
 }
@@ -995,7 +1003,8 @@ __global__ void __launch_bounds__(BIG_NT, 1) k_rbig(RadixFoldArgs F, ErrState *e
         for (unsigned q = blockIdx.x * (BIG_NT / 32) + (tid >> 5); q < nbig; q += wpg) {
             const uint32_t s = F.biglist[q];
             const uint32_t a = F.bnd[s], n = F.bnd[s + 1] - a;
-            const double acc = warp_fold_run(reinterpret_cast<const unsigned long long *>(F.s + a), n);
+            const double acc = warp_fold_run(reinterpret_cast<const unsigned long long *>(F.s + (size_t)a * RF_STRIDE), n,
+                                             RF_STRIDE);
             if (lane == 0) {  // one result: local key 0 in A, its value in B
                 F.scrA[a] = 0ull;
                 F.scrB[a] = (unsigned long long)__double_as_longlong(acc);
@@ -1014,7 +1023,7 @@ __global__ void __launch_bounds__(BIG_NT, 1) k_rbig(RadixFoldArgs F, ErrState *e
         unsigned long long *A = F.scrA + a;
         unsigned long long *B = F.scrB + a;
         for (uint32_t k = tid; k < n; k += BIG_NT) {
-            const int2 rc = __ldg(F.rc + a + k);
+            const int2 rc = __ldg(F.rc + (size_t)(a + k) * RF_STRIDE);
             const uint32_t key = lkey(rc.y, rc.x, F.z, F.rbits, c0, roff);
             A[k] = ((unsigned long long)key << 32) | k;
         }
@@ -1027,7 +1036,7 @@ __global__ void __launch_bounds__(BIG_NT, 1) k_rbig(RadixFoldArgs F, ErrState *e
             dst = t;
         }
         for (uint32_t k = tid; k < n; k += BIG_NT)
-            dst[k] = (unsigned long long)__double_as_longlong(__ldg(F.s + a + (uint32_t)src[k]));
+            dst[k] = (unsigned long long)__double_as_longlong(__ldg(F.s + ((size_t)a + (uint32_t)src[k]) * RF_STRIDE));
         __syncthreads();
         if (tid == 0) s_nlong = 0;
         __syncthreads();
@@ -1328,8 +1337,10 @@ __global__ void __launch_bounds__(RF_NT, RF_MINB) k_rfold(RadixFoldArgs F, ErrSt
 
     // ---- 1. groups -------------------------------------------------------
     {  // the sub-bucket's values into L2 while the groups are built (staged later)
-        const char *vb = reinterpret_cast<const char *>(F.s + a);
-        const uint32_t nb = n * 8u;
+        // (16-byte records: keys and values share their lines)
+        const char *vb = SA_AOS ? reinterpret_cast<const char *>(F.rc + (size_t)a * RF_STRIDE)
+                                : reinterpret_cast<const char *>(F.s + a);
+        const uint32_t nb = n * 8u * RF_STRIDE;
         for (uint32_t o = (uint32_t)tid * 128u; o < nb; o += RF_NT * 128u)
             asm volatile("prefetch.global.L2 [%0];" ::"l"(vb + o));
     }
@@ -1359,7 +1370,7 @@ __global__ void __launch_bounds__(RF_NT, RF_MINB) k_rfold(RadixFoldArgs F, ErrSt
         const uint32_t k = tid + u * RF_NT;
         kk[u] = 0u;
         if (k < n) {
-            const int2 rc = __ldg(F.rc + a + k);  // {row, col}
+            const int2 rc = __ldg(F.rc + (size_t)(a + k) * RF_STRIDE);  // {row, col}
 #if SA_FOLD_K32
             // local key + 1 in 32 bits: ((col - 1 - c0) << rbits) + row - roff
             // (column-block plan: roff = 0; row-split plan: col - 1 == c0)
@@ -1374,8 +1385,8 @@ __global__ void __launch_bounds__(RF_NT, RF_MINB) k_rfold(RadixFoldArgs F, ErrSt
         const int64_t sp = s + F.nres;
         if (sp < F.nsub) {
             const uint32_t a2 = F.bnd[sp], n2 = min(F.bnd[sp + 1] - a2, (uint32_t)RF_CAP);
-            const char *kb = reinterpret_cast<const char *>(F.rc + a2);
-            for (uint32_t o = (uint32_t)tid * 128u; o < n2 * 8u; o += RF_NT * 128u)
+            const char *kb = reinterpret_cast<const char *>(F.rc + (size_t)a2 * RF_STRIDE);
+            for (uint32_t o = (uint32_t)tid * 128u; o < n2 * 8u * RF_STRIDE; o += RF_NT * 128u)
                 asm volatile("prefetch.global.L2 [%0];" ::"l"(kb + o));
         }
     }
@@ -1553,7 +1564,7 @@ __global__ void __launch_bounds__(RF_NT, RF_MINB) k_rfold(RadixFoldArgs F, ErrSt
     // the sub-bucket's values into shared memory (the dead hash table, member
     // counts and group slots: the ranking above was the last reader of ckey),
     // in flight while the offset is looked back; the fallback sort below
-    // uses the same space, so it reads the values from global memory
+    // uses the same space first
     static_assert(sizeof(uint32_t) * (RF_HS + RF_HS / 2) + sizeof(uint16_t) * RF_CAP >= 8 * RF_CAP,
                   "staged values");
     double *Vs = reinterpret_cast<double *>(&S.key[0]);
@@ -1562,9 +1573,6 @@ __global__ void __launch_bounds__(RF_NT, RF_MINB) k_rfold(RadixFoldArgs F, ErrSt
         for (int u = 0; u < RIPT; ++u) {
             if (tid + u * RF_NT < U) S.gid[opos[u] & 0xffffu] = (uint16_t)(opos[u] >> 16);  // gid := group of output entry
         }
-        const double *sg = F.s + a;
-        for (uint32_t k = tid; k < n; k += RF_NT) rf_cp_async8(&Vs[k], sg + k);
-        asm volatile("cp.async.commit_group;" ::: "memory");
     } else {  // CTA bitonic sort of all groups by key (a column with > 64 distinct rows)
         unsigned long long *items = reinterpret_cast<unsigned long long *>(S.key);
         int np2 = 1;
@@ -1593,6 +1601,11 @@ __global__ void __launch_bounds__(RF_NT, RF_MINB) k_rfold(RadixFoldArgs F, ErrSt
             if (S.gstart[g + 1] - S.gstart[g] > 8) dl[atomicAdd(&S.ndef, 1)] = (uint16_t)p;
         }
     }
+    {  // (after the sort, if any: its items were last read before the barrier above)
+        const double *sg = F.s + (size_t)a * RF_STRIDE;
+        for (uint32_t k = tid; k < n; k += RF_NT) rf_cp_async8(&Vs[k], sg + (size_t)k * RF_STRIDE);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    }
     // ---- 5. offset, fold, outputs -------------------------------------------------
     if (warp == 0) {
         const unsigned long long e = ep_walk_warp(F.lbf, s, F.tag);
@@ -1607,7 +1620,7 @@ __global__ void __launch_bounds__(RF_NT, RF_MINB) k_rfold(RadixFoldArgs F, ErrSt
     __syncthreads();
     RTRACE(7)
     const long long off = S.off;
-    const double *__restrict__ sv = sortall ? F.s + a : Vs;
+    const double *__restrict__ sv = Vs;
     // groups of more than 8 members (Poisson(5) repeats: 7 % of the groups)
     // were listed by the ranking: folded one per thread, taken from the last
     // thread down -- the warps with the fewest entries of the loop below -- so
