@@ -268,6 +268,33 @@ __device__ __forceinline__ T block_excl_sum(T v, T *s_warp, T &total) {
     return wpre + x - v;
 }
 
+// The same with one barrier: every warp scans the NT/32 warp totals itself.
+// No trailing barrier: the caller must pass a barrier before s_warp is
+// written again (and NT/32 <= 32).
+template <int NT, typename T>
+__device__ __forceinline__ T block_excl_sum1(T v, T *s_warp, T &total) {
+    static_assert(NT / 32 <= 32, "one lane per warp total");
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    T x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        T y = __shfl_up_sync(FULL, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) s_warp[w] = x;
+    __syncthreads();
+    T t = (lane < NT / 32) ? s_warp[lane] : T(0);
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        T y = __shfl_up_sync(FULL, t, o);
+        if (lane >= o) t += y;
+    }
+    total = __shfl_sync(FULL, t, NT / 32 - 1);
+    const T winc = __shfl_sync(FULL, t, w);  // inclusive over warps 0..w
+    const T wtot = __shfl_sync(FULL, x, 31);
+    return winc - wtot + x - v;
+}
+
 // In-place exclusive sum over arr[0..n) in shared memory (n <= NT*IPT).
 // Returns the total.  Each thread owns IPT consecutive entries.
 template <int NT, int IPT, typename T>

@@ -411,6 +411,9 @@ __device__ __forceinline__ void put_rec(const RadixPassArgs &A, uint32_t o, uint
 #ifndef SA_PASS_V2
 #define SA_PASS_V2 1
 #endif
+#ifndef SA_SCAN1
+#define SA_SCAN1 1
+#endif
 #ifndef SA_PASS_NOIDX
 #define SA_PASS_NOIDX 1
 #endif
@@ -483,7 +486,12 @@ __device__ __forceinline__ void rp_scan(uint32_t *cnt, uint32_t *red, uint32_t &
     const uint32_t totp = __shfl_sync(FULL, inc, lane | 3);
     t0 = totp & 0xffffu;
     t1 = totp >> 16;
+#if SA_SCAN1
+    // (one barrier; red is next written a chunk half later, barriers away)
+    const uint32_t exq = block_excl_sum1<RP_NT, uint32_t>(q == 0 ? t0 + t1 : 0u, red, ctot);
+#else
     const uint32_t exq = block_excl_sum<RP_NT, uint32_t>(q == 0 ? t0 + t1 : 0u, red, ctot);
+#endif
     ex = __shfl_sync(FULL, exq, lane & ~3);
     if (p < npair) {
         const uint32_t add = (ex + (before & 0xffffu)) | ((ex + t0 + (before >> 16)) << 16);

@@ -1,3 +1,4 @@
-O=gpurun_out/w19; mkdir -p $O
-timeout 1500 python -m pytest tests -m gpu -x -q > $O/pytest.log 2>&1; echo rc=$? >> $O/pytest.log
-python bench.py --steps 10 --warmup 3 > $O/bench_cfg4.json 2> $O/bench_cfg4.err
+O=gpurun_out/w22; mkdir -p $O
+bash tools/abn.sh w22 4 r0 r1
+cp paper_1406_1066_b200/lib/libsa_r1.so paper_1406_1066_b200/lib/libsa_b200.so
+timeout 600 python tools/radix_check.py > $O/check.txt 2>&1
