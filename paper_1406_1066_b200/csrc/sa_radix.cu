@@ -134,6 +134,9 @@ __device__ __forceinline__ bool call_failed(const ErrState *err) {
 #ifndef SA_PAIRS
 #define SA_PAIRS 1
 #endif
+#ifndef SA_RUP_PRED
+#define SA_RUP_PRED 1
+#endif
 
 // k_rup: per-chunk digit histograms cnt[c][d] (16-bit) of the pass input (jj)
 // and the block's sums bsum[B][d].  The first pass also validates the
@@ -205,6 +208,12 @@ __global__ void __launch_bounds__(RU_NT) k_rup(const int32_t *__restrict__ ii, c
             int vn[UPT];
             if (c + 1 < ce) load(c + 1, vn, vnr);
             uint32_t *hc = h[c & 1];
+#if SA_RUP_PRED
+            if (!ROWKEY && vecmode(c)) {  // whole chunk of stored (valid) columns: no tests
+#pragma unroll
+                for (int u = 0; u < UPT; ++u) atomicAdd(&hc[((unsigned)(v[u] - 1) >> csh) & dmask], 1u);
+            } else
+#endif
 #pragma unroll
             for (int u = 0; u < UPT; ++u) {
                 const int cc = v[u];
@@ -263,6 +272,35 @@ __global__ void __launch_bounds__(RU_NT) k_rup(const int32_t *__restrict__ ii, c
         auto eidx = [&](int u) -> int {
             return vec ? 4 * ((int)threadIdx.x + (u >> 2) * RU_NT) + (u & 3) : (int)threadIdx.x + u * RU_NT;
         };
+#if SA_RUP_PRED
+        if (vec && !ROWKEY) {
+            // whole chunk, column digits: branch-free -- a predicated shared
+            // reduction per element, the valid ones counted; the (rare) bad
+            // indices are looked at afterwards
+            const unsigned hb = (unsigned)__cvta_generic_to_shared(hc);
+            unsigned nok = 0, nbad = 0;
+#pragma unroll
+            for (int u = 0; u < UPT; ++u) {
+                const unsigned c1 = (unsigned)v[u] - 1u;
+                const unsigned ok = (!FIRST || c1 < (unsigned)N) ? 1u : 0u;
+                const unsigned a = hb + (((c1 >> csh) & dmask) << 2);
+                asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %1, 0;\n\t@p red.shared.add.u32 [%0], 1;\n\t}"
+                             ::"r"(a), "r"(ok) : "memory");
+                nok += ok;
+                nbad += 1u - ok;
+            }
+            nval += nok;
+            if (FIRST && nbad) {
+#pragma unroll
+                for (int u = 0; u < UPT; ++u) {
+                    const int cc = v[u];
+                    if ((unsigned)(cc - 1) < (unsigned)N) continue;
+                    if (cc < 1) bad = min(bad, (unsigned long long)(lo + eidx(u)));
+                    else over = 1;
+                }
+            }
+        } else
+#endif
 #pragma unroll
         for (int u = 0; u < UPT; ++u) {
             const int cc = v[u];
