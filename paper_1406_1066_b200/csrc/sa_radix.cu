@@ -160,7 +160,12 @@ __global__ void __launch_bounds__(RU_NT) k_rup(const int32_t *__restrict__ ii, c
     unsigned long long bad = ~0ull;
     unsigned over = 0, nval = 0;
     uint32_t bs = 0;  // block sum of digit threadIdx.x
-    constexpr int UPT = RP_CHUNK / RU_NT;
+    // a chunk is counted in RU_SUB pieces (at most 8 K triplets each: the piece in
+    // hand and the one in flight stay in registers)
+    constexpr int RU_SUB = RP_CHUNK > 8192 ? 2 : 1;
+    constexpr int RU_PIECE = RP_CHUNK / RU_SUB;
+    constexpr int UPT = RU_PIECE / RU_NT;
+    static_assert(RU_PIECE % (2 * RU_NT) == 0, "16- and 8-byte loads of whole pieces");
     const int64_t cb = (int64_t)blockIdx.x * cpb, ce = min(nchunk, cb + cpb);
     // Whole chunks of a 16-byte aligned array are read with 16-byte loads
     // (thread t holds the elements 4 (t + 512 u) .. + 3: a histogram does not
@@ -176,9 +181,9 @@ __global__ void __launch_bounds__(RU_NT) k_rup(const int32_t *__restrict__ ii, c
         // thread t holds the pairs 2 (t + RU_NT u), + 1 of a whole chunk (one
         // 16-byte load each), or t + RU_NT u of a partial / unaligned one
         int vr[ROWKEY ? UPT : 1], vnr[ROWKEY ? UPT : 1];
-        auto vecmode = [&](int64_t c) { return al16 && (c + 1) * RP_CHUNK <= Lp; };
+        auto vecmode = [&](int64_t q) { return al16 && (q + 1) * RU_PIECE <= Lp; };
         auto load = [&](int64_t c, int (&x)[UPT], int (&xr)[ROWKEY ? UPT : 1]) {
-            const int64_t lo = c * RP_CHUNK;
+            const int64_t lo = c * RU_PIECE;
             if (vecmode(c)) {
                 const int4 *p4 = reinterpret_cast<const int4 *>(rc + lo) + threadIdx.x;
 #pragma unroll
@@ -192,7 +197,7 @@ __global__ void __launch_bounds__(RU_NT) k_rup(const int32_t *__restrict__ ii, c
                     }
                 }
             } else {
-                const int64_t hi = min(Lp, lo + RP_CHUNK);
+                const int64_t hi = min(Lp, lo + RU_PIECE);
 #pragma unroll
                 for (int u = 0; u < UPT; ++u) {
                     const int64_t t = lo + threadIdx.x + (int64_t)u * RU_NT;
@@ -202,12 +207,12 @@ __global__ void __launch_bounds__(RU_NT) k_rup(const int32_t *__restrict__ ii, c
                 }
             }
         };
-        if (cb < ce) load(cb, v, vr);
+        if (cb < ce) load(cb * RU_SUB, v, vr);
         __syncthreads();
-        for (int64_t c = cb; c < ce; ++c) {
+        for (int64_t c = cb * RU_SUB; c < ce * RU_SUB; ++c) {  // c: piece; chunk c / RU_SUB
             int vn[UPT];
-            if (c + 1 < ce) load(c + 1, vn, vnr);
-            uint32_t *hc = h[c & 1];
+            if (c + 1 < ce * RU_SUB) load(c + 1, vn, vnr);
+            uint32_t *hc = h[(c / RU_SUB) & 1];
 #if SA_RUP_PRED
             if (!ROWKEY && vecmode(c)) {  // whole chunk of stored (valid) columns: no tests
 #pragma unroll
@@ -221,11 +226,13 @@ __global__ void __launch_bounds__(RU_NT) k_rup(const int32_t *__restrict__ ii, c
                 if (ROWKEY) atomicAdd(&hc[key_digit(cc, vr[ROWKEY ? u : 0], shift, rbits, dmask)], 1u);
                 else atomicAdd(&hc[((unsigned)(cc - 1) >> csh) & dmask], 1u);
             }
-            __syncthreads();
-            for (int k = threadIdx.x; k < ndig; k += RU_NT) {
-                cnt[c * RP_MAXD + k] = (uint16_t)hc[k];
-                bs += hc[k];  // RU_NT == RP_MAXD: thread k owns digit k
-                hc[k] = 0;
+            if (c % RU_SUB == RU_SUB - 1) {  // the chunk's last piece
+                __syncthreads();
+                for (int k = threadIdx.x; k < ndig; k += RU_NT) {
+                    cnt[(c / RU_SUB) * RP_MAXD + k] = (uint16_t)hc[k];
+                    bs += hc[k];  // RU_NT == RP_MAXD: thread k owns digit k
+                    hc[k] = 0;
+                }
             }
 #pragma unroll
             for (int u = 0; u < UPT; ++u) {
@@ -238,9 +245,9 @@ __global__ void __launch_bounds__(RU_NT) k_rup(const int32_t *__restrict__ ii, c
         return;
     }
 #endif
-    auto vecmode = [&](int64_t c) { return al16 && (c + 1) * RP_CHUNK <= Lp; };
+    auto vecmode = [&](int64_t q) { return al16 && (q + 1) * RU_PIECE <= Lp; };
     auto load = [&](int64_t c, int (&x)[UPT]) {
-        const int64_t lo = c * RP_CHUNK;
+        const int64_t lo = c * RU_PIECE;
         if (vecmode(c)) {
             const int4 *p4 = reinterpret_cast<const int4 *>(jj + lo) + threadIdx.x;
 #pragma unroll
@@ -251,8 +258,14 @@ __global__ void __launch_bounds__(RU_NT) k_rup(const int32_t *__restrict__ ii, c
                 x[4 * u + 2] = q.z;
                 x[4 * u + 3] = q.w;
             }
+            if (UPT % 4) {  // the piece's tail: one 8-byte load (UPT % 4 == 2)
+                constexpr int U4 = UPT / 4 * 4;
+                const int2 q = __ldcs(reinterpret_cast<const int2 *>(jj + lo + U4 * RU_NT) + threadIdx.x);
+                x[U4] = q.x;
+                x[U4 + 1] = q.y;
+            }
         } else {
-            const int64_t hi = min(Lp, lo + RP_CHUNK);
+            const int64_t hi = min(Lp, lo + RU_PIECE);
 #pragma unroll
             for (int u = 0; u < UPT; ++u) {
                 const int64_t t = lo + threadIdx.x + (int64_t)u * RU_NT;
@@ -260,17 +273,20 @@ __global__ void __launch_bounds__(RU_NT) k_rup(const int32_t *__restrict__ ii, c
             }
         }
     };
-    if (cb < ce) load(cb, v);
+    if (cb < ce) load(cb * RU_SUB, v);
     __syncthreads();
-    for (int64_t c = cb; c < ce; ++c) {
+    for (int64_t c = cb * RU_SUB; c < ce * RU_SUB; ++c) {  // c: piece; chunk c / RU_SUB
         int vn[UPT];
-        if (c + 1 < ce) load(c + 1, vn);
-        uint32_t *hc = h[c & 1];
-        const int64_t lo = c * RP_CHUNK, hi = min(Lp, lo + RP_CHUNK);
+        if (c + 1 < ce * RU_SUB) load(c + 1, vn);
+        uint32_t *hc = h[(c / RU_SUB) & 1];
+        const int64_t lo = c * RU_PIECE, hi = min(Lp, lo + RU_PIECE);
         const bool vec = vecmode(c);
         // element index of v[u] within the chunk
         auto eidx = [&](int u) -> int {
-            return vec ? 4 * ((int)threadIdx.x + (u >> 2) * RU_NT) + (u & 3) : (int)threadIdx.x + u * RU_NT;
+            constexpr int U4 = UPT / 4 * 4;
+            if (!vec) return (int)threadIdx.x + u * RU_NT;
+            return u < U4 ? 4 * ((int)threadIdx.x + (u >> 2) * RU_NT) + (u & 3)
+                          : U4 * RU_NT + 2 * (int)threadIdx.x + (u - U4);
         };
 #if SA_RUP_PRED
         if (vec && !ROWKEY) {
@@ -316,11 +332,13 @@ __global__ void __launch_bounds__(RU_NT) k_rup(const int32_t *__restrict__ ii, c
                 else over = 1;
             }
         }
-        __syncthreads();
-        for (int k = threadIdx.x; k < ndig; k += RU_NT) {
-            cnt[c * RP_MAXD + k] = (uint16_t)hc[k];
-            bs += hc[k];  // RU_NT == RP_MAXD: thread k owns digit k
-            hc[k] = 0;
+        if (c % RU_SUB == RU_SUB - 1) {  // the chunk's last piece
+            __syncthreads();
+            for (int k = threadIdx.x; k < ndig; k += RU_NT) {
+                cnt[(c / RU_SUB) * RP_MAXD + k] = (uint16_t)hc[k];
+                bs += hc[k];  // RU_NT == RP_MAXD: thread k owns digit k
+                hc[k] = 0;
+            }
         }
 #pragma unroll
         for (int u = 0; u < UPT; ++u) v[u] = vn[u];
@@ -554,9 +572,10 @@ __device__ __forceinline__ void rp_scan(uint32_t *cnt, uint32_t *red, uint32_t &
 // ---------------------------------------------------------------------------
 struct PassSmem {
     uint4 rec[RP_CHUNK];              // reordered {row, col, value}
+#if !SA_PASS_NOIDX
     uint32_t oidx[RP_CHUNK];          // output index of reordered slot k
+#endif
     uint32_t cnt[RP_NW][RP_CS];       // per warp, digit pair (16-bit halves): running count, then base
-    uint32_t dtot[RP_MAXD];           // digit totals of the chunk
     uint32_t run[RP_MAXD];            // the chunk's global base per digit
     uint32_t red[RP_NW];
 };
@@ -684,12 +703,21 @@ __global__ void __launch_bounds__(RP_NT, 1) k_rpass(RadixPassArgs A, ErrState *e
                                      ((rk[r >> 1] >> ((r & 1) * 16)) & 0xffffu);
                 const unsigned long long vb = (unsigned long long)__double_as_longlong(val[r]);
                 S.rec[pos] = make_uint4((uint32_t)row[r], (uint32_t)col[r], (uint32_t)vb, (uint32_t)(vb >> 32));
+#if !SA_PASS_NOIDX
                 S.oidx[pos] = S.run[d] + pos;
+#endif
             }
         }
         __syncthreads();
         const unsigned long long pol = l2_evict_last();
+#if SA_PASS_NOIDX
+        for (int k = tid; k < (int)ctot; k += RP_NT) {  // (output index from the record's own digit)
+            const uint4 v = S.rec[k];
+            put_rec<LAST>(A, S.run[key_digit((int)v.y, (int)v.x, shift, A.rbits, dmask)] + (uint32_t)k, v, pol);
+        }
+#else
         for (int k = tid; k < (int)ctot; k += RP_NT) put_rec<LAST>(A, S.oidx[k], S.rec[k], pol);
+#endif
     }
     pdl_trigger();
     if (FIRST) {
@@ -720,7 +748,9 @@ constexpr int RT_HALF = RP_CHUNK / 2;
 constexpr int RT_IPT = RT_HALF / RP_NT;
 struct PassTmaSmem {
     uint4 buf[2][RT_HALF];            // staged {ii[], jj[], s[]} of a half, then its sorted records
+#if !SA_PASS_NOIDX
     uint32_t oidx[RT_HALF];           // output index of sorted slot k
+#endif
     uint32_t cnt[RP_NW][RP_CS];       // per warp, digit pair (16-bit halves)
     uint32_t hb[RP_MAXD];             // the half's global base per digit
     uint32_t run[RP_MAXD];

@@ -1,5 +1,5 @@
-O=gpurun_out/w23; mkdir -p $O
-bash tools/abn.sh w23 4 u0 u1
-cp paper_1406_1066_b200/lib/libsa_u1.so paper_1406_1066_b200/lib/libsa_b200.so
+O=gpurun_out/w25; mkdir -p $O
+bash tools/abn.sh w25 4 b200
 timeout 600 python tools/radix_check.py > $O/check.txt 2>&1
-timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "error or fuzz or three_pass or unaligned" > $O/pytest.log 2>&1; echo rc=$? >> $O/pytest.log
+timeout 1500 python -m pytest tests -m gpu -x -q > $O/pytest.log 2>&1; echo rc=$? >> $O/pytest.log
+python bench.py --steps 10 --warmup 3 > $O/bench_cfg4.json 2> $O/bench_cfg4.err
