@@ -476,11 +476,12 @@ cudaError_t launch_tile_fold(Launch &lc, const uint32_t *sstart, const int2 *til
 // ---- radix path (sa_radix.cu) -------------------------------------------------
 constexpr int RP_NT = 1024;                 // partition pass: threads per CTA (one CTA per SM)
 constexpr int RP_NW = RP_NT / 32;
-// (10: chunks of 10240 triplets, two TMA-staged halves of 5120 -- 160 KB of
-// staging per CTA; longer digit runs per half than with 8: cfg4 passes 5.07 /
-// 4.62 -> 4.74 / 4.31 ms)
+// (12: chunks of 12288 triplets, two TMA-staged halves of 6144 -- 192 KB of
+// staging, 226 KB of shared memory per CTA, the most an SM has; longer digit
+// runs per half and fewer per-half overheads than with 8: cfg4 passes 5.07 /
+// 4.62 -> 4.43 / 4.08 ms; 10: 4.62 / 4.28)
 #ifndef SA_RP_IPT
-#define SA_RP_IPT 10
+#define SA_RP_IPT 12
 #endif
 constexpr int RP_IPT = SA_RP_IPT;           // triplets per thread
 constexpr int RP_CHUNK = RP_NT * RP_IPT;    // triplets per chunk (CTA)

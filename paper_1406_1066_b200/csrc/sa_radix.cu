@@ -752,7 +752,6 @@ struct PassTmaSmem {
     uint32_t oidx[RT_HALF];           // output index of sorted slot k
 #endif
     uint32_t cnt[RP_NW][RP_CS];       // per warp, digit pair (16-bit halves)
-    uint32_t hb[RP_MAXD];             // the half's global base per digit
     uint32_t run[RP_MAXD];
     uint32_t red[RP_NW];
     unsigned long long mbar[2];
@@ -827,9 +826,13 @@ __global__ void __launch_bounds__(RP_NT, 1) k_rpass_tma(RadixPassArgs A, ErrStat
     // TMA only for whole halves (16-byte multiples); a partial tail half is
     // loaded by the threads
     if (tid == 0 && nmine > 0 && half_len(0) == RT_HALF) rt_issue<PAIRS>(S, 0, A, half_start(0), RT_HALF);
-    // the chunk's digit bases, fetched one chunk ahead (thread d holds digit d)
-    static_assert(RP_MAXD <= RP_NT, "one digit base per thread");
-    uint32_t hbn = (tid < ndig && nmine > 0) ? A.off[(int64_t)blockIdx.x * RP_MAXD + tid] : 0u;
+    // the chunk's digit bases live in the registers of the scan's pair owners
+    // (thread 4 p: digits 2 p, 2 p + 1), fetched one chunk ahead
+    static_assert(RP_MAXD / 2 * 4 <= RP_NT && RP_MAXD % 2 == 0, "one digit pair per owner thread");
+    const bool owner = (tid & 3) == 0 && (tid >> 2) < npair;
+    const uint2 *offp = reinterpret_cast<const uint2 *>(A.off) + (tid >> 2);  // (+ chunk * RP_MAXD / 2)
+    uint2 hbn = (owner && nmine > 0) ? offp[(int64_t)blockIdx.x * (RP_MAXD / 2)] : make_uint2(0u, 0u);
+    uint32_t hb0 = 0, hb1 = 0;
     for (int64_t k = 0; k < nmine; ++k) {
         const int b = (int)(k & 1);
         const int64_t h0 = half_start(k);
@@ -841,11 +844,10 @@ __global__ void __launch_bounds__(RP_NT, 1) k_rpass_tma(RadixPassArgs A, ErrStat
             static_assert(sizeof(S.cnt) % 16 == 0 && offsetof(PassTmaSmem, cnt) % 16 == 0, "vector clear");
             uint4 *c128 = reinterpret_cast<uint4 *>(&S.cnt[0][0]);
             for (int q = tid; q < (int)(sizeof(S.cnt) / 16); q += RP_NT) c128[q] = make_uint4(0u, 0u, 0u, 0u);
-            if ((k & 1) == 0) {
-                if (tid < ndig) {
-                    S.hb[tid] = hbn;
-                    if (k + 2 < nmine) hbn = A.off[(c + gridDim.x) * RP_MAXD + tid];
-                }
+            if ((k & 1) == 0 && owner) {
+                hb0 = hbn.x;
+                hb1 = hbn.y;
+                if (k + 2 < nmine) hbn = offp[(c + gridDim.x) * (RP_MAXD / 2)];
             }
         }
         int32_t *si = reinterpret_cast<int32_t *>(&S.buf[b][0]);
@@ -898,66 +900,24 @@ __global__ void __launch_bounds__(RP_NT, 1) k_rpass_tma(RadixPassArgs A, ErrStat
             }
             const bool valid = live && (unsigned)(col[r] - 1) < (unsigned)N;
             const unsigned d = key_digit(col[r], row[r], shift, A.rbits, dmask);
-#if SA_PASS_V2
             const unsigned rr = rp_rank(&S.cnt[w][0], d, valid, lt);
-#else
-            unsigned peers = __ballot_sync(FULL, valid);
-#pragma unroll
-            for (int i = 0; i < BITS; ++i) {
-                const unsigned bb = __ballot_sync(FULL, (d >> i) & 1u);
-                peers &= bb ^ (((d >> i) & 1u) - 1u);
-            }
-            const int leader = __ffs(peers) - 1;
-            const unsigned sh = (d & 1u) * 16u;
-            unsigned old = 0;
-            if (lane == leader && valid) old = atomicAdd(&S.cnt[w][d >> 1], (unsigned)__popc(peers) << sh);
-            const unsigned rr = ((__shfl_sync(FULL, old, leader & 31) >> sh) & 0xffffu) + __popc(peers & lt);
-#endif
             if (r & 1) rk[r >> 1] |= rr << 16;
             else rk[r >> 1] = rr;
         }
         __syncthreads();
-#if SA_PASS_V2
         uint32_t t0, t1, ex, ctot;
         rp_scan<BITS>(&S.cnt[0][0], S.red, t0, t1, ex, ctot);
-        if ((tid & 3) == 0 && (tid >> 2) < npair) {
+        if (owner) {
             // global position of the half-local slot 0 of each digit; the next
             // half of the chunk starts where this one ends
             const int pp = tid >> 2;
-            S.run[2 * pp] = S.hb[2 * pp] - ex;
-            S.hb[2 * pp] += t0;
+            S.run[2 * pp] = hb0 - ex;
+            hb0 += t0;
             if (2 * pp + 1 < ndig) {
-                S.run[2 * pp + 1] = S.hb[2 * pp + 1] - (ex + t0);
-                S.hb[2 * pp + 1] += t1;
+                S.run[2 * pp + 1] = hb1 - (ex + t0);
+                hb1 += t1;
             }
         }
-#else
-        uint32_t t0 = 0, t1 = 0;
-        if (tid < npair) {
-#pragma unroll 8
-            for (int ww = 0; ww < RP_NW; ++ww) {
-                const uint32_t cc = S.cnt[ww][tid];
-                S.cnt[ww][tid] = t0 | (t1 << 16);
-                t0 += cc & 0xffffu;
-                t1 += cc >> 16;
-            }
-        }
-        uint32_t ctot;
-        const uint32_t ex = block_excl_sum<RP_NT, uint32_t>(t0 + t1, S.red, ctot);
-        if (tid < npair) {
-            const uint32_t add = ex | ((ex + t0) << 16);
-#pragma unroll 8
-            for (int ww = 0; ww < RP_NW; ++ww) S.cnt[ww][tid] += add;
-            // global position of the half-local slot 0 of each digit; the next
-            // half of the chunk starts where this one ends
-            S.run[2 * tid] = S.hb[2 * tid] - ex;
-            S.hb[2 * tid] += t0;
-            if (2 * tid + 1 < ndig) {
-                S.run[2 * tid + 1] = S.hb[2 * tid + 1] - (ex + t0);
-                S.hb[2 * tid + 1] += t1;
-            }
-        }
-#endif
         __syncthreads();
         uint4 *rec = &S.buf[b][0];
 #pragma unroll
