@@ -1779,20 +1779,29 @@ static cudaError_t launch_rpass_t(Launch &lc, const RadixPassArgs &A, int nseg, 
         const int smem = (int)sizeof(PassTmaSmem);
         cudaError_t e = ensure_smem_attr((const void *)k_rpass_tma<FIRST, LAST, BITS>, smem);
         if (e != cudaSuccess) return e;
-        // grid: the first pass runs best with many short-lived CTAs (cfg4:
-        // 9.6 ms at one CTA per SM, 6.75 / 6.19 / 5.95 / 5.94 / 5.92 / 6.22 ms
-        // at 16 / 8 / 4 / 3 / 2 / 1 chunks per CTA), the later ones with one
-        // CTA per SM (4.67 ms; 4 / 2 / 1 chunks per CTA: 4.75 / 4.85 / 5.30
-        // ms) -- measured, tools/abn.sh
+        // grid: the first pass runs best on several waves of short-lived CTAs
+        // (cfg4, 40691 chunks of 12288: 5.54 ms at one CTA per SM; 4.52 / 4.44 /
+        // 4.38 / 4.33 / 4.31 / 4.28 / 4.37 ms at 2 / 3 / 4 / 6 / 8 / 12 / 16 chunks per
+        // CTA -- 12 and 16 differ by the last, partly filled wave, so large
+        // inputs get whole waves of about SA_RP_FIRST_CPC chunks per CTA), the
+        // later ones with one CTA per SM (4.07 ms; 2 chunks per CTA: 4.21 ms)
+        // -- measured, tools/abn.sh
 #ifndef SA_RP_FIRST_CPC
-#define SA_RP_FIRST_CPC 3
+#define SA_RP_FIRST_CPC 12
 #endif
 #ifndef SA_RP_LATER_CPC
 #define SA_RP_LATER_CPC 0
 #endif
         const int64_t nch = (A.L + RP_CHUNK - 1) / RP_CHUNK;
-        const int cpc = FIRST ? SA_RP_FIRST_CPC : SA_RP_LATER_CPC;  // chunks per CTA (0: one CTA per SM)
-        const int64_t grid = cpc ? std::max<int64_t>(lc.num_sms, (nch + cpc - 1) / cpc) : lc.num_sms;
+        int64_t grid = lc.num_sms;
+        if (FIRST && SA_RP_FIRST_CPC) {
+            const int64_t per_wave = (int64_t)SA_RP_FIRST_CPC * lc.num_sms;
+            if (nch >= 2 * per_wave) grid = (nch + per_wave / 2) / per_wave * lc.num_sms;  // whole waves
+            else grid = std::max<int64_t>(lc.num_sms, (nch + 2) / 3);                      // 3 chunks per CTA
+        } else if (!FIRST && SA_RP_LATER_CPC) {
+            constexpr int64_t lc_cpc = SA_RP_LATER_CPC ? SA_RP_LATER_CPC : 1;
+            grid = std::max<int64_t>(lc.num_sms, (nch + lc_cpc - 1) / lc_cpc);
+        }
         return launch_pdl(k_rpass_tma<FIRST, LAST, BITS>, dim3((unsigned)grid), dim3(RP_NT), smem, lc.stream,
                           A, err);
     }
