@@ -1740,7 +1740,10 @@ namespace sa {
 // Chunks per upsweep block: RP_BLK, fewer for small inputs so that every SM
 // gets about four blocks.
 int rup_cpb(int64_t nchunk, int num_sms) {
-    return (int)std::max<int64_t>(1, std::min<int64_t>(RP_BLK, nchunk / (4 * (int64_t)num_sms)));
+#ifndef SA_RUP_BLK
+#define SA_RUP_BLK RP_BLK
+#endif
+    return (int)std::max<int64_t>(1, std::min<int64_t>(SA_RUP_BLK, nchunk / (4 * (int64_t)num_sms)));
 }
 
 cudaError_t launch_rup(Launch &lc, bool first, const int32_t *ii, const int32_t *jj, const int2 *rc, int64_t L,
