@@ -1,3 +1,2 @@
-O=gpurun_out/w32; mkdir -p $O
+O=gpurun_out/w35; mkdir -p $O
 timeout 1500 python -m pytest tests -m gpu -x -q > $O/pytest.log 2>&1; echo rc=$? >> $O/pytest.log
-python bench.py --steps 10 --warmup 3 > $O/bench_cfg4.json 2> $O/bench_cfg4.err
